@@ -1,0 +1,398 @@
+#!/usr/bin/env python3
+"""Experience-making throughput (logprob + KL + advantage + loss) at V=152k.
+
+Workload (BASELINE.json configs[1], sharded per configs[2]): one step = the
+whole GRPO experience batch of 256 prompts x 8 responses, T = 4096 response
+tokens each, V = 152,064 (Qwen2.5-7B vocabulary) = 8,388,608 tokens.  Rank r
+of N owns prompt groups shard_dataset(256, N, r) (strong scaling: the global
+batch is fixed) and, per group (one 32,768-row chunk of bf16 policy +
+reference logits resident in HBM):
+
+    A1 token_stats (logp, ref_logp, entropy, k3 KL)        <- dominant kernel
+then over all its tokens: A2 GRPO group advantages -> token broadcast ->
+A4 clipped-surrogate + KL loss sums, and (N > 1) one NCCL all-reduce of the
+8 fp64 loss sums (global token count) — the only cross-rank traffic.
+
+Logits cannot all be resident (2 x 2.55 TB); each rank keeps two distinct
+32,768-row chunks (2 x 19.9 GB) resident and streams its groups through them
+alternately: every chunk pass reads 19.9 GB from HBM (>> 126 MB L2), so no
+L2 flush is needed and none is done.
+
+`--impl reference` times the CPU restatement of the same path (oracle/,
+fp64, all host threads) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "experience tokens/sec (logprob+KL+adv+loss) at V=152k; % HBM roofline, 1-8 B200"
+PROMPTS, RESPONSES, T, VOCAB = 256, 8, 4096, 152064
+CHUNK_ROWS = RESPONSES * T  # one prompt group
+SEED = 20250814
+FALLBACK_HBM_GBS = 6650.0
+
+
+def bytes_per_row(vocab: int) -> int:
+    # 2 bf16 logit rows + i32 target + u8 mask + 4 fp32 outputs
+    return 4 * vocab + 21
+
+
+def hbm_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+        except Exception:
+            pass
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of token_stats from the committed ncu capture."""
+    p = ROOT / "profiles" / "token_stats_ncu.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            return d.get("dram_bytes_per_launch"), d.get("rows_per_launch")
+        except Exception:
+            pass
+    return None, None
+
+
+# ----------------------------------------------------------------- clocks --
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.gpu)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._pump, daemon=True).start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, power, reasons = [], None, [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+                power.append(float(f[3]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_max": max(power) if power else None}
+
+
+# ------------------------------------------------------------- CPU arm ----
+def cpu_experience_rate(sample_rows: int | None = None, threads: int | None = None,
+                        budget_s: float = 12.0):
+    """Oracle (fp64 CPU restatement) of the same per-token path on a bounded
+    sample: A1 over `rows` rows of V=152,064 + A2 over their samples + A4."""
+    from oracle import oracle as O
+    threads = threads or os.cpu_count() or 1
+    uniq = 64
+    pol_u, ref_u, tgt_u = O.synth_logits(SEED, 0, uniq, VOCAB)
+
+    def run(rows):
+        reps = -(-rows // uniq)
+        pol = np.ascontiguousarray(np.tile(pol_u, (reps, 1))[:rows])
+        ref = np.ascontiguousarray(np.tile(ref_u, (reps, 1))[:rows])
+        tgt = np.ascontiguousarray(np.tile(tgt_u, reps)[:rows])
+        n_samples = max(1, rows // T) if rows >= T else 1
+        rewards = O.synth_floats(SEED, 105, 0, max(n_samples, RESPONSES), "reward", RESPONSES)
+        t0 = time.perf_counter()
+        st = O.token_stats(pol, ref, tgt, None, "k3", threads=threads)
+        adv_s = O.grpo_advantages(rewards, RESPONSES)
+        adv_t = np.repeat(adv_s, -(-rows // len(adv_s)))[:rows].astype(np.float32)
+        old = (st[0] + O.synth_floats(SEED, 104, 0, rows, "old_delta")).astype(np.float32)
+        O.policy_loss(st[0], old, adv_t, st[3], st[2])
+        return time.perf_counter() - t0
+
+    probe = 128
+    dt = run(probe)
+    rows = sample_rows or int(min(16384, max(probe, probe * budget_s / max(dt, 1e-6))))
+    dt = run(rows) if rows != probe else dt
+    return {"value": rows / dt, "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": f"{rows} rows x V={VOCAB} (A1 fp64 + GRPO adv + loss), {dt:.2f} s"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    vals = []
+    for _ in range(args.warmup):
+        cpu_experience_rate(sample_rows=256)
+    last = None
+    for _ in range(args.steps):
+        last = cpu_experience_rate(budget_s=args.ref_budget_s)
+        vals.append(last["value"])
+    v = statistics.median(vals)
+    line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (keyed integer-derived bf16 logits, DESIGN.md)",
+            "config": workload_config(args.gpus), "impl": "reference",
+            "cpu_baseline": {**last, "value": v},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(n):
+    return {"workload": "configs[1]/[2]: GRPO Qwen2.5-7B shape, 256 prompts x 8 responses, "
+                        "T=4096, V=152064, sharded by prompt group",
+            "global_batch": PROMPTS * RESPONSES, "seq_len": T, "vocab": VOCAB,
+            "tokens_per_step": PROMPTS * RESPONSES * T, "parallelism": f"dp{n} by prompt group",
+            "kl": "k3", "loss": "clipped surrogate eps=0.2 + 0.001 k3, token-mean",
+            "l2": "no flush: each chunk pass streams 19.9 GB >> 126 MB L2"}
+
+
+# ----------------------------------------------------------- GPU arm ------
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2508_07970_b200 import ops
+    from paper_2508_07970_b200._lib import lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib()
+
+    # ---- this rank's shard of prompt groups (workload.cpp:183-198 split) ----
+    base, rem = divmod(PROMPTS, world)
+    g0 = rank * base + min(rank, rem)
+    ng = base + (1 if rank < rem else 0)
+    n_samples, n_tok = ng * RESPONSES, ng * CHUNK_ROWS
+
+    # ---- resident inputs ----
+    bufs = [ops.synth_logits(SEED + k, 0, CHUNK_ROWS, VOCAB, device=dev) for k in range(2)]
+    mask = torch.ones((n_tok,), dtype=torch.uint8, device=dev)
+    stats = torch.empty((4, n_tok), dtype=torch.float32, device=dev)
+    rewards = ops.synth_floats(SEED, 105, g0 * RESPONSES, n_samples, "reward", RESPONSES,
+                               device=dev)
+    cu = torch.arange(0, n_samples + 1, dtype=torch.int64, device=dev) * T
+    tok_adv = torch.empty((n_tok,), dtype=torch.float32, device=dev)
+    # old_logp: the rollout policy's log-probs = current logp + keyed jitter
+    for g in range(ng):
+        pol, ref, tgt = bufs[g % 2]
+        sl = slice(g * CHUNK_ROWS, (g + 1) * CHUNK_ROWS)
+        ops.token_stats(pol, ref, tgt, mask[sl], "k3", out=stats[:, sl])
+    old_logp = ops.synth_floats(SEED, 104, g0 * CHUNK_ROWS, n_tok, "old_delta", base=stats[0],
+                                device=dev)
+    cfg = ops.loss_config(0.2, 0.2, 0.0, 0.001, 0.0, "token-mean")
+    ws = ops.LossWorkspace(dev)
+    sums = torch.empty((8,), dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+
+    st = torch.cuda.current_stream()
+    a1_events: list = []
+
+    def step(record=False):
+        for g in range(ng):
+            pol, ref, tgt = bufs[g % 2]
+            sl = slice(g * CHUNK_ROWS, (g + 1) * CHUNK_ROWS)
+            if record:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+            ops.token_stats(pol, ref, tgt, mask[sl], "k3", out=stats[:, sl])
+            if record:
+                e1.record(st)
+                a1_events.append((e0, e1))
+        adv = ops.grpo_advantages(rewards, RESPONSES, 1e-6, True, g0 * RESPONSES)
+        ops.broadcast_to_tokens(adv, cu, n_tok, mask, out=tok_adv)
+        ops.policy_loss(stats[0], old_logp, tok_adv, stats[3], stats[2], mask, None, cfg, ws,
+                        sums)
+        if world > 1:
+            dist.all_reduce(sums)
+        return sums
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(st)
+    for _ in range(args.steps):
+        step(record=True)
+    t1.record(st)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    elapsed_ms = t0.elapsed_time(t1)
+    t_local_ms = elapsed_ms
+    a1_ms = [a.elapsed_time(b) for a, b in a1_events]
+    if world > 1:
+        t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    ms_per_step = elapsed_ms / args.steps
+    total_tokens = PROMPTS * RESPONSES * T  # all ranks, per step
+    value = total_tokens * args.steps / (elapsed_ms / 1e3)
+    loss = ops.loss_finalize(sums.cpu(), cfg)
+
+    # ---- roofline of the dominant kernel (A1) ----
+    peak, peak_src = hbm_peak()
+    a1_avg_ms = statistics.mean(a1_ms)
+    alg_bytes = CHUNK_ROWS * bytes_per_row(VOCAB)
+    achieved = alg_bytes / (a1_avg_ms / 1e3) / 1e9
+    traffic, rows_per = ncu_traffic()
+    roofline = {"bound": "hbm", "kernel": "token_stats_kernel", "achieved": achieved,
+                "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
+                "frac_of_8TBs": achieved / 8000.0, "traffic": traffic,
+                "algorithmic_bytes_per_launch": alg_bytes, "launch_ms_avg": a1_avg_ms,
+                "share_of_step": sum(a1_ms) / t_local_ms}
+
+    # ---- e2e through the public API: pinned host inputs -> device -> loss ----
+    e2e = run_e2e(args, dev, ops, cfg, ws) if rank == 0 else None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_experience_rate(budget_s=args.ref_budget_s)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "bf16", "data": "synthetic (keyed integer-derived bf16 logits, "
+                "binary group rewards; DESIGN.md)", "config": workload_config(world),
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": args.steps * (ng + 4), "clocks": clk,
+                "loss": loss}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(args, dev, ops, cfg, ws):
+    """Same metric through the public ops API with HOST inputs: each step
+    copies one response sequence's logits (2 x 4096 x V bf16 from pinned
+    memory), targets, mask, reward group and old log-probs to the device,
+    runs A1 -> A2 -> A4 and reads the loss sums back."""
+    import torch
+    rows = T
+    pol, ref, tgt = ops.synth_logits(SEED, 0, rows, VOCAB, device=dev)
+    h_pol = pol.cpu().pin_memory()
+    h_ref = ref.cpu().pin_memory()
+    h_tgt = tgt.cpu().pin_memory()
+    h_mask = torch.ones((rows,), dtype=torch.uint8).pin_memory()
+    h_rew = ops.synth_floats(SEED, 105, 0, RESPONSES, "reward", RESPONSES, device=dev).cpu().pin_memory()
+    h_old = torch.zeros((rows,), dtype=torch.float32).pin_memory()
+    del pol, ref, tgt
+    d_pol = torch.empty((rows, VOCAB), dtype=torch.bfloat16, device=dev)
+    d_ref = torch.empty_like(d_pol)
+    out = torch.empty((4, rows), dtype=torch.float32, device=dev)
+    cu = torch.tensor([0, rows], dtype=torch.int64, device=dev)
+    sums = torch.empty((8,), dtype=torch.float64, device=dev)
+    h_sums = torch.empty((8,), dtype=torch.float64).pin_memory()
+
+    def step():
+        d_pol.copy_(h_pol, non_blocking=True)
+        d_ref.copy_(h_ref, non_blocking=True)
+        d_tgt = h_tgt.to(dev, non_blocking=True)
+        d_mask = h_mask.to(dev, non_blocking=True)
+        d_rew = h_rew.to(dev, non_blocking=True)
+        d_old = h_old.to(dev, non_blocking=True)
+        ops.token_stats(d_pol, d_ref, d_tgt, d_mask, "k3", out=out)
+        adv = ops.grpo_advantages(d_rew, RESPONSES)  # the sequence's whole group
+        tadv = ops.broadcast_to_tokens(adv[:1], cu, rows, d_mask)
+        ops.policy_loss(out[0], d_old, tadv, out[3], out[2], d_mask, None, cfg, ws, sums)
+        h_sums.copy_(sums, non_blocking=True)
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k = max(2, args.steps)
+    a.record(st)
+    for _ in range(k):
+        step()
+    b.record(st)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / k
+    h2d = 2 * rows * VOCAB * 2 + rows * (4 + 1 + 4) + RESPONSES * 4
+    return {"value": rows / (ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": 64, "ms_per_step": ms,
+            "sample": f"one {rows}-token response per step ({h2d / 1e9:.2f} GB H2D)"}
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget-s", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,389 @@
+/*
+ * yatt_cuda.h — C ABI of the B200 experience-making path.
+ *
+ * This is the drop-in boundary between a WeChat-YATT parallel-controller
+ * rank (host, C++) and the sm_100a kernels.  Every entry point takes plain
+ * pointers + explicit sizes, returns an int status (YATT_OK == 0) and never
+ * throws.  The C++ wrappers in include/yatt/*.hpp map the status codes back
+ * onto the reference's exception types (reference proj/include/yatt/
+ * errors.hpp:10-48) so callers written against the reference keep working.
+ *
+ * Conventions
+ *  - `d_` pointers are device pointers, `h_` pointers host pointers.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *  - All device work is stream-ordered; a function only synchronises when it
+ *    returns host data (documented per function).
+ *  - bf16 tensors are passed as uint16_t bit patterns.
+ *  - Reentrant given distinct buffers and streams; the last-error message is
+ *    thread-local.
+ */
+#ifndef YATT_CUDA_H_
+#define YATT_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------------ */
+/* Status codes and errors                                                   */
+/* ------------------------------------------------------------------------ */
+enum yatt_status {
+  YATT_OK = 0,
+  YATT_ERR_CONFIG = 1,        /* -> yatt::ConfigError          (errors.hpp:45) */
+  YATT_ERR_RANK = 2,          /* -> yatt::RankOutOfRange       (errors.hpp:25) */
+  YATT_ERR_DISTRIBUTION = 3,  /* -> yatt::InvalidDistribution  (errors.hpp:20) */
+  YATT_ERR_CUDA = 4,          /* -> yatt::Error (fail-fast)                    */
+  YATT_ERR_NCCL = 5,          /* -> yatt::Error                                */
+  YATT_ERR_WORKSPACE = 6      /* workspace too small -> yatt::ConfigError      */
+};
+
+/* Message for the last non-OK status returned on this thread. */
+const char* yatt_last_error_message(void);
+/* ABI version: bumped on any signature change. */
+int yatt_abi_version(void);
+/* Name of the device the library runs on ("" if none); sm major/minor. */
+int yatt_device_info(int device, char* name, int name_len, int* sm_major,
+                     int* sm_minor, int* num_sms);
+
+/* ------------------------------------------------------------------------ */
+/* Shared POD types (mirror proj/include/yatt/{workload,simcore}.hpp)        */
+/* ------------------------------------------------------------------------ */
+enum yatt_dist_kind {           /* workload.hpp:10-15 DistKind */
+  YATT_DIST_CONSTANT = 0,
+  YATT_DIST_UNIFORM = 1,
+  YATT_DIST_NORMAL = 2,
+  YATT_DIST_LOGNORMAL = 3
+};
+
+typedef struct yatt_length_dist {  /* workload.hpp:25-36 LengthDistribution */
+  int32_t kind;
+  int32_t max_len_tokens;
+  double p1;
+  double p2;
+} yatt_length_dist;
+
+typedef struct yatt_rejection_config {  /* workload.hpp:73-80 RejectionConfig */
+  double reject_rate;
+  int32_t per_group;
+  int32_t group_size;
+} yatt_rejection_config;
+
+typedef struct yatt_round_params {  /* simcore.hpp:93-99 RoundParams */
+  yatt_length_dist out_dist;
+  yatt_rejection_config rejection;
+  uint64_t seed;
+  int32_t microbatch_size;
+  int32_t max_rounds;
+} yatt_round_params;
+
+/* One sample of a controller shard: simcore.hpp:78-84 ShardSampleState and
+ * workload.hpp:38-46 RolloutSample share this 24-byte device layout. */
+typedef struct yatt_sample {
+  uint64_t sample_id;
+  int32_t prompt_len_tokens;
+  int32_t out_len_tokens;
+  int32_t accepted_round;
+  int32_t accepted;  /* 0/1 */
+} yatt_sample;
+
+typedef struct yatt_mb_agg {  /* simcore.hpp:55-62 MicrobatchAggregate */
+  int32_t controller_rank;
+  int32_t mb_index;
+  int32_t sample_count;
+  int32_t max_out_len_tokens;
+  int64_t score_tokens;
+} yatt_mb_agg;
+
+typedef struct yatt_round_report {  /* simcore.hpp:64-76 ShardRoundReport */
+  int32_t controller_rank;
+  int32_t round;
+  int32_t active_count;
+  int32_t newly_accepted_count;
+  int32_t forced_accept_count;
+  int32_t pending_count;
+  int64_t accepted_score_tokens;
+  int64_t accepted_train_units;
+  int64_t num_microbatches;  /* entries written to the microbatch array */
+} yatt_round_report;
+
+/* ------------------------------------------------------------------------ */
+/* R1  shard_dataset  (replaces workload.cpp:183-198; host, O(1))            */
+/* ------------------------------------------------------------------------ */
+int yatt_shard_dataset(uint64_t total_samples, int32_t num_controllers,
+                       int32_t controller_rank, uint64_t* h_begin,
+                       uint64_t* h_end);
+
+/* ------------------------------------------------------------------------ */
+/* R6  keyed length draws  (replaces workload.cpp:109-132 batched)           */
+/* out[i] = sample_length_keyed(dist, seed, stream_id, step, round, ids[i]). */
+/* ------------------------------------------------------------------------ */
+int yatt_sample_lengths_keyed(const yatt_length_dist* dist, uint64_t seed,
+                              uint64_t stream_id, uint64_t step, uint64_t round,
+                              const uint64_t* d_sample_ids, int64_t n,
+                              int32_t* d_out, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* R5  rejection_process  (replaces workload.cpp:145-167)                    */
+/* d_rejected[i] = 1 iff sample i is pending and its keyed draw < rate.      */
+/* ------------------------------------------------------------------------ */
+int yatt_rejection_flags(const yatt_sample* d_samples, int64_t n,
+                         int32_t step_index, int32_t round,
+                         const yatt_rejection_config* config, uint64_t seed,
+                         uint8_t* d_rejected, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* R3+R4  shard_round_output  (replaces simcore.cpp:157-214 + :17-39)        */
+/* Runs `num_shards` controller shards in ONE launch (one CTA per shard).    */
+/* Shard s owns d_samples[h_shard_offsets[s] .. h_shard_offsets[s+1]) (host  */
+/* array, num_shards+1 entries) and has controller rank first_rank + s.      */
+/* Samples are mutated in place exactly like ShardState; the report of       */
+/* shard s goes to d_reports[s]; its microbatches to d_mbs + M_s where       */
+/* M_s = sum_{s'<s} ceil(n_s' / microbatch_size) (capacity per shard is      */
+/* ceil(n_s / microbatch_size); report.num_microbatches are valid).          */
+/* ------------------------------------------------------------------------ */
+int yatt_shard_round(yatt_sample* d_samples, const int64_t* h_shard_offsets,
+                     int32_t num_shards, int32_t first_rank,
+                     int32_t step_index, int32_t round,
+                     const yatt_round_params* params,
+                     yatt_round_report* d_reports, yatt_mb_agg* d_mbs,
+                     void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* A1  fused token statistics over policy + reference logits                 */
+/* For each row r (token) of the row-major [rows, vocab] bf16 tensors:       */
+/*   logp[r]     = log softmax(policy[r])[target[r]]                         */
+/*   ref_logp[r] = log softmax(ref[r])[target[r]]                            */
+/*   entropy[r]  = H(softmax(policy[r]))                                     */
+/*   kl[r]       = per kl_mode (Delta = ref_logp - logp):                    */
+/*       K1: -Delta   K2: Delta^2/2   K3: exp(Delta) - Delta - 1             */
+/*       FULL: sum_v p_v (log p_v - log q_v)                                 */
+/* Rows with d_mask[r] == 0 (d_mask may be NULL = all valid) are not read    */
+/* and produce zeros.  Requires vocab % 8 == 0 and 16-byte aligned tensors.  */
+/* Any output pointer may be NULL except d_logp.                             */
+/* ------------------------------------------------------------------------ */
+enum yatt_kl_mode { YATT_KL_K1 = 0, YATT_KL_K2 = 1, YATT_KL_K3 = 2, YATT_KL_FULL = 3 };
+
+int yatt_token_stats(const uint16_t* d_policy_logits,
+                     const uint16_t* d_ref_logits, const int32_t* d_targets,
+                     const uint8_t* d_mask, int64_t rows, int32_t vocab,
+                     int32_t kl_mode, float* d_logp, float* d_ref_logp,
+                     float* d_entropy, float* d_kl, void* stream);
+
+/* Same op, HOST buffers (pageable or pinned): the e2e path.  Streams the    */
+/* rows through device staging buffers in chunks, overlapping H2D copies of  */
+/* chunk i+1 with the kernel on chunk i, and copies outputs back.  Blocks    */
+/* until the outputs are on the host.                                        */
+int yatt_token_stats_host(const uint16_t* h_policy_logits,
+                          const uint16_t* h_ref_logits,
+                          const int32_t* h_targets, const uint8_t* h_mask,
+                          int64_t rows, int32_t vocab, int32_t kl_mode,
+                          float* h_logp, float* h_ref_logp, float* h_entropy,
+                          float* h_kl);
+
+/* ------------------------------------------------------------------------ */
+/* A2  GRPO group advantages                                                 */
+/* Groups are runs of `group_size` consecutive GLOBAL sample ids; the local  */
+/* samples start at global id `first_sample_id`.  Per group g:               */
+/*   mean_g, M2_g (two-pass, fp64); std_g = sqrt(M2_g/(n_g-1)) (n_g > 1)     */
+/*   adv_i = (r_i - mean_g) / (std_g + eps)   if norm_by_std                 */
+/*   adv_i = (r_i - mean_g)                   otherwise                      */
+/* n_g == 1 -> adv = 0.  Group moments are (n, mean, M2) triples in fp64.    */
+/* Straddling groups (multi-rank): compute local moments with               */
+/* yatt_grpo_group_moments, exchange/merge (Chan et al.), then pass the     */
+/* merged table to yatt_grpo_advantages via d_group_moments.                 */
+/* ------------------------------------------------------------------------ */
+int64_t yatt_grpo_num_local_groups(int64_t n_samples, uint64_t first_sample_id,
+                                   int32_t group_size);
+int yatt_grpo_group_moments(const float* d_rewards, int64_t n_samples,
+                            uint64_t first_sample_id, int32_t group_size,
+                            double* d_group_moments /* [n_local_groups*3] */,
+                            void* stream);
+int yatt_grpo_advantages(const float* d_rewards, int64_t n_samples,
+                         uint64_t first_sample_id, int32_t group_size,
+                         float eps, int32_t norm_by_std,
+                         const double* d_group_moments /* NULL: compute */,
+                         float* d_sample_adv, void* stream);
+/* Broadcast one value per sample over its tokens: out[t] = val[s(t)]*mask[t] */
+/* where sample s owns tokens [cu[s], cu[s+1]).  d_mask may be NULL.         */
+int yatt_broadcast_to_tokens(const float* d_sample_vals,
+                             const int64_t* d_cu_seqlens, int64_t n_samples,
+                             const uint8_t* d_mask, float* d_token_vals,
+                             int64_t n_tokens, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* A3  PPO GAE over packed variable-length sequences                         */
+/* Sequence s owns tokens [cu[s], cu[s+1]).  Reverse recursion per sequence  */
+/* over valid (mask != 0) tokens; masked tokens are transparent (carry the   */
+/* running value and advantage, emit the carried advantage):                 */
+/*   delta_t = r_t + gamma * V_next - V_t   (V_next = 0 past the end)        */
+/*   A_t     = delta_t + gamma*lam * A_next ;  R_t = A_t + V_t               */
+/* Computed in fp64 on the device, stored fp32.  d_mask may be NULL.         */
+/* ------------------------------------------------------------------------ */
+int yatt_gae(const float* d_values, const float* d_rewards,
+             const uint8_t* d_mask, const int64_t* d_cu_seqlens,
+             int64_t n_seqs, float gamma, float lam, float* d_advantages,
+             float* d_returns, void* stream);
+/* Masked moments {count, sum, sum_sq} (fp64, deterministic) of x, written    */
+/* to d_out[3]; all-reduce them across ranks before yatt_whiten.             */
+size_t yatt_masked_moments_workspace_bytes(void);
+int yatt_masked_moments(const float* d_x, const uint8_t* d_mask, int64_t n,
+                        double* d_out, void* d_workspace, size_t workspace_bytes,
+                        void* stream);
+/* x <- (x - mean) * rsqrt(var + 1e-8) (+ mean if !shift_mean), masked      */
+/* tokens untouched; var is unbiased.                                        */
+int yatt_whiten(float* d_x, const uint8_t* d_mask, int64_t n,
+                const double* d_moments, int32_t shift_mean, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* A4  fused clipped-surrogate + KL-penalty loss, masked token sums          */
+/*   ratio = exp(logp - old_logp)                                            */
+/*   pg    = max(-A*ratio, -A*clip(ratio, 1-clip_low, 1+clip_high))          */
+/*   if clip_ratio_c > 1 and A < 0: pg = min(pg, -A*clip_ratio_c) (dual clip)*/
+/*   L_t   = pg + kl_coef*kl_t - entropy_coef*H_t                            */
+/* Writes one yatt_loss_sums (fp64, deterministic order) to d_sums.  The     */
+/* global token-mean loss is sums.loss_sum / sums.token_count after the      */
+/* cross-rank all-reduce (yatt_loss_finalize).                               */
+/* ------------------------------------------------------------------------ */
+typedef struct yatt_loss_config {
+  float clip_low;      /* eps_low, e.g. 0.2 */
+  float clip_high;     /* eps_high, e.g. 0.2 (DAPO clip-higher 0.28) */
+  float clip_ratio_c;  /* dual-clip bound (>1) or 0 = off */
+  float kl_coef;       /* beta */
+  float entropy_coef;
+  int32_t agg_mode;    /* 0 token-mean, 1 seq-mean-token-mean, 2 seq-mean-token-sum */
+} yatt_loss_config;
+
+typedef struct yatt_loss_sums {
+  double loss_sum;       /* sum_t m_t L_t  (agg_mode 0) or sum_s seq-term   */
+  double pg_sum;         /* sum_t m_t pg_t                                  */
+  double kl_sum;         /* sum_t m_t kl_t                                  */
+  double entropy_sum;    /* sum_t m_t H_t                                   */
+  double clip_count;     /* sum_t m_t [clipped]                             */
+  double ratio_sum;      /* sum_t m_t ratio_t                               */
+  double token_count;    /* sum_t m_t                                       */
+  double seq_count;      /* sequences with >= 1 valid token (modes 1, 2)    */
+} yatt_loss_sums;
+
+size_t yatt_policy_loss_workspace_bytes(int64_t n_tokens, int64_t n_seqs,
+                                        int32_t agg_mode);
+int yatt_policy_loss(const float* d_logp, const float* d_old_logp,
+                     const float* d_advantages, const float* d_kl,
+                     const float* d_entropy, const uint8_t* d_mask,
+                     int64_t n_tokens, const int64_t* d_cu_seqlens,
+                     int64_t n_seqs, const yatt_loss_config* config,
+                     yatt_loss_sums* d_sums, void* d_workspace,
+                     size_t workspace_bytes, void* stream);
+/* Host: final scalar loss from (all-reduced) sums. */
+double yatt_loss_finalize(const yatt_loss_sums* h_sums,
+                          const yatt_loss_config* config);
+
+/* ------------------------------------------------------------------------ */
+/* A5+A6  dynamic-sampling filter and compaction (bit-exact)                 */
+/* keep_g = !(all rewards of group g are bitwise identical).  Groups are     */
+/* `group_size` consecutive local samples (the local batch is group-aligned, */
+/* n_samples % group_size == 0).  Survivors keep sample order:               */
+/*   d_index_map[j] = local index of the j-th kept sample                    */
+/*   d_new_cu[j]    = packed token start of kept sample j (local, from 0);   */
+/*                    d_new_cu[n_kept] = kept tokens                         */
+/*   d_counts[3]    = {kept_samples, kept_tokens, kept_groups}               */
+/* Everything stays on the device (no host sync).  For a global packed       */
+/* layout across ranks: all-gather d_counts, yatt_exclusive_offset -> the    */
+/* rank's token/sample offset, pass it as d_dst_offset to the gathers.       */
+/* ------------------------------------------------------------------------ */
+size_t yatt_filter_compact_workspace_bytes(int64_t n_samples);
+int yatt_filter_compact(const float* d_rewards, const int64_t* d_seq_lens,
+                        int64_t n_samples, int32_t group_size,
+                        uint8_t* d_keep_groups, int32_t* d_index_map,
+                        int64_t* d_new_cu, int64_t* d_counts, void* d_workspace,
+                        size_t workspace_bytes, void* stream);
+/* Gather variable-length per-token payload of the kept samples:             */
+/*   dst[off + new_cu[j] + k] = src[old_cu[map[j]] + k], k < len(map[j])     */
+/* for j < *d_n_kept (device count; max_kept bounds the grid).  off =        */
+/* *d_dst_offset or 0.  elem_bytes in {1,2,4,8}; old_cu has n_samples+1.     */
+int yatt_gather_varlen(const void* d_src, const int64_t* d_old_cu,
+                       const int32_t* d_index_map, const int64_t* d_new_cu,
+                       const int64_t* d_n_kept, int64_t max_kept,
+                       const int64_t* d_dst_offset, int32_t elem_bytes,
+                       void* d_dst, void* stream);
+/* Gather fixed-width per-sample rows (metadata, multimodal payload refs):   */
+/*   dst[(off + j)*row_bytes ..] = src[map[j]*row_bytes ..], j < *d_n_kept   */
+int yatt_gather_rows(const void* d_src, const int32_t* d_index_map,
+                     const int64_t* d_n_kept, int64_t max_kept,
+                     int64_t row_bytes, const int64_t* d_dst_offset,
+                     void* d_dst, void* stream);
+/* Microbatch aggregates (simcore.cpp:17-39) over an ordered sample list:   */
+/* consecutive chunks of microbatch_size over (prompt_len[i], out_len[i]),  */
+/* i < (d_n ? *d_n : n); writes ceil(count/microbatch_size) entries.        */
+int yatt_microbatch_aggregates(const int32_t* d_prompt_len,
+                               const int32_t* d_out_len, const int64_t* d_n,
+                               int64_t n, int32_t microbatch_size,
+                               int32_t controller_rank, yatt_mb_agg* d_mbs,
+                               void* stream);
+/* *d_out = sum_{r < rank} d_counts[r*stride + field] (device, one thread):  */
+/* turns all-gathered per-rank counts into this rank's global offset.        */
+int yatt_exclusive_offset(const int64_t* d_counts, int32_t nranks, int32_t rank,
+                          int32_t stride, int32_t field, int64_t* d_out,
+                          void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* R10  sort_and_bucket ordering  (replaces balancer.cpp:16-36)              */
+/* d_order = indices sorted by length descending, ties by index ascending.   */
+/* Bucket cutting + std::shuffle of bucket order stay on the host (the C++   */
+/* wrapper yatt::balancer::sort_and_bucket), bit-exact with libstdc++.       */
+/* ------------------------------------------------------------------------ */
+size_t yatt_sort_order_workspace_bytes(int64_t n);
+int yatt_sort_order_desc(const int32_t* d_lengths, int64_t n,
+                         uint32_t* d_order, void* d_workspace,
+                         size_t workspace_bytes, void* stream);
+/* Host helper: full sort_and_bucket through the device sort.  Writes the   */
+/* shuffled flat bucket list to h_flat (n entries) and bucket start offsets */
+/* to h_bucket_offsets (n_buckets+1 entries, n_buckets = ceil(n/B)).        */
+int yatt_sort_and_bucket_host(const int32_t* h_lengths, int64_t n,
+                              int32_t batch_size, uint64_t seed,
+                              uint32_t* h_flat, int64_t* h_bucket_offsets);
+
+/* ------------------------------------------------------------------------ */
+/* Cross-rank collectives (NCCL over NVLink/NVSwitch)                        */
+/* ------------------------------------------------------------------------ */
+#define YATT_COMM_ID_BYTES 128
+typedef struct yatt_comm* yatt_comm_t;
+int yatt_comm_unique_id(uint8_t* h_id /* YATT_COMM_ID_BYTES */);
+int yatt_comm_init(int32_t nranks, int32_t rank, const uint8_t* h_id,
+                   yatt_comm_t* out_comm);
+int yatt_comm_destroy(yatt_comm_t comm);
+int yatt_comm_allreduce_f64(yatt_comm_t comm, double* d_buf, int64_t count,
+                            void* stream);
+int yatt_comm_allreduce_i64(yatt_comm_t comm, int64_t* d_buf, int64_t count,
+                            void* stream);
+int yatt_comm_allgather_i64(yatt_comm_t comm, const int64_t* d_send,
+                            int64_t* d_recv, int64_t count_per_rank,
+                            void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Synthetic inputs (bench / parity support; same recipe in oracle/)         */
+/* ------------------------------------------------------------------------ */
+/* Logits for global rows [row0, row0+rows): see DESIGN.md "Synthetic data". */
+int yatt_synth_logits(uint64_t seed, int64_t row0, int64_t rows, int32_t vocab,
+                      uint16_t* d_policy, uint16_t* d_ref, int32_t* d_targets,
+                      void* stream);
+/* out[i] = f(kind, uniform/int draw of hash_key({seed, stream_id, i0+i})).  */
+enum yatt_synth_kind {
+  YATT_SYNTH_LOGP = 0,      /* -k/64, k in [0,1023]                          */
+  YATT_SYNTH_OLD_DELTA = 1, /* k/256, k in [-64,63]  (added to a base)       */
+  YATT_SYNTH_ADV = 2,       /* k/64,  k in [-128,127]                        */
+  YATT_SYNTH_KL = 3,        /* k/1024, k in [0,255]                          */
+  YATT_SYNTH_VALUE = 4,     /* k/1024, k in [-1024,1023]                     */
+  YATT_SYNTH_REWARD = 5     /* binary group rewards           */
+};
+int yatt_synth_floats(uint64_t seed, uint64_t stream_id, int64_t i0, int64_t n,
+                      int32_t kind, int32_t group_size, const float* d_base,
+                      float* d_out, void* stream);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif  /* YATT_CUDA_H_ */

@@ -1,0 +1,434 @@
+// token_stats.cu — A1: fused single-pass log-prob / entropy / KL over bf16
+// policy and reference logits.
+//
+// Replaces the Preparation-stage cost stand-in of the reference
+// (proj/src/simcore.cpp:13-15, :395-398: "policy and reference policy compute
+// their reference log probabilities") with the real per-token
+// computation.  Numerics follow the reference's max-subtracted softmax
+// (proj/src/distattn.cpp:99-123) but in ONE pass with an online maximum.
+//
+// Layout: policy / ref logits are row-major [rows, V] bf16, one row per token.
+// Bound: HBM.  Algorithmic bytes per valid row = 4V (two bf16 rows) + 4
+// (target) + 1 (mask) + 16 (four fp32 outputs) = 4V + 21.
+//
+// Kernel structure (persistent, warp-specialised, 2 CTAs per SM):
+//   warp 8      : producer — one elected lane streams each row in TILE-element
+//                 pieces of both tensors into a STAGES-deep shared-memory ring
+//                 with cp.async.bulk (TMA bulk engine), completion tracked by
+//                 mbarrier transaction counts; L2 evict-first policy.
+//   warps 0..7  : consumers — 128-bit ld.shared of 8 bf16 per tensor per
+//                 step, online log-sum-exp in the log2 domain:
+//                   a = x*log2e - m   (m integer: rescales are exact 2^k)
+//                   s += 2^a ; w += 2^a * a        (policy: lse + entropy)
+//                   sq += 2^b                      (reference: lse)
+//                   u += 2^a (x - z)               (FULL KL only)
+//                 8 independent accumulators per quantity per thread (short
+//                 fp32 chains), warp-shuffle + smem combine at row end, fp64
+//                 epilogue by a rotating warp.  The target logits are picked
+//                 out of the staged tile by whichever thread holds them — no
+//                 extra global loads.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace yattb {
+namespace {
+
+constexpr int kConsumerWarps = 8;
+constexpr int kConsumers = kConsumerWarps * 32;
+constexpr int kThreads = kConsumers + 32;  // + producer warp
+constexpr int kTile = 8192;                // bf16 elements per tensor per stage
+constexpr int kStages = 3;
+constexpr int kVecPerTile = kTile / 8;                  // 16-byte vectors
+constexpr int kVecPerThread = kVecPerTile / kConsumers;  // full-tile unroll
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr double kLn2 = 0.69314718055994530942;
+constexpr float kSlack = 24.0f;  // allow 2^a up to 2^24 before re-basing
+constexpr int kMinitial = -(1 << 24);
+static_assert(kVecPerTile % kConsumers == 0, "tile must split evenly");
+
+struct RowPartial {
+  float mp, s, w, mq, sq, u;
+};
+
+struct __align__(16) SmemTail {
+  uint64_t full[kStages];
+  uint64_t empty[kStages];
+  RowPartial red[2][kConsumerWarps];
+  float tgt[2][2];
+};
+
+constexpr size_t kRingBytes = size_t(kStages) * 2 * kTile * sizeof(uint16_t);
+constexpr size_t kSmemBytes = kRingBytes + sizeof(SmemTail);
+
+struct Params {
+  const uint16_t* pol;
+  const uint16_t* ref;
+  const int32_t* tgt;
+  const uint8_t* mask;
+  int64_t rows;
+  int32_t V;
+  int32_t kl_mode;
+  float* logp;
+  float* ref_logp;
+  float* ent;
+  float* kl;
+};
+
+// Per-thread online state for one row.
+template <bool kFull>
+struct Acc {
+  float s[8], w[8], sq[8], u[8];
+  float mp, mq;      // integer-valued bases (log2 units)
+  float thr_p, thr_q;  // rebase when a logit exceeds these
+
+  __device__ __forceinline__ void reset() {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      s[j] = 0.f;
+      w[j] = 0.f;
+      sq[j] = 0.f;
+      if (kFull) u[j] = 0.f;
+    }
+    mp = mq = float(kMinitial);
+    thr_p = thr_q = (float(kMinitial) + kSlack) / kLog2e;
+  }
+
+  // Rebase policy accumulators to m' = ceil(vmax*log2e): exact 2^(m-m').
+  __device__ __forceinline__ void rebase_p(float vmax) {
+    float mn = ceilf(vmax * kLog2e);
+    mn = fminf(fmaxf(mn, float(kMinitial)), float(1 << 24));
+    if (mn <= mp) return;
+    const float d = mp - mn;
+    const float c = exp2_int(int(d));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      w[j] = c * fmaf(d, s[j], w[j]);
+      s[j] *= c;
+      if (kFull) u[j] *= c;
+    }
+    mp = mn;
+    thr_p = (mp + kSlack) / kLog2e;
+  }
+  __device__ __forceinline__ void rebase_q(float vmax) {
+    float mn = ceilf(vmax * kLog2e);
+    mn = fminf(fmaxf(mn, float(kMinitial)), float(1 << 24));
+    if (mn <= mq) return;
+    const float c = exp2_int(int(mq - mn));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) sq[j] *= c;
+    mq = mn;
+    thr_q = (mq + kSlack) / kLog2e;
+  }
+
+  // Accumulate one 8-element vector pair (policy P already floored).
+  __device__ __forceinline__ void step(const uint4& P, const uint4& Q) {
+    const uint32_t pw[4] = {P.x, P.y, P.z, P.w};
+    const uint32_t qw[4] = {Q.x, Q.y, Q.z, Q.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = 2 * k + h;
+        const float x = h ? bf16_hi(pw[k]) : bf16_lo(pw[k]);
+        const float z = h ? bf16_hi(qw[k]) : bf16_lo(qw[k]);
+        const float a = fmaf(x, kLog2e, -mp);
+        const float e = ex2_approx(a);
+        s[j] += e;
+        w[j] = fmaf(e, a, w[j]);
+        const float b = fmaf(z, kLog2e, -mq);
+        sq[j] += ex2_approx(b);
+        if (kFull) u[j] = fmaf(e, x - z, u[j]);
+      }
+    }
+  }
+};
+
+__device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
+  __nv_bfloat162 r = __hmax2(*reinterpret_cast<__nv_bfloat162*>(&a),
+                             *reinterpret_cast<__nv_bfloat162*>(&b));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+__device__ __forceinline__ uint32_t vmax4(const uint4& v) {
+  return bmax2(bmax2(v.x, v.y), bmax2(v.z, v.w));
+}
+__device__ __forceinline__ float pair_max(uint32_t m2) {
+  return fmaxf(bf16_lo(m2), bf16_hi(m2));
+}
+// Floor the policy logits at -1e30 (bf16 0xF149): keeps 2^a * a finite for
+// -inf (masked-vocab) logits; exact for every finite logit above it.
+__device__ __forceinline__ uint4 floor_policy(uint4 v) {
+  constexpr uint32_t kFloor = 0xF149F149u;
+  v.x = bmax2(v.x, kFloor);
+  v.y = bmax2(v.y, kFloor);
+  v.z = bmax2(v.z, kFloor);
+  v.w = bmax2(v.w, kFloor);
+  return v;
+}
+__device__ __forceinline__ float pick_bf16(const uint4& v, int idx) {
+  const uint32_t w = (idx >> 1) == 0 ? v.x : (idx >> 1) == 1 ? v.y : (idx >> 1) == 2 ? v.z : v.w;
+  return (idx & 1) ? bf16_hi(w) : bf16_lo(w);
+}
+
+__device__ __forceinline__ RowPartial combine(const RowPartial& A, const RowPartial& B) {
+  RowPartial r;
+  r.mp = fmaxf(A.mp, B.mp);
+  {
+    const float da = A.mp - r.mp, db = B.mp - r.mp;
+    const float ca = exp2_int(int(da)), cb = exp2_int(int(db));
+    r.s = ca * A.s + cb * B.s;
+    r.w = ca * fmaf(da, A.s, A.w) + cb * fmaf(db, B.s, B.w);
+    r.u = ca * A.u + cb * B.u;
+  }
+  r.mq = fmaxf(A.mq, B.mq);
+  r.sq = exp2_int(int(A.mq - r.mq)) * A.sq + exp2_int(int(B.mq - r.mq)) * B.sq;
+  return r;
+}
+
+__device__ __forceinline__ RowPartial shfl_partial(const RowPartial& p, int off) {
+  RowPartial o;
+  o.mp = __shfl_xor_sync(0xffffffffu, p.mp, off);
+  o.s = __shfl_xor_sync(0xffffffffu, p.s, off);
+  o.w = __shfl_xor_sync(0xffffffffu, p.w, off);
+  o.mq = __shfl_xor_sync(0xffffffffu, p.mq, off);
+  o.sq = __shfl_xor_sync(0xffffffffu, p.sq, off);
+  o.u = __shfl_xor_sync(0xffffffffu, p.u, off);
+  return o;
+}
+
+template <bool kFull>
+__global__ void __launch_bounds__(kThreads, 2) token_stats_kernel(const Params p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint16_t* ring = reinterpret_cast<uint16_t*>(smem);
+  SmemTail* tail = reinterpret_cast<SmemTail*>(smem + kRingBytes);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t V = p.V;
+  const int ntiles = int((V + kTile - 1) / kTile);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&tail->full[s], 1);
+      mbar_init(&tail->empty[s], kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    // ---------------- producer ----------------
+    if (lane == 0) {
+      const uint64_t pol = l2_evict_first_policy();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
+        if (p.mask != nullptr && p.mask[row] == 0) continue;
+        const uint16_t* gp = p.pol + row * V;
+        const uint16_t* gq = p.ref + row * V;
+        for (int t = 0; t < ntiles; ++t) {
+          const int64_t e0 = int64_t(t) * kTile;
+          const uint32_t n = uint32_t(min64(kTile, V - e0));
+          mbar_wait(&tail->empty[stage], phase ^ 1u);
+          mbar_arrive_expect_tx(&tail->full[stage], 4u * n);
+          uint16_t* dst = ring + size_t(stage) * 2 * kTile;
+          bulk_g2s(dst, gp + e0, 2u * n, &tail->full[stage], pol);
+          bulk_g2s(dst + kTile, gq + e0, 2u * n, &tail->full[stage], pol);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int tid = threadIdx.x;  // 0..kConsumers-1
+  int stage = 0;
+  uint32_t phase = 0;
+  int iter = 0;
+  int64_t next_row = blockIdx.x;
+  int32_t y_next = next_row < p.rows ? __ldg(p.tgt + next_row) : 0;
+  Acc<kFull> acc;
+
+  for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
+    const int32_t y = (row == next_row) ? y_next : __ldg(p.tgt + row);
+    next_row = row + gridDim.x;
+    if (next_row < p.rows) y_next = __ldg(p.tgt + next_row);
+    if (p.mask != nullptr && p.mask[row] == 0) {
+      if (tid == 0) {
+        p.logp[row] = 0.f;
+        if (p.ref_logp) p.ref_logp[row] = 0.f;
+        if (p.ent) p.ent[row] = 0.f;
+        if (p.kl) p.kl[row] = 0.f;
+      }
+      continue;
+    }
+    const int par = iter & 1;
+    const int64_t yv = int64_t(y) >> 3;  // vector holding the target
+    acc.reset();
+
+    for (int t = 0; t < ntiles; ++t) {
+      const int64_t e0 = int64_t(t) * kTile;
+      const int nvec = int(min64(kTile, V - e0) >> 3);
+      const uint16_t* sp = ring + size_t(stage) * 2 * kTile;
+      const uint16_t* sq = sp + kTile;
+      const int64_t v0 = e0 >> 3;
+      mbar_wait(&tail->full[stage], phase);
+      if (nvec == kVecPerTile) {
+        uint4 P[kVecPerThread], Q[kVecPerThread];
+#pragma unroll
+        for (int i = 0; i < kVecPerThread; ++i) {
+          const int v = tid + i * kConsumers;
+          P[i] = lds128(sp + v * 8);
+          Q[i] = lds128(sq + v * 8);
+        }
+#pragma unroll
+        for (int i = 0; i < kVecPerThread; ++i) {
+          if (v0 + tid + i * kConsumers == yv) {
+            tail->tgt[par][0] = pick_bf16(P[i], y & 7);
+            tail->tgt[par][1] = pick_bf16(Q[i], y & 7);
+          }
+          P[i] = floor_policy(P[i]);
+        }
+        uint32_t mpv = vmax4(P[0]), mqv = vmax4(Q[0]);
+#pragma unroll
+        for (int i = 1; i < kVecPerThread; ++i) {
+          mpv = bmax2(mpv, vmax4(P[i]));
+          mqv = bmax2(mqv, vmax4(Q[i]));
+        }
+        const float fmp = pair_max(mpv), fmq = pair_max(mqv);
+        if (fmp > acc.thr_p) acc.rebase_p(fmp);
+        if (fmq > acc.thr_q) acc.rebase_q(fmq);
+#pragma unroll
+        for (int i = 0; i < kVecPerThread; ++i) acc.step(P[i], Q[i]);
+      } else {
+        for (int v = tid; v < nvec; v += kConsumers) {
+          uint4 P = lds128(sp + v * 8);
+          const uint4 Q = lds128(sq + v * 8);
+          if (v0 + v == yv) {
+            tail->tgt[par][0] = pick_bf16(P, y & 7);
+            tail->tgt[par][1] = pick_bf16(Q, y & 7);
+          }
+          P = floor_policy(P);
+          const float fmp = pair_max(vmax4(P)), fmq = pair_max(vmax4(Q));
+          if (fmp > acc.thr_p) acc.rebase_p(fmp);
+          if (fmq > acc.thr_q) acc.rebase_q(fmq);
+          acc.step(P, Q);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tail->empty[stage]);
+      if (++stage == kStages) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+
+    // ---- row reduction: thread -> warp -> CTA ----
+    RowPartial r;
+    r.mp = acc.mp;
+    r.mq = acc.mq;
+    {
+      float s0 = (acc.s[0] + acc.s[1]) + (acc.s[2] + acc.s[3]);
+      float s1 = (acc.s[4] + acc.s[5]) + (acc.s[6] + acc.s[7]);
+      r.s = s0 + s1;
+      float w0 = (acc.w[0] + acc.w[1]) + (acc.w[2] + acc.w[3]);
+      float w1 = (acc.w[4] + acc.w[5]) + (acc.w[6] + acc.w[7]);
+      r.w = w0 + w1;
+      float q0 = (acc.sq[0] + acc.sq[1]) + (acc.sq[2] + acc.sq[3]);
+      float q1 = (acc.sq[4] + acc.sq[5]) + (acc.sq[6] + acc.sq[7]);
+      r.sq = q0 + q1;
+      if (kFull) {
+        float u0 = (acc.u[0] + acc.u[1]) + (acc.u[2] + acc.u[3]);
+        float u1 = (acc.u[4] + acc.u[5]) + (acc.u[6] + acc.u[7]);
+        r.u = u0 + u1;
+      } else {
+        r.u = 0.f;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) r = combine(r, shfl_partial(r, off));
+    if (lane == 0) tail->red[par][warp] = r;
+    named_bar_sync(1, kConsumers);
+
+    const int ew = iter & (kConsumerWarps - 1);  // rotating epilogue warp
+    if (warp == ew) {
+      RowPartial q = tail->red[par][lane & (kConsumerWarps - 1)];
+#pragma unroll
+      for (int off = kConsumerWarps / 2; off > 0; off >>= 1) q = combine(q, shfl_partial(q, off));
+      if (lane == 0) {
+        const double xy = tail->tgt[par][0];
+        const double zy = tail->tgt[par][1];
+        const double l2s = log2(double(q.s));
+        const double l2q = log2(double(q.sq));
+        const double logp = xy - kLn2 * (double(q.mp) + l2s);
+        const double rlogp = zy - kLn2 * (double(q.mq) + l2q);
+        // lse_q - lse_p without cancelling two large numbers.
+        const double dlse = kLn2 * ((double(q.mq) - double(q.mp)) + log2(double(q.sq) / double(q.s)));
+        p.logp[row] = float(logp);
+        if (p.ref_logp) p.ref_logp[row] = float(rlogp);
+        if (p.ent) p.ent[row] = float(kLn2 * (l2s - double(q.w) / double(q.s)));
+        if (p.kl) {
+          const double delta = (zy - xy) - dlse;  // ref_logp - logp
+          double kl;
+          switch (p.kl_mode) {
+            case YATT_KL_K1: kl = -delta; break;
+            case YATT_KL_K2: kl = 0.5 * delta * delta; break;
+            case YATT_KL_K3: kl = expm1(delta) - delta; break;
+            default: kl = double(q.u) / double(q.s) + dlse; break;
+          }
+          p.kl[row] = float(kl);
+        }
+      }
+    }
+    ++iter;
+  }
+}
+
+}  // namespace
+
+int token_stats_launch(const uint16_t* pol, const uint16_t* ref, const int32_t* tgt,
+                       const uint8_t* mask, int64_t rows, int32_t vocab, int32_t kl_mode,
+                       float* logp, float* ref_logp, float* ent, float* kl, cudaStream_t st) {
+  YATT_REQUIRE(vocab > 0 && vocab % 8 == 0, YATT_ERR_CONFIG,
+               "token_stats: vocab must be a positive multiple of 8 (got %d)", vocab);
+  YATT_REQUIRE(rows >= 0, YATT_ERR_CONFIG, "token_stats: rows must be >= 0");
+  YATT_REQUIRE(kl_mode >= YATT_KL_K1 && kl_mode <= YATT_KL_FULL, YATT_ERR_CONFIG,
+               "token_stats: unknown kl_mode %d", kl_mode);
+  YATT_REQUIRE(logp != nullptr, YATT_ERR_CONFIG, "token_stats: logp output is required");
+  if (rows == 0) return YATT_OK;
+  YATT_REQUIRE(pol && ref && tgt, YATT_ERR_CONFIG, "token_stats: null input pointer");
+  YATT_REQUIRE((reinterpret_cast<uintptr_t>(pol) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(ref) & 15) == 0,
+               YATT_ERR_CONFIG, "token_stats: logits must be 16-byte aligned");
+  Params p{pol, ref, tgt, mask, rows, vocab, kl_mode, logp, ref_logp, ent, kl};
+  const int grid = int(min64(rows, int64_t(2) * num_sms()));
+  if (kl_mode == YATT_KL_FULL) {
+    static bool attr_full = false;
+    if (!attr_full) {
+      YATT_TRY_CUDA(cudaFuncSetAttribute(token_stats_kernel<true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(kSmemBytes)));
+      attr_full = true;
+    }
+    token_stats_kernel<true><<<grid, kThreads, kSmemBytes, st>>>(p);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      YATT_TRY_CUDA(cudaFuncSetAttribute(token_stats_kernel<false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(kSmemBytes)));
+      attr = true;
+    }
+    token_stats_kernel<false><<<grid, kThreads, kSmemBytes, st>>>(p);
+  }
+  return check_launch("token_stats_kernel");
+}
+
+}  // namespace yattb

@@ -1,0 +1,253 @@
+"""Device ops over torch tensors, each one C-ABI call into libyatt_b200.so.
+
+torch is only plumbing here (device memory, the current stream); the compute
+is the sm_100a kernels behind include/yatt_cuda.h.  Every op runs on the
+caller's current CUDA stream and does not synchronise unless it returns host
+data.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from ._lib import (LossConfigC, LossSumsC, check, lib)
+
+KL_MODES = {"k1": 0, "k2": 1, "k3": 2, "low_var_kl": 2, "full": 3}
+SYNTH = {"logp": 0, "old_delta": 1, "adv": 2, "kl": 3, "value": 4, "reward": 5}
+AGG_MODES = {"token-mean": 0, "seq-mean-token-mean": 1, "seq-mean-token-sum": 2}
+
+
+def _p(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _st() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _dev(t: torch.Tensor, dtype: torch.dtype, name: str) -> torch.Tensor:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+def _mask(mask: torch.Tensor | None) -> torch.Tensor | None:
+    if mask is None:
+        return None
+    if mask.dtype == torch.bool:
+        mask = mask.to(torch.uint8)
+    return _dev(mask, torch.uint8, "mask")
+
+
+# ------------------------------------------------------------------ A1 ----
+def token_stats(policy_logits: torch.Tensor, ref_logits: torch.Tensor, targets: torch.Tensor,
+                mask: torch.Tensor | None = None, kl_mode: str = "k3", out=None):
+    """Fused per-token (logp, ref_logp, entropy, kl) over [rows, V] bf16 logits."""
+    _dev(policy_logits, torch.bfloat16, "policy_logits")
+    _dev(ref_logits, torch.bfloat16, "ref_logits")
+    _dev(targets, torch.int32, "targets")
+    rows, vocab = policy_logits.shape
+    if ref_logits.shape != policy_logits.shape or targets.shape != (rows,):
+        raise ValueError("shape mismatch between logits / targets")
+    m = _mask(mask)
+    if out is None:
+        out = torch.empty((4, rows), dtype=torch.float32, device=policy_logits.device)
+    check(lib().yatt_token_stats(_p(policy_logits), _p(ref_logits), _p(targets), _p(m), rows,
+                                 vocab, KL_MODES[kl_mode], _p(out[0]), _p(out[1]), _p(out[2]),
+                                 _p(out[3]), _st()))
+    return out[0], out[1], out[2], out[3]
+
+
+def token_stats_host(policy: np.ndarray, ref: np.ndarray, targets: np.ndarray,
+                     mask: np.ndarray | None = None, kl_mode: str = "k3", out: np.ndarray | None = None):
+    """Same op on HOST buffers (uint16 bf16 bits): H2D, kernel, D2H inside."""
+    rows, vocab = policy.shape
+    if out is None:
+        out = np.empty((4, rows), dtype=np.float32)
+    for a in (policy, ref, targets, out):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("host buffers must be C-contiguous")
+    mp = None if mask is None else mask.ctypes.data
+    check(lib().yatt_token_stats_host(policy.ctypes.data, ref.ctypes.data, targets.ctypes.data, mp,
+                                      rows, vocab, KL_MODES[kl_mode], out[0].ctypes.data,
+                                      out[1].ctypes.data, out[2].ctypes.data, out[3].ctypes.data))
+    return out
+
+
+# ------------------------------------------------------------ synthetic ----
+def synth_logits(seed: int, row0: int, rows: int, vocab: int, device="cuda", out=None):
+    if out is None:
+        pol = torch.empty((rows, vocab), dtype=torch.bfloat16, device=device)
+        ref = torch.empty_like(pol)
+        tgt = torch.empty((rows,), dtype=torch.int32, device=device)
+    else:
+        pol, ref, tgt = out
+    check(lib().yatt_synth_logits(seed, row0, rows, vocab, _p(pol), _p(ref), _p(tgt), _st()))
+    return pol, ref, tgt
+
+
+def synth_floats(seed: int, stream_id: int, i0: int, n: int, kind: str, group_size: int = 1,
+                 base: torch.Tensor | None = None, device="cuda") -> torch.Tensor:
+    out = torch.empty((n,), dtype=torch.float32, device=device)
+    check(lib().yatt_synth_floats(seed, stream_id, i0, n, SYNTH[kind], group_size, _p(base),
+                                  _p(out), _st()))
+    return out
+
+
+# ------------------------------------------------------------------ A2 ----
+def grpo_group_moments(rewards: torch.Tensor, group_size: int, first_sample_id: int = 0):
+    _dev(rewards, torch.float32, "rewards")
+    n = rewards.numel()
+    ng = lib().yatt_grpo_num_local_groups(n, first_sample_id, group_size)
+    out = torch.empty((max(ng, 0), 3), dtype=torch.float64, device=rewards.device)
+    check(lib().yatt_grpo_group_moments(_p(rewards), n, first_sample_id, group_size, _p(out),
+                                        _st()))
+    return out
+
+
+def grpo_advantages(rewards: torch.Tensor, group_size: int, eps: float = 1e-6,
+                    norm_by_std: bool = True, first_sample_id: int = 0,
+                    moments: torch.Tensor | None = None) -> torch.Tensor:
+    _dev(rewards, torch.float32, "rewards")
+    adv = torch.empty_like(rewards)
+    check(lib().yatt_grpo_advantages(_p(rewards), rewards.numel(), first_sample_id, group_size,
+                                     eps, int(norm_by_std), _p(moments), _p(adv), _st()))
+    return adv
+
+
+def broadcast_to_tokens(sample_vals: torch.Tensor, cu_seqlens: torch.Tensor, n_tokens: int,
+                        mask: torch.Tensor | None = None, out: torch.Tensor | None = None):
+    _dev(cu_seqlens, torch.int64, "cu_seqlens")
+    if out is None:
+        out = torch.empty((n_tokens,), dtype=torch.float32, device=sample_vals.device)
+    check(lib().yatt_broadcast_to_tokens(_p(sample_vals), _p(cu_seqlens), sample_vals.numel(),
+                                         _p(_mask(mask)), _p(out), n_tokens, _st()))
+    return out
+
+
+# ------------------------------------------------------------------ A3 ----
+def gae(values: torch.Tensor, rewards: torch.Tensor, cu_seqlens: torch.Tensor,
+        mask: torch.Tensor | None = None, gamma: float = 1.0, lam: float = 0.95):
+    _dev(values, torch.float32, "values")
+    _dev(rewards, torch.float32, "rewards")
+    _dev(cu_seqlens, torch.int64, "cu_seqlens")
+    adv = torch.empty_like(values)
+    ret = torch.empty_like(values)
+    check(lib().yatt_gae(_p(values), _p(rewards), _p(_mask(mask)), _p(cu_seqlens),
+                         cu_seqlens.numel() - 1, gamma, lam, _p(adv), _p(ret), _st()))
+    return adv, ret
+
+
+def masked_moments(x: torch.Tensor, mask: torch.Tensor | None = None) -> torch.Tensor:
+    out = torch.empty((3,), dtype=torch.float64, device=x.device)
+    wsb = lib().yatt_masked_moments_workspace_bytes()
+    ws = torch.empty((wsb,), dtype=torch.uint8, device=x.device)
+    check(lib().yatt_masked_moments(_p(x), _p(_mask(mask)), x.numel(), _p(out), _p(ws), wsb, _st()))
+    return out
+
+
+def whiten(x: torch.Tensor, moments: torch.Tensor, mask: torch.Tensor | None = None,
+           shift_mean: bool = True) -> torch.Tensor:
+    check(lib().yatt_whiten(_p(x), _p(_mask(mask)), x.numel(), _p(moments), int(shift_mean), _st()))
+    return x
+
+
+# ------------------------------------------------------------------ A4 ----
+def loss_config(clip_low=0.2, clip_high=0.2, clip_ratio_c=0.0, kl_coef=0.001, entropy_coef=0.0,
+                agg_mode="token-mean") -> LossConfigC:
+    return LossConfigC(clip_low, clip_high, clip_ratio_c, kl_coef, entropy_coef,
+                       AGG_MODES[agg_mode] if isinstance(agg_mode, str) else int(agg_mode))
+
+
+class LossWorkspace:
+    def __init__(self, device="cuda"):
+        nb = lib().yatt_policy_loss_workspace_bytes(0, 0, 0)
+        self.buf = torch.empty((nb,), dtype=torch.uint8, device=device)
+
+
+def policy_loss(logp, old_logp, advantages, kl, entropy, mask=None, cu_seqlens=None,
+                config: LossConfigC | None = None, workspace: LossWorkspace | None = None,
+                sums: torch.Tensor | None = None) -> torch.Tensor:
+    """Returns the 8 fp64 yatt_loss_sums fields as a device tensor."""
+    cfg = config or loss_config()
+    ws = workspace or LossWorkspace(logp.device)
+    if sums is None:
+        sums = torch.empty((8,), dtype=torch.float64, device=logp.device)
+    nseq = 0 if cu_seqlens is None else cu_seqlens.numel() - 1
+    check(lib().yatt_policy_loss(_p(logp), _p(old_logp), _p(advantages), _p(kl), _p(entropy),
+                                 _p(_mask(mask)), logp.numel(), _p(cu_seqlens), nseq,
+                                 C.byref(cfg), _p(sums), _p(ws.buf), ws.buf.numel(), _st()))
+    return sums
+
+
+def loss_finalize(sums, config: LossConfigC | None = None) -> float:
+    s = LossSumsC(*[float(v) for v in (sums.tolist() if hasattr(sums, "tolist") else sums)])
+    return lib().yatt_loss_finalize(C.byref(s), C.byref(config or loss_config()))
+
+
+# ------------------------------------------------------------- A5 / A6 ----
+def filter_compact(rewards: torch.Tensor, seq_lens: torch.Tensor, group_size: int):
+    _dev(rewards, torch.float32, "rewards")
+    _dev(seq_lens, torch.int64, "seq_lens")
+    n = rewards.numel()
+    dev = rewards.device
+    keep = torch.empty((max(n // group_size, 1),), dtype=torch.uint8, device=dev)
+    imap = torch.empty((max(n, 1),), dtype=torch.int32, device=dev)
+    new_cu = torch.empty((n + 1,), dtype=torch.int64, device=dev)
+    counts = torch.empty((3,), dtype=torch.int64, device=dev)
+    wsb = lib().yatt_filter_compact_workspace_bytes(n)
+    ws = torch.empty((wsb,), dtype=torch.uint8, device=dev)
+    check(lib().yatt_filter_compact(_p(rewards), _p(seq_lens), n, group_size, _p(keep), _p(imap),
+                                    _p(new_cu), _p(counts), _p(ws), wsb, _st()))
+    return {"keep_groups": keep[: n // group_size], "index_map": imap, "new_cu": new_cu,
+            "counts": counts}
+
+
+def gather_varlen(src: torch.Tensor, old_cu: torch.Tensor, index_map: torch.Tensor,
+                  new_cu: torch.Tensor, n_kept: torch.Tensor, max_kept: int, dst: torch.Tensor,
+                  dst_offset: torch.Tensor | None = None) -> torch.Tensor:
+    check(lib().yatt_gather_varlen(_p(src), _p(old_cu), _p(index_map), _p(new_cu), _p(n_kept),
+                                   max_kept, _p(dst_offset), src.element_size(), _p(dst), _st()))
+    return dst
+
+
+def gather_rows(src: torch.Tensor, index_map: torch.Tensor, n_kept: torch.Tensor, max_kept: int,
+                dst: torch.Tensor, dst_offset: torch.Tensor | None = None) -> torch.Tensor:
+    row_bytes = src[0].numel() * src.element_size() if src.dim() > 1 else src.element_size()
+    check(lib().yatt_gather_rows(_p(src), _p(index_map), _p(n_kept), max_kept, row_bytes,
+                                 _p(dst_offset), _p(dst), _st()))
+    return dst
+
+
+def microbatch_aggregates(prompt_len: torch.Tensor, out_len: torch.Tensor, microbatch_size: int,
+                          controller_rank: int = 0, n: torch.Tensor | None = None,
+                          max_n: int | None = None) -> torch.Tensor:
+    cap = prompt_len.numel() if max_n is None else max_n
+    nmb = -(-cap // microbatch_size)
+    out = torch.zeros((max(nmb, 1), 6), dtype=torch.int32, device=prompt_len.device)  # 24 B rows
+    check(lib().yatt_microbatch_aggregates(_p(prompt_len), _p(out_len), _p(n), cap,
+                                           microbatch_size, controller_rank, _p(out), _st()))
+    return out[:nmb]
+
+
+def exclusive_offset(counts: torch.Tensor, nranks: int, rank: int, stride: int, field: int):
+    out = torch.empty((1,), dtype=torch.int64, device=counts.device)
+    check(lib().yatt_exclusive_offset(_p(counts), nranks, rank, stride, field, _p(out), _st()))
+    return out
+
+
+# ------------------------------------------------------------------ R10 ---
+def sort_order_desc(lengths: torch.Tensor) -> torch.Tensor:
+    _dev(lengths, torch.int32, "lengths")
+    n = lengths.numel()
+    order = torch.empty((n,), dtype=torch.int32, device=lengths.device)
+    wsb = lib().yatt_sort_order_workspace_bytes(n)
+    ws = torch.empty((wsb,), dtype=torch.uint8, device=lengths.device)
+    check(lib().yatt_sort_order_desc(_p(lengths), n, _p(order), _p(ws), wsb, _st()))
+    return order
