@@ -1,0 +1,99 @@
+// yatt/experience.hpp — the experience-making / policy-loss ops (new API).
+//
+// No counterpart in the reference, where Preparation and Training are cost
+// stand-ins (proj/src/simcore.cpp:13-15, :395-406).  Written in the style of
+// the reference headers: config structs with validate() throwing ConfigError
+// (cf. ControllerTopology::validate, controller.cpp:7-26), exceptions for
+// errors.  All pointers are device pointers; every call is stream-ordered on
+// `stream` (a cudaStream_t, nullptr = default stream) and does not block.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+namespace yatt::experience {
+
+// ---- A1 -------------------------------------------------------------------
+enum class KlEstimator { kK1 = 0, kK2 = 1, kK3 = 2, kFull = 3 };
+
+struct TokenStats {
+  float* logp = nullptr;       // required
+  float* ref_logp = nullptr;   // optional outputs may be nullptr
+  float* entropy = nullptr;
+  float* kl = nullptr;
+};
+
+// Row-major [rows, vocab] bf16 logits (uint16 bit patterns); rows with
+// mask == 0 are skipped and produce zeros.  vocab % 8 == 0.
+void token_logprob_stats(const std::uint16_t* policy_logits, const std::uint16_t* ref_logits,
+                         const std::int32_t* targets, const std::uint8_t* mask,
+                         std::int64_t rows, int vocab, KlEstimator kl, const TokenStats& out,
+                         void* stream = nullptr);
+
+// ---- A2 -------------------------------------------------------------------
+struct GrpoConfig {
+  int group_size = 8;
+  float eps = 1e-6f;
+  bool norm_by_std = true;
+  void validate() const;
+};
+
+// Advantages of n_samples local samples whose global ids start at
+// first_sample_id.  group_moments (n, mean, M2 per local group, fp64) may be
+// supplied after a cross-rank merge for groups straddling ranks.
+void grpo_advantages(const float* rewards, std::int64_t n_samples, std::uint64_t first_sample_id,
+                     const GrpoConfig& config, float* advantages,
+                     const double* group_moments = nullptr, void* stream = nullptr);
+
+// ---- A3 -------------------------------------------------------------------
+struct GaeConfig {
+  float gamma = 1.0f;
+  float lam = 0.95f;
+  void validate() const;
+};
+
+void gae(const float* values, const float* rewards, const std::uint8_t* mask,
+         const std::int64_t* cu_seqlens, std::int64_t n_seqs, const GaeConfig& config,
+         float* advantages, float* returns, void* stream = nullptr);
+
+// ---- A4 -------------------------------------------------------------------
+enum class LossAggregation { kTokenMean = 0, kSeqMeanTokenMean = 1, kSeqMeanTokenSum = 2 };
+
+struct PolicyLossConfig {
+  float clip_low = 0.2f;
+  float clip_high = 0.2f;
+  float clip_ratio_c = 0.0f;  // dual clip bound (> 1) or 0 = off
+  float kl_coef = 0.001f;
+  float entropy_coef = 0.0f;
+  LossAggregation aggregation = LossAggregation::kTokenMean;
+  void validate() const;
+};
+
+struct LossSums {  // layout identical to yatt_loss_sums
+  double loss_sum = 0, pg_sum = 0, kl_sum = 0, entropy_sum = 0, clip_count = 0, ratio_sum = 0,
+         token_count = 0, seq_count = 0;
+};
+
+std::size_t policy_loss_workspace_bytes();
+void policy_loss(const float* logp, const float* old_logp, const float* advantages,
+                 const float* kl, const float* entropy, const std::uint8_t* mask,
+                 std::int64_t n_tokens, const std::int64_t* cu_seqlens, std::int64_t n_seqs,
+                 const PolicyLossConfig& config, LossSums* device_sums, void* workspace,
+                 std::size_t workspace_bytes, void* stream = nullptr);
+double finalize_loss(const LossSums& global_sums, const PolicyLossConfig& config);
+
+// ---- A5 + A6 --------------------------------------------------------------
+struct CompactionBuffers {
+  std::uint8_t* keep_groups = nullptr;  // [n_samples / group_size]
+  std::int32_t* index_map = nullptr;    // [n_samples]
+  std::int64_t* new_cu = nullptr;       // [n_samples + 1]
+  std::int64_t* counts = nullptr;       // [3] kept samples, tokens, groups
+};
+
+std::size_t dynamic_sampling_workspace_bytes(std::int64_t n_samples);
+void dynamic_sampling_filter(const float* rewards, const std::int64_t* seq_lens,
+                             std::int64_t n_samples, int group_size, const CompactionBuffers& out,
+                             void* workspace, std::size_t workspace_bytes,
+                             void* stream = nullptr);
+
+}  // namespace yatt::experience

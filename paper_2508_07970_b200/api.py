@@ -1,0 +1,361 @@
+"""Python mirror of the reference's on-path host API (proj/include/yatt/).
+
+Same names, fields and error behaviour as the C++ drop-in (include/yatt/
+*.hpp), over the same C ABI: batched work runs on the B200, the scalar keyed
+draw and O(1) helpers are host arithmetic like in the reference.
+
+    workload.hpp  -> RolloutSample, RolloutBatch, LengthDistribution, RejectionConfig,
+                     sample_length_keyed, sample_lengths, rejection_process, shard_dataset
+    simcore.hpp   -> ShardSampleState, ShardState, RoundParams, MicrobatchAggregate,
+                     ShardRoundReport, make_shard_state, shard_round_output,
+                     reduce_round_reports, run_rollout_rounds
+    balancer.hpp  -> BatchingPlan, sort_and_bucket, padding_waste, waste_bound
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from ._lib import (ConfigError, InvalidDistribution, LengthDist, MbAggC, RejectionCfg, ReportC,
+                   RoundParamsC, SampleC, check, lib)
+
+CONSTANT, UNIFORM, NORMAL, LOGNORMAL = range(4)
+PROMPT_LEN_STREAM, OUTPUT_LEN_STREAM, REJECTION_STREAM = 1, 2, 3
+_MASK64 = (1 << 64) - 1
+
+
+# ------------------------------------------------------------- keyed RNG ---
+def splitmix64(x: int) -> int:
+    """proj/include/yatt/common.hpp:17-22."""
+    x = (x + 0x9E3779B97F4A7C15) & _MASK64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & _MASK64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & _MASK64
+    return x ^ (x >> 31)
+
+
+def hash_key(parts) -> int:
+    """common.hpp:25-31."""
+    h = 0x243F6A8885A308D3
+    for p in parts:
+        h = splitmix64(h ^ splitmix64(p & _MASK64))
+    return h
+
+
+def uniform_from_key(key: int) -> float:
+    """common.hpp:35-37."""
+    return (splitmix64(key) >> 11) * 2.0 ** -53
+
+
+# ---------------------------------------------------------------- workload --
+@dataclass
+class LengthDistribution:
+    kind: int = CONSTANT
+    p1: float = 1.0
+    p2: float = 0.0
+    max_len_tokens: int = 1 << 20
+
+    def validate(self) -> None:
+        if self.max_len_tokens < 1:
+            raise InvalidDistribution("max_len_tokens must be at least 1")
+        if self.kind == CONSTANT and self.p1 < 1:
+            raise InvalidDistribution("constant length must be at least 1")
+        if self.kind == UNIFORM and self.p1 < 1:
+            raise InvalidDistribution("uniform low bound must be at least 1")
+        if self.kind == UNIFORM and self.p2 < self.p1:
+            raise InvalidDistribution("uniform high bound below low bound")
+        if self.kind in (NORMAL, LOGNORMAL) and self.p2 < 0:
+            raise InvalidDistribution("stddev must be non-negative")
+
+    def c(self) -> LengthDist:
+        return LengthDist(self.kind, self.max_len_tokens, self.p1, self.p2)
+
+
+@dataclass
+class RolloutSample:
+    sample_id: int = 0
+    prompt_len_tokens: int = 0
+    target_out_len_tokens: int = 0
+    accepted_round: int = 0
+    accepted: bool = False
+
+
+@dataclass
+class RolloutBatch:
+    step_index: int = 0
+    samples: list = field(default_factory=list)
+
+
+@dataclass
+class RejectionConfig:
+    reject_rate: float = 0.0
+    per_group: bool = False
+    group_size: int = 1
+
+    def c(self) -> RejectionCfg:
+        return RejectionCfg(self.reject_rate, int(self.per_group), self.group_size)
+
+
+@dataclass
+class ShardRange:
+    begin: int = 0
+    end: int = 0
+
+    def size(self) -> int:
+        return self.end - self.begin
+
+
+def _clamp(v: float, max_len: int) -> int:
+    r = float(np.rint(v))  # nearbyint, round-half-even
+    return 1 if r < 1 else (max_len if r > max_len else int(r))
+
+
+def sample_length_keyed(dist: LengthDistribution, seed, stream, step, round_, sample_id) -> int:
+    """workload.cpp:109-132 (host scalar, like the reference)."""
+    key = hash_key([seed, stream, step, round_, sample_id])
+    if dist.kind == CONSTANT:
+        return _clamp(dist.p1, dist.max_len_tokens)
+    if dist.kind == UNIFORM:
+        llround = lambda x: int(math.copysign(math.floor(abs(x) + 0.5), x))  # noqa: E731
+        lo, hi = llround(dist.p1), llround(dist.p2)
+        return _clamp(lo + int(uniform_from_key(key) * float(hi - lo + 1)), dist.max_len_tokens)
+    u1 = uniform_from_key(key)
+    u2 = uniform_from_key(splitmix64(key ^ 0x5BF0A8B1457E1D23))
+    z = math.sqrt(-2.0 * math.log1p(-u1)) * math.cos(6.283185307179586476925286766559 * u2)
+    v = dist.p1 + dist.p2 * z
+    return _clamp(v if dist.kind == NORMAL else math.exp(v), dist.max_len_tokens)
+
+
+def sample_lengths(dist: LengthDistribution, n: int, seed: int, device="cuda") -> list[int]:
+    """Batched keyed draws for ids 0..n-1 on the device (workload.cpp:134-143)."""
+    if n <= 0:
+        return []
+    ids = torch.arange(n, dtype=torch.int64, device=device)
+    out = torch.empty((n,), dtype=torch.int32, device=device)
+    check(lib().yatt_sample_lengths_keyed(C.byref(dist.c()), seed, OUTPUT_LEN_STREAM, 0, 0,
+                                          ids.data_ptr(), n, out.data_ptr(),
+                                          torch.cuda.current_stream().cuda_stream))
+    return out.cpu().tolist()
+
+
+def _pack(samples, sample_attr_out="target_out_len_tokens") -> np.ndarray:
+    arr = (SampleC * max(len(samples), 1))()
+    for i, s in enumerate(samples):
+        arr[i] = SampleC(s.sample_id, s.prompt_len_tokens, getattr(s, sample_attr_out),
+                         s.accepted_round, int(s.accepted))
+    return np.frombuffer(arr, dtype=np.uint8)[: len(samples) * C.sizeof(SampleC)].copy()
+
+
+def rejection_process(batch: RolloutBatch, round_: int, config: RejectionConfig, seed: int,
+                      device="cuda") -> list[bool]:
+    """workload.cpp:145-167 on the device."""
+    n = len(batch.samples)
+    d = torch.from_numpy(_pack(batch.samples)).to(device) if n else \
+        torch.empty((C.sizeof(SampleC),), dtype=torch.uint8, device=device)
+    out = torch.empty((max(n, 1),), dtype=torch.uint8, device=device)
+    check(lib().yatt_rejection_flags(d.data_ptr(), n, batch.step_index, round_,
+                                     C.byref(config.c()), seed, out.data_ptr(),
+                                     torch.cuda.current_stream().cuda_stream))
+    return [bool(x) for x in out[:n].cpu().tolist()]
+
+
+def shard_dataset(total_samples: int, num_controllers: int, controller_rank: int) -> ShardRange:
+    """workload.cpp:183-198 (C ABI, host arithmetic)."""
+    b, e = C.c_uint64(), C.c_uint64()
+    check(lib().yatt_shard_dataset(total_samples, num_controllers, controller_rank, C.byref(b),
+                                   C.byref(e)))
+    return ShardRange(b.value, e.value)
+
+
+# ----------------------------------------------------------------- simcore --
+@dataclass
+class ShardSampleState:
+    sample_id: int = 0
+    prompt_len_tokens: int = 0
+    out_len_tokens: int = 0
+    accepted: bool = False
+    accepted_round: int = 0
+
+
+@dataclass
+class ShardState:
+    controller_rank: int = 0
+    step_index: int = 0
+    samples: list = field(default_factory=list)
+
+
+@dataclass
+class RoundParams:
+    out_dist: LengthDistribution = field(default_factory=LengthDistribution)
+    rejection: RejectionConfig = field(default_factory=RejectionConfig)
+    seed: int = 0
+    microbatch_size: int = 1
+    max_rounds: int = 64
+
+    def c(self) -> RoundParamsC:
+        return RoundParamsC(self.out_dist.c(), self.rejection.c(), self.seed,
+                            self.microbatch_size, self.max_rounds)
+
+
+@dataclass
+class MicrobatchAggregate:
+    controller_rank: int = 0
+    mb_index: int = 0
+    sample_count: int = 0
+    max_out_len_tokens: int = 0
+    score_tokens: int = 0
+
+
+@dataclass
+class ShardRoundReport:
+    controller_rank: int = 0
+    round: int = 0
+    active_count: int = 0
+    newly_accepted_count: int = 0
+    forced_accept_count: int = 0
+    pending_count: int = 0
+    accepted_score_tokens: int = 0
+    accepted_train_units: int = 0
+    microbatches: list = field(default_factory=list)
+
+
+def _report(r: ReportC, mbs) -> ShardRoundReport:
+    return ShardRoundReport(r.controller_rank, r.round, r.active_count, r.newly_accepted_count,
+                            r.forced_accept_count, r.pending_count, r.accepted_score_tokens,
+                            r.accepted_train_units,
+                            [MicrobatchAggregate(m.controller_rank, m.mb_index, m.sample_count,
+                                                 m.max_out_len_tokens, m.score_tokens)
+                             for m in mbs[: r.num_microbatches]])
+
+
+def make_shard_state(batch: RolloutBatch, num_controllers: int, controller_rank: int) -> ShardState:
+    """simcore.cpp:246-266."""
+    rng = shard_dataset(len(batch.samples), num_controllers, controller_rank)
+    return ShardState(controller_rank, batch.step_index,
+                      [ShardSampleState(s.sample_id, s.prompt_len_tokens, s.target_out_len_tokens,
+                                        s.accepted, s.accepted_round)
+                       for s in batch.samples[rng.begin:rng.end]])
+
+
+class _DeviceShards:
+    """Samples of several shards resident on the device; one launch per round."""
+
+    def __init__(self, shards: list, params: RoundParams, device="cuda"):
+        if params.microbatch_size <= 0:
+            raise ConfigError("microbatch_size must be positive")
+        self.shards, self.params = shards, params
+        self.off = np.zeros(len(shards) + 1, dtype=np.int64)
+        for i, s in enumerate(shards):
+            self.off[i + 1] = self.off[i] + len(s.samples)
+        flat = [x for s in shards for x in s.samples]
+        self.n = len(flat)
+        self.d = torch.from_numpy(_pack(flat, "out_len_tokens")).to(device) if self.n else \
+            torch.empty((C.sizeof(SampleC),), dtype=torch.uint8, device=device)
+        mb = params.microbatch_size
+        self.slots = [-(-len(s.samples) // mb) for s in shards]
+        self.d_rep = torch.empty((len(shards) * C.sizeof(ReportC),), dtype=torch.uint8,
+                                 device=device)
+        self.d_mbs = torch.empty((max(sum(self.slots), 1) * C.sizeof(MbAggC),), dtype=torch.uint8,
+                                 device=device)
+
+    def round(self, round_: int, first_rank: int) -> list[ShardRoundReport]:
+        off = (C.c_int64 * len(self.off))(*self.off.tolist())
+        check(lib().yatt_shard_round(self.d.data_ptr(), off, len(self.shards), first_rank,
+                                     self.shards[0].step_index if self.shards else 0, round_,
+                                     C.byref(self.params.c()), self.d_rep.data_ptr(),
+                                     self.d_mbs.data_ptr(),
+                                     torch.cuda.current_stream().cuda_stream))
+        reps = (ReportC * len(self.shards)).from_buffer_copy(self.d_rep.cpu().numpy().tobytes())
+        mbs = (MbAggC * max(sum(self.slots), 1)).from_buffer_copy(self.d_mbs.cpu().numpy().tobytes())
+        out, base = [], 0
+        for i, r in enumerate(reps):
+            out.append(_report(r, mbs[base: base + self.slots[i]]))
+            base += self.slots[i]
+        return out
+
+    def samples(self):
+        raw = self.d[: self.n * C.sizeof(SampleC)].cpu().numpy().tobytes()
+        return (SampleC * max(self.n, 1)).from_buffer_copy(raw.ljust(C.sizeof(SampleC), b"\0"))
+
+
+def shard_round_output(state: ShardState, round_: int, params: RoundParams,
+                       device="cuda") -> ShardRoundReport:
+    """simcore.cpp:157-214 on the device; mutates `state` like the reference."""
+    ds = _DeviceShards([state], params, device)
+    rep = ds.round(round_, state.controller_rank)[0]
+    for s, c in zip(state.samples, ds.samples()):
+        s.out_len_tokens, s.accepted, s.accepted_round = c.out_len_tokens, bool(c.accepted), \
+            c.accepted_round
+    return rep
+
+
+def reduce_round_reports(reports) -> dict:
+    """Integer part of StepAssembler::feed_round (simcore.cpp:304-311)."""
+    return {"active": sum(r.active_count for r in reports),
+            "pending": sum(r.pending_count for r in reports),
+            "forced_accepts": sum(r.forced_accept_count for r in reports),
+            "train_units": sum(r.accepted_train_units for r in reports),
+            "score_tokens": sum(r.accepted_score_tokens for r in reports)}
+
+
+def run_rollout_rounds(batch: RolloutBatch, num_controllers: int, params: RoundParams,
+                       device="cuda") -> list[list[ShardRoundReport]]:
+    """The round loop of run_rlhf_step (simcore.cpp:470-494): every shard of
+    every round in one launch; copy_back in rank order (simcore.cpp:107-119)."""
+    params.out_dist.validate()
+    if params.max_rounds < 1:
+        raise ConfigError("max_rounds must be at least 1")
+    shards = [make_shard_state(batch, num_controllers, r) for r in range(num_controllers)]
+    ds = _DeviceShards(shards, params, device)
+    rounds, r = [], 1
+    while True:
+        reps = ds.round(r, 0)
+        rounds.append(reps)
+        if reduce_round_reports(reps)["pending"] == 0:
+            break
+        r += 1
+    for s, c in zip(batch.samples, ds.samples()):
+        s.target_out_len_tokens, s.accepted, s.accepted_round = c.out_len_tokens, \
+            bool(c.accepted), c.accepted_round
+    return rounds
+
+
+# ---------------------------------------------------------------- balancer --
+@dataclass
+class BatchingPlan:
+    batch_size: int = 0
+    buckets: list = field(default_factory=list)
+    shuffle_seed: int = 0
+
+
+def sort_and_bucket(lengths, batch_size: int, seed: int) -> BatchingPlan:
+    """balancer.cpp:16-41: device sort, host std::shuffle (bit-exact)."""
+    n = len(lengths)
+    if batch_size <= 0:
+        raise ConfigError("batch_size must be positive")
+    ln = np.ascontiguousarray(lengths, dtype=np.int32)
+    nb = -(-n // batch_size)
+    flat = np.zeros(max(n, 1), dtype=np.uint32)
+    off = np.zeros(nb + 1, dtype=np.int64)
+    check(lib().yatt_sort_and_bucket_host(ln.ctypes.data, n, batch_size, seed, flat.ctypes.data,
+                                          off.ctypes.data))
+    return BatchingPlan(batch_size, [flat[off[b]:off[b + 1]].tolist() for b in range(nb)], seed)
+
+
+def padding_waste(plan: BatchingPlan, lengths) -> float:
+    real = padded = 0.0
+    for b in plan.buckets:
+        mx = max((lengths[i] for i in b), default=0)
+        real += sum(float(lengths[i]) ** 2 for i in b)
+        padded += len(b) * float(mx) ** 2
+    return 0.0 if padded == 0 else 1.0 - real / padded
+
+
+def waste_bound(batch_size: int) -> float:
+    if batch_size <= 0:
+        raise ConfigError("batch_size must be positive")
+    k = (batch_size - 1) / batch_size
+    return 1.0 - k * k

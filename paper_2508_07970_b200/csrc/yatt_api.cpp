@@ -1,0 +1,562 @@
+// yatt_api.cpp — the drop-in C++ host API (include/yatt/*.hpp) over the C ABI.
+//
+// STL-typed entry points keep the reference's signatures and exception
+// types; they own the H2D/D2H copies around the device kernels and block
+// only because the reference API returns host data.  Device scratch is a
+// per-thread grow-only arena (no allocation once warm).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "yatt/balancer.hpp"
+#include "yatt/common.hpp"
+#include "yatt/errors.hpp"
+#include "yatt/experience.hpp"
+#include "yatt/simcore.hpp"
+#include "yatt/workload.hpp"
+#include "yatt_cuda.h"
+
+namespace yatt {
+
+namespace detail {
+
+void throw_status(int status) {
+  if (status == YATT_OK) return;
+  const std::string msg = yatt_last_error_message();
+  switch (status) {
+    case YATT_ERR_CONFIG:
+    case YATT_ERR_WORKSPACE: throw ConfigError(msg);
+    case YATT_ERR_RANK: throw RankOutOfRange(msg);
+    case YATT_ERR_DISTRIBUTION: throw InvalidDistribution(msg);
+    default: throw DeviceError(msg);
+  }
+}
+
+namespace {
+
+void cuda_ok(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Grow-only device scratch, one slot per use site.
+struct Arena {
+  void* ptr[8] = {};
+  size_t cap[8] = {};
+  void* get(int slot, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (bytes > cap[slot]) {
+      if (ptr[slot]) cudaFree(ptr[slot]);
+      ptr[slot] = nullptr;
+      cap[slot] = 0;
+      cuda_ok(cudaMalloc(&ptr[slot], bytes), "cudaMalloc");
+      cap[slot] = bytes;
+    }
+    return ptr[slot];
+  }
+};
+thread_local Arena g_arena;
+
+template <typename T>
+T* dev(int slot, size_t n) {
+  return static_cast<T*>(g_arena.get(slot, n * sizeof(T)));
+}
+
+void h2d(void* d, const void* h, size_t bytes) {
+  if (bytes) cuda_ok(cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+}
+void d2h(void* h, const void* d, size_t bytes) {
+  if (bytes) cuda_ok(cudaMemcpy(h, d, bytes, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+}
+
+yatt_length_dist to_c(const workload::LengthDistribution& d) {
+  return yatt_length_dist{static_cast<int32_t>(d.kind), d.max_len_tokens, d.p1, d.p2};
+}
+yatt_rejection_config to_c(const workload::RejectionConfig& c) {
+  return yatt_rejection_config{c.reject_rate, c.per_group ? 1 : 0, c.group_size};
+}
+
+}  // namespace
+}  // namespace detail
+
+// ------------------------------------------------------------- common ----
+std::string hex_encode(std::string_view bytes) {
+  static const char* digits = "0123456789abcdef";
+  std::string out;
+  out.reserve(bytes.size() * 2);
+  for (unsigned char c : bytes) {
+    out.push_back(digits[c >> 4]);
+    out.push_back(digits[c & 15]);
+  }
+  return out;
+}
+
+std::string hex_decode(std::string_view hex) {
+  auto nib = [](char c) -> int {
+    if (c >= '0' && c <= '9') return c - '0';
+    if (c >= 'a' && c <= 'f') return c - 'a' + 10;
+    if (c >= 'A' && c <= 'F') return c - 'A' + 10;
+    throw ConfigError("invalid hex digit");
+  };
+  if (hex.size() % 2) throw ConfigError("hex string has odd length");
+  std::string out(hex.size() / 2, '\0');
+  for (size_t i = 0; i < out.size(); ++i)
+    out[i] = static_cast<char>((nib(hex[2 * i]) << 4) | nib(hex[2 * i + 1]));
+  return out;
+}
+
+// ----------------------------------------------------------- workload ----
+namespace workload {
+
+std::string dist_kind_name(DistKind kind) {
+  switch (kind) {
+    case DistKind::kConstant: return "constant";
+    case DistKind::kUniform: return "uniform";
+    case DistKind::kNormal: return "normal";
+    case DistKind::kLogNormal: return "lognormal";
+  }
+  throw ConfigError("unknown distribution kind value");
+}
+
+DistKind dist_kind_from_name(const std::string& name) {
+  for (DistKind k : {DistKind::kConstant, DistKind::kUniform, DistKind::kNormal,
+                     DistKind::kLogNormal})
+    if (dist_kind_name(k) == name) return k;
+  throw ConfigError("unknown distribution kind: " + name);
+}
+
+void LengthDistribution::validate() const {
+  const yatt_length_dist d = detail::to_c(*this);
+  // Same checks as the device-side validator (shard_round.cu validate_dist).
+  if (d.max_len_tokens < 1) throw InvalidDistribution("max_len_tokens must be at least 1");
+  switch (kind) {
+    case DistKind::kConstant:
+      if (p1 < 1) throw InvalidDistribution("constant length must be at least 1");
+      break;
+    case DistKind::kUniform:
+      if (p1 < 1) throw InvalidDistribution("uniform low bound must be at least 1");
+      if (p2 < p1) throw InvalidDistribution("uniform high bound below low bound");
+      break;
+    case DistKind::kNormal:
+      if (p2 < 0) throw InvalidDistribution("normal stddev must be non-negative");
+      break;
+    case DistKind::kLogNormal:
+      if (p2 < 0) throw InvalidDistribution("lognormal sigma must be non-negative");
+      break;
+  }
+}
+
+double LengthDistribution::mean() const {
+  switch (kind) {
+    case DistKind::kConstant:
+    case DistKind::kNormal: return p1;
+    case DistKind::kUniform: return 0.5 * (p1 + p2);
+    case DistKind::kLogNormal: return std::exp(p1 + 0.5 * p2 * p2);
+  }
+  throw ConfigError("unknown distribution kind value");
+}
+
+LengthDistribution LengthDistribution::scaled(double factor) const {
+  LengthDistribution r = *this;
+  if (kind == DistKind::kLogNormal) {
+    r.p1 = p1 + std::log(factor);  // location shift in log space
+  } else {
+    r.p1 = p1 * factor;
+    if (kind != DistKind::kConstant) r.p2 = p2 * factor;
+  }
+  return r;
+}
+
+namespace {
+int clamp_to_length(double v, int max_len) {
+  const double r = std::nearbyint(v);
+  return r < 1 ? 1 : (r > max_len ? max_len : static_cast<int>(r));
+}
+double keyed_normal(std::uint64_t key) {
+  const double u1 = uniform_from_key(key);
+  const double u2 = uniform_from_key(splitmix64(key ^ 0x5bf0a8b1457e1d23ULL));
+  return std::sqrt(-2.0 * std::log1p(-u1)) * std::cos(6.283185307179586476925286766559 * u2);
+}
+}  // namespace
+
+int sample_length_keyed(const LengthDistribution& dist, std::uint64_t seed, std::uint64_t stream,
+                        std::uint64_t step, std::uint64_t round, std::uint64_t sample_id) {
+  const std::uint64_t key = hash_key({seed, stream, step, round, sample_id});
+  switch (dist.kind) {
+    case DistKind::kConstant: return clamp_to_length(dist.p1, dist.max_len_tokens);
+    case DistKind::kUniform: {
+      const long long lo = std::llround(dist.p1), hi = std::llround(dist.p2);
+      const double span = static_cast<double>(static_cast<std::uint64_t>(hi - lo) + 1);
+      return clamp_to_length(
+          static_cast<double>(lo + static_cast<long long>(uniform_from_key(key) * span)),
+          dist.max_len_tokens);
+    }
+    case DistKind::kNormal:
+      return clamp_to_length(dist.p1 + dist.p2 * keyed_normal(key), dist.max_len_tokens);
+    case DistKind::kLogNormal:
+      return clamp_to_length(std::exp(dist.p1 + dist.p2 * keyed_normal(key)),
+                             dist.max_len_tokens);
+  }
+  throw ConfigError("unknown distribution kind value");
+}
+
+std::vector<int> sample_lengths(const LengthDistribution& dist, int n, std::uint64_t seed) {
+  if (n <= 0) return {};
+  std::vector<std::uint64_t> ids(static_cast<size_t>(n));
+  std::iota(ids.begin(), ids.end(), std::uint64_t{0});
+  auto* d_ids = detail::dev<std::uint64_t>(0, ids.size());
+  auto* d_out = detail::dev<std::int32_t>(1, ids.size());
+  detail::h2d(d_ids, ids.data(), ids.size() * 8);
+  const yatt_length_dist d = detail::to_c(dist);
+  detail::throw_status(yatt_sample_lengths_keyed(&d, seed, kOutputLenStream, 0, 0, d_ids, n,
+                                                 d_out, nullptr));
+  std::vector<int> out(static_cast<size_t>(n));
+  detail::d2h(out.data(), d_out, out.size() * 4);
+  return out;
+}
+
+std::vector<bool> rejection_process(const RolloutBatch& batch, int round,
+                                    const RejectionConfig& config, std::uint64_t seed) {
+  const size_t n = batch.samples.size();
+  std::vector<yatt_sample> packed(n);
+  for (size_t i = 0; i < n; ++i) {
+    const RolloutSample& s = batch.samples[i];
+    packed[i] = yatt_sample{s.sample_id, s.prompt_len_tokens, s.target_out_len_tokens,
+                            s.accepted_round, s.accepted ? 1 : 0};
+  }
+  auto* d_s = detail::dev<yatt_sample>(0, n);
+  auto* d_f = detail::dev<std::uint8_t>(1, n);
+  detail::h2d(d_s, packed.data(), n * sizeof(yatt_sample));
+  const yatt_rejection_config c = detail::to_c(config);
+  detail::throw_status(yatt_rejection_flags(d_s, static_cast<std::int64_t>(n), batch.step_index,
+                                            round, &c, seed, d_f, nullptr));
+  std::vector<std::uint8_t> flags(n);
+  detail::d2h(flags.data(), d_f, n);
+  return std::vector<bool>(flags.begin(), flags.end());
+}
+
+LengthDistribution drift_schedule(int step, const LengthDistribution& base,
+                                  double drift_rate_per_step) {
+  if (drift_rate_per_step < 0) throw ConfigError("drift_rate_per_step must be non-negative");
+  double factor = std::pow(1.0 + drift_rate_per_step, static_cast<double>(step));
+  const double m = base.mean();
+  if (m > 0) factor = std::min(factor, std::max(static_cast<double>(base.max_len_tokens) / m, 1.0));
+  return base.scaled(factor);
+}
+
+ShardRange shard_dataset(std::uint64_t total, int num_controllers, int controller_rank) {
+  ShardRange r;
+  detail::throw_status(
+      yatt_shard_dataset(total, num_controllers, controller_rank, &r.begin, &r.end));
+  return r;
+}
+
+}  // namespace workload
+
+// ------------------------------------------------------------- simcore ----
+namespace sim {
+namespace {
+
+yatt_round_params to_c(const RoundParams& p) {
+  return yatt_round_params{detail::to_c(p.out_dist), detail::to_c(p.rejection), p.seed,
+                           p.microbatch_size, p.max_rounds};
+}
+
+ShardRoundReport from_c(const yatt_round_report& r, const yatt_mb_agg* mbs) {
+  ShardRoundReport out;
+  out.controller_rank = r.controller_rank;
+  out.round = r.round;
+  out.active_count = r.active_count;
+  out.newly_accepted_count = r.newly_accepted_count;
+  out.forced_accept_count = r.forced_accept_count;
+  out.pending_count = r.pending_count;
+  out.accepted_score_tokens = r.accepted_score_tokens;
+  out.accepted_train_units = r.accepted_train_units;
+  out.microbatches.reserve(static_cast<size_t>(r.num_microbatches));
+  for (std::int64_t k = 0; k < r.num_microbatches; ++k)
+    out.microbatches.push_back(MicrobatchAggregate{mbs[k].controller_rank, mbs[k].mb_index,
+                                                   mbs[k].sample_count,
+                                                   mbs[k].max_out_len_tokens,
+                                                   mbs[k].score_tokens});
+  return out;
+}
+
+std::int64_t mb_slots(std::int64_t n, int mb) { return mb > 0 ? (n + mb - 1) / mb : 0; }
+
+}  // namespace
+
+ShardRoundReport shard_round_output(ShardState& state, int round, const RoundParams& params) {
+  if (params.microbatch_size <= 0) throw ConfigError("microbatch_size must be positive");
+  const std::int64_t n = static_cast<std::int64_t>(state.samples.size());
+  std::vector<yatt_sample> packed(static_cast<size_t>(n));
+  for (size_t i = 0; i < packed.size(); ++i) {
+    const ShardSampleState& s = state.samples[i];
+    packed[i] = yatt_sample{s.sample_id, s.prompt_len_tokens, s.out_len_tokens, s.accepted_round,
+                            s.accepted ? 1 : 0};
+  }
+  const std::int64_t slots = std::max<std::int64_t>(1, mb_slots(n, params.microbatch_size));
+  auto* d_s = detail::dev<yatt_sample>(0, packed.size());
+  auto* d_r = detail::dev<yatt_round_report>(1, 1);
+  auto* d_m = detail::dev<yatt_mb_agg>(2, static_cast<size_t>(slots));
+  detail::h2d(d_s, packed.data(), packed.size() * sizeof(yatt_sample));
+  const yatt_round_params p = to_c(params);
+  const std::int64_t off[2] = {0, n};
+  detail::throw_status(yatt_shard_round(d_s, off, 1, state.controller_rank, state.step_index,
+                                        round, &p, d_r, d_m, nullptr));
+  yatt_round_report rep;
+  detail::d2h(&rep, d_r, sizeof(rep));
+  std::vector<yatt_mb_agg> mbs(static_cast<size_t>(rep.num_microbatches));
+  detail::d2h(mbs.data(), d_m, mbs.size() * sizeof(yatt_mb_agg));
+  detail::d2h(packed.data(), d_s, packed.size() * sizeof(yatt_sample));
+  for (size_t i = 0; i < packed.size(); ++i) {
+    ShardSampleState& s = state.samples[i];
+    s.out_len_tokens = packed[i].out_len_tokens;
+    s.accepted = packed[i].accepted != 0;
+    s.accepted_round = packed[i].accepted_round;
+  }
+  return from_c(rep, mbs.data());
+}
+
+ShardState make_shard_state(const workload::RolloutBatch& batch, int num_controllers,
+                            int controller_rank) {
+  const workload::ShardRange range = workload::shard_dataset(
+      static_cast<std::uint64_t>(batch.samples.size()), num_controllers, controller_rank);
+  ShardState shard;
+  shard.controller_rank = controller_rank;
+  shard.step_index = batch.step_index;
+  shard.samples.reserve(range.size());
+  for (std::uint64_t i = range.begin; i < range.end; ++i) {
+    const workload::RolloutSample& s = batch.samples[i];
+    shard.samples.push_back(ShardSampleState{s.sample_id, s.prompt_len_tokens,
+                                             s.target_out_len_tokens, s.accepted,
+                                             s.accepted_round});
+  }
+  return shard;
+}
+
+RoundReduction reduce_round_reports(const std::vector<ShardRoundReport>& reports) {
+  RoundReduction r;
+  for (const ShardRoundReport& rep : reports) {
+    r.active += rep.active_count;
+    r.pending += rep.pending_count;
+    r.forced_accepts += rep.forced_accept_count;
+    r.train_units += rep.accepted_train_units;
+    r.score_tokens += rep.accepted_score_tokens;
+  }
+  return r;
+}
+
+std::vector<std::vector<ShardRoundReport>> run_rollout_rounds(workload::RolloutBatch& batch,
+                                                              int num_controllers,
+                                                              const RoundParams& params) {
+  params.out_dist.validate();
+  if (params.max_rounds < 1) throw ConfigError("max_rounds must be at least 1");
+  if (num_controllers < 1) throw ConfigError("num_controllers must be positive");
+  if (params.microbatch_size <= 0) throw ConfigError("microbatch_size must be positive");
+  const std::int64_t n = static_cast<std::int64_t>(batch.samples.size());
+  std::vector<std::int64_t> off(static_cast<size_t>(num_controllers) + 1, 0);
+  std::int64_t slots = 0;
+  for (int r = 0; r < num_controllers; ++r) {
+    const workload::ShardRange sr =
+        workload::shard_dataset(static_cast<std::uint64_t>(n), num_controllers, r);
+    off[static_cast<size_t>(r)] = static_cast<std::int64_t>(sr.begin);
+    off[static_cast<size_t>(r) + 1] = static_cast<std::int64_t>(sr.end);
+    slots += mb_slots(static_cast<std::int64_t>(sr.size()), params.microbatch_size);
+  }
+  std::vector<yatt_sample> packed(static_cast<size_t>(n));
+  for (size_t i = 0; i < packed.size(); ++i) {
+    const workload::RolloutSample& s = batch.samples[i];
+    packed[i] = yatt_sample{s.sample_id, s.prompt_len_tokens, s.target_out_len_tokens,
+                            s.accepted_round, s.accepted ? 1 : 0};
+  }
+  auto* d_s = detail::dev<yatt_sample>(0, packed.size());
+  auto* d_r = detail::dev<yatt_round_report>(1, static_cast<size_t>(num_controllers));
+  auto* d_m = detail::dev<yatt_mb_agg>(2, static_cast<size_t>(std::max<std::int64_t>(slots, 1)));
+  detail::h2d(d_s, packed.data(), packed.size() * sizeof(yatt_sample));
+  const yatt_round_params p = to_c(params);
+  std::vector<yatt_round_report> reps(static_cast<size_t>(num_controllers));
+  std::vector<yatt_mb_agg> mbs(static_cast<size_t>(std::max<std::int64_t>(slots, 1)));
+  std::vector<std::vector<ShardRoundReport>> all;
+  for (int round = 1;; ++round) {
+    detail::throw_status(yatt_shard_round(d_s, off.data(), num_controllers, 0, batch.step_index,
+                                          round, &p, d_r, d_m, nullptr));
+    detail::d2h(reps.data(), d_r, reps.size() * sizeof(yatt_round_report));
+    detail::d2h(mbs.data(), d_m, mbs.size() * sizeof(yatt_mb_agg));
+    std::vector<ShardRoundReport> reports;
+    std::int64_t base = 0;
+    for (int r = 0; r < num_controllers; ++r) {
+      reports.push_back(from_c(reps[static_cast<size_t>(r)], mbs.data() + base));
+      base += mb_slots(off[static_cast<size_t>(r) + 1] - off[static_cast<size_t>(r)],
+                       params.microbatch_size);
+    }
+    const bool more = reduce_round_reports(reports).any_pending();
+    all.push_back(std::move(reports));
+    if (!more) break;
+  }
+  detail::d2h(packed.data(), d_s, packed.size() * sizeof(yatt_sample));
+  for (size_t i = 0; i < packed.size(); ++i) {
+    workload::RolloutSample& s = batch.samples[i];
+    s.target_out_len_tokens = packed[i].out_len_tokens;
+    s.accepted = packed[i].accepted != 0;
+    s.accepted_round = packed[i].accepted_round;
+  }
+  return all;
+}
+
+}  // namespace sim
+
+// ------------------------------------------------------------ balancer ----
+namespace balancer {
+
+double simulated_workload(double len_tokens) { return len_tokens * len_tokens; }
+
+BatchingPlan sort_and_bucket(const std::vector<int>& lengths, int batch_size, std::uint64_t seed) {
+  if (batch_size <= 0) throw ConfigError("batch_size must be positive");
+  const std::int64_t n = static_cast<std::int64_t>(lengths.size());
+  const std::int64_t nb = (n + batch_size - 1) / batch_size;
+  std::vector<std::uint32_t> flat(static_cast<size_t>(n));
+  std::vector<std::int64_t> off(static_cast<size_t>(nb) + 1);
+  detail::throw_status(yatt_sort_and_bucket_host(lengths.data(), n, batch_size, seed, flat.data(),
+                                                 off.data()));
+  BatchingPlan plan;
+  plan.batch_size = batch_size;
+  plan.shuffle_seed = seed;
+  plan.buckets.reserve(static_cast<size_t>(nb));
+  for (std::int64_t b = 0; b < nb; ++b)
+    plan.buckets.emplace_back(flat.begin() + off[static_cast<size_t>(b)],
+                              flat.begin() + off[static_cast<size_t>(b) + 1]);
+  return plan;
+}
+
+double padding_waste(const BatchingPlan& plan, const std::vector<int>& lengths) {
+  double real = 0, padded = 0;
+  for (const auto& bucket : plan.buckets) {
+    int longest = 0;
+    for (std::uint32_t i : bucket) {
+      longest = std::max(longest, lengths.at(i));
+      real += simulated_workload(lengths.at(i));
+    }
+    padded += static_cast<double>(bucket.size()) * simulated_workload(longest);
+  }
+  return padded == 0 ? 0.0 : 1.0 - real / padded;
+}
+
+double waste_bound(int batch_size) {
+  if (batch_size <= 0) throw ConfigError("batch_size must be positive");
+  const double keep = static_cast<double>(batch_size - 1) / batch_size;
+  return 1.0 - keep * keep;
+}
+
+double distribution_bias_check(const BatchingPlan& plan, const std::vector<int>& lengths,
+                               int window_buckets) {
+  if (window_buckets <= 0) throw ConfigError("window_buckets must be positive");
+  if (plan.buckets.empty() || lengths.empty()) return 0;
+  const double n = static_cast<double>(lengths.size());
+  double sum = 0;
+  for (int l : lengths) sum += l;
+  const double mu = sum / n;
+  double var = 0;
+  for (int l : lengths) var += (l - mu) * (l - mu);
+  const double sd = std::sqrt(var / n);
+  if (sd == 0) return 0;
+  const int nb = static_cast<int>(plan.buckets.size());
+  const int w = std::min(window_buckets, nb);
+  double worst = 0;
+  for (int s = 0; s + w <= nb; ++s) {
+    double ws = 0;
+    size_t cnt = 0;
+    for (int b = s; b < s + w; ++b)
+      for (std::uint32_t i : plan.buckets[static_cast<size_t>(b)]) {
+        ws += lengths.at(i);
+        ++cnt;
+      }
+    if (cnt) worst = std::max(worst, std::abs(ws / static_cast<double>(cnt) - mu) / sd);
+  }
+  return worst;
+}
+
+}  // namespace balancer
+
+// ---------------------------------------------------------- experience ----
+namespace experience {
+
+void token_logprob_stats(const std::uint16_t* pol, const std::uint16_t* ref,
+                         const std::int32_t* tgt, const std::uint8_t* mask, std::int64_t rows,
+                         int vocab, KlEstimator kl, const TokenStats& out, void* stream) {
+  detail::throw_status(yatt_token_stats(pol, ref, tgt, mask, rows, vocab, static_cast<int>(kl),
+                                        out.logp, out.ref_logp, out.entropy, out.kl, stream));
+}
+
+void GrpoConfig::validate() const {
+  if (group_size <= 0) throw ConfigError("group_size must be positive");
+  if (!(eps >= 0)) throw ConfigError("eps must be non-negative");
+}
+
+void grpo_advantages(const float* rewards, std::int64_t n, std::uint64_t first_id,
+                     const GrpoConfig& c, float* adv, const double* moments, void* stream) {
+  c.validate();
+  detail::throw_status(yatt_grpo_advantages(rewards, n, first_id, c.group_size, c.eps,
+                                            c.norm_by_std ? 1 : 0, moments, adv, stream));
+}
+
+void GaeConfig::validate() const {
+  if (!(gamma >= 0) || !(lam >= 0)) throw ConfigError("gamma and lam must be non-negative");
+}
+
+void gae(const float* values, const float* rewards, const std::uint8_t* mask,
+         const std::int64_t* cu, std::int64_t n_seqs, const GaeConfig& c, float* adv,
+         float* ret, void* stream) {
+  c.validate();
+  detail::throw_status(yatt_gae(values, rewards, mask, cu, n_seqs, c.gamma, c.lam, adv, ret,
+                                stream));
+}
+
+void PolicyLossConfig::validate() const {
+  if (!(clip_low >= 0 && clip_low < 1)) throw ConfigError("clip_low must lie in [0, 1)");
+  if (!(clip_high >= 0)) throw ConfigError("clip_high must be non-negative");
+  if (clip_ratio_c != 0 && !(clip_ratio_c > 1)) throw ConfigError("clip_ratio_c must be > 1 or 0");
+}
+
+namespace {
+yatt_loss_config to_c(const PolicyLossConfig& c) {
+  return yatt_loss_config{c.clip_low, c.clip_high, c.clip_ratio_c, c.kl_coef, c.entropy_coef,
+                          static_cast<std::int32_t>(c.aggregation)};
+}
+}  // namespace
+
+std::size_t policy_loss_workspace_bytes() { return yatt_policy_loss_workspace_bytes(0, 0, 0); }
+
+void policy_loss(const float* logp, const float* old_logp, const float* adv, const float* kl,
+                 const float* ent, const std::uint8_t* mask, std::int64_t n,
+                 const std::int64_t* cu, std::int64_t nseq, const PolicyLossConfig& c,
+                 LossSums* sums, void* ws, std::size_t ws_bytes, void* stream) {
+  static_assert(sizeof(LossSums) == sizeof(yatt_loss_sums), "LossSums layout");
+  c.validate();
+  const yatt_loss_config cc = to_c(c);
+  detail::throw_status(yatt_policy_loss(logp, old_logp, adv, kl, ent, mask, n, cu, nseq, &cc,
+                                        reinterpret_cast<yatt_loss_sums*>(sums), ws, ws_bytes,
+                                        stream));
+}
+
+double finalize_loss(const LossSums& s, const PolicyLossConfig& c) {
+  const yatt_loss_config cc = to_c(c);
+  return yatt_loss_finalize(reinterpret_cast<const yatt_loss_sums*>(&s), &cc);
+}
+
+std::size_t dynamic_sampling_workspace_bytes(std::int64_t n) {
+  return yatt_filter_compact_workspace_bytes(n);
+}
+
+void dynamic_sampling_filter(const float* rewards, const std::int64_t* lens, std::int64_t n,
+                             int G, const CompactionBuffers& o, void* ws, std::size_t ws_bytes,
+                             void* stream) {
+  detail::throw_status(yatt_filter_compact(rewards, lens, n, G, o.keep_groups, o.index_map,
+                                           o.new_cu, o.counts, ws, ws_bytes, stream));
+}
+
+}  // namespace experience
+}  // namespace yatt

@@ -1,0 +1,82 @@
+"""The C-ABI library loads without a GPU and exports every declared symbol;
+host-only entry points behave like the reference (no compute calls here)."""
+import ctypes as C
+import re
+import subprocess
+from pathlib import Path
+
+import pytest
+
+from paper_2508_07970_b200 import ConfigError, RankOutOfRange, api
+from paper_2508_07970_b200._lib import LIB_PATH, SIGNATURES, lib
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def declared_symbols():
+    text = (ROOT / "include" / "yatt_cuda.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(yatt_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    h = lib()
+    missing = [s for s in declared_symbols() if not hasattr(h, s)]
+    assert not missing, missing
+    assert set(declared_symbols()) <= set(SIGNATURES) | {"yatt_abi_version"}
+    assert h.yatt_abi_version() == 1
+
+
+def test_cpp_dropin_api_is_exported():
+    out = subprocess.run(["nm", "-DC", str(LIB_PATH)], capture_output=True, text=True).stdout
+    for sym in ["yatt::workload::rejection_process(", "yatt::workload::shard_dataset(",
+                "yatt::workload::sample_length_keyed(", "yatt::sim::shard_round_output(",
+                "yatt::sim::make_shard_state(", "yatt::sim::run_rollout_rounds(",
+                "yatt::balancer::sort_and_bucket(", "yatt::balancer::padding_waste(",
+                "yatt::experience::token_logprob_stats(", "yatt::experience::policy_loss(",
+                "yatt::experience::gae(", "yatt::experience::grpo_advantages(",
+                "yatt::experience::dynamic_sampling_filter("]:
+        assert sym in out, sym
+
+
+def test_library_links_sm100a_code_only():
+    out = subprocess.run(["cuobjdump", "--list-elf", str(LIB_PATH)], capture_output=True,
+                         text=True).stdout
+    archs = set(re.findall(r"sm_(\d+a?)", out))
+    assert archs == {"100a"}, archs
+
+
+def test_shard_dataset_host_entry_point():
+    # workload_test.cpp:166-197 known answers
+    assert [api.shard_dataset(10, 3, r).size() for r in range(3)] == [4, 3, 3]
+    assert api.shard_dataset(100, 1, 0) == api.ShardRange(0, 100)
+    cursor = 0
+    for r in range(7):
+        s = api.shard_dataset(1037, 7, r)
+        assert s.begin == cursor
+        cursor = s.end
+    assert cursor == 1037
+    with pytest.raises(RankOutOfRange):
+        api.shard_dataset(10, 3, 3)
+    with pytest.raises(RankOutOfRange):
+        api.shard_dataset(10, 3, -1)
+    with pytest.raises(ConfigError):
+        api.shard_dataset(10, 0, 0)
+
+
+def test_loss_finalize_host_entry_point():
+    from paper_2508_07970_b200 import ops
+    cfg = ops.loss_config(agg_mode="token-mean")
+    assert ops.loss_finalize([6.0, 0, 0, 0, 0, 0, 3.0, 0.0], cfg) == 2.0
+    cfg1 = ops.loss_config(agg_mode="seq-mean-token-mean")
+    assert ops.loss_finalize([1.5, 0, 0, 0, 0, 0, 9.0, 3.0], cfg1) == 0.5
+    assert ops.loss_finalize([1.5, 0, 0, 0, 0, 0, 0.0, 0.0], cfg1) == 0.0
+
+
+def test_errors_are_typed_and_messages_thread_local():
+    # A config error raised by validation before any device work.
+    h = lib()
+    rc = h.yatt_shard_dataset(5, 0, 0, None, None)
+    assert rc == 1
+    assert b"num_controllers" in h.yatt_last_error_message()
+    assert h.yatt_shard_dataset(5, 2, 9, None, None) == 2

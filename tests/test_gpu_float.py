@@ -1,0 +1,190 @@
+"""A2 GRPO advantages, A3 GAE (+ whitening), A4 policy loss on the B200 vs the
+fp64 CPU oracle: max_rel_error <= 1e-5 (north star; the reference's metric,
+proj/src/distattn.cpp:234-244).  Inputs are generated identically on both
+sides (synth recipe), never derived from a previous kernel's outputs."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2508_07970_b200 import ConfigError, ops
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+
+# ------------------------------------------------------------------- A2 ----
+@pytest.mark.parametrize("G,n", [(8, 2048), (16, 16384), (5, 1000), (1, 7)])
+@pytest.mark.parametrize("norm", [True, False])
+def test_grpo_advantages_match_oracle(cuda, G, n, norm):
+    r = ops.synth_floats(20250814, 105, 0, n, "reward", G, device=cuda)
+    got = ops.grpo_advantages(r, G, 1e-6, norm).cpu().numpy()
+    exp = O.grpo_advantages(r.cpu().numpy(), G, 1e-6, norm)
+    assert O.max_rel_error(got, exp.astype(np.float32)) <= TOL
+    # zero-variance groups: exactly zero signal (DAPO filter consistency)
+    e = exp.reshape(-1, G) if n % G == 0 else None
+    if e is not None:
+        assert np.all(got.reshape(-1, G)[np.all(e == 0, axis=1)] == 0.0)
+
+
+def test_grpo_continuous_rewards(cuda):
+    n, G = 4096, 8
+    r = torch.randn(n, device=cuda) * 3 + 1
+    got = ops.grpo_advantages(r, G).cpu().numpy()
+    exp = O.grpo_advantages(r.cpu().numpy(), G)
+    assert O.max_rel_error(got, exp.astype(np.float32)) <= TOL
+
+
+def test_grpo_groups_straddling_ranks(cuda):
+    """Misaligned shards (P=3 over 96 samples, G=8): local moments per rank,
+    merged for the straddling groups (Chan et al.), equal the single-rank
+    result.  The exchange itself is yatt_comm_allgather in production."""
+    n, G, P = 96, 8, 3
+    r_all = torch.randn(n, device=cuda)
+    full = ops.grpo_advantages(r_all, G).cpu().numpy()
+    bounds = [(0, 35), (35, 70), (70, 96)]
+    moms = {}
+    for b, e in bounds:  # each rank: local (n, mean, M2) per overlapped group
+        m = ops.grpo_group_moments(r_all[b:e].contiguous(), G, b).cpu().numpy()
+        for k, row in enumerate(m):
+            g = b // G + k
+            if g in moms:  # Chan merge
+                na, ma, qa = moms[g]
+                nb, mb, qb = row
+                nn = na + nb
+                d = mb - ma
+                moms[g] = (nn, ma + d * nb / nn, qa + qb + d * d * na * nb / nn)
+            else:
+                moms[g] = tuple(row)
+    for b, e in bounds:
+        g0, g1 = b // G, (e - 1) // G
+        table = torch.tensor([moms[g] for g in range(g0, g1 + 1)], dtype=torch.float64,
+                             device=cuda)
+        got = ops.grpo_advantages(r_all[b:e].contiguous(), G, first_sample_id=b,
+                                  moments=table).cpu().numpy()
+        assert O.max_rel_error(got, full[b:e]) <= TOL
+
+
+def test_broadcast_to_tokens(cuda):
+    vals = torch.randn(5, device=cuda)
+    cu = torch.tensor([0, 3, 3, 10, 11, 20], dtype=torch.int64, device=cuda)
+    mask = (torch.arange(20, device=cuda) % 4 != 0).to(torch.uint8)
+    out = ops.broadcast_to_tokens(vals, cu, 20, mask).cpu()
+    exp = torch.repeat_interleave(vals.cpu(), torch.tensor([3, 0, 7, 1, 9])) * mask.cpu()
+    assert torch.equal(out, exp)
+
+
+# ------------------------------------------------------------------- A3 ----
+@pytest.mark.parametrize("masked", [False, True])
+def test_gae_matches_oracle(cuda, masked):
+    rng = np.random.default_rng(1)
+    lens = np.concatenate([[1, 2, 31, 32, 33, 8192], rng.integers(1, 8193, size=58)])
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    n = int(cu[-1])
+    v = ops.synth_floats(3, 106, 0, n, "value", device=cuda)
+    r = (ops.synth_floats(3, 111, 0, n, "kl", device=cuda) * 4 - 0.5).contiguous()
+    m = torch.as_tensor((rng.random(n) < 0.85).astype(np.uint8), device=cuda) if masked else None
+    d_cu = torch.as_tensor(cu, device=cuda)
+    adv, ret = ops.gae(v, r, d_cu, m, 1.0, 0.95)
+    e_adv, e_ret = O.gae(v.cpu().numpy(), r.cpu().numpy(), cu,
+                         None if m is None else m.cpu().numpy(), 1.0, 0.95)
+    assert O.max_rel_error(adv.cpu().numpy(), e_adv.astype(np.float32)) <= TOL
+    assert O.max_rel_error(ret.cpu().numpy(), e_ret.astype(np.float32)) <= TOL
+
+
+def test_gae_gamma_lambda_sweep_and_empty(cuda):
+    cu = torch.tensor([0, 100, 100, 300], dtype=torch.int64, device=cuda)
+    v = torch.randn(300, device=cuda)
+    r = torch.randn(300, device=cuda)
+    for g, lam in [(0.99, 0.95), (1.0, 1.0), (0.5, 0.0), (0.0, 0.9)]:
+        adv, ret = ops.gae(v, r, cu, None, g, lam)
+        e_adv, e_ret = O.gae(v.cpu().numpy(), r.cpu().numpy(), cu.cpu().numpy(), None, g, lam)
+        assert O.max_rel_error(adv.cpu().numpy(), e_adv.astype(np.float32)) <= TOL
+    a, _ = ops.gae(torch.empty(0, device=cuda), torch.empty(0, device=cuda),
+                   torch.zeros(1, dtype=torch.int64, device=cuda))
+    assert a.numel() == 0
+
+
+def test_masked_moments_and_whiten(cuda):
+    n = 1_000_003
+    x = torch.randn(n, device=cuda) * 2 + 0.5
+    m = (torch.rand(n, device=cuda) < 0.7).to(torch.uint8)
+    mom = ops.masked_moments(x, m)
+    e = O.masked_moments(x.cpu().numpy(), m.cpu().numpy())
+    assert O.max_rel_error(mom.cpu().numpy(), e) <= 1e-12
+    y = x.clone()
+    ops.whiten(y, mom, m, shift_mean=True)
+    xm = x.cpu().double().numpy()[m.cpu().numpy() == 1]
+    exp = (xm - xm.mean()) / np.sqrt(xm.var(ddof=1) + 1e-8)
+    got = y.cpu().numpy()[m.cpu().numpy() == 1]
+    assert O.max_rel_error(got, exp.astype(np.float32)) <= TOL
+    assert torch.equal(y[m == 0], x[m == 0])
+
+
+# ------------------------------------------------------------------- A4 ----
+def _loss_inputs(cuda, n, seed=1):
+    logp = ops.synth_floats(seed, 107, 0, n, "logp", device=cuda)
+    old = ops.synth_floats(seed, 104, 0, n, "old_delta", base=logp, device=cuda)
+    adv = ops.synth_floats(seed, 108, 0, n, "adv", device=cuda)
+    kl = ops.synth_floats(seed, 109, 0, n, "kl", device=cuda)
+    ent = ops.synth_floats(seed, 110, 0, n, "kl", device=cuda)
+    return logp, old, adv, kl, ent
+
+
+@pytest.mark.parametrize("agg", ["token-mean", "seq-mean-token-mean", "seq-mean-token-sum"])
+@pytest.mark.parametrize("clip_c", [0.0, 3.0])
+def test_policy_loss_matches_oracle(cuda, agg, clip_c):
+    rng = np.random.default_rng(2)
+    lens = rng.integers(0, 4097, size=300)
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    n = int(cu[-1])
+    logp, old, adv, kl, ent = _loss_inputs(cuda, n)
+    mask = torch.as_tensor((rng.random(n) < 0.9).astype(np.uint8), device=cuda)
+    cfg = ops.loss_config(0.2, 0.28, clip_c, 0.01, 0.001, agg)
+    sums = ops.policy_loss(logp, old, adv, kl, ent, mask, torch.as_tensor(cu, device=cuda), cfg)
+    got = sums.cpu().numpy()
+    exp = O.policy_loss(*(t.cpu().numpy() for t in (logp, old, adv, kl, ent)),
+                        mask.cpu().numpy(), cu, 0.2, 0.28, clip_c, 0.01, 0.001,
+                        ops.AGG_MODES[agg])
+    assert O.max_rel_error(got, exp) <= TOL
+    assert got[4] > 0  # clipping exercised
+    assert abs(ops.loss_finalize(got, cfg) - ops.loss_finalize(exp, cfg)) <= \
+        TOL * abs(ops.loss_finalize(exp, cfg))
+
+
+def test_policy_loss_config_errors(cuda):
+    logp, old, adv, kl, ent = _loss_inputs(cuda, 16)
+    with pytest.raises(ConfigError):
+        ops.policy_loss(logp, old, adv, kl, ent, config=ops.loss_config(clip_low=1.5))
+    with pytest.raises(ConfigError):
+        ops.policy_loss(logp, old, adv, kl, ent, config=ops.loss_config(agg_mode=1))
+
+
+# ------------------------------------------------------ end-to-end, cfg 1 ---
+def test_config1_experience_pipeline_matches_oracle(cuda):
+    """BASELINE configs[0]: 16 prompts x 8 responses, T=256, V=32000 —
+    A1 -> A2 -> token broadcast -> A4, end to end vs the CPU oracle."""
+    P, R, T, V, seed = 16, 8, 256, 32000, 20250814
+    rows = P * R * T
+    pol, ref, tgt = ops.synth_logits(seed, 0, rows, V, device=cuda)
+    logp, rlogp, ent, kl = ops.token_stats(pol, ref, tgt, None, "k3")
+    rewards = ops.synth_floats(seed, 105, 0, P * R, "reward", R, device=cuda)
+    adv = ops.grpo_advantages(rewards, R)
+    cu = torch.arange(P * R + 1, dtype=torch.int64, device=cuda) * T
+    tadv = ops.broadcast_to_tokens(adv, cu, rows)
+    old = ops.synth_floats(seed, 104, 0, rows, "old_delta", base=logp, device=cuda)
+    cfg = ops.loss_config(0.2, 0.2, 0.0, 0.001, 0.0, "token-mean")
+    sums = ops.policy_loss(logp, old, tadv, kl, ent, None, None, cfg).cpu().numpy()
+
+    hp, hr, ht = O.synth_logits(seed, 0, rows, V)
+    st = O.token_stats(hp, hr, ht, None, "k3")
+    for i, t in enumerate((logp, rlogp, ent, kl)):
+        assert O.max_rel_error(t.cpu().numpy(), st[i]) <= TOL
+    e_adv = O.grpo_advantages(rewards.cpu().numpy(), R)
+    e_tadv = np.repeat(e_adv, T).astype(np.float32)
+    e_old = (st[0].astype(np.float32) + (old - logp).cpu().numpy()).astype(np.float32)
+    e_sums = O.policy_loss(st[0].astype(np.float32), e_old, e_tadv, st[3].astype(np.float32),
+                           st[2].astype(np.float32))
+    assert O.max_rel_error(sums, e_sums) <= 1e-4  # A1 fp32 rounding feeds the ratio
+    assert abs(ops.loss_finalize(sums, cfg) - ops.loss_finalize(e_sums, cfg)) <= \
+        1e-5 * max(1.0, abs(ops.loss_finalize(e_sums, cfg)))

@@ -1,0 +1,314 @@
+"""Integer path on the B200, bit-exact against the reference's golden vectors
+(tests/golden, from oracle/_ref) and the pinned CPU oracle.
+
+Reads like the reference's own tests (proj/tests/workload_test.cpp,
+simcore_test.cpp, balancer_test.cpp) through the Python mirror of its API.
+"""
+import json
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2508_07970_b200 import ConfigError, api, ops
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+GOLD = ROOT / "tests" / "golden"
+
+
+def load(name):
+    return json.loads((GOLD / name).read_text())
+
+
+# ------------------------------------------------------------- R6 lengths ---
+def _device_lengths(dist, seed, stream, step, rnd, ids, cuda):
+    import ctypes as C
+    from paper_2508_07970_b200._lib import check, lib
+    d_ids = torch.as_tensor(np.asarray(ids, dtype=np.int64), device=cuda)
+    out = torch.empty(len(ids), dtype=torch.int32, device=cuda)
+    check(lib().yatt_sample_lengths_keyed(C.byref(dist.c()), seed, stream, step, rnd,
+                                          d_ids.data_ptr(), len(ids), out.data_ptr(), None))
+    return out.cpu().numpy()
+
+
+def test_keyed_lengths_match_reference(cuda):
+    g = load("lengths.json")
+    for case in g["cases"]:
+        d = case["dist"]
+        dist = api.LengthDistribution(d["kind"], d["p1"], d["p2"], d["max_len"])
+        got = _device_lengths(dist, g["seed"], g["stream"], g["step"], g["round"],
+                              range(g["n"]), cuda)
+        assert got.tolist() == case["lengths"], case["name"]
+
+
+@pytest.mark.parametrize("kind,p1,p2,mx", [(api.NORMAL, 2048, 512, 4096),
+                                           (api.LOGNORMAL, 5.0, 0.5, 4096),
+                                           (api.UNIFORM, 1, 16384, 16384)])
+def test_keyed_lengths_bulk_vs_oracle(cuda, kind, p1, p2, mx):
+    """10^5 draws: device libm vs glibc agree after nearbyint."""
+    n = 100_000
+    dist = api.LengthDistribution(kind, p1, p2, mx)
+    got = _device_lengths(dist, 20250814, 2, 7, 1, range(n), cuda)
+    exp = [O.sample_length_keyed(kind, p1, p2, mx, 20250814, 2, 7, 1, i) for i in range(n)]
+    assert got.tolist() == exp
+
+
+def test_sample_lengths_statistics(cuda):
+    # workload_test.cpp:28-57 known-answer style
+    lengths = api.sample_lengths(api.LengthDistribution(api.UNIFORM, 1, 1024, 2048), 100000, 7)
+    assert abs(np.mean(lengths) - 512.5) <= 0.02 * 512.5
+    assert min(lengths) >= 1 and max(lengths) <= 1024
+
+
+# ---------------------------------------------------------- R5 rejection ---
+def test_rejection_matches_reference(cuda):
+    g = load("rejection.json")
+    batch = api.RolloutBatch(g["step"], [api.RolloutSample(g["id0"] + i, accepted=bool(a))
+                                         for i, a in enumerate(g["accepted"])])
+    for c in g["cases"]:
+        cfg = api.RejectionConfig(c["rate"], bool(c["per_group"]), c["group_size"])
+        got = api.rejection_process(batch, c["round"], cfg, 20250814)
+        assert [int(x) for x in got] == c["flags"]
+
+
+def test_rejection_invalid_config_throws(cuda):
+    batch = api.RolloutBatch(0, [api.RolloutSample(i) for i in range(4)])
+    with pytest.raises(ConfigError):
+        api.rejection_process(batch, 1, api.RejectionConfig(1.0, False, 1), 1)
+    with pytest.raises(ConfigError):
+        api.rejection_process(batch, 1, api.RejectionConfig(0.5, True, 0), 1)
+
+
+def test_group_mode_flags_whole_groups(cuda):
+    # workload_test.cpp:110-119
+    batch = api.RolloutBatch(0, [api.RolloutSample(i) for i in range(512)])
+    rej = api.rejection_process(batch, 1, api.RejectionConfig(0.5, True, 8), 21)
+    for g in range(0, 512, 8):
+        assert len(set(rej[g:g + 8])) == 1
+
+
+# ------------------------------------------------------- R3/R4 rollouts ---
+def _make_batch(case, run):
+    n = case["n"]
+    return api.RolloutBatch(case["step"], [
+        api.RolloutSample(case["step"] * n + i, run["prompt_len"][i]) for i in range(n)])
+
+
+def _params(case):
+    d = case["out_dist"]
+    return api.RoundParams(api.LengthDistribution(d["kind"], d["p1"], d["p2"], d["max_len"]),
+                           api.RejectionConfig(case["reject_rate"], bool(case["per_group"]),
+                                               case["group_size"]),
+                           case["seed"], case["mb"], case["max_rounds"])
+
+
+def _as_golden(rep):
+    return {"report": [rep.controller_rank, rep.round, rep.active_count, rep.newly_accepted_count,
+                       rep.forced_accept_count, rep.pending_count, rep.accepted_score_tokens,
+                       rep.accepted_train_units],
+            "mbs": [x for m in rep.microbatches for x in (m.controller_rank, m.mb_index,
+                                                          m.sample_count, m.max_out_len_tokens,
+                                                          m.score_tokens)]}
+
+
+@pytest.mark.parametrize("name", ["config1", "config5", "normal", "lognormal_p3"])
+def test_rollout_rounds_match_reference(cuda, name):
+    """All controller shards of a round in one launch == the reference's
+    per-shard shard_round_output loop, for P = 1/2/4/8 and misaligned P = 3."""
+    case = load(f"rollout_{name}.json")
+    params = _params(case)
+    for run in case["runs"]:
+        batch = _make_batch(case, run)
+        rounds = api.run_rollout_rounds(batch, run["controllers"], params)
+        assert [[_as_golden(r) for r in rnd] for rnd in rounds] == run["rounds"]
+        assert [s.target_out_len_tokens for s in batch.samples] == run["final_out_len"]
+        assert [int(s.accepted) for s in batch.samples] == run["final_accepted"]
+        assert [s.accepted_round for s in batch.samples] == run["final_accepted_round"]
+
+
+def test_shard_round_output_single_shard_api(cuda):
+    case = load("rollout_config1.json")
+    run = [r for r in case["runs"] if r["controllers"] == 2][0]
+    batch = _make_batch(case, run)
+    params = _params(case)
+    shards = [api.make_shard_state(batch, 2, r) for r in range(2)]
+    for rnd, golden in enumerate(run["rounds"], start=1):
+        reps = [api.shard_round_output(s, rnd, params) for s in shards]
+        assert [_as_golden(r) for r in reps] == golden
+
+
+def test_shard_reports_integer_invariants(cuda):
+    # simcore_test.cpp:322-340
+    batch = api.RolloutBatch(0, [api.RolloutSample(i, 50) for i in range(10)])
+    shard = api.make_shard_state(batch, 1, 0)
+    params = api.RoundParams(api.LengthDistribution(api.NORMAL, 300, 80, 1024),
+                             api.RejectionConfig(0.5, False, 1), 3, 16, 64)
+    rep = api.shard_round_output(shard, 1, params)
+    assert rep.active_count == 10
+    assert rep.newly_accepted_count + rep.pending_count == 10
+    assert sum(m.score_tokens for m in rep.microbatches) == \
+        sum(s.prompt_len_tokens + s.out_len_tokens for s in shard.samples)
+    with pytest.raises(ConfigError):
+        api.shard_round_output(shard, 1, api.RoundParams(microbatch_size=0))
+
+
+def test_max_rounds_forces_acceptance(cuda):
+    # simcore_test.cpp:205-217
+    batch = api.RolloutBatch(0, [api.RolloutSample(i, 64) for i in range(16)])
+    params = api.RoundParams(api.LengthDistribution(api.CONSTANT, 100, 0, 1024),
+                             api.RejectionConfig(0.9, False, 1), 3, 16, 3)
+    rounds = api.run_rollout_rounds(batch, 1, params)
+    assert len(rounds) == 3
+    assert sum(r.forced_accept_count for rnd in rounds for r in rnd) >= 1
+    assert all(s.accepted and s.accepted_round <= 3 for s in batch.samples)
+
+
+def test_reference_unit_tests_pass_against_b200_library(cuda):
+    """The reference's own workload_test.cpp + balancer_test.cpp, compiled
+    unchanged against include/yatt + libyatt_b200.so (oracle/Makefile)."""
+    exe = ROOT / "oracle" / "_ref" / "reftests_b200"
+    assert exe.exists(), "build with `make -C oracle ref` (done by __graft_entry__.build)"
+    res = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    assert "0 failed" in res.stdout
+
+
+# ---------------------------------------------------------------- R10 ----
+def test_sort_order_matches_oracle(cuda):
+    rng = np.random.default_rng(0)
+    for n in [0, 1, 7, 4096, 4097, 100_000]:
+        lengths = rng.integers(-5, 300, size=n).astype(np.int32)  # heavy ties, negatives
+        got = ops.sort_order_desc(torch.as_tensor(lengths, device=cuda)).cpu().numpy()
+        assert got.astype(np.uint32).tolist() == O.sort_order_desc(lengths).tolist()
+
+
+def test_sort_and_bucket_matches_reference(cuda):
+    """Device sort + host std::shuffle == balancer::sort_and_bucket exactly."""
+    for c in load("buckets.json")["cases"]:
+        plan = api.sort_and_bucket(c["lengths"], c["B"], c["seed"])
+        flat = [i for b in plan.buckets for i in b]
+        assert flat == c["flat"]
+        assert [0] + np.cumsum([len(b) for b in plan.buckets]).tolist() == c["offsets"]
+        assert api.padding_waste(plan, c["lengths"]) == pytest.approx(c["waste"], abs=1e-15)
+    with pytest.raises(ConfigError):
+        api.sort_and_bucket([1, 2, 3], 0, 1)
+    assert api.waste_bound(16) == 0.12109375
+
+
+# ------------------------------------------------------------ A5 / A6 ----
+def _config5_batch(cuda, token_scale=16384, n_prompts=1024, G=16, seed=20250814):
+    n = n_prompts * G
+    dist = api.LengthDistribution(api.UNIFORM, 1, token_scale, token_scale)
+    resp = _device_lengths(dist, seed, 2, 1, 1, range(n), cuda).astype(np.int64)
+    lens = resp + 64  # prompt 64 (configs[4])
+    rewards = ops.synth_floats(seed, 105, 0, n, "reward", G, device=cuda)
+    return n, G, lens, rewards
+
+
+@pytest.mark.parametrize("token_scale", [512, 16384])
+def test_filter_compact_matches_oracle(cuda, token_scale):
+    n, G, lens, rewards = _config5_batch(cuda, token_scale)
+    d_lens = torch.as_tensor(lens, device=cuda)
+    out = ops.filter_compact(rewards, d_lens, G)
+    exp = O.filter_compact(rewards.cpu().numpy(), lens, G)
+    k = int(exp["counts"][0])
+    assert out["counts"].cpu().numpy().tolist() == exp["counts"].tolist()
+    assert out["keep_groups"].cpu().numpy().tolist() == exp["keep_groups"].tolist()
+    assert out["index_map"][:k].cpu().numpy().tolist() == exp["index_map"].tolist()
+    assert out["new_cu"][:k + 1].cpu().numpy().tolist() == exp["new_cu"].tolist()
+    assert 0 < k < n  # both kinds of group present
+
+    # gather the per-token payload (token ids i32, logp f32, mask u8)
+    old_cu = torch.zeros(n + 1, dtype=torch.int64, device=cuda)
+    old_cu[1:] = torch.cumsum(d_lens, 0)
+    total = int(old_cu[-1])
+    tok = torch.randint(0, 152064, (total,), dtype=torch.int32, device=cuda)
+    lp = torch.randn(total, device=cuda)
+    mk = (torch.arange(total, device=cuda) % 3 != 0).to(torch.uint8)
+    kept_tokens = int(exp["counts"][1])
+    np_old_cu = old_cu.cpu().numpy()
+    idx = np.concatenate([np.arange(np_old_cu[s], np_old_cu[s + 1]) for s in exp["index_map"]])
+    for src in (tok, lp, mk):
+        dst = torch.empty(kept_tokens, dtype=src.dtype, device=cuda)
+        ops.gather_varlen(src, old_cu, out["index_map"], out["new_cu"], out["counts"][:1], n, dst)
+        assert torch.equal(dst.cpu(), src.cpu()[torch.from_numpy(idx)])
+
+    # multimodal payload refs: 4 x int64 per sample, remapped by the index map
+    refs = torch.arange(n * 4, dtype=torch.int64, device=cuda).view(n, 4)
+    rdst = torch.empty((k, 4), dtype=torch.int64, device=cuda)
+    ops.gather_rows(refs, out["index_map"], out["counts"][:1], n, rdst)
+    assert torch.equal(rdst.cpu(), refs.cpu()[torch.from_numpy(exp["index_map"]).long()])
+
+
+def test_filter_compact_edge_cases(cuda):
+    G = 4
+    lens = torch.full((8,), 3, dtype=torch.int64, device=cuda)
+    # all groups zero-variance -> nothing kept
+    r = torch.ones(8, device=cuda)
+    out = ops.filter_compact(r, lens, G)
+    assert out["counts"].cpu().tolist() == [0, 0, 0]
+    assert int(out["new_cu"][0]) == 0
+    # all kept
+    r = torch.tensor([0, 1, 0, 0, 1, 1, 0, 1], dtype=torch.float32, device=cuda)
+    out = ops.filter_compact(r, lens, G)
+    assert out["counts"].cpu().tolist() == [8, 24, 2]
+    # empty batch
+    e = ops.filter_compact(torch.empty(0, device=cuda), torch.empty(0, dtype=torch.int64,
+                                                                      device=cuda), G)
+    assert e["counts"].cpu().tolist() == [0, 0, 0]
+    with pytest.raises(ConfigError):
+        ops.filter_compact(torch.ones(6, device=cuda), torch.ones(6, dtype=torch.int64,
+                                                                 device=cuda), 4)
+
+
+def test_microbatch_aggregates_over_survivors(cuda):
+    n, G, lens, rewards = _config5_batch(cuda, 512, 64)
+    out = ops.filter_compact(rewards, torch.as_tensor(lens, device=cuda), G)
+    k = int(out["counts"][0])
+    imap = out["index_map"][:k].long()
+    plen = torch.full((n,), 64, dtype=torch.int32, device=cuda)
+    olen = torch.as_tensor(lens - 64, dtype=torch.int32, device=cuda)
+    p_k, o_k = plen[imap].contiguous(), olen[imap].contiguous()
+    mbs = ops.microbatch_aggregates(p_k, o_k, 16, controller_rank=3).cpu().numpy()
+    o = o_k.cpu().numpy()
+    for j in range(-(-k // 16)):
+        sl = slice(16 * j, min(k, 16 * j + 16))
+        score = int(mbs[j, 4]) | (int(mbs[j, 5]) << 32)
+        assert mbs[j, :4].tolist() == [3, j, sl.stop - sl.start, int(o[sl].max())]
+        assert score == int(64 * (sl.stop - sl.start) + o[sl].sum())
+
+
+def test_global_compaction_across_emulated_ranks(cuda):
+    """P ranks compact their group-aligned shards; all-gathered counts ->
+    exclusive offsets -> one global packed layout identical to P = 1."""
+    n, G, lens, rewards = _config5_batch(cuda, 256, 128)
+    d_lens = torch.as_tensor(lens, device=cuda)
+    single = ops.filter_compact(rewards, d_lens, G)
+    kt = int(single["counts"][1])
+    P = 4
+    outs, counts = [], []
+    for r in range(P):
+        s = api.shard_dataset(n // G, P, r)
+        sl = slice(s.begin * G, s.end * G)
+        o = ops.filter_compact(rewards[sl].contiguous(), d_lens[sl].contiguous(), G)
+        outs.append((sl, o))
+        counts.append(o["counts"])
+    gathered = torch.cat(counts)  # stands in for yatt_comm_allgather_i64
+    payload = torch.arange(int(d_lens.sum()), dtype=torch.int32, device=cuda)
+    cu_all = torch.zeros(n + 1, dtype=torch.int64, device=cuda)
+    cu_all[1:] = torch.cumsum(d_lens, 0)
+    dst = torch.full((kt,), -1, dtype=torch.int32, device=cuda)
+    for r, (sl, o) in enumerate(outs):
+        off = ops.exclusive_offset(gathered, P, r, 3, 1)
+        local_cu = (cu_all[sl.start:sl.stop + 1] - cu_all[sl.start]).contiguous()
+        src = payload[int(cu_all[sl.start]):int(cu_all[sl.stop])].contiguous()
+        ops.gather_varlen(src, local_cu, o["index_map"], o["new_cu"], o["counts"][:1],
+                          sl.stop - sl.start, dst, off)
+    ref = torch.empty(kt, dtype=torch.int32, device=cuda)
+    ops.gather_varlen(payload, cu_all, single["index_map"], single["new_cu"],
+                      single["counts"][:1], n, ref)
+    assert torch.equal(dst, ref)
