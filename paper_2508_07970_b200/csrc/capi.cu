@@ -179,8 +179,8 @@ int yatt_token_stats_host(const uint16_t* h_pol, const uint16_t* h_ref, const in
   YATT_REQUIRE(vocab > 0 && vocab % 8 == 0, YATT_ERR_CONFIG,
                "token_stats: vocab must be a positive multiple of 8 (got %d)", vocab);
   YATT_REQUIRE(rows >= 0, YATT_ERR_CONFIG, "token_stats: rows must be >= 0");
-  YATT_REQUIRE(h_logp != nullptr, YATT_ERR_CONFIG, "token_stats: logp output is required");
   if (rows == 0) return YATT_OK;
+  YATT_REQUIRE(h_logp != nullptr, YATT_ERR_CONFIG, "token_stats: logp output is required");
   YATT_REQUIRE(h_pol && h_ref && h_tgt, YATT_ERR_CONFIG, "token_stats: null input pointer");
   // ~128 MiB per tensor per chunk: long enough to amortise per-copy
   // overhead, short enough that two slots overlap copy and compute.

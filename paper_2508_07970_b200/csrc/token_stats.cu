@@ -47,6 +47,7 @@ constexpr int kVecPerTile = kTile / 8;                  // 16-byte vectors
 constexpr int kVecPerThread = kVecPerTile / kConsumers;  // full-tile unroll
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr double kLn2 = 0.69314718055994530942;
+constexpr float kLn2f = 0.69314718f;
 constexpr float kSlack = 24.0f;  // allow 2^a up to 2^24 before re-basing
 constexpr int kMinitial = -(1 << 24);
 static_assert(kVecPerTile % kConsumers == 0, "tile must split evenly");
@@ -79,23 +80,29 @@ struct Params {
   float* kl;
 };
 
-// Per-thread online state for one row.
+// Per-thread online state for one row.  Element pairs (the two bf16 of one
+// 32-bit word) are processed with Blackwell's packed f32x2 FMA/ADD
+// (FFMA2/FADD2: two IEEE fp32 RN operations per instruction), halving the
+// FMA-pipe issue count; each lane keeps the exact per-element arithmetic.
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 ex2x2(float2 a) {
+  return make_float2(ex2_approx(a.x), ex2_approx(a.y));
+}
+
 template <bool kFull>
 struct Acc {
-  float s[8], w[8], sq[8], u[8];
-  float mp, mq;      // integer-valued bases (log2 units)
+  float2 s[4], w[4], sq[4], u[4];
+  float mp, mq;        // integer-valued bases (log2 units)
   float thr_p, thr_q;  // rebase when a logit exceeds these
 
   __device__ __forceinline__ void reset() {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      s[j] = 0.f;
-      w[j] = 0.f;
-      sq[j] = 0.f;
-      if (kFull) u[j] = 0.f;
+    for (int k = 0; k < 4; ++k) {
+      s[k] = w[k] = sq[k] = f2(0.f, 0.f);
+      if (kFull) u[k] = f2(0.f, 0.f);
     }
     mp = mq = float(kMinitial);
-    thr_p = thr_q = (float(kMinitial) + kSlack) / kLog2e;
+    thr_p = thr_q = (float(kMinitial) + kSlack) * kLn2f;
   }
 
   // Rebase policy accumulators to m' = ceil(vmax*log2e): exact 2^(m-m').
@@ -105,14 +112,15 @@ struct Acc {
     if (mn <= mp) return;
     const float d = mp - mn;
     const float c = exp2_int(int(d));
+    const float2 c2 = f2(c, c), d2 = f2(d, d);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      w[j] = c * fmaf(d, s[j], w[j]);
-      s[j] *= c;
-      if (kFull) u[j] *= c;
+    for (int k = 0; k < 4; ++k) {
+      w[k] = __fmul2_rn(c2, __ffma2_rn(d2, s[k], w[k]));
+      s[k] = __fmul2_rn(c2, s[k]);
+      if (kFull) u[k] = __fmul2_rn(c2, u[k]);
     }
     mp = mn;
-    thr_p = (mp + kSlack) / kLog2e;
+    thr_p = (mp + kSlack) * kLn2f;
   }
   __device__ __forceinline__ void rebase_q(float vmax) {
     float mn = ceilf(vmax * kLog2e);
@@ -120,31 +128,34 @@ struct Acc {
     if (mn <= mq) return;
     const float c = exp2_int(int(mq - mn));
 #pragma unroll
-    for (int j = 0; j < 8; ++j) sq[j] *= c;
+    for (int k = 0; k < 4; ++k) sq[k] = __fmul2_rn(f2(c, c), sq[k]);
     mq = mn;
-    thr_q = (mq + kSlack) / kLog2e;
+    thr_q = (mq + kSlack) * kLn2f;
   }
 
   // Accumulate one 8-element vector pair (policy P already floored).
   __device__ __forceinline__ void step(const uint4& P, const uint4& Q) {
     const uint32_t pw[4] = {P.x, P.y, P.z, P.w};
     const uint32_t qw[4] = {Q.x, Q.y, Q.z, Q.w};
+    const float2 L2 = f2(kLog2e, kLog2e);
+    const float2 nmp = f2(-mp, -mp), nmq = f2(-mq, -mq);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int j = 2 * k + h;
-        const float x = h ? bf16_hi(pw[k]) : bf16_lo(pw[k]);
-        const float z = h ? bf16_hi(qw[k]) : bf16_lo(qw[k]);
-        const float a = fmaf(x, kLog2e, -mp);
-        const float e = ex2_approx(a);
-        s[j] += e;
-        w[j] = fmaf(e, a, w[j]);
-        const float b = fmaf(z, kLog2e, -mq);
-        sq[j] += ex2_approx(b);
-        if (kFull) u[j] = fmaf(e, x - z, u[j]);
-      }
+      const float2 x = f2(bf16_lo(pw[k]), bf16_hi(pw[k]));
+      const float2 z = f2(bf16_lo(qw[k]), bf16_hi(qw[k]));
+      const float2 a = __ffma2_rn(x, L2, nmp);
+      const float2 e = ex2x2(a);
+      s[k] = __fadd2_rn(s[k], e);
+      w[k] = __ffma2_rn(e, a, w[k]);
+      const float2 b = __ffma2_rn(z, L2, nmq);
+      sq[k] = __fadd2_rn(sq[k], ex2x2(b));
+      if (kFull) u[k] = __ffma2_rn(e, __ffma2_rn(z, f2(-1.f, -1.f), x), u[k]);
     }
+  }
+
+  // Thread total of one accumulator set (pairwise tree).
+  __device__ __forceinline__ static float total(const float2 (&v)[4]) {
+    return ((v[0].x + v[0].y) + (v[1].x + v[1].y)) + ((v[2].x + v[2].y) + (v[3].x + v[3].y));
   }
 };
 
@@ -168,10 +179,6 @@ __device__ __forceinline__ uint4 floor_policy(uint4 v) {
   v.z = bmax2(v.z, kFloor);
   v.w = bmax2(v.w, kFloor);
   return v;
-}
-__device__ __forceinline__ float pick_bf16(const uint4& v, int idx) {
-  const uint32_t w = (idx >> 1) == 0 ? v.x : (idx >> 1) == 1 ? v.y : (idx >> 1) == 2 ? v.z : v.w;
-  return (idx & 1) ? bf16_hi(w) : bf16_lo(w);
 }
 
 __device__ __forceinline__ RowPartial combine(const RowPartial& A, const RowPartial& B) {
@@ -270,7 +277,8 @@ __global__ void __launch_bounds__(kThreads, 2) token_stats_kernel(const Params p
       continue;
     }
     const int par = iter & 1;
-    const int64_t yv = int64_t(y) >> 3;  // vector holding the target
+    const int ty = y / kTile;           // tile holding the target logit
+    const int yin = y - ty * kTile;
     acc.reset();
 
     for (int t = 0; t < ntiles; ++t) {
@@ -278,8 +286,11 @@ __global__ void __launch_bounds__(kThreads, 2) token_stats_kernel(const Params p
       const int nvec = int(min64(kTile, V - e0) >> 3);
       const uint16_t* sp = ring + size_t(stage) * 2 * kTile;
       const uint16_t* sq = sp + kTile;
-      const int64_t v0 = e0 >> 3;
       mbar_wait(&tail->full[stage], phase);
+      if (t == ty && tid == 0) {  // target logits straight from the staged tile
+        tail->tgt[par][0] = __uint_as_float(uint32_t(sp[yin]) << 16);
+        tail->tgt[par][1] = __uint_as_float(uint32_t(sq[yin]) << 16);
+      }
       if (nvec == kVecPerTile) {
         uint4 P[kVecPerThread], Q[kVecPerThread];
 #pragma unroll
@@ -289,13 +300,7 @@ __global__ void __launch_bounds__(kThreads, 2) token_stats_kernel(const Params p
           Q[i] = lds128(sq + v * 8);
         }
 #pragma unroll
-        for (int i = 0; i < kVecPerThread; ++i) {
-          if (v0 + tid + i * kConsumers == yv) {
-            tail->tgt[par][0] = pick_bf16(P[i], y & 7);
-            tail->tgt[par][1] = pick_bf16(Q[i], y & 7);
-          }
-          P[i] = floor_policy(P[i]);
-        }
+        for (int i = 0; i < kVecPerThread; ++i) P[i] = floor_policy(P[i]);
         uint32_t mpv = vmax4(P[0]), mqv = vmax4(Q[0]);
 #pragma unroll
         for (int i = 1; i < kVecPerThread; ++i) {
@@ -311,10 +316,6 @@ __global__ void __launch_bounds__(kThreads, 2) token_stats_kernel(const Params p
         for (int v = tid; v < nvec; v += kConsumers) {
           uint4 P = lds128(sp + v * 8);
           const uint4 Q = lds128(sq + v * 8);
-          if (v0 + v == yv) {
-            tail->tgt[par][0] = pick_bf16(P, y & 7);
-            tail->tgt[par][1] = pick_bf16(Q, y & 7);
-          }
           P = floor_policy(P);
           const float fmp = pair_max(vmax4(P)), fmq = pair_max(vmax4(Q));
           if (fmp > acc.thr_p) acc.rebase_p(fmp);
@@ -334,24 +335,10 @@ __global__ void __launch_bounds__(kThreads, 2) token_stats_kernel(const Params p
     RowPartial r;
     r.mp = acc.mp;
     r.mq = acc.mq;
-    {
-      float s0 = (acc.s[0] + acc.s[1]) + (acc.s[2] + acc.s[3]);
-      float s1 = (acc.s[4] + acc.s[5]) + (acc.s[6] + acc.s[7]);
-      r.s = s0 + s1;
-      float w0 = (acc.w[0] + acc.w[1]) + (acc.w[2] + acc.w[3]);
-      float w1 = (acc.w[4] + acc.w[5]) + (acc.w[6] + acc.w[7]);
-      r.w = w0 + w1;
-      float q0 = (acc.sq[0] + acc.sq[1]) + (acc.sq[2] + acc.sq[3]);
-      float q1 = (acc.sq[4] + acc.sq[5]) + (acc.sq[6] + acc.sq[7]);
-      r.sq = q0 + q1;
-      if (kFull) {
-        float u0 = (acc.u[0] + acc.u[1]) + (acc.u[2] + acc.u[3]);
-        float u1 = (acc.u[4] + acc.u[5]) + (acc.u[6] + acc.u[7]);
-        r.u = u0 + u1;
-      } else {
-        r.u = 0.f;
-      }
-    }
+    r.s = Acc<kFull>::total(acc.s);
+    r.w = Acc<kFull>::total(acc.w);
+    r.sq = Acc<kFull>::total(acc.sq);
+    r.u = kFull ? Acc<kFull>::total(acc.u) : 0.f;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) r = combine(r, shfl_partial(r, off));
     if (lane == 0) tail->red[par][warp] = r;
@@ -401,8 +388,8 @@ int token_stats_launch(const uint16_t* pol, const uint16_t* ref, const int32_t* 
   YATT_REQUIRE(rows >= 0, YATT_ERR_CONFIG, "token_stats: rows must be >= 0");
   YATT_REQUIRE(kl_mode >= YATT_KL_K1 && kl_mode <= YATT_KL_FULL, YATT_ERR_CONFIG,
                "token_stats: unknown kl_mode %d", kl_mode);
-  YATT_REQUIRE(logp != nullptr, YATT_ERR_CONFIG, "token_stats: logp output is required");
   if (rows == 0) return YATT_OK;
+  YATT_REQUIRE(logp != nullptr, YATT_ERR_CONFIG, "token_stats: logp output is required");
   YATT_REQUIRE(pol && ref && tgt, YATT_ERR_CONFIG, "token_stats: null input pointer");
   YATT_REQUIRE((reinterpret_cast<uintptr_t>(pol) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(ref) & 15) == 0,
