@@ -1,0 +1,130 @@
+"""Parallel-controller rank plumbing: sharding by prompt group and the tiny
+cross-rank exchanges of the experience step.
+
+The reference runs one controller per rank over a contiguous shard
+(workload::shard_dataset, proj/src/workload.cpp:183-198) and reduces the
+per-rank integer reports on a coordinator over JSON/TCP RPC
+(proj/src/demo.cpp:261-274, simcore.cpp:304-311).  Here every rank owns whole
+prompt groups and the only traffic is
+  * all-reduce(sum) of the 8 fp64 loss sums (global token / sequence count),
+  * all-gather of per-rank survivor counts -> exclusive offsets into one
+    global packed layout (dynamic sampling),
+  * for shards that split a group (P not dividing the group count): an
+    all-gather of the boundary groups' (n, mean, M2) moments, merged with
+    Chan et al.'s pairwise update so advantages match a single rank.
+Transport: a torch.distributed group (NCCL for device tensors, gloo on CPU)
+or the C-ABI NCCL communicator (YattComm).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from ._lib import check, lib
+
+
+def shard_groups(n_groups: int, world: int, rank: int) -> tuple[int, int]:
+    """[g_begin, g_end) of the prompt groups owned by `rank` (the reference's
+    near-even split applied to groups, so groups never straddle ranks)."""
+    if world <= 0:
+        from ._lib import ConfigError
+        raise ConfigError("num_controllers must be positive")
+    base, rem = divmod(n_groups, world)
+    b = rank * base + min(rank, rem)
+    return b, b + base + (1 if rank < rem else 0)
+
+
+def merge_moments(a, b):
+    """Chan et al. pairwise merge of (n, mean, M2) triples (fp64)."""
+    na, ma, qa = a
+    nb, mb, qb = b
+    if na == 0:
+        return (nb, mb, qb)
+    if nb == 0:
+        return (na, ma, qa)
+    n = na + nb
+    d = mb - ma
+    return (n, ma + d * nb / n, qa + qb + d * d * na * nb / n)
+
+
+def merged_boundary_moments(local: torch.Tensor, first_group: int, all_boundaries):
+    """Fix up the first/last rows of this rank's (n, mean, M2) table with the
+    other ranks' partial moments of the same global groups.
+
+    all_boundaries: list over ranks of (first_group, first_row, last_group,
+    last_row) as gathered from every rank (all_gather_object / a tiny
+    all-gather of 8 doubles)."""
+    table = local.clone()
+    parts: dict[int, list] = {}
+    for fg, frow, lg, lrow in all_boundaries:
+        parts.setdefault(fg, []).append(tuple(frow))
+        if lg != fg:
+            parts.setdefault(lg, []).append(tuple(lrow))
+    for k in (0, table.shape[0] - 1):
+        g = first_group + k
+        acc = (0.0, 0.0, 0.0)
+        for p in parts.get(g, []):
+            acc = merge_moments(acc, p)
+        if parts.get(g):
+            table[k] = torch.tensor(acc, dtype=table.dtype, device=table.device)
+    return table
+
+
+class YattComm:
+    """The C-ABI NCCL communicator (yatt_comm_*): device buffers, caller's
+    current stream.  The 128-byte unique id travels out of band."""
+
+    def __init__(self, world: int, rank: int, unique_id: bytes):
+        self.world, self.rank = world, rank
+        self.h = C.c_void_p()
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        check(lib().yatt_comm_init(world, rank, C.addressof(buf), C.byref(self.h)))
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(lib().yatt_comm_unique_id(C.addressof(buf)))
+        return bytes(buf)
+
+    def _st(self):
+        return torch.cuda.current_stream().cuda_stream
+
+    def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
+        fn = lib().yatt_comm_allreduce_f64 if t.dtype == torch.float64 else \
+            lib().yatt_comm_allreduce_i64
+        check(fn(self.h, t.data_ptr(), t.numel(), self._st()))
+        return t
+
+    def allgather(self, t: torch.Tensor) -> torch.Tensor:
+        out = torch.empty((self.world * t.numel(),), dtype=t.dtype, device=t.device)
+        check(lib().yatt_comm_allgather_i64(self.h, t.data_ptr(), out.data_ptr(), t.numel(),
+                                            self._st()))
+        return out
+
+    def close(self):
+        if self.h:
+            check(lib().yatt_comm_destroy(self.h))
+            self.h = C.c_void_p()
+
+
+def allreduce_sums(sums: torch.Tensor, comm=None) -> torch.Tensor:
+    """Sum the fp64 loss sums over ranks (in place)."""
+    if comm is None:
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+            dist.all_reduce(sums)
+        return sums
+    return comm.allreduce_(sums)
+
+
+def allgather_counts(counts: torch.Tensor, comm=None) -> torch.Tensor:
+    """Per-rank int64 count vectors, rank-major (world * counts.numel())."""
+    if comm is None:
+        import torch.distributed as dist
+        if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+            return counts.clone()
+        out = [torch.empty_like(counts) for _ in range(dist.get_world_size())]
+        dist.all_gather(out, counts)
+        return torch.cat(out)
+    return comm.allgather(counts)

@@ -1,0 +1,93 @@
+"""Multi-GPU check of the rank-level path (run under torchrun, N >= 2).
+
+Each rank owns prompt groups shard_groups(16, N, r) of a config-1-shaped
+GRPO batch (16 prompts x 8 responses, T=256, V=32000) and runs
+A1 -> A2 -> broadcast -> A4 on its own GPU; the loss sums are all-reduced
+through the C-ABI NCCL communicator (yatt_comm_*).  Dynamic-sampling
+compaction uses yatt_comm_allgather_i64 + yatt_exclusive_offset to write one
+global packed layout.  Both must equal the single-GPU result bit for bit
+(sums: up to fp64 reassociation).  Prints "mgpu ok" on success.
+"""
+import os
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from paper_2508_07970_b200 import ops, ranks  # noqa: E402
+
+P, R, T, V, SEED = 16, 8, 256, 32000, 20250814
+
+
+def step(g0, g1, dev):
+    rows = (g1 - g0) * R * T
+    pol, ref, tgt = ops.synth_logits(SEED, g0 * R * T, rows, V, device=dev)
+    logp, rlogp, ent, kl = ops.token_stats(pol, ref, tgt, None, "k3")
+    rewards = ops.synth_floats(SEED, 105, g0 * R, (g1 - g0) * R, "reward", R, device=dev)
+    adv = ops.grpo_advantages(rewards, R, 1e-6, True, g0 * R)
+    cu = torch.arange((g1 - g0) * R + 1, dtype=torch.int64, device=dev) * T
+    tadv = ops.broadcast_to_tokens(adv, cu, rows)
+    old = ops.synth_floats(SEED, 104, g0 * R * T, rows, "old_delta", base=logp, device=dev)
+    return ops.policy_loss(logp, old, tadv, kl, ent), rewards
+
+
+def main():
+    world, rank = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    uid = [ranks.YattComm.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = ranks.YattComm(world, rank, uid[0])
+
+    # collectives sanity
+    x = torch.full((5,), float(rank + 1), dtype=torch.float64, device=dev)
+    comm.allreduce_(x)
+    assert torch.all(x == world * (world + 1) / 2)
+    c = torch.tensor([rank, 10 * rank], dtype=torch.int64, device=dev)
+    g = comm.allgather(c)
+    assert g.tolist() == [v for r in range(world) for v in (r, 10 * r)]
+
+    # sharded GRPO experience step vs the full batch on one GPU
+    g0, g1 = ranks.shard_groups(P, world, rank)
+    sums, _ = step(g0, g1, dev)
+    comm.allreduce_(sums)
+    full, rewards_all = step(0, P, dev)
+    torch.cuda.synchronize()
+    rel = ((sums - full).abs() / (full.abs() + 1e-12)).max().item()
+    assert rel <= 1e-12, (rank, rel, sums.tolist(), full.tolist())
+
+    # global compaction across ranks
+    lens_all = torch.full((P * R,), T, dtype=torch.int64, device=dev) + \
+        torch.arange(P * R, dtype=torch.int64, device=dev) % 7
+    single = ops.filter_compact(rewards_all, lens_all, R)
+    loc = ops.filter_compact(rewards_all[g0 * R:g1 * R].contiguous(),
+                             lens_all[g0 * R:g1 * R].contiguous(), R)
+    counts = comm.allgather(loc["counts"])
+    off = ops.exclusive_offset(counts, world, rank, 3, 1)
+    cu_all = torch.zeros(P * R + 1, dtype=torch.int64, device=dev)
+    cu_all[1:] = torch.cumsum(lens_all, 0)
+    payload = torch.arange(int(cu_all[-1]), dtype=torch.int32, device=dev)
+    kt = int(single["counts"][1])
+    dst = torch.zeros(kt, dtype=torch.int32, device=dev)
+    local_cu = (cu_all[g0 * R:g1 * R + 1] - cu_all[g0 * R]).contiguous()
+    src = payload[int(cu_all[g0 * R]):int(cu_all[g1 * R])].contiguous()
+    ops.gather_varlen(src, local_cu, loc["index_map"], loc["new_cu"], loc["counts"][:1],
+                      (g1 - g0) * R, dst, off)
+    dist.all_reduce(dst)  # ranks wrote disjoint ranges into zero-initialised buffers
+    ref = torch.empty(kt, dtype=torch.int32, device=dev)
+    ops.gather_varlen(payload, cu_all, single["index_map"], single["new_cu"],
+                      single["counts"][:1], P * R, ref)
+    assert torch.equal(dst, ref)
+    comm.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    if rank == 0:
+        print(f"mgpu ok world={world}")
+
+
+if __name__ == "__main__":
+    main()
