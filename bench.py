@@ -179,7 +179,7 @@ def run_reference(args):
             "cpu_baseline": {**last, "value": v},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -320,7 +320,7 @@ def run_b200(args):
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": args.steps * (ng + 4), "clocks": clk,
                 "loss": loss}
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -380,7 +380,23 @@ def run_e2e(args, dev, ops, cfg, ws):
             "sample": f"one {rows}-token response per step ({h2d / 1e9:.2f} GB H2D)"}
 
 
+_JSON_OUT = None
+
+
+def emit(line: dict) -> None:
+    """The one JSON line on the real stdout (everything else goes to stderr)."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    global _JSON_OUT
+    # Libraries (NCCL, torch) may print banners on stdout; keep stdout for the
+    # single JSON line by pointing fd 1 at stderr for the rest of the run.
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
