@@ -6,9 +6,11 @@ shared object is missing the import of any op raises immediately.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libyatt_b200.so"
+LIB_PATH = Path(os.environ.get("YATT_B200_LIB") or
+                Path(__file__).resolve().parent / "libyatt_b200.so")
 
 c_i32, c_i64, c_u64, c_f32, c_f64, c_p, c_sz = (C.c_int32, C.c_int64, C.c_uint64, C.c_float,
                                                 C.c_double, C.c_void_p, C.c_size_t)

@@ -49,9 +49,9 @@ def _digest(path: Path, flags: list[str]) -> str:
     return h.hexdigest()[:16]
 
 
-def _compile(src: Path, verbose: bool) -> Path:
+def _compile(src: Path, verbose: bool, extra: tuple = ()) -> Path:
     is_cu = src.suffix == ".cu"
-    flags = NVCC_FLAGS if is_cu else CXX_FLAGS
+    flags = (NVCC_FLAGS if is_cu else CXX_FLAGS) + list(extra)
     obj = BUILD / f"{src.stem}.{_digest(src, flags)}.o"
     if obj.exists():
         return obj
@@ -88,5 +88,24 @@ def build(verbose: bool = False) -> Path:
     return LIB
 
 
+def build_variant(name: str, defines: dict) -> Path:
+    """Experiment build: token_stats.cu recompiled with -D overrides, linked
+    into _variants/libyatt_b200_<name>.so (load it with YATT_B200_LIB=...)."""
+    BUILD.mkdir(parents=True, exist_ok=True)
+    extra = tuple(f"-D{k}={v}" for k, v in sorted(defines.items()))
+    objs = []
+    for src in sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp")):
+        objs.append(_compile(src, False, extra if src.name == "token_stats.cu" else ()))
+    out = PKG / "_variants" / f"libyatt_b200_{name}.so"
+    out.parent.mkdir(exist_ok=True)
+    cmd = [nvcc(), "-shared", "-o", str(out)] + ARCH + [str(o) for o in objs] + [
+        "-L/usr/lib/x86_64-linux-gnu", "-lnccl", "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+    subprocess.run(cmd, check=True, capture_output=True)
+    return out
+
+
 if __name__ == "__main__":
-    print(build(verbose=True))
+    if len(sys.argv) > 2 and sys.argv[1] == "variant":
+        print(build_variant(sys.argv[2], dict(a.split("=") for a in sys.argv[3:])))
+    else:
+        print(build(verbose=True))

@@ -100,39 +100,94 @@ __device__ __forceinline__ Aff shfl_down_aff(const Aff& x, int d) {
              __shfl_down_sync(0xffffffffu, x.q, d)};
 }
 
-__global__ void gae_kernel(const float* values, const float* rewards, const uint8_t* mask,
-                           const int64_t* cu, int64_t nseq, double gamma, double lam, float* adv,
-                           float* ret) {
-  const int warps_per_block = blockDim.x >> 5;
-  const int lane = threadIdx.x & 31;
+// One CTA per sequence.  A segment of up to kGaeSeg tokens is staged in
+// shared memory with coalesced loads (padded [thread][token] layout, no bank
+// conflicts); thread i owns kGaeTpt contiguous tokens: it composes their maps
+// right-to-left, a block scan (warp shuffles + smem across warps) gives every
+// thread the composite of everything to its right, then it replays its tokens
+// with the incoming state, writes A/R back to smem, and the CTA stores them
+// coalesced.  Longer sequences loop over segments right-to-left with a carry.
+constexpr int kGaeThreads = 256;
+constexpr int kGaeTpt = 16;
+constexpr int kGaeSeg = kGaeThreads * kGaeTpt;
+constexpr int kGaePad = kGaeTpt + 1;
+
+__device__ __forceinline__ int gae_slot(int idx) { return (idx / kGaeTpt) * kGaePad + idx % kGaeTpt; }
+
+__global__ void __launch_bounds__(kGaeThreads) gae_kernel(
+    const float* values, const float* rewards, const uint8_t* mask, const int64_t* cu,
+    int64_t nseq, double gamma, double lam, float* adv, float* ret) {
+  __shared__ float sv[kGaeThreads * kGaePad];
+  __shared__ float sr[kGaeThreads * kGaePad];
+  __shared__ uint8_t sm[kGaeThreads * kGaePad];
+  __shared__ Aff wtot[kGaeThreads / 32];
+  __shared__ double carry[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double gl = gamma * lam;
-  for (int64_t s = int64_t(blockIdx.x) * warps_per_block + (threadIdx.x >> 5); s < nseq;
-       s += int64_t(gridDim.x) * warps_per_block) {
+  for (int64_t s = blockIdx.x; s < nseq; s += gridDim.x) {
     const int64_t b = cu[s], e = cu[s + 1];
-    double cA = 0.0, cV = 0.0;  // carry entering from the right
-    for (int64_t hi = e; hi > b; hi -= 32) {
-      const int64_t t = hi - 32 + lane;
-      const bool inr = t >= b;
-      double v = 0.0;
-      Aff f{1.0, 0.0, 1.0, 0.0, 0.0};
-      if (inr) {
-        v = double(values[t]);
-        if (mask == nullptr || mask[t]) f = Aff{gl, gamma, 0.0, double(rewards[t]) - v, v};
+    double cA = 0.0, cV = 0.0;  // state entering from the right of the segment
+    for (int64_t hi = e; hi > b; hi -= kGaeSeg) {
+      const int64_t lo = max64(b, hi - kGaeSeg);
+      const int n = int(hi - lo);
+      for (int i = tid; i < n; i += kGaeThreads) {
+        const int k = gae_slot(i);
+        sv[k] = values[lo + i];
+        sr[k] = rewards[lo + i];
+        sm[k] = mask == nullptr ? uint8_t(1) : mask[lo + i];
       }
-      // inclusive scan from the right: f_l <- f_l o f_{l+1} o ... o f_31
+      __syncthreads();
+      // this thread's tokens [t0, t1) within the segment
+      const int t0 = tid * kGaeTpt, t1 = min(n, t0 + kGaeTpt);
+      Aff f{1.0, 0.0, 1.0, 0.0, 0.0};
+      for (int t = t1 - 1; t >= t0; --t) {
+        const int k = gae_slot(t);
+        if (sm[k]) {
+          const double v = sv[k];
+          f = Aff{gl * f.a, gl * f.b + gamma * f.k, 0.0, gl * f.p + gamma * f.q + (double(sr[k]) - v),
+                  v};
+        }
+      }
+      // exclusive composite of the threads to the right: inclusive warp scan
+      // from the right, then compose with the totals of later warps
+      Aff inc = f;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
-        const Aff o = shfl_down_aff(f, d);
-        if (lane + d < 32) f = compose(f, o);
+        const Aff o = shfl_down_aff(inc, d);
+        if (lane + d < 32) inc = compose(inc, o);
       }
-      const double A = f.a * cA + f.b * cV + f.p;
-      const double Vn = f.k * cV + f.q;
-      if (inr) {
-        adv[t] = float(A);
-        ret[t] = float(A + v);
+      if (lane == 0) wtot[warp] = inc;
+      __syncthreads();
+      Aff right{1.0, 0.0, 1.0, 0.0, 0.0};  // composite of later warps
+      for (int w = kGaeThreads / 32 - 1; w > warp; --w) right = compose(wtot[w], right);
+      Aff ex = shfl_down_aff(inc, 1);      // lanes to my right in this warp
+      if (lane == 31) ex = Aff{1.0, 0.0, 1.0, 0.0, 0.0};
+      ex = compose(ex, right);
+      double A = ex.a * cA + ex.b * cV + ex.p;
+      double Vn = ex.k * cV + ex.q;
+      for (int t = t1 - 1; t >= t0; --t) {
+        const int k = gae_slot(t);
+        const double v = sv[k];
+        if (sm[k]) {
+          A = (double(sr[k]) - v) + gamma * Vn + gl * A;
+          Vn = v;
+        }
+        sv[k] = float(A);      // advantage
+        sr[k] = float(A + v);  // return
       }
-      cA = __shfl_sync(0xffffffffu, A, 0);
-      cV = __shfl_sync(0xffffffffu, Vn, 0);
+      if (tid == 0) {
+        carry[0] = A;
+        carry[1] = Vn;
+      }
+      __syncthreads();
+      for (int i = tid; i < n; i += kGaeThreads) {
+        const int k = gae_slot(i);
+        adv[lo + i] = sv[k];
+        ret[lo + i] = sr[k];
+      }
+      cA = carry[0];
+      cV = carry[1];
+      __syncthreads();
     }
   }
 }
@@ -246,9 +301,8 @@ int gae_launch(const float* values, const float* rewards, const uint8_t* mask, c
   YATT_REQUIRE(nseq >= 0, YATT_ERR_CONFIG, "gae: n_seqs must be >= 0");
   YATT_REQUIRE(gamma >= 0.f && lam >= 0.f, YATT_ERR_CONFIG, "gae: gamma/lam must be >= 0");
   if (nseq == 0) return YATT_OK;
-  constexpr int kWarps = 8;
-  const int grid = int(min64(ceil_div(nseq, kWarps), int64_t(num_sms()) * 8));
-  gae_kernel<<<grid, kWarps * 32, 0, st>>>(values, rewards, mask, cu, nseq, double(gamma),
+  const int grid = int(min64(nseq, int64_t(num_sms()) * 8));
+  gae_kernel<<<grid, kGaeThreads, 0, st>>>(values, rewards, mask, cu, nseq, double(gamma),
                                            double(lam), adv, ret);
   return check_launch("gae_kernel");
 }

@@ -7,12 +7,13 @@
 //   shard_round_output    proj/src/simcore.cpp:157-214 (+ build_microbatches
 //                         :17-39)
 //
-// One CTA per controller shard (all ranks of an in-process step in ONE launch,
-// the loop of run_rlhf_step, simcore.cpp:482-484).  Each CTA walks its shard
-// in 1024-sample tiles: keyed draw + rejection per pending sample, a block
-// scan gives each pending sample its position in the ordered pending list
-// (the reference's compaction order), microbatch aggregates accumulate with
-// shared-memory integer atomics (exact and order-independent).
+// All controller shards of an in-process step are processed by one set of
+// launches (the loop of run_rlhf_step, simcore.cpp:482-484), one CTA per
+// 256-sample tile of any shard: keyed draw + rejection per pending sample, a
+// ballot scan plus the pending count of the earlier tiles gives each pending
+// sample its position in the ordered pending list (the reference's
+// compaction order), microbatch aggregates and report counters accumulate
+// with integer atomics (exact and order-independent).
 //
 // Exactness: Constant/Uniform draws are pure IEEE multiply + nearbyint and
 // match glibc bit for bit.  Normal/LogNormal use device libm (log1p, cos, sqrt,
@@ -28,7 +29,7 @@
 namespace yattb {
 namespace {
 
-constexpr int kRoundThreads = 1024;
+
 constexpr double kTwoPi = 6.283185307179586476925286766559;
 
 __device__ __forceinline__ int clamp_length(double value, int max_len) {
@@ -85,106 +86,132 @@ __global__ void rejection_kernel(const yatt_sample* s, int64_t n, uint64_t step,
 }
 
 constexpr int kMaxShardsPerLaunch = 64;
+
+// Three stream-ordered launches per round (all shards at once):
+//   init     : zero every shard's report and microbatch slots
+//   tile     : one CTA per 256-sample tile of any shard (the whole GPU works
+//              on a 16K-sample round); the tile's first pending index is the
+//              count of pending samples earlier in its shard (input state,
+//              independent of this round's draws), the in-tile order comes
+//              from a ballot/warp scan; results accumulate with integer
+//              atomics (exact, order-free)
+//   finalize : num_microbatches = ceil(active / microbatch_size)
+constexpr int kTileSamples = 256;
+// Transient `accepted` value of samples accepted by the running launch: other
+// CTAs still count them as pending-at-round-start (race-free tile bases).
+constexpr int32_t kAcceptedThisRound = 0x7f000001;
+__device__ __forceinline__ int pending_at_start(int32_t a) {
+  return (a == 0 || a == kAcceptedThisRound) ? 1 : 0;
+}
 struct ShardTable {
   int64_t off[kMaxShardsPerLaunch + 1];
   int64_t mb_off[kMaxShardsPerLaunch];
+  int64_t tile_off[kMaxShardsPerLaunch + 1];
+  int32_t nshards;
 };
 
-__global__ void __launch_bounds__(kRoundThreads) shard_round_kernel(
-    yatt_sample* samples, const ShardTable tab, int32_t first_rank, uint64_t step, int32_t round,
-    const yatt_round_params prm, yatt_round_report* reports, yatt_mb_agg* mbs_all) {
+__global__ void shard_round_init_kernel(const ShardTable tab, int32_t first_rank, int32_t round,
+                                        int32_t mb, yatt_round_report* reports,
+                                        yatt_mb_agg* mbs_all) {
   const int shard = blockIdx.x;
   const int rank = first_rank + shard;
+  const int64_t n = tab.off[shard + 1] - tab.off[shard];
+  yatt_mb_agg* mbs = mbs_all + tab.mb_off[shard];
+  for (int64_t k = threadIdx.x; k < (n + mb - 1) / mb; k += blockDim.x)
+    mbs[k] = yatt_mb_agg{rank, int32_t(k), 0, 0, 0};
+  if (threadIdx.x == 0) reports[shard] = yatt_round_report{rank, round, 0, 0, 0, 0, 0, 0, 0};
+}
+
+__global__ void __launch_bounds__(kTileSamples) shard_round_tile_kernel(
+    yatt_sample* samples, const ShardTable tab, uint64_t step, int32_t round,
+    const yatt_round_params prm, yatt_round_report* reports, yatt_mb_agg* mbs_all) {
+  int shard = 0;
+  while (shard + 1 < tab.nshards && tab.tile_off[shard + 1] <= blockIdx.x) ++shard;
   const int64_t b = tab.off[shard], e = tab.off[shard + 1];
-  const int64_t n = e - b;
+  const int64_t t0 = b + (int64_t(blockIdx.x) - tab.tile_off[shard]) * kTileSamples;
   const int32_t mb = prm.microbatch_size;
   yatt_mb_agg* mbs = mbs_all + tab.mb_off[shard];
-  const int64_t mb_cap = (n + mb - 1) / mb;
+  yatt_round_report* rep = reports + shard;
   const bool final_round = round >= prm.max_rounds;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __shared__ int s_wsum[kTileSamples / 32];
+  __shared__ int s_before;
 
-  __shared__ unsigned long long s_score, s_units;
-  __shared__ int s_active, s_acc, s_forced, s_pend;
-  __shared__ int s_wsum[kRoundThreads / 32];
-  __shared__ int s_base;
-
-  for (int64_t k = threadIdx.x; k < mb_cap; k += blockDim.x)
-    mbs[k] = yatt_mb_agg{rank, int32_t(k), 0, 0, 0};
+  // pending samples of this shard before the tile
+  int cnt = 0;
+  for (int64_t i = b + threadIdx.x; i < t0; i += kTileSamples) cnt += pending_at_start(samples[i].accepted);
+  cnt = warp_sum(cnt);
+  if (lane == 0) s_wsum[w] = cnt;
+  __syncthreads();
   if (threadIdx.x == 0) {
-    s_score = s_units = 0;
-    s_active = s_acc = s_forced = s_pend = 0;
-    s_base = 0;
+    int s = 0;
+    for (int k = 0; k < kTileSamples / 32; ++k) s += s_wsum[k];
+    s_before = s;
   }
   __syncthreads();
 
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int64_t t0 = 0; t0 < n; t0 += kRoundThreads) {
-    const int64_t i = t0 + threadIdx.x;
-    yatt_sample x{};
-    bool pending = false;
-    if (i < n) {
-      x = samples[b + i];
-      pending = !x.accepted;
-    }
-    // position among this round's pending samples (ordered compaction)
-    const unsigned bal = __ballot_sync(0xffffffffu, pending);
-    if (lane == 0) s_wsum[w] = __popc(bal);
-    __syncthreads();
-    if (w == 0) {
-      int v = s_wsum[lane];
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int o = __shfl_up_sync(0xffffffffu, v, d);
-        if (lane >= d) v += o;
-      }
-      s_wsum[lane] = v;  // inclusive
-    }
-    __syncthreads();
-    const int tile_base = s_base;
-    const int before = (w > 0 ? s_wsum[w - 1] : 0) + __popc(bal & ((1u << lane) - 1u));
-    const int tile_total = s_wsum[31];
-    if (pending) {
-      const int pidx = tile_base + before;
-      x.out_len_tokens = length_keyed(prm.out_dist, prm.seed, kOutputLenStream, step,
-                                      uint64_t(round), x.sample_id);
-      yatt_mb_agg* m = mbs + pidx / mb;
-      atomicAdd(&m->sample_count, 1);
-      atomicMax(&m->max_out_len_tokens, x.out_len_tokens);
-      atomicAdd(reinterpret_cast<unsigned long long*>(&m->score_tokens),
-                (unsigned long long)(int64_t(x.prompt_len_tokens) + x.out_len_tokens));
-      const bool rej = rejected_keyed(prm.rejection, prm.seed, step, uint64_t(round), x.sample_id);
-      if (rej && !final_round) {
-        atomicAdd(&s_pend, 1);
-      } else {
-        if (rej) atomicAdd(&s_forced, 1);
-        x.accepted = 1;
-        x.accepted_round = round;
-        atomicAdd(&s_acc, 1);
-        const long long tok = (long long)x.prompt_len_tokens + x.out_len_tokens;
-        atomicAdd(&s_score, (unsigned long long)tok);
-        atomicAdd(&s_units, (unsigned long long)(tok * tok));
-      }
-      samples[b + i] = x;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      s_base = tile_base + tile_total;
-      s_active += tile_total;
-    }
-    __syncthreads();
+  const int64_t i = t0 + threadIdx.x;
+  yatt_sample x{};
+  bool pending = false;
+  if (i < e) {
+    x = samples[i];
+    pending = x.accepted == 0;
   }
-  if (threadIdx.x == 0) {
-    yatt_round_report r;
-    r.controller_rank = rank;
-    r.round = round;
-    r.active_count = s_active;
-    r.newly_accepted_count = s_acc;
-    r.forced_accept_count = s_forced;
-    r.pending_count = s_pend;
-    r.accepted_score_tokens = (long long)s_score;
-    r.accepted_train_units = (long long)s_units;
-    r.num_microbatches = (s_active + mb - 1) / mb;
-    reports[shard] = r;
+  const unsigned bal = __ballot_sync(0xffffffffu, pending);
+  if (lane == 0) s_wsum[w] = __popc(bal);
+  __syncthreads();
+  int before = s_before + __popc(bal & ((1u << lane) - 1u));
+  for (int k = 0; k < w; ++k) before += s_wsum[k];
+  int tile_pending = 0, acc = 0, forced = 0, pend = 0;
+  unsigned long long score = 0, units = 0;
+  if (pending) {
+    tile_pending = 1;
+    x.out_len_tokens = length_keyed(prm.out_dist, prm.seed, kOutputLenStream, step,
+                                    uint64_t(round), x.sample_id);
+    yatt_mb_agg* m = mbs + before / mb;
+    atomicAdd(&m->sample_count, 1);
+    atomicMax(&m->max_out_len_tokens, x.out_len_tokens);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&m->score_tokens),
+              (unsigned long long)(int64_t(x.prompt_len_tokens) + x.out_len_tokens));
+    const bool rej = rejected_keyed(prm.rejection, prm.seed, step, uint64_t(round), x.sample_id);
+    if (rej && !final_round) {
+      pend = 1;
+    } else {
+      forced = rej ? 1 : 0;
+      x.accepted = kAcceptedThisRound;  // -> 1 in finalize
+      x.accepted_round = round;
+      acc = 1;
+      const long long tok = (long long)x.prompt_len_tokens + x.out_len_tokens;
+      score = (unsigned long long)tok;
+      units = (unsigned long long)(tok * tok);
+    }
+    samples[i] = x;
   }
+  // warp-aggregate, then one atomic per warp per field
+  tile_pending = warp_sum(tile_pending);
+  acc = warp_sum(acc);
+  forced = warp_sum(forced);
+  pend = warp_sum(pend);
+  score = warp_sum(score);
+  units = warp_sum(units);
+  if (lane == 0 && tile_pending) {
+    atomicAdd(&rep->active_count, tile_pending);
+    atomicAdd(&rep->newly_accepted_count, acc);
+    atomicAdd(&rep->forced_accept_count, forced);
+    atomicAdd(&rep->pending_count, pend);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&rep->accepted_score_tokens), score);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&rep->accepted_train_units), units);
+  }
+}
+
+__global__ void shard_round_finalize_kernel(int32_t nshards, int32_t mb, yatt_sample* samples,
+                                            int64_t lo, int64_t hi,
+                                            yatt_round_report* reports) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < nshards) reports[s].num_microbatches = (reports[s].active_count + mb - 1) / mb;
+  for (int64_t i = lo + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < hi;
+       i += int64_t(gridDim.x) * blockDim.x)
+    if (samples[i].accepted == kAcceptedThisRound) samples[i].accepted = 1;
 }
 
 }  // namespace
@@ -259,21 +286,37 @@ int shard_round_launch(yatt_sample* samples, const int64_t* h_off, int32_t nshar
   for (int32_t s0 = 0; s0 < nshards; s0 += kMaxShardsPerLaunch) {
     const int32_t cnt = min(kMaxShardsPerLaunch, nshards - s0);
     ShardTable tab;
+    tab.nshards = cnt;
     int64_t mb_acc = 0;
+    tab.tile_off[0] = 0;
     for (int32_t k = 0; k <= cnt; ++k) tab.off[k] = h_off[s0 + k];
     for (int32_t k = 0; k < cnt; ++k) {
       YATT_REQUIRE(tab.off[k + 1] >= tab.off[k], YATT_ERR_CONFIG, "shard offsets must ascend");
+      YATT_REQUIRE(tab.off[k + 1] - tab.off[k] < (int64_t(1) << 31), YATT_ERR_CONFIG,
+                   "shard_round: shard too large");
       tab.mb_off[k] = mb_acc;
       mb_acc += ceil_div(tab.off[k + 1] - tab.off[k], prm->microbatch_size);
+      tab.tile_off[k + 1] = tab.tile_off[k] + ceil_div(tab.off[k + 1] - tab.off[k], kTileSamples);
     }
     // microbatch slots of earlier launches
     int64_t mb_before = 0;
     for (int32_t k = 0; k < s0; ++k)
       mb_before += ceil_div(h_off[k + 1] - h_off[k], prm->microbatch_size);
-    shard_round_kernel<<<cnt, kRoundThreads, 0, st>>>(
-        samples, tab, first_rank + s0, uint64_t(int64_t(step)), round, *prm, reports + s0,
-        mbs + mb_before);
-    int rc = check_launch("shard_round_kernel");
+    if (cnt == 0) continue;
+    shard_round_init_kernel<<<cnt, 256, 0, st>>>(tab, first_rank + s0, round,
+                                                 prm->microbatch_size, reports + s0,
+                                                 mbs + mb_before);
+    int rc = check_launch("shard_round_init_kernel");
+    if (rc) return rc;
+    if (tab.tile_off[cnt] > 0) {
+      shard_round_tile_kernel<<<unsigned(tab.tile_off[cnt]), kTileSamples, 0, st>>>(
+          samples, tab, uint64_t(int64_t(step)), round, *prm, reports + s0, mbs + mb_before);
+      rc = check_launch("shard_round_tile_kernel");
+      if (rc) return rc;
+    }
+    shard_round_finalize_kernel<<<unsigned(max64(1, min64(ceil_div(tab.off[cnt] - tab.off[0], 256), 4 * num_sms()))), 256, 0, st>>>(
+        cnt, prm->microbatch_size, samples, tab.off[0], tab.off[cnt], reports + s0);
+    rc = check_launch("shard_round_finalize_kernel");
     if (rc) return rc;
   }
   return YATT_OK;

@@ -50,6 +50,13 @@ constexpr double kLn2 = 0.69314718055994530942;
 constexpr float kLn2f = 0.69314718f;
 constexpr float kSlack = 24.0f;  // allow 2^a up to 2^24 before re-basing
 constexpr int kMinitial = -(1 << 24);
+// Words (bf16 pairs) of each 8-element vector whose 2^a goes through the FMA
+// pipe (polynomial) instead of MUFU.EX2, per tensor: balances the MUFU pipe
+// (16 ex2/clk/SM) against the issue port.  0 = all MUFU.
+#ifndef YATT_A1_POLY_WORDS
+#define YATT_A1_POLY_WORDS 0
+#endif
+constexpr int kPolyWords = YATT_A1_POLY_WORDS;
 static_assert(kVecPerTile % kConsumers == 0, "tile must split evenly");
 
 struct RowPartial {
@@ -85,6 +92,27 @@ struct Params {
 // (FFMA2/FADD2: two IEEE fp32 RN operations per instruction), halving the
 // FMA-pipe issue count; each lane keeps the exact per-element arithmetic.
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+// 2^a on the FMA pipe for a pair: Cody-Waite split a = n + r (|r| <= 1/2)
+// with the 1.5*2^23 rounding trick, degree-5 near-minimax polynomial for
+// 2^r (max rel err 2.3e-7 in fp32, same class as ex2.approx), exponent
+// inserted with one integer multiply-add.  a is clamped to >= -125 so the
+// exponent insertion cannot wrap (2^-125 ~ 0 for masked-vocab logits).
+__device__ __forceinline__ float2 ex2_poly2(float2& a) {
+  a = f2(fmaxf(a.x, -125.f), fmaxf(a.y, -125.f));
+  const float2 magic = f2(12582912.f, 12582912.f);
+  const float2 j = __fadd2_rn(a, magic);
+  const float2 n = __fadd2_rn(j, f2(-12582912.f, -12582912.f));
+  const float2 r = __ffma2_rn(n, f2(-1.f, -1.f), a);
+  float2 p = __ffma2_rn(f2(0.001327647129073739f, 0.001327647129073739f), r,
+                        f2(0.009675541892647743f, 0.009675541892647743f));
+  p = __ffma2_rn(p, r, f2(0.05550713092088699f, 0.05550713092088699f));
+  p = __ffma2_rn(p, r, f2(0.24022120237350464f, 0.24022120237350464f));
+  p = __ffma2_rn(p, r, f2(0.6931469440460205f, 0.6931469440460205f));
+  p = __ffma2_rn(p, r, f2(1.0000001192092896f, 1.0000001192092896f));
+  return f2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(j.x) << 23)),
+            __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(j.y) << 23)));
+}
+
 __device__ __forceinline__ float2 ex2x2(float2 a) {
   return make_float2(ex2_approx(a.x), ex2_approx(a.y));
 }
@@ -144,11 +172,13 @@ struct Acc {
       const float2 x = f2(bf16_lo(pw[k]), bf16_hi(pw[k]));
       const float2 z = f2(bf16_lo(qw[k]), bf16_hi(qw[k]));
       const float2 a = __ffma2_rn(x, L2, nmp);
-      const float2 e = ex2x2(a);
+      float2 a_used = a;
+      const float2 e = k < kPolyWords ? ex2_poly2(a_used) : ex2x2(a);
       s[k] = __fadd2_rn(s[k], e);
-      w[k] = __ffma2_rn(e, a, w[k]);
+      w[k] = __ffma2_rn(e, a_used, w[k]);
       const float2 b = __ffma2_rn(z, L2, nmq);
-      sq[k] = __fadd2_rn(sq[k], ex2x2(b));
+      float2 b_used = b;
+      sq[k] = __fadd2_rn(sq[k], k < kPolyWords ? ex2_poly2(b_used) : ex2x2(b));
       if (kFull) u[k] = __ffma2_rn(e, __ffma2_rn(z, f2(-1.f, -1.f), x), u[k]);
     }
   }
