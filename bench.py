@@ -298,6 +298,8 @@ def run_b200(args):
     alg_bytes = CHUNK_ROWS * bytes_per_row(VOCAB)
     achieved = alg_bytes / (a1_avg_ms / 1e3) / 1e9
     traffic, rows_per = ncu_traffic()
+    if traffic is not None and rows_per:  # ncu capture size -> this launch size
+        traffic = traffic * CHUNK_ROWS / rows_per
     roofline = {"bound": "hbm", "kernel": "token_stats_kernel", "achieved": achieved,
                 "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
                 "frac_of_8TBs": achieved / 8000.0, "traffic": traffic,
