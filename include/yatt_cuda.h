@@ -281,6 +281,33 @@ double yatt_loss_finalize(const yatt_loss_sums* h_sums,
                           const yatt_loss_config* config);
 
 /* ------------------------------------------------------------------------ */
+/* Backward into the policy logits                        */
+/* Per token t: dL/dx_v = g (1[v=y] - p_v) + h p_v (log p_v + H)              */
+/*                        + f p_v (log p_v - log q_v - KL)                   */
+/* for the loss of yatt_policy_loss with the same config and kl_mode.        */
+/* Step 1: per-token coefficients (8 floats/token: g, h, f, lse_p, lse_q, H,  */
+/* KL, scratch); `norm` = the GLOBAL normaliser after the all-reduce:        */
+/* token_count (token-mean) or seq_count (seq-mean modes).  FULL KL needs     */
+/* the reference logits + ref_logp; other modes may pass NULL for them.      */
+/* Step 2: stream the policy logits (+ reference for FULL) and write the     */
+/* gradient as bf16 [rows, vocab]; masked rows get zeros.                    */
+/* ------------------------------------------------------------------------ */
+int yatt_policy_grad_coef(const uint16_t* d_policy_logits,
+                          const uint16_t* d_ref_logits, const int32_t* d_targets,
+                          const float* d_logp, const float* d_ref_logp,
+                          const float* d_old_logp, const float* d_advantages,
+                          const float* d_entropy, const float* d_kl,
+                          const uint8_t* d_mask, int64_t n_tokens, int32_t vocab,
+                          const int64_t* d_cu_seqlens, int64_t n_seqs,
+                          const yatt_loss_config* config, int32_t kl_mode,
+                          double norm, float* d_coef, void* stream);
+int yatt_logits_backward(const uint16_t* d_policy_logits,
+                         const uint16_t* d_ref_logits, const int32_t* d_targets,
+                         const uint8_t* d_mask, int64_t rows, int32_t vocab,
+                         const float* d_coef, int32_t full_kl, uint16_t* d_grad,
+                         void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* A5+A6  dynamic-sampling filter and compaction (bit-exact)                 */
 /* keep_g = !(all rewards of group g are bitwise identical).  Groups are     */
 /* `group_size` consecutive local samples (the local batch is group-aligned, */

@@ -253,3 +253,28 @@ def max_rel_error(actual, expected) -> float:
     if a.size == 0:
         return 0.0
     return float(np.max(np.abs(a - e) / (np.abs(e) + 1e-12)))
+
+
+def logits_backward(pol, ref, tgt, logp, ref_logp, old_logp, adv, mask=None, cu=None,
+                    clip_low=0.2, clip_high=0.2, clip_ratio_c=0.0, kl_coef=0.001,
+                    entropy_coef=0.0, agg_mode=0, kl_mode="k3", norm=1.0):
+    """fp64 dL/dx [rows, V] (+ per-row g, h, f, lse) — see yatt_oracle.c."""
+    L = lib()
+    if not getattr(L, "_bwd_ready", False):
+        L.yo_logits_backward.argtypes = [C.c_void_p] * 4 + [C.c_int64, C.c_int32] + \
+            [C.c_void_p] * 5 + [C.c_int64] + [C.c_float] * 5 + [C.c_int, C.c_int, C.c_double,
+                                                               C.c_void_p, C.c_void_p]
+        L._bwd_ready = True
+    rows, V = pol.shape
+    f = lambda a: None if a is None else np.ascontiguousarray(a, dtype=np.float32)  # noqa: E731
+    grad = np.zeros((rows, V), dtype=np.float64)
+    coef = np.zeros((rows, 4), dtype=np.float64)
+    m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8)
+    c = None if cu is None else np.ascontiguousarray(cu, dtype=np.int64)
+    args = [f(logp), f(ref_logp), f(old_logp), f(adv)]
+    L.yo_logits_backward(_ptr(pol), _ptr(ref), _ptr(np.ascontiguousarray(tgt, dtype=np.int32)),
+                         _ptr(m), rows, V, *[_ptr(a) for a in args], _ptr(c),
+                         0 if c is None else len(c) - 1, clip_low, clip_high, clip_ratio_c,
+                         kl_coef, entropy_coef, agg_mode, KL_MODES[kl_mode], norm, _ptr(grad),
+                         _ptr(coef))
+    return grad, coef

@@ -498,3 +498,87 @@ int64_t yo_filter_compact(const float* r, const int64_t* lens, int64_t n, int G,
   counts[2] = kg;
   return j;
 }
+
+/* ------------------------------------------------------- backward (8f#1) */
+/* dL/dx for the policy loss of yo_policy_loss (same config), fp64, from the
+ * logits with exact two-pass softmaxes.  Per-token inputs (logp, ref_logp,
+ * old_logp, adv) are the fp32 arrays the device also consumes, so clip
+ * decisions match.  norm: global token count (agg 0) or seq count (1, 2). */
+void yo_logits_backward(const uint16_t* pol, const uint16_t* ref, const int32_t* tgt,
+                        const uint8_t* mask, int64_t rows, int32_t V, const float* logp,
+                        const float* ref_logp, const float* old_logp, const float* adv,
+                        const int64_t* cu, int64_t nseq, float clip_low, float clip_high,
+                        float clip_c, float kl_coef, float ent_coef, int agg_mode, int kl_mode,
+                        double norm, double* grad, double* coef_out) {
+  for (int64_t r = 0; r < rows; ++r) {
+    double* gr = grad + r * (int64_t)V;
+    if (mask && !mask[r]) {
+      for (int32_t v = 0; v < V; ++v) gr[v] = 0;
+      continue;
+    }
+    double scale = 1.0 / norm;
+    if (agg_mode == 1) {
+      int64_t s = 0;
+      while (!(cu[s] <= r && r < cu[s + 1])) ++s;
+      double cnt = 0;
+      for (int64_t i = cu[s]; i < cu[s + 1]; ++i) cnt += (!mask || mask[i]);
+      scale /= cnt;
+    }
+    const double lp = logp[r], A = adv[r];
+    const double ratio = exp(lp - (double)old_logp[r]);
+    const double pg1 = -A * ratio;
+    double cl = ratio;
+    if (cl < 1.0 - (double)clip_low) cl = 1.0 - (double)clip_low;
+    if (cl > 1.0 + (double)clip_high) cl = 1.0 + (double)clip_high;
+    const double pg2 = -A * cl;
+    const double pg = pg1 > pg2 ? pg1 : pg2;
+    int active = !(pg2 > pg1);
+    if (clip_c > 1.f && A < 0 && -A * (double)clip_c < pg) active = 0;
+    const double dpg = active ? -A * ratio : 0.0;
+    const double rl = ref_logp ? (double)ref_logp[r] : lp;
+    double dkl = 0;
+    if (kl_mode == 0) dkl = 1.0;
+    else if (kl_mode == 1) dkl = lp - rl;
+    else if (kl_mode == 2) dkl = -expm1(rl - lp);
+    const double g = scale * (dpg + (kl_mode == 3 ? 0.0 : (double)kl_coef * dkl));
+    const double h = scale * (double)ent_coef;
+    const double f = kl_mode == 3 ? scale * (double)kl_coef : 0.0;
+    const uint16_t* x = pol + r * (int64_t)V;
+    const uint16_t* z = ref ? ref + r * (int64_t)V : NULL;
+    double mx = -INFINITY, mz = -INFINITY;
+    for (int32_t v = 0; v < V; ++v) {
+      const double a = bf16_to_f(x[v]);
+      if (a > mx) mx = a;
+      if (z) {
+        const double b = bf16_to_f(z[v]);
+        if (b > mz) mz = b;
+      }
+    }
+    double sx = 0, sz = 0;
+    for (int32_t v = 0; v < V; ++v) {
+      sx += exp(bf16_to_f(x[v]) - mx);
+      if (z) sz += exp(bf16_to_f(z[v]) - mz);
+    }
+    const double lse = mx + log(sx), lseq = z ? mz + log(sz) : 0.0;
+    double H = 0, KL = 0;
+    for (int32_t v = 0; v < V; ++v) {
+      const double lpv = bf16_to_f(x[v]) - lse;
+      const double pv = exp(lpv);
+      if (pv > 0) H -= pv * lpv;
+      if (z && pv > 0) KL += pv * (lpv - (bf16_to_f(z[v]) - lseq));
+    }
+    for (int32_t v = 0; v < V; ++v) {
+      const double lpv = bf16_to_f(x[v]) - lse;
+      const double pv = exp(lpv);
+      double val = g * ((v == tgt[r]) - pv) + h * pv * (lpv + H);
+      if (f != 0) val += f * pv * (lpv - (bf16_to_f(z[v]) - lseq) - KL);
+      gr[v] = val;
+    }
+    if (coef_out) {
+      coef_out[4 * r + 0] = g;
+      coef_out[4 * r + 1] = h;
+      coef_out[4 * r + 2] = f;
+      coef_out[4 * r + 3] = lse;
+    }
+  }
+}

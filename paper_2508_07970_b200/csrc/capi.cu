@@ -63,6 +63,12 @@ int shard_round_launch(yatt_sample*, const int64_t*, int32_t, int32_t, int32_t, 
                        const yatt_round_params*, yatt_round_report*, yatt_mb_agg*, cudaStream_t);
 size_t sort_workspace_bytes(int64_t);
 int sort_order_launch(const int32_t*, int64_t, uint32_t*, void*, size_t, cudaStream_t);
+int grad_coef_launch(const uint16_t*, const uint16_t*, const int32_t*, const float*, const float*,
+                     const float*, const float*, const float*, const float*, const uint8_t*,
+                     int64_t, int32_t, const int64_t*, int64_t, const yatt_loss_config*, int32_t,
+                     double, float*, cudaStream_t);
+int logits_backward_launch(const uint16_t*, const uint16_t*, const int32_t*, const uint8_t*,
+                           int64_t, int32_t, const float*, int32_t, uint16_t*, cudaStream_t);
 
 // ---- errors ---------------------------------------------------------------
 namespace {
@@ -280,6 +286,23 @@ int yatt_policy_loss(const float* logp, const float* old_logp, const float* adv,
 
 double yatt_loss_finalize(const yatt_loss_sums* s, const yatt_loss_config* c) {
   return loss_finalize(s, c);
+}
+
+int yatt_policy_grad_coef(const uint16_t* pol, const uint16_t* ref, const int32_t* tgt,
+                          const float* logp, const float* ref_logp, const float* old_logp,
+                          const float* adv, const float* ent, const float* kl,
+                          const uint8_t* mask, int64_t n, int32_t vocab, const int64_t* cu,
+                          int64_t nseq, const yatt_loss_config* cfg, int32_t kl_mode,
+                          double norm, float* coef, void* stream) {
+  return grad_coef_launch(pol, ref, tgt, logp, ref_logp, old_logp, adv, ent, kl, mask, n, vocab,
+                          cu, nseq, cfg, kl_mode, norm, coef, as_stream(stream));
+}
+
+int yatt_logits_backward(const uint16_t* pol, const uint16_t* ref, const int32_t* tgt,
+                         const uint8_t* mask, int64_t rows, int32_t vocab, const float* coef,
+                         int32_t full_kl, uint16_t* grad, void* stream) {
+  return logits_backward_launch(pol, ref, tgt, mask, rows, vocab, coef, full_kl, grad,
+                                as_stream(stream));
 }
 
 size_t yatt_filter_compact_workspace_bytes(int64_t n) { return compact_workspace_bytes(n); }

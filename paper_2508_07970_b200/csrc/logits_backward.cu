@@ -1,0 +1,339 @@
+// logits_backward.cu — §8f next #1: the loss gradient w.r.t. the policy
+// logits, the Stage-4 consumer of A1 (token_stats) and A4 (policy_loss).
+// Replaces the Training-stage cost stand-in (proj/src/simcore.cpp:404-406,
+// PAPER.md:66) for the first backward step of the actor.
+//
+// With p = softmax(x_t), H = entropy, y the target and per-token scalars
+//   g = s_t * (dpg/dlogp + beta * dkl/dlogp)    (k1/k2/k3 KL)
+//   h = s_t * entropy_coef                      (loss has -entropy_coef * H)
+//   f = s_t * beta                              (FULL KL only)
+//   s_t = mask_t / norm  (norm = global token count, or per-seq for seq-mean)
+// the gradient row is
+//   dL/dx_v = g (1[v=y] - p_v) + h p_v (log p_v + H) + f p_v (log p_v - log q_v - KL)
+// dpg/dlogp = -A * ratio on the unclipped branch, 0 when the clipped (or dual
+// clipped) branch is active; dkl/dlogp = 1 (k1), logp - ref_logp (k2),
+// 1 - exp(ref_logp - logp) (k3).
+//
+// Kernel 1 (grad_coef): per token, fp64, gathers the target logits to rebuild
+//   lse_p = x_y - logp and lse_q = z_y - ref_logp; writes 8 floats per token.
+// Kernel 2 (logits_backward): persistent, the A1 streaming design — a producer
+//   warp feeds a 3-stage shared-memory ring with cp.async.bulk (policy tile, +
+//   reference tile for FULL), 8 consumer warps compute the row with packed
+//   f32x2 math and MUFU ex2, convert to bf16x2 and store 16 B per thread.
+// Bytes per valid row: 2V read + 2V written (+2V read for FULL) + 32 B coef.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "common.cuh"
+
+namespace yattb {
+namespace {
+
+constexpr int kConsumerWarps = 8;
+constexpr int kConsumers = kConsumerWarps * 32;
+constexpr int kThreads = kConsumers + 32;
+constexpr int kTile = 8192;
+constexpr int kStages = 3;
+constexpr int kVecPerTile = kTile / 8;
+constexpr int kVecPerThread = kVecPerTile / kConsumers;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2f = 0.69314718055994530942f;
+constexpr int kCoef = 8;  // g, h, f, lse_p, lse_q, H, KL, pad
+
+struct GradParams {
+  const uint16_t* pol;
+  const uint16_t* ref;
+  const int32_t* tgt;
+  const uint8_t* mask;
+  const float* coef;
+  int64_t rows;
+  int32_t V;
+  uint16_t* grad;
+};
+
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+__device__ __forceinline__ void stg_cs_128(void* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+struct RowCoef {
+  float g, h, f, lsep2, lseq2, H, KL;  // lse in log2 units (lse * log2e)
+};
+
+// grad for 8 elements (one 16-byte vector) of policy P (and ref Q if kFull).
+template <bool kFull>
+__device__ __forceinline__ uint4 grad_vec(const uint4& P, const uint4& Q, const RowCoef& c) {
+  const uint32_t pw[4] = {P.x, P.y, P.z, P.w};
+  const uint32_t qw[4] = {Q.x, Q.y, Q.z, Q.w};
+  uint32_t out[4];
+  const float2 L2 = f2(kLog2e, kLog2e), nl = f2(-c.lsep2, -c.lsep2);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 x = f2(bf16_lo(pw[k]), bf16_hi(pw[k]));
+    const float2 a = __ffma2_rn(x, L2, nl);            // log2 p
+    const float2 p = f2(ex2_approx(a.x), ex2_approx(a.y));
+    const float2 lnp = __fmul2_rn(a, f2(kLn2f, kLn2f));  // log p
+    // g * (-p) + h * p * (log p + H)
+    float2 t = __ffma2_rn(f2(c.h, c.h), __fadd2_rn(lnp, f2(c.H, c.H)), f2(-c.g, -c.g));
+    if (kFull) {
+      const float2 z = f2(bf16_lo(qw[k]), bf16_hi(qw[k]));
+      const float2 lnq = __fmul2_rn(__ffma2_rn(z, L2, f2(-c.lseq2, -c.lseq2)), f2(kLn2f, kLn2f));
+      const float2 d = __fadd2_rn(__fadd2_rn(lnp, f2(-lnq.x, -lnq.y)), f2(-c.KL, -c.KL));
+      t = __ffma2_rn(f2(c.f, c.f), d, t);
+    }
+    const float2 gr = __fmul2_rn(p, t);
+    out[k] = pack_bf16x2(gr.x, gr.y);
+  }
+  return make_uint4(out[0], out[1], out[2], out[3]);
+}
+
+struct __align__(16) BwdTail {
+  uint64_t full[kStages];
+  uint64_t empty[kStages];
+};
+
+template <bool kFull>
+__global__ void __launch_bounds__(kThreads, 2) logits_backward_kernel(const GradParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int kPerStage = kFull ? 2 : 1;
+  uint16_t* ring = reinterpret_cast<uint16_t*>(smem);
+  BwdTail* tail = reinterpret_cast<BwdTail*>(smem + size_t(kStages) * kPerStage * kTile * 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t V = p.V;
+  const int ntiles = int((V + kTile - 1) / kTile);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&tail->full[s], 1);
+      mbar_init(&tail->empty[s], kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    if (lane == 0) {
+      const uint64_t pol = l2_evict_first_policy();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
+        if (p.mask != nullptr && p.mask[row] == 0) continue;
+        for (int t = 0; t < ntiles; ++t) {
+          const int64_t e0 = int64_t(t) * kTile;
+          const uint32_t n = uint32_t(min64(kTile, V - e0));
+          mbar_wait(&tail->empty[stage], phase ^ 1u);
+          mbar_arrive_expect_tx(&tail->full[stage], 2u * n * kPerStage);
+          uint16_t* dst = ring + size_t(stage) * kPerStage * kTile;
+          bulk_g2s(dst, p.pol + row * V + e0, 2u * n, &tail->full[stage], pol);
+          if (kFull) bulk_g2s(dst + kTile, p.ref + row * V + e0, 2u * n, &tail->full[stage], pol);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  const int tid = threadIdx.x;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
+    uint16_t* grow = p.grad + row * V;
+    if (p.mask != nullptr && p.mask[row] == 0) {
+      for (int64_t v = tid; v < V / 8; v += kConsumers)
+        stg_cs_128(grow + v * 8, make_uint4(0, 0, 0, 0));
+      continue;
+    }
+    const float* cf = p.coef + row * kCoef;
+    RowCoef c{cf[0], cf[1], cf[2], cf[3] * kLog2e, cf[4] * kLog2e, cf[5], cf[6]};
+    const int32_t y = __ldg(p.tgt + row);
+    for (int t = 0; t < ntiles; ++t) {
+      const int64_t e0 = int64_t(t) * kTile;
+      const int nvec = int(min64(kTile, V - e0) >> 3);
+      const uint16_t* sp = ring + size_t(stage) * kPerStage * kTile;
+      const uint16_t* sq = sp + kTile;
+      mbar_wait(&tail->full[stage], phase);
+      for (int v = tid; v < nvec; v += kConsumers) {
+        const uint4 P = lds128(sp + v * 8);
+        const uint4 Q = kFull ? lds128(sq + v * 8) : P;
+        uint4 G = grad_vec<kFull>(P, Q, c);
+        const int64_t gv = e0 / 8 + v;
+        if (gv == (y >> 3)) {  // the target element gets + g
+          const int j = y & 7;
+          uint32_t* gw = reinterpret_cast<uint32_t*>(&G);
+          const float2 pr = f2(bf16_lo(gw[j >> 1]), bf16_hi(gw[j >> 1]));
+          // recompute the target element in fp32 to avoid double rounding
+          const float x = (j & 1) ? bf16_hi(reinterpret_cast<const uint32_t*>(&P)[j >> 1])
+                                  : bf16_lo(reinterpret_cast<const uint32_t*>(&P)[j >> 1]);
+          const float a = fmaf(x, kLog2e, -c.lsep2);
+          const float pp = ex2_approx(a);
+          float val = pp * fmaf(c.h, a * kLn2f + c.H, -c.g) + c.g;
+          if (kFull) {
+            const float z = (j & 1) ? bf16_hi(reinterpret_cast<const uint32_t*>(&Q)[j >> 1])
+                                    : bf16_lo(reinterpret_cast<const uint32_t*>(&Q)[j >> 1]);
+            const float lnq = fmaf(z, kLog2e, -c.lseq2) * kLn2f;
+            val = fmaf(c.f * pp, a * kLn2f - lnq - c.KL, val);
+          }
+          gw[j >> 1] = (j & 1) ? pack_bf16x2(pr.x, val) : pack_bf16x2(val, pr.y);
+        }
+        stg_cs_128(grow + e0 + v * 8, G);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tail->empty[stage]);
+      if (++stage == kStages) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ float bf16_at(const uint16_t* base, int64_t idx) {
+  return __uint_as_float(uint32_t(base[idx]) << 16);
+}
+
+__global__ void grad_coef_kernel(const uint16_t* pol, const uint16_t* ref, const int32_t* tgt,
+                                 const float* logp, const float* ref_logp, const float* old_logp,
+                                 const float* adv, const float* ent, const float* kl,
+                                 const uint8_t* mask, int64_t n, int32_t V, const int64_t* cu,
+                                 int64_t nseq, const yatt_loss_config c, int32_t kl_mode,
+                                 double norm, float* coef) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  float* o = coef + t * kCoef;
+  const bool valid = mask == nullptr || mask[t];
+  double scale = valid ? 1.0 / norm : 0.0;
+  if (valid && c.agg_mode == 1) {  // seq-mean-token-mean: also / valid tokens of the sequence
+    int64_t lo = 0, hi = nseq;     // find s with cu[s] <= t < cu[s+1]
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (cu[mid] <= t) lo = mid;
+      else hi = mid;
+    }
+    scale /= double(coef[cu[lo] * kCoef + 7]);  // count left by seq_count_kernel
+  }
+  const double lp = logp[t], old = old_logp[t], A = adv[t];
+  const double ratio = exp(lp - old);
+  const double pg1 = -A * ratio;
+  const double pg2 = -A * fmin(fmax(ratio, 1.0 - double(c.clip_low)), 1.0 + double(c.clip_high));
+  double pg = fmax(pg1, pg2);
+  bool active = !(pg2 > pg1);
+  if (c.clip_ratio_c > 1.f && A < 0.0 && -A * double(c.clip_ratio_c) < pg) active = false;
+  const double dpg = active ? -A * ratio : 0.0;
+  const double rl = ref_logp ? double(ref_logp[t]) : lp;
+  double dkl = 0.0;
+  if (kl_mode == YATT_KL_K1) dkl = 1.0;
+  else if (kl_mode == YATT_KL_K2) dkl = lp - rl;
+  else if (kl_mode == YATT_KL_K3) dkl = -expm1(rl - lp);
+  const double beta = double(c.kl_coef);
+  const int32_t y = tgt[t];
+  const double xy = bf16_at(pol, t * int64_t(V) + y);
+  o[0] = float(scale * (dpg + (kl_mode == YATT_KL_FULL ? 0.0 : beta * dkl)));
+  o[1] = float(scale * double(c.entropy_coef));
+  o[2] = float(kl_mode == YATT_KL_FULL ? scale * beta : 0.0);
+  o[3] = float(xy - lp);  // lse_p
+  o[4] = (kl_mode == YATT_KL_FULL && ref) ? float(double(bf16_at(ref, t * int64_t(V) + y)) - rl)
+                                          : 0.f;
+  o[5] = ent ? ent[t] : 0.f;
+  o[6] = kl ? kl[t] : 0.f;
+  // o[7] is scratch: the valid-token count of the sequence at its first token
+}
+
+// Valid tokens per sequence -> coef[cu[s]*8 + 7] (seq-mean-token-mean only).
+__global__ void seq_count_kernel(const uint8_t* mask, const int64_t* cu, int64_t nseq,
+                                 float* coef) {
+  for (int64_t s = blockIdx.x; s < nseq; s += gridDim.x) {
+    const int64_t b = cu[s], e = cu[s + 1];
+    int cnt = 0;
+    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) cnt += (mask == nullptr || mask[i]);
+    cnt = warp_sum(cnt);
+    __shared__ int red[8];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0 && e > b) {
+      int tot = 0;
+      for (int k = 0; k < int(blockDim.x >> 5); ++k) tot += red[k];
+      coef[b * kCoef + 7] = float(tot);
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+int grad_coef_launch(const uint16_t* pol, const uint16_t* ref, const int32_t* tgt,
+                     const float* logp, const float* ref_logp, const float* old_logp,
+                     const float* adv, const float* ent, const float* kl, const uint8_t* mask,
+                     int64_t n, int32_t V, const int64_t* cu, int64_t nseq,
+                     const yatt_loss_config* cfg, int32_t kl_mode, double norm, float* coef,
+                     cudaStream_t st) {
+  YATT_REQUIRE(cfg != nullptr, YATT_ERR_CONFIG, "grad_coef: null config");
+  YATT_REQUIRE(cfg->agg_mode >= 0 && cfg->agg_mode <= 2, YATT_ERR_CONFIG, "unknown agg_mode");
+  YATT_REQUIRE(kl_mode >= 0 && kl_mode <= 3, YATT_ERR_CONFIG, "unknown kl_mode %d", kl_mode);
+  YATT_REQUIRE(norm > 0, YATT_ERR_CONFIG, "grad_coef: norm must be positive");
+  YATT_REQUIRE(cfg->agg_mode != 1 || cu != nullptr, YATT_ERR_CONFIG,
+               "seq-mean-token-mean needs cu_seqlens");
+  YATT_REQUIRE(kl_mode != YATT_KL_FULL || (ref && ref_logp), YATT_ERR_CONFIG,
+               "FULL KL gradient needs the reference logits and ref_logp");
+  if (n <= 0) return YATT_OK;
+  if (cfg->agg_mode == 1 && nseq > 0) {
+    seq_count_kernel<<<unsigned(min64(nseq, int64_t(num_sms()) * 8)), 256, 0, st>>>(mask, cu, nseq,
+                                                                                   coef);
+    const int rc = check_launch("seq_count_kernel");
+    if (rc) return rc;
+  }
+  grad_coef_kernel<<<unsigned(ceil_div(n, 256)), 256, 0, st>>>(
+      pol, ref, tgt, logp, ref_logp, old_logp, adv, ent, kl, mask, n, V, cu, nseq, *cfg, kl_mode,
+      norm, coef);
+  return check_launch("grad_coef_kernel");
+}
+
+int logits_backward_launch(const uint16_t* pol, const uint16_t* ref, const int32_t* tgt,
+                           const uint8_t* mask, int64_t rows, int32_t V, const float* coef,
+                           int32_t full_kl, uint16_t* grad, cudaStream_t st) {
+  YATT_REQUIRE(V > 0 && V % 8 == 0, YATT_ERR_CONFIG, "logits_backward: vocab must be a multiple of 8");
+  YATT_REQUIRE(rows >= 0, YATT_ERR_CONFIG, "logits_backward: rows must be >= 0");
+  if (rows == 0) return YATT_OK;
+  YATT_REQUIRE(pol && tgt && coef && grad && (!full_kl || ref), YATT_ERR_CONFIG,
+               "logits_backward: null pointer");
+  YATT_REQUIRE((reinterpret_cast<uintptr_t>(pol) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(grad) & 15) == 0 &&
+                   (!full_kl || (reinterpret_cast<uintptr_t>(ref) & 15) == 0),
+               YATT_ERR_CONFIG, "logits_backward: tensors must be 16-byte aligned");
+  GradParams prm{pol, ref, tgt, mask, coef, rows, V, grad};
+  const int grid = int(min64(rows, int64_t(2) * num_sms()));
+  if (full_kl) {
+    constexpr size_t smem = size_t(kStages) * 2 * kTile * 2 + sizeof(BwdTail);
+    static bool attr = false;
+    if (!attr) {
+      YATT_TRY_CUDA(cudaFuncSetAttribute(logits_backward_kernel<true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      attr = true;
+    }
+    logits_backward_kernel<true><<<grid, kThreads, smem, st>>>(prm);
+  } else {
+    constexpr size_t smem = size_t(kStages) * kTile * 2 + sizeof(BwdTail);
+    static bool attr = false;
+    if (!attr) {
+      YATT_TRY_CUDA(cudaFuncSetAttribute(logits_backward_kernel<false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      attr = true;
+    }
+    logits_backward_kernel<false><<<grid, kThreads, smem, st>>>(prm);
+  }
+  return check_launch("logits_backward_kernel");
+}
+
+}  // namespace yattb

@@ -251,3 +251,28 @@ def sort_order_desc(lengths: torch.Tensor) -> torch.Tensor:
     ws = torch.empty((wsb,), dtype=torch.uint8, device=lengths.device)
     check(lib().yatt_sort_order_desc(_p(lengths), n, _p(order), _p(ws), wsb, _st()))
     return order
+
+
+# --------------------------------------------------- backward (§8f #1) ----
+def logits_grad(policy_logits, ref_logits, targets, logp, ref_logp, old_logp, advantages,
+                entropy, kl, mask=None, cu_seqlens=None, config=None, kl_mode="k3",
+                norm: float = 1.0, grad=None):
+    """dL/d(policy logits) of the A4 loss (bf16 [rows, V]) + the per-token
+    coefficient table (fp32 [rows, 8]: g, h, f, lse_p, lse_q, H, KL, scratch)."""
+    cfg = config or loss_config()
+    rows, vocab = policy_logits.shape
+    coef = torch.empty((rows, 8), dtype=torch.float32, device=policy_logits.device)
+    m = _mask(mask)
+    nseq = 0 if cu_seqlens is None else cu_seqlens.numel() - 1
+    check(lib().yatt_policy_grad_coef(_p(policy_logits), _p(ref_logits), _p(targets), _p(logp),
+                                      _p(ref_logp), _p(old_logp), _p(advantages), _p(entropy),
+                                      _p(kl), _p(m), rows, vocab, _p(cu_seqlens), nseq,
+                                      C.byref(cfg), KL_MODES[kl_mode], float(norm), _p(coef),
+                                      _st()))
+    if grad is None:
+        grad = torch.empty_like(policy_logits)
+    full = int(KL_MODES[kl_mode] == 3)
+    check(lib().yatt_logits_backward(_p(policy_logits), _p(ref_logits) if full else None,
+                                     _p(targets), _p(m), rows, vocab, _p(coef), full, _p(grad),
+                                     _st()))
+    return grad, coef
