@@ -35,7 +35,13 @@ constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kThreads = kConsumers + 32;
 constexpr int kTile = 8192;
-constexpr int kStages = 3;
+// Ring depth: ~96 KB in flight per CTA either way (policy-only tiles are half
+// the size, so twice the stages).
+constexpr int kMaxStages = 6;
+template <bool kFull>
+constexpr int stages_of() {
+  return kFull ? 3 : 6;
+}
 constexpr int kVecPerTile = kTile / 8;
 constexpr int kVecPerThread = kVecPerTile / kConsumers;
 constexpr float kLog2e = 1.4426950408889634f;
@@ -99,14 +105,15 @@ __device__ __forceinline__ uint4 grad_vec(const uint4& P, const uint4& Q, const 
 }
 
 struct __align__(16) BwdTail {
-  uint64_t full[kStages];
-  uint64_t empty[kStages];
+  uint64_t full[kMaxStages];
+  uint64_t empty[kMaxStages];
 };
 
 template <bool kFull>
 __global__ void __launch_bounds__(kThreads, 2) logits_backward_kernel(const GradParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int kPerStage = kFull ? 2 : 1;
+  constexpr int kStages = stages_of<kFull>();
   uint16_t* ring = reinterpret_cast<uint16_t*>(smem);
   BwdTail* tail = reinterpret_cast<BwdTail*>(smem + size_t(kStages) * kPerStage * kTile * 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -149,46 +156,65 @@ __global__ void __launch_bounds__(kThreads, 2) logits_backward_kernel(const Grad
   const int tid = threadIdx.x;
   int stage = 0;
   uint32_t phase = 0;
+  // per-row scalars, prefetched one row ahead (no load latency at row start)
+  auto load_row = [&](int64_t r, float4& c0, float4& c1, int32_t& y) {
+    if (r < p.rows) {
+      const float4* cf = reinterpret_cast<const float4*>(p.coef + r * kCoef);
+      c0 = __ldg(cf);
+      c1 = __ldg(cf + 1);
+      y = __ldg(p.tgt + r);
+    }
+  };
+  float4 n0 = make_float4(0, 0, 0, 0), n1 = n0;
+  int32_t ny = 0;
+  load_row(blockIdx.x, n0, n1, ny);
   for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
+    const float4 c0 = n0, c1 = n1;
+    const int32_t y = ny;
+    load_row(row + gridDim.x, n0, n1, ny);
     uint16_t* grow = p.grad + row * V;
     if (p.mask != nullptr && p.mask[row] == 0) {
       for (int64_t v = tid; v < V / 8; v += kConsumers)
         stg_cs_128(grow + v * 8, make_uint4(0, 0, 0, 0));
       continue;
     }
-    const float* cf = p.coef + row * kCoef;
-    RowCoef c{cf[0], cf[1], cf[2], cf[3] * kLog2e, cf[4] * kLog2e, cf[5], cf[6]};
-    const int32_t y = __ldg(p.tgt + row);
+    const RowCoef c{c0.x, c0.y, c0.z, c0.w * kLog2e, c1.x * kLog2e, c1.y, c1.z};
     for (int t = 0; t < ntiles; ++t) {
       const int64_t e0 = int64_t(t) * kTile;
       const int nvec = int(min64(kTile, V - e0) >> 3);
       const uint16_t* sp = ring + size_t(stage) * kPerStage * kTile;
       const uint16_t* sq = sp + kTile;
       mbar_wait(&tail->full[stage], phase);
-      for (int v = tid; v < nvec; v += kConsumers) {
-        const uint4 P = lds128(sp + v * 8);
-        const uint4 Q = kFull ? lds128(sq + v * 8) : P;
-        uint4 G = grad_vec<kFull>(P, Q, c);
-        const int64_t gv = e0 / 8 + v;
-        if (gv == (y >> 3)) {  // the target element gets + g
-          const int j = y & 7;
-          uint32_t* gw = reinterpret_cast<uint32_t*>(&G);
-          const float2 pr = f2(bf16_lo(gw[j >> 1]), bf16_hi(gw[j >> 1]));
-          // recompute the target element in fp32 to avoid double rounding
-          const float x = (j & 1) ? bf16_hi(reinterpret_cast<const uint32_t*>(&P)[j >> 1])
-                                  : bf16_lo(reinterpret_cast<const uint32_t*>(&P)[j >> 1]);
-          const float a = fmaf(x, kLog2e, -c.lsep2);
-          const float pp = ex2_approx(a);
-          float val = pp * fmaf(c.h, a * kLn2f + c.H, -c.g) + c.g;
-          if (kFull) {
-            const float z = (j & 1) ? bf16_hi(reinterpret_cast<const uint32_t*>(&Q)[j >> 1])
-                                    : bf16_lo(reinterpret_cast<const uint32_t*>(&Q)[j >> 1]);
-            const float lnq = fmaf(z, kLog2e, -c.lseq2) * kLn2f;
-            val = fmaf(c.f * pp, a * kLn2f - lnq - c.KL, val);
-          }
-          gw[j >> 1] = (j & 1) ? pack_bf16x2(pr.x, val) : pack_bf16x2(val, pr.y);
+      if (nvec == kVecPerTile) {
+        uint4 P[kVecPerThread], Q[kVecPerThread];
+#pragma unroll
+        for (int i = 0; i < kVecPerThread; ++i) {
+          P[i] = lds128(sp + (tid + i * kConsumers) * 8);
+          Q[i] = kFull ? lds128(sq + (tid + i * kConsumers) * 8) : P[i];
         }
-        stg_cs_128(grow + e0 + v * 8, G);
+#pragma unroll
+        for (int i = 0; i < kVecPerThread; ++i)
+          stg_cs_128(grow + e0 + (tid + i * kConsumers) * 8, grad_vec<kFull>(P[i], Q[i], c));
+      } else {
+        for (int v = tid; v < nvec; v += kConsumers) {
+          const uint4 P = lds128(sp + v * 8);
+          const uint4 Q = kFull ? lds128(sq + v * 8) : P;
+          stg_cs_128(grow + e0 + v * 8, grad_vec<kFull>(P, Q, c));
+        }
+      }
+      // the target element gets + g: its owner rewrites those two bytes
+      // (same thread, program order after the vector store)
+      if (y >= e0 && y < e0 + kTile && tid == ((y - e0) >> 3) % kConsumers) {
+        const float x = __uint_as_float(uint32_t(sp[y - e0]) << 16);
+        const float a = fmaf(x, kLog2e, -c.lsep2);
+        const float pp = ex2_approx(a);
+        float val = pp * fmaf(c.h, a * kLn2f + c.H, -c.g) + c.g;
+        if (kFull) {
+          const float z = __uint_as_float(uint32_t(sq[y - e0]) << 16);
+          const float lnq = fmaf(z, kLog2e, -c.lseq2) * kLn2f;
+          val = fmaf(c.f * pp, a * kLn2f - lnq - c.KL, val);
+        }
+        grow[y] = uint16_t(pack_bf16x2(val, 0.f) & 0xffffu);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&tail->empty[stage]);
@@ -315,7 +341,7 @@ int logits_backward_launch(const uint16_t* pol, const uint16_t* ref, const int32
   GradParams prm{pol, ref, tgt, mask, coef, rows, V, grad};
   const int grid = int(min64(rows, int64_t(2) * num_sms()));
   if (full_kl) {
-    constexpr size_t smem = size_t(kStages) * 2 * kTile * 2 + sizeof(BwdTail);
+    constexpr size_t smem = size_t(stages_of<true>()) * 2 * kTile * 2 + sizeof(BwdTail);
     static bool attr = false;
     if (!attr) {
       YATT_TRY_CUDA(cudaFuncSetAttribute(logits_backward_kernel<true>,
@@ -324,7 +350,7 @@ int logits_backward_launch(const uint16_t* pol, const uint16_t* ref, const int32
     }
     logits_backward_kernel<true><<<grid, kThreads, smem, st>>>(prm);
   } else {
-    constexpr size_t smem = size_t(kStages) * kTile * 2 + sizeof(BwdTail);
+    constexpr size_t smem = size_t(stages_of<false>()) * kTile * 2 + sizeof(BwdTail);
     static bool attr = false;
     if (!attr) {
       YATT_TRY_CUDA(cudaFuncSetAttribute(logits_backward_kernel<false>,
