@@ -1,0 +1,152 @@
+// yatt_rank.cpp — one WeChat-YATT parallel-controller rank written against the
+// drop-in C++ API only (include/yatt/*.hpp), the way the reference's runner /
+// demo worker would call it after the link swap described in INTEGRATION.md.
+//
+//   1. build the step batch like runner::make_step_batch (runner.cpp:152-166)
+//   2. dynamic-sampling rounds for all controller shards on the device
+//      (sim::run_rollout_rounds = the shard loop of run_rlhf_step)
+//   3. repack accepted lengths into balanced buckets (balancer::sort_and_bucket)
+//   4. experience making on the device: logprob/entropy/KL, GRPO advantages,
+//      clipped-surrogate + KL loss (experience.hpp), loss finalised on host
+// Prints a short report and "rank ok"; exits non-zero on any mismatch.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "yatt/balancer.hpp"
+#include "yatt/errors.hpp"
+#include "yatt/experience.hpp"
+#include "yatt/simcore.hpp"
+#include "yatt/workload.hpp"
+#include "yatt_cuda.h"
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    std::fprintf(stderr, "%s: %s\n", what, cudaGetErrorString(e));
+    std::exit(2);
+  }
+}
+
+template <typename T>
+T* dalloc(size_t n) {
+  void* p = nullptr;
+  ck(cudaMalloc(&p, n * sizeof(T) + 16), "cudaMalloc");
+  return static_cast<T*>(p);
+}
+
+}  // namespace
+
+int main() {
+  using namespace yatt;
+  const int prompts = 16, group = 8, T = 256, vocab = 32000, controllers = 4;
+  const std::uint64_t seed = 20250814;
+
+  // 1. step batch (sample_id = step * B + i, keyed prompt lengths)
+  workload::RolloutBatch batch;
+  batch.step_index = 0;
+  const workload::LengthDistribution prompt_dist{workload::DistKind::kUniform, 16, 64, 4096};
+  for (int i = 0; i < prompts * group; ++i) {
+    workload::RolloutSample s;
+    s.sample_id = static_cast<std::uint64_t>(i);
+    s.prompt_len_tokens = workload::sample_length_keyed(prompt_dist, seed,
+                                                        workload::kPromptLenStream, 0, 0,
+                                                        s.sample_id);
+    batch.samples.push_back(s);
+  }
+
+  // 2. dynamic-sampling rounds, every controller shard per launch
+  sim::RoundParams params;
+  params.out_dist = {workload::DistKind::kUniform, 1, double(T), T};
+  params.rejection = {0.3, true, group};
+  params.seed = seed;
+  params.microbatch_size = 8;
+  params.max_rounds = 4;
+  const auto rounds = sim::run_rollout_rounds(batch, controllers, params);
+  long long units = 0;
+  for (const auto& reps : rounds) units += sim::reduce_round_reports(reps).train_units;
+  int accepted = 0;
+  std::vector<int> lengths;
+  for (const auto& s : batch.samples) {
+    accepted += s.accepted;
+    lengths.push_back(s.prompt_len_tokens + s.target_out_len_tokens);
+  }
+  std::printf("rollout: %zu rounds, %d/%zu accepted, train_units=%lld\n", rounds.size(), accepted,
+              batch.samples.size(), units);
+  if (accepted != int(batch.samples.size())) return 1;
+
+  // same rounds from one controller must give the same totals (controller invariance)
+  workload::RolloutBatch one = batch;
+  for (auto& s : one.samples) s.accepted = false, s.accepted_round = 0, s.target_out_len_tokens = 0;
+  long long units1 = 0;
+  for (const auto& reps : sim::run_rollout_rounds(one, 1, params))
+    units1 += sim::reduce_round_reports(reps).train_units;
+  if (units1 != units) {
+    std::fprintf(stderr, "controller invariance violated: %lld vs %lld\n", units1, units);
+    return 1;
+  }
+
+  // 3. balanced repack of the accepted samples
+  const balancer::BatchingPlan plan = balancer::sort_and_bucket(lengths, 16, seed);
+  const double waste = balancer::padding_waste(plan, lengths);
+  std::printf("buckets: %zu, padding waste %.4f (bound %.4f)\n", plan.buckets.size(), waste,
+              balancer::waste_bound(16));
+
+  // 4. experience making on the device
+  const std::int64_t rows = std::int64_t(prompts) * group * T;
+  auto* pol = dalloc<std::uint16_t>(size_t(rows) * vocab);
+  auto* ref = dalloc<std::uint16_t>(size_t(rows) * vocab);
+  auto* tgt = dalloc<std::int32_t>(size_t(rows));
+  auto* stats = dalloc<float>(size_t(rows) * 4);
+  auto* rewards = dalloc<float>(size_t(prompts) * group);
+  auto* sadv = dalloc<float>(size_t(prompts) * group);
+  auto* tadv = dalloc<float>(size_t(rows));
+  auto* old = dalloc<float>(size_t(rows));
+  auto* cu = dalloc<std::int64_t>(size_t(prompts) * group + 1);
+  auto* sums = dalloc<experience::LossSums>(1);
+  const size_t ws_bytes = experience::policy_loss_workspace_bytes();
+  void* ws = dalloc<std::uint8_t>(ws_bytes);
+  detail::throw_status(yatt_synth_logits(seed, 0, rows, vocab, pol, ref, tgt, nullptr));
+  detail::throw_status(yatt_synth_floats(seed, 105, 0, prompts * group, YATT_SYNTH_REWARD, group,
+                                         nullptr, rewards, nullptr));
+  std::vector<std::int64_t> hcu(size_t(prompts) * group + 1);
+  for (size_t i = 0; i < hcu.size(); ++i) hcu[i] = std::int64_t(i) * T;
+  ck(cudaMemcpy(cu, hcu.data(), hcu.size() * 8, cudaMemcpyHostToDevice), "H2D cu");
+
+  float *logp = stats, *ref_logp = stats + rows, *ent = stats + 2 * rows, *kl = stats + 3 * rows;
+  experience::token_logprob_stats(pol, ref, tgt, nullptr, rows, vocab,
+                                  experience::KlEstimator::kK3, {logp, ref_logp, ent, kl});
+  detail::throw_status(yatt_synth_floats(seed, 104, 0, rows, YATT_SYNTH_OLD_DELTA, 1, logp, old,
+                                         nullptr));
+  experience::grpo_advantages(rewards, prompts * group, 0, experience::GrpoConfig{group}, sadv);
+  detail::throw_status(yatt_broadcast_to_tokens(sadv, cu, prompts * group, nullptr, tadv, rows,
+                                                nullptr));
+  const experience::PolicyLossConfig cfg;
+  experience::policy_loss(logp, old, tadv, kl, ent, nullptr, rows, nullptr, 0, cfg, sums, ws,
+                          ws_bytes);
+  experience::LossSums h;
+  ck(cudaMemcpy(&h, sums, sizeof(h), cudaMemcpyDeviceToHost), "D2H sums");
+  const double loss = experience::finalize_loss(h, cfg);
+  std::printf("experience: %lld tokens, loss %.6f, mean kl %.6f, mean entropy %.4f, clipfrac %.4f\n",
+              (long long)h.token_count, loss, h.kl_sum / h.token_count,
+              h.entropy_sum / h.token_count, h.clip_count / h.token_count);
+  if (!(h.token_count == double(rows)) || !std::isfinite(loss)) return 1;
+
+  // errors keep the reference's types
+  try {
+    balancer::sort_and_bucket(lengths, 0, 1);
+    return 1;
+  } catch (const ConfigError&) {
+  }
+  try {
+    workload::shard_dataset(10, 3, 3);
+    return 1;
+  } catch (const RankOutOfRange&) {
+  }
+  std::printf("rank ok\n");
+  return 0;
+}
