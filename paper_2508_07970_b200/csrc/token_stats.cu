@@ -237,6 +237,62 @@ __device__ __forceinline__ RowPartial shfl_partial(const RowPartial& p, int off)
   return o;
 }
 
+#ifndef YATT_A1_FASTPATH
+#define YATT_A1_FASTPATH 1
+#endif
+constexpr bool kFastPath = YATT_A1_FASTPATH != 0;
+constexpr uint32_t kFixupSentinel = 0x7fc0fadeu;  // quiet NaN payload: "recompute me"
+
+// Re-base a thread's partial so its sum lies in [1, 2): makes the cross-
+// thread combine safe even when the fast path let a thread's terms grow far
+// above (or below) its base.  Exact (power-of-two scaling).
+__device__ __forceinline__ RowPartial normalize(RowPartial r) {
+  if (r.s > 0.f && r.s <= 3.4e38f) {
+    const int k = ilogbf(r.s);
+    r.w = ldexpf(fmaf(-float(k), r.s, r.w), -k);
+    r.s = ldexpf(r.s, -k);
+    r.u = ldexpf(r.u, -k);
+    r.mp += float(k);
+  }
+  if (r.sq > 0.f && r.sq <= 3.4e38f) {
+    const int k = ilogbf(r.sq);
+    r.sq = ldexpf(r.sq, -k);
+    r.mq += float(k);
+  }
+  return r;
+}
+
+template <bool kFull>
+__device__ __forceinline__ bool partial_finite(const RowPartial& q) {
+  return isfinite(q.s) && isfinite(q.w) && isfinite(q.sq) && (!kFull || isfinite(q.u)) &&
+         q.s > 0.f && q.sq > 0.f;
+}
+
+// fp64 epilogue of one row from its combined partial and target logits.
+__device__ __forceinline__ void emit_row(const Params& p, int64_t row, const RowPartial& q,
+                                         double xy, double zy) {
+  const double l2s = log2(double(q.s));
+  const double l2q = log2(double(q.sq));
+  const double logp = xy - kLn2 * (double(q.mp) + l2s);
+  const double rlogp = zy - kLn2 * (double(q.mq) + l2q);
+  // lse_q - lse_p without cancelling two large numbers.
+  const double dlse = kLn2 * ((double(q.mq) - double(q.mp)) + log2(double(q.sq) / double(q.s)));
+  p.logp[row] = float(logp);
+  if (p.ref_logp) p.ref_logp[row] = float(rlogp);
+  if (p.ent) p.ent[row] = float(kLn2 * (l2s - double(q.w) / double(q.s)));
+  if (p.kl) {
+    const double delta = (zy - xy) - dlse;  // ref_logp - logp
+    double kl;
+    switch (p.kl_mode) {
+      case YATT_KL_K1: kl = -delta; break;
+      case YATT_KL_K2: kl = 0.5 * delta * delta; break;
+      case YATT_KL_K3: kl = expm1(delta) - delta; break;
+      default: kl = double(q.u) / double(q.s) + dlse; break;
+    }
+    p.kl[row] = float(kl);
+  }
+}
+
 template <bool kFull>
 __global__ void __launch_bounds__(kThreads, 2) token_stats_kernel(const Params p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -330,23 +386,34 @@ __global__ void __launch_bounds__(kThreads, 2) token_stats_kernel(const Params p
           Q[i] = lds128(sq + v * 8);
         }
 #pragma unroll
-        for (int i = 0; i < kVecPerThread; ++i) P[i] = floor_policy(P[i]);
-        uint32_t mpv = vmax4(P[0]), mqv = vmax4(Q[0]);
-#pragma unroll
-        for (int i = 1; i < kVecPerThread; ++i) {
-          mpv = bmax2(mpv, vmax4(P[i]));
-          mqv = bmax2(mqv, vmax4(Q[i]));
+        for (int i = 0; i < kVecPerThread; ++i) {
+          P[i] = floor_policy(P[i]);
+          if (kFull) Q[i] = floor_policy(Q[i]);  // x - z finite when both are -inf
         }
-        const float fmp = pair_max(mpv), fmq = pair_max(mqv);
-        if (fmp > acc.thr_p) acc.rebase_p(fmp);
-        if (fmq > acc.thr_q) acc.rebase_q(fmq);
+        // Fast path: the per-thread bases come from the row's first tile only;
+        // later full tiles skip the max check (fewer instructions = less power
+        // on this power-capped kernel).  A row whose later logits exceed a
+        // thread's base by > ~88 nats overflows to inf, is flagged in the
+        // epilogue and recomputed by token_stats_fixup_kernel.
+        if (!kFastPath || t == 0) {
+          uint32_t mpv = vmax4(P[0]), mqv = vmax4(Q[0]);
+#pragma unroll
+          for (int i = 1; i < kVecPerThread; ++i) {
+            mpv = bmax2(mpv, vmax4(P[i]));
+            mqv = bmax2(mqv, vmax4(Q[i]));
+          }
+          const float fmp = pair_max(mpv), fmq = pair_max(mqv);
+          if (fmp > acc.thr_p) acc.rebase_p(fmp);
+          if (fmq > acc.thr_q) acc.rebase_q(fmq);
+        }
 #pragma unroll
         for (int i = 0; i < kVecPerThread; ++i) acc.step(P[i], Q[i]);
       } else {
         for (int v = tid; v < nvec; v += kConsumers) {
           uint4 P = lds128(sp + v * 8);
-          const uint4 Q = lds128(sq + v * 8);
+          uint4 Q = lds128(sq + v * 8);
           P = floor_policy(P);
+          if (kFull) Q = floor_policy(Q);
           const float fmp = pair_max(vmax4(P)), fmq = pair_max(vmax4(Q));
           if (fmp > acc.thr_p) acc.rebase_p(fmp);
           if (fmq > acc.thr_q) acc.rebase_q(fmq);
@@ -369,6 +436,7 @@ __global__ void __launch_bounds__(kThreads, 2) token_stats_kernel(const Params p
     r.w = Acc<kFull>::total(acc.w);
     r.sq = Acc<kFull>::total(acc.sq);
     r.u = kFull ? Acc<kFull>::total(acc.u) : 0.f;
+    r = normalize(r);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) r = combine(r, shfl_partial(r, off));
     if (lane == 0) tail->red[par][warp] = r;
@@ -380,31 +448,68 @@ __global__ void __launch_bounds__(kThreads, 2) token_stats_kernel(const Params p
 #pragma unroll
       for (int off = kConsumerWarps / 2; off > 0; off >>= 1) q = combine(q, shfl_partial(q, off));
       if (lane == 0) {
-        const double xy = tail->tgt[par][0];
-        const double zy = tail->tgt[par][1];
-        const double l2s = log2(double(q.s));
-        const double l2q = log2(double(q.sq));
-        const double logp = xy - kLn2 * (double(q.mp) + l2s);
-        const double rlogp = zy - kLn2 * (double(q.mq) + l2q);
-        // lse_q - lse_p without cancelling two large numbers.
-        const double dlse = kLn2 * ((double(q.mq) - double(q.mp)) + log2(double(q.sq) / double(q.s)));
-        p.logp[row] = float(logp);
-        if (p.ref_logp) p.ref_logp[row] = float(rlogp);
-        if (p.ent) p.ent[row] = float(kLn2 * (l2s - double(q.w) / double(q.s)));
-        if (p.kl) {
-          const double delta = (zy - xy) - dlse;  // ref_logp - logp
-          double kl;
-          switch (p.kl_mode) {
-            case YATT_KL_K1: kl = -delta; break;
-            case YATT_KL_K2: kl = 0.5 * delta * delta; break;
-            case YATT_KL_K3: kl = expm1(delta) - delta; break;
-            default: kl = double(q.u) / double(q.s) + dlse; break;
-          }
-          p.kl[row] = float(kl);
+        if (kFastPath && !partial_finite<kFull>(q)) {
+          p.logp[row] = __uint_as_float(kFixupSentinel);  // token_stats_fixup_kernel redoes it
+        } else {
+          emit_row(p, row, q, tail->tgt[par][0], tail->tgt[par][1]);
         }
       }
     }
     ++iter;
+  }
+}
+
+// Robust recomputation of flagged rows (fast-path overflow): per-vector
+// rebase checks, global loads, one CTA per row.  Launched after every
+// token_stats_kernel; with no flagged row it only reads logp (4 B/row).
+template <bool kFull>
+__global__ void __launch_bounds__(kConsumers) token_stats_fixup_kernel(const Params p) {
+  __shared__ int64_t list[kConsumers];
+  __shared__ int count;
+  __shared__ RowPartial red[kConsumerWarps];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t V = p.V;
+  for (int64_t base = int64_t(blockIdx.x) * kConsumers; base < p.rows;
+       base += int64_t(gridDim.x) * kConsumers) {
+    if (tid == 0) count = 0;
+    __syncthreads();
+    const int64_t r = base + tid;
+    if (r < p.rows && __float_as_uint(p.logp[r]) == kFixupSentinel) list[atomicAdd(&count, 1)] = r;
+    __syncthreads();
+    const int n = count;
+    for (int k = 0; k < n; ++k) {
+      const int64_t row = list[k];
+      Acc<kFull> acc;
+      acc.reset();
+      const uint4* gp = reinterpret_cast<const uint4*>(p.pol + row * V);
+      const uint4* gq = reinterpret_cast<const uint4*>(p.ref + row * V);
+      for (int64_t v = tid; v < V / 8; v += kConsumers) {
+        const uint4 P = floor_policy(__ldg(gp + v));
+        const uint4 Q = kFull ? floor_policy(__ldg(gq + v)) : __ldg(gq + v);
+        const float fmp = pair_max(vmax4(P)), fmq = pair_max(vmax4(Q));
+        if (fmp > acc.thr_p) acc.rebase_p(fmp);
+        if (fmq > acc.thr_q) acc.rebase_q(fmq);
+        acc.step(P, Q);
+      }
+      RowPartial q{acc.mp, Acc<kFull>::total(acc.s), Acc<kFull>::total(acc.w), acc.mq,
+                   Acc<kFull>::total(acc.sq), kFull ? Acc<kFull>::total(acc.u) : 0.f};
+      q = normalize(q);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) q = combine(q, shfl_partial(q, off));
+      if (lane == 0) red[warp] = q;
+      __syncthreads();
+      if (warp == 0) {
+        q = red[lane & (kConsumerWarps - 1)];
+#pragma unroll
+        for (int off = kConsumerWarps / 2; off > 0; off >>= 1) q = combine(q, shfl_partial(q, off));
+        if (lane == 0) {
+          const int32_t y = p.tgt[row];
+          emit_row(p, row, q, __uint_as_float(uint32_t(p.pol[row * V + y]) << 16),
+                   __uint_as_float(uint32_t(p.ref[row * V + y]) << 16));
+        }
+      }
+      __syncthreads();
+    }
   }
 }
 
@@ -445,7 +550,14 @@ int token_stats_launch(const uint16_t* pol, const uint16_t* ref, const int32_t* 
     }
     token_stats_kernel<false><<<grid, kThreads, kSmemBytes, st>>>(p);
   }
-  return check_launch("token_stats_kernel");
+  int rc = check_launch("token_stats_kernel");
+  if (rc || !kFastPath) return rc;
+  const int fgrid = int(min64(ceil_div(rows, kConsumers), int64_t(num_sms())));
+  if (kl_mode == YATT_KL_FULL)
+    token_stats_fixup_kernel<true><<<fgrid, kConsumers, 0, st>>>(p);
+  else
+    token_stats_fixup_kernel<false><<<fgrid, kConsumers, 0, st>>>(p);
+  return check_launch("token_stats_fixup_kernel");
 }
 
 }  // namespace yattb

@@ -95,6 +95,36 @@ def test_token_stats_masked_vocab_and_peaked_rows(cuda):
     assert abs(out[0][3] - exp[0][3]) < 1e-6 and abs(out[2][3] - exp[2][3]) < 1e-6
 
 
+@pytest.mark.parametrize("kl_mode", ["k3", "full"])
+def test_token_stats_fast_path_overflow_rows_are_recomputed(cuda, kl_mode):
+    """Rows whose later tiles exceed the first tile's bases by > 88 nats
+    overflow the fast path and must come back exact from the fix-up kernel;
+    a 70-nat jump stays on the fast path (per-thread normalisation)."""
+    rows, vocab = 12, 152064
+    pol, ref, tgt = ops.synth_logits(9, 0, rows, vocab, device=cuda)
+    ar = torch.arange(rows, device=cuda)
+    keep_p, keep_r = pol[ar, tgt.long()].clone(), ref[ar, tgt.long()].clone()
+    pol[0, 150000] = 100.0                 # huge late logit (overflow -> fix-up)
+    ref[1, 149000] = 96.0
+    pol[2, :8192] = float("-inf")          # whole first tile masked
+    ref[2, :8192] = float("-inf")
+    pol[3, :8192] -= 30.0                  # late values 30+ nats above: fast path
+    pol[3, 140000:140100] = 40.0
+    pol[4, :] = 60.0                       # constant rows
+    ref[4, :] = -60.0
+    pol[5, 100000] = 88.0                  # just below the overflow threshold
+    pol[ar, tgt.long()], ref[ar, tgt.long()] = keep_p, keep_r
+    out = torch.stack(ops.token_stats(pol, ref, tgt, None, kl_mode)).cpu().numpy()
+    hp = pol.view(torch.int16).cpu().numpy().view(np.uint16)
+    hr = ref.view(torch.int16).cpu().numpy().view(np.uint16)
+    exp = O.token_stats(hp, hr, tgt.cpu().numpy(), None, kl_mode)
+    assert np.all(np.isfinite(out))
+    # row 4 has p(target) ~ 1 (log-prob ~ 0): relative error is meaningless
+    # there, an fp32 pipeline is accurate to ~1e-6 absolute
+    for i in range(4):
+        assert np.all(np.abs(out[i] - exp[i]) <= TOL * np.abs(exp[i]) + 4e-6), i
+
+
 def test_token_stats_host_buffers_match_device(cuda):
     rows, vocab = 300, 32000
     hp, hr, ht = O.synth_logits(11, 0, rows, vocab)
