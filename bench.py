@@ -320,7 +320,9 @@ def run_b200(args):
                 "dtype": "bf16", "data": "synthetic (keyed integer-derived bf16 logits, "
                 "binary group rewards; DESIGN.md)", "config": workload_config(world),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": args.steps * (ng + 4), "clocks": clk,
+                # per group: token_stats + its fix-up pass; per step: grpo_adv,
+                # broadcast, loss partials + final
+                "gpu_launches": args.steps * (2 * ng + 4), "clocks": clk,
                 "loss": loss}
         emit(line)
     if world > 1:
