@@ -151,6 +151,14 @@ int yatt_shard_round(yatt_sample* d_samples, const int64_t* h_shard_offsets,
                      yatt_round_report* d_reports, yatt_mb_agg* d_mbs,
                      void* stream);
 
+/* R8  integer part of StepAssembler::feed_round (simcore.cpp:304-311) on the */
+/* device, over n reports (all ranks' reports after an all-gather of the     */
+/* 48-byte structs = the binary wire format replacing demo.cpp:32-76):       */
+/* d_out[6] = {sum active, sum pending, sum forced, sum train_units,          */
+/*             sum score_tokens, continue (= sum pending > 0)}.              */
+int yatt_reduce_round_reports(const yatt_round_report* d_reports, int32_t n,
+                              int64_t* d_out, void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* A1  fused token statistics over policy + reference logits                 */
 /* For each row r (token) of the row-major [rows, vocab] bf16 tensors:       */

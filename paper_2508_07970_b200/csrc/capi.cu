@@ -63,6 +63,7 @@ int shard_round_launch(yatt_sample*, const int64_t*, int32_t, int32_t, int32_t, 
                        const yatt_round_params*, yatt_round_report*, yatt_mb_agg*, cudaStream_t);
 size_t sort_workspace_bytes(int64_t);
 int sort_order_launch(const int32_t*, int64_t, uint32_t*, void*, size_t, cudaStream_t);
+int reduce_reports_launch(const yatt_round_report*, int32_t, int64_t*, cudaStream_t);
 int grad_coef_launch(const uint16_t*, const uint16_t*, const int32_t*, const float*, const float*,
                      const float*, const float*, const float*, const float*, const uint8_t*,
                      int64_t, int32_t, const int64_t*, int64_t, const yatt_loss_config*, int32_t,
@@ -170,6 +171,10 @@ int yatt_shard_round(yatt_sample* samples, const int64_t* h_off, int32_t nshards
                      yatt_round_report* reports, yatt_mb_agg* mbs, void* stream) {
   return shard_round_launch(samples, h_off, nshards, first_rank, step, round, p, reports, mbs,
                             as_stream(stream));
+}
+
+int yatt_reduce_round_reports(const yatt_round_report* r, int32_t n, int64_t* out, void* stream) {
+  return reduce_reports_launch(r, n, out, as_stream(stream));
 }
 
 int yatt_token_stats(const uint16_t* pol, const uint16_t* ref, const int32_t* tgt,

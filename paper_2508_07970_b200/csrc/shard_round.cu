@@ -214,7 +214,38 @@ __global__ void shard_round_finalize_kernel(int32_t nshards, int32_t mb, yatt_sa
     if (samples[i].accepted == kAcceptedThisRound) samples[i].accepted = 1;
 }
 
+// One warp: sums of the reports' integer fields (order-free, exact).
+__global__ void reduce_reports_kernel(const yatt_round_report* r, int32_t n, int64_t* out) {
+  long long a = 0, p = 0, f = 0, u = 0, sc = 0;
+  for (int i = threadIdx.x; i < n; i += 32) {
+    a += r[i].active_count;
+    p += r[i].pending_count;
+    f += r[i].forced_accept_count;
+    u += r[i].accepted_train_units;
+    sc += r[i].accepted_score_tokens;
+  }
+  a = warp_sum(a);
+  p = warp_sum(p);
+  f = warp_sum(f);
+  u = warp_sum(u);
+  sc = warp_sum(sc);
+  if (threadIdx.x == 0) {
+    out[0] = a;
+    out[1] = p;
+    out[2] = f;
+    out[3] = u;
+    out[4] = sc;
+    out[5] = p > 0 ? 1 : 0;
+  }
+}
+
 }  // namespace
+
+int reduce_reports_launch(const yatt_round_report* r, int32_t n, int64_t* out, cudaStream_t st) {
+  YATT_REQUIRE(n >= 0 && out != nullptr, YATT_ERR_CONFIG, "reduce_round_reports: bad arguments");
+  reduce_reports_kernel<<<1, 32, 0, st>>>(r, n, out);
+  return check_launch("reduce_reports_kernel");
+}
 
 int validate_dist(const yatt_length_dist* d) {
   YATT_REQUIRE(d != nullptr, YATT_ERR_CONFIG, "null length distribution");

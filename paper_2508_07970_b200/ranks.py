@@ -108,6 +108,25 @@ class YattComm:
             self.h = C.c_void_p()
 
 
+REPORT_WORDS = 6  # yatt_round_report = 48 bytes = 6 int64 words (binary wire format)
+MB_WORDS = 3      # yatt_mb_agg = 24 bytes
+
+
+def exchange_round_reports(d_reports: torch.Tensor, d_mbs: torch.Tensor, comm=None):
+    """All-gather this rank's round reports (+ microbatch aggregates, fixed
+    per-rank capacity) as raw int64 words and reduce them on the device —
+    the binary replacement of the reference's JSON `submit_round` RPC and
+    coordinator reduce (demo.cpp:32-76, :261-274; simcore.cpp:304-311).
+    Returns (all_reports_words, all_mb_words, reduction[6]) on the device;
+    reduction = {active, pending, forced, train_units, score_tokens, continue}."""
+    rep = allgather_counts(d_reports.view(torch.int64).contiguous(), comm)
+    mbs = allgather_counts(d_mbs.view(torch.int64).contiguous(), comm)
+    out = torch.empty((6,), dtype=torch.int64, device=d_reports.device)
+    check(lib().yatt_reduce_round_reports(rep.data_ptr(), rep.numel() // REPORT_WORDS,
+                                          out.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    return rep, mbs, out
+
+
 def allreduce_sums(sums: torch.Tensor, comm=None) -> torch.Tensor:
     """Sum the fp64 loss sums over ranks (in place)."""
     if comm is None:

@@ -82,6 +82,38 @@ def main():
     ops.gather_varlen(payload, cu_all, single["index_map"], single["new_cu"],
                       single["counts"][:1], P * R, ref)
     assert torch.equal(dst, ref)
+
+    # dynamic-sampling rounds across real ranks: each rank runs its own shard,
+    # reports travel as 48-byte structs over NCCL, the feed_round reduce runs
+    # on the device; must equal the single-process loop over all shards
+    import ctypes as C
+    from paper_2508_07970_b200 import api
+    from paper_2508_07970_b200._lib import ReportC, check, lib
+    n_all = 2048
+    params = api.RoundParams(api.LengthDistribution(api.UNIFORM, 1, 4096, 4096),
+                             api.RejectionConfig(0.3, True, 8), SEED, 8, 5)
+    mk = lambda: api.RolloutBatch(0, [api.RolloutSample(i, 64 + i % 13) for i in range(n_all)])  # noqa
+    ref_rounds = api.run_rollout_rounds(mk(), world, params)
+    shard = api.make_shard_state(mk(), world, rank)
+    ds = api._DeviceShards([shard], params, dev)
+    off = (C.c_int64 * 2)(0, len(shard.samples))
+    rnd = 0
+    while True:
+        rnd += 1
+        check(lib().yatt_shard_round(ds.d.data_ptr(), off, 1, rank, 0, rnd, C.byref(params.c()),
+                                     ds.d_rep.data_ptr(), ds.d_mbs.data_ptr(),
+                                     torch.cuda.current_stream().cuda_stream))
+        reps, mbs, red = ranks.exchange_round_reports(ds.d_rep, ds.d_mbs, comm)
+        all_reps = (ReportC * world).from_buffer_copy(reps.cpu().numpy().tobytes())
+        got = [(r.controller_rank, r.active_count, r.pending_count, r.accepted_train_units)
+               for r in all_reps]
+        exp = [(r.controller_rank, r.active_count, r.pending_count, r.accepted_train_units)
+               for r in ref_rounds[rnd - 1]]
+        assert got == exp, (rank, rnd, got, exp)
+        assert int(red[1]) == sum(r.pending_count for r in ref_rounds[rnd - 1])
+        if int(red[5]) == 0:  # continue flag decided on the device
+            break
+    assert rnd == len(ref_rounds)
     comm.close()
     dist.barrier()
     dist.destroy_process_group()
