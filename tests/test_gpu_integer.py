@@ -130,6 +130,28 @@ def test_rollout_rounds_match_reference(cuda, name):
         assert [s.accepted_round for s in batch.samples] == run["final_accepted_round"]
 
 
+def test_feed_round_reduce_on_device(cuda):
+    """yatt_reduce_round_reports == the integer sums of feed_round
+    (simcore.cpp:304-311) over the golden per-round reports."""
+    import ctypes as C
+    from paper_2508_07970_b200._lib import ReportC, check, lib
+    case = load("rollout_config5.json")
+    for run in case["runs"]:
+        for rnd in run["rounds"]:
+            arr = (ReportC * len(rnd))()
+            for i, r in enumerate(rnd):
+                rk, ro, act, acc, forced, pend, score, units = r["report"]
+                arr[i] = ReportC(rk, ro, act, acc, forced, pend, score, units, 0)
+            d = torch.frombuffer(bytearray(bytes(arr)), dtype=torch.uint8).to(cuda)
+            out = torch.empty(6, dtype=torch.int64, device=cuda)
+            check(lib().yatt_reduce_round_reports(d.data_ptr(), len(rnd), out.data_ptr(), None))
+            pend = sum(r["report"][5] for r in rnd)
+            assert out.cpu().tolist() == [sum(r["report"][2] for r in rnd), pend,
+                                          sum(r["report"][4] for r in rnd),
+                                          sum(r["report"][7] for r in rnd),
+                                          sum(r["report"][6] for r in rnd), int(pend > 0)]
+
+
 def test_shard_round_output_single_shard_api(cuda):
     case = load("rollout_config1.json")
     run = [r for r in case["runs"] if r["controllers"] == 2][0]
