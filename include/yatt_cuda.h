@@ -289,6 +289,26 @@ double yatt_loss_finalize(const yatt_loss_sums* h_sums,
                           const yatt_loss_config* config);
 
 /* ------------------------------------------------------------------------ */
+/* Fused LM-head GEMM + online log-softmax on tcgen05     */
+/* logits = hidden[rows, hidden] . lm_head[vocab, hidden]^T (bf16, fp32       */
+/* accumulate in TMEM) are never materialised; per row writes               */
+/* logp (target log-prob), entropy and lse (any output but logp may be      */
+/* NULL).  n_split splits the vocabulary across CTAs (1..64) to fill the    */
+/* GPU when rows are few; hidden % 8 == 0; operands 16-byte aligned.         */
+/* Run once per model (policy, reference) then yatt_kl_from_logps.           */
+/* ------------------------------------------------------------------------ */
+size_t yatt_lmhead_workspace_bytes(int64_t rows, int32_t vocab, int32_t n_split);
+int yatt_lmhead_token_stats(const uint16_t* d_hidden, const uint16_t* d_lm_head,
+                            const int32_t* d_targets, int64_t rows,
+                            int32_t hidden, int32_t vocab, int32_t n_split,
+                            float* d_logp, float* d_entropy, float* d_lse,
+                            void* d_workspace, size_t workspace_bytes,
+                            void* stream);
+/* kl[i] from token log-probs (K1 / K2 / K3; Delta = ref_logp - logp). */
+int yatt_kl_from_logps(const float* d_logp, const float* d_ref_logp, int64_t n,
+                       int32_t kl_mode, float* d_kl, void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* Backward into the policy logits                        */
 /* Per token t: dL/dx_v = g (1[v=y] - p_v) + h p_v (log p_v + H)              */
 /*                        + f p_v (log p_v - log q_v - KL)                   */

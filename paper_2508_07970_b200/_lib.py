@@ -95,6 +95,10 @@ SIGNATURES = {
     "yatt_shard_round": (C.c_int, [c_p, P(c_i64), c_i32, c_i32, c_i32, c_i32, P(RoundParamsC), c_p,
                                    c_p, c_p]),
     "yatt_reduce_round_reports": (C.c_int, [c_p, c_i32, c_p, c_p]),
+    "yatt_lmhead_workspace_bytes": (c_sz, [c_i64, c_i32, c_i32]),
+    "yatt_lmhead_token_stats": (C.c_int, [c_p, c_p, c_p, c_i64, c_i32, c_i32, c_i32, c_p, c_p,
+                                          c_p, c_p, c_sz, c_p]),
+    "yatt_kl_from_logps": (C.c_int, [c_p, c_p, c_i64, c_i32, c_p, c_p]),
     "yatt_token_stats": (C.c_int, [c_p, c_p, c_p, c_p, c_i64, c_i32, c_i32, c_p, c_p, c_p, c_p,
                                    c_p]),
     "yatt_token_stats_host": (C.c_int, [c_p, c_p, c_p, c_p, c_i64, c_i32, c_i32, c_p, c_p, c_p,

@@ -64,6 +64,11 @@ int shard_round_launch(yatt_sample*, const int64_t*, int32_t, int32_t, int32_t, 
 size_t sort_workspace_bytes(int64_t);
 int sort_order_launch(const int32_t*, int64_t, uint32_t*, void*, size_t, cudaStream_t);
 int reduce_reports_launch(const yatt_round_report*, int32_t, int64_t*, cudaStream_t);
+size_t lmhead_workspace_bytes(int64_t, int32_t, int32_t);
+int lmhead_token_stats_launch(const uint16_t*, const uint16_t*, const int32_t*, int64_t, int32_t,
+                              int32_t, int32_t, float*, float*, float*, void*, size_t,
+                              cudaStream_t);
+int kl_from_logps_launch(const float*, const float*, int64_t, int32_t, float*, cudaStream_t);
 int grad_coef_launch(const uint16_t*, const uint16_t*, const int32_t*, const float*, const float*,
                      const float*, const float*, const float*, const float*, const uint8_t*,
                      int64_t, int32_t, const int64_t*, int64_t, const yatt_loss_config*, int32_t,
@@ -171,6 +176,22 @@ int yatt_shard_round(yatt_sample* samples, const int64_t* h_off, int32_t nshards
                      yatt_round_report* reports, yatt_mb_agg* mbs, void* stream) {
   return shard_round_launch(samples, h_off, nshards, first_rank, step, round, p, reports, mbs,
                             as_stream(stream));
+}
+
+size_t yatt_lmhead_workspace_bytes(int64_t rows, int32_t vocab, int32_t n_split) {
+  return lmhead_workspace_bytes(rows, vocab, n_split);
+}
+
+int yatt_lmhead_token_stats(const uint16_t* hidden, const uint16_t* w, const int32_t* tgt,
+                            int64_t rows, int32_t d, int32_t vocab, int32_t n_split, float* logp,
+                            float* ent, float* lse, void* ws, size_t ws_bytes, void* stream) {
+  return lmhead_token_stats_launch(hidden, w, tgt, rows, d, vocab, n_split, logp, ent, lse, ws,
+                                   ws_bytes, as_stream(stream));
+}
+
+int yatt_kl_from_logps(const float* logp, const float* ref_logp, int64_t n, int32_t mode,
+                       float* kl, void* stream) {
+  return kl_from_logps_launch(logp, ref_logp, n, mode, kl, as_stream(stream));
 }
 
 int yatt_reduce_round_reports(const yatt_round_report* r, int32_t n, int64_t* out, void* stream) {

@@ -253,6 +253,37 @@ def sort_order_desc(lengths: torch.Tensor) -> torch.Tensor:
     return order
 
 
+# ------------------------------------- fused LM head + log-softmax (§8f #4) --
+def lmhead_token_stats(hidden: torch.Tensor, lm_head: torch.Tensor, targets: torch.Tensor,
+                       n_split: int | None = None, out: torch.Tensor | None = None):
+    """(logp, entropy, lse) per row of softmax(hidden @ lm_head^T) without
+    materialising the logits (tcgen05 GEMM + online LSE epilogue)."""
+    _dev(hidden, torch.bfloat16, "hidden")
+    _dev(lm_head, torch.bfloat16, "lm_head")
+    _dev(targets, torch.int32, "targets")
+    rows, d = hidden.shape
+    vocab = lm_head.shape[0]
+    if n_split is None:  # measured (tools/lmhead_sweep.py): few splits keep the weight
+        # stream shared in L2; enough splits to fill the SMs when rows are few
+        sms = torch.cuda.get_device_properties(hidden.device).multi_processor_count
+        n_split = min(64, max(2, sms // max(1, -(-rows // 128))))
+    if out is None:
+        out = torch.empty((3, rows), dtype=torch.float32, device=hidden.device)
+    wsb = lib().yatt_lmhead_workspace_bytes(rows, vocab, n_split)
+    ws = torch.empty((max(wsb, 16),), dtype=torch.uint8, device=hidden.device)
+    check(lib().yatt_lmhead_token_stats(_p(hidden), _p(lm_head), _p(targets), rows, d, vocab,
+                                        n_split, _p(out[0]), _p(out[1]), _p(out[2]), _p(ws),
+                                        wsb, _st()))
+    return out[0], out[1], out[2]
+
+
+def kl_from_logps(logp: torch.Tensor, ref_logp: torch.Tensor, kl_mode: str = "k3"):
+    kl = torch.empty_like(logp)
+    check(lib().yatt_kl_from_logps(_p(logp), _p(ref_logp), logp.numel(), KL_MODES[kl_mode],
+                                   _p(kl), _st()))
+    return kl
+
+
 # --------------------------------------------------- backward (§8f #1) ----
 def logits_grad(policy_logits, ref_logits, targets, logp, ref_logp, old_logp, advantages,
                 entropy, kl, mask=None, cu_seqlens=None, config=None, kl_mode="k3",
