@@ -459,33 +459,63 @@ __global__ void __launch_bounds__(kThreads, 2) token_stats_kernel(const Params p
   }
 }
 
-// Robust recomputation of flagged rows (fast-path overflow): per-vector
-// rebase checks, global loads, one CTA per row.  Launched after every
-// token_stats_kernel; with no flagged row it only reads logp (4 B/row).
-template <bool kFull>
+// 8 bf16 from an arbitrarily aligned row, -inf past the end (contributes 0).
+__device__ __forceinline__ uint4 load8_any(const uint16_t* row, int64_t e0, int64_t V) {
+  uint32_t w[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t lo = e0 + 2 * k < V ? uint32_t(__ldg(row + e0 + 2 * k)) : 0xFF80u;
+    const uint32_t hi = e0 + 2 * k + 1 < V ? uint32_t(__ldg(row + e0 + 2 * k + 1)) : 0xFF80u;
+    w[k] = lo | (hi << 16);
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// Robust per-row path, one CTA per row, per-vector rebase checks, global
+// loads.  kGeneric = false: recompute the rows the fast path flagged
+// (launched after every token_stats_kernel; with none flagged it only reads
+// logp, 4 B/row).  kGeneric = true: every row, for vocabularies or tensors
+// the TMA path cannot take (V % 8 != 0 or unaligned), with scalar loads.
+template <bool kFull, bool kGeneric>
 __global__ void __launch_bounds__(kConsumers) token_stats_fixup_kernel(const Params p) {
   __shared__ int64_t list[kConsumers];
   __shared__ int count;
   __shared__ RowPartial red[kConsumerWarps];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t V = p.V;
-  for (int64_t base = int64_t(blockIdx.x) * kConsumers; base < p.rows;
-       base += int64_t(gridDim.x) * kConsumers) {
+  constexpr int kChunk = kGeneric ? 8 : kConsumers;  // rows examined per CTA iteration
+  for (int64_t base = int64_t(blockIdx.x) * kChunk; base < p.rows;
+       base += int64_t(gridDim.x) * kChunk) {
     if (tid == 0) count = 0;
     __syncthreads();
     const int64_t r = base + tid;
-    if (r < p.rows && __float_as_uint(p.logp[r]) == kFixupSentinel) list[atomicAdd(&count, 1)] = r;
+    if (tid < kChunk && r < p.rows) {
+      if (kGeneric) {
+        if (p.mask != nullptr && p.mask[r] == 0) {
+          p.logp[r] = 0.f;
+          if (p.ref_logp) p.ref_logp[r] = 0.f;
+          if (p.ent) p.ent[r] = 0.f;
+          if (p.kl) p.kl[r] = 0.f;
+        } else {
+          list[atomicAdd(&count, 1)] = r;
+        }
+      } else if (__float_as_uint(p.logp[r]) == kFixupSentinel) {
+        list[atomicAdd(&count, 1)] = r;
+      }
+    }
     __syncthreads();
     const int n = count;
     for (int k = 0; k < n; ++k) {
       const int64_t row = list[k];
       Acc<kFull> acc;
       acc.reset();
-      const uint4* gp = reinterpret_cast<const uint4*>(p.pol + row * V);
-      const uint4* gq = reinterpret_cast<const uint4*>(p.ref + row * V);
-      for (int64_t v = tid; v < V / 8; v += kConsumers) {
-        const uint4 P = floor_policy(__ldg(gp + v));
-        const uint4 Q = kFull ? floor_policy(__ldg(gq + v)) : __ldg(gq + v);
+      const uint16_t* rp = p.pol + row * V;
+      const uint16_t* rq = p.ref + row * V;
+      for (int64_t v = tid; v < (V + 7) / 8; v += kConsumers) {
+        const uint4 P0 = kGeneric ? load8_any(rp, v * 8, V) : __ldg(reinterpret_cast<const uint4*>(rp) + v);
+        const uint4 Q0 = kGeneric ? load8_any(rq, v * 8, V) : __ldg(reinterpret_cast<const uint4*>(rq) + v);
+        const uint4 P = floor_policy(P0);
+        const uint4 Q = kFull ? floor_policy(Q0) : Q0;
         const float fmp = pair_max(vmax4(P)), fmq = pair_max(vmax4(Q));
         if (fmp > acc.thr_p) acc.rebase_p(fmp);
         if (fmq > acc.thr_q) acc.rebase_q(fmq);
@@ -518,18 +548,24 @@ __global__ void __launch_bounds__(kConsumers) token_stats_fixup_kernel(const Par
 int token_stats_launch(const uint16_t* pol, const uint16_t* ref, const int32_t* tgt,
                        const uint8_t* mask, int64_t rows, int32_t vocab, int32_t kl_mode,
                        float* logp, float* ref_logp, float* ent, float* kl, cudaStream_t st) {
-  YATT_REQUIRE(vocab > 0 && vocab % 8 == 0, YATT_ERR_CONFIG,
-               "token_stats: vocab must be a positive multiple of 8 (got %d)", vocab);
+  YATT_REQUIRE(vocab > 0, YATT_ERR_CONFIG, "token_stats: vocab must be positive (got %d)", vocab);
   YATT_REQUIRE(rows >= 0, YATT_ERR_CONFIG, "token_stats: rows must be >= 0");
   YATT_REQUIRE(kl_mode >= YATT_KL_K1 && kl_mode <= YATT_KL_FULL, YATT_ERR_CONFIG,
                "token_stats: unknown kl_mode %d", kl_mode);
   if (rows == 0) return YATT_OK;
   YATT_REQUIRE(logp != nullptr, YATT_ERR_CONFIG, "token_stats: logp output is required");
   YATT_REQUIRE(pol && ref && tgt, YATT_ERR_CONFIG, "token_stats: null input pointer");
-  YATT_REQUIRE((reinterpret_cast<uintptr_t>(pol) & 15) == 0 &&
-                   (reinterpret_cast<uintptr_t>(ref) & 15) == 0,
-               YATT_ERR_CONFIG, "token_stats: logits must be 16-byte aligned");
   Params p{pol, ref, tgt, mask, rows, vocab, kl_mode, logp, ref_logp, ent, kl};
+  const bool tma_ok = vocab % 8 == 0 && (reinterpret_cast<uintptr_t>(pol) & 15) == 0 &&
+                      (reinterpret_cast<uintptr_t>(ref) & 15) == 0;
+  if (!tma_ok) {  // generic path: any vocabulary size / alignment, scalar loads
+    const int ggrid = int(min64(ceil_div(rows, 8), int64_t(num_sms()) * 8));
+    if (kl_mode == YATT_KL_FULL)
+      token_stats_fixup_kernel<true, true><<<ggrid, kConsumers, 0, st>>>(p);
+    else
+      token_stats_fixup_kernel<false, true><<<ggrid, kConsumers, 0, st>>>(p);
+    return check_launch("token_stats_generic_kernel");
+  }
   const int grid = int(min64(rows, int64_t(2) * num_sms()));
   if (kl_mode == YATT_KL_FULL) {
     static bool attr_full = false;
@@ -554,9 +590,9 @@ int token_stats_launch(const uint16_t* pol, const uint16_t* ref, const int32_t* 
   if (rc || !kFastPath) return rc;
   const int fgrid = int(min64(ceil_div(rows, kConsumers), int64_t(num_sms())));
   if (kl_mode == YATT_KL_FULL)
-    token_stats_fixup_kernel<true><<<fgrid, kConsumers, 0, st>>>(p);
+    token_stats_fixup_kernel<true, false><<<fgrid, kConsumers, 0, st>>>(p);
   else
-    token_stats_fixup_kernel<false><<<fgrid, kConsumers, 0, st>>>(p);
+    token_stats_fixup_kernel<false, false><<<fgrid, kConsumers, 0, st>>>(p);
   return check_launch("token_stats_fixup_kernel");
 }
 

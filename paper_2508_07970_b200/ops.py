@@ -12,11 +12,19 @@ import ctypes as C
 import numpy as np
 import torch
 
-from ._lib import (LossConfigC, LossSumsC, check, lib)
+from ._lib import (ConfigError, LossConfigC, LossSumsC, check, lib)
 
-KL_MODES = {"k1": 0, "k2": 1, "k3": 2, "low_var_kl": 2, "full": 3}
-SYNTH = {"logp": 0, "old_delta": 1, "adv": 2, "kl": 3, "value": 4, "reward": 5}
-AGG_MODES = {"token-mean": 0, "seq-mean-token-mean": 1, "seq-mean-token-sum": 2}
+
+class _Modes(dict):
+    """Name -> ABI enum; unknown names raise ConfigError like the C ABI."""
+
+    def __missing__(self, key):
+        raise ConfigError(f"unknown mode {key!r} (expected one of {sorted(self)})")
+
+
+KL_MODES = _Modes({"k1": 0, "k2": 1, "k3": 2, "low_var_kl": 2, "full": 3})
+SYNTH = _Modes({"logp": 0, "old_delta": 1, "adv": 2, "kl": 3, "value": 4, "reward": 5})
+AGG_MODES = _Modes({"token-mean": 0, "seq-mean-token-mean": 1, "seq-mean-token-sum": 2})
 
 
 def _p(t: torch.Tensor | None) -> int | None:

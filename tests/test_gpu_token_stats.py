@@ -70,7 +70,39 @@ def test_token_stats_empty_and_errors(cuda):
     assert out[0].numel() == 0
     bad = torch.zeros((4, 36), dtype=torch.bfloat16, device=cuda)
     with pytest.raises(ConfigError):
-        ops.token_stats(bad, bad, torch.zeros(4, dtype=torch.int32, device=cuda))
+        ops.token_stats(bad, bad, torch.zeros(4, dtype=torch.int32, device=cuda), kl_mode="k9")
+
+
+@pytest.mark.parametrize("vocab", [50257, 1001, 3])
+@pytest.mark.parametrize("kl_mode", ["k3", "full"])
+def test_token_stats_any_vocab_and_alignment(cuda, vocab, kl_mode):
+    """V % 8 != 0 (GPT-2's 50,257) and unaligned row starts take the generic
+    path: same results as the oracle."""
+    rows = 40
+    g = torch.Generator(device=cuda).manual_seed(vocab)
+    pol = (torch.randn(rows, vocab, device=cuda, generator=g) * 3).to(torch.bfloat16)
+    ref = (pol.float() + 0.3 * torch.randn(rows, vocab, device=cuda, generator=g)).to(
+        torch.bfloat16)
+    tgt = torch.randint(0, vocab, (rows,), device=cuda, generator=g, dtype=torch.int32)
+    got = torch.stack(ops.token_stats(pol, ref, tgt, None, kl_mode)).cpu().numpy()
+    hp = pol.view(torch.int16).cpu().numpy().view(np.uint16)
+    hr = ref.view(torch.int16).cpu().numpy().view(np.uint16)
+    exp = O.token_stats(hp, hr, tgt.cpu().numpy(), None, kl_mode)
+    for i in range(3):  # tiny vocabularies put logp / entropy near 0: mixed bound
+        assert np.all(np.abs(got[i] - exp[i]) <= TOL * np.abs(exp[i]) + 1e-6), i
+    d = exp[1] - exp[0]
+    slope = np.abs(np.expm1(d)) if kl_mode == "k3" else 1.0
+    assert np.all(np.abs(got[3] - exp[3]) <= TOL * np.abs(exp[3]) + 1e-6 * slope + 1e-9)
+    # unaligned: a view starting one element into a buffer, aligned vocab
+    if vocab == 1001:
+        buf = torch.empty(rows * 1000 + 1, dtype=torch.bfloat16, device=cuda)
+        pv = buf[1:].view(rows, 1000)
+        pv.copy_(pol[:, :1000])
+        t2 = tgt % 1000
+        g2 = torch.stack(ops.token_stats(pv, pv, t2, None, "k3")).cpu().numpy()
+        hp2 = pv.view(torch.int16).cpu().numpy().view(np.uint16)
+        e2 = O.token_stats(hp2, hp2, t2.cpu().numpy(), None, "k3")
+        assert O.max_rel_error(g2[0], e2[0]) <= TOL and O.max_rel_error(g2[2], e2[2]) <= TOL
 
 
 def test_token_stats_masked_vocab_and_peaked_rows(cuda):
