@@ -169,7 +169,9 @@ int yatt_reduce_round_reports(const yatt_round_report* d_reports, int32_t n,
 /*       K1: -Delta   K2: Delta^2/2   K3: exp(Delta) - Delta - 1             */
 /*       FULL: sum_v p_v (log p_v - log q_v)                                 */
 /* Rows with d_mask[r] == 0 (d_mask may be NULL = all valid) are not read    */
-/* and produce zeros.  Requires vocab % 8 == 0 and 16-byte aligned tensors.  */
+/* and produce zeros.  Any vocab size / alignment; vocab % 8 == 0 with      */
+/* 16-byte aligned tensors takes the TMA streaming path, others a generic   */
+/* scalar-load path with identical results.                                 */
 /* Any output pointer may be NULL except d_logp.                             */
 /* ------------------------------------------------------------------------ */
 enum yatt_kl_mode { YATT_KL_K1 = 0, YATT_KL_K2 = 1, YATT_KL_K3 = 2, YATT_KL_FULL = 3 };

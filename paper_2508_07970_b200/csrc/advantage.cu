@@ -130,11 +130,12 @@ __global__ void __launch_bounds__(kGaeThreads) gae_kernel(
     for (int64_t hi = e; hi > b; hi -= kGaeSeg) {
       const int64_t lo = max64(b, hi - kGaeSeg);
       const int n = int(hi - lo);
-      for (int i = tid; i < n; i += kGaeThreads) {
+#pragma unroll 8
+      for (int i = tid; i < n; i += kGaeThreads) {  // unrolled: many loads in flight
         const int k = gae_slot(i);
-        sv[k] = values[lo + i];
-        sr[k] = rewards[lo + i];
-        sm[k] = mask == nullptr ? uint8_t(1) : mask[lo + i];
+        sv[k] = __ldg(values + lo + i);
+        sr[k] = __ldg(rewards + lo + i);
+        sm[k] = mask == nullptr ? uint8_t(1) : __ldg(mask + lo + i);
       }
       __syncthreads();
       // this thread's tokens [t0, t1) within the segment

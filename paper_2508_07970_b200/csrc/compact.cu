@@ -21,6 +21,7 @@ namespace yattb {
 namespace {
 
 constexpr int kScanThreads = 1024;
+constexpr int kGatherThreads = 256;  // gather_varlen_kernel block size
 constexpr int kScanPerThread = 4;
 constexpr int kScanTile = kScanThreads * kScanPerThread;
 
@@ -180,16 +181,17 @@ __global__ void gather_varlen_kernel(const T* src, const int64_t* old_cu, const 
     const int64_t b = old_cu[s], len = old_cu[s + 1] - b;
     const T* sp = src + b;
     T* dp = dst + (new_cu[j] + off);
+    // 8 independent coalesced loads in flight per thread before the stores
+    constexpr int kU = 8, kB = kGatherThreads;
     int64_t k = threadIdx.x;
-    for (; k + 3 * blockDim.x < len; k += 4 * blockDim.x) {
-      const T v0 = sp[k], v1 = sp[k + blockDim.x], v2 = sp[k + 2 * blockDim.x],
-              v3 = sp[k + 3 * blockDim.x];
-      dp[k] = v0;
-      dp[k + blockDim.x] = v1;
-      dp[k + 2 * blockDim.x] = v2;
-      dp[k + 3 * blockDim.x] = v3;
+    for (; k + (kU - 1) * kB < len; k += kU * kB) {
+      T v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) v[u] = __ldg(sp + k + u * kB);
+#pragma unroll
+      for (int u = 0; u < kU; ++u) dp[k + u * kB] = v[u];
     }
-    for (; k < len; k += blockDim.x) dp[k] = sp[k];
+    for (; k < len; k += kB) dp[k] = __ldg(sp + k);
   }
 }
 
