@@ -332,10 +332,12 @@ def run_b200(args):
 
 
 def run_e2e(args, dev, ops, cfg, ws):
-    """Same metric through the public ops API with HOST inputs: each step
-    copies one response sequence's logits (2 x 4096 x V bf16 from pinned
-    memory), targets, mask, reward group and old log-probs to the device,
-    runs A1 -> A2 -> A4 and reads the loss sums back."""
+    """Same metric through the reference-facing C-ABI call with HOST buffers
+    (yatt_grpo_step_host): each step hands pinned host logits (one prompt
+    group: 8 responses x 512 tokens = 4,096 rows, 2 x 1.25 GB bf16), targets,
+    mask, the group's rewards and old log-probs to one call that streams them
+    H2D (chunked, overlapped with A1), runs A1 -> GRPO -> A4 and returns the
+    loss sums to the host.  Wall-clock around the blocking call."""
     import torch
     rows = T
     pol, ref, tgt = ops.synth_logits(SEED, 0, rows, VOCAB, device=dev)
@@ -343,45 +345,31 @@ def run_e2e(args, dev, ops, cfg, ws):
     h_ref = ref.cpu().pin_memory()
     h_tgt = tgt.cpu().pin_memory()
     h_mask = torch.ones((rows,), dtype=torch.uint8).pin_memory()
-    h_rew = ops.synth_floats(SEED, 105, 0, RESPONSES, "reward", RESPONSES, device=dev).cpu().pin_memory()
-    h_old = torch.zeros((rows,), dtype=torch.float32).pin_memory()
-    del pol, ref, tgt
-    d_pol = torch.empty((rows, VOCAB), dtype=torch.bfloat16, device=dev)
-    d_ref = torch.empty_like(d_pol)
-    out = torch.empty((4, rows), dtype=torch.float32, device=dev)
-    cu = torch.tensor([0, rows], dtype=torch.int64, device=dev)
-    sums = torch.empty((8,), dtype=torch.float64, device=dev)
-    h_sums = torch.empty((8,), dtype=torch.float64).pin_memory()
+    h_rew = ops.synth_floats(SEED, 105, 0, RESPONSES, "reward", RESPONSES,
+                             device=dev).cpu().pin_memory()
+    logp = ops.token_stats(pol, ref, tgt, None, "k3")[0]
+    h_old = ops.synth_floats(SEED, 104, 0, rows, "old_delta", base=logp,
+                             device=dev).cpu().pin_memory()
+    del pol, ref, tgt, logp
+    torch.cuda.synchronize()
 
     def step():
-        d_pol.copy_(h_pol, non_blocking=True)
-        d_ref.copy_(h_ref, non_blocking=True)
-        d_tgt = h_tgt.to(dev, non_blocking=True)
-        d_mask = h_mask.to(dev, non_blocking=True)
-        d_rew = h_rew.to(dev, non_blocking=True)
-        d_old = h_old.to(dev, non_blocking=True)
-        ops.token_stats(d_pol, d_ref, d_tgt, d_mask, "k3", out=out)
-        adv = ops.grpo_advantages(d_rew, RESPONSES)  # the sequence's whole group
-        tadv = ops.broadcast_to_tokens(adv[:1], cu, rows, d_mask)
-        ops.policy_loss(out[0], d_old, tadv, out[3], out[2], d_mask, None, cfg, ws, sums)
-        h_sums.copy_(sums, non_blocking=True)
+        return ops.grpo_step_host(h_pol, h_ref, h_tgt, h_rew, h_old, RESPONSES, h_mask,
+                                  0, cfg, "k3")
 
     for _ in range(max(1, args.warmup)):
         step()
-    torch.cuda.synchronize()
-    st = torch.cuda.current_stream()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     k = max(2, args.steps)
-    a.record(st)
+    t0 = time.perf_counter()
     for _ in range(k):
         step()
-    b.record(st)
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / k
+    ms = (time.perf_counter() - t0) * 1e3 / k
     h2d = 2 * rows * VOCAB * 2 + rows * (4 + 1 + 4) + RESPONSES * 4
     return {"value": rows / (ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": 64, "ms_per_step": ms,
-            "sample": f"one {rows}-token response per step ({h2d / 1e9:.2f} GB H2D)"}
+            "d2h_bytes_per_step": 64, "ms_per_step": ms, "h2d_gbs": h2d / (ms / 1e3) / 1e9,
+            "api": "yatt_grpo_step_host (C ABI, host buffers)",
+            "sample": f"one prompt group of {RESPONSES} x {rows // RESPONSES} tokens per step "
+                      f"({h2d / 1e9:.2f} GB H2D from pinned memory)"}
 
 
 _JSON_OUT = None

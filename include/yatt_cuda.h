@@ -290,6 +290,21 @@ int yatt_policy_loss(const float* d_logp, const float* d_old_logp,
 double yatt_loss_finalize(const yatt_loss_sums* h_sums,
                           const yatt_loss_config* config);
 
+/* One GRPO experience step from HOST buffers (the e2e plugin call): rows =  */
+/* n_samples * T tokens (T = rows / n_samples per sample, sample-major),     */
+/* logits streamed H2D in chunks overlapped with A1, then GRPO advantages    */
+/* (groups of group_size samples, global ids from first_sample_id), token    */
+/* broadcast and the A4 loss; writes the 8 loss sums to h_sums and, if       */
+/* non-NULL, the per-token stats to h_stats [4][rows] (logp, ref_logp,       */
+/* entropy, kl).  Blocks until h_sums is valid.                              */
+int yatt_grpo_step_host(const uint16_t* h_policy_logits,
+                        const uint16_t* h_ref_logits, const int32_t* h_targets,
+                        const uint8_t* h_mask, int64_t rows, int32_t vocab,
+                        const float* h_rewards, int64_t n_samples,
+                        uint64_t first_sample_id, int32_t group_size,
+                        const float* h_old_logp, const yatt_loss_config* config,
+                        int32_t kl_mode, yatt_loss_sums* h_sums, float* h_stats);
+
 /* ------------------------------------------------------------------------ */
 /* Fused LM-head GEMM + online log-softmax on tcgen05     */
 /* logits = hidden[rows, hidden] . lm_head[vocab, hidden]^T (bf16, fp32       */

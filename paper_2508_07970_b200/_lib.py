@@ -103,6 +103,8 @@ SIGNATURES = {
                                    c_p]),
     "yatt_token_stats_host": (C.c_int, [c_p, c_p, c_p, c_p, c_i64, c_i32, c_i32, c_p, c_p, c_p,
                                         c_p]),
+    "yatt_grpo_step_host": (C.c_int, [c_p, c_p, c_p, c_p, c_i64, c_i32, c_p, c_i64, c_u64, c_i32,
+                                      c_p, P(LossConfigC), c_i32, c_p, c_p]),
     "yatt_grpo_num_local_groups": (c_i64, [c_i64, c_u64, c_i32]),
     "yatt_grpo_group_moments": (C.c_int, [c_p, c_i64, c_u64, c_i32, c_p, c_p]),
     "yatt_grpo_advantages": (C.c_int, [c_p, c_i64, c_u64, c_i32, c_f32, c_i32, c_p, c_p, c_p]),

@@ -258,6 +258,90 @@ int yatt_token_stats_host(const uint16_t* h_pol, const uint16_t* h_ref, const in
   return YATT_OK;
 }
 
+int yatt_grpo_step_host(const uint16_t* h_pol, const uint16_t* h_ref, const int32_t* h_tgt,
+                        const uint8_t* h_mask, int64_t rows, int32_t vocab,
+                        const float* h_rewards, int64_t n_samples, uint64_t first_id, int32_t G,
+                        const float* h_old, const yatt_loss_config* cfg, int32_t kl_mode,
+                        yatt_loss_sums* h_sums, float* h_stats) {
+  YATT_REQUIRE(vocab > 0 && rows > 0 && n_samples > 0 && rows % n_samples == 0, YATT_ERR_CONFIG,
+               "grpo_step: rows must be a positive multiple of n_samples");
+  YATT_REQUIRE(h_pol && h_ref && h_tgt && h_rewards && h_old && cfg && h_sums, YATT_ERR_CONFIG,
+               "grpo_step: null argument");
+  const int64_t T = rows / n_samples;
+  const int64_t row_bytes = int64_t(vocab) * 2;
+  const int64_t chunk = max64(1, min64(rows, (int64_t(128) << 20) / row_bytes));
+  struct Slot {
+    DevBuf pol, ref, tgt;
+    cudaStream_t st = nullptr;
+  };
+  static thread_local Slot slots[2];
+  static thread_local DevBuf stats, mask, rew, adv, tadv, old, cu, sums, ws;
+  for (Slot& s : slots) {
+    if (!s.st) YATT_TRY_CUDA(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
+    int rc = s.pol.reserve(size_t(chunk * row_bytes));
+    if (!rc) rc = s.ref.reserve(size_t(chunk * row_bytes));
+    if (!rc) rc = s.tgt.reserve(size_t(chunk) * 4);
+    if (rc) return rc;
+  }
+  int rc = stats.reserve(size_t(rows) * 16);
+  if (!rc) rc = mask.reserve(size_t(rows));
+  if (!rc) rc = rew.reserve(size_t(n_samples) * 4);
+  if (!rc) rc = adv.reserve(size_t(n_samples) * 4);
+  if (!rc) rc = tadv.reserve(size_t(rows) * 4);
+  if (!rc) rc = old.reserve(size_t(rows) * 4);
+  if (!rc) rc = cu.reserve(size_t(n_samples + 1) * 8);
+  if (!rc) rc = sums.reserve(sizeof(yatt_loss_sums));
+  if (!rc) rc = ws.reserve(loss_workspace_bytes());
+  if (rc) return rc;
+  float* st4 = static_cast<float*>(stats.p);
+  uint8_t* dmask = static_cast<uint8_t*>(mask.p);
+  // 1. stream the logits through two staging slots, A1 into the stats arrays
+  int k = 0;
+  for (int64_t r0 = 0; r0 < rows; r0 += chunk, k ^= 1) {
+    Slot& s = slots[k];
+    const int64_t n = min64(chunk, rows - r0);
+    YATT_TRY_CUDA(cudaMemcpyAsync(s.pol.p, h_pol + r0 * vocab, size_t(n * row_bytes),
+                                  cudaMemcpyHostToDevice, s.st));
+    YATT_TRY_CUDA(cudaMemcpyAsync(s.ref.p, h_ref + r0 * vocab, size_t(n * row_bytes),
+                                  cudaMemcpyHostToDevice, s.st));
+    YATT_TRY_CUDA(cudaMemcpyAsync(s.tgt.p, h_tgt + r0, size_t(n) * 4, cudaMemcpyHostToDevice, s.st));
+    if (h_mask)
+      YATT_TRY_CUDA(cudaMemcpyAsync(dmask + r0, h_mask + r0, size_t(n), cudaMemcpyHostToDevice,
+                                    s.st));
+    else
+      YATT_TRY_CUDA(cudaMemsetAsync(dmask + r0, 1, size_t(n), s.st));
+    rc = token_stats_launch(static_cast<uint16_t*>(s.pol.p), static_cast<uint16_t*>(s.ref.p),
+                            static_cast<int32_t*>(s.tgt.p), dmask + r0, n, vocab, kl_mode,
+                            st4 + r0, st4 + rows + r0, st4 + 2 * rows + r0, st4 + 3 * rows + r0,
+                            s.st);
+    if (rc) return rc;
+  }
+  YATT_TRY_CUDA(cudaStreamSynchronize(slots[1].st));
+  cudaStream_t st = slots[0].st;
+  // 2. GRPO advantages -> tokens -> loss sums
+  std::vector<int64_t> hcu(static_cast<size_t>(n_samples + 1));
+  for (int64_t i = 0; i <= n_samples; ++i) hcu[size_t(i)] = i * T;
+  YATT_TRY_CUDA(cudaMemcpyAsync(rew.p, h_rewards, size_t(n_samples) * 4, cudaMemcpyHostToDevice, st));
+  YATT_TRY_CUDA(cudaMemcpyAsync(old.p, h_old, size_t(rows) * 4, cudaMemcpyHostToDevice, st));
+  YATT_TRY_CUDA(cudaMemcpyAsync(cu.p, hcu.data(), hcu.size() * 8, cudaMemcpyHostToDevice, st));
+  rc = grpo_adv_launch(static_cast<float*>(rew.p), n_samples, first_id, G, 1e-6f, 1, nullptr,
+                       static_cast<float*>(adv.p), st);
+  if (!rc)
+    rc = broadcast_launch(static_cast<float*>(adv.p), static_cast<int64_t*>(cu.p), n_samples, dmask,
+                          static_cast<float*>(tadv.p), st);
+  if (!rc)
+    rc = policy_loss_launch(st4, static_cast<float*>(old.p), static_cast<float*>(tadv.p),
+                            st4 + 3 * rows, st4 + 2 * rows, dmask, rows,
+                            static_cast<int64_t*>(cu.p), n_samples, cfg,
+                            static_cast<yatt_loss_sums*>(sums.p), ws.p, ws.bytes, st);
+  if (rc) return rc;
+  YATT_TRY_CUDA(cudaMemcpyAsync(h_sums, sums.p, sizeof(yatt_loss_sums), cudaMemcpyDeviceToHost, st));
+  if (h_stats)
+    YATT_TRY_CUDA(cudaMemcpyAsync(h_stats, st4, size_t(rows) * 16, cudaMemcpyDeviceToHost, st));
+  YATT_TRY_CUDA(cudaStreamSynchronize(st));
+  return YATT_OK;
+}
+
 int64_t yatt_grpo_num_local_groups(int64_t n, uint64_t first_id, int32_t G) {
   return grpo_num_local_groups(n, first_id, G);
 }

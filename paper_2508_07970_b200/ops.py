@@ -88,6 +88,24 @@ def token_stats_host(policy: np.ndarray, ref: np.ndarray, targets: np.ndarray,
     return out
 
 
+def grpo_step_host(policy, ref, targets, rewards, old_logp, group_size: int, mask=None,
+                   first_sample_id: int = 0, config: LossConfigC | None = None,
+                   kl_mode: str = "k3", stats_out=None):
+    """One GRPO experience step through the C ABI from HOST buffers (numpy or
+    CPU torch tensors, pinned for full PCIe speed): returns the 8 loss sums."""
+    def ptr(a):
+        if a is None:
+            return None
+        return a.data_ptr() if isinstance(a, torch.Tensor) else a.ctypes.data
+    rows, vocab = policy.shape
+    sums = LossSumsC()
+    check(lib().yatt_grpo_step_host(ptr(policy), ptr(ref), ptr(targets), ptr(mask), rows, vocab,
+                                    ptr(rewards), len(rewards), first_sample_id, group_size,
+                                    ptr(old_logp), C.byref(config or loss_config()),
+                                    KL_MODES[kl_mode], C.byref(sums), ptr(stats_out)))
+    return [getattr(sums, f) for f, _ in LossSumsC._fields_]
+
+
 # ------------------------------------------------------------ synthetic ----
 def synth_logits(seed: int, row0: int, rows: int, vocab: int, device="cuda", out=None):
     if out is None:

@@ -160,6 +160,26 @@ def test_policy_loss_config_errors(cuda):
         ops.policy_loss(logp, old, adv, kl, ent, config=ops.loss_config(agg_mode=1))
 
 
+def test_grpo_step_host_matches_device_pipeline(cuda):
+    """yatt_grpo_step_host (host buffers, one C-ABI call) == the same ops
+    composed on the device."""
+    R, T, V, seed = 8, 96, 32000, 5
+    rows = R * T
+    pol, ref, tgt = ops.synth_logits(seed, 0, rows, V, device=cuda)
+    rew = ops.synth_floats(seed, 105, 0, R, "reward", R, device=cuda)
+    logp, rlogp, ent, kl = ops.token_stats(pol, ref, tgt, None, "k3")
+    old = ops.synth_floats(seed, 104, 0, rows, "old_delta", base=logp, device=cuda)
+    cu = torch.arange(R + 1, dtype=torch.int64, device=cuda) * T
+    tadv = ops.broadcast_to_tokens(ops.grpo_advantages(rew, R), cu, rows)
+    cfg = ops.loss_config(0.2, 0.28, 0.0, 0.01, 0.001)
+    dev_sums = ops.policy_loss(logp, old, tadv, kl, ent, None, None, cfg).cpu().numpy()
+    stats = np.empty((4, rows), dtype=np.float32)
+    host_sums = ops.grpo_step_host(pol.cpu(), ref.cpu(), tgt.cpu(), rew.cpu(), old.cpu(), R,
+                                   None, 0, cfg, "k3", stats)
+    assert O.max_rel_error(np.array(host_sums), dev_sums) <= 1e-12
+    assert np.array_equal(stats, torch.stack([logp, rlogp, ent, kl]).cpu().numpy())
+
+
 # ------------------------------------------------------ end-to-end, cfg 1 ---
 def test_config1_experience_pipeline_matches_oracle(cuda):
     """BASELINE configs[0]: 16 prompts x 8 responses, T=256, V=32000 —
