@@ -102,6 +102,37 @@ struct LseState {
   double s, w;    // sum 2^a, sum 2^a * a (fp64 across the ~5K chunks of a row)
 };
 
+__device__ __forceinline__ void tma_load_2d_mcast(void* dst, const CUtensorMap* map, int x, int y,
+                                                  uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_mcast(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+// kCluster = 2: CTA pairs on adjacent row tiles (cluster dims 1x2) share the
+// weight tile: each loads its own hidden tile and HALF of the weight tile,
+// multicast into both CTAs' shared memory (a third less L2->SM traffic per
+// CTA); a ring stage is reused only after BOTH CTAs' MMAs retired it
+// (multicast tcgen05.commit, empty barriers count 2).
+template <int kCluster>
 __global__ void __launch_bounds__(kGemmThreads, 1) lmhead_lse_kernel(
     const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
     int64_t rows, int32_t V, int32_t d, int32_t v_per_split, float4* partial) {
@@ -123,7 +154,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) lmhead_lse_kernel(
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStagesG; ++s) {
       mbar_init(&bars->full[s], 1);
-      mbar_init(&bars->empty[s], 1);
+      mbar_init(&bars->empty[s], kCluster);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&bars->tfull[a], 1);
@@ -142,8 +173,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) lmhead_lse_kernel(
   }
   tc_fence_before();
   __syncthreads();
+  if (kCluster > 1) cluster_sync_all();  // peer barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
+  const uint32_t crank = kCluster > 1 ? cluster_rank() : 0u;
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer ----
@@ -156,7 +189,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) lmhead_lse_kernel(
           mbar_arrive_expect_tx(&bars->full[stage], kStageBytes);
           uint8_t* sa = smem + size_t(stage) * kStageBytes;
           tma_load_2d(sa, &tmA, kb * BK, int(m0), &bars->full[stage]);
-          tma_load_2d(sa + kABytes, &tmB, kb * BK, n0, &bars->full[stage]);
+          if (kCluster > 1)  // my half of the weight tile, into both CTAs
+            tma_load_2d_mcast(sa + kABytes + crank * (kBBytes / 2), &tmB, kb * BK,
+                              n0 + int(crank) * (BN / 2), &bars->full[stage], uint16_t(0x3));
+          else
+            tma_load_2d(sa + kABytes, &tmB, kb * BK, n0, &bars->full[stage]);
           if (++stage == kStagesG) {
             stage = 0;
             phase ^= 1u;
@@ -186,7 +223,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) lmhead_lse_kernel(
             umma(tmem_d, adesc + uint64_t(2 * kk), bdesc + uint64_t(2 * kk),
                  (kb | kk) != 0 ? 1u : 0u);
           }
-          umma_commit(&bars->empty[stage]);  // stage free once these MMAs retire
+          if (kCluster > 1)  // stage free once BOTH CTAs' MMAs retired it
+            umma_commit_mcast(&bars->empty[stage], uint16_t(0x3));
+          else
+            umma_commit(&bars->empty[stage]);
           if (++stage == kStagesG) {
             stage = 0;
             phase ^= 1u;
@@ -252,6 +292,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) lmhead_lse_kernel(
     }
   }
   __syncthreads();
+  if (kCluster > 1) cluster_sync_all();  // no remote arrivals/writes pending on exit
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
@@ -352,24 +393,54 @@ int lmhead_token_stats_launch(const uint16_t* hidden, const uint16_t* W, const i
   YATT_REQUIRE((reinterpret_cast<uintptr_t>(hidden) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(W) & 15) == 0,
                YATT_ERR_CONFIG, "lmhead: operands must be 16-byte aligned");
+  // Single CTAs by default; YATT_LMHEAD_CLUSTER=2 selects CTA pairs sharing
+  // weight tiles through TMA multicast.  Measured (profiles/r1_lmhead_*):
+  // the 1-CTA kernel is already tensor-bound (93% pipe active) after the
+  // split-fastest rasterisation, and pairing adds lock-step coupling
+  // (1,261 vs 1,296 TFLOP/s at 32K rows), so the pair path stays opt-in.
+  static const int cluster = [] {
+    const char* e = getenv("YATT_LMHEAD_CLUSTER");
+    return (e && e[0] == '2') ? 2 : 1;
+  }();
   CUtensorMap ta, tb;
   int rc = make_map(&ta, hidden, rows, d, BM);
-  if (!rc) rc = make_map(&tb, W, V, d, BN);
+  if (!rc) rc = make_map(&tb, W, V, d, cluster == 2 ? BN / 2 : BN);
   if (rc) return rc;
   int v_per_split = int(ceil_div(ceil_div(V, nsplit), BN) * BN);
   const int nsplit_eff = int(ceil_div(V, v_per_split));
   static bool attr = false;
   if (!attr) {
-    YATT_TRY_CUDA(cudaFuncSetAttribute(lmhead_lse_kernel,
+    YATT_TRY_CUDA(cudaFuncSetAttribute(lmhead_lse_kernel<1>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(kGemmSmem)));
+    YATT_TRY_CUDA(cudaFuncSetAttribute(lmhead_lse_kernel<2>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(kGemmSmem)));
     attr = true;
   }
-  YATT_REQUIRE(ceil_div(rows, BM) <= 65535, YATT_ERR_CONFIG, "lmhead: too many rows per launch");
-  dim3 grid(unsigned(nsplit_eff), unsigned(ceil_div(rows, BM)));
+  const int64_t mtiles = ceil_div(ceil_div(rows, BM), cluster) * cluster;
+  YATT_REQUIRE(mtiles <= 65535, YATT_ERR_CONFIG, "lmhead: too many rows per launch");
+  const dim3 grid{unsigned(nsplit_eff), unsigned(mtiles), 1u};
   float4* partial = static_cast<float4*>(ws);
-  lmhead_lse_kernel<<<grid, kGemmThreads, kGemmSmem, st>>>(ta, tb, rows, V, d, v_per_split,
-                                                           partial);
+  if (cluster == 2) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = grid;
+    lc.blockDim = dim3(kGemmThreads);
+    lc.dynamicSmemBytes = kGemmSmem;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 1;
+    at[0].val.clusterDim.y = 2;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    YATT_TRY_CUDA(cudaLaunchKernelEx(&lc, lmhead_lse_kernel<2>, ta, tb, rows, V, d, v_per_split,
+                                     partial));
+  } else {
+    lmhead_lse_kernel<1><<<grid, kGemmThreads, kGemmSmem, st>>>(ta, tb, rows, V, d, v_per_split,
+                                                                partial);
+  }
   rc = check_launch("lmhead_lse_kernel");
   if (rc) return rc;
   lmhead_combine_kernel<<<unsigned(ceil_div(rows * 32, 256)), 256, 0, st>>>(

@@ -69,6 +69,30 @@ def test_lmhead_policy_and_reference_kl(cuda):
     assert np.all(np.abs(kl - exp) <= 1e-5 * np.abs(exp) + 1e-6 * np.abs(np.expm1(dlt)) + 1e-9)
 
 
+def test_lmhead_cluster_multicast_variant(cuda):
+    """The CTA-pair / TMA-multicast variant (YATT_LMHEAD_CLUSTER=2) gives the
+    same results (separate process: the mode is read once per process)."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, '.');"
+            "import torch, numpy as np; from paper_2508_07970_b200 import ops;"
+            "g=torch.Generator(device='cuda').manual_seed(3);"
+            "h=torch.randn(300,512,device='cuda',generator=g).to(torch.bfloat16);"
+            "w=(torch.randn(4100,512,device='cuda',generator=g)*0.06).to(torch.bfloat16);"
+            "y=torch.randint(0,4100,(300,),device='cuda',generator=g,dtype=torch.int32);"
+            "o=torch.stack(ops.lmhead_token_stats(h,w,y,n_split=3)).cpu().numpy();"
+            "np.save(sys.argv[1], o)")
+    import os
+    import tempfile
+    outs = []
+    for mode in ("1", "2"):
+        f = tempfile.mktemp(suffix=".npy")
+        subprocess.run([sys.executable, "-c", code, f], check=True, timeout=120,
+                       env={**os.environ, "YATT_LMHEAD_CLUSTER": mode})
+        outs.append(np.load(f))
+    assert np.allclose(outs[0], outs[1], rtol=1e-6, atol=1e-6)
+
+
 def test_lmhead_errors(cuda):
     h = torch.zeros((4, 12), dtype=torch.bfloat16, device=cuda)
     w = torch.zeros((16, 12), dtype=torch.bfloat16, device=cuda)
