@@ -108,6 +108,19 @@ int num_sms() {
   return cache[dev];
 }
 
+int ensure_dynamic_smem(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;
+  int dev = 0;
+  YATT_TRY_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  for (const auto& d : done)
+    if (d.first == kernel && d.second == dev) return YATT_OK;
+  YATT_TRY_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.emplace_back(kernel, dev);
+  return YATT_OK;
+}
+
 // Grow-only device buffer cache for the host-buffer entry points.
 namespace {
 struct DevBuf {

@@ -37,6 +37,10 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // Number of SMs of the current device (cached per device).
 int num_sms();
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// function attributes live in each device's context.
+int ensure_dynamic_smem(const void* kernel, int bytes);
+
 // ---------------------------------------------------------------------------
 // Keyed RNG — common.hpp:17-37 (splitmix64, hash_key, uniform_from_key)
 // ---------------------------------------------------------------------------

@@ -408,16 +408,14 @@ int lmhead_token_stats_launch(const uint16_t* hidden, const uint16_t* W, const i
   if (rc) return rc;
   int v_per_split = int(ceil_div(ceil_div(V, nsplit), BN) * BN);
   const int nsplit_eff = int(ceil_div(V, v_per_split));
-  static bool attr = false;
-  if (!attr) {
-    YATT_TRY_CUDA(cudaFuncSetAttribute(lmhead_lse_kernel<1>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(kGemmSmem)));
-    YATT_TRY_CUDA(cudaFuncSetAttribute(lmhead_lse_kernel<2>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(kGemmSmem)));
-    attr = true;
-  }
+  {
+      const int rc_ = ensure_dynamic_smem(reinterpret_cast<const void*>(lmhead_lse_kernel<1>), int(kGemmSmem));
+      if (rc_) return rc_;
+    }
+    {
+      const int rc_ = ensure_dynamic_smem(reinterpret_cast<const void*>(lmhead_lse_kernel<2>), int(kGemmSmem));
+      if (rc_) return rc_;
+    }
   const int64_t mtiles = ceil_div(ceil_div(rows, BM), cluster) * cluster;
   YATT_REQUIRE(mtiles <= 65535, YATT_ERR_CONFIG, "lmhead: too many rows per launch");
   const dim3 grid{unsigned(nsplit_eff), unsigned(mtiles), 1u};

@@ -342,20 +342,16 @@ int logits_backward_launch(const uint16_t* pol, const uint16_t* ref, const int32
   const int grid = int(min64(rows, int64_t(2) * num_sms()));
   if (full_kl) {
     constexpr size_t smem = size_t(stages_of<true>()) * 2 * kTile * 2 + sizeof(BwdTail);
-    static bool attr = false;
-    if (!attr) {
-      YATT_TRY_CUDA(cudaFuncSetAttribute(logits_backward_kernel<true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      attr = true;
+    {
+      const int rc_ = ensure_dynamic_smem(reinterpret_cast<const void*>(logits_backward_kernel<true>), int(smem));
+      if (rc_) return rc_;
     }
     logits_backward_kernel<true><<<grid, kThreads, smem, st>>>(prm);
   } else {
     constexpr size_t smem = size_t(stages_of<false>()) * kTile * 2 + sizeof(BwdTail);
-    static bool attr = false;
-    if (!attr) {
-      YATT_TRY_CUDA(cudaFuncSetAttribute(logits_backward_kernel<false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      attr = true;
+    {
+      const int rc_ = ensure_dynamic_smem(reinterpret_cast<const void*>(logits_backward_kernel<false>), int(smem));
+      if (rc_) return rc_;
     }
     logits_backward_kernel<false><<<grid, kThreads, smem, st>>>(prm);
   }

@@ -568,21 +568,15 @@ int token_stats_launch(const uint16_t* pol, const uint16_t* ref, const int32_t* 
   }
   const int grid = int(min64(rows, int64_t(2) * num_sms()));
   if (kl_mode == YATT_KL_FULL) {
-    static bool attr_full = false;
-    if (!attr_full) {
-      YATT_TRY_CUDA(cudaFuncSetAttribute(token_stats_kernel<true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(kSmemBytes)));
-      attr_full = true;
+    {
+      const int rc_ = ensure_dynamic_smem(reinterpret_cast<const void*>(token_stats_kernel<true>), int(kSmemBytes));
+      if (rc_) return rc_;
     }
     token_stats_kernel<true><<<grid, kThreads, kSmemBytes, st>>>(p);
   } else {
-    static bool attr = false;
-    if (!attr) {
-      YATT_TRY_CUDA(cudaFuncSetAttribute(token_stats_kernel<false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(kSmemBytes)));
-      attr = true;
+    {
+      const int rc_ = ensure_dynamic_smem(reinterpret_cast<const void*>(token_stats_kernel<false>), int(kSmemBytes));
+      if (rc_) return rc_;
     }
     token_stats_kernel<false><<<grid, kThreads, kSmemBytes, st>>>(p);
   }
