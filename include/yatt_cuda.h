@@ -16,6 +16,11 @@
  *  - bf16 tensors are passed as uint16_t bit patterns.
  *  - Reentrant given distinct buffers and streams; the last-error message is
  *    thread-local.
+ *  - Every pointer must be naturally aligned for its element type (structs:
+ *    8 bytes; workspaces: 8, the LM-head one 16); the logits-backward `coef`
+ *    table and the policy/ref/grad logits of the TMA kernels need 16 bytes.
+ *    A misaligned pointer returns YATT_ERR_CONFIG before any launch.
+ *    yatt_token_stats alone accepts 2-byte-aligned logits (generic path).
  */
 #ifndef YATT_CUDA_H_
 #define YATT_CUDA_H_

@@ -142,6 +142,20 @@ struct DevBuf {
 
 using namespace yattb;
 
+// Natural-alignment contract of every pointer argument (the kernels issue
+// vector / 64-bit accesses): a misaligned pointer is a YATT_ERR_CONFIG, not a
+// device fault that poisons the context.  Null pointers pass (optional args).
+#define YATT_ALIGNED(fn, ptr, a)                                                          \
+  YATT_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & uintptr_t((a) - 1)) == 0, YATT_ERR_CONFIG, \
+               "%s: %s must be %d-byte aligned", fn, #ptr, int(a))
+#define YATT_ALIGNED4(fn, a, b, c, d) \
+  do {                                \
+    YATT_ALIGNED(fn, a, 4);           \
+    YATT_ALIGNED(fn, b, 4);           \
+    YATT_ALIGNED(fn, c, 4);           \
+    YATT_ALIGNED(fn, d, 4);           \
+  } while (0)
+
 extern "C" {
 
 const char* yatt_last_error_message(void) { return yattb::g_err; }
@@ -175,18 +189,24 @@ int yatt_shard_dataset(uint64_t total, int32_t p, int32_t r, uint64_t* begin, ui
 int yatt_sample_lengths_keyed(const yatt_length_dist* d, uint64_t seed, uint64_t stream_id,
                               uint64_t step, uint64_t round, const uint64_t* ids, int64_t n,
                               int32_t* out, void* stream) {
+  YATT_ALIGNED("sample_lengths_keyed", ids, 8);
+  YATT_ALIGNED("sample_lengths_keyed", out, 4);
   return lengths_launch(d, seed, stream_id, step, round, ids, n, out, as_stream(stream));
 }
 
 int yatt_rejection_flags(const yatt_sample* s, int64_t n, int32_t step, int32_t round,
                          const yatt_rejection_config* c, uint64_t seed, uint8_t* out,
                          void* stream) {
+  YATT_ALIGNED("rejection_flags", s, 8);
   return rejection_launch(s, n, step, round, c, seed, out, as_stream(stream));
 }
 
 int yatt_shard_round(yatt_sample* samples, const int64_t* h_off, int32_t nshards,
                      int32_t first_rank, int32_t step, int32_t round, const yatt_round_params* p,
                      yatt_round_report* reports, yatt_mb_agg* mbs, void* stream) {
+  YATT_ALIGNED("shard_round", samples, 8);
+  YATT_ALIGNED("shard_round", reports, 8);
+  YATT_ALIGNED("shard_round", mbs, 8);
   return shard_round_launch(samples, h_off, nshards, first_rank, step, round, p, reports, mbs,
                             as_stream(stream));
 }
@@ -198,22 +218,31 @@ size_t yatt_lmhead_workspace_bytes(int64_t rows, int32_t vocab, int32_t n_split)
 int yatt_lmhead_token_stats(const uint16_t* hidden, const uint16_t* w, const int32_t* tgt,
                             int64_t rows, int32_t d, int32_t vocab, int32_t n_split, float* logp,
                             float* ent, float* lse, void* ws, size_t ws_bytes, void* stream) {
+  YATT_ALIGNED4("lmhead_token_stats", tgt, logp, ent, lse);
+  YATT_ALIGNED("lmhead_token_stats", ws, 16);
   return lmhead_token_stats_launch(hidden, w, tgt, rows, d, vocab, n_split, logp, ent, lse, ws,
                                    ws_bytes, as_stream(stream));
 }
 
 int yatt_kl_from_logps(const float* logp, const float* ref_logp, int64_t n, int32_t mode,
                        float* kl, void* stream) {
+  YATT_ALIGNED4("kl_from_logps", logp, ref_logp, kl, nullptr);
   return kl_from_logps_launch(logp, ref_logp, n, mode, kl, as_stream(stream));
 }
 
 int yatt_reduce_round_reports(const yatt_round_report* r, int32_t n, int64_t* out, void* stream) {
+  YATT_ALIGNED("reduce_round_reports", r, 8);
+  YATT_ALIGNED("reduce_round_reports", out, 8);
   return reduce_reports_launch(r, n, out, as_stream(stream));
 }
 
 int yatt_token_stats(const uint16_t* pol, const uint16_t* ref, const int32_t* tgt,
                      const uint8_t* mask, int64_t rows, int32_t vocab, int32_t kl_mode,
                      float* logp, float* ref_logp, float* ent, float* kl, void* stream) {
+  YATT_ALIGNED4("token_stats", logp, ref_logp, ent, kl);
+  YATT_ALIGNED("token_stats", tgt, 4);
+  YATT_ALIGNED("token_stats", pol, 2);
+  YATT_ALIGNED("token_stats", ref, 2);
   return token_stats_launch(pol, ref, tgt, mask, rows, vocab, kl_mode, logp, ref_logp, ent, kl,
                             as_stream(stream));
 }
@@ -361,22 +390,30 @@ int64_t yatt_grpo_num_local_groups(int64_t n, uint64_t first_id, int32_t G) {
 
 int yatt_grpo_group_moments(const float* r, int64_t n, uint64_t first_id, int32_t G, double* out,
                             void* stream) {
+  YATT_ALIGNED("grpo_group_moments", r, 4);
+  YATT_ALIGNED("grpo_group_moments", out, 8);
   return grpo_moments_launch(r, n, first_id, G, out, as_stream(stream));
 }
 
 int yatt_grpo_advantages(const float* r, int64_t n, uint64_t first_id, int32_t G, float eps,
                          int32_t norm_by_std, const double* moments, float* adv, void* stream) {
+  YATT_ALIGNED4("grpo_advantages", r, adv, nullptr, nullptr);
+  YATT_ALIGNED("grpo_advantages", moments, 8);
   return grpo_adv_launch(r, n, first_id, G, eps, norm_by_std, moments, adv, as_stream(stream));
 }
 
 int yatt_broadcast_to_tokens(const float* vals, const int64_t* cu, int64_t nsamples,
                              const uint8_t* mask, float* out, int64_t n_tokens, void* stream) {
+  YATT_ALIGNED4("broadcast_to_tokens", vals, out, nullptr, nullptr);
+  YATT_ALIGNED("broadcast_to_tokens", cu, 8);
   (void)n_tokens;
   return broadcast_launch(vals, cu, nsamples, mask, out, as_stream(stream));
 }
 
 int yatt_gae(const float* values, const float* rewards, const uint8_t* mask, const int64_t* cu,
              int64_t nseq, float gamma, float lam, float* adv, float* ret, void* stream) {
+  YATT_ALIGNED4("gae", values, rewards, adv, ret);
+  YATT_ALIGNED("gae", cu, 8);
   return gae_launch(values, rewards, mask, cu, nseq, gamma, lam, adv, ret, as_stream(stream));
 }
 
@@ -384,6 +421,9 @@ size_t yatt_masked_moments_workspace_bytes(void) { return moments_workspace_byte
 
 int yatt_masked_moments(const float* x, const uint8_t* mask, int64_t n, double* out, void* ws,
                         size_t ws_bytes, void* stream) {
+  YATT_ALIGNED("masked_moments", x, 4);
+  YATT_ALIGNED("masked_moments", out, 8);
+  YATT_ALIGNED("masked_moments", ws, 8);
   YATT_REQUIRE(ws != nullptr && ws_bytes >= moments_workspace_bytes(), YATT_ERR_WORKSPACE,
                "masked_moments: workspace too small");
   return masked_moments_launch(x, mask, n, out, static_cast<double*>(ws), as_stream(stream));
@@ -391,6 +431,8 @@ int yatt_masked_moments(const float* x, const uint8_t* mask, int64_t n, double* 
 
 int yatt_whiten(float* x, const uint8_t* mask, int64_t n, const double* mom, int32_t shift,
                 void* stream) {
+  YATT_ALIGNED("whiten", x, 4);
+  YATT_ALIGNED("whiten", mom, 8);
   return whiten_launch(x, mask, n, mom, shift, as_stream(stream));
 }
 
@@ -402,6 +444,11 @@ int yatt_policy_loss(const float* logp, const float* old_logp, const float* adv,
                      const float* ent, const uint8_t* mask, int64_t n, const int64_t* cu,
                      int64_t nseq, const yatt_loss_config* cfg, yatt_loss_sums* sums, void* ws,
                      size_t ws_bytes, void* stream) {
+  YATT_ALIGNED4("policy_loss", logp, old_logp, adv, kl);
+  YATT_ALIGNED("policy_loss", ent, 4);
+  YATT_ALIGNED("policy_loss", cu, 8);
+  YATT_ALIGNED("policy_loss", sums, 8);
+  YATT_ALIGNED("policy_loss", ws, 8);
   return policy_loss_launch(logp, old_logp, adv, kl, ent, mask, n, cu, nseq, cfg, sums, ws,
                             ws_bytes, as_stream(stream));
 }
@@ -416,6 +463,10 @@ int yatt_policy_grad_coef(const uint16_t* pol, const uint16_t* ref, const int32_
                           const uint8_t* mask, int64_t n, int32_t vocab, const int64_t* cu,
                           int64_t nseq, const yatt_loss_config* cfg, int32_t kl_mode,
                           double norm, float* coef, void* stream) {
+  YATT_ALIGNED4("policy_grad_coef", logp, ref_logp, old_logp, adv);
+  YATT_ALIGNED4("policy_grad_coef", ent, kl, tgt, nullptr);
+  YATT_ALIGNED("policy_grad_coef", cu, 8);
+  YATT_ALIGNED("policy_grad_coef", coef, 16);
   return grad_coef_launch(pol, ref, tgt, logp, ref_logp, old_logp, adv, ent, kl, mask, n, vocab,
                           cu, nseq, cfg, kl_mode, norm, coef, as_stream(stream));
 }
@@ -423,6 +474,8 @@ int yatt_policy_grad_coef(const uint16_t* pol, const uint16_t* ref, const int32_
 int yatt_logits_backward(const uint16_t* pol, const uint16_t* ref, const int32_t* tgt,
                          const uint8_t* mask, int64_t rows, int32_t vocab, const float* coef,
                          int32_t full_kl, uint16_t* grad, void* stream) {
+  YATT_ALIGNED("logits_backward", tgt, 4);
+  YATT_ALIGNED("logits_backward", coef, 16);
   return logits_backward_launch(pol, ref, tgt, mask, rows, vocab, coef, full_kl, grad,
                                 as_stream(stream));
 }
@@ -432,6 +485,11 @@ size_t yatt_filter_compact_workspace_bytes(int64_t n) { return compact_workspace
 int yatt_filter_compact(const float* r, const int64_t* lens, int64_t n, int32_t G, uint8_t* keep,
                         int32_t* map, int64_t* new_cu, int64_t* counts, void* ws, size_t ws_bytes,
                         void* stream) {
+  YATT_ALIGNED4("filter_compact", r, map, nullptr, nullptr);
+  YATT_ALIGNED("filter_compact", lens, 8);
+  YATT_ALIGNED("filter_compact", new_cu, 8);
+  YATT_ALIGNED("filter_compact", counts, 8);
+  YATT_ALIGNED("filter_compact", ws, 8);
   return filter_compact_launch(r, lens, n, G, keep, map, new_cu, counts, ws, ws_bytes,
                                as_stream(stream));
 }
@@ -439,6 +497,11 @@ int yatt_filter_compact(const float* r, const int64_t* lens, int64_t n, int32_t 
 int yatt_gather_varlen(const void* src, const int64_t* old_cu, const int32_t* map,
                        const int64_t* new_cu, const int64_t* d_n_kept, int64_t max_kept,
                        const int64_t* d_dst_offset, int32_t elem_bytes, void* dst, void* stream) {
+  YATT_ALIGNED("gather_varlen", old_cu, 8);
+  YATT_ALIGNED("gather_varlen", map, 4);
+  YATT_ALIGNED("gather_varlen", new_cu, 8);
+  YATT_ALIGNED("gather_varlen", d_n_kept, 8);
+  YATT_ALIGNED("gather_varlen", d_dst_offset, 8);
   return gather_varlen_launch(src, old_cu, map, new_cu, d_n_kept, max_kept, d_dst_offset,
                               elem_bytes, dst, as_stream(stream));
 }
@@ -446,6 +509,9 @@ int yatt_gather_varlen(const void* src, const int64_t* old_cu, const int32_t* ma
 int yatt_gather_rows(const void* src, const int32_t* map, const int64_t* d_n_kept,
                      int64_t max_kept, int64_t row_bytes, const int64_t* d_dst_offset, void* dst,
                      void* stream) {
+  YATT_ALIGNED("gather_rows", map, 4);
+  YATT_ALIGNED("gather_rows", d_n_kept, 8);
+  YATT_ALIGNED("gather_rows", d_dst_offset, 8);
   return gather_rows_launch(src, map, d_n_kept, max_kept, row_bytes, d_dst_offset, dst,
                             as_stream(stream));
 }
@@ -453,11 +519,16 @@ int yatt_gather_rows(const void* src, const int32_t* map, const int64_t* d_n_kep
 int yatt_microbatch_aggregates(const int32_t* plen, const int32_t* olen, const int64_t* d_n,
                                int64_t n, int32_t mb, int32_t rank, yatt_mb_agg* out,
                                void* stream) {
+  YATT_ALIGNED4("microbatch_aggregates", plen, olen, nullptr, nullptr);
+  YATT_ALIGNED("microbatch_aggregates", d_n, 8);
+  YATT_ALIGNED("microbatch_aggregates", out, 8);
   return microbatch_launch(plen, olen, d_n, n, mb, rank, out, as_stream(stream));
 }
 
 int yatt_exclusive_offset(const int64_t* d_counts, int32_t nranks, int32_t rank, int32_t stride,
                           int32_t field, int64_t* d_out, void* stream) {
+  YATT_ALIGNED("exclusive_offset", d_counts, 8);
+  YATT_ALIGNED("exclusive_offset", d_out, 8);
   return exclusive_offset_launch(d_counts, nranks, rank, stride, field, d_out, as_stream(stream));
 }
 
@@ -465,6 +536,8 @@ size_t yatt_sort_order_workspace_bytes(int64_t n) { return sort_workspace_bytes(
 
 int yatt_sort_order_desc(const int32_t* len, int64_t n, uint32_t* order, void* ws,
                          size_t ws_bytes, void* stream) {
+  YATT_ALIGNED4("sort_order_desc", len, order, nullptr, nullptr);
+  YATT_ALIGNED("sort_order_desc", ws, 8);
   return sort_order_launch(len, n, order, ws, ws_bytes, as_stream(stream));
 }
 
@@ -507,11 +580,15 @@ int yatt_sort_and_bucket_host(const int32_t* h_len, int64_t n, int32_t B, uint64
 
 int yatt_synth_logits(uint64_t seed, int64_t row0, int64_t rows, int32_t vocab, uint16_t* pol,
                       uint16_t* ref, int32_t* tgt, void* stream) {
+  YATT_ALIGNED("synth_logits", pol, 16);
+  YATT_ALIGNED("synth_logits", ref, 16);
+  YATT_ALIGNED("synth_logits", tgt, 4);
   return synth_logits_launch(seed, row0, rows, vocab, pol, ref, tgt, as_stream(stream));
 }
 
 int yatt_synth_floats(uint64_t seed, uint64_t stream_id, int64_t i0, int64_t n, int32_t kind,
                       int32_t group_size, const float* base, float* out, void* stream) {
+  YATT_ALIGNED4("synth_floats", base, out, nullptr, nullptr);
   return synth_floats_launch(seed, stream_id, i0, n, kind, group_size, base, out,
                              as_stream(stream));
 }

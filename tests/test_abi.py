@@ -80,3 +80,25 @@ def test_errors_are_typed_and_messages_thread_local():
     assert rc == 1
     assert b"num_controllers" in h.yatt_last_error_message()
     assert h.yatt_shard_dataset(5, 2, 9, None, None) == 2
+
+
+def test_misaligned_pointers_are_config_errors_before_any_launch():
+    """Alignment contract (yatt_cuda.h "Conventions"): checked before any CUDA
+    call, so fake addresses never reach the device and this runs on CPU."""
+    from paper_2508_07970_b200._lib import check
+    A, M = 0x10000, 0x10001  # aligned / misaligned fake device addresses
+    calls = [
+        ("gae", lambda: lib().yatt_gae(A, A, None, A, 1, 1.0, 1.0, A + 2, A, None)),
+        ("coef", lambda: lib().yatt_logits_backward(A, None, A, None, 1, 8, A + 4, 0, A, None)),
+        ("mbs", lambda: lib().yatt_microbatch_aggregates(A, A, None, 1, 1, 0, A + 4, None)),
+        ("sums", lambda: lib().yatt_policy_loss(A, A, A, A, A, None, 1, None, 0, None, A + 4, A, 64,
+                                                None)),
+        ("order", lambda: lib().yatt_sort_order_desc(A, 1, M, A, 64, None)),
+        ("new_cu", lambda: lib().yatt_filter_compact(A, A, 1, 1, A, A, A + 4, A, A, 64, None)),
+        ("out", lambda: lib().yatt_token_stats(A, A, A, None, 1, 8, 2, A, A, A + 1, A, None)),
+        ("ws", lambda: lib().yatt_lmhead_token_stats(A, A, A, 1, 64, 8, 1, A, A, A, A + 8, 64,
+                                                     None)),
+    ]
+    for what, fn in calls:
+        with pytest.raises(ConfigError, match="aligned"):
+            check(fn())
