@@ -18,9 +18,10 @@
  *    thread-local.
  *  - Every pointer must be naturally aligned for its element type (structs:
  *    8 bytes; workspaces: 8, the LM-head one 16); the logits-backward `coef`
- *    table and the policy/ref/grad logits of the TMA kernels need 16 bytes.
+ *    table and synth_logits outputs need 16 bytes.
  *    A misaligned pointer returns YATT_ERR_CONFIG before any launch.
- *    yatt_token_stats alone accepts 2-byte-aligned logits (generic path).
+ *    yatt_token_stats and yatt_logits_backward accept any vocab and 2-byte
+ *    aligned logits (a generic element-wise kernel; the TMA path otherwise).
  */
 #ifndef YATT_CUDA_H_
 #define YATT_CUDA_H_

@@ -230,6 +230,37 @@ __device__ __forceinline__ float bf16_at(const uint16_t* base, int64_t idx) {
   return __uint_as_float(uint32_t(base[idx]) << 16);
 }
 
+// Any vocab / any 2-byte alignment (V % 8 != 0 or an unaligned view): one CTA
+// per row, element-wise 2-byte loads and stores — the same per-element formula
+// as the tile kernel's target patch, so both paths round identically.
+template <bool kFull>
+__global__ void __launch_bounds__(256) logits_backward_generic_kernel(const GradParams p) {
+  const int64_t V = p.V;
+  for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
+    uint16_t* grow = p.grad + row * V;
+    if (p.mask != nullptr && p.mask[row] == 0) {
+      for (int64_t v = threadIdx.x; v < V; v += blockDim.x) grow[v] = 0;
+      continue;
+    }
+    const float* cf = p.coef + row * kCoef;
+    const RowCoef c{cf[0], cf[1], cf[2], cf[3] * kLog2e, cf[4] * kLog2e, cf[5], cf[6]};
+    const int32_t y = p.tgt[row];
+    const uint16_t* xp = p.pol + row * V;
+    const uint16_t* xq = kFull ? p.ref + row * V : nullptr;
+    for (int64_t v = threadIdx.x; v < V; v += blockDim.x) {
+      const float a = fmaf(bf16_at(xp, v), kLog2e, -c.lsep2);
+      const float pp = ex2_approx(a);
+      float val = pp * fmaf(c.h, a * kLn2f + c.H, -c.g);
+      if (kFull) {
+        const float lnq = fmaf(bf16_at(xq, v), kLog2e, -c.lseq2) * kLn2f;
+        val = fmaf(c.f * pp, a * kLn2f - lnq - c.KL, val);
+      }
+      if (v == y) val += c.g;
+      grow[v] = uint16_t(pack_bf16x2(val, 0.f) & 0xffffu);
+    }
+  }
+}
+
 __global__ void grad_coef_kernel(const uint16_t* pol, const uint16_t* ref, const int32_t* tgt,
                                  const float* logp, const float* ref_logp, const float* old_logp,
                                  const float* adv, const float* ent, const float* kl,
@@ -329,16 +360,23 @@ int grad_coef_launch(const uint16_t* pol, const uint16_t* ref, const int32_t* tg
 int logits_backward_launch(const uint16_t* pol, const uint16_t* ref, const int32_t* tgt,
                            const uint8_t* mask, int64_t rows, int32_t V, const float* coef,
                            int32_t full_kl, uint16_t* grad, cudaStream_t st) {
-  YATT_REQUIRE(V > 0 && V % 8 == 0, YATT_ERR_CONFIG, "logits_backward: vocab must be a multiple of 8");
+  YATT_REQUIRE(V > 0, YATT_ERR_CONFIG, "logits_backward: vocab must be positive");
   YATT_REQUIRE(rows >= 0, YATT_ERR_CONFIG, "logits_backward: rows must be >= 0");
   if (rows == 0) return YATT_OK;
   YATT_REQUIRE(pol && tgt && coef && grad && (!full_kl || ref), YATT_ERR_CONFIG,
                "logits_backward: null pointer");
-  YATT_REQUIRE((reinterpret_cast<uintptr_t>(pol) & 15) == 0 &&
-                   (reinterpret_cast<uintptr_t>(grad) & 15) == 0 &&
-                   (!full_kl || (reinterpret_cast<uintptr_t>(ref) & 15) == 0),
-               YATT_ERR_CONFIG, "logits_backward: tensors must be 16-byte aligned");
   GradParams prm{pol, ref, tgt, mask, coef, rows, V, grad};
+  const bool tma_ok = V % 8 == 0 && (reinterpret_cast<uintptr_t>(pol) & 15) == 0 &&
+                      (reinterpret_cast<uintptr_t>(grad) & 15) == 0 &&
+                      (!full_kl || (reinterpret_cast<uintptr_t>(ref) & 15) == 0);
+  if (!tma_ok) {
+    const int g = int(min64(rows, int64_t(8) * num_sms()));
+    if (full_kl)
+      logits_backward_generic_kernel<true><<<g, 256, 0, st>>>(prm);
+    else
+      logits_backward_generic_kernel<false><<<g, 256, 0, st>>>(prm);
+    return check_launch("logits_backward_generic_kernel");
+  }
   const int grid = int(min64(rows, int64_t(2) * num_sms()));
   if (full_kl) {
     constexpr size_t smem = size_t(stages_of<true>()) * 2 * kTile * 2 + sizeof(BwdTail);

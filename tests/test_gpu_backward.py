@@ -24,8 +24,25 @@ def to_f64(bits):
     return (bits.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
 
 
-def _case(cuda, rows, V, kl_mode, agg, ent_coef, clip_c=0.0, masked=False, seed=3):
-    pol, ref, tgt = ops.synth_logits(seed, 0, rows, V, device=cuda)
+def _logits(cuda, rows, V, seed, shifted):
+    """synth_logits when the TMA kernel applies; otherwise (V % 8 != 0, or a
+    view 2 bytes off 16-byte alignment) the generic kernel's inputs."""
+    if V % 8 == 0 and not shifted:
+        return ops.synth_logits(seed, 0, rows, V, device=cuda)
+    g = torch.Generator(device=cuda).manual_seed(seed)
+
+    def mat():
+        buf = torch.empty(rows * V + 1, dtype=torch.bfloat16, device=cuda)
+        t = buf[1:] if shifted else buf[:-1]
+        t.copy_((torch.randn(rows * V, device=cuda, generator=g) * 3).to(torch.bfloat16))
+        return t.view(rows, V)
+    pol, ref = mat(), mat()
+    tgt = torch.randint(0, V, (rows,), device=cuda, generator=g, dtype=torch.int32)
+    return pol, ref, tgt
+
+
+def _case(cuda, rows, V, kl_mode, agg, ent_coef, clip_c=0.0, masked=False, seed=3, shifted=False):
+    pol, ref, tgt = _logits(cuda, rows, V, seed, shifted)
     mask = None
     if masked:
         mask = torch.as_tensor((np.arange(rows) % 5 != 2).astype(np.uint8), device=cuda)
@@ -38,7 +55,7 @@ def _case(cuda, rows, V, kl_mode, agg, ent_coef, clip_c=0.0, masked=False, seed=
     grad, coef = ops.logits_grad(pol, ref, tgt, logp, rlogp, old, adv, ent, kl, mask, cu, cfg,
                                  kl_mode, norm)
     torch.cuda.synchronize()
-    hp, hr = bf16_np(pol), bf16_np(ref)
+    hp, hr = bf16_np(pol.contiguous()), bf16_np(ref.contiguous())
     m = None if mask is None else mask.cpu().numpy()
     eg, ecoef = O.logits_backward(hp, hr, tgt.cpu().numpy(), logp.cpu().numpy(),
                                   rlogp.cpu().numpy(), old.cpu().numpy(), adv.cpu().numpy(), m,
@@ -79,6 +96,13 @@ def test_logits_backward_qwen_vocab_rows_sum_to_zero(cuda):
     got, eg = _case(cuda, 8, 152064, "k3", "token-mean", 0.001)
     # sum_v dL/dx_v = 0 for a softmax-based loss; bf16 rounding leaves ~1e-3 relative of max
     assert np.all(np.abs(got.sum(1)) <= 2e-3 * np.abs(got).max(1) * np.sqrt(got.shape[1]) / 10)
+
+
+@pytest.mark.parametrize("V,shifted", [(1001, False), (12, False), (4096, True), (9001, True)])
+@pytest.mark.parametrize("kl_mode", ["k3", "full"])
+def test_logits_backward_generic_path(cuda, V, shifted, kl_mode):
+    """Any vocab and 2-byte-aligned views take the generic kernel: same bar."""
+    _case(cuda, 19, V, kl_mode, "seq-mean-token-mean", 0.01, masked=True, shifted=shifted)
 
 
 def test_logits_backward_errors(cuda):
