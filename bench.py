@@ -365,8 +365,24 @@ def run_e2e(args, dev, ops, cfg, ws):
         step()
     ms = (time.perf_counter() - t0) * 1e3 / k
     h2d = 2 * rows * VOCAB * 2 + rows * (4 + 1 + 4) + RESPONSES * 4
+    # the link's own ceiling: plain pinned H2D copies of the same two tensors
+    d_pol = torch.empty(h_pol.shape, dtype=h_pol.dtype, device=dev)
+    d_ref = torch.empty_like(d_pol)
+    copy_ms = []
+    for i in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        d_pol.copy_(h_pol, non_blocking=True)
+        d_ref.copy_(h_ref, non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        copy_ms.append(a.elapsed_time(b))
+    del d_pol, d_ref
+    link_gbs = 2 * h_pol.numel() * 2 / (min(copy_ms[1:]) / 1e3) / 1e9
     return {"value": rows / (ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": 64, "ms_per_step": ms, "h2d_gbs": h2d / (ms / 1e3) / 1e9,
+            "h2d_copy_peak_gbs": link_gbs,
+            "frac_of_h2d_copy_peak": h2d / (ms / 1e3) / 1e9 / link_gbs,
             "api": "yatt_grpo_step_host (C ABI, host buffers)",
             "sample": f"one prompt group of {RESPONSES} x {rows // RESPONSES} tokens per step "
                       f"({h2d / 1e9:.2f} GB H2D from pinned memory)"}

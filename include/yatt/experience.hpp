@@ -52,9 +52,12 @@ struct GaeConfig {
   void validate() const;
 };
 
+// n_tokens = length of the packed arrays; workspace of gae_workspace_bytes(n_tokens).
+std::size_t gae_workspace_bytes(std::int64_t n_tokens);
 void gae(const float* values, const float* rewards, const std::uint8_t* mask,
-         const std::int64_t* cu_seqlens, std::int64_t n_seqs, const GaeConfig& config,
-         float* advantages, float* returns, void* stream = nullptr);
+         const std::int64_t* cu_seqlens, std::int64_t n_seqs, std::int64_t n_tokens,
+         const GaeConfig& config, float* advantages, float* returns, void* workspace,
+         std::size_t workspace_bytes, void* stream = nullptr);
 
 // ---- A4 -------------------------------------------------------------------
 enum class LossAggregation { kTokenMean = 0, kSeqMeanTokenMean = 1, kSeqMeanTokenSum = 2 };

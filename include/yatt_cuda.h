@@ -237,11 +237,16 @@ int yatt_broadcast_to_tokens(const float* d_sample_vals,
 /*   delta_t = r_t + gamma * V_next - V_t   (V_next = 0 past the end)        */
 /*   A_t     = delta_t + gamma*lam * A_next ;  R_t = A_t + V_t               */
 /* Computed in fp64 on the device, stored fp32.  d_mask may be NULL.         */
+/* n_tokens: length of the packed arrays (tokens outside [cu[0], cu[n_seqs]) */
+/* are not written).  One pass over the tokens: a tiled scan whose tiles    */
+/* exchange carries through the workspace (yatt_gae_workspace_bytes).       */
 /* ------------------------------------------------------------------------ */
+size_t yatt_gae_workspace_bytes(int64_t n_tokens);
 int yatt_gae(const float* d_values, const float* d_rewards,
              const uint8_t* d_mask, const int64_t* d_cu_seqlens,
-             int64_t n_seqs, float gamma, float lam, float* d_advantages,
-             float* d_returns, void* stream);
+             int64_t n_seqs, int64_t n_tokens, float gamma, float lam,
+             float* d_advantages, float* d_returns, void* d_workspace,
+             size_t workspace_bytes, void* stream);
 /* Masked moments {count, sum, sum_sq} (fp64, deterministic) of x, written    */
 /* to d_out[3]; all-reduce them across ranks before yatt_whiten.             */
 size_t yatt_masked_moments_workspace_bytes(void);

@@ -73,23 +73,50 @@ __global__ void grpo_adv_kernel(const float* r, int64_t n, uint64_t first_id, in
   adv[i] = float(a);
 }
 
+__device__ __forceinline__ float bcast_val(float v, const uint8_t* mask, int64_t t) {
+  return (mask == nullptr || mask[t]) ? v : 0.f;
+}
+
+// One CTA per sample: scalar head to the first 4-aligned token, 16-byte
+// streaming stores over the body (out 16-B aligned, mask read as u32), tail.
+template <bool kVec>
 __global__ void broadcast_kernel(const float* vals, const int64_t* cu, int64_t nsamples,
                                  const uint8_t* mask, float* out) {
   for (int64_t s = blockIdx.x; s < nsamples; s += gridDim.x) {
     const float v = vals[s];
     const int64_t b = cu[s], e = cu[s + 1];
-    for (int64_t t = b + threadIdx.x; t < e; t += blockDim.x)
-      out[t] = (mask == nullptr || mask[t]) ? v : 0.f;
+    if (!kVec) {
+      for (int64_t t = b + threadIdx.x; t < e; t += blockDim.x) out[t] = bcast_val(v, mask, t);
+      continue;
+    }
+    const int64_t hb = min64(e, (b + 3) & ~int64_t(3));
+    const int64_t jb = hb >> 2, je = max64(jb, e >> 2);
+    if (b + int64_t(threadIdx.x) < hb) out[b + threadIdx.x] = bcast_val(v, mask, b + threadIdx.x);
+    for (int64_t j = jb + threadIdx.x; j < je; j += blockDim.x) {
+      float4 o = make_float4(v, v, v, v);
+      if (mask != nullptr) {
+        const uint32_t m = __ldg(reinterpret_cast<const uint32_t*>(mask + 4 * j));
+        o.x = (m & 0xffu) ? v : 0.f;
+        o.y = (m & 0xff00u) ? v : 0.f;
+        o.z = (m & 0xff0000u) ? v : 0.f;
+        o.w = (m & 0xff000000u) ? v : 0.f;
+      }
+      __stcs(reinterpret_cast<float4*>(out + 4 * j), o);
+    }
+    const int64_t tb = max64(hb, 4 * je);
+    if (tb + int64_t(threadIdx.x) < e) out[tb + threadIdx.x] = bcast_val(v, mask, tb + threadIdx.x);
   }
 }
 
 // ----------------------------------------------------------------- GAE ----
 // State flowing right-to-left: (A_next, V_next).  A valid token maps it to
 //   A' = gl*A + g*V + (r - v),  V' = v      ->  M = [[gl, g], [0, 0]], o = (r-v, v)
-// a masked token is the identity.  Maps compose by warp scan (fp64).
+// a masked token is the identity; the last token of a sequence first resets
+// the state to (0, 0) (the zero map).  Maps compose associatively (fp64).
 struct Aff {
   double a, b, k, p, q;  // M = [[a, b], [0, k]], offset (p, q)
 };
+__device__ __forceinline__ Aff aff_id() { return Aff{1.0, 0.0, 1.0, 0.0, 0.0}; }
 __device__ __forceinline__ Aff compose(const Aff& F, const Aff& G) {  // F after G
   return Aff{F.a * G.a, F.a * G.b + F.b * G.k, F.k * G.k, F.a * G.p + F.b * G.q + F.p,
              F.k * G.q + F.q};
@@ -100,114 +127,302 @@ __device__ __forceinline__ Aff shfl_down_aff(const Aff& x, int d) {
              __shfl_down_sync(0xffffffffu, x.q, d)};
 }
 
-// One CTA per sequence.  A segment of up to kGaeSeg tokens is staged in
-// shared memory with coalesced loads (padded [thread][token] layout, no bank
-// conflicts); thread i owns kGaeTpt contiguous tokens: it composes their maps
-// right-to-left, a block scan (warp shuffles + smem across warps) gives every
-// thread the composite of everything to its right, then it replays its tokens
-// with the incoming state, writes A/R back to smem, and the CTA stores them
-// coalesced.  Longer sequences loop over segments right-to-left with a carry.
-constexpr int kGaeThreads = 256;
+// Single-pass scan over the packed token array with decoupled look-back.
+// The array is cut into 2,048-token tiles (thread i of a 128-thread CTA owns
+// 16 contiguous tokens, loaded/stored as float4; ~5 CTAs per SM hide each
+// other's look-back latency).  CTAs claim tiles right to
+// left by an atomic ticket, so a tile only waits on tiles claimed by CTAs
+// already running.  Each tile publishes its composite map (flag 1) and, once
+// its incoming state is known, its outgoing state (flag 2); a tile holding a
+// sequence end has a constant composite and publishes flag 2 at once, so
+// look-back chains stop at the first sequence boundary.  Bytes: 9 read +
+// 8 written per token, once.
+constexpr int kGaeThreads = 128;
 constexpr int kGaeTpt = 16;
-constexpr int kGaeSeg = kGaeThreads * kGaeTpt;
-constexpr int kGaePad = kGaeTpt + 1;
+constexpr int kGaeTile = kGaeThreads * kGaeTpt;
 
-__device__ __forceinline__ int gae_slot(int idx) { return (idx / kGaeTpt) * kGaePad + idx % kGaeTpt; }
+struct GaeWs {  // device workspace layout (yatt_gae_workspace_bytes)
+  uint32_t* ticket;
+  uint32_t* flag;  // [ntiles]
+  Aff* agg;        // [ntiles]
+  double2* incl;   // [ntiles] state (A, V) leaving the tile to the left
+};
+__host__ __device__ inline size_t gae_align(size_t x) { return (x + 15) & ~size_t(15); }
+__host__ __device__ inline GaeWs gae_ws(void* base, int64_t ntiles) {
+  uint8_t* b = static_cast<uint8_t*>(base);
+  GaeWs w;
+  w.ticket = reinterpret_cast<uint32_t*>(b);
+  w.flag = reinterpret_cast<uint32_t*>(b + 16);
+  size_t off = gae_align(16 + 4 * size_t(ntiles));
+  w.agg = reinterpret_cast<Aff*>(b + off);
+  off = gae_align(off + sizeof(Aff) * size_t(ntiles));
+  w.incl = reinterpret_cast<double2*>(b + off);
+  return w;
+}
+size_t gae_ws_bytes(int64_t ntiles) {
+  return gae_align(gae_align(gae_align(16 + 4 * size_t(ntiles)) + sizeof(Aff) * size_t(ntiles)) +
+                   sizeof(double2) * size_t(ntiles));
+}
+size_t gae_zero_bytes(int64_t ntiles) { return 16 + 4 * size_t(ntiles); }
 
-__global__ void __launch_bounds__(kGaeThreads) gae_kernel(
-    const float* values, const float* rewards, const uint8_t* mask, const int64_t* cu,
-    int64_t nseq, double gamma, double lam, float* adv, float* ret) {
-  __shared__ float sv[kGaeThreads * kGaePad];
-  __shared__ float sr[kGaeThreads * kGaePad];
-  __shared__ uint8_t sm[kGaeThreads * kGaePad];
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// First index k in [k0, k1) with a[k] >= key (k1 if none), a non-decreasing;
+// one warp, 32-ary: positions >= k1 count as +inf, so the predicate is
+// monotone in the lane and the answer stays inside [k0, k1].
+__device__ int64_t warp_lower_bound(const int64_t* a, int64_t k0, int64_t k1, int64_t key,
+                                    int lane) {
+  while (k1 - k0 > 32) {
+    const int64_t step = (k1 - k0 + 31) / 32;
+    const int64_t idx = k0 + lane * step;
+    const bool ge = idx >= k1 || __ldg(a + idx) >= key;
+    const uint32_t bal = __ballot_sync(0xffffffffu, ge);
+    if (bal & 1u) return k0;
+    const int f = bal ? __ffs(bal) - 1 : 32;
+    const int64_t nk0 = k0 + int64_t(f - 1) * step + 1;
+    if (f < 32) k1 = min64(k1, k0 + int64_t(f) * step);
+    k0 = nk0;
+  }
+  const bool ge = k0 + lane < k1 && __ldg(a + k0 + lane) >= key;
+  const uint32_t bal = __ballot_sync(0xffffffffu, ge);
+  return bal ? k0 + __ffs(bal) - 1 : k1;
+}
+
+template <bool kVec>
+__global__ void __launch_bounds__(kGaeThreads) gae_scan_kernel(
+    const float* __restrict__ values, const float* __restrict__ rewards,
+    const uint8_t* __restrict__ mask, const int64_t* __restrict__ cu, int64_t nseq,
+    int64_t n_tokens, int64_t ntiles, double gamma, double lam, float* adv, float* ret, GaeWs ws) {
+  __shared__ uint32_t last_bits[kGaeTile / 32];  // bit j: token lo+j ends a sequence
   __shared__ Aff wtot[kGaeThreads / 32];
-  __shared__ double carry[2];
+  __shared__ double2 carry;
+  __shared__ int64_t s_tile, s_k0, s_k1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double gl = gamma * lam;
-  for (int64_t s = blockIdx.x; s < nseq; s += gridDim.x) {
-    const int64_t b = cu[s], e = cu[s + 1];
-    double cA = 0.0, cV = 0.0;  // state entering from the right of the segment
-    for (int64_t hi = e; hi > b; hi -= kGaeSeg) {
-      const int64_t lo = max64(b, hi - kGaeSeg);
-      const int n = int(hi - lo);
-#pragma unroll 8
-      for (int i = tid; i < n; i += kGaeThreads) {  // unrolled: many loads in flight
-        const int k = gae_slot(i);
-        sv[k] = __ldg(values + lo + i);
-        sr[k] = __ldg(rewards + lo + i);
-        sm[k] = mask == nullptr ? uint8_t(1) : __ldg(mask + lo + i);
-      }
-      __syncthreads();
-      // this thread's tokens [t0, t1) within the segment
-      const int t0 = tid * kGaeTpt, t1 = min(n, t0 + kGaeTpt);
-      Aff f{1.0, 0.0, 1.0, 0.0, 0.0};
-      for (int t = t1 - 1; t >= t0; --t) {
-        const int k = gae_slot(t);
-        if (sm[k]) {
-          const double v = sv[k];
-          f = Aff{gl * f.a, gl * f.b + gamma * f.k, 0.0, gl * f.p + gamma * f.q + (double(sr[k]) - v),
-                  v};
-        }
-      }
-      // exclusive composite of the threads to the right: inclusive warp scan
-      // from the right, then compose with the totals of later warps
-      Aff inc = f;
+
+  if (tid == 0) s_tile = ntiles - 1 - int64_t(atomicAdd(ws.ticket, 1u));
+  for (int i = tid; i < kGaeTile / 32; i += kGaeThreads) last_bits[i] = 0u;
+  __syncthreads();
+  const int64_t t = s_tile;
+  const int64_t lo = t * kGaeTile, hi = min64(n_tokens, lo + kGaeTile);
+  const int64_t x0 = lo + int64_t(tid) * kGaeTpt;  // this thread's first token
+  const int nmine = int(max64(0, min64(kGaeTpt, hi - x0)));
+
+  // issue this thread's loads first (they fly while the boundaries are found)
+  float v[kGaeTpt], r[kGaeTpt];
+  uint32_t mw[kGaeTpt / 4];
+  if (kVec && nmine == kGaeTpt) {
 #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const Aff o = shfl_down_aff(inc, d);
-        if (lane + d < 32) inc = compose(inc, o);
-      }
-      if (lane == 0) wtot[warp] = inc;
-      __syncthreads();
-      Aff right{1.0, 0.0, 1.0, 0.0, 0.0};  // composite of later warps
-      for (int w = kGaeThreads / 32 - 1; w > warp; --w) right = compose(wtot[w], right);
-      Aff ex = shfl_down_aff(inc, 1);      // lanes to my right in this warp
-      if (lane == 31) ex = Aff{1.0, 0.0, 1.0, 0.0, 0.0};
-      ex = compose(ex, right);
-      double A = ex.a * cA + ex.b * cV + ex.p;
-      double Vn = ex.k * cV + ex.q;
-      for (int t = t1 - 1; t >= t0; --t) {
-        const int k = gae_slot(t);
-        const double v = sv[k];
-        if (sm[k]) {
-          A = (double(sr[k]) - v) + gamma * Vn + gl * A;
-          Vn = v;
-        }
-        sv[k] = float(A);      // advantage
-        sr[k] = float(A + v);  // return
-      }
-      if (tid == 0) {
-        carry[0] = A;
-        carry[1] = Vn;
-      }
-      __syncthreads();
-      for (int i = tid; i < n; i += kGaeThreads) {
-        const int k = gae_slot(i);
-        adv[lo + i] = sv[k];
-        ret[lo + i] = sr[k];
-      }
-      cA = carry[0];
-      cV = carry[1];
-      __syncthreads();
+    for (int q = 0; q < kGaeTpt / 4; ++q) {
+      const float4 a = __ldcs(reinterpret_cast<const float4*>(values + x0) + q);
+      const float4 b = __ldcs(reinterpret_cast<const float4*>(rewards + x0) + q);
+      v[4 * q] = a.x, v[4 * q + 1] = a.y, v[4 * q + 2] = a.z, v[4 * q + 3] = a.w;
+      r[4 * q] = b.x, r[4 * q + 1] = b.y, r[4 * q + 2] = b.z, r[4 * q + 3] = b.w;
     }
+    if (mask != nullptr) {
+      const uint4 m = __ldcs(reinterpret_cast<const uint4*>(mask + x0));
+      mw[0] = m.x, mw[1] = m.y, mw[2] = m.z, mw[3] = m.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kGaeTpt; ++j) {
+      v[j] = j < nmine ? values[x0 + j] : 0.f;
+      r[j] = j < nmine ? rewards[x0 + j] : 0.f;
+    }
+    if (mask != nullptr) {
+#pragma unroll
+      for (int q = 0; q < kGaeTpt / 4; ++q) {
+        uint32_t w = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (4 * q + u < nmine && mask[x0 + 4 * q + u]) w |= 1u << (8 * u);
+        mw[q] = w;
+      }
+    }
+  }
+  if (mask == nullptr) {
+#pragma unroll
+    for (int q = 0; q < kGaeTpt / 4; ++q) mw[q] = 0x01010101u;
+  }
+
+  // sequence ends inside the tile: k with cu[k] in [lo+1, hi], k in [1, nseq]
+  if (warp < 2) {  // the two searches run in parallel on warps 0 and 1
+    const int64_t k = warp_lower_bound(cu, 1, nseq + 1, (warp == 0 ? lo : hi) + 1, lane);
+    if (lane == 0) (warp == 0 ? s_k0 : s_k1) = k;
+  }
+  __syncthreads();
+  for (int64_t k = s_k0 + tid; k < s_k1; k += kGaeThreads) {
+    const int64_t j = __ldg(cu + k) - 1 - lo;
+    atomicOr(&last_bits[j >> 5], 1u << (j & 31));
+  }
+  const int64_t in_lo = __ldg(cu), in_hi = min64(n_tokens, __ldg(cu + nseq));
+  __syncthreads();
+  // this thread's 16 "last" bits (x0 - lo is a multiple of 16)
+  const uint32_t lb = (last_bits[(x0 - lo) >> 5] >> ((x0 - lo) & 31)) & 0xffffu;
+  auto inside = [&](int j) { return j < nmine && x0 + j >= in_lo && x0 + j < in_hi; };
+  auto valid = [&](int j) { return ((mw[j >> 2] >> (8 * (j & 3))) & 0xffu) != 0u; };
+
+  // compose this thread's tokens right to left
+  Aff f = aff_id();
+#pragma unroll
+  for (int j = kGaeTpt - 1; j >= 0; --j) {
+    if (!inside(j)) continue;
+    if ((lb >> j) & 1u) f = Aff{0.0, 0.0, 0.0, 0.0, 0.0};
+    if (valid(j)) {
+      const double vv = v[j];
+      f = Aff{gl * f.a, gl * f.b + gamma * f.k, 0.0, gl * f.p + gamma * f.q + (double(r[j]) - vv),
+              vv};
+    }
+  }
+  // inclusive scan from the right inside the warp, then warp totals
+  Aff inc = f;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const Aff o = shfl_down_aff(inc, d);
+    if (lane + d < 32) inc = compose(inc, o);
+  }
+  if (lane == 0) wtot[warp] = inc;
+  __syncthreads();
+  if (tid == 0) {
+    Aff tot = wtot[kGaeThreads / 32 - 1];
+    for (int w = kGaeThreads / 32 - 2; w >= 0; --w) tot = compose(wtot[w], tot);
+    const bool constant = tot.a == 0.0 && tot.b == 0.0 && tot.k == 0.0;
+    if (constant) {
+      ws.incl[t] = make_double2(tot.p, tot.q);
+      st_release(ws.flag + t, 2u);
+    } else {
+      ws.agg[t] = tot;
+      st_release(ws.flag + t, 1u);
+    }
+    // look-back: state entering from the right = M_{t+1} o ... o (state of the
+    // first tile to the right that published its outgoing state)
+    Aff c = aff_id();
+    double2 st = make_double2(0.0, 0.0);
+    for (int64_t j = t + 1; j < ntiles; ++j) {
+      uint32_t fl;
+      int spins = 0;
+      while ((fl = ld_acquire(ws.flag + j)) == 0u)
+        if (++spins > 8) __nanosleep(64);
+      if (fl == 2u) {
+        st = __ldcg(ws.incl + j);
+        break;
+      }
+      const Aff* g = ws.agg + j;
+      c = compose(c, Aff{__ldcg(&g->a), __ldcg(&g->b), __ldcg(&g->k), __ldcg(&g->p),
+                         __ldcg(&g->q)});
+    }
+    const double2 in_state =
+        make_double2(c.a * st.x + c.b * st.y + c.p, c.k * st.y + c.q);
+    if (!constant) {
+      ws.incl[t] = make_double2(tot.a * in_state.x + tot.b * in_state.y + tot.p,
+                                tot.k * in_state.y + tot.q);
+      st_release(ws.flag + t, 2u);
+    }
+    carry = in_state;
+  }
+  // composite of the threads to my right: later lanes, then later warps
+  Aff right = aff_id();
+  for (int w = kGaeThreads / 32 - 1; w > warp; --w) right = compose(wtot[w], right);
+  Aff ex = shfl_down_aff(inc, 1);
+  if (lane == 31) ex = aff_id();
+  ex = compose(ex, right);
+  __syncthreads();
+  const double2 cs = carry;
+  double A = ex.a * cs.x + ex.b * cs.y + ex.p;
+  double Vn = ex.k * cs.y + ex.q;
+  // replay right to left; v[] becomes the advantage, r[] the return
+#pragma unroll
+  for (int j = kGaeTpt - 1; j >= 0; --j) {
+    if (!inside(j)) continue;
+    if ((lb >> j) & 1u) A = 0.0, Vn = 0.0;
+    const double vv = v[j];
+    if (valid(j)) {
+      A = (double(r[j]) - vv) + gamma * Vn + gl * A;
+      Vn = vv;
+    }
+    v[j] = float(A);
+    r[j] = float(A + vv);
+  }
+  const bool all_in = nmine == kGaeTpt && x0 >= in_lo && x0 + kGaeTpt <= in_hi;
+  if (kVec && all_in) {
+#pragma unroll
+    for (int q = 0; q < kGaeTpt / 4; ++q) {
+      __stcs(reinterpret_cast<float4*>(adv + x0) + q,
+             make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+      __stcs(reinterpret_cast<float4*>(ret + x0) + q,
+             make_float4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]));
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kGaeTpt; ++j)
+      if (inside(j)) {
+        adv[x0 + j] = v[j];
+        ret[x0 + j] = r[j];
+      }
   }
 }
 
 // ------------------------------------------------------- masked moments ----
-__global__ void moments_partial_kernel(const float* x, const uint8_t* mask, int64_t n,
-                                       double* part) {
-  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
-  const int64_t lo = int64_t(blockIdx.x) * per, hi = min64(n, lo + per);
-  double c = 0, s = 0, q = 0;
-  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-    if (mask == nullptr || mask[i]) {
-      const double v = x[i];
-      c += 1.0;
-      s += v;
-      q += v * v;
-    }
+constexpr int kMomThreads = 256;
+constexpr int kMomMaxParts = 640;
+
+__device__ __forceinline__ void mom_add(float x, bool valid, double& c, double& s, double& q) {
+  if (valid) {
+    const double v = f2d(x);
+    c += 1.0;
+    s += v;
+    q += v * v;
   }
-  __shared__ double red[3][32];
+}
+__device__ __forceinline__ void mom_add4(const float4& x, uint32_t m, double& c, double& s,
+                                         double& q) {
+  mom_add(x.x, m & 0xffu, c, s, q);
+  mom_add(x.y, m & 0xff00u, c, s, q);
+  mom_add(x.z, m & 0xff0000u, c, s, q);
+  mom_add(x.w, m & 0xff000000u, c, s, q);
+}
+__device__ __forceinline__ uint32_t mask4(const uint8_t* mask, int64_t j) {
+  return mask == nullptr ? 0x01010101u : __ldg(reinterpret_cast<const uint32_t*>(mask + 4 * j));
+}
+
+// Contiguous ranges of 4-element vectors per block, two in flight per thread;
+// the n % 4 tail goes to the last block.  fp64 (count, sum, sum of squares).
+template <bool kVec>
+__global__ void __launch_bounds__(kMomThreads) moments_partial_kernel(const float* x,
+                                                                      const uint8_t* mask,
+                                                                      int64_t n, double* part) {
+  double c = 0, s = 0, q = 0;
+  if (kVec) {
+    const int64_t nv = n >> 2;
+    const int64_t per = (nv + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = int64_t(blockIdx.x) * per, hi = min64(nv, lo + per);
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    int64_t j = lo + threadIdx.x;
+    for (; j + kMomThreads < hi; j += 2 * kMomThreads) {
+      const float4 a = __ldg(x4 + j), b = __ldg(x4 + j + kMomThreads);
+      const uint32_t ma = mask4(mask, j), mb = mask4(mask, j + kMomThreads);
+      mom_add4(a, ma, c, s, q);
+      mom_add4(b, mb, c, s, q);
+    }
+    if (j < hi) mom_add4(__ldg(x4 + j), mask4(mask, j), c, s, q);
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x < (n & 3)) {
+      const int64_t i = 4 * nv + threadIdx.x;
+      mom_add(x[i], mask == nullptr || mask[i], c, s, q);
+    }
+  } else {
+    const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = int64_t(blockIdx.x) * per, hi = min64(n, lo + per);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += kMomThreads)
+      mom_add(x[i], mask == nullptr || mask[i], c, s, q);
+  }
+  __shared__ double red[3][kMomThreads / 32];
   c = warp_sum(c);
   s = warp_sum(s);
   q = warp_sum(q);
@@ -220,7 +435,7 @@ __global__ void moments_partial_kernel(const float* x, const uint8_t* mask, int6
   __syncthreads();
   if (threadIdx.x == 0) {
     double a = 0, bsum = 0, cc = 0;
-    for (int i = 0; i < int(blockDim.x >> 5); ++i) {
+    for (int i = 0; i < kMomThreads / 32; ++i) {
       a += red[0][i];
       bsum += red[1][i];
       cc += red[2][i];
@@ -231,33 +446,51 @@ __global__ void moments_partial_kernel(const float* x, const uint8_t* mask, int6
   }
 }
 
-__global__ void moments_final_kernel(const double* part, int nparts, double* out) {
-  if (threadIdx.x != 0) return;
-  double a = 0, b = 0, c = 0;
-  for (int i = 0; i < nparts; ++i) {
-    a += part[3 * i];
-    b += part[3 * i + 1];
-    c += part[3 * i + 2];
-  }
-  out[0] = a;
-  out[1] = b;
-  out[2] = c;
-}
-
-__global__ void whiten_kernel(float* x, const uint8_t* mask, int64_t n, const double* mom,
-                              int32_t shift_mean) {
+struct WhitenCoef {
+  double mean, inv;
+};
+__device__ __forceinline__ WhitenCoef whiten_coef(const double* mom) {
   const double cnt = mom[0];
   const double mean = cnt > 0 ? mom[1] / cnt : 0.0;
   const double var = cnt > 1 ? (mom[2] - mom[1] * mean) / (cnt - 1.0) : 0.0;
-  const double inv = 1.0 / sqrt(var + 1e-8);
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    if (mask == nullptr || mask[i]) {
-      double v = (double(x[i]) - mean) * inv;
-      if (!shift_mean) v += mean;
-      x[i] = float(v);
+  return WhitenCoef{mean, 1.0 / sqrt(var + 1e-8)};
+}
+__device__ __forceinline__ float whiten1(float x, const WhitenCoef& w, int32_t shift_mean) {
+  double v = (f2d(x) - w.mean) * w.inv;
+  if (!shift_mean) v += w.mean;
+  return float(v);
+}
+
+template <bool kVec>
+__global__ void whiten_kernel(float* x, const uint8_t* mask, int64_t n, const double* mom,
+                              int32_t shift_mean) {
+  const WhitenCoef w = whiten_coef(mom);
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const int64_t t0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (kVec) {
+    const int64_t nv = n >> 2;
+    float4* x4 = reinterpret_cast<float4*>(x);
+    for (int64_t j = t0; j < nv; j += stride) {
+      float4 a = x4[j];
+      const uint32_t m = mask4(mask, j);
+      if (m & 0xffu) a.x = whiten1(a.x, w, shift_mean);
+      if (m & 0xff00u) a.y = whiten1(a.y, w, shift_mean);
+      if (m & 0xff0000u) a.z = whiten1(a.z, w, shift_mean);
+      if (m & 0xff000000u) a.w = whiten1(a.w, w, shift_mean);
+      x4[j] = a;
     }
+    if (t0 < (n & 3)) {
+      const int64_t i = 4 * nv + t0;
+      if (mask == nullptr || mask[i]) x[i] = whiten1(x[i], w, shift_mean);
+    }
+  } else {
+    for (int64_t i = t0; i < n; i += stride)
+      if (mask == nullptr || mask[i]) x[i] = whiten1(x[i], w, shift_mean);
   }
+}
+
+bool vec_ok(const void* f32, const uint8_t* mask) {
+  return (reinterpret_cast<uintptr_t>(f32) & 15) == 0 && (reinterpret_cast<uintptr_t>(mask) & 3) == 0;
 }
 
 }  // namespace
@@ -293,40 +526,65 @@ int broadcast_launch(const float* vals, const int64_t* cu, int64_t nsamples, con
   YATT_REQUIRE(nsamples >= 0, YATT_ERR_CONFIG, "broadcast: n_samples must be >= 0");
   if (nsamples == 0) return YATT_OK;
   const int grid = int(min64(nsamples, int64_t(num_sms()) * 8));
-  broadcast_kernel<<<grid, 256, 0, st>>>(vals, cu, nsamples, mask, out);
+  if (vec_ok(out, mask))
+    broadcast_kernel<true><<<grid, 256, 0, st>>>(vals, cu, nsamples, mask, out);
+  else
+    broadcast_kernel<false><<<grid, 256, 0, st>>>(vals, cu, nsamples, mask, out);
   return check_launch("broadcast_kernel");
 }
 
-int gae_launch(const float* values, const float* rewards, const uint8_t* mask, const int64_t* cu,
-               int64_t nseq, float gamma, float lam, float* adv, float* ret, cudaStream_t st) {
-  YATT_REQUIRE(nseq >= 0, YATT_ERR_CONFIG, "gae: n_seqs must be >= 0");
-  YATT_REQUIRE(gamma >= 0.f && lam >= 0.f, YATT_ERR_CONFIG, "gae: gamma/lam must be >= 0");
-  if (nseq == 0) return YATT_OK;
-  const int grid = int(min64(nseq, int64_t(num_sms()) * 8));
-  gae_kernel<<<grid, kGaeThreads, 0, st>>>(values, rewards, mask, cu, nseq, double(gamma),
-                                           double(lam), adv, ret);
-  return check_launch("gae_kernel");
+size_t gae_workspace_bytes(int64_t n_tokens) {
+  return gae_ws_bytes(ceil_div(max64(n_tokens, 0), kGaeTile));
 }
 
-size_t moments_workspace_bytes() { return size_t(3) * 2 * 160 * sizeof(double); }
+int gae_launch(const float* values, const float* rewards, const uint8_t* mask, const int64_t* cu,
+               int64_t nseq, int64_t n_tokens, float gamma, float lam, float* adv, float* ret,
+               void* ws, size_t ws_bytes, cudaStream_t st) {
+  YATT_REQUIRE(nseq >= 0 && n_tokens >= 0, YATT_ERR_CONFIG, "gae: n_seqs and n_tokens must be >= 0");
+  YATT_REQUIRE(gamma >= 0.f && lam >= 0.f, YATT_ERR_CONFIG, "gae: gamma/lam must be >= 0");
+  if (nseq == 0 || n_tokens == 0) return YATT_OK;
+  YATT_REQUIRE(values && rewards && cu && adv && ret, YATT_ERR_CONFIG, "gae: null pointer");
+  const int64_t ntiles = ceil_div(n_tokens, kGaeTile);
+  YATT_REQUIRE(ws != nullptr && ws_bytes >= gae_ws_bytes(ntiles), YATT_ERR_WORKSPACE,
+               "gae: workspace too small (%zu < %zu)", ws_bytes, gae_ws_bytes(ntiles));
+  YATT_REQUIRE(ntiles < (int64_t(1) << 31), YATT_ERR_CONFIG, "gae: too many tokens");
+  YATT_TRY_CUDA(cudaMemsetAsync(ws, 0, gae_zero_bytes(ntiles), st));
+  auto a16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  const GaeWs w = gae_ws(ws, ntiles);
+  if (a16(values) && a16(rewards) && a16(mask) && a16(adv) && a16(ret))
+    gae_scan_kernel<true><<<unsigned(ntiles), kGaeThreads, 0, st>>>(
+        values, rewards, mask, cu, nseq, n_tokens, ntiles, double(gamma), double(lam), adv, ret, w);
+  else
+    gae_scan_kernel<false><<<unsigned(ntiles), kGaeThreads, 0, st>>>(
+        values, rewards, mask, cu, nseq, n_tokens, ntiles, double(gamma), double(lam), adv, ret, w);
+  return check_launch("gae_scan_kernel");
+}
+
+size_t moments_workspace_bytes() { return size_t(3) * kMomMaxParts * sizeof(double); }
 
 int masked_moments_launch(const float* x, const uint8_t* mask, int64_t n, double* out,
                           double* ws, cudaStream_t st) {
   YATT_REQUIRE(n >= 0, YATT_ERR_CONFIG, "moments: n must be >= 0");
-  const int parts = min(2 * num_sms(), 320);
-  moments_partial_kernel<<<parts, 256, 0, st>>>(x, mask, n, ws);
+  const int parts = min(4 * num_sms(), kMomMaxParts);
+  if (vec_ok(x, mask))
+    moments_partial_kernel<true><<<parts, kMomThreads, 0, st>>>(x, mask, n, ws);
+  else
+    moments_partial_kernel<false><<<parts, kMomThreads, 0, st>>>(x, mask, n, ws);
   int rc = check_launch("moments_partial_kernel");
   if (rc) return rc;
-  moments_final_kernel<<<1, 32, 0, st>>>(ws, parts, out);
-  return check_launch("moments_final_kernel");
+  reduce_parts_kernel<3><<<1, 256, 0, st>>>(ws, parts, out);
+  return check_launch("reduce_parts_kernel<3>");
 }
 
 int whiten_launch(float* x, const uint8_t* mask, int64_t n, const double* mom, int32_t shift,
                   cudaStream_t st) {
   YATT_REQUIRE(n >= 0, YATT_ERR_CONFIG, "whiten: n must be >= 0");
   if (n == 0) return YATT_OK;
-  const int grid = int(min64(ceil_div(n, 256), int64_t(num_sms()) * 8));
-  whiten_kernel<<<grid, 256, 0, st>>>(x, mask, n, mom, shift);
+  const int grid = int(min64(ceil_div(ceil_div(n, 4), 256), int64_t(num_sms()) * 8));
+  if (vec_ok(x, mask))
+    whiten_kernel<true><<<grid, 256, 0, st>>>(x, mask, n, mom, shift);
+  else
+    whiten_kernel<false><<<grid, 256, 0, st>>>(x, mask, n, mom, shift);
   return check_launch("whiten_kernel");
 }
 

@@ -32,8 +32,9 @@ int grpo_moments_launch(const float*, int64_t, uint64_t, int32_t, double*, cudaS
 int grpo_adv_launch(const float*, int64_t, uint64_t, int32_t, float, int32_t, const double*,
                     float*, cudaStream_t);
 int broadcast_launch(const float*, const int64_t*, int64_t, const uint8_t*, float*, cudaStream_t);
-int gae_launch(const float*, const float*, const uint8_t*, const int64_t*, int64_t, float, float,
-               float*, float*, cudaStream_t);
+int gae_launch(const float*, const float*, const uint8_t*, const int64_t*, int64_t, int64_t, float,
+               float, float*, float*, void*, size_t, cudaStream_t);
+size_t gae_workspace_bytes(int64_t);
 size_t moments_workspace_bytes();
 int masked_moments_launch(const float*, const uint8_t*, int64_t, double*, double*, cudaStream_t);
 int whiten_launch(float*, const uint8_t*, int64_t, const double*, int32_t, cudaStream_t);
@@ -159,7 +160,7 @@ using namespace yattb;
 extern "C" {
 
 const char* yatt_last_error_message(void) { return yattb::g_err; }
-int yatt_abi_version(void) { return 1; }
+int yatt_abi_version(void) { return 2; }
 
 int yatt_device_info(int device, char* name, int name_len, int* sm_major, int* sm_minor,
                      int* nsms) {
@@ -410,11 +411,16 @@ int yatt_broadcast_to_tokens(const float* vals, const int64_t* cu, int64_t nsamp
   return broadcast_launch(vals, cu, nsamples, mask, out, as_stream(stream));
 }
 
+size_t yatt_gae_workspace_bytes(int64_t n_tokens) { return gae_workspace_bytes(n_tokens); }
+
 int yatt_gae(const float* values, const float* rewards, const uint8_t* mask, const int64_t* cu,
-             int64_t nseq, float gamma, float lam, float* adv, float* ret, void* stream) {
+             int64_t nseq, int64_t n_tokens, float gamma, float lam, float* adv, float* ret,
+             void* ws, size_t ws_bytes, void* stream) {
   YATT_ALIGNED4("gae", values, rewards, adv, ret);
   YATT_ALIGNED("gae", cu, 8);
-  return gae_launch(values, rewards, mask, cu, nseq, gamma, lam, adv, ret, as_stream(stream));
+  YATT_ALIGNED("gae", ws, 16);
+  return gae_launch(values, rewards, mask, cu, nseq, n_tokens, gamma, lam, adv, ret, ws, ws_bytes,
+                    as_stream(stream));
 }
 
 size_t yatt_masked_moments_workspace_bytes(void) { return moments_workspace_bytes(); }

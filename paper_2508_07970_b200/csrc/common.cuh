@@ -84,6 +84,46 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
+// Exact float -> double on the integer pipes (F2F.F64.F32 runs on the XU
+// pipe, which bounds streaming fp64 kernels): normals and +-0 by rebiasing
+// the exponent; denormals, inf and NaN (rare) take the conversion instruction.
+__device__ __forceinline__ double f2d(float f) {
+  const uint32_t u = __float_as_uint(f), a = u & 0x7fffffffu;
+  if (__builtin_expect(a - 0x00800000u >= 0x7f000000u, 0) && a != 0u) return double(f);
+  const uint32_t hi = (u & 0x80000000u) | (a != 0u ? (a >> 3) + 0x38000000u : 0u);
+  return __hiloint2double(int(hi), int(u << 29));
+}
+
+// Deterministic reduction of nparts partial records of kF doubles
+// (part[kF*i + f]) into out[f], one 256-thread block: thread t sums parts
+// t, t+256, ... in order, then a fixed-shape warp/block tree.  Same order on
+// every run for a given nparts.
+template <int kF>
+__global__ void __launch_bounds__(256) reduce_parts_kernel(const double* part, int nparts,
+                                                           double* out) {
+  __shared__ double red[kF][8];
+  double v[kF];
+#pragma unroll
+  for (int f = 0; f < kF; ++f) v[f] = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += 256) {
+#pragma unroll
+    for (int f = 0; f < kF; ++f) v[f] += part[kF * i + f];
+  }
+  const int w = threadIdx.x >> 5;
+#pragma unroll
+  for (int f = 0; f < kF; ++f) {
+    v[f] = warp_sum(v[f]);
+    if ((threadIdx.x & 31) == 0) red[f][w] = v[f];
+  }
+  __syncthreads();
+  if (threadIdx.x < kF) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += red[threadIdx.x][k];
+    out[threadIdx.x] = s;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // mbarrier + bulk-copy (TMA) PTX wrappers
 // ---------------------------------------------------------------------------

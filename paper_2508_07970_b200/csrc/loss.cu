@@ -2,7 +2,8 @@
 // token sums.  Replaces the Training-stage cost stand-in of the reference
 // (proj/src/simcore.cpp:404-406) for the loss value itself.
 //
-// Per valid token t (fp64 arithmetic, deterministic reduction order):
+// Per valid token t (fp64 ratio/clip arithmetic, deterministic reduction
+// order; see Acc below for how the sums are formed):
 //   ratio = exp(logp - old_logp)
 //   pg    = max(-A*ratio, -A*clip(ratio, 1-eps_lo, 1+eps_hi))     [clipped if 2nd > 1st]
 //   dual clip (clip_ratio_c > 1, A < 0): pg = min(pg, -A*clip_ratio_c)
@@ -26,27 +27,86 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kFields = 8;  // yatt_loss_sums fields
 
-struct TokenTerms {
-  double L, pg, kl, ent, clipped, ratio;
+// Per-thread accumulators.  Only the ratio/clip algebra is fp64 per token;
+// loss_sum follows by linearity (sum L = sum pg + kl_coef sum kl -
+// entropy_coef sum H), kl and H enter as fp32 sums of at most four tokens
+// (one rounding per vector, relative 2^-23 of same-sign terms), counts are
+// integers.  Inputs reach fp64 through f2d (integer pipes).
+struct Acc {
+  double pg = 0, ratio = 0, kl = 0, ent = 0;
+  int32_t clip = 0, cnt = 0;
+};
+struct LossCfg {
+  double lo, hi, cc;
+  bool dual;
+};
+__device__ __forceinline__ LossCfg loss_cfg(const yatt_loss_config& c) {
+  return LossCfg{1.0 - double(c.clip_low), 1.0 + double(c.clip_high), double(c.clip_ratio_c),
+                 c.clip_ratio_c > 1.f};
+}
+
+__device__ __forceinline__ void pg_term(float logp, float old_logp, float A, const LossCfg& c,
+                                        Acc& s) {
+  const double ratio = exp(f2d(logp) - f2d(old_logp));
+  const double a = f2d(A);
+  const double pg1 = -a * ratio;
+  const double pg2 = -a * fmin(fmax(ratio, c.lo), c.hi);
+  double pg = fmax(pg1, pg2);
+  s.clip += pg2 > pg1 ? 1 : 0;
+  if (c.dual && a < 0.0) pg = fmin(pg, -a * c.cc);
+  s.pg += pg;
+  s.ratio += ratio;
+  s.cnt += 1;
+}
+
+struct LossIn {
+  const float *logp, *old_logp, *adv, *kl, *ent;
+  const uint8_t* mask;
 };
 
-__device__ __forceinline__ TokenTerms token_terms(float logp, float old_logp, float A, float kl,
-                                                  float H, const yatt_loss_config& c) {
-  TokenTerms t;
-  const double ratio = exp(double(logp) - double(old_logp));
-  const double a = double(A);
-  const double pg1 = -a * ratio;
-  const double lo = 1.0 - double(c.clip_low), hi = 1.0 + double(c.clip_high);
-  const double pg2 = -a * fmin(fmax(ratio, lo), hi);
-  double pg = fmax(pg1, pg2);
-  t.clipped = pg2 > pg1 ? 1.0 : 0.0;
-  if (c.clip_ratio_c > 1.f && a < 0.0) pg = fmin(pg, -a * double(c.clip_ratio_c));
-  t.pg = pg;
-  t.kl = double(kl);
-  t.ent = double(H);
-  t.L = pg + double(c.kl_coef) * t.kl - double(c.entropy_coef) * t.ent;
-  t.ratio = ratio;
-  return t;
+__device__ __forceinline__ float4 ldg4(const float* p, int64_t i) {
+  return __ldg(reinterpret_cast<const float4*>(p + i));
+}
+
+// Token i (scalar path).
+__device__ __forceinline__ void add_token(const LossIn& in, int64_t i, const LossCfg& c, Acc& s) {
+  if (in.mask != nullptr && !in.mask[i]) return;
+  pg_term(__ldg(in.logp + i), __ldg(in.old_logp + i), __ldg(in.adv + i), c, s);
+  if (in.kl) s.kl += f2d(__ldg(in.kl + i));
+  if (in.ent) s.ent += f2d(__ldg(in.ent + i));
+}
+
+// Four tokens [4j, 4j+4) from 16-byte loads (float inputs 16-B aligned, mask
+// 4-B aligned).
+struct Vec4 {
+  float4 lp, olp, a, kl, h;
+  uint32_t m;
+};
+__device__ __forceinline__ Vec4 load_vec(const LossIn& in, int64_t j) {
+  Vec4 x;
+  const int64_t i = 4 * j;
+  x.lp = ldg4(in.logp, i);
+  x.olp = ldg4(in.old_logp, i);
+  x.a = ldg4(in.adv, i);
+  x.kl = in.kl ? ldg4(in.kl, i) : make_float4(0.f, 0.f, 0.f, 0.f);
+  x.h = in.ent ? ldg4(in.ent, i) : make_float4(0.f, 0.f, 0.f, 0.f);
+  x.m = in.mask ? __ldg(reinterpret_cast<const uint32_t*>(in.mask + i)) : 0x01010101u;
+  return x;
+}
+__device__ __forceinline__ void add_vec(const Vec4& x, const LossCfg& c, Acc& s) {
+  const float lp[4] = {x.lp.x, x.lp.y, x.lp.z, x.lp.w}, olp[4] = {x.olp.x, x.olp.y, x.olp.z, x.olp.w};
+  const float a[4] = {x.a.x, x.a.y, x.a.z, x.a.w}, kl[4] = {x.kl.x, x.kl.y, x.kl.z, x.kl.w};
+  const float h[4] = {x.h.x, x.h.y, x.h.z, x.h.w};
+  float k4 = 0.f, h4 = 0.f;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (((x.m >> (8 * k)) & 0xffu) == 0) continue;
+    pg_term(lp[k], olp[k], a[k], c, s);
+    k4 += kl[k];
+    h4 += h[k];
+  }
+  s.kl += f2d(k4);
+  s.ent += f2d(h4);
 }
 
 // Block-wide sum of kFields doubles; result valid in thread 0.
@@ -69,88 +129,123 @@ __device__ __forceinline__ void block_sum(double (&v)[kFields], double (*red)[kT
   }
 }
 
-// agg_mode 0: contiguous token ranges per block.
-__global__ void __launch_bounds__(kThreads) loss_token_kernel(
-    const float* logp, const float* old_logp, const float* adv, const float* kl,
-    const float* ent, const uint8_t* mask, int64_t n, const yatt_loss_config c, double* part) {
-  __shared__ double red[kFields][kThreads / 32];
-  double v[kFields] = {0, 0, 0, 0, 0, 0, 0, 0};
-  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
-  const int64_t lo = int64_t(blockIdx.x) * per, hi = min64(n, lo + per);
-  for (int64_t i = lo + threadIdx.x; i < hi; i += kThreads) {
-    if (mask != nullptr && !mask[i]) continue;
-    const TokenTerms t = token_terms(logp[i], old_logp[i], adv[i], kl ? kl[i] : 0.f,
-                                     ent ? ent[i] : 0.f, c);
-    v[0] += t.L;
-    v[1] += t.pg;
-    v[2] += t.kl;
-    v[3] += t.ent;
-    v[4] += t.clipped;
-    v[5] += t.ratio;
-    v[6] += 1.0;
-  }
+// Writes the block's record: loss_sum from the linear combination unless the
+// caller formed it per sequence (seq modes pass loss/seqs in v0/v7).
+__device__ __forceinline__ void emit_part(const Acc& s, double v0, double v7,
+                                          const yatt_loss_config& c, bool token_mode,
+                                          double (*red)[kThreads / 32], double* part) {
+  double v[kFields] = {v0, s.pg, s.kl, s.ent, double(s.clip), s.ratio, double(s.cnt), v7};
   block_sum(v, red);
   if (threadIdx.x == 0) {
+    if (token_mode) v[0] = v[1] + double(c.kl_coef) * v[2] - double(c.entropy_coef) * v[3];
 #pragma unroll
     for (int f = 0; f < kFields; ++f) part[kFields * blockIdx.x + f] = v[f];
   }
 }
 
-// agg_mode 1/2: one warp per sequence; the sequence term is formed in-warp.
-__global__ void __launch_bounds__(kThreads) loss_seq_kernel(
-    const float* logp, const float* old_logp, const float* adv, const float* kl,
-    const float* ent, const uint8_t* mask, const int64_t* cu, int64_t nseq,
-    const yatt_loss_config c, double* part) {
+// agg_mode 0: contiguous ranges of 4-token vectors per block, two vectors in
+// flight per thread; the n % 4 tail goes to the last block.
+template <bool kVec>
+__global__ void __launch_bounds__(kThreads) loss_token_kernel(const LossIn in, int64_t n,
+                                                              const yatt_loss_config cfg,
+                                                              double* part) {
   __shared__ double red[kFields][kThreads / 32];
-  double v[kFields] = {0, 0, 0, 0, 0, 0, 0, 0};
-  const int lane = threadIdx.x & 31;
-  const int64_t per = (nseq + gridDim.x - 1) / gridDim.x;
-  const int64_t lo = int64_t(blockIdx.x) * per, hi = min64(nseq, lo + per);
-  for (int64_t s = lo + (threadIdx.x >> 5); s < hi; s += kThreads / 32) {
-    double sl = 0, cnt = 0;
-    for (int64_t i = cu[s] + lane; i < cu[s + 1]; i += 32) {
-      if (mask != nullptr && !mask[i]) continue;
-      const TokenTerms t = token_terms(logp[i], old_logp[i], adv[i], kl ? kl[i] : 0.f,
-                                       ent ? ent[i] : 0.f, c);
-      sl += t.L;
-      v[1] += t.pg;
-      v[2] += t.kl;
-      v[3] += t.ent;
-      v[4] += t.clipped;
-      v[5] += t.ratio;
-      cnt += 1.0;
+  const LossCfg c = loss_cfg(cfg);
+  Acc s;
+  if (kVec) {
+    const int64_t nv = n >> 2;
+    const int64_t per = (nv + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = int64_t(blockIdx.x) * per, hi = min64(nv, lo + per);
+    int64_t j = lo + threadIdx.x;
+    for (; j + kThreads < hi; j += 2 * kThreads) {
+      const Vec4 x0 = load_vec(in, j), x1 = load_vec(in, j + kThreads);
+      add_vec(x0, c, s);
+      add_vec(x1, c, s);
     }
-    sl = warp_sum(sl);
-    cnt = warp_sum(cnt);
-    if (lane == 0 && cnt > 0) {
-      v[0] += c.agg_mode == 1 ? sl / cnt : sl;
-      v[6] += cnt;
-      v[7] += 1.0;
-    }
+    if (j < hi) add_vec(load_vec(in, j), c, s);
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x < (n & 3)) add_token(in, 4 * nv + threadIdx.x, c, s);
+  } else {
+    const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = int64_t(blockIdx.x) * per, hi = min64(n, lo + per);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += kThreads) add_token(in, i, c, s);
   }
-  block_sum(v, red);
-  if (threadIdx.x == 0) {
+  emit_part(s, 0.0, 0.0, cfg, true, red, part);
+}
+
+// agg_mode 1/2: one CTA per sequence (grid-stride over sequences); the
+// sequence's (pg, kl, H, count) are block-reduced to form its term, the other
+// fields accumulate per thread.  Vector path: scalar head up to the first
+// 4-aligned token, 16-byte body (two vectors in flight), scalar tail.
+template <bool kVec>
+__global__ void __launch_bounds__(kThreads) loss_seq_kernel(const LossIn in, const int64_t* cu,
+                                                            int64_t nseq,
+                                                            const yatt_loss_config cfg,
+                                                            double* part) {
+  __shared__ double red[kFields][kThreads / 32];
+  __shared__ double sred[4][kThreads / 32];
+  const LossCfg c = loss_cfg(cfg);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const double beta = cfg.kl_coef, ec = cfg.entropy_coef;
+  Acc tot;
+  double loss = 0.0, seqs = 0.0;  // thread 0 only
+  for (int64_t sq = blockIdx.x; sq < nseq; sq += gridDim.x) {
+    const int64_t b = __ldg(cu + sq), e = __ldg(cu + sq + 1);
+    Acc s;
+    if (kVec) {
+      const int64_t hb = min64(e, (b + 3) & ~int64_t(3));  // end of the scalar head
+      const int64_t jb = hb >> 2, je = max64(jb, e >> 2);   // body vectors [jb, je)
+      if (b + int64_t(threadIdx.x) < hb) add_token(in, b + threadIdx.x, c, s);
+      int64_t j = jb + threadIdx.x;
+      for (; j + kThreads < je; j += 2 * kThreads) {
+        const Vec4 x0 = load_vec(in, j), x1 = load_vec(in, j + kThreads);
+        add_vec(x0, c, s);
+        add_vec(x1, c, s);
+      }
+      if (j < je) add_vec(load_vec(in, j), c, s);
+      const int64_t tb = max64(hb, 4 * je);
+      if (tb + int64_t(threadIdx.x) < e) add_token(in, tb + threadIdx.x, c, s);
+    } else {
+      for (int64_t i = b + threadIdx.x; i < e; i += kThreads) add_token(in, i, c, s);
+    }
+    double q[4] = {s.pg, s.kl, s.ent, double(s.cnt)};
 #pragma unroll
-    for (int f = 0; f < kFields; ++f) part[kFields * blockIdx.x + f] = v[f];
+    for (int f = 0; f < 4; ++f) {
+      q[f] = warp_sum(q[f]);
+      if (lane == 0) sred[f][w] = q[f];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t[4] = {0, 0, 0, 0};
+      for (int k = 0; k < kThreads / 32; ++k)
+#pragma unroll
+        for (int f = 0; f < 4; ++f) t[f] += sred[f][k];
+      if (t[3] > 0) {
+        const double Ls = t[0] + beta * t[1] - ec * t[2];
+        loss += cfg.agg_mode == 1 ? Ls / t[3] : Ls;
+        seqs += 1.0;
+      }
+    }
+    __syncthreads();
+    tot.pg += s.pg;
+    tot.kl += s.kl;
+    tot.ent += s.ent;
+    tot.ratio += s.ratio;
+    tot.clip += s.clip;
+    tot.cnt += s.cnt;
   }
+  emit_part(tot, loss, seqs, cfg, false, red, part);
 }
-
-__global__ void loss_final_kernel(const double* part, int nparts, int32_t agg_mode,
-                                  yatt_loss_sums* out) {
-  const int f = threadIdx.x;
-  if (f >= kFields) return;
-  double s = 0;
-  for (int i = 0; i < nparts; ++i) s += part[kFields * i + f];
-  double* o = reinterpret_cast<double*>(out);
-  o[f] = s;
-  (void)agg_mode;
-}
-
-int loss_parts() { return min(2 * num_sms(), 512); }
 
 }  // namespace
 
-size_t loss_workspace_bytes() { return size_t(512) * kFields * sizeof(double); }
+
+namespace {
+constexpr int kMaxParts = 2048;
+int token_parts() { return min(4 * num_sms(), kMaxParts); }
+int seq_parts(int64_t nseq) { return int(max64(1, min64(nseq, int64_t(8) * num_sms()))); }
+}  // namespace
+
+size_t loss_workspace_bytes() { return size_t(kMaxParts) * kFields * sizeof(double); }
 
 int policy_loss_launch(const float* logp, const float* old_logp, const float* adv,
                        const float* kl, const float* ent, const uint8_t* mask, int64_t n,
@@ -166,19 +261,28 @@ int policy_loss_launch(const float* logp, const float* old_logp, const float* ad
                "policy_loss: seq-mean modes need cu_seqlens");
   YATT_REQUIRE(ws_bytes >= loss_workspace_bytes() && ws != nullptr, YATT_ERR_WORKSPACE,
                "policy_loss: workspace too small (%zu < %zu)", ws_bytes, loss_workspace_bytes());
-  const int parts = loss_parts();
+  const int parts = cfg->agg_mode == 0 ? token_parts() : int(min64(seq_parts(nseq), kMaxParts));
   double* part = static_cast<double*>(ws);
+  const LossIn in{logp, old_logp, adv, kl, ent, mask};
+  auto a16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  const bool vec = a16(logp) && a16(old_logp) && a16(adv) && a16(kl) && a16(ent) &&
+                   (reinterpret_cast<uintptr_t>(mask) & 3) == 0;
   if (cfg->agg_mode == 0) {
-    loss_token_kernel<<<parts, kThreads, 0, st>>>(logp, old_logp, adv, kl, ent, mask, n, *cfg,
-                                                  part);
+    if (vec)
+      loss_token_kernel<true><<<parts, kThreads, 0, st>>>(in, n, *cfg, part);
+    else
+      loss_token_kernel<false><<<parts, kThreads, 0, st>>>(in, n, *cfg, part);
   } else {
-    loss_seq_kernel<<<parts, kThreads, 0, st>>>(logp, old_logp, adv, kl, ent, mask, cu, nseq,
-                                                *cfg, part);
+    if (vec)
+      loss_seq_kernel<true><<<parts, kThreads, 0, st>>>(in, cu, nseq, *cfg, part);
+    else
+      loss_seq_kernel<false><<<parts, kThreads, 0, st>>>(in, cu, nseq, *cfg, part);
   }
   int rc = check_launch("policy_loss_kernel");
   if (rc) return rc;
-  loss_final_kernel<<<1, 32, 0, st>>>(part, parts, cfg->agg_mode, sums);
-  return check_launch("loss_final_kernel");
+  static_assert(sizeof(yatt_loss_sums) == kFields * sizeof(double), "yatt_loss_sums layout");
+  reduce_parts_kernel<kFields><<<1, 256, 0, st>>>(part, parts, reinterpret_cast<double*>(sums));
+  return check_launch("reduce_parts_kernel<8>");
 }
 
 double loss_finalize(const yatt_loss_sums* s, const yatt_loss_config* c) {

@@ -507,12 +507,14 @@ void GaeConfig::validate() const {
   if (!(gamma >= 0) || !(lam >= 0)) throw ConfigError("gamma and lam must be non-negative");
 }
 
+std::size_t gae_workspace_bytes(std::int64_t n_tokens) { return yatt_gae_workspace_bytes(n_tokens); }
+
 void gae(const float* values, const float* rewards, const std::uint8_t* mask,
-         const std::int64_t* cu, std::int64_t n_seqs, const GaeConfig& c, float* adv,
-         float* ret, void* stream) {
+         const std::int64_t* cu, std::int64_t n_seqs, std::int64_t n_tokens, const GaeConfig& c,
+         float* adv, float* ret, void* ws, std::size_t ws_bytes, void* stream) {
   c.validate();
-  detail::throw_status(yatt_gae(values, rewards, mask, cu, n_seqs, c.gamma, c.lam, adv, ret,
-                                stream));
+  detail::throw_status(yatt_gae(values, rewards, mask, cu, n_seqs, n_tokens, c.gamma, c.lam, adv,
+                                ret, ws, ws_bytes, stream));
 }
 
 void PolicyLossConfig::validate() const {

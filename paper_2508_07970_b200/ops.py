@@ -165,8 +165,12 @@ def gae(values: torch.Tensor, rewards: torch.Tensor, cu_seqlens: torch.Tensor,
     _dev(cu_seqlens, torch.int64, "cu_seqlens")
     adv = torch.empty_like(values)
     ret = torch.empty_like(values)
+    n = values.numel()
+    wsb = lib().yatt_gae_workspace_bytes(n)
+    ws = torch.empty((max(wsb, 16),), dtype=torch.uint8, device=values.device)
     check(lib().yatt_gae(_p(values), _p(rewards), _p(_mask(mask)), _p(cu_seqlens),
-                         cu_seqlens.numel() - 1, gamma, lam, _p(adv), _p(ret), _st()))
+                         cu_seqlens.numel() - 1, n, gamma, lam, _p(adv), _p(ret), _p(ws), wsb,
+                         _st()))
     return adv, ret
 
 

@@ -24,7 +24,7 @@ def test_library_exports_every_declared_symbol():
     missing = [s for s in declared_symbols() if not hasattr(h, s)]
     assert not missing, missing
     assert set(declared_symbols()) <= set(SIGNATURES) | {"yatt_abi_version"}
-    assert h.yatt_abi_version() == 1
+    assert h.yatt_abi_version() == 2
 
 
 def test_cpp_dropin_api_is_exported():
@@ -88,7 +88,7 @@ def test_misaligned_pointers_are_config_errors_before_any_launch():
     from paper_2508_07970_b200._lib import check
     A, M = 0x10000, 0x10001  # aligned / misaligned fake device addresses
     calls = [
-        ("gae", lambda: lib().yatt_gae(A, A, None, A, 1, 1.0, 1.0, A + 2, A, None)),
+        ("gae", lambda: lib().yatt_gae(A, A, None, A, 1, 1, 1.0, 1.0, A + 2, A, A, 64, None)),
         ("coef", lambda: lib().yatt_logits_backward(A, None, A, None, 1, 8, A + 4, 0, A, None)),
         ("mbs", lambda: lib().yatt_microbatch_aggregates(A, A, None, 1, 1, 0, A + 4, None)),
         ("sums", lambda: lib().yatt_policy_loss(A, A, A, A, A, None, 1, None, 0, None, A + 4, A, 64,

@@ -92,6 +92,54 @@ def test_gae_matches_oracle(cuda, masked):
     assert O.max_rel_error(ret.cpu().numpy(), e_ret.astype(np.float32)) <= TOL
 
 
+@pytest.mark.parametrize("layout", ["multi_tile", "tiny_seqs", "offset_and_pad", "unaligned"])
+def test_gae_tiled_scan_layouts(cuda, layout):
+    """The scan's tile carries: sequences spanning several 4,096-token tiles,
+    thousands of 1-token sequences per tile, packed arrays that start after
+    token 0 / end before n_tokens (untouched outside), and an unaligned view
+    (scalar path)."""
+    rng = np.random.default_rng(7)
+    lead, tail, shift = 0, 0, 0
+    if layout == "multi_tile":
+        lens = np.array([3 * 4096 + 5, 4096, 1, 4095, 20000, 3])
+    elif layout == "tiny_seqs":
+        lens = np.concatenate([np.ones(5000, dtype=np.int64), [4097], np.ones(3000, dtype=np.int64),
+                               rng.integers(1, 6, size=2000)])
+    elif layout == "offset_and_pad":
+        lens, lead, tail = rng.integers(1, 9000, size=40), 4093, 5000
+    else:
+        lens, shift = rng.integers(1, 9000, size=40), 1
+    n = lead + int(lens.sum()) + tail
+    cu = np.concatenate([[lead], lead + np.cumsum(lens)]).astype(np.int64)
+    buf = ops.synth_floats(5, 106, 0, n + shift, "value", device=cuda)
+    v = buf[shift:]
+    r = (ops.synth_floats(5, 111, 0, n, "kl", device=cuda) * 4 - 0.5).contiguous()
+    for masked in (False, True):
+        m = torch.as_tensor((rng.random(n) < 0.8).astype(np.uint8), device=cuda) if masked else None
+        adv, ret = ops.gae(v, r, torch.as_tensor(cu, device=cuda), m, 0.99, 0.95)
+        hv, hr = v.cpu().numpy(), r.cpu().numpy()
+        e_adv, e_ret = O.gae(hv, hr, cu, None if m is None else m.cpu().numpy(), 0.99, 0.95)
+        sl = slice(lead, n - tail)
+        assert O.max_rel_error(adv.cpu().numpy()[sl], e_adv[sl].astype(np.float32)) <= TOL
+        assert O.max_rel_error(ret.cpu().numpy()[sl], e_ret[sl].astype(np.float32)) <= TOL
+    if lead or tail:  # tokens outside [cu[0], cu[n_seqs]) keep their contents
+        from paper_2508_07970_b200._lib import check, lib
+        a = torch.full((n,), 7.0, device=cuda)
+        b = torch.full((n,), 7.0, device=cuda)
+        wsb = lib().yatt_gae_workspace_bytes(n)
+        ws = torch.empty((wsb,), dtype=torch.uint8, device=cuda)
+        d_cu = torch.as_tensor(cu, device=cuda)
+        check(lib().yatt_gae(v.data_ptr(), r.data_ptr(), None, d_cu.data_ptr(), len(lens), n,
+                             0.99, 0.95, a.data_ptr(), b.data_ptr(), ws.data_ptr(), wsb,
+                             torch.cuda.current_stream().cuda_stream))
+        out = torch.cat([a[:lead], a[n - tail:], b[:lead], b[n - tail:]])
+        assert bool((out == 7.0).all())
+        with pytest.raises(ConfigError):  # workspace sized for fewer tokens
+            check(lib().yatt_gae(v.data_ptr(), r.data_ptr(), None, d_cu.data_ptr(), len(lens), n,
+                                 0.99, 0.95, a.data_ptr(), b.data_ptr(), ws.data_ptr(),
+                                 lib().yatt_gae_workspace_bytes(n - 4096), None))
+
+
 def test_gae_gamma_lambda_sweep_and_empty(cuda):
     cu = torch.tensor([0, 100, 100, 300], dtype=torch.int64, device=cuda)
     v = torch.randn(300, device=cuda)

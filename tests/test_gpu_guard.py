@@ -108,8 +108,10 @@ def test_gae_moments_whiten_loss_guard(cuda, lens):
     v = torch.randn(n, device=cuda)
     m = (torch.rand(n, device=cuda) < 0.7).to(torch.uint8)
     adv, ret = Guarded(n, torch.float32, cuda), Guarded(n, torch.float32, cuda)
+    gwb = lib().yatt_gae_workspace_bytes(n)
+    gws = Guarded(gwb, torch.uint8, cuda, shift=0)
     check(lib().yatt_gae(v.data_ptr(), (v * 0.3).data_ptr(), m.data_ptr(), cu.data_ptr(),
-                         len(lens), 1.0, 0.95, adv.p, ret.p, _st()))
+                         len(lens), n, 1.0, 0.95, adv.p, ret.p, gws.p, gwb, _st()))
     mom = Guarded(3, torch.float64, cuda)
     wsb = lib().yatt_masked_moments_workspace_bytes()
     ws = Guarded(wsb, torch.uint8, cuda, shift=0)
@@ -126,7 +128,7 @@ def test_gae_moments_whiten_loss_guard(cuda, lens):
         torch.cuda.synchronize()
         assert sums.intact() and lws.intact()
     torch.cuda.synchronize()
-    assert adv.intact() and ret.intact() and mom.intact() and ws.intact()
+    assert adv.intact() and ret.intact() and mom.intact() and ws.intact() and gws.intact()
 
 
 @pytest.mark.parametrize("n,G", [(16, 16), (1000, 8), (5000, 4)])

@@ -11,7 +11,8 @@ achieved algorithmic GB/s vs the measured HBM peak.  One JSON line per op.
   A6  gather_varlen     survivors' 17 B/token payload (~135M tokens total)
   R3  shard_round       16,384 samples, 8 controller shards, one launch
   R10 sort_order_desc   16,384 lengths
-Timing: CUDA events, median of 20 after 3 warm-ups, inputs resident.
+Timing: CUDA-graph replay between CUDA events (no host overhead), L2 flushed
+before each replay, median of 20 after 3 warm-ups, inputs resident.
 """
 import json
 import statistics
@@ -29,15 +30,41 @@ PEAK = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").
     "hbm_gbs"] if (Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").exists() else 6650.0
 
 
+_FLUSH = None
+
+
 def timeit(fn, iters=20, warm=3):
+    """Device time of one call: the call is captured once into a CUDA graph
+    (so host-side Python/ctypes overhead is not timed) and replayed between
+    CUDA events, with L2 flushed (256 MB write) before every replay.  Ops that
+    cannot be captured (host syncs inside) fall back to eager timing."""
+    global _FLUSH
+    if _FLUSH is None:
+        _FLUSH = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
+    run = fn
+    try:
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            fn()
+        torch.cuda.current_stream().wait_stream(s)
+        with torch.cuda.graph(g):
+            fn()
+        g.replay()
+        torch.cuda.synchronize()
+        run = g.replay
+    except Exception:  # noqa: BLE001 - host sync inside the op: time it eagerly
+        torch.cuda.synchronize()
     ts = []
     for _ in range(iters):
+        _FLUSH.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        fn()
+        run()
         b.record()
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
