@@ -89,13 +89,14 @@ def build(verbose: bool = False) -> Path:
 
 
 def build_variant(name: str, defines: dict) -> Path:
-    """Experiment build: token_stats.cu recompiled with -D overrides, linked
-    into _variants/libyatt_b200_<name>.so (load it with YATT_B200_LIB=...)."""
+    """Experiment build: every source recompiled with -D overrides (knobs are
+    namespaced, e.g. YATT_A1_*, YATT_GAE_*), linked into
+    _variants/libyatt_b200_<name>.so (load it with YATT_B200_LIB=...)."""
     BUILD.mkdir(parents=True, exist_ok=True)
     extra = tuple(f"-D{k}={v}" for k, v in sorted(defines.items()))
     objs = []
     for src in sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp")):
-        objs.append(_compile(src, False, extra if src.name == "token_stats.cu" else ()))
+        objs.append(_compile(src, False, extra if src.suffix == ".cu" else ()))
     out = PKG / "_variants" / f"libyatt_b200_{name}.so"
     out.parent.mkdir(exist_ok=True)
     cmd = [nvcc(), "-shared", "-o", str(out)] + ARCH + [str(o) for o in objs] + [

@@ -128,42 +128,46 @@ __device__ __forceinline__ Aff shfl_down_aff(const Aff& x, int d) {
 }
 
 // Single-pass scan over the packed token array with decoupled look-back.
-// The array is cut into 2,048-token tiles (thread i of a 128-thread CTA owns
-// 16 contiguous tokens, loaded/stored as float4; ~5 CTAs per SM hide each
-// other's look-back latency).  CTAs claim tiles right to
-// left by an atomic ticket, so a tile only waits on tiles claimed by CTAs
-// already running.  Each tile publishes its composite map (flag 1) and, once
-// its incoming state is known, its outgoing state (flag 2); a tile holding a
-// sequence end has a constant composite and publishes flag 2 at once, so
-// look-back chains stop at the first sequence boundary.  Bytes: 9 read +
-// 8 written per token, once.
+// The array is cut into 2,048-token tiles; thread i of a 128-thread CTA owns
+// 16 contiguous tokens.  Persistent CTAs claim tiles right to left by an
+// atomic ticket (a tile only waits on tiles with earlier tickets, whose
+// holders are running: the smallest unfinished ticket is always being
+// processed, so the scan cannot deadlock) and keep the NEXT tile's values,
+// rewards and mask in flight (cp.async.bulk into the other shared-memory
+// stage) while the current tile is scanned.  Each tile publishes its
+// composite map (flag 1) and, once its incoming state is known, its outgoing
+// state (flag 2); a tile holding a sequence end has a constant composite and
+// publishes flag 2 at once, so look-back chains stop at the first sequence
+// boundary.  Bytes: 9 read + 8 written per token, once.
 constexpr int kGaeThreads = 128;
 constexpr int kGaeTpt = 16;
 constexpr int kGaeTile = kGaeThreads * kGaeTpt;
 
-struct GaeWs {  // device workspace layout (yatt_gae_workspace_bytes)
+// Device workspace (yatt_gae_workspace_bytes): ticket | incl[ntiles] |
+// aflag[ntiles] (zeroed per call) | agg[ntiles].  incl[t] is one 16-byte
+// record {double A; float V; u32 flag}: the state leaving tile t to the left
+// (V is an input value or 0, so fp32 holds it exactly) and its ready flag in
+// the same single 16-byte store, so a look-back step is one L2 round trip.
+struct GaeWs {
   uint32_t* ticket;
-  uint32_t* flag;  // [ntiles]
-  Aff* agg;        // [ntiles]
-  double2* incl;   // [ntiles] state (A, V) leaving the tile to the left
+  uint4* incl;      // [ntiles]
+  uint32_t* aflag;  // [ntiles] agg[t] published
+  Aff* agg;         // [ntiles] composite map of tile t
 };
 __host__ __device__ inline size_t gae_align(size_t x) { return (x + 15) & ~size_t(15); }
 __host__ __device__ inline GaeWs gae_ws(void* base, int64_t ntiles) {
   uint8_t* b = static_cast<uint8_t*>(base);
   GaeWs w;
   w.ticket = reinterpret_cast<uint32_t*>(b);
-  w.flag = reinterpret_cast<uint32_t*>(b + 16);
-  size_t off = gae_align(16 + 4 * size_t(ntiles));
-  w.agg = reinterpret_cast<Aff*>(b + off);
-  off = gae_align(off + sizeof(Aff) * size_t(ntiles));
-  w.incl = reinterpret_cast<double2*>(b + off);
+  w.incl = reinterpret_cast<uint4*>(b + 16);
+  w.aflag = reinterpret_cast<uint32_t*>(b + 16 + 16 * size_t(ntiles));
+  w.agg = reinterpret_cast<Aff*>(b + gae_align(16 + 20 * size_t(ntiles)));
   return w;
 }
 size_t gae_ws_bytes(int64_t ntiles) {
-  return gae_align(gae_align(gae_align(16 + 4 * size_t(ntiles)) + sizeof(Aff) * size_t(ntiles)) +
-                   sizeof(double2) * size_t(ntiles));
+  return gae_align(16 + 20 * size_t(ntiles)) + sizeof(Aff) * size_t(ntiles);
 }
-size_t gae_zero_bytes(int64_t ntiles) { return 16 + 4 * size_t(ntiles); }
+size_t gae_zero_bytes(int64_t ntiles) { return 16 + 20 * size_t(ntiles); }
 
 __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -172,6 +176,21 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+__device__ __forceinline__ void st_incl(uint4* p, double A, double V) {
+  const uint4 w = make_uint4(uint32_t(__double2loint(A)), uint32_t(__double2hiint(A)),
+                             __float_as_uint(float(V)), 2u);
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(w.x), "r"(w.y),
+               "r"(w.z), "r"(w.w)
+               : "memory");
+}
+__device__ __forceinline__ uint4 ld_incl(const uint4* p) {
+  uint4 w;
+  asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+               : "l"(p)
+               : "memory");
+  return w;
 }
 
 // First index k in [k0, k1) with a[k] >= key (k1 if none), a non-decreasing;
@@ -195,178 +214,256 @@ __device__ int64_t warp_lower_bound(const int64_t* a, int64_t k0, int64_t k1, in
   return bal ? k0 + __ffs(bal) - 1 : k1;
 }
 
-template <bool kVec>
-__global__ void __launch_bounds__(kGaeThreads) gae_scan_kernel(
-    const float* __restrict__ values, const float* __restrict__ rewards,
-    const uint8_t* __restrict__ mask, const int64_t* __restrict__ cu, int64_t nseq,
-    int64_t n_tokens, int64_t ntiles, double gamma, double lam, float* adv, float* ret, GaeWs ws) {
+struct __align__(128) GaeStage {
+  float v[kGaeTile];
+  float r[kGaeTile];
+  uint8_t m[kGaeTile];
+};
+
+struct GaeArgs {
+  const float* values;
+  const float* rewards;
+  const uint8_t* mask;
+  const int64_t* cu;
+  int64_t nseq, n_tokens, ntiles;
+  double gamma, lam;
+  float* adv;
+  float* ret;
+};
+
+#ifdef YATT_GAE_PROFILE
+// Phase timestamps per tile (variant builds only): start, data ready, ends
+// marked, scan done, carry known, tile done.
+__device__ long long g_gae_prof[16384][6];
+#define GAE_STAMP(k) \
+  if (tid == ((k) == 4 ? kGaeThreads - 32 : 0) && t < 16384) g_gae_prof[t][k] = clock64()
+#else
+#define GAE_STAMP(k)
+#endif
+
+template <bool kBulk>
+__global__ void __launch_bounds__(kGaeThreads) gae_pipe_kernel(const GaeArgs g, GaeWs ws) {
+  __shared__ GaeStage stg[2];
+  __shared__ __align__(8) uint64_t full[2];
   __shared__ uint32_t last_bits[kGaeTile / 32];  // bit j: token lo+j ends a sequence
   __shared__ Aff wtot[kGaeThreads / 32];
   __shared__ double2 carry;
-  __shared__ int64_t s_tile, s_k0, s_k1;
+  __shared__ int64_t s_tile[2], s_k[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const double gl = gamma * lam;
-
-  if (tid == 0) s_tile = ntiles - 1 - int64_t(atomicAdd(ws.ticket, 1u));
-  for (int i = tid; i < kGaeTile / 32; i += kGaeThreads) last_bits[i] = 0u;
-  __syncthreads();
-  const int64_t t = s_tile;
-  const int64_t lo = t * kGaeTile, hi = min64(n_tokens, lo + kGaeTile);
-  const int64_t x0 = lo + int64_t(tid) * kGaeTpt;  // this thread's first token
-  const int nmine = int(max64(0, min64(kGaeTpt, hi - x0)));
-
-  // issue this thread's loads first (they fly while the boundaries are found)
-  float v[kGaeTpt], r[kGaeTpt];
-  uint32_t mw[kGaeTpt / 4];
-  if (kVec && nmine == kGaeTpt) {
-#pragma unroll
-    for (int q = 0; q < kGaeTpt / 4; ++q) {
-      const float4 a = __ldcs(reinterpret_cast<const float4*>(values + x0) + q);
-      const float4 b = __ldcs(reinterpret_cast<const float4*>(rewards + x0) + q);
-      v[4 * q] = a.x, v[4 * q + 1] = a.y, v[4 * q + 2] = a.z, v[4 * q + 3] = a.w;
-      r[4 * q] = b.x, r[4 * q + 1] = b.y, r[4 * q + 2] = b.z, r[4 * q + 3] = b.w;
-    }
-    if (mask != nullptr) {
-      const uint4 m = __ldcs(reinterpret_cast<const uint4*>(mask + x0));
-      mw[0] = m.x, mw[1] = m.y, mw[2] = m.z, mw[3] = m.w;
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < kGaeTpt; ++j) {
-      v[j] = j < nmine ? values[x0 + j] : 0.f;
-      r[j] = j < nmine ? rewards[x0 + j] : 0.f;
-    }
-    if (mask != nullptr) {
-#pragma unroll
-      for (int q = 0; q < kGaeTpt / 4; ++q) {
-        uint32_t w = 0;
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (4 * q + u < nmine && mask[x0 + 4 * q + u]) w |= 1u << (8 * u);
-        mw[q] = w;
-      }
-    }
-  }
-  if (mask == nullptr) {
-#pragma unroll
-    for (int q = 0; q < kGaeTpt / 4; ++q) mw[q] = 0x01010101u;
-  }
-
-  // sequence ends inside the tile: k with cu[k] in [lo+1, hi], k in [1, nseq]
-  if (warp < 2) {  // the two searches run in parallel on warps 0 and 1
-    const int64_t k = warp_lower_bound(cu, 1, nseq + 1, (warp == 0 ? lo : hi) + 1, lane);
-    if (lane == 0) (warp == 0 ? s_k0 : s_k1) = k;
-  }
-  __syncthreads();
-  for (int64_t k = s_k0 + tid; k < s_k1; k += kGaeThreads) {
-    const int64_t j = __ldg(cu + k) - 1 - lo;
-    atomicOr(&last_bits[j >> 5], 1u << (j & 31));
-  }
-  const int64_t in_lo = __ldg(cu), in_hi = min64(n_tokens, __ldg(cu + nseq));
-  __syncthreads();
-  // this thread's 16 "last" bits (x0 - lo is a multiple of 16)
-  const uint32_t lb = (last_bits[(x0 - lo) >> 5] >> ((x0 - lo) & 31)) & 0xffffu;
-  auto inside = [&](int j) { return j < nmine && x0 + j >= in_lo && x0 + j < in_hi; };
-  auto valid = [&](int j) { return ((mw[j >> 2] >> (8 * (j & 3))) & 0xffu) != 0u; };
-
-  // compose this thread's tokens right to left
-  Aff f = aff_id();
-#pragma unroll
-  for (int j = kGaeTpt - 1; j >= 0; --j) {
-    if (!inside(j)) continue;
-    if ((lb >> j) & 1u) f = Aff{0.0, 0.0, 0.0, 0.0, 0.0};
-    if (valid(j)) {
-      const double vv = v[j];
-      f = Aff{gl * f.a, gl * f.b + gamma * f.k, 0.0, gl * f.p + gamma * f.q + (double(r[j]) - vv),
-              vv};
-    }
-  }
-  // inclusive scan from the right inside the warp, then warp totals
-  Aff inc = f;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const Aff o = shfl_down_aff(inc, d);
-    if (lane + d < 32) inc = compose(inc, o);
-  }
-  if (lane == 0) wtot[warp] = inc;
-  __syncthreads();
+  const double gamma = g.gamma, gl = g.gamma * g.lam;
+  const int64_t in_lo = __ldg(g.cu), in_hi = min64(g.n_tokens, __ldg(g.cu + g.nseq));
+  // a tile goes by bulk copy when it is full (sizes multiple of 16 B)
+  auto bulk_ok = [&](int64_t t) { return kBulk && (t + 1) * kGaeTile <= g.n_tokens; };
+  auto claim = [&]() { return g.ntiles - 1 - int64_t(atomicAdd(ws.ticket, 1u)); };
+  auto issue = [&](int64_t t, int s) {  // thread 0
+    const int64_t lo = t * kGaeTile;
+    const uint64_t pol = l2_evict_first_policy();
+    mbar_arrive_expect_tx(&full[s], (g.mask ? 9u : 8u) * kGaeTile);
+    bulk_g2s(stg[s].v, g.values + lo, 4u * kGaeTile, &full[s], pol);
+    bulk_g2s(stg[s].r, g.rewards + lo, 4u * kGaeTile, &full[s], pol);
+    if (g.mask) bulk_g2s(stg[s].m, g.mask + lo, kGaeTile, &full[s], pol);
+  };
   if (tid == 0) {
-    Aff tot = wtot[kGaeThreads / 32 - 1];
-    for (int w = kGaeThreads / 32 - 2; w >= 0; --w) tot = compose(wtot[w], tot);
-    const bool constant = tot.a == 0.0 && tot.b == 0.0 && tot.k == 0.0;
-    if (constant) {
-      ws.incl[t] = make_double2(tot.p, tot.q);
-      st_release(ws.flag + t, 2u);
-    } else {
-      ws.agg[t] = tot;
-      st_release(ws.flag + t, 1u);
-    }
-    // look-back: state entering from the right = M_{t+1} o ... o (state of the
-    // first tile to the right that published its outgoing state)
-    Aff c = aff_id();
-    double2 st = make_double2(0.0, 0.0);
-    for (int64_t j = t + 1; j < ntiles; ++j) {
-      uint32_t fl;
-      int spins = 0;
-      while ((fl = ld_acquire(ws.flag + j)) == 0u)
-        if (++spins > 8) __nanosleep(64);
-      if (fl == 2u) {
-        st = __ldcg(ws.incl + j);
-        break;
-      }
-      const Aff* g = ws.agg + j;
-      c = compose(c, Aff{__ldcg(&g->a), __ldcg(&g->b), __ldcg(&g->k), __ldcg(&g->p),
-                         __ldcg(&g->q)});
-    }
-    const double2 in_state =
-        make_double2(c.a * st.x + c.b * st.y + c.p, c.k * st.y + c.q);
-    if (!constant) {
-      ws.incl[t] = make_double2(tot.a * in_state.x + tot.b * in_state.y + tot.p,
-                                tot.k * in_state.y + tot.q);
-      st_release(ws.flag + t, 2u);
-    }
-    carry = in_state;
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_mbar_init();
+    const int64_t t0 = claim();
+    s_tile[0] = t0;
+    if (t0 >= 0 && bulk_ok(t0)) issue(t0, 0);
   }
-  // composite of the threads to my right: later lanes, then later warps
-  Aff right = aff_id();
-  for (int w = kGaeThreads / 32 - 1; w > warp; --w) right = compose(wtot[w], right);
-  Aff ex = shfl_down_aff(inc, 1);
-  if (lane == 31) ex = aff_id();
-  ex = compose(ex, right);
   __syncthreads();
-  const double2 cs = carry;
-  double A = ex.a * cs.x + ex.b * cs.y + ex.p;
-  double Vn = ex.k * cs.y + ex.q;
-  // replay right to left; v[] becomes the advantage, r[] the return
-#pragma unroll
-  for (int j = kGaeTpt - 1; j >= 0; --j) {
-    if (!inside(j)) continue;
-    if ((lb >> j) & 1u) A = 0.0, Vn = 0.0;
-    const double vv = v[j];
-    if (valid(j)) {
-      A = (double(r[j]) - vv) + gamma * Vn + gl * A;
-      Vn = vv;
+  int s = 0;
+  uint32_t phase[2] = {0u, 0u};
+  for (int64_t t = s_tile[0]; t >= 0; t = s_tile[s ^= 1]) {
+    if (tid == 0) {  // keep the next tile in flight while this one is scanned
+      const int64_t nx = claim();
+      s_tile[s ^ 1] = nx;
+      if (nx >= 0 && bulk_ok(nx)) issue(nx, s ^ 1);
     }
-    v[j] = float(A);
-    r[j] = float(A + vv);
-  }
-  const bool all_in = nmine == kGaeTpt && x0 >= in_lo && x0 + kGaeTpt <= in_hi;
-  if (kVec && all_in) {
-#pragma unroll
-    for (int q = 0; q < kGaeTpt / 4; ++q) {
-      __stcs(reinterpret_cast<float4*>(adv + x0) + q,
-             make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
-      __stcs(reinterpret_cast<float4*>(ret + x0) + q,
-             make_float4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]));
+    GAE_STAMP(0);
+    const int64_t lo = t * kGaeTile, hi = min64(g.n_tokens, lo + kGaeTile);
+    for (int i = tid; i < kGaeTile / 32; i += kGaeThreads) last_bits[i] = 0u;
+    if (warp < 2) {  // sequence ends in the tile: k with cu[k] in [lo+1, hi]
+      const int64_t k = warp_lower_bound(g.cu, 1, g.nseq + 1, (warp == 0 ? lo : hi) + 1, lane);
+      if (lane == 0) s_k[warp] = k;
     }
-  } else {
-#pragma unroll
-    for (int j = 0; j < kGaeTpt; ++j)
-      if (inside(j)) {
-        adv[x0 + j] = v[j];
-        ret[x0 + j] = r[j];
+    GaeStage& S = stg[s];
+    if (bulk_ok(t)) {
+      mbar_wait(&full[s], phase[s]);
+      phase[s] ^= 1u;
+      GAE_STAMP(1);
+    } else {  // ragged last tile or unaligned arrays: cooperative element loads
+      for (int64_t i = lo + tid; i < lo + kGaeTile; i += kGaeThreads) {
+        const bool ok = i < hi;
+        S.v[i - lo] = ok ? g.values[i] : 0.f;
+        S.r[i - lo] = ok ? g.rewards[i] : 0.f;
+        S.m[i - lo] = ok ? (g.mask ? g.mask[i] : uint8_t(1)) : uint8_t(0);
       }
+    }
+    __syncthreads();
+    for (int64_t k = s_k[0] + tid; k < s_k[1]; k += kGaeThreads) {
+      const int64_t j = __ldg(g.cu + k) - 1 - lo;
+      atomicOr(&last_bits[j >> 5], 1u << (j & 31));
+    }
+    __syncthreads();
+    GAE_STAMP(2);
+    const int j0 = tid * kGaeTpt;  // this thread's first token within the tile
+    const int64_t x0 = lo + j0;
+    const int nmine = int(max64(0, min64(kGaeTpt, hi - x0)));
+    // 16-bit masks over this thread's tokens: inside [cu[0], cu[nseq]) and
+    // the array, valid (mask != 0), last token of a sequence
+    const uint32_t lb = (last_bits[j0 >> 5] >> (j0 & 31)) & 0xffffu;
+    uint32_t insm = 0u, validm = 0xffffu;
+    {
+      const int64_t a = max64(0, in_lo - x0), b = min64(nmine, in_hi - x0);
+      if (b > a) insm = ((1u << b) - 1u) & ~((1u << a) - 1u);
+    }
+    if (g.mask) {
+      const uint4 m4 = *reinterpret_cast<const uint4*>(S.m + j0);
+      const uint32_t mw[4] = {m4.x, m4.y, m4.z, m4.w};
+      validm = 0u;
+#pragma unroll
+      for (int j = 0; j < kGaeTpt; ++j)
+        validm |= ((mw[j >> 2] >> (8 * (j & 3))) & 0xffu) ? (1u << j) : 0u;
+    }
+
+    // compose this thread's tokens right to left
+    Aff f = aff_id();
+#pragma unroll
+    for (int q = kGaeTpt / 4 - 1; q >= 0; --q) {
+      const float4 v4 = *reinterpret_cast<const float4*>(S.v + j0 + 4 * q);
+      const float4 r4 = *reinterpret_cast<const float4*>(S.r + j0 + 4 * q);
+      const float vq[4] = {v4.x, v4.y, v4.z, v4.w}, rq[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+      for (int u = 3; u >= 0; --u) {
+        const uint32_t bit = 1u << (4 * q + u);
+        if (!(insm & bit)) continue;
+        if (lb & bit) f = Aff{0.0, 0.0, 0.0, 0.0, 0.0};
+        if (validm & bit) {
+          const double vv = f2d(vq[u]);
+          f = Aff{gl * f.a, gl * f.b + gamma * f.k, 0.0,
+                  gl * f.p + gamma * f.q + (f2d(rq[u]) - vv), vv};
+        }
+      }
+    }
+    // inclusive scan from the right inside the warp, then warp totals
+    Aff inc = f;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const Aff o = shfl_down_aff(inc, d);
+      if (lane + d < 32) inc = compose(inc, o);
+    }
+    if (lane == 0) wtot[warp] = inc;
+    __syncthreads();
+    GAE_STAMP(3);
+    // composite of the threads to my right: later lanes, then later warps
+    Aff right = aff_id();
+    for (int w = kGaeThreads / 32 - 1; w > warp; --w) right = compose(wtot[w], right);
+    Aff ex = shfl_down_aff(inc, 1);
+    if (lane == 31) ex = aff_id();
+    ex = compose(ex, right);
+    // replay right to left from shared memory, four tokens per step
+    const bool all_in = insm == 0xffffu;
+    auto replay = [&](double A, double Vn) {
+#pragma unroll
+      for (int q = kGaeTpt / 4 - 1; q >= 0; --q) {
+        const float4 v4 = *reinterpret_cast<const float4*>(S.v + j0 + 4 * q);
+        const float4 r4 = *reinterpret_cast<const float4*>(S.r + j0 + 4 * q);
+        const float vq[4] = {v4.x, v4.y, v4.z, v4.w}, rq[4] = {r4.x, r4.y, r4.z, r4.w};
+        float ao[4], ro[4];
+#pragma unroll
+        for (int u = 3; u >= 0; --u) {
+          const uint32_t bit = 1u << (4 * q + u);
+          ao[u] = 0.f, ro[u] = 0.f;
+          if (!(insm & bit)) continue;
+          if (lb & bit) A = 0.0, Vn = 0.0;
+          const double vv = f2d(vq[u]);
+          if (validm & bit) {
+            A = (f2d(rq[u]) - vv) + gamma * Vn + gl * A;
+            Vn = vv;
+          }
+          ao[u] = float(A);
+          ro[u] = float(A + vv);
+        }
+        if (kBulk && all_in) {
+          __stcs(reinterpret_cast<float4*>(g.adv + x0) + q, make_float4(ao[0], ao[1], ao[2], ao[3]));
+          __stcs(reinterpret_cast<float4*>(g.ret + x0) + q, make_float4(ro[0], ro[1], ro[2], ro[3]));
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (insm & (1u << (4 * q + u))) {
+              g.adv[x0 + 4 * q + u] = ao[u];
+              g.ret[x0 + 4 * q + u] = ro[u];
+            }
+        }
+      }
+    };
+    // lane 0 of the last warp publishes the tile and looks back; meanwhile
+    // every thread with a sequence end to its right inside the tile (constant
+    // right composite) replays without waiting for the carry
+    if (tid == kGaeThreads - 32) {
+      Aff tot = wtot[kGaeThreads / 32 - 1];
+      for (int w = kGaeThreads / 32 - 2; w >= 0; --w) tot = compose(wtot[w], tot);
+      const bool constant = tot.a == 0.0 && tot.b == 0.0 && tot.k == 0.0;
+      if (constant) {
+        st_incl(ws.incl + t, tot.p, tot.q);
+      } else {
+        ws.agg[t] = tot;
+        st_release(ws.aflag + t, 1u);
+      }
+      // look-back: state entering from the right = M_{t+1} o ... o (state of
+      // the first tile to the right that published its outgoing state)
+      Aff c = aff_id();
+      double2 st = make_double2(0.0, 0.0);
+      for (int64_t j = t + 1; j < g.ntiles; ++j) {
+        int spins = 0;
+        for (;;) {
+          const uint4 w = ld_incl(ws.incl + j);
+          if (w.w != 0u) {
+            st = make_double2(__hiloint2double(int(w.y), int(w.x)), double(__uint_as_float(w.z)));
+            j = g.ntiles;  // done
+            break;
+          }
+          if (ld_acquire(ws.aflag + j) != 0u) {
+            const Aff* a = ws.agg + j;
+            c = compose(c, Aff{__ldcg(&a->a), __ldcg(&a->b), __ldcg(&a->k), __ldcg(&a->p),
+                               __ldcg(&a->q)});
+            break;
+          }
+          if (++spins > 4) __nanosleep(32);
+        }
+      }
+      const double2 in_state = make_double2(c.a * st.x + c.b * st.y + c.p, c.k * st.y + c.q);
+      if (!constant)
+        st_incl(ws.incl + t, tot.a * in_state.x + tot.b * in_state.y + tot.p,
+                tot.k * in_state.y + tot.q);
+      carry = in_state;
+      GAE_STAMP(4);
+    }
+    const bool need_carry = !(ex.a == 0.0 && ex.b == 0.0 && ex.k == 0.0);
+    if (!need_carry) replay(ex.p, ex.q);
+    __syncthreads();
+    if (need_carry) {
+      const double2 cs = carry;
+      replay(ex.a * cs.x + ex.b * cs.y + ex.p, ex.k * cs.y + ex.q);
+    }
+    __syncthreads();  // stage s, last_bits, wtot and carry are reused next
+    GAE_STAMP(5);
   }
+}
+
+int gae_pipe_occupancy(bool bulk) {
+  static int occ[2] = {0, 0};
+  int& o = occ[bulk ? 1 : 0];
+  if (o == 0) {
+    int n = 0;
+    if (bulk)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, gae_pipe_kernel<true>, kGaeThreads, 0);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, gae_pipe_kernel<false>, kGaeThreads, 0);
+    o = n > 0 ? n : 1;
+  }
+  return o;
 }
 
 // ------------------------------------------------------- masked moments ----
@@ -550,14 +647,15 @@ int gae_launch(const float* values, const float* rewards, const uint8_t* mask, c
   YATT_REQUIRE(ntiles < (int64_t(1) << 31), YATT_ERR_CONFIG, "gae: too many tokens");
   YATT_TRY_CUDA(cudaMemsetAsync(ws, 0, gae_zero_bytes(ntiles), st));
   auto a16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
-  const GaeWs w = gae_ws(ws, ntiles);
-  if (a16(values) && a16(rewards) && a16(mask) && a16(adv) && a16(ret))
-    gae_scan_kernel<true><<<unsigned(ntiles), kGaeThreads, 0, st>>>(
-        values, rewards, mask, cu, nseq, n_tokens, ntiles, double(gamma), double(lam), adv, ret, w);
+  const bool bulk = a16(values) && a16(rewards) && a16(mask) && a16(adv) && a16(ret);
+  const GaeArgs args{values, rewards, mask, cu, nseq, n_tokens, ntiles, double(gamma), double(lam),
+                     adv, ret};
+  const int grid = int(min64(ntiles, int64_t(num_sms()) * gae_pipe_occupancy(bulk)));
+  if (bulk)
+    gae_pipe_kernel<true><<<grid, kGaeThreads, 0, st>>>(args, gae_ws(ws, ntiles));
   else
-    gae_scan_kernel<false><<<unsigned(ntiles), kGaeThreads, 0, st>>>(
-        values, rewards, mask, cu, nseq, n_tokens, ntiles, double(gamma), double(lam), adv, ret, w);
-  return check_launch("gae_scan_kernel");
+    gae_pipe_kernel<false><<<grid, kGaeThreads, 0, st>>>(args, gae_ws(ws, ntiles));
+  return check_launch("gae_pipe_kernel");
 }
 
 size_t moments_workspace_bytes() { return size_t(3) * kMomMaxParts * sizeof(double); }
@@ -589,3 +687,10 @@ int whiten_launch(float* x, const uint8_t* mask, int64_t n, const double* mom, i
 }
 
 }  // namespace yattb
+
+#ifdef YATT_GAE_PROFILE
+extern "C" int yatt_debug_gae_profile(long long* out, int ntiles) {
+  return int(cudaMemcpyFromSymbol(out, yattb::g_gae_prof, sizeof(long long) * 6 *
+                                                            size_t(ntiles < 16384 ? ntiles : 16384)));
+}
+#endif
