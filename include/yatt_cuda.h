@@ -391,6 +391,17 @@ int yatt_gather_varlen(const void* d_src, const int64_t* d_old_cu,
                        const int64_t* d_n_kept, int64_t max_kept,
                        const int64_t* d_dst_offset, int32_t elem_bytes,
                        void* d_dst, void* stream);
+/* The same for up to YATT_GATHER_MAX_ARRAYS per-token arrays in ONE launch */
+/* (e.g. the 17 B/token payload: token i32, logp/ref_logp/adv f32, mask u8):  */
+/* h_srcs / h_dsts / h_elem_bytes are HOST arrays of n_arrays device         */
+/* pointers and element sizes; each sample's index lookup is shared.        */
+#define YATT_GATHER_MAX_ARRAYS 8
+int yatt_gather_varlen_multi(int32_t n_arrays, const void* const* h_srcs,
+                             void* const* h_dsts, const int32_t* h_elem_bytes,
+                             const int64_t* d_old_cu, const int32_t* d_index_map,
+                             const int64_t* d_new_cu, const int64_t* d_n_kept,
+                             int64_t max_kept, const int64_t* d_dst_offset,
+                             void* stream);
 /* Gather fixed-width per-sample rows (metadata, multimodal payload refs):   */
 /*   dst[(off + j)*row_bytes ..] = src[map[j]*row_bytes ..], j < *d_n_kept   */
 int yatt_gather_rows(const void* d_src, const int32_t* d_index_map,

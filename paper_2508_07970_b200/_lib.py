@@ -125,6 +125,8 @@ SIGNATURES = {
     "yatt_filter_compact_workspace_bytes": (c_sz, [c_i64]),
     "yatt_filter_compact": (C.c_int, [c_p, c_p, c_i64, c_i32, c_p, c_p, c_p, c_p, c_p, c_sz, c_p]),
     "yatt_gather_varlen": (C.c_int, [c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_i32, c_p, c_p]),
+    "yatt_gather_varlen_multi": (C.c_int, [c_i32, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p,
+                                           c_p]),
     "yatt_gather_rows": (C.c_int, [c_p, c_p, c_p, c_i64, c_i64, c_p, c_p, c_p]),
     "yatt_microbatch_aggregates": (C.c_int, [c_p, c_p, c_p, c_i64, c_i32, c_i32, c_p, c_p]),
     "yatt_exclusive_offset": (C.c_int, [c_p, c_i32, c_i32, c_i32, c_i32, c_p, c_p]),

@@ -46,6 +46,9 @@ double loss_finalize(const yatt_loss_sums*, const yatt_loss_config*);
 size_t compact_workspace_bytes(int64_t);
 int filter_compact_launch(const float*, const int64_t*, int64_t, int32_t, uint8_t*, int32_t*,
                           int64_t*, int64_t*, void*, size_t, cudaStream_t);
+int gather_varlen_multi_launch(int32_t, const void* const*, void* const*, const int32_t*,
+                               const int64_t*, const int32_t*, const int64_t*, const int64_t*,
+                               int64_t, const int64_t*, cudaStream_t);
 int gather_varlen_launch(const void*, const int64_t*, const int32_t*, const int64_t*,
                          const int64_t*, int64_t, const int64_t*, int32_t, void*, cudaStream_t);
 int gather_rows_launch(const void*, const int32_t*, const int64_t*, int64_t, int64_t,
@@ -510,6 +513,19 @@ int yatt_gather_varlen(const void* src, const int64_t* old_cu, const int32_t* ma
   YATT_ALIGNED("gather_varlen", d_dst_offset, 8);
   return gather_varlen_launch(src, old_cu, map, new_cu, d_n_kept, max_kept, d_dst_offset,
                               elem_bytes, dst, as_stream(stream));
+}
+
+int yatt_gather_varlen_multi(int32_t n_arrays, const void* const* srcs, void* const* dsts,
+                             const int32_t* esz, const int64_t* old_cu, const int32_t* map,
+                             const int64_t* new_cu, const int64_t* d_n_kept, int64_t max_kept,
+                             const int64_t* d_dst_offset, void* stream) {
+  YATT_ALIGNED("gather_varlen_multi", old_cu, 8);
+  YATT_ALIGNED("gather_varlen_multi", map, 4);
+  YATT_ALIGNED("gather_varlen_multi", new_cu, 8);
+  YATT_ALIGNED("gather_varlen_multi", d_n_kept, 8);
+  YATT_ALIGNED("gather_varlen_multi", d_dst_offset, 8);
+  return gather_varlen_multi_launch(n_arrays, srcs, dsts, esz, old_cu, map, new_cu, d_n_kept,
+                                    max_kept, d_dst_offset, as_stream(stream));
 }
 
 int yatt_gather_rows(const void* src, const int32_t* map, const int64_t* d_n_kept,

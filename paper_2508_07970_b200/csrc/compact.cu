@@ -170,39 +170,131 @@ __global__ void __launch_bounds__(kScanThreads) compact_scatter_kernel(
   }
 }
 
-template <typename T>
-__global__ void gather_varlen_kernel(const T* src, const int64_t* old_cu, const int32_t* map,
-                                     const int64_t* new_cu, const int64_t* n_kept,
-                                     const int64_t* dst_off, T* dst) {
-  const int64_t nk = *n_kept;
-  const int64_t off = dst_off ? *dst_off : 0;
-  for (int64_t j = blockIdx.x; j < nk; j += gridDim.x) {
-    const int32_t s = map[j];
-    const int64_t b = old_cu[s], len = old_cu[s + 1] - b;
-    const T* sp = src + b;
-    T* dp = dst + (new_cu[j] + off);
-    // 8 independent coalesced loads in flight per thread before the stores
-    constexpr int kU = 8, kB = kGatherThreads;
-    int64_t k = threadIdx.x;
-    for (; k + (kU - 1) * kB < len; k += kU * kB) {
-      T v[kU];
+// ---- byte-exact gathers ---------------------------------------------------
+__device__ __forceinline__ uint4 ldg16(const uint8_t* p) {
+  return __ldg(reinterpret_cast<const uint4*>(p));
+}
+// bytes [s, s+16) of the 32-byte window (a ++ b), s in [0, 16)
+__device__ __forceinline__ uint4 window16(const uint4& a, const uint4& b, int s) {
+  const uint32_t r = uint32_t(s & 3) * 8u;
+  switch (s >> 2) {
+    case 0:
+      return make_uint4(__funnelshift_r(a.x, a.y, r), __funnelshift_r(a.y, a.z, r),
+                        __funnelshift_r(a.z, a.w, r), __funnelshift_r(a.w, b.x, r));
+    case 1:
+      return make_uint4(__funnelshift_r(a.y, a.z, r), __funnelshift_r(a.z, a.w, r),
+                        __funnelshift_r(a.w, b.x, r), __funnelshift_r(b.x, b.y, r));
+    case 2:
+      return make_uint4(__funnelshift_r(a.z, a.w, r), __funnelshift_r(a.w, b.x, r),
+                        __funnelshift_r(b.x, b.y, r), __funnelshift_r(b.y, b.z, r));
+    default:
+      return make_uint4(__funnelshift_r(a.w, b.x, r), __funnelshift_r(b.x, b.y, r),
+                        __funnelshift_r(b.y, b.z, r), __funnelshift_r(b.z, b.w, r));
+  }
+}
+__device__ __forceinline__ uint4 shfl_down16(const uint4& v) {
+  return make_uint4(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1),
+                    __shfl_down_sync(0xffffffffu, v.z, 1), __shfl_down_sync(0xffffffffu, v.w, 1));
+}
+
+// One CTA copies L bytes src -> dst for any relative alignment: bytewise
+// head up to dst's first 16-B boundary, then aligned 16-B stores; each lane
+// loads one ALIGNED 16-B source chunk, takes its right neighbour's chunk by
+// shuffle (the last lane loads it) and funnel-shifts the 16 bytes it needs
+// out of the 32-byte window.  Loads touch only aligned chunks holding needed
+// bytes; four 512-B groups per warp are in flight per iteration.
+__device__ __forceinline__ void cta_copy_bytes(const uint8_t* src, uint8_t* dst, int64_t L) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int64_t head = min64(L, int64_t((16u - (reinterpret_cast<uintptr_t>(dst) & 15u)) & 15u));
+  const int64_t nch = (L - head) >> 4;
+  const int64_t tail0 = head + nch * 16;
+  if (tid < head) dst[tid] = src[tid];
+  if (tid < L - tail0) dst[tail0 + tid] = src[tail0 + tid];
+  const uint8_t* s0 = src + head;
+  uint8_t* d0 = dst + head;
+  const int sh = int(reinterpret_cast<uintptr_t>(s0) & 15u);
+  const uint8_t* sb = s0 - sh;  // aligned
+  // chunk nch (when sh != 0) holds the last body chunk's final sh bytes
+  const int64_t nload = nch + (sh != 0 ? 1 : 0);
+  constexpr int kU = 4;
+  for (int64_t g0 = int64_t(warp) * 32 * kU; g0 < nch; g0 += int64_t(nwarps) * 32 * kU) {
+    uint4 a[kU], b[kU];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) v[u] = __ldg(sp + k + u * kB);
-#pragma unroll
-      for (int u = 0; u < kU; ++u) dp[k + u * kB] = v[u];
+    for (int u = 0; u < kU; ++u) {
+      const int64_t c = g0 + u * 32 + lane;
+      a[u] = c < nload ? ldg16(sb + 16 * c) : make_uint4(0, 0, 0, 0);
     }
-    for (; k < len; k += kB) dp[k] = __ldg(sp + k);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      b[u] = shfl_down16(a[u]);
+      const int64_t c = g0 + u * 32 + lane;
+      if (lane == 31 && sh != 0 && c < nch) b[u] = ldg16(sb + 16 * (c + 1));
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t c = g0 + u * 32 + lane;
+      if (c < nch) *reinterpret_cast<uint4*>(d0 + 16 * c) = sh ? window16(a[u], b[u], sh) : a[u];
+    }
   }
 }
 
-__global__ void gather_rows_kernel(const uint8_t* src, const int32_t* map, const int64_t* n_kept,
-                                   int64_t row_bytes, const int64_t* dst_off, uint8_t* dst) {
+struct GatherArrays {
+  const uint8_t* src[YATT_GATHER_MAX_ARRAYS];
+  uint8_t* dst[YATT_GATHER_MAX_ARRAYS];
+  int32_t esz[YATT_GATHER_MAX_ARRAYS];
+  int32_t n;
+};
+
+// One CTA per kept sample (grid-stride), all arrays of the sample in turn;
+// thread 0 fetches the NEXT sample's (map -> old_cu, new_cu) chain while the
+// current one is copied.
+__global__ void __launch_bounds__(kGatherThreads) gather_varlen_kernel(
+    const GatherArrays arr, const int64_t* old_cu, const int32_t* map, const int64_t* new_cu,
+    const int64_t* n_kept, const int64_t* dst_off) {
+  __shared__ int64_t meta[2][3];  // src element offset, length, dst element offset
   const int64_t nk = *n_kept;
   const int64_t off = dst_off ? *dst_off : 0;
-  for (int64_t j = blockIdx.x; j < nk; j += gridDim.x) {
-    const uint8_t* sp = src + int64_t(map[j]) * row_bytes;
-    uint8_t* dp = dst + (j + off) * row_bytes;
-    for (int64_t k = threadIdx.x; k < row_bytes; k += blockDim.x) dp[k] = sp[k];
+  auto fetch = [&](int64_t j, int64_t* m) {
+    const int32_t s = __ldg(map + j);
+    const int64_t b = __ldg(old_cu + s);
+    m[0] = b;
+    m[1] = __ldg(old_cu + s + 1) - b;
+    m[2] = __ldg(new_cu + j) + off;
+  };
+  int64_t j = blockIdx.x;
+  if (threadIdx.x == 0 && j < nk) fetch(j, meta[0]);
+  __syncthreads();
+  for (int buf = 0; j < nk; j += gridDim.x, buf ^= 1) {
+    int64_t nxt[3];
+    const bool more = j + gridDim.x < nk;
+    if (threadIdx.x == 0 && more) fetch(j + gridDim.x, nxt);  // in flight during the copy
+    for (int a = 0; a < arr.n; ++a) {
+      const int64_t e = arr.esz[a];
+      cta_copy_bytes(arr.src[a] + meta[buf][0] * e, arr.dst[a] + meta[buf][2] * e, meta[buf][1] * e);
+    }
+    if (threadIdx.x == 0 && more) {
+      meta[buf ^ 1][0] = nxt[0];
+      meta[buf ^ 1][1] = nxt[1];
+      meta[buf ^ 1][2] = nxt[2];
+    }
+    __syncthreads();
+  }
+}
+
+// Rows: flattened over (kept row, w-byte word), w = widest of 16/8/4/1 that
+// divides row_bytes and both base alignments.
+template <typename W>
+__global__ void gather_rows_kernel(const uint8_t* src, const int32_t* map, const int64_t* n_kept,
+                                   int64_t words_per_row, const int64_t* dst_off, uint8_t* dst) {
+  const int64_t nk = *n_kept;
+  const int64_t off = dst_off ? *dst_off : 0;
+  const W* s = reinterpret_cast<const W*>(src);
+  W* d = reinterpret_cast<W*>(dst);
+  const int64_t total = nk * words_per_row;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t j = i / words_per_row, w = i - j * words_per_row;
+    d[(j + off) * words_per_row + w] = s[int64_t(map[j]) * words_per_row + w];
   }
 }
 
@@ -269,38 +361,40 @@ int filter_compact_launch(const float* r, const int64_t* lens, int64_t n, int32_
   return rc;
 }
 
+int gather_varlen_multi_launch(int32_t n_arrays, const void* const* srcs, void* const* dsts,
+                               const int32_t* esz, const int64_t* old_cu, const int32_t* map,
+                               const int64_t* new_cu, const int64_t* n_kept, int64_t max_kept,
+                               const int64_t* dst_off, cudaStream_t st) {
+  YATT_REQUIRE(max_kept >= 0, YATT_ERR_CONFIG, "gather_varlen: max_kept must be >= 0");
+  YATT_REQUIRE(n_arrays >= 1 && n_arrays <= YATT_GATHER_MAX_ARRAYS, YATT_ERR_CONFIG,
+               "gather_varlen: n_arrays must be in [1, %d] (got %d)", YATT_GATHER_MAX_ARRAYS,
+               n_arrays);
+  YATT_REQUIRE(srcs && dsts && esz, YATT_ERR_CONFIG, "gather_varlen: null array list");
+  GatherArrays arr{};
+  arr.n = n_arrays;
+  for (int a = 0; a < n_arrays; ++a) {
+    YATT_REQUIRE(esz[a] == 1 || esz[a] == 2 || esz[a] == 4 || esz[a] == 8, YATT_ERR_CONFIG,
+                 "gather_varlen: elem_bytes must be 1, 2, 4 or 8 (got %d)", esz[a]);
+    YATT_REQUIRE((reinterpret_cast<uintptr_t>(srcs[a]) % uintptr_t(esz[a])) == 0 &&
+                     (reinterpret_cast<uintptr_t>(dsts[a]) % uintptr_t(esz[a])) == 0,
+                 YATT_ERR_CONFIG, "gather_varlen: array %d not aligned to its element size", a);
+    arr.src[a] = static_cast<const uint8_t*>(srcs[a]);
+    arr.dst[a] = static_cast<uint8_t*>(dsts[a]);
+    arr.esz[a] = esz[a];
+  }
+  if (max_kept == 0) return YATT_OK;
+  // ~one CTA per sample: the block scheduler balances the ragged lengths
+  const int grid = int(min64(max_kept, int64_t(num_sms()) * 64));
+  gather_varlen_kernel<<<grid, kGatherThreads, 0, st>>>(arr, old_cu, map, new_cu, n_kept, dst_off);
+  return check_launch("gather_varlen_kernel");
+}
+
 int gather_varlen_launch(const void* src, const int64_t* old_cu, const int32_t* map,
                          const int64_t* new_cu, const int64_t* n_kept, int64_t max_kept,
                          const int64_t* dst_off, int32_t elem_bytes, void* dst, cudaStream_t st) {
-  YATT_REQUIRE(max_kept >= 0, YATT_ERR_CONFIG, "gather_varlen: max_kept must be >= 0");
-  if (max_kept == 0) return YATT_OK;
-  const int grid = int(min64(max_kept, int64_t(num_sms()) * 16));
-  switch (elem_bytes) {
-    case 1:
-      gather_varlen_kernel<uint8_t><<<grid, 256, 0, st>>>(
-          static_cast<const uint8_t*>(src), old_cu, map, new_cu, n_kept, dst_off,
-          static_cast<uint8_t*>(dst));
-      break;
-    case 2:
-      gather_varlen_kernel<uint16_t><<<grid, 256, 0, st>>>(
-          static_cast<const uint16_t*>(src), old_cu, map, new_cu, n_kept, dst_off,
-          static_cast<uint16_t*>(dst));
-      break;
-    case 4:
-      gather_varlen_kernel<uint32_t><<<grid, 256, 0, st>>>(
-          static_cast<const uint32_t*>(src), old_cu, map, new_cu, n_kept, dst_off,
-          static_cast<uint32_t*>(dst));
-      break;
-    case 8:
-      gather_varlen_kernel<uint64_t><<<grid, 256, 0, st>>>(
-          static_cast<const uint64_t*>(src), old_cu, map, new_cu, n_kept, dst_off,
-          static_cast<uint64_t*>(dst));
-      break;
-    default:
-      return set_error(YATT_ERR_CONFIG, "gather_varlen: elem_bytes must be 1, 2, 4 or 8 (got %d)",
-                       elem_bytes);
-  }
-  return check_launch("gather_varlen_kernel");
+  void* d = dst;
+  return gather_varlen_multi_launch(1, &src, &d, &elem_bytes, old_cu, map, new_cu, n_kept,
+                                    max_kept, dst_off, st);
 }
 
 int gather_rows_launch(const void* src, const int32_t* map, const int64_t* n_kept,
@@ -308,9 +402,19 @@ int gather_rows_launch(const void* src, const int32_t* map, const int64_t* n_kep
                        cudaStream_t st) {
   YATT_REQUIRE(row_bytes > 0 && max_kept >= 0, YATT_ERR_CONFIG, "gather_rows: bad sizes");
   if (max_kept == 0) return YATT_OK;
-  const int grid = int(min64(max_kept, int64_t(num_sms()) * 16));
-  gather_rows_kernel<<<grid, 128, 0, st>>>(static_cast<const uint8_t*>(src), map, n_kept,
-                                           row_bytes, dst_off, static_cast<uint8_t*>(dst));
+  const uintptr_t al = reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) |
+                       uintptr_t(row_bytes);
+  const int w = (al & 15) == 0 ? 16 : (al & 7) == 0 ? 8 : (al & 3) == 0 ? 4 : 1;
+  const int64_t wpr = row_bytes / w;
+  const int grid = int(max64(1, min64(ceil_div(max_kept * wpr, 256), int64_t(num_sms()) * 8)));
+  const uint8_t* s8 = static_cast<const uint8_t*>(src);
+  uint8_t* d8 = static_cast<uint8_t*>(dst);
+  switch (w) {
+    case 16: gather_rows_kernel<uint4><<<grid, 256, 0, st>>>(s8, map, n_kept, wpr, dst_off, d8); break;
+    case 8: gather_rows_kernel<uint2><<<grid, 256, 0, st>>>(s8, map, n_kept, wpr, dst_off, d8); break;
+    case 4: gather_rows_kernel<uint32_t><<<grid, 256, 0, st>>>(s8, map, n_kept, wpr, dst_off, d8); break;
+    default: gather_rows_kernel<uint8_t><<<grid, 256, 0, st>>>(s8, map, n_kept, wpr, dst_off, d8);
+  }
   return check_launch("gather_rows_kernel");
 }
 

@@ -247,6 +247,21 @@ def gather_varlen(src: torch.Tensor, old_cu: torch.Tensor, index_map: torch.Tens
     return dst
 
 
+def gather_varlen_multi(srcs, old_cu: torch.Tensor, index_map: torch.Tensor, new_cu: torch.Tensor,
+                        n_kept: torch.Tensor, max_kept: int, dsts,
+                        dst_offset: torch.Tensor | None = None):
+    """gather_varlen over several per-token arrays (<= 8) in one launch."""
+    n = len(srcs)
+    if n != len(dsts):
+        raise ValueError("srcs and dsts differ in length")
+    h_src = (C.c_void_p * n)(*[t.data_ptr() for t in srcs])
+    h_dst = (C.c_void_p * n)(*[t.data_ptr() for t in dsts])
+    h_esz = (C.c_int32 * n)(*[t.element_size() for t in srcs])
+    check(lib().yatt_gather_varlen_multi(n, h_src, h_dst, h_esz, _p(old_cu), _p(index_map),
+                                         _p(new_cu), _p(n_kept), max_kept, _p(dst_offset), _st()))
+    return dsts
+
+
 def gather_rows(src: torch.Tensor, index_map: torch.Tensor, n_kept: torch.Tensor, max_kept: int,
                 dst: torch.Tensor, dst_offset: torch.Tensor | None = None) -> torch.Tensor:
     row_bytes = src[0].numel() * src.element_size() if src.dim() > 1 else src.element_size()

@@ -334,3 +334,82 @@ def test_global_compaction_across_emulated_ranks(cuda):
     ops.gather_varlen(payload, cu_all, single["index_map"], single["new_cu"],
                       single["counts"][:1], n, ref)
     assert torch.equal(dst, ref)
+
+
+@pytest.mark.parametrize("esz", [1, 2, 4, 8])
+def test_gather_varlen_every_relative_alignment(cuda, esz):
+    """Byte-exact gather for every (src, dst) misalignment mod 16 and lengths
+    around the 16-byte / 512-byte / 8-KB copy granules; a dst_offset shifts
+    the destination base too."""
+    rng = np.random.default_rng(esz)
+    lens = np.concatenate([np.arange(0, 40), [511, 512, 513, 2047, 2048, 2049, 8191, 8193, 70001],
+                           rng.integers(0, 3000, size=200)]).astype(np.int64)
+    n = len(lens)
+    old_cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    total = int(old_cu[-1])
+    src = torch.randint(0, 256, (total * esz + 64,), dtype=torch.uint8, device=cuda)
+    keep = rng.random(n) < 0.7
+    idx = np.nonzero(keep)[0].astype(np.int32)
+    kl = lens[idx]
+    new_cu = np.concatenate([[0], np.cumsum(kl)]).astype(np.int64)
+    for src_shift, off in [(0, 0), (esz, 3), (3 * esz, 1), (7 * esz, 5)]:
+        s = src[src_shift: src_shift + total * esz]
+        dst = torch.zeros(((int(new_cu[-1]) + off) * esz + 32,), dtype=torch.uint8, device=cuda)
+        d_off = torch.tensor([off], dtype=torch.int64, device=cuda)
+        nk = torch.tensor([len(idx)], dtype=torch.int64, device=cuda)
+        from paper_2508_07970_b200._lib import check, lib
+        d_old, d_idx, d_new = (torch.as_tensor(a, device=cuda) for a in (old_cu, idx, new_cu))
+        check(lib().yatt_gather_varlen(
+            s.data_ptr(), d_old.data_ptr(), d_idx.data_ptr(), d_new.data_ptr(), nk.data_ptr(), n,
+            d_off.data_ptr(), esz, dst.data_ptr(), torch.cuda.current_stream().cuda_stream))
+        hs = s.cpu().numpy()
+        want = np.concatenate([hs[old_cu[i] * esz: old_cu[i + 1] * esz] for i in idx])
+        got = dst.cpu().numpy()
+        assert np.array_equal(got[off * esz: off * esz + len(want)], want)
+        assert not got[: off * esz].any() and not got[off * esz + len(want):].any()
+
+
+@pytest.mark.parametrize("row_bytes,shift", [(32, 0), (24, 8), (12, 4), (7, 1), (48, 16)])
+def test_gather_rows_widths(cuda, row_bytes, shift):
+    n = 1000
+    buf = torch.randint(0, 256, (n * row_bytes + shift,), dtype=torch.uint8, device=cuda)
+    src = buf[shift:]
+    idx = np.nonzero(np.random.default_rng(row_bytes).random(n) < 0.6)[0].astype(np.int32)
+    out = torch.zeros((len(idx) * row_bytes,), dtype=torch.uint8, device=cuda)
+    from paper_2508_07970_b200._lib import check, lib
+    nk = torch.tensor([len(idx)], dtype=torch.int64, device=cuda)
+    d_idx = torch.as_tensor(idx, device=cuda)
+    check(lib().yatt_gather_rows(src.data_ptr(), d_idx.data_ptr(),
+                                 nk.data_ptr(), n, row_bytes, None, out.data_ptr(),
+                                 torch.cuda.current_stream().cuda_stream))
+    want = src.cpu().numpy().reshape(n, row_bytes)[idx].reshape(-1)
+    assert np.array_equal(out.cpu().numpy(), want)
+
+
+def test_gather_varlen_multi_matches_single(cuda):
+    """The fused five-array gather (17 B/token payload) == five single gathers."""
+    rng = np.random.default_rng(11)
+    n, G = 4096, 16
+    lens = torch.as_tensor(rng.integers(1, 700, size=n), device=cuda)
+    rw = ops.synth_floats(3, 105, 0, n, "reward", G, device=cuda)
+    plan = ops.filter_compact(rw, lens, G)
+    old_cu = torch.zeros(n + 1, dtype=torch.int64, device=cuda)
+    old_cu[1:] = torch.cumsum(lens, 0)
+    tot, kt = int(old_cu[-1]), int(plan["counts"][1])
+    srcs = [torch.randint(-2**31, 2**31 - 1, (tot,), dtype=torch.int32, device=cuda),
+            torch.randn(tot, device=cuda), torch.randn(tot, device=cuda),
+            torch.randn(tot, device=cuda),
+            torch.randint(0, 2, (tot,), dtype=torch.uint8, device=cuda)]
+    off = torch.tensor([5], dtype=torch.int64, device=cuda)
+    fused = [torch.zeros(kt + 5, dtype=t.dtype, device=cuda) for t in srcs]
+    single = [torch.zeros(kt + 5, dtype=t.dtype, device=cuda) for t in srcs]
+    ops.gather_varlen_multi(srcs, old_cu, plan["index_map"], plan["new_cu"], plan["counts"][:1], n,
+                            fused, off)
+    for s_, d_ in zip(srcs, single):
+        ops.gather_varlen(s_, old_cu, plan["index_map"], plan["new_cu"], plan["counts"][:1], n, d_,
+                          off)
+    for a, b in zip(fused, single):
+        assert torch.equal(a.view(torch.uint8), b.view(torch.uint8))
+    with pytest.raises(ConfigError):
+        ops.gather_varlen_multi(srcs * 2, old_cu, plan["index_map"], plan["new_cu"],
+                                plan["counts"][:1], n, fused * 2)

@@ -121,8 +121,8 @@ def config5():
         check(lib().yatt_shard_round(ds.d.data_ptr(), off, 1, 0, 1, 1, C.byref(params.c()),
                                      ds.d_rep.data_ptr(), ds.d_mbs.data_ptr(), None))
         pl = ops.filter_compact(rew, d_lens, G)
-        for src, dst in zip(payload, outs):
-            ops.gather_varlen(src, old_cu, pl["index_map"], pl["new_cu"], pl["counts"][:1], n, dst)
+        ops.gather_varlen_multi(payload, old_cu, pl["index_map"], pl["new_cu"], pl["counts"][:1], n,
+                                outs)
         ops.gather_rows(refs, pl["index_map"], pl["counts"][:1], n, rout)
         ops.sort_order_desc(l32)
         ops.microbatch_aggregates(p32, l32, 16)

@@ -146,7 +146,12 @@ def main():
         for s, d in zip(srcs, dsts):
             ops.gather_varlen(s, old_cu, res["index_map"], res["new_cu"], res["counts"][:1], ns, d)
     ms = timeit(gather_all, iters=10)
-    report("gather_varlen 17 B/token payload", ms, kt * 17 * 2, kt, "tokens", total_tokens=total)
+    report("gather_varlen 17 B/token payload (5 launches)", ms, kt * 17 * 2, kt, "tokens",
+           total_tokens=total)
+    ms = timeit(lambda: ops.gather_varlen_multi(srcs, old_cu, res["index_map"], res["new_cu"],
+                                                res["counts"][:1], ns, dsts), iters=10)
+    report("gather_varlen_multi 17 B/token payload (1 launch)", ms, kt * 17 * 2, kt, "tokens",
+           total_tokens=total)
     # R3
     P = 8
     batch = api.RolloutBatch(1, [api.RolloutSample(ns + i, 64) for i in range(ns)])
