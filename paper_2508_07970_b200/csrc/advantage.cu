@@ -127,98 +127,30 @@ __device__ __forceinline__ Aff shfl_down_aff(const Aff& x, int d) {
              __shfl_down_sync(0xffffffffu, x.q, d)};
 }
 
-// Single-pass scan over the packed token array with decoupled look-back.
-// The array is cut into 2,048-token tiles; thread i of a 128-thread CTA owns
-// 16 contiguous tokens.  Persistent CTAs claim tiles right to left by an
-// atomic ticket (a tile only waits on tiles with earlier tickets, whose
-// holders are running: the smallest unfinished ticket is always being
-// processed, so the scan cannot deadlock) and keep the NEXT tile's values,
-// rewards and mask in flight (cp.async.bulk into the other shared-memory
-// stage) while the current tile is scanned.  Each tile publishes its
-// composite map (flag 1) and, once its incoming state is known, its outgoing
-// state (flag 2); a tile holding a sequence end has a constant composite and
-// publishes flag 2 at once, so look-back chains stop at the first sequence
-// boundary.  Bytes: 9 read + 8 written per token, once.
-constexpr int kGaeThreads = 128;
+// Single-pass scan over the packed token array with decoupled look-back,
+// one 512-token tile per warp (lane l owns 16 contiguous tokens).  Warps
+// claim tiles right to left by an atomic ticket: a tile only waits on tiles
+// with earlier tickets, whose warps are running, so the smallest unfinished
+// ticket always progresses and the scan cannot deadlock.  Bytes: 9 read + 8
+// written per token, once (+1 bit per token for the sequence-end mask).
 constexpr int kGaeTpt = 16;
-constexpr int kGaeTile = kGaeThreads * kGaeTpt;
+constexpr int kGaeWTile = 32 * kGaeTpt;
 
-// Device workspace (yatt_gae_workspace_bytes): ticket | incl[ntiles] |
-// aflag[ntiles] (zeroed per call) | agg[ntiles].  incl[t] is one 16-byte
-// record {double A; float V; u32 flag}: the state leaving tile t to the left
-// (V is an input value or 0, so fp32 holds it exactly) and its ready flag in
-// the same single 16-byte store, so a look-back step is one L2 round trip.
+// Device workspace (yatt_gae_workspace_bytes), zeroed per call:
+//   ticket | rec[ntiles] (16 B each) | ends[ntiles * 16] (bit i: token i is
+//   the last token of a sequence).
 struct GaeWs {
   uint32_t* ticket;
-  uint4* incl;      // [ntiles]
-  uint32_t* aflag;  // [ntiles] agg[t] published
-  Aff* agg;         // [ntiles] composite map of tile t
+  uint4* rec;
+  uint32_t* ends;
 };
 __host__ __device__ inline size_t gae_align(size_t x) { return (x + 15) & ~size_t(15); }
 __host__ __device__ inline GaeWs gae_ws(void* base, int64_t ntiles) {
   uint8_t* b = static_cast<uint8_t*>(base);
-  GaeWs w;
-  w.ticket = reinterpret_cast<uint32_t*>(b);
-  w.incl = reinterpret_cast<uint4*>(b + 16);
-  w.aflag = reinterpret_cast<uint32_t*>(b + 16 + 16 * size_t(ntiles));
-  w.agg = reinterpret_cast<Aff*>(b + gae_align(16 + 20 * size_t(ntiles)));
-  return w;
+  return GaeWs{reinterpret_cast<uint32_t*>(b), reinterpret_cast<uint4*>(b + 16),
+               reinterpret_cast<uint32_t*>(b + 16 + 16 * size_t(ntiles))};
 }
-size_t gae_ws_bytes(int64_t ntiles) {
-  return gae_align(16 + 20 * size_t(ntiles)) + sizeof(Aff) * size_t(ntiles);
-}
-size_t gae_zero_bytes(int64_t ntiles) { return 16 + 20 * size_t(ntiles); }
-
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_incl(uint4* p, double A, double V) {
-  const uint4 w = make_uint4(uint32_t(__double2loint(A)), uint32_t(__double2hiint(A)),
-                             __float_as_uint(float(V)), 2u);
-  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(w.x), "r"(w.y),
-               "r"(w.z), "r"(w.w)
-               : "memory");
-}
-__device__ __forceinline__ uint4 ld_incl(const uint4* p) {
-  uint4 w;
-  asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
-               : "l"(p)
-               : "memory");
-  return w;
-}
-
-// First index k in [k0, k1) with a[k] >= key (k1 if none), a non-decreasing;
-// one warp, 32-ary: positions >= k1 count as +inf, so the predicate is
-// monotone in the lane and the answer stays inside [k0, k1].
-__device__ int64_t warp_lower_bound(const int64_t* a, int64_t k0, int64_t k1, int64_t key,
-                                    int lane) {
-  while (k1 - k0 > 32) {
-    const int64_t step = (k1 - k0 + 31) / 32;
-    const int64_t idx = k0 + lane * step;
-    const bool ge = idx >= k1 || __ldg(a + idx) >= key;
-    const uint32_t bal = __ballot_sync(0xffffffffu, ge);
-    if (bal & 1u) return k0;
-    const int f = bal ? __ffs(bal) - 1 : 32;
-    const int64_t nk0 = k0 + int64_t(f - 1) * step + 1;
-    if (f < 32) k1 = min64(k1, k0 + int64_t(f) * step);
-    k0 = nk0;
-  }
-  const bool ge = k0 + lane < k1 && __ldg(a + k0 + lane) >= key;
-  const uint32_t bal = __ballot_sync(0xffffffffu, ge);
-  return bal ? k0 + __ffs(bal) - 1 : k1;
-}
-
-struct __align__(128) GaeStage {
-  float v[kGaeTile];
-  float r[kGaeTile];
-  uint8_t m[kGaeTile];
-};
+size_t gae_ws_bytes(int64_t ntiles) { return gae_align(16 + 16 * size_t(ntiles) + 64 * size_t(ntiles)); }
 
 struct GaeArgs {
   const float* values;
@@ -231,240 +163,262 @@ struct GaeArgs {
   float* ret;
 };
 
+__device__ __forceinline__ uint4 ld_incl(const uint4* p) {
+  uint4 w;
+  asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+               : "l"(p)
+               : "memory");
+  return w;
+}
+
+// Tile record for the warp kernel (one 16-byte word per tile, written with
+// a single store, so data and flag arrive together and no fence is needed):
+//   flag 2: {double A, float V}     state leaving the tile to the left
+//   flag 1: {double p, float q, m}  composite of a tile without a sequence
+//           end: m valid tokens -> a = gl^m, b = g gl^(m-1), k = 0 (m = 0:
+//           identity)
+__device__ __forceinline__ void st_rec(uint4* p, double x, double y, uint32_t tag) {
+  const uint4 w = make_uint4(uint32_t(__double2loint(x)), uint32_t(__double2hiint(x)),
+                             __float_as_uint(float(y)), tag);
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(w.x), "r"(w.y),
+               "r"(w.z), "r"(w.w)
+               : "memory");
+}
+__device__ __forceinline__ double ipow(double x, uint32_t m) {
+  double r = 1.0;
+  while (m) {
+    if (m & 1u) r *= x;
+    x *= x;
+    m >>= 1;
+  }
+  return r;
+}
+__device__ __forceinline__ Aff rec_map(const uint4& w, double gamma, double gl) {
+  const double x = __hiloint2double(int(w.y), int(w.x)), y = double(__uint_as_float(w.z));
+  if ((w.w & 3u) == 2u) return Aff{0.0, 0.0, 0.0, x, y};
+  const uint32_t m = w.w >> 2;
+  if (m == 0u) return aff_id();
+  return Aff{ipow(gl, m), gamma * ipow(gl, m - 1u), 0.0, x, y};
+}
+
+// ---- the scan kernel: one 512-token tile per warp, no CTA barriers ----
+// Lane l owns tokens [lo + 16l, lo + 16l + 16) in registers (float4 loads)
+// and their 16 sequence-end bits; lanes whose 16 tokens are all inside, valid
+// and not sequence ends take a straight-line fp64 path.  Compose, shuffle
+// scan, publish the tile record, then the look-back reads 32 predecessor
+// records at once (lane i -> tile t+1+i) and composes them up to the first
+// published state with one shuffle tree: one L2 round trip per 32 tiles.
+__device__ __forceinline__ Aff shfl_aff(const Aff& x, int src) {
+  return Aff{__shfl_sync(0xffffffffu, x.a, src), __shfl_sync(0xffffffffu, x.b, src),
+             __shfl_sync(0xffffffffu, x.k, src), __shfl_sync(0xffffffffu, x.p, src),
+             __shfl_sync(0xffffffffu, x.q, src)};
+}
+
 #ifdef YATT_GAE_PROFILE
-// Phase timestamps per tile (variant builds only): start, data ready, ends
-// marked, scan done, carry known, tile done.
+// Phase timestamps per tile (variant builds only; tools/gae_phases.py):
+// start, ticket, ends/data, scan done, carry known, tile done.
 __device__ long long g_gae_prof[16384][6];
-#define GAE_STAMP(k) \
-  if (tid == ((k) == 4 ? kGaeThreads - 32 : 0) && t < 16384) g_gae_prof[t][k] = clock64()
+#define GAE_WSTAMP(k) \
+  if (lane == 0 && t >= 0 && t < 16384) g_gae_prof[t][k] = clock64()
 #else
-#define GAE_STAMP(k)
+#define GAE_WSTAMP(k)
 #endif
 
-template <bool kBulk>
-__global__ void __launch_bounds__(kGaeThreads) gae_pipe_kernel(const GaeArgs g, GaeWs ws) {
-  __shared__ GaeStage stg[2];
-  __shared__ __align__(8) uint64_t full[2];
-  __shared__ uint32_t last_bits[kGaeTile / 32];  // bit j: token lo+j ends a sequence
-  __shared__ Aff wtot[kGaeThreads / 32];
-  __shared__ double2 carry;
-  __shared__ int64_t s_tile[2], s_k[2];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// Marks the last token of every non-empty sequence in the ends bitmask.
+__global__ void gae_mark_ends_kernel(const int64_t* cu, int64_t nseq, int64_t n_tokens,
+                                     uint32_t* ends) {
+  const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= nseq) return;
+  const int64_t b = __ldg(cu + k), e = min64(__ldg(cu + k + 1), n_tokens);
+  if (e > b && e >= 1) atomicOr(ends + ((e - 1) >> 5), 1u << ((e - 1) & 31));
+}
+
+template <bool kVec>
+__global__ void __launch_bounds__(128) gae_warp_kernel(const GaeArgs g, GaeWs ws) {
+  const int lane = threadIdx.x & 31;
   const double gamma = g.gamma, gl = g.gamma * g.lam;
-  const int64_t in_lo = __ldg(g.cu), in_hi = min64(g.n_tokens, __ldg(g.cu + g.nseq));
-  // a tile goes by bulk copy when it is full (sizes multiple of 16 B)
-  auto bulk_ok = [&](int64_t t) { return kBulk && (t + 1) * kGaeTile <= g.n_tokens; };
-  auto claim = [&]() { return g.ntiles - 1 - int64_t(atomicAdd(ws.ticket, 1u)); };
-  auto issue = [&](int64_t t, int s) {  // thread 0
-    const int64_t lo = t * kGaeTile;
-    const uint64_t pol = l2_evict_first_policy();
-    mbar_arrive_expect_tx(&full[s], (g.mask ? 9u : 8u) * kGaeTile);
-    bulk_g2s(stg[s].v, g.values + lo, 4u * kGaeTile, &full[s], pol);
-    bulk_g2s(stg[s].r, g.rewards + lo, 4u * kGaeTile, &full[s], pol);
-    if (g.mask) bulk_g2s(stg[s].m, g.mask + lo, kGaeTile, &full[s], pol);
-  };
-  if (tid == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
-    fence_mbar_init();
-    const int64_t t0 = claim();
-    s_tile[0] = t0;
-    if (t0 >= 0 && bulk_ok(t0)) issue(t0, 0);
-  }
-  __syncthreads();
-  int s = 0;
-  uint32_t phase[2] = {0u, 0u};
-  for (int64_t t = s_tile[0]; t >= 0; t = s_tile[s ^= 1]) {
-    if (tid == 0) {  // keep the next tile in flight while this one is scanned
-      const int64_t nx = claim();
-      s_tile[s ^ 1] = nx;
-      if (nx >= 0 && bulk_ok(nx)) issue(nx, s ^ 1);
-    }
-    GAE_STAMP(0);
-    const int64_t lo = t * kGaeTile, hi = min64(g.n_tokens, lo + kGaeTile);
-    for (int i = tid; i < kGaeTile / 32; i += kGaeThreads) last_bits[i] = 0u;
-    if (warp < 2) {  // sequence ends in the tile: k with cu[k] in [lo+1, hi]
-      const int64_t k = warp_lower_bound(g.cu, 1, g.nseq + 1, (warp == 0 ? lo : hi) + 1, lane);
-      if (lane == 0) s_k[warp] = k;
-    }
-    GaeStage& S = stg[s];
-    if (bulk_ok(t)) {
-      mbar_wait(&full[s], phase[s]);
-      phase[s] ^= 1u;
-      GAE_STAMP(1);
-    } else {  // ragged last tile or unaligned arrays: cooperative element loads
-      for (int64_t i = lo + tid; i < lo + kGaeTile; i += kGaeThreads) {
-        const bool ok = i < hi;
-        S.v[i - lo] = ok ? g.values[i] : 0.f;
-        S.r[i - lo] = ok ? g.rewards[i] : 0.f;
-        S.m[i - lo] = ok ? (g.mask ? g.mask[i] : uint8_t(1)) : uint8_t(0);
-      }
-    }
-    __syncthreads();
-    for (int64_t k = s_k[0] + tid; k < s_k[1]; k += kGaeThreads) {
-      const int64_t j = __ldg(g.cu + k) - 1 - lo;
-      atomicOr(&last_bits[j >> 5], 1u << (j & 31));
-    }
-    __syncthreads();
-    GAE_STAMP(2);
-    const int j0 = tid * kGaeTpt;  // this thread's first token within the tile
-    const int64_t x0 = lo + j0;
-    const int nmine = int(max64(0, min64(kGaeTpt, hi - x0)));
-    // 16-bit masks over this thread's tokens: inside [cu[0], cu[nseq]) and
-    // the array, valid (mask != 0), last token of a sequence
-    const uint32_t lb = (last_bits[j0 >> 5] >> (j0 & 31)) & 0xffffu;
-    uint32_t insm = 0u, validm = 0xffffu;
-    {
-      const int64_t a = max64(0, in_lo - x0), b = min64(nmine, in_hi - x0);
-      if (b > a) insm = ((1u << b) - 1u) & ~((1u << a) - 1u);
+  int64_t t = 0;
+#ifdef YATT_GAE_PROFILE
+  const long long t_start = clock64();
+#endif
+  if (lane == 0) t = g.ntiles - 1 - int64_t(atomicAdd(ws.ticket, 1u));
+  t = __shfl_sync(0xffffffffu, t, 0);
+  if (t < 0) return;
+#ifdef YATT_GAE_PROFILE
+  if (lane == 0 && t < 16384) g_gae_prof[t][0] = t_start;
+#endif
+  GAE_WSTAMP(1);
+  const int64_t lo = t * kGaeWTile, hi = min64(g.n_tokens, lo + kGaeWTile);
+  const int64_t x0 = lo + int64_t(lane) * kGaeTpt;
+  const int nmine = int(max64(0, min64(kGaeTpt, hi - x0)));
+  // loads first: they fly while the sequence ends are found
+  float v[kGaeTpt], r[kGaeTpt];
+  uint32_t validm = 0xffffu;
+  if (kVec && nmine == kGaeTpt) {
+#pragma unroll
+    for (int q = 0; q < kGaeTpt / 4; ++q) {
+      const float4 a = __ldcs(reinterpret_cast<const float4*>(g.values + x0) + q);
+      const float4 b = __ldcs(reinterpret_cast<const float4*>(g.rewards + x0) + q);
+      v[4 * q] = a.x, v[4 * q + 1] = a.y, v[4 * q + 2] = a.z, v[4 * q + 3] = a.w;
+      r[4 * q] = b.x, r[4 * q + 1] = b.y, r[4 * q + 2] = b.z, r[4 * q + 3] = b.w;
     }
     if (g.mask) {
-      const uint4 m4 = *reinterpret_cast<const uint4*>(S.m + j0);
+      const uint4 m4 = __ldcs(reinterpret_cast<const uint4*>(g.mask + x0));
       const uint32_t mw[4] = {m4.x, m4.y, m4.z, m4.w};
       validm = 0u;
 #pragma unroll
       for (int j = 0; j < kGaeTpt; ++j)
         validm |= ((mw[j >> 2] >> (8 * (j & 3))) & 0xffu) ? (1u << j) : 0u;
     }
-
-    // compose this thread's tokens right to left
-    Aff f = aff_id();
+  } else {
 #pragma unroll
-    for (int q = kGaeTpt / 4 - 1; q >= 0; --q) {
-      const float4 v4 = *reinterpret_cast<const float4*>(S.v + j0 + 4 * q);
-      const float4 r4 = *reinterpret_cast<const float4*>(S.r + j0 + 4 * q);
-      const float vq[4] = {v4.x, v4.y, v4.z, v4.w}, rq[4] = {r4.x, r4.y, r4.z, r4.w};
-#pragma unroll
-      for (int u = 3; u >= 0; --u) {
-        const uint32_t bit = 1u << (4 * q + u);
-        if (!(insm & bit)) continue;
-        if (lb & bit) f = Aff{0.0, 0.0, 0.0, 0.0, 0.0};
-        if (validm & bit) {
-          const double vv = f2d(vq[u]);
-          f = Aff{gl * f.a, gl * f.b + gamma * f.k, 0.0,
-                  gl * f.p + gamma * f.q + (f2d(rq[u]) - vv), vv};
-        }
-      }
+    for (int j = 0; j < kGaeTpt; ++j) {
+      v[j] = j < nmine ? g.values[x0 + j] : 0.f;
+      r[j] = j < nmine ? g.rewards[x0 + j] : 0.f;
     }
-    // inclusive scan from the right inside the warp, then warp totals
-    Aff inc = f;
+    if (g.mask) {
+      validm = 0u;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const Aff o = shfl_down_aff(inc, d);
-      if (lane + d < 32) inc = compose(inc, o);
+      for (int j = 0; j < kGaeTpt; ++j) validm |= (j < nmine && g.mask[x0 + j]) ? (1u << j) : 0u;
     }
-    if (lane == 0) wtot[warp] = inc;
-    __syncthreads();
-    GAE_STAMP(3);
-    // composite of the threads to my right: later lanes, then later warps
-    Aff right = aff_id();
-    for (int w = kGaeThreads / 32 - 1; w > warp; --w) right = compose(wtot[w], right);
-    Aff ex = shfl_down_aff(inc, 1);
-    if (lane == 31) ex = aff_id();
-    ex = compose(ex, right);
-    // replay right to left from shared memory, four tokens per step
-    const bool all_in = insm == 0xffffu;
-    auto replay = [&](double A, double Vn) {
-#pragma unroll
-      for (int q = kGaeTpt / 4 - 1; q >= 0; --q) {
-        const float4 v4 = *reinterpret_cast<const float4*>(S.v + j0 + 4 * q);
-        const float4 r4 = *reinterpret_cast<const float4*>(S.r + j0 + 4 * q);
-        const float vq[4] = {v4.x, v4.y, v4.z, v4.w}, rq[4] = {r4.x, r4.y, r4.z, r4.w};
-        float ao[4], ro[4];
-#pragma unroll
-        for (int u = 3; u >= 0; --u) {
-          const uint32_t bit = 1u << (4 * q + u);
-          ao[u] = 0.f, ro[u] = 0.f;
-          if (!(insm & bit)) continue;
-          if (lb & bit) A = 0.0, Vn = 0.0;
-          const double vv = f2d(vq[u]);
-          if (validm & bit) {
-            A = (f2d(rq[u]) - vv) + gamma * Vn + gl * A;
-            Vn = vv;
-          }
-          ao[u] = float(A);
-          ro[u] = float(A + vv);
-        }
-        if (kBulk && all_in) {
-          __stcs(reinterpret_cast<float4*>(g.adv + x0) + q, make_float4(ao[0], ao[1], ao[2], ao[3]));
-          __stcs(reinterpret_cast<float4*>(g.ret + x0) + q, make_float4(ro[0], ro[1], ro[2], ro[3]));
-        } else {
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (insm & (1u << (4 * q + u))) {
-              g.adv[x0 + 4 * q + u] = ao[u];
-              g.ret[x0 + 4 * q + u] = ro[u];
-            }
-        }
-      }
-    };
-    // lane 0 of the last warp publishes the tile and looks back; meanwhile
-    // every thread with a sequence end to its right inside the tile (constant
-    // right composite) replays without waiting for the carry
-    if (tid == kGaeThreads - 32) {
-      Aff tot = wtot[kGaeThreads / 32 - 1];
-      for (int w = kGaeThreads / 32 - 2; w >= 0; --w) tot = compose(wtot[w], tot);
-      const bool constant = tot.a == 0.0 && tot.b == 0.0 && tot.k == 0.0;
-      if (constant) {
-        st_incl(ws.incl + t, tot.p, tot.q);
-      } else {
-        ws.agg[t] = tot;
-        st_release(ws.aflag + t, 1u);
-      }
-      // look-back: state entering from the right = M_{t+1} o ... o (state of
-      // the first tile to the right that published its outgoing state)
-      Aff c = aff_id();
-      double2 st = make_double2(0.0, 0.0);
-      for (int64_t j = t + 1; j < g.ntiles; ++j) {
-        int spins = 0;
-        for (;;) {
-          const uint4 w = ld_incl(ws.incl + j);
-          if (w.w != 0u) {
-            st = make_double2(__hiloint2double(int(w.y), int(w.x)), double(__uint_as_float(w.z)));
-            j = g.ntiles;  // done
-            break;
-          }
-          if (ld_acquire(ws.aflag + j) != 0u) {
-            const Aff* a = ws.agg + j;
-            c = compose(c, Aff{__ldcg(&a->a), __ldcg(&a->b), __ldcg(&a->k), __ldcg(&a->p),
-                               __ldcg(&a->q)});
-            break;
-          }
-          if (++spins > 4) __nanosleep(32);
-        }
-      }
-      const double2 in_state = make_double2(c.a * st.x + c.b * st.y + c.p, c.k * st.y + c.q);
-      if (!constant)
-        st_incl(ws.incl + t, tot.a * in_state.x + tot.b * in_state.y + tot.p,
-                tot.k * in_state.y + tot.q);
-      carry = in_state;
-      GAE_STAMP(4);
-    }
-    const bool need_carry = !(ex.a == 0.0 && ex.b == 0.0 && ex.k == 0.0);
-    if (!need_carry) replay(ex.p, ex.q);
-    __syncthreads();
-    if (need_carry) {
-      const double2 cs = carry;
-      replay(ex.a * cs.x + ex.b * cs.y + ex.p, ex.k * cs.y + ex.q);
-    }
-    __syncthreads();  // stage s, last_bits, wtot and carry are reused next
-    GAE_STAMP(5);
   }
+  // this lane's 16 sequence-end bits (marked by gae_mark_ends_kernel)
+  const uint32_t lb = (__ldcg(ws.ends + (x0 >> 5)) >> (x0 & 31)) & 0xffffu;
+  const int64_t in_lo = __ldg(g.cu), in_hi = min64(g.n_tokens, __ldg(g.cu + g.nseq));
+  GAE_WSTAMP(2);
+  uint32_t insm = 0u;
+  {
+    const int64_t a = max64(0, in_lo - x0), b = min64(nmine, in_hi - x0);
+    if (b > a) insm = ((1u << b) - 1u) & ~((1u << a) - 1u);
+  }
+  // compose this lane's tokens right to left.  Fast path (most lanes): all 16
+  // tokens inside, valid and not sequence ends -> a = gl^16, b = g gl^15,
+  // k = 0 and only the offset chain is computed.
+  const bool plain = insm == 0xffffu && validm == 0xffffu && lb == 0u;
+  Aff f = aff_id();
+  if (plain) {
+    double p = 0.0, q = 0.0;
+#pragma unroll
+    for (int j = kGaeTpt - 1; j >= 0; --j) {
+      const double vv = f2d(v[j]);
+      p = fma(gl, p, fma(gamma, q, f2d(r[j]) - vv));
+      q = vv;
+    }
+    double a = gl, b = gamma;
+#pragma unroll
+    for (int j = 1; j < kGaeTpt; ++j) a *= gl, b *= gl;
+    f = Aff{a, b, 0.0, p, q};
+  } else {
+#pragma unroll
+    for (int j = kGaeTpt - 1; j >= 0; --j) {
+      const uint32_t bit = 1u << j;
+      if (!(insm & bit)) continue;
+      if (lb & bit) f = Aff{0.0, 0.0, 0.0, 0.0, 0.0};
+      if (validm & bit) {
+        const double vv = f2d(v[j]);
+        f = Aff{gl * f.a, gl * f.b + gamma * f.k, 0.0, gl * f.p + gamma * f.q + (f2d(r[j]) - vv),
+                vv};
+      }
+    }
+  }
+  // inclusive scan from the right: lane 0 ends with the tile's composite
+  Aff inc = f;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const Aff o = shfl_down_aff(inc, d);
+    if (lane + d < 32) inc = compose(inc, o);
+  }
+  Aff ex = shfl_down_aff(inc, 1);  // lanes to my right
+  if (lane == 31) ex = aff_id();
+  const Aff tot = shfl_aff(inc, 0);
+  const bool constant = tot.a == 0.0 && tot.b == 0.0 && tot.k == 0.0;
+  GAE_WSTAMP(3);
+  if (!constant) {  // valid tokens of a tile without sequence ends
+    const uint32_t m = __reduce_add_sync(0xffffffffu, uint32_t(__popc(validm & insm)));
+    if (lane == 0) st_rec(ws.rec + t, tot.p, tot.q, (m << 2) | 1u);
+  } else if (lane == 0) {
+    st_rec(ws.rec + t, tot.p, tot.q, 2u);
+  }
+  // the carry: composite of the tiles to the right up to the first published
+  // outgoing state (the array end counts as state (0, 0)); one 16-byte record
+  // per tile, 32 tiles per round trip
+  Aff c = aff_id();
+  for (int64_t base = t + 1;; base += 32) {
+    const int64_t j = base + lane;
+    Aff m = aff_id();
+    int first;
+    for (int spins = 0;; ++spins) {
+      const uint4 w = j < g.ntiles ? ld_incl(ws.rec + j) : make_uint4(0u, 0u, 0u, 2u);
+      const uint32_t bi = __ballot_sync(0xffffffffu, (w.w & 3u) == 2u);
+      const uint32_t ba = __ballot_sync(0xffffffffu, (w.w & 3u) != 0u);
+      first = bi ? __ffs(bi) - 1 : 32;
+      const uint32_t need = first == 32 ? 0xffffffffu : ((2u << first) - 1u);
+      if ((ba & need) == need) {
+        if (lane <= first) m = rec_map(w, gamma, gl);
+        break;
+      }
+      if (spins > 4) __nanosleep(32);
+    }
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {  // lane 0: m_0 o m_1 o ... o m_31
+      const Aff o = shfl_down_aff(m, d);
+      if (lane + d < 32) m = compose(m, o);
+    }
+    c = compose(c, shfl_aff(m, 0));
+    if (first < 32) break;
+  }
+  const double cA = c.p, cV = c.q;  // c ends in a constant map
+  GAE_WSTAMP(4);
+  if (lane == 0 && !constant)
+    st_rec(ws.rec + t, tot.a * cA + tot.b * cV + tot.p, tot.k * cV + tot.q, 2u);
+  double A = ex.a * cA + ex.b * cV + ex.p;
+  double Vn = ex.k * cV + ex.q;
+  float ao[kGaeTpt], ro[kGaeTpt];
+  if (plain) {
+#pragma unroll
+    for (int j = kGaeTpt - 1; j >= 0; --j) {
+      const double vv = f2d(v[j]);
+      A = (f2d(r[j]) - vv) + gamma * Vn + gl * A;
+      Vn = vv;
+      ao[j] = float(A);
+      ro[j] = float(A + vv);
+    }
+  } else {
+#pragma unroll
+    for (int j = kGaeTpt - 1; j >= 0; --j) {
+      const uint32_t bit = 1u << j;
+      ao[j] = 0.f, ro[j] = 0.f;
+      if (!(insm & bit)) continue;
+      if (lb & bit) A = 0.0, Vn = 0.0;
+      const double vv = f2d(v[j]);
+      if (validm & bit) {
+        A = (f2d(r[j]) - vv) + gamma * Vn + gl * A;
+        Vn = vv;
+      }
+      ao[j] = float(A);
+      ro[j] = float(A + vv);
+    }
+  }
+  if (kVec && insm == 0xffffu) {
+#pragma unroll
+    for (int q = 0; q < kGaeTpt / 4; ++q) {
+      __stcs(reinterpret_cast<float4*>(g.adv + x0) + q,
+             make_float4(ao[4 * q], ao[4 * q + 1], ao[4 * q + 2], ao[4 * q + 3]));
+      __stcs(reinterpret_cast<float4*>(g.ret + x0) + q,
+             make_float4(ro[4 * q], ro[4 * q + 1], ro[4 * q + 2], ro[4 * q + 3]));
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kGaeTpt; ++j)
+      if (insm & (1u << j)) {
+        g.adv[x0 + j] = ao[j];
+        g.ret[x0 + j] = ro[j];
+      }
+  }
+  GAE_WSTAMP(5);
 }
 
-int gae_pipe_occupancy(bool bulk) {
-  static int occ[2] = {0, 0};
-  int& o = occ[bulk ? 1 : 0];
-  if (o == 0) {
-    int n = 0;
-    if (bulk)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, gae_pipe_kernel<true>, kGaeThreads, 0);
-    else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, gae_pipe_kernel<false>, kGaeThreads, 0);
-    o = n > 0 ? n : 1;
-  }
-  return o;
-}
 
 // ------------------------------------------------------- masked moments ----
 constexpr int kMomThreads = 256;
@@ -631,7 +585,7 @@ int broadcast_launch(const float* vals, const int64_t* cu, int64_t nsamples, con
 }
 
 size_t gae_workspace_bytes(int64_t n_tokens) {
-  return gae_ws_bytes(ceil_div(max64(n_tokens, 0), kGaeTile));
+  return gae_ws_bytes(ceil_div(max64(n_tokens, 0), kGaeWTile));
 }
 
 int gae_launch(const float* values, const float* rewards, const uint8_t* mask, const int64_t* cu,
@@ -641,21 +595,23 @@ int gae_launch(const float* values, const float* rewards, const uint8_t* mask, c
   YATT_REQUIRE(gamma >= 0.f && lam >= 0.f, YATT_ERR_CONFIG, "gae: gamma/lam must be >= 0");
   if (nseq == 0 || n_tokens == 0) return YATT_OK;
   YATT_REQUIRE(values && rewards && cu && adv && ret, YATT_ERR_CONFIG, "gae: null pointer");
-  const int64_t ntiles = ceil_div(n_tokens, kGaeTile);
+  const int64_t ntiles = ceil_div(n_tokens, kGaeWTile);
   YATT_REQUIRE(ws != nullptr && ws_bytes >= gae_ws_bytes(ntiles), YATT_ERR_WORKSPACE,
                "gae: workspace too small (%zu < %zu)", ws_bytes, gae_ws_bytes(ntiles));
   YATT_REQUIRE(ntiles < (int64_t(1) << 31), YATT_ERR_CONFIG, "gae: too many tokens");
-  YATT_TRY_CUDA(cudaMemsetAsync(ws, 0, gae_zero_bytes(ntiles), st));
+  YATT_TRY_CUDA(cudaMemsetAsync(ws, 0, gae_ws_bytes(ntiles), st));
   auto a16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
-  const bool bulk = a16(values) && a16(rewards) && a16(mask) && a16(adv) && a16(ret);
+  const bool vec = a16(values) && a16(rewards) && a16(mask) && a16(adv) && a16(ret);
   const GaeArgs args{values, rewards, mask, cu, nseq, n_tokens, ntiles, double(gamma), double(lam),
                      adv, ret};
-  const int grid = int(min64(ntiles, int64_t(num_sms()) * gae_pipe_occupancy(bulk)));
-  if (bulk)
-    gae_pipe_kernel<true><<<grid, kGaeThreads, 0, st>>>(args, gae_ws(ws, ntiles));
+  const GaeWs w = gae_ws(ws, ntiles);
+  gae_mark_ends_kernel<<<unsigned(ceil_div(nseq, 256)), 256, 0, st>>>(cu, nseq, n_tokens, w.ends);
+  const unsigned grid = unsigned(ceil_div(ntiles, 4));  // 4 warps = 4 tiles per CTA
+  if (vec)
+    gae_warp_kernel<true><<<grid, 128, 0, st>>>(args, w);
   else
-    gae_pipe_kernel<false><<<grid, kGaeThreads, 0, st>>>(args, gae_ws(ws, ntiles));
-  return check_launch("gae_pipe_kernel");
+    gae_warp_kernel<false><<<grid, 128, 0, st>>>(args, w);
+  return check_launch("gae_kernel");
 }
 
 size_t moments_workspace_bytes() { return size_t(3) * kMomMaxParts * sizeof(double); }

@@ -24,13 +24,16 @@ m = torch.ones(n, dtype=torch.uint8, device="cuda")
 for _ in range(3):
     ops.gae(v, r, cu, m, 1.0, 0.95)
 torch.cuda.synchronize()
-ntiles = -(-n // 2048)
+import os
+tile = int(os.environ.get("GAE_TILE", "512"))
+ntiles = -(-n // tile)
 buf = np.zeros((ntiles, 6), dtype=np.int64)
 f = lib().yatt_debug_gae_profile
 f.argtypes = [C.c_void_p, C.c_int]
 assert f(buf.ctypes.data, ntiles) == 0
 d = np.diff(buf, axis=1) / 1.9e3  # us at ~1.9 GHz
-names = ["wait data", "mark ends", "compose+scan", "lookback", "replay+store"]
+names = (["wait data", "mark ends", "compose+scan", "lookback", "replay+store"] if tile == 2048 else
+         ["ticket", "load+search+mark", "compose+scan", "publish+lookback", "replay+store"])
 print(f"{ntiles} tiles; per-tile phase durations (us): mean / p50 / p90")
 for i, nm in enumerate(names):
     col = d[:, i]
