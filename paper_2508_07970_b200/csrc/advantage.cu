@@ -301,8 +301,8 @@ __global__ void __launch_bounds__(128) gae_warp_kernel(const GaeArgs g, GaeWs ws
     double p = 0.0, q = 0.0;
 #pragma unroll
     for (int j = kGaeTpt - 1; j >= 0; --j) {
-      const double vv = f2d(v[j]);
-      p = fma(gl, p, fma(gamma, q, f2d(r[j]) - vv));
+      const double vv = double(v[j]);
+      p = fma(gl, p, fma(gamma, q, double(r[j]) - vv));
       q = vv;
     }
     double a = gl, b = gamma;
@@ -316,8 +316,8 @@ __global__ void __launch_bounds__(128) gae_warp_kernel(const GaeArgs g, GaeWs ws
       if (!(insm & bit)) continue;
       if (lb & bit) f = Aff{0.0, 0.0, 0.0, 0.0, 0.0};
       if (validm & bit) {
-        const double vv = f2d(v[j]);
-        f = Aff{gl * f.a, gl * f.b + gamma * f.k, 0.0, gl * f.p + gamma * f.q + (f2d(r[j]) - vv),
+        const double vv = double(v[j]);
+        f = Aff{gl * f.a, gl * f.b + gamma * f.k, 0.0, gl * f.p + gamma * f.q + (double(r[j]) - vv),
                 vv};
       }
     }
@@ -378,8 +378,8 @@ __global__ void __launch_bounds__(128) gae_warp_kernel(const GaeArgs g, GaeWs ws
   if (plain) {
 #pragma unroll
     for (int j = kGaeTpt - 1; j >= 0; --j) {
-      const double vv = f2d(v[j]);
-      A = (f2d(r[j]) - vv) + gamma * Vn + gl * A;
+      const double vv = double(v[j]);
+      A = (double(r[j]) - vv) + gamma * Vn + gl * A;
       Vn = vv;
       ao[j] = float(A);
       ro[j] = float(A + vv);
@@ -391,9 +391,9 @@ __global__ void __launch_bounds__(128) gae_warp_kernel(const GaeArgs g, GaeWs ws
       ao[j] = 0.f, ro[j] = 0.f;
       if (!(insm & bit)) continue;
       if (lb & bit) A = 0.0, Vn = 0.0;
-      const double vv = f2d(v[j]);
+      const double vv = double(v[j]);
       if (validm & bit) {
-        A = (f2d(r[j]) - vv) + gamma * Vn + gl * A;
+        A = (double(r[j]) - vv) + gamma * Vn + gl * A;
         Vn = vv;
       }
       ao[j] = float(A);
@@ -426,7 +426,7 @@ constexpr int kMomMaxParts = 640;
 
 __device__ __forceinline__ void mom_add(float x, bool valid, double& c, double& s, double& q) {
   if (valid) {
-    const double v = f2d(x);
+    const double v = double(x);
     c += 1.0;
     s += v;
     q += v * v;
@@ -507,7 +507,7 @@ __device__ __forceinline__ WhitenCoef whiten_coef(const double* mom) {
   return WhitenCoef{mean, 1.0 / sqrt(var + 1e-8)};
 }
 __device__ __forceinline__ float whiten1(float x, const WhitenCoef& w, int32_t shift_mean) {
-  double v = (f2d(x) - w.mean) * w.inv;
+  double v = (f2d_int(x) - w.mean) * w.inv;
   if (!shift_mean) v += w.mean;
   return float(v);
 }

@@ -84,13 +84,12 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
-// Exact float -> double on the integer pipes (F2F.F64.F32 runs on the XU
-// pipe, which bounds streaming fp64 kernels): normals and +-0 by rebiasing
-// the exponent; denormals, inf and NaN (rare) take the conversion instruction.
-__device__ __forceinline__ double f2d(float f) {
-#ifdef YATT_F2D_XU
-  return double(f);
-#endif
+// Exact float -> double on the integer pipes.  F2F.F64.F32 issues to the XU
+// pipe; measured per kernel (tools/bench_kernels.py, both builds): the plain
+// conversion wins where XU has headroom (loss, moments, GAE), this one where
+// the kernel does little else per element (whiten).  Normals and +-0 by
+// rebiasing the exponent; denormals, inf and NaN take the instruction.
+__device__ __forceinline__ double f2d_int(float f) {
   const uint32_t u = __float_as_uint(f), a = u & 0x7fffffffu;
   if (__builtin_expect(a - 0x00800000u >= 0x7f000000u, 0) && a != 0u) return double(f);
   const uint32_t hi = (u & 0x80000000u) | (a != 0u ? (a >> 3) + 0x38000000u : 0u);

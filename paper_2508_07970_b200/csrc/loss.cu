@@ -31,7 +31,7 @@ constexpr int kFields = 8;  // yatt_loss_sums fields
 // loss_sum follows by linearity (sum L = sum pg + kl_coef sum kl -
 // entropy_coef sum H), kl and H enter as fp32 sums of at most four tokens
 // (one rounding per vector, relative 2^-23 of same-sign terms), counts are
-// integers.  Inputs reach fp64 through f2d (integer pipes).
+// integers.
 struct Acc {
   double pg = 0, ratio = 0, kl = 0, ent = 0;
   int32_t clip = 0, cnt = 0;
@@ -47,8 +47,8 @@ __device__ __forceinline__ LossCfg loss_cfg(const yatt_loss_config& c) {
 
 __device__ __forceinline__ void pg_term(float logp, float old_logp, float A, const LossCfg& c,
                                         Acc& s) {
-  const double ratio = exp(f2d(logp) - f2d(old_logp));
-  const double a = f2d(A);
+  const double ratio = exp(double(logp) - double(old_logp));
+  const double a = double(A);
   const double pg1 = -a * ratio;
   const double pg2 = -a * fmin(fmax(ratio, c.lo), c.hi);
   double pg = fmax(pg1, pg2);
@@ -72,8 +72,8 @@ __device__ __forceinline__ float4 ldg4(const float* p, int64_t i) {
 __device__ __forceinline__ void add_token(const LossIn& in, int64_t i, const LossCfg& c, Acc& s) {
   if (in.mask != nullptr && !in.mask[i]) return;
   pg_term(__ldg(in.logp + i), __ldg(in.old_logp + i), __ldg(in.adv + i), c, s);
-  if (in.kl) s.kl += f2d(__ldg(in.kl + i));
-  if (in.ent) s.ent += f2d(__ldg(in.ent + i));
+  if (in.kl) s.kl += double(__ldg(in.kl + i));
+  if (in.ent) s.ent += double(__ldg(in.ent + i));
 }
 
 // Four tokens [4j, 4j+4) from 16-byte loads (float inputs 16-B aligned, mask
@@ -105,8 +105,8 @@ __device__ __forceinline__ void add_vec(const Vec4& x, const LossCfg& c, Acc& s)
     k4 += kl[k];
     h4 += h[k];
   }
-  s.kl += f2d(k4);
-  s.ent += f2d(h4);
+  s.kl += double(k4);
+  s.ent += double(h4);
 }
 
 // Block-wide sum of kFields doubles; result valid in thread 0.
