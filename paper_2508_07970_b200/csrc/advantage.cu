@@ -172,12 +172,14 @@ __device__ __forceinline__ uint4 ld_incl(const uint4* p) {
   return w;
 }
 
-// Tile record for the warp kernel (one 16-byte word per tile, written with
-// a single store, so data and flag arrive together and no fence is needed):
-//   flag 2: {double A, float V}     state leaving the tile to the left
-//   flag 1: {double p, float q, m}  composite of a tile without a sequence
-//           end: m valid tokens -> a = gl^m, b = g gl^(m-1), k = 0 (m = 0:
-//           identity)
+// Tile record (one 16-byte word per tile, written once with a single store,
+// so data and flag arrive together and no fence is needed; both kinds depend
+// only on the tile's own tokens, so every look-back composes the same maps in
+// the same order: the scan is run-to-run bit-deterministic):
+//   flag 2: {double A, float V}     tile holding a sequence end: the state it
+//                                   passes to the left (constant composite)
+//   flag 1: {double p, float q, m}  tile without one: its composite, m valid
+//           tokens -> a = gl^m, b = g gl^(m-1), k = 0 (m = 0: identity)
 __device__ __forceinline__ void st_rec(uint4* p, double x, double y, uint32_t tag) {
   const uint4 w = make_uint4(uint32_t(__double2loint(x)), uint32_t(__double2hiint(x)),
                              __float_as_uint(float(y)), tag);
@@ -208,7 +210,8 @@ __device__ __forceinline__ Aff rec_map(const uint4& w, double gamma, double gl) 
 // and not sequence ends take a straight-line fp64 path.  Compose, shuffle
 // scan, publish the tile record, then the look-back reads 32 predecessor
 // records at once (lane i -> tile t+1+i) and composes them up to the first
-// published state with one shuffle tree: one L2 round trip per 32 tiles.
+// tile holding a sequence end with one shuffle tree: one L2 round trip per 32
+// tiles, and no tile waits on another tile's look-back.
 __device__ __forceinline__ Aff shfl_aff(const Aff& x, int src) {
   return Aff{__shfl_sync(0xffffffffu, x.a, src), __shfl_sync(0xffffffffu, x.b, src),
              __shfl_sync(0xffffffffu, x.k, src), __shfl_sync(0xffffffffu, x.p, src),
@@ -340,8 +343,8 @@ __global__ void __launch_bounds__(128) gae_warp_kernel(const GaeArgs g, GaeWs ws
   } else if (lane == 0) {
     st_rec(ws.rec + t, tot.p, tot.q, 2u);
   }
-  // the carry: composite of the tiles to the right up to the first published
-  // outgoing state (the array end counts as state (0, 0)); one 16-byte record
+  // the carry: composite of the tiles to the right up to the first one holding
+  // a sequence end (the array end counts as state (0, 0)); one 16-byte record
   // per tile, 32 tiles per round trip
   Aff c = aff_id();
   for (int64_t base = t + 1;; base += 32) {
@@ -370,8 +373,6 @@ __global__ void __launch_bounds__(128) gae_warp_kernel(const GaeArgs g, GaeWs ws
   }
   const double cA = c.p, cV = c.q;  // c ends in a constant map
   GAE_WSTAMP(4);
-  if (lane == 0 && !constant)
-    st_rec(ws.rec + t, tot.a * cA + tot.b * cV + tot.p, tot.k * cV + tot.q, 2u);
   double A = ex.a * cA + ex.b * cV + ex.p;
   double Vn = ex.k * cV + ex.q;
   float ao[kGaeTpt], ro[kGaeTpt];

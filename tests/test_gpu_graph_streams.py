@@ -1,0 +1,116 @@
+"""The C ABI under CUDA graphs and concurrent streams.
+
+* Every hot-path entry point is stream-ordered with caller workspaces and no
+  host sync, so a whole experience step (A1 -> GRPO -> broadcast -> A4, plus
+  GAE / moments / filter / gather) can be captured into one CUDA graph; the
+  replay must reproduce the eager results bit for bit.
+* Reentrancy (yatt_cuda.h "Conventions"): the same ops on two streams at once,
+  each with its own buffers and workspaces, give the single-stream results —
+  including the GAE scan, whose tiles exchange carries through the workspace.
+"""
+import pytest
+import torch
+
+from paper_2508_07970_b200 import api, ops
+
+pytestmark = pytest.mark.gpu
+
+
+def _inputs(dev, seed=7, rows=4096, V=32000, G=8):
+    pol, ref, tgt = ops.synth_logits(seed, 0, rows, V, device=dev)
+    n_samples = rows // 512
+    rew = ops.synth_floats(seed, 105, 0, n_samples, "reward", G, device=dev)
+    cu = torch.arange(n_samples + 1, dtype=torch.int64, device=dev) * 512
+    old = ops.synth_floats(seed, 104, 0, rows, "old_delta", device=dev)
+    lens = api.sample_lengths(api.LengthDistribution(api.UNIFORM, 1, 3000, 3000), 64, seed)
+    gcu = torch.zeros(65, dtype=torch.int64, device=dev)
+    gcu[1:] = torch.cumsum(torch.tensor(lens, device=dev), 0)
+    nt = int(gcu[-1])
+    v = ops.synth_floats(seed, 106, 0, nt, "value", device=dev)
+    r = ops.synth_floats(seed, 111, 0, nt, "kl", device=dev)
+    return dict(pol=pol, ref=ref, tgt=tgt, rew=rew, cu=cu, old=old, G=G, gcu=gcu, v=v, r=r,
+                d_lens=gcu[1:] - gcu[:-1])
+
+
+class Step:
+    """All outputs and workspaces preallocated, so the step is capturable."""
+
+    def __init__(self, x, dev):
+        self.x = x
+        rows = x["pol"].shape[0]
+        self.stats = torch.empty((4, rows), device=dev)
+        self.tadv = torch.empty(rows, device=dev)
+        self.ws = ops.LossWorkspace(dev)
+        self.sums = torch.empty(8, dtype=torch.float64, device=dev)
+        self.adv_out = None
+
+    def __call__(self):
+        x = self.x
+        ops.token_stats(x["pol"], x["ref"], x["tgt"], None, "k3", out=self.stats)
+        adv = ops.grpo_advantages(x["rew"], x["G"])
+        ops.broadcast_to_tokens(adv, x["cu"], self.tadv.numel(), None, self.tadv)
+        ops.policy_loss(self.stats[0], x["old"], self.tadv, self.stats[3], self.stats[2], None,
+                        None, None, self.ws, self.sums)
+        gadv, gret = ops.gae(x["v"], x["r"], x["gcu"], None, 0.99, 0.95)
+        mom = ops.masked_moments(gadv)
+        plan = ops.filter_compact(x["rew"], x["d_lens"][: x["rew"].numel()], x["G"])
+        self.outs = [self.stats, self.tadv, self.sums, gadv, gret, mom, plan["index_map"],
+                     plan["new_cu"], plan["counts"]]
+        return self.outs
+
+
+def test_experience_step_replays_bit_exact_from_a_cuda_graph(cuda):
+    x = _inputs(cuda)
+    step = Step(x, cuda)
+    eager = [t.clone() for t in step()]
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()  # warm-up on a side stream (torch's capture recipe)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        outs = step()
+    for t in outs:
+        t.zero_()
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(eager, outs):
+        assert torch.equal(a, b)
+
+
+def test_two_streams_run_the_path_concurrently(cuda):
+    xa, xb = _inputs(cuda, seed=1), _inputs(cuda, seed=2)
+    ref_a = [t.clone() for t in Step(xa, cuda)()]
+    ref_b = [t.clone() for t in Step(xb, cuda)()]
+    torch.cuda.synchronize()
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    step_a, step_b = Step(xa, cuda), Step(xb, cuda)
+    for _ in range(3):
+        with torch.cuda.stream(sa):
+            oa = step_a()
+        with torch.cuda.stream(sb):
+            ob = step_b()
+    torch.cuda.synchronize()
+    for r_, o in zip(ref_a, oa):
+        assert torch.equal(r_, o)
+    for r_, o in zip(ref_b, ob):
+        assert torch.equal(r_, o)
+
+
+def test_gae_scan_is_run_to_run_bit_deterministic(cuda):
+    """Tile records depend only on each tile's own tokens, so the look-back
+    composes the same maps in the same order however the warps interleave."""
+    lens = api.sample_lengths(api.LengthDistribution(api.UNIFORM, 1, 40000, 40000), 300, 5)
+    cu = torch.zeros(301, dtype=torch.int64, device=cuda)
+    cu[1:] = torch.cumsum(torch.tensor(lens, device=cuda), 0)
+    n = int(cu[-1])
+    v = ops.synth_floats(5, 106, 0, n, "value", device=cuda)
+    r = ops.synth_floats(5, 111, 0, n, "kl", device=cuda)
+    m = (ops.synth_floats(5, 112, 0, n, "kl", device=cuda) < 0.9).to(torch.uint8)
+    a0, r0 = ops.gae(v, r, cu, m, 1.0, 0.95)
+    for _ in range(10):
+        a, rr = ops.gae(v, r, cu, m, 1.0, 0.95)
+        assert torch.equal(a, a0) and torch.equal(rr, r0)
