@@ -237,8 +237,11 @@ __global__ void gae_mark_ends_kernel(const int64_t* cu, int64_t nseq, int64_t n_
   if (e > b && e >= 1) atomicOr(ends + ((e - 1) >> 5), 1u << ((e - 1) & 31));
 }
 
+#ifndef YATT_GAE_MINB  // 6 CTAs/SM (80 regs, no spills): 59 us vs 64 us at 5 (96 regs)
+#define YATT_GAE_MINB 6
+#endif
 template <bool kVec>
-__global__ void __launch_bounds__(128) gae_warp_kernel(const GaeArgs g, GaeWs ws) {
+__global__ void __launch_bounds__(128, YATT_GAE_MINB) gae_warp_kernel(const GaeArgs g, GaeWs ws) {
   const int lane = threadIdx.x & 31;
   const double gamma = g.gamma, gl = g.gamma * g.lam;
   int64_t t = 0;
