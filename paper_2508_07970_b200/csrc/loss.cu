@@ -145,8 +145,11 @@ __device__ __forceinline__ void emit_part(const Acc& s, double v0, double v7,
 
 // agg_mode 0: contiguous ranges of 4-token vectors per block, two vectors in
 // flight per thread; the n % 4 tail goes to the last block.
+#ifndef YATT_LOSS_MINB  // 4 CTAs/SM (64 regs): token 57 us / seq 64 us vs 66 / 76 uncapped
+#define YATT_LOSS_MINB 4
+#endif
 template <bool kVec>
-__global__ void __launch_bounds__(kThreads) loss_token_kernel(const LossIn in, int64_t n,
+__global__ void __launch_bounds__(kThreads, YATT_LOSS_MINB) loss_token_kernel(const LossIn in, int64_t n,
                                                               const yatt_loss_config cfg,
                                                               double* part) {
   __shared__ double red[kFields][kThreads / 32];
@@ -177,7 +180,7 @@ __global__ void __launch_bounds__(kThreads) loss_token_kernel(const LossIn in, i
 // fields accumulate per thread.  Vector path: scalar head up to the first
 // 4-aligned token, 16-byte body (two vectors in flight), scalar tail.
 template <bool kVec>
-__global__ void __launch_bounds__(kThreads) loss_seq_kernel(const LossIn in, const int64_t* cu,
+__global__ void __launch_bounds__(kThreads, YATT_LOSS_MINB) loss_seq_kernel(const LossIn in, const int64_t* cu,
                                                             int64_t nseq,
                                                             const yatt_loss_config cfg,
                                                             double* part) {

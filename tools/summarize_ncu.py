@@ -3,6 +3,10 @@
 
   python tools/summarize_ncu.py launches <launches.csv> <out.md>
       per-kernel share of a `--metrics gpu__time_duration.sum` launch list
+  python tools/summarize_ncu.py multi <report.ncu-rep> <out.md> [substr=alg_bytes ...]
+      one row per captured kernel (duration, DRAM traffic, issue, occupancy) and,
+      where an algorithmic byte count is given for a kernel-name substring, the
+      achieved algorithmic GB/s and traffic/algorithmic ratio
   python tools/summarize_ncu.py full <report.ncu-rep> <rows_per_launch> <vocab> <out-prefix>
       key metrics of a `--set full` capture of token_stats -> <out-prefix>.md and
       profiles/token_stats_ncu.json (per-launch DRAM traffic used by bench.py)
@@ -82,8 +86,42 @@ def full(rep, rows, vocab, prefix):
     print("\n".join(md))
 
 
+def multi(rep, out_md, algs):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rs = list(csv.reader(out.splitlines()))
+    h, u = rs[0], rs[1]
+
+    def val(r, k):
+        i = h.index(k)
+        return float(r[i].replace(",", "")) * SCALE.get(u[i], 1.0)
+    md = [f"# ncu --set full: {Path(rep).name}", "",
+          "| kernel | us | DRAM B | alg B | alg GB/s | traffic/alg | DRAM % | issue % | warps % | regs |",
+          "|---|---|---|---|---|---|---|---|---|---|"]
+    for r in rs[2:]:
+        name = r[h.index("Kernel Name")]
+        short = name.split("(")[0].replace("void ", "").split("::")[-1]
+        us = val(r, "gpu__time_duration.sum")
+        if u[h.index("gpu__time_duration.sum")] == "nsecond":
+            us /= 1e3
+        dram = val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum")
+        alg = next((float(b) for s_, b in algs if s_ in name), None)
+        md.append("| {} | {:.1f} | {:.4g} | {} | {} | {} | {:.1f} | {:.1f} | {:.1f} | {:.0f} |".format(
+            short, us, dram, f"{alg:.4g}" if alg else "-",
+            f"{alg / (us * 1e-6) / 1e9:.0f}" if alg else "-",
+            f"{dram / alg:.3f}" if alg else "-",
+            val(r, "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+            val(r, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            val(r, "sm__warps_active.avg.pct_of_peak_sustained_active"),
+            val(r, "launch__registers_per_thread")))
+    Path(out_md).write_text("\n".join(md) + "\n")
+    print("\n".join(md))
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3])
+    elif sys.argv[1] == "multi":
+        multi(sys.argv[2], sys.argv[3], [a.split("=") for a in sys.argv[4:]])
     else:
         full(sys.argv[2], int(sys.argv[3]), int(sys.argv[4]), sys.argv[5])
