@@ -307,7 +307,7 @@ def run_b200(args):
                 "share_of_step": sum(a1_ms) / t_local_ms}
 
     # ---- e2e through the public API: pinned host inputs -> device -> loss ----
-    e2e = run_e2e(args, dev, ops, cfg, ws) if rank == 0 else None
+    e2e = run_e2e(args, dev, ops, cfg, ws, world)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -331,14 +331,17 @@ def run_b200(args):
     return 0
 
 
-def run_e2e(args, dev, ops, cfg, ws):
+def run_e2e(args, dev, ops, cfg, ws, world=1):
     """Same metric through the reference-facing C-ABI call with HOST buffers
     (yatt_grpo_step_host): each step hands pinned host logits (one prompt
     group: 8 responses x 512 tokens = 4,096 rows, 2 x 1.25 GB bf16), targets,
     mask, the group's rewards and old log-probs to one call that streams them
     H2D (chunked, overlapped with A1), runs A1 -> GRPO -> A4 and returns the
-    loss sums to the host.  Wall-clock around the blocking call."""
+    loss sums to the host.  Every rank runs it on its own GPU and host link
+    between barriers; wall-clock around the blocking calls, max over ranks;
+    value = tokens of all ranks / that time."""
     import torch
+    import torch.distributed as dist
     rows = T
     pol, ref, tgt = ops.synth_logits(SEED, 0, rows, VOCAB, device=dev)
     h_pol = pol.cpu().pin_memory()
@@ -360,10 +363,16 @@ def run_e2e(args, dev, ops, cfg, ws):
     for _ in range(max(1, args.warmup)):
         step()
     k = max(2, args.steps)
+    if world > 1:
+        dist.barrier()
     t0 = time.perf_counter()
     for _ in range(k):
         step()
     ms = (time.perf_counter() - t0) * 1e3 / k
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
     h2d = 2 * rows * VOCAB * 2 + rows * (4 + 1 + 4) + RESPONSES * 4
     # the link's own ceiling: plain pinned H2D copies of the same two tensors
     d_pol = torch.empty(h_pol.shape, dtype=h_pol.dtype, device=dev)
@@ -379,12 +388,14 @@ def run_e2e(args, dev, ops, cfg, ws):
         copy_ms.append(a.elapsed_time(b))
     del d_pol, d_ref
     link_gbs = 2 * h_pol.numel() * 2 / (min(copy_ms[1:]) / 1e3) / 1e9
-    return {"value": rows / (ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": 64, "ms_per_step": ms, "h2d_gbs": h2d / (ms / 1e3) / 1e9,
+    return {"value": world * rows / (ms / 1e3), "unit": "tokens/s",
+            "h2d_bytes_per_step": world * h2d, "d2h_bytes_per_step": world * 64,
+            "ms_per_step": ms, "h2d_gbs_per_gpu": h2d / (ms / 1e3) / 1e9,
             "h2d_copy_peak_gbs": link_gbs,
             "frac_of_h2d_copy_peak": h2d / (ms / 1e3) / 1e9 / link_gbs,
+            "ranks": world,
             "api": "yatt_grpo_step_host (C ABI, host buffers)",
-            "sample": f"one prompt group of {RESPONSES} x {rows // RESPONSES} tokens per step "
+            "sample": f"per rank: one prompt group of {RESPONSES} x {rows // RESPONSES} tokens per step "
                       f"({h2d / 1e9:.2f} GB H2D from pinned memory)"}
 
 
