@@ -171,8 +171,12 @@ def run_reference(args):
         last = cpu_experience_rate(budget_s=args.ref_budget_s)
         vals.append(last["value"])
     v = statistics.median(vals)
+    # a full configs[1] step (8.4M tokens) at the sampled rate: each timed
+    # "step" here is a bounded sample of it (cpu_baseline.sample)
+    full_step_ms = PROMPTS * RESPONSES * T / v * 1e3
     line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": full_step_ms,
+            "ms_per_step_note": "extrapolated: one full configs[1] step at the sampled CPU rate",
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (keyed integer-derived bf16 logits, DESIGN.md)",
             "config": workload_config(args.gpus), "impl": "reference",
