@@ -237,11 +237,37 @@ __device__ __forceinline__ RowPartial shfl_partial(const RowPartial& p, int off)
   return o;
 }
 
+// Warp-wide combine: butterfly max of the integer bases, ONE exact
+// power-of-two rescale per thread, then plain butterfly sums (instead of five
+// pairwise combines that each rescale both sides).  Result on all lanes.
+template <bool kFull>
+__device__ __forceinline__ RowPartial warp_combine(RowPartial r) {
+  float Mp = r.mp, Mq = r.mq;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    Mp = fmaxf(Mp, __shfl_xor_sync(0xffffffffu, Mp, off));
+    Mq = fmaxf(Mq, __shfl_xor_sync(0xffffffffu, Mq, off));
+  }
+  const float d = r.mp - Mp;
+  const float c = exp2_int(int(d));
+  float s = c * r.s, w = c * fmaf(d, r.s, r.w), u = kFull ? c * r.u : 0.f;
+  float sq = exp2_int(int(r.mq - Mq)) * r.sq;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, off);
+    w += __shfl_xor_sync(0xffffffffu, w, off);
+    sq += __shfl_xor_sync(0xffffffffu, sq, off);
+    if (kFull) u += __shfl_xor_sync(0xffffffffu, u, off);
+  }
+  return RowPartial{Mp, s, w, Mq, sq, u};
+}
+
 #ifndef YATT_A1_FASTPATH
 #define YATT_A1_FASTPATH 1
 #endif
 constexpr bool kFastPath = YATT_A1_FASTPATH != 0;
 constexpr uint32_t kFixupSentinel = 0x7fc0fadeu;  // quiet NaN payload: "recompute me"
+constexpr uint32_t kNegInf2 = 0xFF80FF80u;        // two bf16 -inf
 
 // Re-base a thread's partial so its sum lies in [1, 2): makes the cross-
 // thread combine safe even when the fast path let a thread's terms grow far
@@ -377,13 +403,17 @@ __global__ void __launch_bounds__(kThreads, 2) token_stats_kernel(const Params p
         tail->tgt[par][0] = __uint_as_float(uint32_t(sp[yin]) << 16);
         tail->tgt[par][1] = __uint_as_float(uint32_t(sq[yin]) << 16);
       }
-      if (nvec == kVecPerTile) {
+      {
+        // Full and partial tiles take the same unrolled path: vectors past the
+        // row end read as -inf (2^-inf = 0 in every sum, also after the floor).
+        const bool full = nvec == kVecPerTile;
         uint4 P[kVecPerThread], Q[kVecPerThread];
 #pragma unroll
         for (int i = 0; i < kVecPerThread; ++i) {
           const int v = tid + i * kConsumers;
-          P[i] = lds128(sp + v * 8);
-          Q[i] = lds128(sq + v * 8);
+          const bool in = full || v < nvec;
+          P[i] = in ? lds128(sp + v * 8) : make_uint4(kNegInf2, kNegInf2, kNegInf2, kNegInf2);
+          Q[i] = in ? lds128(sq + v * 8) : make_uint4(kNegInf2, kNegInf2, kNegInf2, kNegInf2);
         }
 #pragma unroll
         for (int i = 0; i < kVecPerThread; ++i) {
@@ -391,8 +421,8 @@ __global__ void __launch_bounds__(kThreads, 2) token_stats_kernel(const Params p
           if (kFull) Q[i] = floor_policy(Q[i]);  // x - z finite when both are -inf
         }
         // Fast path: the per-thread bases come from the row's first tile only;
-        // later full tiles skip the max check (fewer instructions = less power
-        // on this power-capped kernel).  A row whose later logits exceed a
+        // later tiles skip the max check (fewer instructions = less power on
+        // this power-capped kernel).  A row whose later logits exceed a
         // thread's base by > ~88 nats overflows to inf, is flagged in the
         // epilogue and recomputed by token_stats_fixup_kernel.
         if (!kFastPath || t == 0) {
@@ -408,17 +438,6 @@ __global__ void __launch_bounds__(kThreads, 2) token_stats_kernel(const Params p
         }
 #pragma unroll
         for (int i = 0; i < kVecPerThread; ++i) acc.step(P[i], Q[i]);
-      } else {
-        for (int v = tid; v < nvec; v += kConsumers) {
-          uint4 P = lds128(sp + v * 8);
-          uint4 Q = lds128(sq + v * 8);
-          P = floor_policy(P);
-          if (kFull) Q = floor_policy(Q);
-          const float fmp = pair_max(vmax4(P)), fmq = pair_max(vmax4(Q));
-          if (fmp > acc.thr_p) acc.rebase_p(fmp);
-          if (fmq > acc.thr_q) acc.rebase_q(fmq);
-          acc.step(P, Q);
-        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&tail->empty[stage]);
@@ -437,8 +456,7 @@ __global__ void __launch_bounds__(kThreads, 2) token_stats_kernel(const Params p
     r.sq = Acc<kFull>::total(acc.sq);
     r.u = kFull ? Acc<kFull>::total(acc.u) : 0.f;
     r = normalize(r);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) r = combine(r, shfl_partial(r, off));
+    r = warp_combine<kFull>(r);
     if (lane == 0) tail->red[par][warp] = r;
     named_bar_sync(1, kConsumers);
 
