@@ -237,6 +237,12 @@ def run_b200(args):
     cfg = ops.loss_config(0.2, 0.2, 0.0, 0.001, 0.0, "token-mean")
     ws = ops.LossWorkspace(dev)
     sums = torch.empty((8,), dtype=torch.float64, device=dev)
+    # N > 1: the loss reduction and its all-reduce are ONE kernel over NVLink
+    # peer memory (yatt_policy_loss_allreduce); no NCCL call in the step
+    peer = None
+    if world > 1:
+        from paper_2508_07970_b200 import ranks
+        peer = ranks.PeerGroup(world, rank)
     torch.cuda.synchronize()
 
     st = torch.cuda.current_stream()
@@ -255,10 +261,12 @@ def run_b200(args):
                 a1_events.append((e0, e1))
         adv = ops.grpo_advantages(rewards, RESPONSES, 1e-6, True, g0 * RESPONSES)
         ops.broadcast_to_tokens(adv, cu, n_tok, mask, out=tok_adv)
-        ops.policy_loss(stats[0], old_logp, tok_adv, stats[3], stats[2], mask, None, cfg, ws,
-                        sums)
-        if world > 1:
-            dist.all_reduce(sums)
+        if peer is not None:
+            peer.policy_loss(stats[0], old_logp, tok_adv, stats[3], stats[2], mask, None, cfg, ws,
+                             sums)
+        else:
+            ops.policy_loss(stats[0], old_logp, tok_adv, stats[3], stats[2], mask, None, cfg, ws,
+                            sums)
         return sums
 
     for _ in range(args.warmup):
@@ -331,6 +339,8 @@ def run_b200(args):
         emit(line)
     if world > 1:
         dist.barrier()
+        if peer is not None:
+            peer.close()
         dist.destroy_process_group()
     return 0
 

@@ -476,6 +476,38 @@ int yatt_synth_floats(uint64_t seed, uint64_t stream_id, int64_t i0, int64_t n,
                       int32_t kind, int32_t group_size, const float* d_base,
                       float* d_out, void* stream);
 
+/* ------------------------------------------------------------------------ */
+/* Peer-memory group (one node): compute + all-reduce in ONE kernel over     */
+/* NVLink.  Each rank creates its group member (a small device buffer with   */
+/* a CUDA IPC handle), exchanges the handles out of band (torch.distributed  */
+/* all_gather / the controller rendezvous), then connects.  Calls are        */
+/* collective (every rank, same order); results are bit-identical on every   */
+/* rank (rank-ordered sum).  A peer that never arrives makes the call write  */
+/* NaN after ~10 s and sets yatt_peer_status to 1 instead of hanging.        */
+/* ------------------------------------------------------------------------ */
+#define YATT_PEER_MAX_WORLD 8
+#define YATT_PEER_HANDLE_BYTES 64
+typedef struct yatt_peer* yatt_peer_t;
+int yatt_peer_create(int32_t world, int32_t rank, yatt_peer_t* out_peer,
+                     uint8_t* h_handle /* YATT_PEER_HANDLE_BYTES */);
+int yatt_peer_connect(yatt_peer_t peer,
+                      const uint8_t* h_handles /* world * YATT_PEER_HANDLE_BYTES */);
+int yatt_peer_destroy(yatt_peer_t peer);
+int yatt_peer_status(yatt_peer_t peer, int32_t* h_status);
+/* d_out[i] = sum over ranks of d_in[i], i < n <= 16. */
+int yatt_peer_allreduce_f64(yatt_peer_t peer, const double* d_in, int32_t n,
+                            double* d_out, void* stream);
+/* yatt_policy_loss whose final reduction also all-reduces across the group:  */
+/* d_sums holds the GLOBAL sums on every rank (one kernel after the partials). */
+int yatt_policy_loss_allreduce(yatt_peer_t peer, const float* d_logp,
+                               const float* d_old_logp, const float* d_advantages,
+                               const float* d_kl, const float* d_entropy,
+                               const uint8_t* d_mask, int64_t n_tokens,
+                               const int64_t* d_cu_seqlens, int64_t n_seqs,
+                               const yatt_loss_config* config,
+                               yatt_loss_sums* d_sums, void* d_workspace,
+                               size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }  /* extern "C" */
 #endif

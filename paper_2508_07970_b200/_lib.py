@@ -133,6 +133,13 @@ SIGNATURES = {
     "yatt_sort_order_workspace_bytes": (c_sz, [c_i64]),
     "yatt_sort_order_desc": (C.c_int, [c_p, c_i64, c_p, c_p, c_sz, c_p]),
     "yatt_sort_and_bucket_host": (C.c_int, [c_p, c_i64, c_i32, c_u64, c_p, c_p]),
+    "yatt_peer_create": (C.c_int, [c_i32, c_i32, P(c_p), c_p]),
+    "yatt_peer_connect": (C.c_int, [c_p, c_p]),
+    "yatt_peer_destroy": (C.c_int, [c_p]),
+    "yatt_peer_status": (C.c_int, [c_p, P(c_i32)]),
+    "yatt_peer_allreduce_f64": (C.c_int, [c_p, c_p, c_i32, c_p, c_p]),
+    "yatt_policy_loss_allreduce": (C.c_int, [c_p] * 7 + [c_i64, c_p, c_i64, P(LossConfigC), c_p, c_p,
+                                                         c_sz, c_p]),
     "yatt_comm_unique_id": (C.c_int, [c_p]),
     "yatt_comm_init": (C.c_int, [c_i32, c_i32, c_p, P(c_p)]),
     "yatt_comm_destroy": (C.c_int, [c_p]),

@@ -250,10 +250,10 @@ int seq_parts(int64_t nseq) { return int(max64(1, min64(nseq, int64_t(8) * num_s
 
 size_t loss_workspace_bytes() { return size_t(kMaxParts) * kFields * sizeof(double); }
 
-int policy_loss_launch(const float* logp, const float* old_logp, const float* adv,
-                       const float* kl, const float* ent, const uint8_t* mask, int64_t n,
-                       const int64_t* cu, int64_t nseq, const yatt_loss_config* cfg,
-                       yatt_loss_sums* sums, void* ws, size_t ws_bytes, cudaStream_t st) {
+int policy_loss_parts_launch(const float* logp, const float* old_logp, const float* adv,
+                             const float* kl, const float* ent, const uint8_t* mask, int64_t n,
+                             const int64_t* cu, int64_t nseq, const yatt_loss_config* cfg,
+                             void* ws, size_t ws_bytes, int* nparts, cudaStream_t st) {
   YATT_REQUIRE(cfg != nullptr, YATT_ERR_CONFIG, "policy_loss: null config");
   YATT_REQUIRE(cfg->agg_mode >= 0 && cfg->agg_mode <= 2, YATT_ERR_CONFIG,
                "policy_loss: unknown agg_mode %d", cfg->agg_mode);
@@ -281,10 +281,21 @@ int policy_loss_launch(const float* logp, const float* old_logp, const float* ad
     else
       loss_seq_kernel<false><<<parts, kThreads, 0, st>>>(in, cu, nseq, *cfg, part);
   }
-  int rc = check_launch("policy_loss_kernel");
+  *nparts = parts;
+  return check_launch("policy_loss_kernel");
+}
+
+int policy_loss_launch(const float* logp, const float* old_logp, const float* adv,
+                       const float* kl, const float* ent, const uint8_t* mask, int64_t n,
+                       const int64_t* cu, int64_t nseq, const yatt_loss_config* cfg,
+                       yatt_loss_sums* sums, void* ws, size_t ws_bytes, cudaStream_t st) {
+  int parts = 0;
+  const int rc = policy_loss_parts_launch(logp, old_logp, adv, kl, ent, mask, n, cu, nseq, cfg, ws,
+                                          ws_bytes, &parts, st);
   if (rc) return rc;
   static_assert(sizeof(yatt_loss_sums) == kFields * sizeof(double), "yatt_loss_sums layout");
-  reduce_parts_kernel<kFields><<<1, 256, 0, st>>>(part, parts, reinterpret_cast<double*>(sums));
+  reduce_parts_kernel<kFields><<<1, 256, 0, st>>>(static_cast<const double*>(ws), parts,
+                                                   reinterpret_cast<double*>(sums));
   return check_launch("reduce_parts_kernel<8>");
 }
 

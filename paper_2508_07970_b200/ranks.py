@@ -20,6 +20,7 @@ from __future__ import annotations
 import ctypes as C
 
 import torch
+import torch.distributed as dist
 
 from ._lib import check, lib
 
@@ -105,6 +106,68 @@ class YattComm:
     def close(self):
         if self.h:
             check(lib().yatt_comm_destroy(self.h))
+            self.h = C.c_void_p()
+
+
+class PeerGroup:
+    """The node's ranks joined through NVLink peer memory (yatt_peer_*): one
+    kernel does a reduction AND its cross-rank all-reduce (no NCCL call).
+    Handles (64-byte CUDA IPC handles) are exchanged with torch.distributed's
+    all_gather_object (gloo or nccl group).  Collective: every rank calls the
+    same ops in the same order; results are bit-identical on all ranks."""
+
+    HANDLE = 64
+
+    def __init__(self, world: int | None = None, rank: int | None = None):
+        world = dist.get_world_size() if world is None else world
+        rank = dist.get_rank() if rank is None else rank
+        self.world, self.rank = world, rank
+        self.h = C.c_void_p()
+        mine = (C.c_uint8 * self.HANDLE)()
+        check(lib().yatt_peer_create(world, rank, C.byref(self.h), C.addressof(mine)))
+        handles = [None] * world
+        if world > 1:
+            dist.all_gather_object(handles, bytes(mine))
+        else:
+            handles = [bytes(mine)]
+        allh = (C.c_uint8 * (self.HANDLE * world)).from_buffer_copy(b"".join(handles))
+        check(lib().yatt_peer_connect(self.h, C.addressof(allh)))
+
+    def _st(self):
+        return torch.cuda.current_stream().cuda_stream
+
+    def allreduce_f64(self, t: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        out = torch.empty_like(t) if out is None else out
+        check(lib().yatt_peer_allreduce_f64(self.h, t.data_ptr(), t.numel(), out.data_ptr(),
+                                            self._st()))
+        return out
+
+    def policy_loss(self, logp, old_logp, advantages, kl, entropy, mask=None, cu_seqlens=None,
+                    config=None, workspace=None, sums=None):
+        """ops.policy_loss whose final reduction is also the all-reduce: the
+        GLOBAL yatt_loss_sums on every rank."""
+        from . import ops
+        cfg = config or ops.loss_config()
+        ws = workspace or ops.LossWorkspace(logp.device)
+        if sums is None:
+            sums = torch.empty((8,), dtype=torch.float64, device=logp.device)
+        nseq = 0 if cu_seqlens is None else cu_seqlens.numel() - 1
+        p = lambda t: None if t is None else t.data_ptr()  # noqa: E731
+        m = None if mask is None else mask.view(torch.uint8)
+        check(lib().yatt_policy_loss_allreduce(self.h, p(logp), p(old_logp), p(advantages), p(kl),
+                                               p(entropy), p(m), logp.numel(), p(cu_seqlens),
+                                               nseq, C.byref(cfg), sums.data_ptr(), ws.buf.data_ptr(),
+                                               ws.buf.numel(), self._st()))
+        return sums
+
+    def status(self) -> int:
+        s = C.c_int32()
+        check(lib().yatt_peer_status(self.h, C.byref(s)))
+        return s.value
+
+    def close(self):
+        if self.h:
+            check(lib().yatt_peer_destroy(self.h))
             self.h = C.c_void_p()
 
 

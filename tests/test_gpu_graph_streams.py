@@ -114,3 +114,40 @@ def test_gae_scan_is_run_to_run_bit_deterministic(cuda):
     for _ in range(10):
         a, rr = ops.gae(v, r, cu, m, 1.0, 0.95)
         assert torch.equal(a, a0) and torch.equal(rr, r0)
+
+
+def test_peer_group_single_rank_matches_plain_ops(cuda):
+    """yatt_peer_* with world = 1 (the multi-rank runs are tools/mgpu_check.py
+    under torchrun): the fused reduce + all-reduce kernel equals
+    yatt_policy_loss bit for bit, also when replayed from a CUDA graph."""
+    from paper_2508_07970_b200 import ranks
+    x = _inputs(cuda)
+    step = Step(x, cuda)
+    step()
+    peer = ranks.PeerGroup(1, 0)
+    try:
+        args = (step.stats[0], x["old"], step.tadv, step.stats[3], step.stats[2])
+        plain = ops.policy_loss(*args)
+        fused = peer.policy_loss(*args)
+        v = torch.arange(1, 12, dtype=torch.float64, device=cuda)
+        torch.cuda.synchronize()
+        assert torch.equal(plain, fused)
+        assert torch.equal(peer.allreduce_f64(v), v)
+        ws = ops.LossWorkspace(cuda)
+        out = torch.empty(8, dtype=torch.float64, device=cuda)
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            peer.policy_loss(*args, workspace=ws, sums=out)
+        torch.cuda.current_stream().wait_stream(s)
+        with torch.cuda.graph(g):
+            peer.policy_loss(*args, workspace=ws, sums=out)
+        for _ in range(3):
+            out.zero_()
+            g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, plain)
+        assert peer.status() == 0
+    finally:
+        peer.close()
