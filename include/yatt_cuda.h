@@ -497,6 +497,12 @@ int yatt_peer_status(yatt_peer_t peer, int32_t* h_status);
 /* d_out[i] = sum over ranks of d_in[i], i < n <= 16. */
 int yatt_peer_allreduce_f64(yatt_peer_t peer, const double* d_in, int32_t n,
                             double* d_out, void* stream);
+/* All-gather + exclusive scan over ranks of n <= 16 int64 counters in one    */
+/* kernel: d_prefix[i] = sum over lower ranks, d_total[i] = sum over all      */
+/* (either may be NULL) — e.g. the dynamic-sampling counts -> this rank's     */
+/* offset into the global packed layout (yatt_gather_* d_dst_offset).         */
+int yatt_peer_scan_i64(yatt_peer_t peer, const int64_t* d_in, int32_t n,
+                       int64_t* d_prefix, int64_t* d_total, void* stream);
 /* yatt_policy_loss whose final reduction also all-reduces across the group:  */
 /* d_sums holds the GLOBAL sums on every rank (one kernel after the partials). */
 int yatt_policy_loss_allreduce(yatt_peer_t peer, const float* d_logp,

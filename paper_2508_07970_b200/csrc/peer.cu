@@ -96,8 +96,8 @@ __global__ void __launch_bounds__(256) peer_reduce_allreduce_kernel(const double
     for (int q = 0; q < a.world && !s_fail; ++q) {
       long long spins = 0;
       while (*flag(mine, q) < epoch) {
-        __nanosleep(128);
-        if (++spins > (1ll << 26)) {  // ~10 s: a rank is gone; fail loudly, do not hang
+        if (spins > 64) __nanosleep(32);  // tight polling first: the usual wait is ~1 us
+        if (++spins > (1ll << 27)) {  // ~10 s: a rank is gone; fail loudly, do not hang
           s_fail = 1;
           *reinterpret_cast<volatile uint32_t*>(mine + kStatusOff) = 1u;
           break;
@@ -114,6 +114,61 @@ __global__ void __launch_bounds__(256) peer_reduce_allreduce_kernel(const double
     for (int q = 0; q < a.world; ++q)
       s += reinterpret_cast<volatile double*>(slot(mine, parity, q))[threadIdx.x];
     out[threadIdx.x] = s_fail ? __longlong_as_double(0x7ff8000000000000ll) : s;
+  }
+}
+
+// All-gather + exclusive scan of up to 16 int64 counters per rank in one
+// kernel (the dynamic-sampling global offsets): prefix[f] = sum_{q < rank}
+// c_q[f], total[f] = sum_q c_q[f] — exact integers, identical on all ranks.
+// Shares the slot banks / epoch protocol above (int64 stored as raw words).
+__global__ void peer_scan_i64_kernel(const int64_t* in, int nf, PeerArgs a, int64_t* prefix,
+                                     int64_t* total) {
+  __shared__ uint64_t s_epoch;
+  __shared__ int s_fail;
+  uint8_t* mine = a.buf[a.rank];
+  if (threadIdx.x == 0) {
+    volatile uint64_t* ep = reinterpret_cast<volatile uint64_t*>(mine + kEpochOff);
+    s_epoch = *ep + 1;
+    *ep = s_epoch;
+    s_fail = 0;
+  }
+  __syncthreads();
+  const uint64_t epoch = s_epoch;
+  const int parity = int(epoch & 1u);
+  if (threadIdx.x < nf) {
+    const long long v = in[threadIdx.x];
+    for (int q = 0; q < a.world; ++q)
+      reinterpret_cast<volatile long long*>(slot(a.buf[q], parity, a.rank))[threadIdx.x] = v;
+    __threadfence_system();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int q = 0; q < a.world; ++q) *flag(a.buf[q], a.rank) = epoch;
+    for (int q = 0; q < a.world && !s_fail; ++q) {
+      long long spins = 0;
+      while (*flag(mine, q) < epoch) {
+        if (spins > 64) __nanosleep(32);
+        if (++spins > (1ll << 27)) {
+          s_fail = 1;
+          *reinterpret_cast<volatile uint32_t*>(mine + kStatusOff) = 1u;
+          break;
+        }
+      }
+    }
+    __threadfence_system();
+  }
+  __syncthreads();
+  if (threadIdx.x < nf) {
+    __threadfence_system();
+    long long pre = 0, tot = 0;
+    for (int q = 0; q < a.world; ++q) {
+      const long long c = reinterpret_cast<volatile long long*>(slot(mine, parity, q))[threadIdx.x];
+      if (q < a.rank) pre += c;
+      tot += c;
+    }
+    if (prefix) prefix[threadIdx.x] = s_fail ? -1 : pre;
+    if (total) total[threadIdx.x] = s_fail ? -1 : tot;
   }
 }
 
@@ -222,6 +277,18 @@ int yatt_peer_allreduce_f64(yatt_peer_t p, const double* d_in, int32_t n, double
   const int rc = peer_args(p, &a);
   if (rc) return rc;
   return peer_reduce_launch(a, d_in, 1, n, d_out, as_stream(stream));
+}
+
+int yatt_peer_scan_i64(yatt_peer_t p, const int64_t* d_in, int32_t n, int64_t* d_prefix,
+                       int64_t* d_total, void* stream) {
+  YATT_REQUIRE(n >= 1 && n <= kPeerMaxFields, YATT_ERR_CONFIG,
+               "peer_scan_i64: n must be in [1, %d]", kPeerMaxFields);
+  YATT_REQUIRE(d_in != nullptr, YATT_ERR_CONFIG, "peer_scan_i64: null input");
+  PeerArgs a;
+  const int rc = peer_args(p, &a);
+  if (rc) return rc;
+  peer_scan_i64_kernel<<<1, 32, 0, as_stream(stream)>>>(d_in, n, a, d_prefix, d_total);
+  return check_launch("peer_scan_i64_kernel");
 }
 
 int yatt_policy_loss_allreduce(yatt_peer_t p, const float* logp, const float* old_logp,

@@ -142,6 +142,14 @@ class PeerGroup:
                                             self._st()))
         return out
 
+    def scan_i64(self, t: torch.Tensor):
+        """(exclusive prefix over lower ranks, total over all ranks) of the
+        int64 counters t (<= 16) in one kernel."""
+        pre, tot = torch.empty_like(t), torch.empty_like(t)
+        check(lib().yatt_peer_scan_i64(self.h, t.data_ptr(), t.numel(), pre.data_ptr(),
+                                       tot.data_ptr(), self._st()))
+        return pre, tot
+
     def policy_loss(self, logp, old_logp, advantages, kl, entropy, mask=None, cu_seqlens=None,
                     config=None, workspace=None, sums=None):
         """ops.policy_loss whose final reduction is also the all-reduce: the

@@ -161,6 +161,10 @@ def main():
         graph.replay()
         torch.cuda.synchronize()
         assert torch.equal(gs, fused), (rank, gs.tolist(), fused.tolist())
+    # dynamic-sampling offsets in one kernel: == NCCL all-gather + exclusive_offset
+    pre, tot = peer.scan_i64(loc["counts"])
+    assert int(pre[1]) == int(ops.exclusive_offset(counts, world, rank, 3, 1)[0])
+    assert tot.tolist() == counts.view(world, 3).sum(0).tolist()
     assert peer.status() == 0
     # latency of the 8-double all-reduce: fused peer kernel vs NCCL (device time)
     x8 = torch.ones(8, dtype=torch.float64, device=dev)
