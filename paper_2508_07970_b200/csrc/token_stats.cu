@@ -41,8 +41,14 @@ namespace {
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kThreads = kConsumers + 32;  // + producer warp
-constexpr int kTile = 8192;                // bf16 elements per tensor per stage
-constexpr int kStages = 3;
+#ifndef YATT_A1_TILE
+#define YATT_A1_TILE 8192
+#endif
+#ifndef YATT_A1_STAGES
+#define YATT_A1_STAGES 3
+#endif
+constexpr int kTile = YATT_A1_TILE;        // bf16 elements per tensor per stage
+constexpr int kStages = YATT_A1_STAGES;
 constexpr int kVecPerTile = kTile / 8;                  // 16-byte vectors
 constexpr int kVecPerThread = kVecPerTile / kConsumers;  // full-tile unroll
 constexpr float kLog2e = 1.4426950408889634f;

@@ -102,3 +102,23 @@ def test_misaligned_pointers_are_config_errors_before_any_launch():
     for what, fn in calls:
         with pytest.raises(ConfigError, match="aligned"):
             check(fn())
+
+
+def test_peer_group_argument_errors_before_any_cuda_call():
+    """yatt_peer_* validate world / rank / pointers before touching CUDA."""
+    from paper_2508_07970_b200._lib import check
+    h = C.c_void_p()
+    buf = (C.c_uint8 * 64)()
+    with pytest.raises(ConfigError):
+        check(lib().yatt_peer_create(0, 0, C.byref(h), C.addressof(buf)))
+    with pytest.raises(ConfigError):
+        check(lib().yatt_peer_create(9, 0, C.byref(h), C.addressof(buf)))
+    with pytest.raises(RankOutOfRange):
+        check(lib().yatt_peer_create(2, 2, C.byref(h), C.addressof(buf)))
+    with pytest.raises(ConfigError):
+        check(lib().yatt_peer_connect(None, C.addressof(buf)))
+    with pytest.raises(ConfigError, match="create"):
+        check(lib().yatt_peer_allreduce_f64(None, 0x10000, 4, 0x10000, None))
+    with pytest.raises(ConfigError):
+        check(lib().yatt_peer_scan_i64(None, 0x10000, 17, None, None, None))
+    assert lib().yatt_peer_destroy(None) == 0
