@@ -357,16 +357,16 @@ def run_e2e(args, dev, ops, cfg, ws, world=1):
     import torch
     import torch.distributed as dist
     rows = T
+    def pinned(t):  # device -> pinned host without a pageable staging copy
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t)
+        return h
     pol, ref, tgt = ops.synth_logits(SEED, 0, rows, VOCAB, device=dev)
-    h_pol = pol.cpu().pin_memory()
-    h_ref = ref.cpu().pin_memory()
-    h_tgt = tgt.cpu().pin_memory()
+    h_pol, h_ref, h_tgt = pinned(pol), pinned(ref), pinned(tgt)
     h_mask = torch.ones((rows,), dtype=torch.uint8).pin_memory()
-    h_rew = ops.synth_floats(SEED, 105, 0, RESPONSES, "reward", RESPONSES,
-                             device=dev).cpu().pin_memory()
+    h_rew = pinned(ops.synth_floats(SEED, 105, 0, RESPONSES, "reward", RESPONSES, device=dev))
     logp = ops.token_stats(pol, ref, tgt, None, "k3")[0]
-    h_old = ops.synth_floats(SEED, 104, 0, rows, "old_delta", base=logp,
-                             device=dev).cpu().pin_memory()
+    h_old = pinned(ops.synth_floats(SEED, 104, 0, rows, "old_delta", base=logp, device=dev))
     del pol, ref, tgt, logp
     torch.cuda.synchronize()
 
