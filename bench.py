@@ -187,8 +187,11 @@ def run_reference(args):
     return 0
 
 
-def workload_config(n):
-    return {"workload": "configs[1]/[2]: GRPO Qwen2.5-7B shape, 256 prompts x 8 responses, "
+def workload_config(n, collective="peer"):
+    coll = ("none" if n == 1 else
+            "loss reduce + all-reduce fused in one kernel over NVLink peer memory"
+            if collective == "peer" else "NCCL all-reduce of the loss sums / token count")
+    return {"collective": coll, "workload": "configs[1]/[2]: GRPO Qwen2.5-7B shape, 256 prompts x 8 responses, "
                         "T=4096, V=152064, sharded by prompt group",
             "global_batch": PROMPTS * RESPONSES, "seq_len": T, "vocab": VOCAB,
             "tokens_per_step": PROMPTS * RESPONSES * T, "parallelism": f"dp{n} by prompt group",
@@ -240,7 +243,7 @@ def run_b200(args):
     # N > 1: the loss reduction and its all-reduce are ONE kernel over NVLink
     # peer memory (yatt_policy_loss_allreduce); no NCCL call in the step
     peer = None
-    if world > 1:
+    if world > 1 and args.collective == "peer":
         from paper_2508_07970_b200 import ranks
         peer = ranks.PeerGroup(world, rank)
     torch.cuda.synchronize()
@@ -267,6 +270,8 @@ def run_b200(args):
         else:
             ops.policy_loss(stats[0], old_logp, tok_adv, stats[3], stats[2], mask, None, cfg, ws,
                             sums)
+            if world > 1:
+                dist.all_reduce(sums)
         return sums
 
     for _ in range(args.warmup):
@@ -330,7 +335,7 @@ def run_b200(args):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "bf16", "data": "synthetic (keyed integer-derived bf16 logits, "
-                "binary group rewards; DESIGN.md)", "config": workload_config(world),
+                "binary group rewards; DESIGN.md)", "config": workload_config(world, args.collective),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 # per group: token_stats + its fix-up pass; per step: grpo_adv,
                 # broadcast, loss partials + final
@@ -437,6 +442,9 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=12.0)
+    ap.add_argument("--collective", choices=["peer", "nccl"], default="peer",
+                    help="N>1 loss/token-count all-reduce: fused into the loss's final "
+                         "reduction over NVLink peer memory (default) or NCCL all-reduce")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
