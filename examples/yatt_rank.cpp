@@ -8,11 +8,14 @@
 //   3. repack accepted lengths into balanced buckets (balancer::sort_and_bucket)
 //   4. experience making on the device: logprob/entropy/KL, GRPO advantages,
 //      clipped-surrogate + KL loss (experience.hpp), loss finalised on host
+//   5. the backward into the logits, the node peer group (world = 1 here) and
+//      the survivors' payload gather
 // Prints a short report and "rank ok"; exits non-zero on any mismatch.
 #include <cuda_runtime.h>
 
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 #include <vector>
 
@@ -135,6 +138,70 @@ int main() {
               (long long)h.token_count, loss, h.kl_sum / h.token_count,
               h.entropy_sum / h.token_count, h.clip_count / h.token_count);
   if (!(h.token_count == double(rows)) || !std::isfinite(loss)) return 1;
+
+  // 5a. backward into the policy logits (first 1,024 rows), rows sum to ~0
+  {
+    const std::int64_t gr = 1024;
+    auto* coef = dalloc<float>(size_t(gr) * 8);
+    auto* grad = dalloc<std::uint16_t>(size_t(gr) * vocab);
+    experience::policy_logits_grad(pol, ref, tgt, {logp, ref_logp, ent, kl}, old, tadv, nullptr, gr,
+                                   vocab, nullptr, 0, cfg, experience::KlEstimator::kK3,
+                                   double(rows), coef, grad);
+    std::vector<std::uint16_t> hg(static_cast<size_t>(vocab));
+    ck(cudaMemcpy(hg.data(), grad, hg.size() * 2, cudaMemcpyDeviceToHost), "D2H grad");
+    double sum = 0, amax = 0;
+    for (auto b : hg) {
+      std::uint32_t u = std::uint32_t(b) << 16;
+      float f;
+      std::memcpy(&f, &u, 4);
+      sum += f;
+      amax = std::fmax(amax, std::fabs(f));
+    }
+    std::printf("backward: row 0 grad sum %.3e (max |g| %.3e)\n", sum, amax);
+    if (!std::isfinite(sum) || std::fabs(sum) > 1e-2 * amax * 50) return 1;
+    cudaFree(coef);
+    cudaFree(grad);
+  }
+
+  // 5b. peer group (world = 1): the fused reduce + all-reduce == the plain loss
+  {
+    experience::PeerGroup peer(1, 0);
+    peer.connect(peer.handle());
+    auto* gsums = dalloc<experience::LossSums>(1);
+    peer.policy_loss(logp, old, tadv, kl, ent, nullptr, rows, nullptr, 0, cfg, gsums, ws,
+                     ws_bytes);
+    experience::LossSums g;
+    ck(cudaMemcpy(&g, gsums, sizeof(g), cudaMemcpyDeviceToHost), "D2H peer sums");
+    if (std::memcmp(&g, &h, sizeof(g)) != 0 || peer.status() != 0) {
+      std::fprintf(stderr, "peer group sums differ from policy_loss\n");
+      return 1;
+    }
+    std::printf("peer group: fused loss all-reduce == policy_loss (bit-exact)\n");
+    cudaFree(gsums);
+  }
+
+  // 5c. dynamic sampling on the rewards + the survivors' payload in one launch
+  {
+    const int n = prompts * group;
+    auto* lens = dalloc<std::int64_t>(size_t(n));
+    std::vector<std::int64_t> hl(static_cast<size_t>(n), T);
+    ck(cudaMemcpy(lens, hl.data(), hl.size() * 8, cudaMemcpyHostToDevice), "H2D lens");
+    experience::CompactionBuffers plan{dalloc<std::uint8_t>(size_t(n) / group),
+                                       dalloc<std::int32_t>(size_t(n)),
+                                       dalloc<std::int64_t>(size_t(n) + 1),
+                                       dalloc<std::int64_t>(3)};
+    const size_t cws_bytes = experience::dynamic_sampling_workspace_bytes(n);
+    void* cws = dalloc<std::uint8_t>(cws_bytes);
+    experience::dynamic_sampling_filter(rewards, lens, n, group, plan, cws, cws_bytes);
+    auto* out_logp = dalloc<float>(size_t(rows));
+    auto* out_tgt = dalloc<std::int32_t>(size_t(rows));
+    experience::gather_payload({{logp, out_logp, 4}, {tgt, out_tgt, 4}}, cu, plan, n);
+    std::int64_t counts[3];
+    ck(cudaMemcpy(counts, plan.counts, sizeof(counts), cudaMemcpyDeviceToHost), "D2H counts");
+    std::printf("dynamic sampling: %lld of %d samples kept, %lld tokens gathered\n",
+                (long long)counts[0], n, (long long)counts[1]);
+    if (counts[1] != counts[0] * T) return 1;
+  }
 
   // errors keep the reference's types
   try {

@@ -10,6 +10,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <vector>
 
 namespace yatt::experience {
 
@@ -98,5 +99,67 @@ void dynamic_sampling_filter(const float* rewards, const std::int64_t* seq_lens,
                              std::int64_t n_samples, int group_size, const CompactionBuffers& out,
                              void* workspace, std::size_t workspace_bytes,
                              void* stream = nullptr);
+
+// ---- backward into the policy logits -------------------
+// dL/d(policy logits) of the A4 loss as bf16 [rows, vocab].  `stats` are A1's
+// outputs (logp, ref_logp, entropy, kl); `norm` = the GLOBAL token count for
+// token-mean, the global sequence count for the seq modes (all-reduce first).
+// coef: device scratch of 8 floats per row.  ref_logits are read for kFull
+// only.  Any vocab; TMA streaming when 16-byte aligned with vocab % 8 == 0.
+void policy_logits_grad(const std::uint16_t* policy_logits, const std::uint16_t* ref_logits,
+                        const std::int32_t* targets, const TokenStats& stats,
+                        const float* old_logp, const float* advantages, const std::uint8_t* mask,
+                        std::int64_t rows, int vocab, const std::int64_t* cu_seqlens,
+                        std::int64_t n_seqs, const PolicyLossConfig& config, KlEstimator kl,
+                        double norm, float* coef, std::uint16_t* grad, void* stream = nullptr);
+
+// ---- fused LM head + online log-softmax (tcgen05; §8f #4) -------------------
+// logp / entropy / lse per row of softmax(hidden @ lm_head^T) without writing
+// the logits; hidden [rows, hidden_dim], lm_head [vocab, hidden_dim] bf16.
+std::size_t lmhead_workspace_bytes(std::int64_t rows, int vocab, int n_split);
+void lmhead_token_stats(const std::uint16_t* hidden, const std::uint16_t* lm_head,
+                        const std::int32_t* targets, std::int64_t rows, int hidden_dim, int vocab,
+                        int n_split, float* logp, float* entropy, float* lse, void* workspace,
+                        std::size_t workspace_bytes, void* stream = nullptr);
+
+// ---- survivors' per-token payload (A6), all arrays in one launch ----------
+struct PayloadArray {
+  const void* src = nullptr;  // [old_cu[n_samples]] elements
+  void* dst = nullptr;        // [kept tokens (+ dst_offset)] elements
+  int elem_bytes = 4;         // 1, 2, 4 or 8
+};
+void gather_payload(const std::vector<PayloadArray>& arrays, const std::int64_t* old_cu,
+                    const CompactionBuffers& plan, std::int64_t max_kept,
+                    const std::int64_t* dst_offset = nullptr, void* stream = nullptr);
+
+// ---- the node's ranks joined through NVLink peer memory ---------------------
+// Construct on every rank, exchange handle() (64 bytes each, rank order) over
+// the controller rendezvous, connect().  Collective calls; results are
+// bit-identical on all ranks.  No NCCL involved.
+class PeerGroup {
+ public:
+  PeerGroup(int world, int rank);
+  ~PeerGroup();
+  PeerGroup(const PeerGroup&) = delete;
+  PeerGroup& operator=(const PeerGroup&) = delete;
+  const std::vector<std::uint8_t>& handle() const { return handle_; }
+  void connect(const std::vector<std::uint8_t>& all_handles);
+  // out[i] = sum over ranks of in[i], n <= 16 doubles
+  void allreduce(const double* in, int n, double* out, void* stream = nullptr);
+  // prefix[i] = sum over lower ranks, total[i] = over all ranks (n <= 16)
+  void scan(const std::int64_t* in, int n, std::int64_t* prefix, std::int64_t* total,
+            void* stream = nullptr);
+  // policy_loss whose final reduction is the cross-rank all-reduce: GLOBAL sums
+  void policy_loss(const float* logp, const float* old_logp, const float* advantages,
+                   const float* kl, const float* entropy, const std::uint8_t* mask,
+                   std::int64_t n_tokens, const std::int64_t* cu_seqlens, std::int64_t n_seqs,
+                   const PolicyLossConfig& config, LossSums* device_sums, void* workspace,
+                   std::size_t workspace_bytes, void* stream = nullptr);
+  int status() const;  // 1 after a call timed out waiting for a rank
+
+ private:
+  void* h_ = nullptr;
+  std::vector<std::uint8_t> handle_;
+};
 
 }  // namespace yatt::experience

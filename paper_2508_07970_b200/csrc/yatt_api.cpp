@@ -549,6 +549,94 @@ double finalize_loss(const LossSums& s, const PolicyLossConfig& c) {
   return yatt_loss_finalize(reinterpret_cast<const yatt_loss_sums*>(&s), &cc);
 }
 
+void policy_logits_grad(const std::uint16_t* pol, const std::uint16_t* ref,
+                        const std::int32_t* tgt, const TokenStats& st, const float* old_logp,
+                        const float* adv, const std::uint8_t* mask, std::int64_t rows, int vocab,
+                        const std::int64_t* cu, std::int64_t nseq, const PolicyLossConfig& c,
+                        KlEstimator kl, double norm, float* coef, std::uint16_t* grad,
+                        void* stream) {
+  c.validate();
+  const yatt_loss_config cc = to_c(c);
+  const int mode = static_cast<int>(kl);
+  detail::throw_status(yatt_policy_grad_coef(pol, ref, tgt, st.logp, st.ref_logp, old_logp, adv,
+                                             st.entropy, st.kl, mask, rows, vocab, cu, nseq, &cc,
+                                             mode, norm, coef, stream));
+  detail::throw_status(yatt_logits_backward(pol, kl == KlEstimator::kFull ? ref : nullptr, tgt,
+                                            mask, rows, vocab, coef,
+                                            kl == KlEstimator::kFull ? 1 : 0, grad, stream));
+}
+
+std::size_t lmhead_workspace_bytes(std::int64_t rows, int vocab, int n_split) {
+  return yatt_lmhead_workspace_bytes(rows, vocab, n_split);
+}
+
+void lmhead_token_stats(const std::uint16_t* hidden, const std::uint16_t* w,
+                        const std::int32_t* tgt, std::int64_t rows, int d, int vocab, int n_split,
+                        float* logp, float* ent, float* lse, void* ws, std::size_t ws_bytes,
+                        void* stream) {
+  detail::throw_status(yatt_lmhead_token_stats(hidden, w, tgt, rows, d, vocab, n_split, logp, ent,
+                                               lse, ws, ws_bytes, stream));
+}
+
+void gather_payload(const std::vector<PayloadArray>& arrays, const std::int64_t* old_cu,
+                    const CompactionBuffers& plan, std::int64_t max_kept,
+                    const std::int64_t* dst_offset, void* stream) {
+  if (arrays.empty()) return;
+  std::vector<const void*> src;
+  std::vector<void*> dst;
+  std::vector<std::int32_t> esz;
+  for (const auto& a : arrays) {
+    src.push_back(a.src);
+    dst.push_back(a.dst);
+    esz.push_back(a.elem_bytes);
+  }
+  // counts[0] = kept samples (device), the gather's loop bound
+  detail::throw_status(yatt_gather_varlen_multi(static_cast<std::int32_t>(arrays.size()),
+                                                src.data(), dst.data(), esz.data(), old_cu,
+                                                plan.index_map, plan.new_cu, plan.counts, max_kept,
+                                                dst_offset, stream));
+}
+
+PeerGroup::PeerGroup(int world, int rank) : handle_(YATT_PEER_HANDLE_BYTES) {
+  yatt_peer_t p = nullptr;
+  detail::throw_status(yatt_peer_create(world, rank, &p, handle_.data()));
+  h_ = p;
+}
+
+PeerGroup::~PeerGroup() { yatt_peer_destroy(static_cast<yatt_peer_t>(h_)); }
+
+void PeerGroup::connect(const std::vector<std::uint8_t>& all) {
+  detail::throw_status(yatt_peer_connect(static_cast<yatt_peer_t>(h_), all.data()));
+}
+
+void PeerGroup::allreduce(const double* in, int n, double* out, void* stream) {
+  detail::throw_status(yatt_peer_allreduce_f64(static_cast<yatt_peer_t>(h_), in, n, out, stream));
+}
+
+void PeerGroup::scan(const std::int64_t* in, int n, std::int64_t* prefix, std::int64_t* total,
+                     void* stream) {
+  detail::throw_status(
+      yatt_peer_scan_i64(static_cast<yatt_peer_t>(h_), in, n, prefix, total, stream));
+}
+
+void PeerGroup::policy_loss(const float* logp, const float* old_logp, const float* adv,
+                            const float* kl, const float* ent, const std::uint8_t* mask,
+                            std::int64_t n, const std::int64_t* cu, std::int64_t nseq,
+                            const PolicyLossConfig& c, LossSums* sums, void* ws,
+                            std::size_t ws_bytes, void* stream) {
+  c.validate();
+  const yatt_loss_config cc = to_c(c);
+  detail::throw_status(yatt_policy_loss_allreduce(
+      static_cast<yatt_peer_t>(h_), logp, old_logp, adv, kl, ent, mask, n, cu, nseq, &cc,
+      reinterpret_cast<yatt_loss_sums*>(sums), ws, ws_bytes, stream));
+}
+
+int PeerGroup::status() const {
+  std::int32_t s = 0;
+  detail::throw_status(yatt_peer_status(static_cast<yatt_peer_t>(h_), &s));
+  return s;
+}
+
 std::size_t dynamic_sampling_workspace_bytes(std::int64_t n) {
   return yatt_filter_compact_workspace_bytes(n);
 }

@@ -35,7 +35,10 @@ def test_cpp_dropin_api_is_exported():
                 "yatt::balancer::sort_and_bucket(", "yatt::balancer::padding_waste(",
                 "yatt::experience::token_logprob_stats(", "yatt::experience::policy_loss(",
                 "yatt::experience::gae(", "yatt::experience::grpo_advantages(",
-                "yatt::experience::dynamic_sampling_filter("]:
+                "yatt::experience::dynamic_sampling_filter(",
+                "yatt::experience::policy_logits_grad(", "yatt::experience::lmhead_token_stats(",
+                "yatt::experience::gather_payload(", "yatt::experience::PeerGroup::PeerGroup(",
+                "yatt::experience::PeerGroup::policy_loss("]:
         assert sym in out, sym
 
 
