@@ -159,6 +159,35 @@ def cpu_experience_rate(sample_rows: int | None = None, threads: int | None = No
             "sample": f"{rows} rows x V={VOCAB} (A1 fp64 + GRPO adv + loss), {dt:.2f} s"}
 
 
+def _ref_timing():
+    exe = Path(__file__).resolve().parent / "oracle" / "_ref" / "ref_timing"
+    if not exe.exists():
+        return None
+    return json.loads(subprocess.run([str(exe), "8"], capture_output=True, text=True,
+                                     timeout=300).stdout)
+
+
+def integer_path_baseline():
+    """the reference's own integer path (compiled from its
+    sources into oracle/_ref, `ref_timing`, one host thread per shard) next to
+    the same work through the drop-in C++ API on the GPU
+    (examples/_build/integer_timing: sim::run_rollout_rounds, every shard in one
+    launch per round), on configs[4]'s batch (16,384 samples, 8 controller
+    shards, rounds until none pending); the total train units must agree
+    bit-exactly.  None when oracle/_ref is absent."""
+    exe = Path(__file__).resolve().parent / "oracle" / "_ref" / "ref_timing"
+    if not exe.exists():
+        return None
+    ref = _ref_timing()
+    drv = Path(__file__).resolve().parent / "examples" / "_build" / "integer_timing"
+    ours = json.loads(subprocess.run([str(drv)], capture_output=True, text=True,
+                                     timeout=300).stdout) if drv.exists() else None
+    units = ours["train_units"] if ours else None
+    rounds = ours["rounds"] if ours else None
+    return {"reference_cpu": ref, "b200": ours,
+            "train_units_bit_exact": units == ref["train_units"] and rounds == ref["rounds"]}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -181,6 +210,7 @@ def run_reference(args):
             "data": "synthetic (keyed integer-derived bf16 logits, DESIGN.md)",
             "config": workload_config(args.gpus), "impl": "reference",
             "cpu_baseline": {**last, "value": v},
+            "integer_path_reference_cpu": _ref_timing(),
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     emit(line)
@@ -327,8 +357,10 @@ def run_b200(args):
     e2e = run_e2e(args, dev, ops, cfg, ws, world)
 
     cpu = None
+    integer = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_experience_rate(budget_s=args.ref_budget_s)
+        integer = integer_path_baseline()
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
@@ -337,6 +369,7 @@ def run_b200(args):
                 "dtype": "bf16", "data": "synthetic (keyed integer-derived bf16 logits, "
                 "binary group rewards; DESIGN.md)", "config": workload_config(world, args.collective),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "integer_path": integer,
                 # per group: token_stats + its fix-up pass; per step: grpo_adv,
                 # broadcast, loss partials + final
                 "gpu_launches": args.steps * (2 * ng + 4), "clocks": clk,
