@@ -217,6 +217,18 @@ __device__ __forceinline__ uint4 floor_policy(uint4 v) {
   return v;
 }
 
+// Keep elements [lo, hi) of an 8-element bf16 vector, -inf elsewhere (row
+// edges of an aligned staging superset when V % 8 != 0).
+__device__ __forceinline__ uint4 keep_range(uint4 v, int lo, int hi) {
+  uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (2 * k < lo || 2 * k >= hi) w[k] = (w[k] & 0xffff0000u) | 0xFF80u;
+    if (2 * k + 1 < lo || 2 * k + 1 >= hi) w[k] = (w[k] & 0x0000ffffu) | 0xFF800000u;
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
 __device__ __forceinline__ RowPartial combine(const RowPartial& A, const RowPartial& B) {
   RowPartial r;
   r.mp = fmaxf(A.mp, B.mp);
@@ -333,7 +345,9 @@ __device__ __forceinline__ void emit_row(const Params& p, int64_t row, const Row
   }
 }
 
-template <bool kFull>
+// kEdges: V % 8 != 0 — rows are staged as 16-byte-aligned supersets and the
+// edge vectors masked; false compiles the plain V % 8 == 0 kernel.
+template <bool kFull, bool kEdges>
 __global__ void __launch_bounds__(kThreads, 2) token_stats_kernel(const Params p) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint16_t* ring = reinterpret_cast<uint16_t*>(smem);
@@ -341,7 +355,6 @@ __global__ void __launch_bounds__(kThreads, 2) token_stats_kernel(const Params p
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t V = p.V;
-  const int ntiles = int((V + kTile - 1) / kTile);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -360,11 +373,16 @@ __global__ void __launch_bounds__(kThreads, 2) token_stats_kernel(const Params p
       uint32_t phase = 0;
       for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
         if (p.mask != nullptr && p.mask[row] == 0) continue;
-        const uint16_t* gp = p.pol + row * V;
-        const uint16_t* gq = p.ref + row * V;
-        for (int t = 0; t < ntiles; ++t) {
+        // stage the row's 16-byte-aligned superset: h elements before it
+        // (V % 8 != 0 only) and up to 7 after; consumers mask the edges
+        const int h = kEdges ? int((row * V) & 7) : 0;
+        const int64_t S = kEdges ? ((h + V + 7) & ~int64_t(7)) : V;
+        const int ntiles_r = int((S + kTile - 1) / kTile);
+        const uint16_t* gp = p.pol + row * V - h;
+        const uint16_t* gq = p.ref + row * V - h;
+        for (int t = 0; t < ntiles_r; ++t) {
           const int64_t e0 = int64_t(t) * kTile;
-          const uint32_t n = uint32_t(min64(kTile, V - e0));
+          const uint32_t n = uint32_t(min64(kTile, S - e0));
           mbar_wait(&tail->empty[stage], phase ^ 1u);
           mbar_arrive_expect_tx(&tail->full[stage], 4u * n);
           uint16_t* dst = ring + size_t(stage) * 2 * kTile;
@@ -403,13 +421,16 @@ __global__ void __launch_bounds__(kThreads, 2) token_stats_kernel(const Params p
       continue;
     }
     const int par = iter & 1;
-    const int ty = y / kTile;           // tile holding the target logit
-    const int yin = y - ty * kTile;
+    const int h = kEdges ? int((row * V) & 7) : 0;  // staged row starts h elements early
+    const int64_t S = kEdges ? ((h + V + 7) & ~int64_t(7)) : V;
+    const int ntiles_r = int((S + kTile - 1) / kTile);
+    const int ty = (y + h) / kTile;    // tile holding the target logit
+    const int yin = (y + h) - ty * kTile;
     acc.reset();
 
-    for (int t = 0; t < ntiles; ++t) {
+    for (int t = 0; t < ntiles_r; ++t) {
       const int64_t e0 = int64_t(t) * kTile;
-      const int nvec = int(min64(kTile, V - e0) >> 3);
+      const int nvec = int(min64(kTile, S - e0) >> 3);
       const uint16_t* sp = ring + size_t(stage) * 2 * kTile;
       const uint16_t* sq = sp + kTile;
       mbar_wait(&tail->full[stage], phase);
@@ -428,6 +449,14 @@ __global__ void __launch_bounds__(kThreads, 2) token_stats_kernel(const Params p
           const bool in = full || v < nvec;
           P[i] = in ? lds128(sp + v * 8) : make_uint4(kNegInf2, kNegInf2, kNegInf2, kNegInf2);
           Q[i] = in ? lds128(sq + v * 8) : make_uint4(kNegInf2, kNegInf2, kNegInf2, kNegInf2);
+          if (kEdges) {  // staged elements outside the row read as -inf
+            const int64_t j0 = e0 + int64_t(v) * 8 - h;  // row index of element 0
+            if (in && (j0 < 0 || j0 + 8 > V)) {
+              const int lo = int(max64(0, -j0)), hi = int(min64(8, V - j0));
+              P[i] = keep_range(P[i], lo, hi);
+              Q[i] = keep_range(Q[i], lo, hi);
+            }
+          }
         }
 #pragma unroll
         for (int i = 0; i < kVecPerThread; ++i) {
@@ -590,9 +619,32 @@ int token_stats_launch(const uint16_t* pol, const uint16_t* ref, const int32_t* 
   YATT_REQUIRE(logp != nullptr, YATT_ERR_CONFIG, "token_stats: logp output is required");
   YATT_REQUIRE(pol && ref && tgt, YATT_ERR_CONFIG, "token_stats: null input pointer");
   Params p{pol, ref, tgt, mask, rows, vocab, kl_mode, logp, ref_logp, ent, kl};
-  const bool tma_ok = vocab % 8 == 0 && (reinterpret_cast<uintptr_t>(pol) & 15) == 0 &&
-                      (reinterpret_cast<uintptr_t>(ref) & 15) == 0;
-  if (!tma_ok) {  // generic path: any vocabulary size / alignment, scalar loads
+  // The TMA path needs 16-byte-aligned tensor bases; any vocab: each row is
+  // staged as its aligned superset.  With V % 8 != 0 the last row's superset
+  // could end past the tensor, so that one row takes the generic kernel.
+  const bool tma_ok = (reinterpret_cast<uintptr_t>(pol) & 15) == 0 &&
+                      (reinterpret_cast<uintptr_t>(ref) & 15) == 0 && (vocab % 8 == 0 || rows > 1);
+  if (tma_ok && vocab % 8 != 0) {
+    Params last = p;
+    const int64_t off = (rows - 1) * int64_t(vocab);
+    last.pol = pol + off;
+    last.ref = ref + off;
+    last.tgt = tgt + (rows - 1);
+    last.mask = mask ? mask + (rows - 1) : nullptr;
+    last.rows = 1;
+    last.logp = logp + (rows - 1);
+    last.ref_logp = ref_logp ? ref_logp + (rows - 1) : nullptr;
+    last.ent = ent ? ent + (rows - 1) : nullptr;
+    last.kl = kl ? kl + (rows - 1) : nullptr;
+    if (kl_mode == YATT_KL_FULL)
+      token_stats_fixup_kernel<true, true><<<1, kConsumers, 0, st>>>(last);
+    else
+      token_stats_fixup_kernel<false, true><<<1, kConsumers, 0, st>>>(last);
+    const int rc = check_launch("token_stats_generic_kernel");
+    if (rc) return rc;
+    p.rows = rows - 1;
+  }
+  if (!tma_ok) {  // generic path: unaligned tensors, scalar loads
     const int ggrid = int(min64(ceil_div(rows, 8), int64_t(num_sms()) * 8));
     if (kl_mode == YATT_KL_FULL)
       token_stats_fixup_kernel<true, true><<<ggrid, kConsumers, 0, st>>>(p);
@@ -600,23 +652,30 @@ int token_stats_launch(const uint16_t* pol, const uint16_t* ref, const int32_t* 
       token_stats_fixup_kernel<false, true><<<ggrid, kConsumers, 0, st>>>(p);
     return check_launch("token_stats_generic_kernel");
   }
-  const int grid = int(min64(rows, int64_t(2) * num_sms()));
-  if (kl_mode == YATT_KL_FULL) {
-    {
-      const int rc_ = ensure_dynamic_smem(reinterpret_cast<const void*>(token_stats_kernel<true>), int(kSmemBytes));
-      if (rc_) return rc_;
+  const int grid = int(min64(p.rows, int64_t(2) * num_sms()));
+  {
+    const bool edges = vocab % 8 != 0, full = kl_mode == YATT_KL_FULL;
+    const void* k = edges ? (full ? reinterpret_cast<const void*>(token_stats_kernel<true, true>)
+                                  : reinterpret_cast<const void*>(token_stats_kernel<false, true>))
+                          : (full ? reinterpret_cast<const void*>(token_stats_kernel<true, false>)
+                                  : reinterpret_cast<const void*>(token_stats_kernel<false, false>));
+    const int rc_ = ensure_dynamic_smem(k, int(kSmemBytes));
+    if (rc_) return rc_;
+    if (edges) {
+      if (full)
+        token_stats_kernel<true, true><<<grid, kThreads, kSmemBytes, st>>>(p);
+      else
+        token_stats_kernel<false, true><<<grid, kThreads, kSmemBytes, st>>>(p);
+    } else {
+      if (full)
+        token_stats_kernel<true, false><<<grid, kThreads, kSmemBytes, st>>>(p);
+      else
+        token_stats_kernel<false, false><<<grid, kThreads, kSmemBytes, st>>>(p);
     }
-    token_stats_kernel<true><<<grid, kThreads, kSmemBytes, st>>>(p);
-  } else {
-    {
-      const int rc_ = ensure_dynamic_smem(reinterpret_cast<const void*>(token_stats_kernel<false>), int(kSmemBytes));
-      if (rc_) return rc_;
-    }
-    token_stats_kernel<false><<<grid, kThreads, kSmemBytes, st>>>(p);
   }
   int rc = check_launch("token_stats_kernel");
   if (rc || !kFastPath) return rc;
-  const int fgrid = int(min64(ceil_div(rows, kConsumers), int64_t(num_sms())));
+  const int fgrid = int(min64(ceil_div(p.rows, kConsumers), int64_t(num_sms())));
   if (kl_mode == YATT_KL_FULL)
     token_stats_fixup_kernel<true, false><<<fgrid, kConsumers, 0, st>>>(p);
   else

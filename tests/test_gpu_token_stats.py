@@ -105,6 +105,39 @@ def test_token_stats_any_vocab_and_alignment(cuda, vocab, kl_mode):
         assert O.max_rel_error(g2[0], e2[0]) <= TOL and O.max_rel_error(g2[2], e2[2]) <= TOL
 
 
+@pytest.mark.parametrize("vocab", [9, 8191, 8193, 16385, 50257])
+@pytest.mark.parametrize("kl_mode", ["k3", "full"])
+def test_token_stats_odd_vocab_row_edges(cuda, vocab, kl_mode):
+    """V % 8 != 0 on the TMA path: each row is staged as its 16-byte-aligned
+    superset (up to 7 elements of the neighbouring rows on each side, masked
+    to -inf).  Targets on the first / last element of the row, peaked rows
+    whose maximum sits on a row edge, masked rows."""
+    rows = 64
+    g = torch.Generator(device=cuda).manual_seed(vocab + 7)
+    pol = (torch.randn(rows, vocab, device=cuda, generator=g) * 2).to(torch.bfloat16)
+    ref = (pol.float() + 0.2 * torch.randn(rows, vocab, device=cuda, generator=g)).to(
+        torch.bfloat16)
+    pol[1::4, 0] = 30.0          # maxima on the row edges: a leak of the
+    pol[2::4, vocab - 1] = 30.0  # neighbour's elements would shift the lse
+    tgt = torch.where(torch.arange(rows, device=cuda) % 2 == 0, 0, vocab - 1).to(torch.int32)
+    mask = (torch.arange(rows, device=cuda) % 7 != 3).to(torch.uint8)
+    got = torch.stack(ops.token_stats(pol, ref, tgt, mask, kl_mode)).cpu().numpy()
+    hp = pol.view(torch.int16).cpu().numpy().view(np.uint16)
+    hr = ref.view(torch.int16).cpu().numpy().view(np.uint16)
+    m = mask.cpu().numpy()
+    exp = O.token_stats(hp, hr, tgt.cpu().numpy(), m, kl_mode)
+    for i in range(2):
+        assert np.all(np.abs(got[i] - exp[i]) <= TOL * np.abs(exp[i]) + 1e-6), (i, vocab)
+    # entropy of a peaked row is lse - sum p x, two numbers ~ max|x| cancelling
+    # to ~1e-7: fp32's absolute floor there is ~max|x| * 2^-23
+    amax = np.abs(pol.float().cpu().numpy()).max(1)
+    assert np.all(np.abs(got[2] - exp[2]) <= TOL * np.abs(exp[2]) + 1e-7 * amax + 1e-6), vocab
+    d = exp[1] - exp[0]
+    slope = np.abs(np.expm1(d)) if kl_mode == "k3" else 1.0
+    assert np.all(np.abs(got[3] - exp[3]) <= TOL * np.abs(exp[3]) + 1e-6 * slope + 1e-9)
+    assert np.all(got[:, m == 0] == 0)
+
+
 def test_token_stats_masked_vocab_and_peaked_rows(cuda):
     """-inf (masked-vocab) logits and a near-one-hot row: finite, accurate."""
     rows, vocab = 16, 32000

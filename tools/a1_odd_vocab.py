@@ -1,0 +1,18 @@
+import sys, torch
+sys.path.insert(0, "/root/repo")
+from paper_2508_07970_b200 import ops
+dev = torch.device("cuda:0")
+for rows, V in [(16384, 50257), (16384, 50264), (4096, 151937)]:
+    g = torch.Generator(device=dev).manual_seed(1)
+    pol = (torch.randn(rows, V, device=dev, generator=g) * 2).to(torch.bfloat16)
+    ref = (pol.float() + 0.1 * torch.randn(rows, V, device=dev, generator=g)).to(torch.bfloat16)
+    tgt = torch.randint(0, V, (rows,), device=dev, generator=g, dtype=torch.int32)
+    out = torch.empty((4, rows), device=dev)
+    for _ in range(2): ops.token_stats(pol, ref, tgt, None, "k3", out=out)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(5): ops.token_stats(pol, ref, tgt, None, "k3", out=out)
+    b.record(); torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / 5
+    print(rows, V, round(ms, 3), "ms", round(rows * (4 * V + 21) / ms / 1e6), "GB/s")
