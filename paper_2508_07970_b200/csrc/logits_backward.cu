@@ -109,7 +109,26 @@ struct __align__(16) BwdTail {
   uint64_t empty[kMaxStages];
 };
 
-template <bool kFull>
+// Stores one gradient vector at staged index j (of a row staged from h
+// elements before its start); with kEdges, a vector straddling the row's
+// ends writes only its in-row elements (the neighbours own the rest).
+template <bool kEdges>
+__device__ __forceinline__ void store_grad(uint16_t* gs, int64_t j, uint4 g, int h, int64_t V) {
+  if (!kEdges || (j >= h && j + 8 <= h + V)) {
+    stg_cs_128(gs + j, g);
+    return;
+  }
+  const uint32_t w[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int64_t idx = j + k;
+    if (idx >= h && idx < h + V) gs[idx] = uint16_t((w[k >> 1] >> (16 * (k & 1))) & 0xffffu);
+  }
+}
+
+// kEdges: V % 8 != 0 — rows staged as 16-byte-aligned supersets (as in A1);
+// the gradient tensor has the same layout, so interior vectors stay aligned.
+template <bool kFull, bool kEdges>
 __global__ void __launch_bounds__(kThreads, 2) logits_backward_kernel(const GradParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int kPerStage = kFull ? 2 : 1;
@@ -118,7 +137,6 @@ __global__ void __launch_bounds__(kThreads, 2) logits_backward_kernel(const Grad
   BwdTail* tail = reinterpret_cast<BwdTail*>(smem + size_t(kStages) * kPerStage * kTile * 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t V = p.V;
-  const int ntiles = int((V + kTile - 1) / kTile);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&tail->full[s], 1);
@@ -135,14 +153,18 @@ __global__ void __launch_bounds__(kThreads, 2) logits_backward_kernel(const Grad
       uint32_t phase = 0;
       for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
         if (p.mask != nullptr && p.mask[row] == 0) continue;
-        for (int t = 0; t < ntiles; ++t) {
+        const int h = kEdges ? int((row * V) & 7) : 0;
+        const int64_t S = kEdges ? ((h + V + 7) & ~int64_t(7)) : V;
+        const int ntiles_r = int((S + kTile - 1) / kTile);
+        for (int t = 0; t < ntiles_r; ++t) {
           const int64_t e0 = int64_t(t) * kTile;
-          const uint32_t n = uint32_t(min64(kTile, V - e0));
+          const uint32_t n = uint32_t(min64(kTile, S - e0));
           mbar_wait(&tail->empty[stage], phase ^ 1u);
           mbar_arrive_expect_tx(&tail->full[stage], 2u * n * kPerStage);
           uint16_t* dst = ring + size_t(stage) * kPerStage * kTile;
-          bulk_g2s(dst, p.pol + row * V + e0, 2u * n, &tail->full[stage], pol);
-          if (kFull) bulk_g2s(dst + kTile, p.ref + row * V + e0, 2u * n, &tail->full[stage], pol);
+          bulk_g2s(dst, p.pol + row * V - h + e0, 2u * n, &tail->full[stage], pol);
+          if (kFull)
+            bulk_g2s(dst + kTile, p.ref + row * V - h + e0, 2u * n, &tail->full[stage], pol);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1u;
@@ -172,16 +194,20 @@ __global__ void __launch_bounds__(kThreads, 2) logits_backward_kernel(const Grad
     const float4 c0 = n0, c1 = n1;
     const int32_t y = ny;
     load_row(row + gridDim.x, n0, n1, ny);
-    uint16_t* grow = p.grad + row * V;
+    const int h = kEdges ? int((row * V) & 7) : 0;
+    const int64_t S = kEdges ? ((h + V + 7) & ~int64_t(7)) : V;
+    const int ntiles_r = int((S + kTile - 1) / kTile);
+    uint16_t* gs = p.grad + row * V - h;  // staged coordinates
     if (p.mask != nullptr && p.mask[row] == 0) {
-      for (int64_t v = tid; v < V / 8; v += kConsumers)
-        stg_cs_128(grow + v * 8, make_uint4(0, 0, 0, 0));
+      for (int64_t v = tid; v < S / 8; v += kConsumers)
+        store_grad<kEdges>(gs, v * 8, make_uint4(0, 0, 0, 0), h, V);
       continue;
     }
     const RowCoef c{c0.x, c0.y, c0.z, c0.w * kLog2e, c1.x * kLog2e, c1.y, c1.z};
-    for (int t = 0; t < ntiles; ++t) {
+    const int64_t ys = int64_t(y) + h;  // the target in staged coordinates
+    for (int t = 0; t < ntiles_r; ++t) {
       const int64_t e0 = int64_t(t) * kTile;
-      const int nvec = int(min64(kTile, V - e0) >> 3);
+      const int nvec = int(min64(kTile, S - e0) >> 3);
       const uint16_t* sp = ring + size_t(stage) * kPerStage * kTile;
       const uint16_t* sq = sp + kTile;
       mbar_wait(&tail->full[stage], phase);
@@ -194,27 +220,28 @@ __global__ void __launch_bounds__(kThreads, 2) logits_backward_kernel(const Grad
         }
 #pragma unroll
         for (int i = 0; i < kVecPerThread; ++i)
-          stg_cs_128(grow + e0 + (tid + i * kConsumers) * 8, grad_vec<kFull>(P[i], Q[i], c));
+          store_grad<kEdges>(gs, e0 + (tid + i * kConsumers) * 8, grad_vec<kFull>(P[i], Q[i], c), h,
+                             V);
       } else {
         for (int v = tid; v < nvec; v += kConsumers) {
           const uint4 P = lds128(sp + v * 8);
           const uint4 Q = kFull ? lds128(sq + v * 8) : P;
-          stg_cs_128(grow + e0 + v * 8, grad_vec<kFull>(P, Q, c));
+          store_grad<kEdges>(gs, e0 + v * 8, grad_vec<kFull>(P, Q, c), h, V);
         }
       }
       // the target element gets + g: its owner rewrites those two bytes
       // (same thread, program order after the vector store)
-      if (y >= e0 && y < e0 + kTile && tid == ((y - e0) >> 3) % kConsumers) {
-        const float x = __uint_as_float(uint32_t(sp[y - e0]) << 16);
+      if (ys >= e0 && ys < e0 + kTile && tid == ((ys - e0) >> 3) % kConsumers) {
+        const float x = __uint_as_float(uint32_t(sp[ys - e0]) << 16);
         const float a = fmaf(x, kLog2e, -c.lsep2);
         const float pp = ex2_approx(a);
         float val = pp * fmaf(c.h, a * kLn2f + c.H, -c.g) + c.g;
         if (kFull) {
-          const float z = __uint_as_float(uint32_t(sq[y - e0]) << 16);
+          const float z = __uint_as_float(uint32_t(sq[ys - e0]) << 16);
           const float lnq = fmaf(z, kLog2e, -c.lseq2) * kLn2f;
           val = fmaf(c.f * pp, a * kLn2f - lnq - c.KL, val);
         }
-        grow[y] = uint16_t(pack_bf16x2(val, 0.f) & 0xffffu);
+        gs[ys] = uint16_t(pack_bf16x2(val, 0.f) & 0xffffu);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&tail->empty[stage]);
@@ -366,32 +393,48 @@ int logits_backward_launch(const uint16_t* pol, const uint16_t* ref, const int32
   YATT_REQUIRE(pol && tgt && coef && grad && (!full_kl || ref), YATT_ERR_CONFIG,
                "logits_backward: null pointer");
   GradParams prm{pol, ref, tgt, mask, coef, rows, V, grad};
-  const bool tma_ok = V % 8 == 0 && (reinterpret_cast<uintptr_t>(pol) & 15) == 0 &&
-                      (reinterpret_cast<uintptr_t>(grad) & 15) == 0 &&
-                      (!full_kl || (reinterpret_cast<uintptr_t>(ref) & 15) == 0);
-  if (!tma_ok) {
-    const int g = int(min64(rows, int64_t(8) * num_sms()));
+  auto a16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  const bool tma_ok = a16(pol) && a16(grad) && (!full_kl || a16(ref)) && (V % 8 == 0 || rows > 1);
+  auto generic = [&](const GradParams& g) {
+    const int gg = int(min64(g.rows, int64_t(8) * num_sms()));
     if (full_kl)
-      logits_backward_generic_kernel<true><<<g, 256, 0, st>>>(prm);
+      logits_backward_generic_kernel<true><<<gg, 256, 0, st>>>(g);
     else
-      logits_backward_generic_kernel<false><<<g, 256, 0, st>>>(prm);
+      logits_backward_generic_kernel<false><<<gg, 256, 0, st>>>(g);
     return check_launch("logits_backward_generic_kernel");
+  };
+  if (!tma_ok) return generic(prm);
+  const bool edges = V % 8 != 0;
+  if (edges) {  // the last row's aligned superset could end past the tensors
+    const int64_t off = (rows - 1) * int64_t(V);
+    GradParams last{pol + off, full_kl ? ref + off : nullptr, tgt + (rows - 1),
+                    mask ? mask + (rows - 1) : nullptr, coef + (rows - 1) * kCoef, 1, V,
+                    grad + off};
+    const int rc = generic(last);
+    if (rc) return rc;
+    prm.rows = rows - 1;
   }
-  const int grid = int(min64(rows, int64_t(2) * num_sms()));
+  const int grid = int(min64(prm.rows, int64_t(2) * num_sms()));
   if (full_kl) {
     constexpr size_t smem = size_t(stages_of<true>()) * 2 * kTile * 2 + sizeof(BwdTail);
-    {
-      const int rc_ = ensure_dynamic_smem(reinterpret_cast<const void*>(logits_backward_kernel<true>), int(smem));
-      if (rc_) return rc_;
-    }
-    logits_backward_kernel<true><<<grid, kThreads, smem, st>>>(prm);
+    const void* k = edges ? reinterpret_cast<const void*>(logits_backward_kernel<true, true>)
+                          : reinterpret_cast<const void*>(logits_backward_kernel<true, false>);
+    const int rc_ = ensure_dynamic_smem(k, int(smem));
+    if (rc_) return rc_;
+    if (edges)
+      logits_backward_kernel<true, true><<<grid, kThreads, smem, st>>>(prm);
+    else
+      logits_backward_kernel<true, false><<<grid, kThreads, smem, st>>>(prm);
   } else {
     constexpr size_t smem = size_t(stages_of<false>()) * kTile * 2 + sizeof(BwdTail);
-    {
-      const int rc_ = ensure_dynamic_smem(reinterpret_cast<const void*>(logits_backward_kernel<false>), int(smem));
-      if (rc_) return rc_;
-    }
-    logits_backward_kernel<false><<<grid, kThreads, smem, st>>>(prm);
+    const void* k = edges ? reinterpret_cast<const void*>(logits_backward_kernel<false, true>)
+                          : reinterpret_cast<const void*>(logits_backward_kernel<false, false>);
+    const int rc_ = ensure_dynamic_smem(k, int(smem));
+    if (rc_) return rc_;
+    if (edges)
+      logits_backward_kernel<false, true><<<grid, kThreads, smem, st>>>(prm);
+    else
+      logits_backward_kernel<false, false><<<grid, kThreads, smem, st>>>(prm);
   }
   return check_launch("logits_backward_kernel");
 }
