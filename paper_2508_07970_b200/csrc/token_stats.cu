@@ -27,6 +27,9 @@
 //                 epilogue by a rotating warp.  The target logits are picked
 //                 out of the staged tile by whichever thread holds them — no
 //                 extra global loads.
+// Any vocab on 16-byte-aligned tensors: with V % 8 != 0 (kEdges) each row is
+// staged as its aligned superset (up to 7 neighbouring elements per side),
+// the edge vectors masked to -inf; the last row takes the generic kernel.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
