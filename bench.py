@@ -159,12 +159,21 @@ def cpu_experience_rate(sample_rows: int | None = None, threads: int | None = No
             "sample": f"{rows} rows x V={VOCAB} (A1 fp64 + GRPO adv + loss), {dt:.2f} s"}
 
 
+def _run_json(cmd):
+    """One JSON line from a helper binary; an error dict (never an exception)
+    if it is missing or fails, so the bench line is always printed."""
+    try:
+        res = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+        return json.loads(res.stdout)
+    except Exception as e:  # noqa: BLE001
+        return {"error": f"{Path(cmd[0]).name}: {type(e).__name__}: {e}"[:300]}
+
+
 def _ref_timing():
     exe = Path(__file__).resolve().parent / "oracle" / "_ref" / "ref_timing"
     if not exe.exists():
         return None
-    return json.loads(subprocess.run([str(exe), "8"], capture_output=True, text=True,
-                                     timeout=300).stdout)
+    return _run_json([str(exe), "8"])
 
 
 def integer_path_baseline():
@@ -180,12 +189,12 @@ def integer_path_baseline():
         return None
     ref = _ref_timing()
     drv = Path(__file__).resolve().parent / "examples" / "_build" / "integer_timing"
-    ours = json.loads(subprocess.run([str(drv)], capture_output=True, text=True,
-                                     timeout=300).stdout) if drv.exists() else None
-    units = ours["train_units"] if ours else None
-    rounds = ours["rounds"] if ours else None
+    ours = _run_json([str(drv)]) if drv.exists() else None
+    units = ours.get("train_units") if ours else None
+    rounds = ours.get("rounds") if ours else None
     return {"reference_cpu": ref, "b200": ours,
-            "train_units_bit_exact": units == ref["train_units"] and rounds == ref["rounds"]}
+            "train_units_bit_exact": (units is not None and units == ref.get("train_units")
+                                      and rounds == ref.get("rounds"))}
 
 
 def run_reference(args):
