@@ -368,8 +368,14 @@ def run_b200(args):
     cpu = None
     integer = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_experience_rate(budget_s=args.ref_budget_s)
-        integer = integer_path_baseline()
+        try:
+            cpu = cpu_experience_rate(budget_s=args.ref_budget_s)
+        except Exception as e:  # noqa: BLE001 - the bench line must still print
+            cpu = {"error": f"{type(e).__name__}: {e}"[:300]}
+        try:
+            integer = integer_path_baseline()
+        except Exception as e:  # noqa: BLE001
+            integer = {"error": f"{type(e).__name__}: {e}"[:300]}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
