@@ -45,6 +45,20 @@ def _dev(t: torch.Tensor, dtype: torch.dtype, name: str) -> torch.Tensor:
     return t
 
 
+def _devs(dtype: torch.dtype, **named) -> None:
+    """_dev for several (optional) tensors of one dtype."""
+    for name, t in named.items():
+        if t is not None:
+            _dev(t, dtype, name)
+
+
+def _dense(**named) -> None:
+    """CUDA + contiguous, any dtype (byte-level gathers)."""
+    for name, t in named.items():
+        if t is not None:
+            _dev(t, t.dtype, name)
+
+
 def _mask(mask: torch.Tensor | None) -> torch.Tensor | None:
     if mask is None:
         return None
@@ -150,6 +164,7 @@ def grpo_advantages(rewards: torch.Tensor, group_size: int, eps: float = 1e-6,
 def broadcast_to_tokens(sample_vals: torch.Tensor, cu_seqlens: torch.Tensor, n_tokens: int,
                         mask: torch.Tensor | None = None, out: torch.Tensor | None = None):
     _dev(cu_seqlens, torch.int64, "cu_seqlens")
+    _devs(torch.float32, sample_vals=sample_vals, out=out)
     if out is None:
         out = torch.empty((n_tokens,), dtype=torch.float32, device=sample_vals.device)
     check(lib().yatt_broadcast_to_tokens(_p(sample_vals), _p(cu_seqlens), sample_vals.numel(),
@@ -175,6 +190,7 @@ def gae(values: torch.Tensor, rewards: torch.Tensor, cu_seqlens: torch.Tensor,
 
 
 def masked_moments(x: torch.Tensor, mask: torch.Tensor | None = None) -> torch.Tensor:
+    _dev(x, torch.float32, "x")
     out = torch.empty((3,), dtype=torch.float64, device=x.device)
     wsb = lib().yatt_masked_moments_workspace_bytes()
     ws = torch.empty((wsb,), dtype=torch.uint8, device=x.device)
@@ -184,6 +200,8 @@ def masked_moments(x: torch.Tensor, mask: torch.Tensor | None = None) -> torch.T
 
 def whiten(x: torch.Tensor, moments: torch.Tensor, mask: torch.Tensor | None = None,
            shift_mean: bool = True) -> torch.Tensor:
+    _dev(x, torch.float32, "x")
+    _dev(moments, torch.float64, "moments")
     check(lib().yatt_whiten(_p(x), _p(_mask(mask)), x.numel(), _p(moments), int(shift_mean), _st()))
     return x
 
@@ -205,6 +223,10 @@ def policy_loss(logp, old_logp, advantages, kl, entropy, mask=None, cu_seqlens=N
                 config: LossConfigC | None = None, workspace: LossWorkspace | None = None,
                 sums: torch.Tensor | None = None) -> torch.Tensor:
     """Returns the 8 fp64 yatt_loss_sums fields as a device tensor."""
+    _devs(torch.float32, logp=logp, old_logp=old_logp, advantages=advantages, kl=kl,
+          entropy=entropy)
+    if cu_seqlens is not None:
+        _dev(cu_seqlens, torch.int64, "cu_seqlens")
     cfg = config or loss_config()
     ws = workspace or LossWorkspace(logp.device)
     if sums is None:
@@ -242,6 +264,7 @@ def filter_compact(rewards: torch.Tensor, seq_lens: torch.Tensor, group_size: in
 def gather_varlen(src: torch.Tensor, old_cu: torch.Tensor, index_map: torch.Tensor,
                   new_cu: torch.Tensor, n_kept: torch.Tensor, max_kept: int, dst: torch.Tensor,
                   dst_offset: torch.Tensor | None = None) -> torch.Tensor:
+    _dense(src=src, dst=dst)
     check(lib().yatt_gather_varlen(_p(src), _p(old_cu), _p(index_map), _p(new_cu), _p(n_kept),
                                    max_kept, _p(dst_offset), src.element_size(), _p(dst), _st()))
     return dst
@@ -254,6 +277,10 @@ def gather_varlen_multi(srcs, old_cu: torch.Tensor, index_map: torch.Tensor, new
     n = len(srcs)
     if n != len(dsts):
         raise ValueError("srcs and dsts differ in length")
+    for i, (a, b) in enumerate(zip(srcs, dsts)):
+        _dense(**{f"srcs[{i}]": a, f"dsts[{i}]": b})
+        if a.dtype != b.dtype:
+            raise TypeError(f"srcs[{i}] and dsts[{i}] differ in dtype")
     h_src = (C.c_void_p * n)(*[t.data_ptr() for t in srcs])
     h_dst = (C.c_void_p * n)(*[t.data_ptr() for t in dsts])
     h_esz = (C.c_int32 * n)(*[t.element_size() for t in srcs])
@@ -264,6 +291,7 @@ def gather_varlen_multi(srcs, old_cu: torch.Tensor, index_map: torch.Tensor, new
 
 def gather_rows(src: torch.Tensor, index_map: torch.Tensor, n_kept: torch.Tensor, max_kept: int,
                 dst: torch.Tensor, dst_offset: torch.Tensor | None = None) -> torch.Tensor:
+    _dense(src=src, dst=dst)
     row_bytes = src[0].numel() * src.element_size() if src.dim() > 1 else src.element_size()
     check(lib().yatt_gather_rows(_p(src), _p(index_map), _p(n_kept), max_kept, row_bytes,
                                  _p(dst_offset), _p(dst), _st()))
@@ -323,6 +351,7 @@ def lmhead_token_stats(hidden: torch.Tensor, lm_head: torch.Tensor, targets: tor
 
 
 def kl_from_logps(logp: torch.Tensor, ref_logp: torch.Tensor, kl_mode: str = "k3"):
+    _devs(torch.float32, logp=logp, ref_logp=ref_logp)
     kl = torch.empty_like(logp)
     check(lib().yatt_kl_from_logps(_p(logp), _p(ref_logp), logp.numel(), KL_MODES[kl_mode],
                                    _p(kl), _st()))
@@ -336,6 +365,10 @@ def logits_grad(policy_logits, ref_logits, targets, logp, ref_logp, old_logp, ad
     """dL/d(policy logits) of the A4 loss (bf16 [rows, V]) + the per-token
     coefficient table (fp32 [rows, 8]: g, h, f, lse_p, lse_q, H, KL, scratch)."""
     cfg = config or loss_config()
+    _devs(torch.bfloat16, policy_logits=policy_logits, ref_logits=ref_logits, grad=grad)
+    _devs(torch.float32, logp=logp, ref_logp=ref_logp, old_logp=old_logp, advantages=advantages,
+          entropy=entropy, kl=kl)
+    _dev(targets, torch.int32, "targets")
     rows, vocab = policy_logits.shape
     coef = torch.empty((rows, 8), dtype=torch.float32, device=policy_logits.device)
     m = _mask(mask)

@@ -256,3 +256,20 @@ def test_config1_experience_pipeline_matches_oracle(cuda):
     assert O.max_rel_error(sums, e_sums) <= 1e-4  # A1 fp32 rounding feeds the ratio
     assert abs(ops.loss_finalize(sums, cfg) - ops.loss_finalize(e_sums, cfg)) <= \
         1e-5 * max(1.0, abs(ops.loss_finalize(e_sums, cfg)))
+
+
+def test_ops_reject_strided_and_mistyped_inputs(cuda):
+    """The kernels read dense arrays: a strided view or a wrong dtype must be
+    rejected in the ops layer instead of being read as if it were dense."""
+    x = torch.randn(64, device=cuda)
+    with pytest.raises(ValueError, match="contiguous"):
+        ops.policy_loss(x[::2], x[::2].contiguous(), x[:32], x[:32], x[:32])
+    with pytest.raises(TypeError):
+        ops.policy_loss(x.double(), x, x, x, x)
+    with pytest.raises(ValueError, match="contiguous"):
+        ops.masked_moments(x[::2])
+    with pytest.raises(ValueError, match="contiguous"):
+        ops.gather_varlen(x[::2], torch.zeros(2, dtype=torch.int64, device=cuda),
+                          torch.zeros(1, dtype=torch.int32, device=cuda),
+                          torch.zeros(2, dtype=torch.int64, device=cuda),
+                          torch.zeros(1, dtype=torch.int64, device=cuda), 1, x[:16])
