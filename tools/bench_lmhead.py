@@ -1,6 +1,6 @@
 """§8f #4 benchmark: fused tcgen05 LM-head + online log-softmax vs the unfused
 path (cuBLAS bf16 GEMM writing [rows, V] logits + the A1-style streaming
-read), Qwen2.5-7B head: d=3584, V=152,064.  TFLOP/s vs the measured cuBLAS
+read); default Qwen2.5-7B head d=3584, V=152,064 (argv: rows [d V]).  TFLOP/s vs the measured cuBLAS
 bf16 peak (MEASURED_PEAKS.json).  One JSON line per measurement."""
 import json
 import statistics
@@ -34,7 +34,8 @@ def timeit(fn, iters=10, warm=3):
 
 
 rows = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
-d, V = 3584, 152064
+d = int(sys.argv[2]) if len(sys.argv) > 2 else 3584      # Qwen2.5-7B hidden
+V = int(sys.argv[3]) if len(sys.argv) > 3 else 152064    # Qwen2.5 vocabulary
 g = torch.Generator(device="cuda").manual_seed(0)
 h = torch.randn(rows, d, device="cuda", generator=g).to(torch.bfloat16)
 w = (torch.randn(V, d, device="cuda", generator=g) * (2.0 / d ** 0.5)).to(torch.bfloat16)
@@ -48,7 +49,8 @@ print(json.dumps({"op": "fused lmhead_token_stats (tcgen05)", "rows": rows, "d":
 
 logits = torch.empty((rows, V), dtype=torch.bfloat16, device="cuda")
 ms_gemm = timeit(lambda: torch.matmul(h, w.t(), out=logits))
-print(json.dumps({"op": "cuBLAS bf16 GEMM (logits materialised)", "rows": rows, "ms": ms_gemm,
+print(json.dumps({"op": "cuBLAS bf16 GEMM (logits materialised)", "rows": rows, "d": d, "V": V,
+                  "ms": ms_gemm,
                   "tflops": flops / ms_gemm / 1e9}), flush=True)
 # the unfused path: GEMM + streaming log-softmax statistics over the logits
 # (token_stats reads two tensors; the single-model read is half of that)
