@@ -1,5 +1,12 @@
-import sys, torch
-sys.path.insert(0, "/root/repo")
+"""A1 (and the backward) at vocabularies not divisible by 8 (GPT-2's 50,257,
+151,937) next to the nearest aligned size: the aligned-superset staging of
+the TMA path.  One line per shape: ms and algorithmic GB/s."""
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2508_07970_b200 import ops
 dev = torch.device("cuda:0")
 for rows, V in [(16384, 50257), (16384, 50264), (4096, 151937)]:

@@ -1,5 +1,11 @@
-import sys, torch
-sys.path.insert(0, "/root/repo")
+"""A1 throughput across vocabularies (8,192 .. 152,064) and row counts, CUDA
+events, L2 flushed between launches: the per-row overhead at small V."""
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2508_07970_b200 import ops
 dev = torch.device("cuda:0")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
