@@ -55,10 +55,12 @@ struct GaeConfig {
 
 // n_tokens = length of the packed arrays; workspace of gae_workspace_bytes(n_tokens).
 std::size_t gae_workspace_bytes(std::int64_t n_tokens);
+// device_moments (optional, 3 doubles): masked {count, sum, sum_sq} of the
+// advantages from the same pass (the whitening statistics).
 void gae(const float* values, const float* rewards, const std::uint8_t* mask,
          const std::int64_t* cu_seqlens, std::int64_t n_seqs, std::int64_t n_tokens,
          const GaeConfig& config, float* advantages, float* returns, void* workspace,
-         std::size_t workspace_bytes, void* stream = nullptr);
+         std::size_t workspace_bytes, void* stream = nullptr, double* device_moments = nullptr);
 
 // ---- A4 -------------------------------------------------------------------
 enum class LossAggregation { kTokenMean = 0, kSeqMeanTokenMean = 1, kSeqMeanTokenSum = 2 };

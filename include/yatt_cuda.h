@@ -247,6 +247,14 @@ int yatt_gae(const float* d_values, const float* d_rewards,
              int64_t n_seqs, int64_t n_tokens, float gamma, float lam,
              float* d_advantages, float* d_returns, void* d_workspace,
              size_t workspace_bytes, void* stream);
+/* yatt_gae that also writes the masked moments {count, sum, sum_sq} of the   */
+/* advantages it stores (the whitening statistics of yatt_masked_moments,     */
+/* accumulated in the same pass; same workspace).                            */
+int yatt_gae_with_moments(const float* d_values, const float* d_rewards,
+                          const uint8_t* d_mask, const int64_t* d_cu_seqlens,
+                          int64_t n_seqs, int64_t n_tokens, float gamma, float lam,
+                          float* d_advantages, float* d_returns, double* d_moments,
+                          void* d_workspace, size_t workspace_bytes, void* stream);
 /* Masked moments {count, sum, sum_sq} (fp64, deterministic) of x, written    */
 /* to d_out[3]; all-reduce them across ranks before yatt_whiten.             */
 size_t yatt_masked_moments_workspace_bytes(void);

@@ -110,6 +110,8 @@ SIGNATURES = {
     "yatt_grpo_advantages": (C.c_int, [c_p, c_i64, c_u64, c_i32, c_f32, c_i32, c_p, c_p, c_p]),
     "yatt_broadcast_to_tokens": (C.c_int, [c_p, c_p, c_i64, c_p, c_p, c_i64, c_p]),
     "yatt_gae_workspace_bytes": (c_sz, [c_i64]),
+    "yatt_gae_with_moments": (C.c_int, [c_p, c_p, c_p, c_p, c_i64, c_i64, c_f32, c_f32, c_p, c_p,
+                                        c_p, c_p, c_sz, c_p]),
     "yatt_gae": (C.c_int, [c_p, c_p, c_p, c_p, c_i64, c_i64, c_f32, c_f32, c_p, c_p, c_p, c_sz,
                            c_p]),
     "yatt_masked_moments_workspace_bytes": (c_sz, []),

@@ -143,14 +143,19 @@ struct GaeWs {
   uint32_t* ticket;
   uint4* rec;
   uint32_t* ends;
+  double* mom;  // [ntiles][3] masked (count, sum, sum^2) of the stored advantages
 };
 __host__ __device__ inline size_t gae_align(size_t x) { return (x + 15) & ~size_t(15); }
 __host__ __device__ inline GaeWs gae_ws(void* base, int64_t ntiles) {
   uint8_t* b = static_cast<uint8_t*>(base);
+  const size_t mom_off = gae_align(16 + 16 * size_t(ntiles) + 64 * size_t(ntiles));
   return GaeWs{reinterpret_cast<uint32_t*>(b), reinterpret_cast<uint4*>(b + 16),
-               reinterpret_cast<uint32_t*>(b + 16 + 16 * size_t(ntiles))};
+               reinterpret_cast<uint32_t*>(b + 16 + 16 * size_t(ntiles)),
+               reinterpret_cast<double*>(b + mom_off)};
 }
-size_t gae_ws_bytes(int64_t ntiles) { return gae_align(16 + 16 * size_t(ntiles) + 64 * size_t(ntiles)); }
+size_t gae_ws_bytes(int64_t ntiles) {
+  return gae_align(16 + 16 * size_t(ntiles) + 64 * size_t(ntiles)) + 24 * size_t(ntiles);
+}
 
 struct GaeArgs {
   const float* values;
@@ -240,7 +245,9 @@ __global__ void gae_mark_ends_kernel(const int64_t* cu, int64_t nseq, int64_t n_
 #ifndef YATT_GAE_MINB  // 6 CTAs/SM (80 regs, no spills): 59 us vs 64 us at 5 (96 regs)
 #define YATT_GAE_MINB 6
 #endif
-template <bool kVec>
+// kMom: also the masked moments (count, sum, sum^2) of the advantages it
+// stores, one fp64 partial per tile (whitening without a second pass).
+template <bool kVec, bool kMom>
 __global__ void __launch_bounds__(128, YATT_GAE_MINB) gae_warp_kernel(const GaeArgs g, GaeWs ws) {
   const int lane = threadIdx.x & 31;
   const double gamma = g.gamma, gl = g.gamma * g.lam;
@@ -379,6 +386,7 @@ __global__ void __launch_bounds__(128, YATT_GAE_MINB) gae_warp_kernel(const GaeA
   double A = ex.a * cA + ex.b * cV + ex.p;
   double Vn = ex.k * cV + ex.q;
   float ao[kGaeTpt], ro[kGaeTpt];
+  double mc = 0.0, ms = 0.0, mq = 0.0;
   if (plain) {
 #pragma unroll
     for (int j = kGaeTpt - 1; j >= 0; --j) {
@@ -387,7 +395,13 @@ __global__ void __launch_bounds__(128, YATT_GAE_MINB) gae_warp_kernel(const GaeA
       Vn = vv;
       ao[j] = float(A);
       ro[j] = float(A + vv);
+      if (kMom) {
+        const double af = double(ao[j]);
+        ms += af;
+        mq += af * af;
+      }
     }
+    if (kMom) mc = double(kGaeTpt);
   } else {
 #pragma unroll
     for (int j = kGaeTpt - 1; j >= 0; --j) {
@@ -402,6 +416,22 @@ __global__ void __launch_bounds__(128, YATT_GAE_MINB) gae_warp_kernel(const GaeA
       }
       ao[j] = float(A);
       ro[j] = float(A + vv);
+      if (kMom && (validm & bit)) {
+        const double af = double(ao[j]);
+        mc += 1.0;
+        ms += af;
+        mq += af * af;
+      }
+    }
+  }
+  if (kMom) {  // fixed-order warp reduction -> this tile's partial
+    mc = warp_sum(mc);
+    ms = warp_sum(ms);
+    mq = warp_sum(mq);
+    if (lane == 0) {
+      ws.mom[3 * t] = mc;
+      ws.mom[3 * t + 1] = ms;
+      ws.mom[3 * t + 2] = mq;
     }
   }
   if (kVec && insm == 0xffffu) {
@@ -594,10 +624,13 @@ size_t gae_workspace_bytes(int64_t n_tokens) {
 
 int gae_launch(const float* values, const float* rewards, const uint8_t* mask, const int64_t* cu,
                int64_t nseq, int64_t n_tokens, float gamma, float lam, float* adv, float* ret,
-               void* ws, size_t ws_bytes, cudaStream_t st) {
+               void* ws, size_t ws_bytes, cudaStream_t st, double* moments) {
   YATT_REQUIRE(nseq >= 0 && n_tokens >= 0, YATT_ERR_CONFIG, "gae: n_seqs and n_tokens must be >= 0");
   YATT_REQUIRE(gamma >= 0.f && lam >= 0.f, YATT_ERR_CONFIG, "gae: gamma/lam must be >= 0");
-  if (nseq == 0 || n_tokens == 0) return YATT_OK;
+  if (nseq == 0 || n_tokens == 0) {
+    if (moments) YATT_TRY_CUDA(cudaMemsetAsync(moments, 0, 3 * sizeof(double), st));
+    return YATT_OK;
+  }
   YATT_REQUIRE(values && rewards && cu && adv && ret, YATT_ERR_CONFIG, "gae: null pointer");
   const int64_t ntiles = ceil_div(n_tokens, kGaeWTile);
   YATT_REQUIRE(ws != nullptr && ws_bytes >= gae_ws_bytes(ntiles), YATT_ERR_WORKSPACE,
@@ -611,10 +644,20 @@ int gae_launch(const float* values, const float* rewards, const uint8_t* mask, c
   const GaeWs w = gae_ws(ws, ntiles);
   gae_mark_ends_kernel<<<unsigned(ceil_div(nseq, 256)), 256, 0, st>>>(cu, nseq, n_tokens, w.ends);
   const unsigned grid = unsigned(ceil_div(ntiles, 4));  // 4 warps = 4 tiles per CTA
+  if (moments) {
+    if (vec)
+      gae_warp_kernel<true, true><<<grid, 128, 0, st>>>(args, w);
+    else
+      gae_warp_kernel<false, true><<<grid, 128, 0, st>>>(args, w);
+    const int rc = check_launch("gae_kernel");
+    if (rc) return rc;
+    reduce_parts_kernel<3><<<1, 256, 0, st>>>(w.mom, int(ntiles), moments);
+    return check_launch("reduce_parts_kernel<3>");
+  }
   if (vec)
-    gae_warp_kernel<true><<<grid, 128, 0, st>>>(args, w);
+    gae_warp_kernel<true, false><<<grid, 128, 0, st>>>(args, w);
   else
-    gae_warp_kernel<false><<<grid, 128, 0, st>>>(args, w);
+    gae_warp_kernel<false, false><<<grid, 128, 0, st>>>(args, w);
   return check_launch("gae_kernel");
 }
 

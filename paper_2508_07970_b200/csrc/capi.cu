@@ -33,7 +33,7 @@ int grpo_adv_launch(const float*, int64_t, uint64_t, int32_t, float, int32_t, co
                     float*, cudaStream_t);
 int broadcast_launch(const float*, const int64_t*, int64_t, const uint8_t*, float*, cudaStream_t);
 int gae_launch(const float*, const float*, const uint8_t*, const int64_t*, int64_t, int64_t, float,
-               float, float*, float*, void*, size_t, cudaStream_t);
+               float, float*, float*, void*, size_t, cudaStream_t, double* moments = nullptr);
 size_t gae_workspace_bytes(int64_t);
 size_t moments_workspace_bytes();
 int masked_moments_launch(const float*, const uint8_t*, int64_t, double*, double*, cudaStream_t);
@@ -424,6 +424,19 @@ int yatt_gae(const float* values, const float* rewards, const uint8_t* mask, con
   YATT_ALIGNED("gae", ws, 16);
   return gae_launch(values, rewards, mask, cu, nseq, n_tokens, gamma, lam, adv, ret, ws, ws_bytes,
                     as_stream(stream));
+}
+
+int yatt_gae_with_moments(const float* values, const float* rewards, const uint8_t* mask,
+                          const int64_t* cu, int64_t nseq, int64_t n_tokens, float gamma,
+                          float lam, float* adv, float* ret, double* moments, void* ws,
+                          size_t ws_bytes, void* stream) {
+  YATT_ALIGNED4("gae_with_moments", values, rewards, adv, ret);
+  YATT_ALIGNED("gae_with_moments", cu, 8);
+  YATT_ALIGNED("gae_with_moments", ws, 16);
+  YATT_ALIGNED("gae_with_moments", moments, 8);
+  YATT_REQUIRE(moments != nullptr, YATT_ERR_CONFIG, "gae_with_moments: null moments");
+  return gae_launch(values, rewards, mask, cu, nseq, n_tokens, gamma, lam, adv, ret, ws, ws_bytes,
+                    as_stream(stream), moments);
 }
 
 size_t yatt_masked_moments_workspace_bytes(void) { return moments_workspace_bytes(); }

@@ -511,10 +511,16 @@ std::size_t gae_workspace_bytes(std::int64_t n_tokens) { return yatt_gae_workspa
 
 void gae(const float* values, const float* rewards, const std::uint8_t* mask,
          const std::int64_t* cu, std::int64_t n_seqs, std::int64_t n_tokens, const GaeConfig& c,
-         float* adv, float* ret, void* ws, std::size_t ws_bytes, void* stream) {
+         float* adv, float* ret, void* ws, std::size_t ws_bytes, void* stream,
+         double* moments) {
   c.validate();
-  detail::throw_status(yatt_gae(values, rewards, mask, cu, n_seqs, n_tokens, c.gamma, c.lam, adv,
-                                ret, ws, ws_bytes, stream));
+  if (moments)
+    detail::throw_status(yatt_gae_with_moments(values, rewards, mask, cu, n_seqs, n_tokens,
+                                               c.gamma, c.lam, adv, ret, moments, ws, ws_bytes,
+                                               stream));
+  else
+    detail::throw_status(yatt_gae(values, rewards, mask, cu, n_seqs, n_tokens, c.gamma, c.lam,
+                                  adv, ret, ws, ws_bytes, stream));
 }
 
 void PolicyLossConfig::validate() const {

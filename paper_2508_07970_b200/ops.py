@@ -174,7 +174,10 @@ def broadcast_to_tokens(sample_vals: torch.Tensor, cu_seqlens: torch.Tensor, n_t
 
 # ------------------------------------------------------------------ A3 ----
 def gae(values: torch.Tensor, rewards: torch.Tensor, cu_seqlens: torch.Tensor,
-        mask: torch.Tensor | None = None, gamma: float = 1.0, lam: float = 0.95):
+        mask: torch.Tensor | None = None, gamma: float = 1.0, lam: float = 0.95,
+        return_moments: bool = False):
+    """(advantages, returns) — and with return_moments the masked moments
+    {count, sum, sum_sq} (fp64) of the advantages, from the same pass."""
     _dev(values, torch.float32, "values")
     _dev(rewards, torch.float32, "rewards")
     _dev(cu_seqlens, torch.int64, "cu_seqlens")
@@ -183,6 +186,12 @@ def gae(values: torch.Tensor, rewards: torch.Tensor, cu_seqlens: torch.Tensor,
     n = values.numel()
     wsb = lib().yatt_gae_workspace_bytes(n)
     ws = torch.empty((max(wsb, 16),), dtype=torch.uint8, device=values.device)
+    if return_moments:
+        mom = torch.empty((3,), dtype=torch.float64, device=values.device)
+        check(lib().yatt_gae_with_moments(_p(values), _p(rewards), _p(_mask(mask)),
+                                          _p(cu_seqlens), cu_seqlens.numel() - 1, n, gamma, lam,
+                                          _p(adv), _p(ret), _p(mom), _p(ws), wsb, _st()))
+        return adv, ret, mom
     check(lib().yatt_gae(_p(values), _p(rewards), _p(_mask(mask)), _p(cu_seqlens),
                          cu_seqlens.numel() - 1, n, gamma, lam, _p(adv), _p(ret), _p(ws), wsb,
                          _st()))

@@ -273,3 +273,23 @@ def test_ops_reject_strided_and_mistyped_inputs(cuda):
                           torch.zeros(1, dtype=torch.int32, device=cuda),
                           torch.zeros(2, dtype=torch.int64, device=cuda),
                           torch.zeros(1, dtype=torch.int64, device=cuda), 1, x[:16])
+
+
+@pytest.mark.parametrize("masked", [False, True])
+def test_gae_fused_whitening_moments(cuda, masked):
+    """yatt_gae_with_moments: the advantages' masked moments come out of the
+    scan itself and equal yatt_masked_moments over the stored advantages."""
+    rng = np.random.default_rng(5)
+    lens = rng.integers(1, 9000, size=300)
+    cu = torch.as_tensor(np.concatenate([[0], np.cumsum(lens)]).astype(np.int64), device=cuda)
+    n = int(cu[-1])
+    v = ops.synth_floats(7, 106, 0, n, "value", device=cuda)
+    r = (ops.synth_floats(7, 111, 0, n, "kl", device=cuda) * 4 - 0.5).contiguous()
+    m = torch.as_tensor((rng.random(n) < 0.8).astype(np.uint8), device=cuda) if masked else None
+    adv, ret, mom = ops.gae(v, r, cu, m, 0.99, 0.95, return_moments=True)
+    adv2, ret2 = ops.gae(v, r, cu, m, 0.99, 0.95)
+    assert torch.equal(adv, adv2) and torch.equal(ret, ret2)
+    ref = ops.masked_moments(adv, m).cpu().numpy()
+    got = mom.cpu().numpy()
+    assert got[0] == ref[0]
+    assert np.all(np.abs(got - ref) <= 1e-12 * np.abs(ref) + 1e-9)

@@ -79,8 +79,8 @@ def config4():
             n = min(chunk, ntok - c0)
             pol, ref, tgt = bufs[(c0 // chunk) % 2]
             ops.token_stats(pol[:n], ref[:n], tgt[:n], None, "k3", out=stats[:, c0:c0 + n])
-        adv, ret = ops.gae(values, rewards, cu, None, 1.0, 0.95)
-        ops.whiten(adv, ops.masked_moments(adv))
+        adv, ret, mom = ops.gae(values, rewards, cu, None, 1.0, 0.95, return_moments=True)
+        ops.whiten(adv, mom)  # whitening statistics from the GAE pass itself
         ops.policy_loss(stats[0], old, adv, stats[3], stats[2], None, None, cfg, ws)
     ms = timeit(run, iters=2)
     return {"config": "configs[3] PPO 2048 packed seqs U[1,8192], V=152064, GAE g=1 l=0.95",
