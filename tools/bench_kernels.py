@@ -101,6 +101,14 @@ def main():
     m = torch.ones(n, dtype=torch.uint8, device=dev)
     ms = timeit(lambda: ops.gae(v, rw, cu, m, 1.0, 0.95))
     report("gae (2048 packed seqs)", ms, n * 17, n, "tokens")
+    ms = timeit(lambda: ops.gae(v, rw, cu, m, 1.0, 0.95, return_moments=True))
+    report("gae + whitening moments fused (one pass)", ms, n * 17, n, "tokens")
+
+    def gae_then_moments():
+        a, _ = ops.gae(v, rw, cu, m, 1.0, 0.95)
+        ops.masked_moments(a, m)
+    ms = timeit(gae_then_moments)
+    report("gae then masked_moments (two passes)", ms, n * 22, n, "tokens")
     mom = ops.masked_moments(v, m)
     ms = timeit(lambda: ops.masked_moments(v, m))
     report("masked_moments", ms, n * 5, n, "tokens")
