@@ -12,7 +12,8 @@ achieved algorithmic GB/s vs the measured HBM peak.  One JSON line per op.
   R3  shard_round       16,384 samples, 8 controller shards, one launch
   R10 sort_order_desc   16,384 lengths
 Timing: CUDA-graph replay between CUDA events (no host overhead), L2 flushed
-before each replay, median of 20 after 3 warm-ups, inputs resident.
+before each replay (write, then a read that cleans the dirty lines), median
+of 20 after 3 warm-ups, inputs resident.
 """
 import json
 import statistics
@@ -30,17 +31,21 @@ PEAK = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").
     "hbm_gbs"] if (Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").exists() else 6650.0
 
 
-_FLUSH = None
+_FLUSH = _FLUSH_RD = None
 
 
 def timeit(fn, iters=20, warm=3):
     """Device time of one call: the call is captured once into a CUDA graph
     (so host-side Python/ctypes overhead is not timed) and replayed between
-    CUDA events, with L2 flushed (256 MB write) before every replay.  Ops that
-    cannot be captured (host syncs inside) fall back to eager timing."""
-    global _FLUSH
+    CUDA events, with L2 flushed before every replay: a 256 MB write, then a
+    256 MB read of a second buffer, so the write-back of the dirty lines the
+    write leaves happens before the timed region (otherwise the timed kernel
+    pays up to 126 MB of write-back).  Ops that cannot be captured (host syncs
+    inside) fall back to eager timing."""
+    global _FLUSH, _FLUSH_RD
     if _FLUSH is None:
         _FLUSH = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        _FLUSH_RD = torch.ones(64 << 20, dtype=torch.float32, device=dev)
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
@@ -62,6 +67,7 @@ def timeit(fn, iters=20, warm=3):
     ts = []
     for _ in range(iters):
         _FLUSH.zero_()
+        _FLUSH_RD.sum()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         run()
@@ -80,6 +86,13 @@ def report(name, ms, alg_bytes, units, unit_name, **extra):
 
 def main():
     seed = 20250814
+    # harness calibration: a plain device copy (torch) at the small kernels' sizes
+    for mb in (42, 150):
+        src = torch.ones(mb << 17, dtype=torch.float32, device=dev)  # mb/2 MB each way
+        dst = torch.empty_like(src)
+        ms = timeit(lambda: dst.copy_(src))
+        report(f"harness: torch copy_ {mb} MB moved", ms, 2 * src.numel() * 4, src.numel(), "floats")
+        del src, dst
     # A2
     for n, G in [(2048, 8), (16384, 16)]:
         r = ops.synth_floats(seed, 105, 0, n, "reward", G, device=dev)
