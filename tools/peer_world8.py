@@ -1,0 +1,102 @@
+"""World-8 check of the NVLink peer-memory collectives on a box with fewer GPUs.
+
+The driver's scaling run goes to 8 ranks, one per GPU; gpurun offers at most 4
+GPUs, and NCCL refuses two ranks on one GPU.  This script oversubscribes:
+rank r runs on GPU r % ngpus with gloo for the plumbing (handle exchange,
+barriers), so the world-8 code of yatt_peer_* runs for real: 8 mapped IPC
+buffers, 8-way rank-order sums, the epoch-parity slot banks, the scan.  Two
+processes on one GPU time-slice (no MPS), so nothing here is timed.
+
+Checks (vs single-process results, fixed rank order => bit-exact where the
+math is exact):
+  * allreduce_f64 of integer-valued doubles, 50 back-to-back calls;
+  * scan_i64: exclusive prefix + total of per-rank counters;
+  * policy_loss over 8 prompt-group shards == the full batch on one rank
+    (max rel 1e-12: fp64 reassociation only);
+  * the same under CUDA-graph replay.
+Run: torchrun --nproc-per-node 8 tools/peer_world8.py   -> "peer world8 ok".
+"""
+import os
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from paper_2508_07970_b200 import ops, ranks  # noqa: E402
+
+P, R, T, V, SEED = 16, 8, 64, 4096, 20250814
+
+
+def loss_inputs(g0, g1, dev):
+    rows = (g1 - g0) * R * T
+    pol, ref, tgt = ops.synth_logits(SEED, g0 * R * T, rows, V, device=dev)
+    logp, rlogp, ent, kl = ops.token_stats(pol, ref, tgt, None, "k3")
+    rewards = ops.synth_floats(SEED, 105, g0 * R, (g1 - g0) * R, "reward", R, device=dev)
+    adv = ops.grpo_advantages(rewards, R, 1e-6, True, g0 * R)
+    cu = torch.arange((g1 - g0) * R + 1, dtype=torch.int64, device=dev) * T
+    tadv = ops.broadcast_to_tokens(adv, cu, rows)
+    old = ops.synth_floats(SEED, 104, g0 * R * T, rows, "old_delta", base=logp, device=dev)
+    return logp, old, tadv, kl, ent
+
+
+def main():
+    dist.init_process_group("gloo")
+    world, rank = dist.get_world_size(), dist.get_rank()
+    ngpu = torch.cuda.device_count()
+    torch.cuda.set_device(rank % ngpu)
+    dev = torch.device("cuda", rank % ngpu)
+    peer = ranks.PeerGroup(world, rank)
+
+    tri = world * (world + 1) / 2
+    y = peer.allreduce_f64(torch.arange(1, 9, dtype=torch.float64, device=dev) * (rank + 1))
+    assert torch.equal(y, torch.arange(1, 9, dtype=torch.float64, device=dev) * tri), y
+    outs = []
+    for k in range(50):
+        x = torch.full((5,), float(k * world + rank), dtype=torch.float64, device=dev)
+        outs.append(peer.allreduce_f64(x))
+    torch.cuda.synchronize()
+    for k, o in enumerate(outs):
+        assert torch.all(o == float(sum(k * world + r for r in range(world)))), (rank, k, o)
+
+    cnt = torch.tensor([rank + 1, 2 * rank, 7], dtype=torch.int64, device=dev)
+    pre, tot = peer.scan_i64(cnt)
+    assert pre.tolist() == [sum(r + 1 for r in range(rank)), sum(2 * r for r in range(rank)),
+                            7 * rank], pre
+    assert tot.tolist() == [tri, world * (world - 1), 7 * world], tot
+
+    g0, g1 = ranks.shard_groups(P, world, rank)
+    li = loss_inputs(g0, g1, dev)
+    fused = peer.policy_loss(*li)
+    full = ops.policy_loss(*loss_inputs(0, P, dev))
+    torch.cuda.synchronize()
+    rel = ((fused - full).abs() / (full.abs() + 1e-12)).max().item()
+    assert rel <= 1e-12, (rank, rel, fused.tolist(), full.tolist())
+
+    ws = ops.LossWorkspace(dev)
+    gs = torch.empty(8, dtype=torch.float64, device=dev)
+    s_ = torch.cuda.Stream()
+    s_.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s_):
+        peer.policy_loss(*li, workspace=ws, sums=gs)
+    torch.cuda.current_stream().wait_stream(s_)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        peer.policy_loss(*li, workspace=ws, sums=gs)
+    for _ in range(3):
+        gs.zero_()
+        graph.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(gs, fused), (rank, gs.tolist(), fused.tolist())
+    assert peer.status() == 0
+    dist.barrier()
+    peer.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    if rank == 0:
+        print(f"peer world{world} ok on {ngpu} GPUs")
+
+
+if __name__ == "__main__":
+    main()
