@@ -9,6 +9,7 @@ of the source + flags under ``build/``.
 from __future__ import annotations
 
 import hashlib
+import re
 import os
 import shutil
 import subprocess
@@ -41,6 +42,8 @@ def nvcc() -> str:
 def _digest(path: Path, flags: list[str]) -> str:
     h = hashlib.sha256()
     h.update(path.read_bytes())
+    for inc in re.findall(r'#include "(\w+\.cu)"', path.read_text(errors="ignore")):
+        h.update((path.parent / inc).read_bytes())  # e.g. token_stats_small.cu
     for dep in sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "yatt_cuda.h"]:
         h.update(dep.read_bytes())
     for dep in sorted((ROOT / "include" / "yatt").glob("*.hpp")):

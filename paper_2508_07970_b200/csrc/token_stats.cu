@@ -35,6 +35,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -44,14 +45,23 @@ namespace {
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kThreads = kConsumers + 32;  // + producer warp
+#ifdef YATT_A1_SMALL_TU  // token_stats_small.cu: the ring shape for small vocabularies
+#define YATT_A1_TILE YATT_A1_SMALL_TILE
+#define YATT_A1_STAGES YATT_A1_SMALL_STAGES
+#define YATT_A1_MINB YATT_A1_SMALL_MINB
+#endif
 #ifndef YATT_A1_TILE
 #define YATT_A1_TILE 8192
 #endif
 #ifndef YATT_A1_STAGES
 #define YATT_A1_STAGES 3
 #endif
+#ifndef YATT_A1_MINB
+#define YATT_A1_MINB 2
+#endif
 constexpr int kTile = YATT_A1_TILE;        // bf16 elements per tensor per stage
 constexpr int kStages = YATT_A1_STAGES;
+constexpr int kMinBlocks = YATT_A1_MINB;   // resident CTAs per SM (grid = kMinBlocks x SMs)
 constexpr int kVecPerTile = kTile / 8;                  // 16-byte vectors
 constexpr int kVecPerThread = kVecPerTile / kConsumers;  // full-tile unroll
 constexpr float kLog2e = 1.4426950408889634f;
@@ -82,7 +92,10 @@ struct __align__(16) SmemTail {
 constexpr size_t kRingBytes = size_t(kStages) * 2 * kTile * sizeof(uint16_t);
 constexpr size_t kSmemBytes = kRingBytes + sizeof(SmemTail);
 
-struct Params {
+}  // namespace
+
+// Shared by token_stats.cu and token_stats_small.cu (same definition).
+struct A1Params {
   const uint16_t* pol;
   const uint16_t* ref;
   const int32_t* tgt;
@@ -95,6 +108,9 @@ struct Params {
   float* ent;
   float* kl;
 };
+
+namespace {
+
 
 // Per-thread online state for one row.  Element pairs (the two bf16 of one
 // 32-bit word) are processed with Blackwell's packed f32x2 FMA/ADD
@@ -324,7 +340,7 @@ __device__ __forceinline__ bool partial_finite(const RowPartial& q) {
 }
 
 // fp64 epilogue of one row from its combined partial and target logits.
-__device__ __forceinline__ void emit_row(const Params& p, int64_t row, const RowPartial& q,
+__device__ __forceinline__ void emit_row(const A1Params& p, int64_t row, const RowPartial& q,
                                          double xy, double zy) {
   const double l2s = log2(double(q.s));
   const double l2q = log2(double(q.sq));
@@ -351,7 +367,7 @@ __device__ __forceinline__ void emit_row(const Params& p, int64_t row, const Row
 // kEdges: V % 8 != 0 — rows are staged as 16-byte-aligned supersets and the
 // edge vectors masked; false compiles the plain V % 8 == 0 kernel.
 template <bool kFull, bool kEdges>
-__global__ void __launch_bounds__(kThreads, 2) token_stats_kernel(const Params p) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) token_stats_kernel(const A1Params p) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint16_t* ring = reinterpret_cast<uint16_t*>(smem);
   SmemTail* tail = reinterpret_cast<SmemTail*>(smem + kRingBytes);
@@ -543,7 +559,7 @@ __device__ __forceinline__ uint4 load8_any(const uint16_t* row, int64_t e0, int6
 // logp, 4 B/row).  kGeneric = true: every row, for vocabularies or tensors
 // the TMA path cannot take (V % 8 != 0 or unaligned), with scalar loads.
 template <bool kFull, bool kGeneric>
-__global__ void __launch_bounds__(kConsumers) token_stats_fixup_kernel(const Params p) {
+__global__ void __launch_bounds__(kConsumers) token_stats_fixup_kernel(const A1Params p) {
   __shared__ int64_t list[kConsumers];
   __shared__ int count;
   __shared__ RowPartial red[kConsumerWarps];
@@ -611,51 +627,16 @@ __global__ void __launch_bounds__(kConsumers) token_stats_fixup_kernel(const Par
 
 }  // namespace
 
-int token_stats_launch(const uint16_t* pol, const uint16_t* ref, const int32_t* tgt,
-                       const uint8_t* mask, int64_t rows, int32_t vocab, int32_t kl_mode,
-                       float* logp, float* ref_logp, float* ent, float* kl, cudaStream_t st) {
-  YATT_REQUIRE(vocab > 0, YATT_ERR_CONFIG, "token_stats: vocab must be positive (got %d)", vocab);
-  YATT_REQUIRE(rows >= 0, YATT_ERR_CONFIG, "token_stats: rows must be >= 0");
-  YATT_REQUIRE(kl_mode >= YATT_KL_K1 && kl_mode <= YATT_KL_FULL, YATT_ERR_CONFIG,
-               "token_stats: unknown kl_mode %d", kl_mode);
-  if (rows == 0) return YATT_OK;
-  YATT_REQUIRE(logp != nullptr, YATT_ERR_CONFIG, "token_stats: logp output is required");
-  YATT_REQUIRE(pol && ref && tgt, YATT_ERR_CONFIG, "token_stats: null input pointer");
-  Params p{pol, ref, tgt, mask, rows, vocab, kl_mode, logp, ref_logp, ent, kl};
-  // The TMA path needs 16-byte-aligned tensor bases; any vocab: each row is
-  // staged as its aligned superset.  With V % 8 != 0 the last row's superset
-  // could end past the tensor, so that one row takes the generic kernel.
-  const bool tma_ok = (reinterpret_cast<uintptr_t>(pol) & 15) == 0 &&
-                      (reinterpret_cast<uintptr_t>(ref) & 15) == 0 && (vocab % 8 == 0 || rows > 1);
-  if (tma_ok && vocab % 8 != 0) {
-    Params last = p;
-    const int64_t off = (rows - 1) * int64_t(vocab);
-    last.pol = pol + off;
-    last.ref = ref + off;
-    last.tgt = tgt + (rows - 1);
-    last.mask = mask ? mask + (rows - 1) : nullptr;
-    last.rows = 1;
-    last.logp = logp + (rows - 1);
-    last.ref_logp = ref_logp ? ref_logp + (rows - 1) : nullptr;
-    last.ent = ent ? ent + (rows - 1) : nullptr;
-    last.kl = kl ? kl + (rows - 1) : nullptr;
-    if (kl_mode == YATT_KL_FULL)
-      token_stats_fixup_kernel<true, true><<<1, kConsumers, 0, st>>>(last);
-    else
-      token_stats_fixup_kernel<false, true><<<1, kConsumers, 0, st>>>(last);
-    const int rc = check_launch("token_stats_generic_kernel");
-    if (rc) return rc;
-    p.rows = rows - 1;
-  }
-  if (!tma_ok) {  // generic path: unaligned tensors, scalar loads
-    const int ggrid = int(min64(ceil_div(rows, 8), int64_t(num_sms()) * 8));
-    if (kl_mode == YATT_KL_FULL)
-      token_stats_fixup_kernel<true, true><<<ggrid, kConsumers, 0, st>>>(p);
-    else
-      token_stats_fixup_kernel<false, true><<<ggrid, kConsumers, 0, st>>>(p);
-    return check_launch("token_stats_generic_kernel");
-  }
-  const int grid = int(min64(p.rows, int64_t(2) * num_sms()));
+#ifdef YATT_A1_SMALL_TU
+#define YATT_A1_RING token_stats_ring_small
+#else
+#define YATT_A1_RING token_stats_ring_large
+#endif
+// The TMA-ring path with this translation unit's ring shape (16-B-aligned
+// tensors; with V % 8 != 0 the caller has peeled off the last row).
+int YATT_A1_RING(const A1Params& p, cudaStream_t st) {
+  const int32_t vocab = p.V, kl_mode = p.kl_mode;
+  const int grid = int(min64(p.rows, int64_t(kMinBlocks) * num_sms()));
   {
     const bool edges = vocab % 8 != 0, full = kl_mode == YATT_KL_FULL;
     const void* k = edges ? (full ? reinterpret_cast<const void*>(token_stats_kernel<true, true>)
@@ -685,5 +666,73 @@ int token_stats_launch(const uint16_t* pol, const uint16_t* ref, const int32_t* 
     token_stats_fixup_kernel<false, false><<<fgrid, kConsumers, 0, st>>>(p);
   return check_launch("token_stats_fixup_kernel");
 }
+
+#ifndef YATT_A1_SMALL_TU
+int token_stats_ring_small(const A1Params& p, cudaStream_t st);  // token_stats_small.cu
+
+// Vocabularies up to this take the small ring shape (4,096-element tiles x 4
+// stages, 3 CTAs/SM); larger ones the 8,192 x 3, 2 CTAs/SM shape.  Measured
+// (B200, k3, L2 flushed), large vs small shape: V=8,192 3.58 vs 3.92 TB/s,
+// 32,000 5.76 vs 5.95, 50,264 5.76 vs 6.18, 65,536 6.50 vs 6.29, 100,000 6.50
+// vs 6.34, 128,256 6.64 vs 6.42, 152,064 6.84 vs 6.64.  YATT_A1_SMALL_VMAX
+// overrides (measurement only).
+#ifndef YATT_A1_SMALL_VMAX
+#define YATT_A1_SMALL_VMAX 60000
+#endif
+int a1_small_vmax() {
+  static const int v = [] {
+    const char* e = std::getenv("YATT_A1_SMALL_VMAX");
+    return e ? std::atoi(e) : YATT_A1_SMALL_VMAX;
+  }();
+  return v;
+}
+
+int token_stats_launch(const uint16_t* pol, const uint16_t* ref, const int32_t* tgt,
+                       const uint8_t* mask, int64_t rows, int32_t vocab, int32_t kl_mode,
+                       float* logp, float* ref_logp, float* ent, float* kl, cudaStream_t st) {
+  YATT_REQUIRE(vocab > 0, YATT_ERR_CONFIG, "token_stats: vocab must be positive (got %d)", vocab);
+  YATT_REQUIRE(rows >= 0, YATT_ERR_CONFIG, "token_stats: rows must be >= 0");
+  YATT_REQUIRE(kl_mode >= YATT_KL_K1 && kl_mode <= YATT_KL_FULL, YATT_ERR_CONFIG,
+               "token_stats: unknown kl_mode %d", kl_mode);
+  if (rows == 0) return YATT_OK;
+  YATT_REQUIRE(logp != nullptr, YATT_ERR_CONFIG, "token_stats: logp output is required");
+  YATT_REQUIRE(pol && ref && tgt, YATT_ERR_CONFIG, "token_stats: null input pointer");
+  A1Params p{pol, ref, tgt, mask, rows, vocab, kl_mode, logp, ref_logp, ent, kl};
+  // The TMA path needs 16-byte-aligned tensor bases; any vocab: each row is
+  // staged as its aligned superset.  With V % 8 != 0 the last row's superset
+  // could end past the tensor, so that one row takes the generic kernel.
+  const bool tma_ok = (reinterpret_cast<uintptr_t>(pol) & 15) == 0 &&
+                      (reinterpret_cast<uintptr_t>(ref) & 15) == 0 && (vocab % 8 == 0 || rows > 1);
+  if (tma_ok && vocab % 8 != 0) {
+    A1Params last = p;
+    const int64_t off = (rows - 1) * int64_t(vocab);
+    last.pol = pol + off;
+    last.ref = ref + off;
+    last.tgt = tgt + (rows - 1);
+    last.mask = mask ? mask + (rows - 1) : nullptr;
+    last.rows = 1;
+    last.logp = logp + (rows - 1);
+    last.ref_logp = ref_logp ? ref_logp + (rows - 1) : nullptr;
+    last.ent = ent ? ent + (rows - 1) : nullptr;
+    last.kl = kl ? kl + (rows - 1) : nullptr;
+    if (kl_mode == YATT_KL_FULL)
+      token_stats_fixup_kernel<true, true><<<1, kConsumers, 0, st>>>(last);
+    else
+      token_stats_fixup_kernel<false, true><<<1, kConsumers, 0, st>>>(last);
+    const int rc = check_launch("token_stats_generic_kernel");
+    if (rc) return rc;
+    p.rows = rows - 1;
+  }
+  if (!tma_ok) {  // generic path: unaligned tensors, scalar loads
+    const int ggrid = int(min64(ceil_div(rows, 8), int64_t(num_sms()) * 8));
+    if (kl_mode == YATT_KL_FULL)
+      token_stats_fixup_kernel<true, true><<<ggrid, kConsumers, 0, st>>>(p);
+    else
+      token_stats_fixup_kernel<false, true><<<ggrid, kConsumers, 0, st>>>(p);
+    return check_launch("token_stats_generic_kernel");
+  }
+  return vocab <= a1_small_vmax() ? token_stats_ring_small(p, st) : token_stats_ring_large(p, st);
+}
+#endif
 
 }  // namespace yattb
