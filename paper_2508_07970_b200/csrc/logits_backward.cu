@@ -34,13 +34,23 @@ namespace {
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kThreads = kConsumers + 32;
-constexpr int kTile = 8192;
+#ifndef YATT_BWD_TILE
+#define YATT_BWD_TILE 8192
+#endif
+#ifndef YATT_BWD_STAGES
+#define YATT_BWD_STAGES 6  // policy-only (k1/k2/k3) ring; FULL stages both tensors: half
+#endif
+#ifndef YATT_BWD_MINB
+#define YATT_BWD_MINB 2
+#endif
+constexpr int kTile = YATT_BWD_TILE;
+constexpr int kMinBlocks = YATT_BWD_MINB;
 // Ring depth: ~96 KB in flight per CTA either way (policy-only tiles are half
 // the size, so twice the stages).
-constexpr int kMaxStages = 6;
+constexpr int kMaxStages = YATT_BWD_STAGES;
 template <bool kFull>
 constexpr int stages_of() {
-  return kFull ? 3 : 6;
+  return kFull ? YATT_BWD_STAGES / 2 : YATT_BWD_STAGES;
 }
 constexpr int kVecPerTile = kTile / 8;
 constexpr int kVecPerThread = kVecPerTile / kConsumers;
@@ -129,7 +139,7 @@ __device__ __forceinline__ void store_grad(uint16_t* gs, int64_t j, uint4 g, int
 // kEdges: V % 8 != 0 — rows staged as 16-byte-aligned supersets (as in A1);
 // the gradient tensor has the same layout, so interior vectors stay aligned.
 template <bool kFull, bool kEdges>
-__global__ void __launch_bounds__(kThreads, 2) logits_backward_kernel(const GradParams p) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) logits_backward_kernel(const GradParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int kPerStage = kFull ? 2 : 1;
   constexpr int kStages = stages_of<kFull>();
@@ -414,7 +424,7 @@ int logits_backward_launch(const uint16_t* pol, const uint16_t* ref, const int32
     if (rc) return rc;
     prm.rows = rows - 1;
   }
-  const int grid = int(min64(prm.rows, int64_t(2) * num_sms()));
+  const int grid = int(min64(prm.rows, int64_t(kMinBlocks) * num_sms()));
   if (full_kl) {
     constexpr size_t smem = size_t(stages_of<true>()) * 2 * kTile * 2 + sizeof(BwdTail);
     const void* k = edges ? reinterpret_cast<const void*>(logits_backward_kernel<true, true>)

@@ -195,23 +195,25 @@ def main():
     l32 = torch.tensor(lens, dtype=torch.int32, device=dev)
     ms = timeit(lambda: ops.sort_order_desc(l32))
     report("sort_order_desc n=16384", ms, ns * 8, ns, "samples")
-    # §8f #1 backward into the logits: one prompt group, V = 152,064
+    # §8f #1 backward into the logits: one prompt group at V = 152,064; V = 32,000
     del srcs, dsts
     torch.cuda.empty_cache()
-    rows, V = 32768, 152064
-    pol, ref, tgt = ops.synth_logits(seed, 0, rows, V, device=dev)
-    lp, rl, en, kl = ops.token_stats(pol, ref, tgt, None, "k3")
-    old = ops.synth_floats(seed, 104, 0, rows, "old_delta", base=lp, device=dev)
-    a = ops.synth_floats(seed, 108, 0, rows, "adv", device=dev)
-    grad = torch.empty_like(pol)
-    for mode in ["k3", "full"]:
-        kl_m = ops.token_stats(pol, ref, tgt, None, mode)[3]
-        ms = timeit(lambda: ops.logits_grad(pol, ref, tgt, lp, rl, old, a, en, kl_m, None, None,
-                                            ops.loss_config(entropy_coef=0.001), mode,
-                                            float(rows), grad), iters=10)
-        per_row = (6 if mode == "full" else 4) * V + 32
-        report(f"logits_grad {mode} (coef + backward) 32768 x {V}", ms, rows * per_row, rows,
-               "tokens")
+    for rows, V in [(32768, 152064), (65536, 32000)]:
+        pol, ref, tgt = ops.synth_logits(seed, 0, rows, V, device=dev)
+        lp, rl, en, kl = ops.token_stats(pol, ref, tgt, None, "k3")
+        old = ops.synth_floats(seed, 104, 0, rows, "old_delta", base=lp, device=dev)
+        a = ops.synth_floats(seed, 108, 0, rows, "adv", device=dev)
+        grad = torch.empty_like(pol)
+        for mode in ["k3", "full"]:
+            kl_m = ops.token_stats(pol, ref, tgt, None, mode)[3]
+            ms = timeit(lambda: ops.logits_grad(pol, ref, tgt, lp, rl, old, a, en, kl_m, None, None,
+                                                ops.loss_config(entropy_coef=0.001), mode,
+                                                float(rows), grad), iters=10)
+            per_row = (6 if mode == "full" else 4) * V + 32
+            report(f"logits_grad {mode} (coef + backward) {rows} x {V}", ms, rows * per_row, rows,
+                   "tokens")
+        del pol, ref, tgt, grad
+        torch.cuda.empty_cache()
 
 
 if __name__ == "__main__":
