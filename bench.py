@@ -127,8 +127,11 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- CPU arm ----
+_CPU_SAMPLES = {}
+
+
 def cpu_experience_rate(sample_rows: int | None = None, threads: int | None = None,
-                        budget_s: float = 12.0):
+                        budget_s: float = 12.0, repeat: bool = True):
     """Oracle (fp64 CPU restatement) of the same per-token path on a bounded
     sample: A1 over `rows` rows of V=152,064 + A2 over their samples + A4."""
     from oracle import oracle as O
@@ -136,27 +139,44 @@ def cpu_experience_rate(sample_rows: int | None = None, threads: int | None = No
     uniq = 64
     pol_u, ref_u, tgt_u = O.synth_logits(SEED, 0, uniq, VOCAB)
 
-    def run(rows):
+    def prepare(rows):
+        if (rows, threads) in _CPU_SAMPLES:
+            return _CPU_SAMPLES[(rows, threads)]
+        _CPU_SAMPLES.clear()  # one prepared sample at a time (host memory)
         reps = -(-rows // uniq)
         pol = np.ascontiguousarray(np.tile(pol_u, (reps, 1))[:rows])
         ref = np.ascontiguousarray(np.tile(ref_u, (reps, 1))[:rows])
         tgt = np.ascontiguousarray(np.tile(tgt_u, reps)[:rows])
         n_samples = max(1, rows // T) if rows >= T else 1
         rewards = O.synth_floats(SEED, 105, 0, max(n_samples, RESPONSES), "reward", RESPONSES)
-        t0 = time.perf_counter()
-        st = O.token_stats(pol, ref, tgt, None, "k3", threads=threads)
-        adv_s = O.grpo_advantages(rewards, RESPONSES)
-        adv_t = np.repeat(adv_s, -(-rows // len(adv_s)))[:rows].astype(np.float32)
-        old = (st[0] + O.synth_floats(SEED, 104, 0, rows, "old_delta")).astype(np.float32)
-        O.policy_loss(st[0], old, adv_t, st[3], st[2])
-        return time.perf_counter() - t0
+        old_delta = O.synth_floats(SEED, 104, 0, rows, "old_delta")
+
+        def once():
+            t0 = time.perf_counter()
+            st = O.token_stats(pol, ref, tgt, None, "k3", threads=threads)
+            adv_s = O.grpo_advantages(rewards, RESPONSES)
+            adv_t = np.repeat(adv_s, -(-rows // len(adv_s)))[:rows].astype(np.float32)
+            old = (st[0] + old_delta).astype(np.float32)
+            O.policy_loss(st[0], old, adv_t, st[3], st[2])
+            return time.perf_counter() - t0
+        _CPU_SAMPLES[(rows, threads)] = once
+        return once
 
     probe = 128
-    dt = run(probe)
+    dt = prepare(probe)()
+    # host memory caps one pass at 16,384 rows (~10 GB of tiled bf16 logits);
+    # passes repeat over the same rows until ~budget_s of CPU work is done
     rows = sample_rows or int(min(16384, max(probe, probe * budget_s / max(dt, 1e-6))))
-    dt = run(rows) if rows != probe else dt
-    return {"value": rows / dt, "unit": "tokens/s", "cores": threads, "kind": "port",
-            "sample": f"{rows} rows x V={VOCAB} (A1 fp64 + GRPO adv + loss), {dt:.2f} s"}
+    once = prepare(rows) if rows != probe else None
+    passes, total = 0, 0.0
+    if once is None:
+        passes, total = 1, dt
+    while once is not None and (passes == 0 or (repeat and total < 0.8 * budget_s and passes < 32)):
+        total += once()
+        passes += 1
+    return {"value": rows * passes / total, "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": f"{passes} pass(es) over {rows} rows x V={VOCAB} "
+                      f"(A1 fp64 + GRPO adv + loss), {total:.2f} s"}
 
 
 def _run_json(cmd):
@@ -203,7 +223,7 @@ def run_reference(args):
         return 0
     vals = []
     for _ in range(args.warmup):
-        cpu_experience_rate(sample_rows=256)
+        cpu_experience_rate(sample_rows=256, repeat=False)
     last = None
     for _ in range(args.steps):
         last = cpu_experience_rate(budget_s=args.ref_budget_s)
