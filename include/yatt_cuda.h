@@ -371,6 +371,26 @@ int yatt_logits_backward(const uint16_t* d_policy_logits,
                          const float* d_coef, int32_t full_kl, uint16_t* d_grad,
                          void* stream);
 
+/* Training side, fused: the policy loss terms AND d(loss)/d(policy logits)  */
+/* in one kernel (A1 on the policy logits only + A4's per-token coefficients */
+/* + the backward above).  Each row is streamed twice, the second read from  */
+/* L2: HBM bytes 2V read + 2V written per row instead of 6V for              */
+/* yatt_token_stats (policy only) + yatt_logits_backward.  The reference     */
+/* log-probs come from the experience stage (d_ref_logp, per token; NULL =   */
+/* no KL term).  kl_mode K1/K2/K3; token-mean only (config->agg_mode 0,      */
+/* norm = global valid-token count); vocab % 8 == 0, logits and grad 16-byte */
+/* aligned.  Writes per-token logp / entropy / kl (entropy, kl may be NULL)  */
+/* and grad [rows, vocab] bf16 (zero rows where mask == 0); the loss sums    */
+/* follow from yatt_policy_loss on those per-token outputs.                  */
+/* Replaces: Train stand-in simcore.cpp:404-406 (new).          */
+int yatt_policy_loss_grad(const uint16_t* d_policy_logits, const int32_t* d_targets,
+                          const uint8_t* d_mask, const float* d_ref_logp,
+                          const float* d_old_logp, const float* d_advantages,
+                          int64_t rows, int32_t vocab, const yatt_loss_config* config,
+                          int32_t kl_mode, double norm, float* d_logp,
+                          float* d_entropy, float* d_kl, uint16_t* d_grad,
+                          void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* A5+A6  dynamic-sampling filter and compaction (bit-exact)                 */
 /* keep_g = !(all rewards of group g are bitwise identical).  Groups are     */

@@ -77,6 +77,9 @@ int grad_coef_launch(const uint16_t*, const uint16_t*, const int32_t*, const flo
                      const float*, const float*, const float*, const float*, const uint8_t*,
                      int64_t, int32_t, const int64_t*, int64_t, const yatt_loss_config*, int32_t,
                      double, float*, cudaStream_t);
+int policy_loss_grad_launch(const uint16_t*, const int32_t*, const uint8_t*, const float*,
+                            const float*, const float*, int64_t, int32_t, const yatt_loss_config*,
+                            int32_t, double, float*, float*, float*, uint16_t*, cudaStream_t);
 int logits_backward_launch(const uint16_t*, const uint16_t*, const int32_t*, const uint8_t*,
                            int64_t, int32_t, const float*, int32_t, uint16_t*, cudaStream_t);
 
@@ -500,6 +503,19 @@ int yatt_logits_backward(const uint16_t* pol, const uint16_t* ref, const int32_t
   YATT_ALIGNED("logits_backward", coef, 16);
   return logits_backward_launch(pol, ref, tgt, mask, rows, vocab, coef, full_kl, grad,
                                 as_stream(stream));
+}
+
+int yatt_policy_loss_grad(const uint16_t* pol, const int32_t* tgt, const uint8_t* mask,
+                          const float* ref_logp, const float* old_logp, const float* adv,
+                          int64_t rows, int32_t vocab, const yatt_loss_config* cfg,
+                          int32_t kl_mode, double norm, float* logp, float* ent, float* kl,
+                          uint16_t* grad, void* stream) {
+  YATT_ALIGNED("policy_loss_grad", pol, 16);
+  YATT_ALIGNED("policy_loss_grad", grad, 16);
+  YATT_ALIGNED4("policy_loss_grad", tgt, ref_logp, old_logp, adv);
+  YATT_ALIGNED4("policy_loss_grad", logp, ent, kl, nullptr);
+  return policy_loss_grad_launch(pol, tgt, mask, ref_logp, old_logp, adv, rows, vocab, cfg,
+                                 kl_mode, norm, logp, ent, kl, grad, as_stream(stream));
 }
 
 size_t yatt_filter_compact_workspace_bytes(int64_t n) { return compact_workspace_bytes(n); }

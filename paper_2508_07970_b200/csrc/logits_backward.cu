@@ -27,6 +27,7 @@
 #include <cmath>
 
 #include "common.cuh"
+#include "grad_math.cuh"
 
 namespace yattb {
 namespace {
@@ -69,72 +70,17 @@ struct GradParams {
   uint16_t* grad;
 };
 
-__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
-
-__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
-  uint32_t r;
-  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
-  return r;
-}
-
-__device__ __forceinline__ void stg_cs_128(void* p, uint4 v) {
-  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
-               "r"(v.w)
-               : "memory");
-}
-
-struct RowCoef {
-  float g, h, f, lsep2, lseq2, H, KL;  // lse in log2 units (lse * log2e)
-};
-
-// grad for 8 elements (one 16-byte vector) of policy P (and ref Q if kFull).
-template <bool kFull>
-__device__ __forceinline__ uint4 grad_vec(const uint4& P, const uint4& Q, const RowCoef& c) {
-  const uint32_t pw[4] = {P.x, P.y, P.z, P.w};
-  const uint32_t qw[4] = {Q.x, Q.y, Q.z, Q.w};
-  uint32_t out[4];
-  const float2 L2 = f2(kLog2e, kLog2e), nl = f2(-c.lsep2, -c.lsep2);
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const float2 x = f2(bf16_lo(pw[k]), bf16_hi(pw[k]));
-    const float2 a = __ffma2_rn(x, L2, nl);            // log2 p
-    const float2 p = f2(ex2_approx(a.x), ex2_approx(a.y));
-    const float2 lnp = __fmul2_rn(a, f2(kLn2f, kLn2f));  // log p
-    // g * (-p) + h * p * (log p + H)
-    float2 t = __ffma2_rn(f2(c.h, c.h), __fadd2_rn(lnp, f2(c.H, c.H)), f2(-c.g, -c.g));
-    if (kFull) {
-      const float2 z = f2(bf16_lo(qw[k]), bf16_hi(qw[k]));
-      const float2 lnq = __fmul2_rn(__ffma2_rn(z, L2, f2(-c.lseq2, -c.lseq2)), f2(kLn2f, kLn2f));
-      const float2 d = __fadd2_rn(__fadd2_rn(lnp, f2(-lnq.x, -lnq.y)), f2(-c.KL, -c.KL));
-      t = __ffma2_rn(f2(c.f, c.f), d, t);
-    }
-    const float2 gr = __fmul2_rn(p, t);
-    out[k] = pack_bf16x2(gr.x, gr.y);
-  }
-  return make_uint4(out[0], out[1], out[2], out[3]);
-}
+using gm::f2;
+using gm::grad_vec;
+using gm::pack_bf16x2;
+using gm::RowCoef;
+using gm::store_grad;
+using gm::target_grad;
 
 struct __align__(16) BwdTail {
   uint64_t full[kMaxStages];
   uint64_t empty[kMaxStages];
 };
-
-// Stores one gradient vector at staged index j (of a row staged from h
-// elements before its start); with kEdges, a vector straddling the row's
-// ends writes only its in-row elements (the neighbours own the rest).
-template <bool kEdges>
-__device__ __forceinline__ void store_grad(uint16_t* gs, int64_t j, uint4 g, int h, int64_t V) {
-  if (!kEdges || (j >= h && j + 8 <= h + V)) {
-    stg_cs_128(gs + j, g);
-    return;
-  }
-  const uint32_t w[4] = {g.x, g.y, g.z, g.w};
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int64_t idx = j + k;
-    if (idx >= h && idx < h + V) gs[idx] = uint16_t((w[k >> 1] >> (16 * (k & 1))) & 0xffffu);
-  }
-}
 
 // kEdges: V % 8 != 0 — rows staged as 16-byte-aligned supersets (as in A1);
 // the gradient tensor has the same layout, so interior vectors stay aligned.
@@ -243,15 +189,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) logits_backward_kernel(c
       // (same thread, program order after the vector store)
       if (ys >= e0 && ys < e0 + kTile && tid == ((ys - e0) >> 3) % kConsumers) {
         const float x = __uint_as_float(uint32_t(sp[ys - e0]) << 16);
-        const float a = fmaf(x, kLog2e, -c.lsep2);
-        const float pp = ex2_approx(a);
-        float val = pp * fmaf(c.h, a * kLn2f + c.H, -c.g) + c.g;
-        if (kFull) {
-          const float z = __uint_as_float(uint32_t(sq[ys - e0]) << 16);
-          const float lnq = fmaf(z, kLog2e, -c.lseq2) * kLn2f;
-          val = fmaf(c.f * pp, a * kLn2f - lnq - c.KL, val);
-        }
-        gs[ys] = uint16_t(pack_bf16x2(val, 0.f) & 0xffffu);
+        const float z = kFull ? __uint_as_float(uint32_t(sq[ys - e0]) << 16) : 0.f;
+        gs[ys] = uint16_t(pack_bf16x2(target_grad<kFull>(x, z, c), 0.f) & 0xffffu);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&tail->empty[stage]);
@@ -318,23 +257,12 @@ __global__ void grad_coef_kernel(const uint16_t* pol, const uint16_t* ref, const
     }
     scale /= double(coef[cu[lo] * kCoef + 7]);  // count left by seq_count_kernel
   }
-  const double lp = logp[t], old = old_logp[t], A = adv[t];
-  const double ratio = exp(lp - old);
-  const double pg1 = -A * ratio;
-  const double pg2 = -A * fmin(fmax(ratio, 1.0 - double(c.clip_low)), 1.0 + double(c.clip_high));
-  double pg = fmax(pg1, pg2);
-  bool active = !(pg2 > pg1);
-  if (c.clip_ratio_c > 1.f && A < 0.0 && -A * double(c.clip_ratio_c) < pg) active = false;
-  const double dpg = active ? -A * ratio : 0.0;
+  const double lp = logp[t];
   const double rl = ref_logp ? double(ref_logp[t]) : lp;
-  double dkl = 0.0;
-  if (kl_mode == YATT_KL_K1) dkl = 1.0;
-  else if (kl_mode == YATT_KL_K2) dkl = lp - rl;
-  else if (kl_mode == YATT_KL_K3) dkl = -expm1(rl - lp);
   const double beta = double(c.kl_coef);
   const int32_t y = tgt[t];
   const double xy = bf16_at(pol, t * int64_t(V) + y);
-  o[0] = float(scale * (dpg + (kl_mode == YATT_KL_FULL ? 0.0 : beta * dkl)));
+  o[0] = float(scale * gm::dloss_dlogp(lp, old_logp[t], adv[t], rl, c, kl_mode));
   o[1] = float(scale * double(c.entropy_coef));
   o[2] = float(kl_mode == YATT_KL_FULL ? scale * beta : 0.0);
   o[3] = float(xy - lp);  // lse_p

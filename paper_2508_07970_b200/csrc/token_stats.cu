@@ -38,6 +38,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "grad_math.cuh"
 
 namespace yattb {
 namespace {
@@ -142,7 +143,9 @@ __device__ __forceinline__ float2 ex2x2(float2 a) {
   return make_float2(ex2_approx(a.x), ex2_approx(a.y));
 }
 
-template <bool kFull>
+// kRef = false: policy only (no reference logits; the fused loss + gradient
+// kernel), the q accumulators stay empty.
+template <bool kFull, bool kRef = true>
 struct Acc {
   float2 s[4], w[4], sq[4], u[4];
   float mp, mq;        // integer-valued bases (log2 units)
@@ -201,9 +204,11 @@ struct Acc {
       const float2 e = k < kPolyWords ? ex2_poly2(a_used) : ex2x2(a);
       s[k] = __fadd2_rn(s[k], e);
       w[k] = __ffma2_rn(e, a_used, w[k]);
-      const float2 b = __ffma2_rn(z, L2, nmq);
-      float2 b_used = b;
-      sq[k] = __fadd2_rn(sq[k], k < kPolyWords ? ex2_poly2(b_used) : ex2x2(b));
+      if (kRef) {
+        const float2 b = __ffma2_rn(z, L2, nmq);
+        float2 b_used = b;
+        sq[k] = __fadd2_rn(sq[k], k < kPolyWords ? ex2_poly2(b_used) : ex2x2(b));
+      }
       if (kFull) u[k] = __ffma2_rn(e, __ffma2_rn(z, f2(-1.f, -1.f), x), u[k]);
     }
   }
@@ -668,6 +673,270 @@ int YATT_A1_RING(const A1Params& p, cudaStream_t st) {
 }
 
 #ifndef YATT_A1_SMALL_TU
+
+// ======================================================================
+// Training side (SURVEY.md §8f #1 fused with A1 and A4): the policy loss AND
+// its gradient w.r.t. the policy logits in one kernel.  Per row the producer
+// streams the policy logits twice through one policy-only ring: pass 1 with
+// an L2 evict-normal policy (online log2 LSE + entropy, as A1, per-tile
+// rebase so no fix-up pass is needed), pass 2 evict-first — the second read
+// of the row is served from the 126 MB L2 (296 live rows x 304 KB at
+// V=152,064).  Between the passes one warp forms the row's loss terms in
+// fp64 (logp, H, the KL estimator against the stored ref_logp, the clipped
+// surrogate's coefficient, grad_math.cuh) and hands them to all consumers
+// through shared memory; pass 2 writes the bf16 gradient.  HBM bytes per
+// row: 2V read + 2V written (+ ~20 B), vs 2V (A1 policy-only) + 4V (backward)
+// for the two-kernel form.
+// ======================================================================
+struct FusedParams {
+  const uint16_t* pol;
+  const int32_t* tgt;
+  const uint8_t* mask;
+  const float* ref_logp;  // per-token reference log-prob (experience stage), may be null
+  const float* old_logp;
+  const float* adv;
+  int64_t rows;
+  int32_t V;
+  int32_t kl_mode;  // K1 / K2 / K3
+  yatt_loss_config cfg;
+  double inv_norm;  // 1 / global valid-token count (token-mean)
+  float* logp;
+  float* ent;
+  float* kl;
+  uint16_t* grad;
+};
+
+namespace {
+
+using gm::grad_vec;
+using gm::pack_bf16x2;
+using gm::store_grad;
+using gm::target_grad;
+
+constexpr int kFStages = 2 * kStages;  // policy-only tiles: twice the stages in the same bytes
+struct __align__(16) FusedTail {
+  uint64_t full[kFStages];
+  uint64_t empty[kFStages];
+  RowPartial red[kConsumerWarps];
+  float coef[4];  // g, h, lse_p (log2 units), H
+};
+constexpr size_t kFusedSmem = size_t(kFStages) * kTile * sizeof(uint16_t) + sizeof(FusedTail);
+
+__device__ __forceinline__ uint64_t l2_evict_normal_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+
+template <bool kEdges>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) policy_loss_grad_kernel(const FusedParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint16_t* ring = reinterpret_cast<uint16_t*>(smem);
+  FusedTail* tail = reinterpret_cast<FusedTail*>(smem + size_t(kFStages) * kTile * sizeof(uint16_t));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t V = p.V;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kFStages; ++s) {
+      mbar_init(&tail->full[s], 1);
+      mbar_init(&tail->empty[s], kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    // ---------------- producer: every valid row twice ----------------
+    if (lane == 0) {
+      // pass 1 keeps the row in L2 for pass 2 (evict_last / applypriority
+      // demotion measured no better: the rows' reuse distance, not priority,
+      // sets the hit rate)
+      const uint64_t keep = l2_evict_normal_policy(), drop = l2_evict_first_policy();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
+        if (p.mask != nullptr && p.mask[row] == 0) continue;
+        const int h = kEdges ? int((row * V) & 7) : 0;
+        const int64_t S = kEdges ? ((h + V + 7) & ~int64_t(7)) : V;
+        const int ntiles_r = int((S + kTile - 1) / kTile);
+        const uint16_t* gp = p.pol + row * V - h;
+        for (int pass = 0; pass < 2; ++pass) {
+          for (int t = 0; t < ntiles_r; ++t) {
+            const int64_t e0 = int64_t(t) * kTile;
+            const uint32_t n = uint32_t(min64(kTile, S - e0));
+            mbar_wait(&tail->empty[stage], phase ^ 1u);
+            mbar_arrive_expect_tx(&tail->full[stage], 2u * n);
+            bulk_g2s(ring + size_t(stage) * kTile, gp + e0, 2u * n, &tail->full[stage],
+                     pass == 0 ? keep : drop);
+            if (++stage == kFStages) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int tid = threadIdx.x;
+  int stage = 0;
+  uint32_t phase = 0;
+  Acc<false, false> acc;
+  for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
+    const int h = kEdges ? int((row * V) & 7) : 0;
+    const int64_t S = kEdges ? ((h + V + 7) & ~int64_t(7)) : V;
+    const int ntiles_r = int((S + kTile - 1) / kTile);
+    uint16_t* gs = p.grad + row * V - h;  // staged coordinates
+    if (p.mask != nullptr && p.mask[row] == 0) {
+      if (tid == 0) {
+        p.logp[row] = 0.f;
+        if (p.ent) p.ent[row] = 0.f;
+        if (p.kl) p.kl[row] = 0.f;
+      }
+      for (int64_t v = tid; v < S / 8; v += kConsumers)
+        store_grad<kEdges>(gs, v * 8, make_uint4(0, 0, 0, 0), h, V);
+      continue;
+    }
+    const int32_t y = __ldg(p.tgt + row);
+    const int64_t ys = int64_t(y) + h;  // the target in staged coordinates
+    float xy = 0.f;                     // the target logit (thread 0)
+    acc.reset();
+    // ---- pass 1: online log2 LSE + entropy sums ----
+    for (int t = 0; t < ntiles_r; ++t) {
+      const int64_t e0 = int64_t(t) * kTile;
+      const int nvec = int(min64(kTile, S - e0) >> 3);
+      const uint16_t* sp = ring + size_t(stage) * kTile;
+      mbar_wait(&tail->full[stage], phase);
+      if (tid == 0 && ys >= e0 && ys < e0 + kTile) xy = __uint_as_float(uint32_t(sp[ys - e0]) << 16);
+      uint4 P[kVecPerThread];
+#pragma unroll
+      for (int i = 0; i < kVecPerThread; ++i) {
+        const int v = tid + i * kConsumers;
+        const bool in = nvec == kVecPerTile || v < nvec;
+        P[i] = in ? lds128(sp + v * 8) : make_uint4(kNegInf2, kNegInf2, kNegInf2, kNegInf2);
+        if (kEdges) {
+          const int64_t j0 = e0 + int64_t(v) * 8 - h;
+          if (in && (j0 < 0 || j0 + 8 > V))
+            P[i] = keep_range(P[i], int(max64(0, -j0)), int(min64(8, V - j0)));
+        }
+        P[i] = floor_policy(P[i]);
+      }
+      uint32_t mpv = vmax4(P[0]);
+#pragma unroll
+      for (int i = 1; i < kVecPerThread; ++i) mpv = bmax2(mpv, vmax4(P[i]));
+      const float fmp = pair_max(mpv);
+      if (fmp > acc.thr_p) acc.rebase_p(fmp);
+#pragma unroll
+      for (int i = 0; i < kVecPerThread; ++i) acc.step(P[i], P[i]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tail->empty[stage]);
+      if (++stage == kFStages) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+    RowPartial r{acc.mp, Acc<false, false>::total(acc.s), Acc<false, false>::total(acc.w),
+                 float(kMinitial), 0.f, 0.f};
+    r = warp_combine<false>(r);
+    if (lane == 0) tail->red[warp] = r;
+    named_bar_sync(1, kConsumers);
+    if (warp == 0) {
+      RowPartial q = tail->red[lane & (kConsumerWarps - 1)];
+#pragma unroll
+      for (int off = kConsumerWarps / 2; off > 0; off >>= 1) q = combine(q, shfl_partial(q, off));
+      if (lane == 0) {  // fp64 row epilogue: the loss terms and the gradient coefficients
+        const double l2s = log2(double(q.s));
+        const double lse2 = double(q.mp) + l2s;
+        const double lp = double(xy) - kLn2 * lse2;
+        const double H = kLn2 * (l2s - double(q.w) / double(q.s));
+        const double rl = p.ref_logp ? double(__ldg(p.ref_logp + row)) : lp;
+        const double delta = rl - lp;
+        p.logp[row] = float(lp);
+        if (p.ent) p.ent[row] = float(H);
+        if (p.kl) {
+          const double k = p.kl_mode == YATT_KL_K1   ? -delta
+                           : p.kl_mode == YATT_KL_K2 ? 0.5 * delta * delta
+                                                     : expm1(delta) - delta;
+          p.kl[row] = float(k);
+        }
+        const double g = p.inv_norm * gm::dloss_dlogp(lp, double(__ldg(p.old_logp + row)),
+                                                      double(__ldg(p.adv + row)), rl, p.cfg,
+                                                      p.kl_mode);
+        tail->coef[0] = float(g);
+        tail->coef[1] = float(p.inv_norm * double(p.cfg.entropy_coef));
+        tail->coef[2] = float(lse2);
+        tail->coef[3] = float(H);
+      }
+    }
+    named_bar_sync(1, kConsumers);
+    const gm::RowCoef c{tail->coef[0], tail->coef[1], 0.f, tail->coef[2], 0.f, tail->coef[3], 0.f};
+    // ---- pass 2: the gradient (second read of the row, from L2) ----
+    for (int t = 0; t < ntiles_r; ++t) {
+      const int64_t e0 = int64_t(t) * kTile;
+      const int nvec = int(min64(kTile, S - e0) >> 3);
+      const uint16_t* sp = ring + size_t(stage) * kTile;
+      mbar_wait(&tail->full[stage], phase);
+      if (nvec == kVecPerTile) {
+        uint4 P[kVecPerThread];
+#pragma unroll
+        for (int i = 0; i < kVecPerThread; ++i) P[i] = floor_policy(lds128(sp + (tid + i * kConsumers) * 8));
+#pragma unroll
+        for (int i = 0; i < kVecPerThread; ++i)
+          store_grad<kEdges>(gs, e0 + (tid + i * kConsumers) * 8, grad_vec<false>(P[i], P[i], c), h, V);
+      } else {
+        for (int v = tid; v < nvec; v += kConsumers) {
+          const uint4 P = floor_policy(lds128(sp + v * 8));
+          store_grad<kEdges>(gs, e0 + v * 8, grad_vec<false>(P, P, c), h, V);
+        }
+      }
+      if (ys >= e0 && ys < e0 + kTile && tid == ((ys - e0) >> 3) % kConsumers) {
+        const float x = __uint_as_float(uint32_t(sp[ys - e0]) << 16);
+        gs[ys] = uint16_t(pack_bf16x2(target_grad<false>(x, 0.f, c), 0.f) & 0xffffu);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tail->empty[stage]);
+      if (++stage == kFStages) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+int policy_loss_grad_launch(const uint16_t* pol, const int32_t* tgt, const uint8_t* mask,
+                            const float* ref_logp, const float* old_logp, const float* adv,
+                            int64_t rows, int32_t vocab, const yatt_loss_config* cfg,
+                            int32_t kl_mode, double norm, float* logp, float* ent, float* kl,
+                            uint16_t* grad, cudaStream_t st) {
+  YATT_REQUIRE(cfg != nullptr, YATT_ERR_CONFIG, "policy_loss_grad: null config");
+  YATT_REQUIRE(norm > 0.0, YATT_ERR_CONFIG, "policy_loss_grad: norm must be > 0");
+  const FusedParams p{pol, tgt, mask, ref_logp, old_logp, adv, rows, vocab, kl_mode, *cfg,
+                      1.0 / norm, logp, ent, kl, grad};
+  YATT_REQUIRE(p.V > 0 && p.rows >= 0, YATT_ERR_CONFIG, "policy_loss_grad: bad shape");
+  YATT_REQUIRE(p.kl_mode >= YATT_KL_K1 && p.kl_mode <= YATT_KL_K3, YATT_ERR_CONFIG,
+               "policy_loss_grad: kl_mode must be k1, k2 or k3 (full-vocabulary KL needs the "
+               "reference logits: use yatt_policy_grad_coef + yatt_logits_backward)");
+  YATT_REQUIRE(p.cfg.agg_mode == 0, YATT_ERR_CONFIG,
+               "policy_loss_grad: token-mean aggregation only (agg_mode 0)");
+  if (p.rows == 0) return YATT_OK;
+  YATT_REQUIRE(p.pol && p.tgt && p.old_logp && p.adv && p.logp && p.grad, YATT_ERR_CONFIG,
+               "policy_loss_grad: null pointer");
+  // V % 8 != 0: a row's aligned staging superset can end past the tensor on
+  // the last row; the aligned-V contract keeps the fused path simple
+  YATT_REQUIRE(p.V % 8 == 0, YATT_ERR_CONFIG,
+               "policy_loss_grad: vocab must be a multiple of 8 (got %d)", p.V);
+  const int grid = int(min64(p.rows, int64_t(kMinBlocks) * num_sms()));
+  const int rc_ = ensure_dynamic_smem(reinterpret_cast<const void*>(policy_loss_grad_kernel<false>),
+                                      int(kFusedSmem));
+  if (rc_) return rc_;
+  policy_loss_grad_kernel<false><<<grid, kThreads, kFusedSmem, st>>>(p);
+  return check_launch("policy_loss_grad_kernel");
+}
+
 int token_stats_ring_small(const A1Params& p, cudaStream_t st);  // token_stats_small.cu
 
 // Vocabularies up to this take the small ring shape (4,096-element tiles x 4

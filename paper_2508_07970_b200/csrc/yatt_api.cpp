@@ -572,6 +572,17 @@ void policy_logits_grad(const std::uint16_t* pol, const std::uint16_t* ref,
                                             kl == KlEstimator::kFull ? 1 : 0, grad, stream));
 }
 
+void policy_loss_grad(const std::uint16_t* pol, const std::int32_t* tgt, const std::uint8_t* mask,
+                      const float* ref_logp, const float* old_logp, const float* adv,
+                      std::int64_t rows, int vocab, const PolicyLossConfig& c, KlEstimator kl,
+                      double norm, const TokenStats& out, std::uint16_t* grad, void* stream) {
+  c.validate();
+  const yatt_loss_config cc = to_c(c);
+  detail::throw_status(yatt_policy_loss_grad(pol, tgt, mask, ref_logp, old_logp, adv, rows, vocab,
+                                             &cc, static_cast<int>(kl), norm, out.logp,
+                                             out.entropy, out.kl, grad, stream));
+}
+
 std::size_t lmhead_workspace_bytes(std::int64_t rows, int vocab, int n_split) {
   return yatt_lmhead_workspace_bytes(rows, vocab, n_split);
 }

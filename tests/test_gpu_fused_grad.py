@@ -1,0 +1,134 @@
+"""Fused training-side op (yatt_policy_loss_grad, ops.policy_loss_grad): the
+per-token loss terms and d(loss)/d(policy logits) from the policy logits
+alone, each row streamed twice (second read from L2).
+
+Checked against the fp64 oracle: logp / entropy to the A1 bar (1e-5), the
+KL estimator against the stored ref_logp, the gradient with the same bf16 +
+conditioning bound as test_gpu_backward.py (oracle fed the exact fp64 logp),
+and against the two-kernel device path (yatt_policy_grad_coef +
+yatt_logits_backward).  Masked rows are exactly zero; rows sum to ~0."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2508_07970_b200 import ConfigError, ops
+
+pytestmark = pytest.mark.gpu
+
+
+def bf16_np(t):
+    return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def to_f64(bits):
+    return (bits.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+def _case(cuda, rows, V, kl_mode, ent_coef=0.01, masked=False, seed=5, with_ref=True):
+    pol, ref, tgt = ops.synth_logits(seed, 0, rows, V, device=cuda)
+    mask = None
+    if masked:
+        mask = torch.as_tensor((np.arange(rows) % 4 != 1).astype(np.uint8), device=cuda)
+    # the experience stage's stored reference log-probs and old log-probs
+    dlp, drl, _, _ = ops.token_stats(pol, ref, tgt, None, "k3")
+    rlogp = drl if with_ref else None
+    old = ops.synth_floats(seed, 104, 0, rows, "old_delta", base=dlp, device=cuda)
+    adv = ops.synth_floats(seed, 108, 0, rows, "adv", device=cuda)
+    cfg = ops.loss_config(0.2, 0.28, 0.0, 0.05, ent_coef, "token-mean")
+    nvalid = rows if mask is None else int(mask.sum())
+    lp, ent, kl, grad = ops.policy_loss_grad(pol, tgt, old, adv, rlogp, mask, cfg, kl_mode,
+                                             float(nvalid))
+    torch.cuda.synchronize()
+    hp = bf16_np(pol)
+    ht = tgt.cpu().numpy()
+    m = None if mask is None else mask.cpu().numpy()
+    valid = np.ones(rows, bool) if m is None else m.astype(bool)
+    # per-token terms vs the fp64 oracle
+    e_lp, _, e_ent, _ = O.token_stats(hp, hp, ht, None, "k3")
+    assert O.max_rel_error(lp.cpu().numpy()[valid], e_lp[valid]) <= 1e-5
+    assert O.max_rel_error(ent.cpu().numpy()[valid], e_ent[valid]) <= 1e-5
+    e_rl = drl.cpu().numpy().astype(np.float64) if with_ref else e_lp
+    d = e_rl - e_lp
+    e_kl = {"k1": -d, "k2": 0.5 * d * d, "k3": np.expm1(d) - d}[kl_mode]
+    gk = kl.cpu().numpy().astype(np.float64)
+    # kl of (rl - logp): conditioned on |d| (logp carries the 1e-5 A1 bar)
+    tol_kl = 1e-5 * np.abs(e_kl) + 2e-5 * np.abs(e_lp) * (np.abs(d) + 1.0)
+    assert np.all(np.abs(gk[valid] - e_kl[valid]) <= tol_kl[valid])
+    if m is not None:
+        assert np.all(lp.cpu().numpy()[~valid] == 0)
+    # gradient vs the fp64 oracle backward, fed the exact logp
+    eg, ecoef = O.logits_backward(hp, hp, ht, e_lp, e_rl if with_ref else None,
+                                  old.cpu().numpy(), adv.cpu().numpy(), m, None, 0.2, 0.28, 0.0,
+                                  0.05, ent_coef, 0, kl_mode, float(nvalid))
+    got = to_f64(bf16_np(grad))
+    x = to_f64(hp)
+    lpv = x - ecoef[:, 3:4]
+    p = np.exp(lpv)
+    H = -(p * lpv).sum(1, keepdims=True)
+    cond = np.abs(ecoef[:, 0:1]) + np.abs(ecoef[:, 1:2]) * (np.abs(lpv) + H)
+    tol = 2.0 ** -8 * np.abs(eg) + 1e-5 * p * cond + 1e-30
+    # the target element carries + g: relative 1e-5 of g from the logp used
+    tol[np.arange(rows), ht] += 1e-5 * np.abs(ecoef[:, 0])
+    bad = np.abs(got - eg) > tol
+    assert not bad.any(), (np.argwhere(bad)[:5], got[bad][:5], eg[bad][:5])
+    if m is not None:
+        assert np.all(got[~valid] == 0)
+    return pol, ref, tgt, mask, old, adv, rlogp, cfg, nvalid, got
+
+
+@pytest.mark.parametrize("kl_mode", ["k1", "k2", "k3"])
+def test_fused_loss_grad_matches_oracle(cuda, kl_mode):
+    _case(cuda, 40, 32000, kl_mode)
+
+
+def test_fused_masked_rows_and_no_reference(cuda):
+    _case(cuda, 37, 4096, "k3", masked=True)
+    _case(cuda, 16, 4096, "k3", with_ref=False)
+
+
+def test_fused_qwen_vocab_rows_sum_to_zero(cuda):
+    *_, got = _case(cuda, 8, 152064, "k3", ent_coef=0.001)
+    assert np.all(np.abs(got.sum(1)) <= 2e-3 * np.abs(got).max(1) * np.sqrt(got.shape[1]) / 10)
+
+
+def test_fused_matches_two_kernel_path(cuda):
+    """Many rows per CTA (2 x 148 CTAs): the fused gradient equals the
+    two-kernel path's (coef from the same per-token values) to bf16 rounding."""
+    rows, V = 1200, 8192
+    pol, ref, tgt, mask, old, adv, rlogp, cfg, nvalid, got = _case(cuda, rows, V, "k3")
+    lp, ent, kl, _ = ops.policy_loss_grad(pol, tgt, old, adv, rlogp, mask, cfg, "k3",
+                                          float(nvalid))
+    g2, _ = ops.logits_grad(pol, ref, tgt, lp, rlogp, old, adv, ent, kl, mask, None, cfg, "k3",
+                            float(nvalid))
+    two = to_f64(bf16_np(g2))
+    assert np.all(np.abs(got - two) <= 2.0 ** -7 * np.abs(two) + 1e-12 * np.abs(two).max())
+
+
+def test_fused_loss_sums_from_outputs(cuda):
+    """The loss sums follow from the fused per-token outputs."""
+    rows, V = 64, 4096
+    pol, ref, tgt = ops.synth_logits(9, 0, rows, V, device=cuda)
+    dlp, drl, dent, dkl = ops.token_stats(pol, ref, tgt, None, "k3")
+    old = ops.synth_floats(9, 104, 0, rows, "old_delta", base=dlp, device=cuda)
+    adv = ops.synth_floats(9, 108, 0, rows, "adv", device=cuda)
+    cfg = ops.loss_config(0.2, 0.2, 0.0, 0.01, 0.0, "token-mean")
+    lp, ent, kl, _ = ops.policy_loss_grad(pol, tgt, old, adv, drl, None, cfg, "k3", float(rows))
+    a = ops.policy_loss(lp, old, adv, kl, ent, None, None, cfg).cpu().numpy()
+    b = ops.policy_loss(dlp, old, adv, dkl, dent, None, None, cfg).cpu().numpy()
+    assert O.max_rel_error(a, b) <= 1e-5
+
+
+def test_fused_errors(cuda):
+    pol = torch.zeros((2, 12), dtype=torch.bfloat16, device=cuda)
+    tgt = torch.zeros(2, dtype=torch.int32, device=cuda)
+    f = torch.zeros(2, device=cuda)
+    with pytest.raises(ConfigError):  # vocab % 8 != 0
+        ops.policy_loss_grad(pol, tgt, f, f)
+    pol = torch.zeros((2, 16), dtype=torch.bfloat16, device=cuda)
+    with pytest.raises(ConfigError):  # full-vocabulary KL needs the reference logits
+        ops.policy_loss_grad(pol, tgt, f, f, kl_mode="full")
+    with pytest.raises(ConfigError):  # token-mean only
+        ops.policy_loss_grad(pol, tgt, f, f, config=ops.loss_config(agg_mode="seq-mean-token-mean"))
+    with pytest.raises(ConfigError):
+        ops.policy_loss_grad(pol, tgt, f, f, norm=0.0)

@@ -212,6 +212,21 @@ def main():
             per_row = (6 if mode == "full" else 4) * V + 32
             report(f"logits_grad {mode} (coef + backward) {rows} x {V}", ms, rows * per_row, rows,
                    "tokens")
+        # training side fused: loss terms + gradient from the policy logits
+        # (HBM: 2V read + 2V written per row; the second read is from L2)
+        cfg = ops.loss_config(0.2, 0.28, 0.0, 0.001, 0.001, "token-mean")
+        ms = timeit(lambda: ops.policy_loss_grad(pol, tgt, old, a, rl, None, cfg, "k3",
+                                                 float(rows), grad), iters=10)
+        report(f"policy_loss_grad fused (loss terms + grad) {rows} x {V}", ms,
+               rows * (4 * V + 28), rows, "tokens")
+
+        def two_kernel():
+            s_ = ops.token_stats(pol, ref, tgt, None, "k3")
+            ops.logits_grad(pol, ref, tgt, s_[0], rl, old, a, s_[2], s_[3], None, None, cfg,
+                            "k3", float(rows), grad)
+        ms = timeit(two_kernel, iters=10)
+        report(f"token_stats + logits_grad (two-kernel form) {rows} x {V}", ms,
+               rows * (8 * V + 60), rows, "tokens")
         del pol, ref, tgt, grad
         torch.cuda.empty_cache()
 
