@@ -96,15 +96,22 @@ __device__ __forceinline__ float target_grad(float x, float z, const RowCoef& c)
 // d(token loss)/d(logp) of the clipped surrogate (+ dual clip) and, except
 // for the full-vocabulary KL (its gradient is the f term), beta * d(kl)/d(logp)
 // of the per-token estimator; fp64 so clip decisions match the loss kernel.
-__device__ __forceinline__ double dloss_dlogp(double lp, double old, double A, double rl,
-                                              const yatt_loss_config& c, int32_t kl_mode) {
+// The clipped surrogate's part alone: d pg / d logp = -A ratio where the
+// unclipped branch is active, 0 where the clip (or the dual clip) binds.
+__device__ __forceinline__ double dloss_dlogp_pg(double lp, double old, double A,
+                                                 const yatt_loss_config& c) {
   const double ratio = exp(lp - old);
   const double pg1 = -A * ratio;
   const double pg2 = -A * fmin(fmax(ratio, 1.0 - double(c.clip_low)), 1.0 + double(c.clip_high));
   const double pg = fmax(pg1, pg2);
   bool active = !(pg2 > pg1);
   if (c.clip_ratio_c > 1.f && A < 0.0 && -A * double(c.clip_ratio_c) < pg) active = false;
-  const double dpg = active ? -A * ratio : 0.0;
+  return active ? -A * ratio : 0.0;
+}
+
+__device__ __forceinline__ double dloss_dlogp(double lp, double old, double A, double rl,
+                                              const yatt_loss_config& c, int32_t kl_mode) {
+  const double dpg = dloss_dlogp_pg(lp, old, A, c);
   double dkl = 0.0;
   if (kl_mode == YATT_KL_K1) dkl = 1.0;
   else if (kl_mode == YATT_KL_K2) dkl = lp - rl;

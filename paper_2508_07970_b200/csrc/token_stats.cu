@@ -802,6 +802,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) policy_loss_grad_kernel(
     const int32_t y = __ldg(p.tgt + row);
     const int64_t ys = int64_t(y) + h;  // the target in staged coordinates
     float xy = 0.f;                     // the target logit (thread 0)
+    // the row's per-token inputs, loaded now so the row-end epilogue (while
+    // the other warps wait at the barrier) does not wait on global memory
+    float r_old = 0.f, r_adv = 0.f, r_rl = 0.f;
+    if (warp == 0 && lane < 2) {
+      r_old = __ldg(p.old_logp + row);
+      r_adv = __ldg(p.adv + row);
+      r_rl = p.ref_logp ? __ldg(p.ref_logp + row) : 0.f;
+    }
     acc.reset();
     // ---- pass 1: online log2 LSE + entropy sums ----
     for (int t = 0; t < ntiles_r; ++t) {
@@ -846,28 +854,41 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) policy_loss_grad_kernel(
       RowPartial q = tail->red[lane & (kConsumerWarps - 1)];
 #pragma unroll
       for (int off = kConsumerWarps / 2; off > 0; off >>= 1) q = combine(q, shfl_partial(q, off));
-      if (lane == 0) {  // fp64 row epilogue: the loss terms and the gradient coefficients
+      // fp64 row epilogue: lane 0 forms logp / H, then lane 0 takes the
+      // surrogate (exp of the ratio) while lane 1 takes the KL estimator
+      // (expm1) in parallel
+      double lp = 0.0, H = 0.0;
+      if (lane == 0) {
         const double l2s = log2(double(q.s));
         const double lse2 = double(q.mp) + l2s;
-        const double lp = double(xy) - kLn2 * lse2;
-        const double H = kLn2 * (l2s - double(q.w) / double(q.s));
-        const double rl = p.ref_logp ? double(__ldg(p.ref_logp + row)) : lp;
-        const double delta = rl - lp;
+        lp = double(xy) - kLn2 * lse2;
+        H = kLn2 * (l2s - double(q.w) / double(q.s));
         p.logp[row] = float(lp);
         if (p.ent) p.ent[row] = float(H);
-        if (p.kl) {
-          const double k = p.kl_mode == YATT_KL_K1   ? -delta
-                           : p.kl_mode == YATT_KL_K2 ? 0.5 * delta * delta
-                                                     : expm1(delta) - delta;
-          p.kl[row] = float(k);
-        }
-        const double g = p.inv_norm * gm::dloss_dlogp(lp, double(__ldg(p.old_logp + row)),
-                                                      double(__ldg(p.adv + row)), rl, p.cfg,
-                                                      p.kl_mode);
-        tail->coef[0] = float(g);
         tail->coef[1] = float(p.inv_norm * double(p.cfg.entropy_coef));
         tail->coef[2] = float(lse2);
         tail->coef[3] = float(H);
+      }
+      lp = __shfl_sync(0xffffffffu, lp, 0);
+      const double rl = p.ref_logp ? double(r_rl) : lp;
+      double dkl = 0.0;
+      if (lane == 1) {  // the per-token KL estimator and its derivative
+        const double delta = rl - lp;
+        double k;
+        if (p.kl_mode == YATT_KL_K1) k = -delta, dkl = 1.0;
+        else if (p.kl_mode == YATT_KL_K2) k = 0.5 * delta * delta, dkl = -delta;
+        else {
+          const double em1 = expm1(delta);
+          k = em1 - delta;
+          dkl = -em1;
+        }
+        if (p.kl) p.kl[row] = float(k);
+      }
+      dkl = __shfl_sync(0xffffffffu, dkl, 1);
+      if (lane == 0) {
+        const double g = gm::dloss_dlogp_pg(lp, double(r_old), double(r_adv), p.cfg) +
+                         double(p.cfg.kl_coef) * dkl;
+        tail->coef[0] = float(p.inv_norm * g);
       }
     }
     named_bar_sync(1, kConsumers);
