@@ -713,11 +713,24 @@ using gm::pack_bf16x2;
 using gm::store_grad;
 using gm::target_grad;
 
-constexpr int kFStages = 2 * kStages;  // policy-only tiles: twice the stages in the same bytes
+// Shape: YATT_FUSED_CW consumer warps per CTA.  8: A1's shape (2 CTAs/SM,
+// 6 policy stages of 16 KB each); 16: one CTA per SM with 12 stages — the
+// same warps and bytes in flight per SM but half the rows live between their
+// two passes (L2 reuse of the second read).
+#ifndef YATT_FUSED_CW
+#define YATT_FUSED_CW 8
+#endif
+constexpr int kFCW = YATT_FUSED_CW;
+constexpr int kFC = kFCW * 32;
+constexpr int kFThreads = kFC + 32;
+constexpr int kFVpt = kVecPerTile / kFC;
+constexpr int kFMinB = kFCW >= 16 ? 1 : kMinBlocks;
+constexpr int kFStages = (kFCW >= 16 ? 4 : 2) * kStages;  // policy-only 16 KB stages
+static_assert(kVecPerTile % kFC == 0 && (kFCW & (kFCW - 1)) == 0, "fused shape");
 struct __align__(16) FusedTail {
   uint64_t full[kFStages];
   uint64_t empty[kFStages];
-  RowPartial red[kConsumerWarps];
+  RowPartial red[kFCW];
   float coef[4];  // g, h, lse_p (log2 units), H
 };
 constexpr size_t kFusedSmem = size_t(kFStages) * kTile * sizeof(uint16_t) + sizeof(FusedTail);
@@ -730,7 +743,7 @@ __device__ __forceinline__ uint64_t l2_evict_normal_policy() {
 
 
 template <bool kEdges>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) policy_loss_grad_kernel(const FusedParams p) {
+__global__ void __launch_bounds__(kFThreads, kFMinB) policy_loss_grad_kernel(const FusedParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint16_t* ring = reinterpret_cast<uint16_t*>(smem);
   FusedTail* tail = reinterpret_cast<FusedTail*>(smem + size_t(kFStages) * kTile * sizeof(uint16_t));
@@ -739,13 +752,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) policy_loss_grad_kernel(
   if (threadIdx.x == 0) {
     for (int s = 0; s < kFStages; ++s) {
       mbar_init(&tail->full[s], 1);
-      mbar_init(&tail->empty[s], kConsumerWarps);
+      mbar_init(&tail->empty[s], kFCW);
     }
     fence_mbar_init();
   }
   __syncthreads();
 
-  if (warp == kConsumerWarps) {
+  if (warp == kFCW) {
     // ---------------- producer: every valid row twice ----------------
     if (lane == 0) {
       // pass 1 keeps the row in L2 for pass 2 (evict_last / applypriority
@@ -795,7 +808,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) policy_loss_grad_kernel(
         if (p.ent) p.ent[row] = 0.f;
         if (p.kl) p.kl[row] = 0.f;
       }
-      for (int64_t v = tid; v < S / 8; v += kConsumers)
+      for (int64_t v = tid; v < S / 8; v += kFC)
         store_grad<kEdges>(gs, v * 8, make_uint4(0, 0, 0, 0), h, V);
       continue;
     }
@@ -818,10 +831,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) policy_loss_grad_kernel(
       const uint16_t* sp = ring + size_t(stage) * kTile;
       mbar_wait(&tail->full[stage], phase);
       if (tid == 0 && ys >= e0 && ys < e0 + kTile) xy = __uint_as_float(uint32_t(sp[ys - e0]) << 16);
-      uint4 P[kVecPerThread];
+      uint4 P[kFVpt];
 #pragma unroll
-      for (int i = 0; i < kVecPerThread; ++i) {
-        const int v = tid + i * kConsumers;
+      for (int i = 0; i < kFVpt; ++i) {
+        const int v = tid + i * kFC;
         const bool in = nvec == kVecPerTile || v < nvec;
         P[i] = in ? lds128(sp + v * 8) : make_uint4(kNegInf2, kNegInf2, kNegInf2, kNegInf2);
         if (kEdges) {
@@ -833,11 +846,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) policy_loss_grad_kernel(
       }
       uint32_t mpv = vmax4(P[0]);
 #pragma unroll
-      for (int i = 1; i < kVecPerThread; ++i) mpv = bmax2(mpv, vmax4(P[i]));
+      for (int i = 1; i < kFVpt; ++i) mpv = bmax2(mpv, vmax4(P[i]));
       const float fmp = pair_max(mpv);
       if (fmp > acc.thr_p) acc.rebase_p(fmp);
 #pragma unroll
-      for (int i = 0; i < kVecPerThread; ++i) acc.step(P[i], P[i]);
+      for (int i = 0; i < kFVpt; ++i) acc.step(P[i], P[i]);
       __syncwarp();
       if (lane == 0) mbar_arrive(&tail->empty[stage]);
       if (++stage == kFStages) {
@@ -849,11 +862,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) policy_loss_grad_kernel(
                  float(kMinitial), 0.f, 0.f};
     r = warp_combine<false>(r);
     if (lane == 0) tail->red[warp] = r;
-    named_bar_sync(1, kConsumers);
+    named_bar_sync(1, kFC);
     if (warp == 0) {
-      RowPartial q = tail->red[lane & (kConsumerWarps - 1)];
+      RowPartial q = tail->red[lane & (kFCW - 1)];
 #pragma unroll
-      for (int off = kConsumerWarps / 2; off > 0; off >>= 1) q = combine(q, shfl_partial(q, off));
+      for (int off = kFCW / 2; off > 0; off >>= 1) q = combine(q, shfl_partial(q, off));
       // fp64 row epilogue: lane 0 forms logp / H, then lane 0 takes the
       // surrogate (exp of the ratio) while lane 1 takes the KL estimator
       // (expm1) in parallel
@@ -891,7 +904,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) policy_loss_grad_kernel(
         tail->coef[0] = float(p.inv_norm * g);
       }
     }
-    named_bar_sync(1, kConsumers);
+    named_bar_sync(1, kFC);
     const gm::RowCoef c{tail->coef[0], tail->coef[1], 0.f, tail->coef[2], 0.f, tail->coef[3], 0.f};
     // ---- pass 2: the gradient (second read of the row, from L2) ----
     for (int t = 0; t < ntiles_r; ++t) {
@@ -900,19 +913,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) policy_loss_grad_kernel(
       const uint16_t* sp = ring + size_t(stage) * kTile;
       mbar_wait(&tail->full[stage], phase);
       if (nvec == kVecPerTile) {
-        uint4 P[kVecPerThread];
+        uint4 P[kFVpt];
 #pragma unroll
-        for (int i = 0; i < kVecPerThread; ++i) P[i] = floor_policy(lds128(sp + (tid + i * kConsumers) * 8));
+        for (int i = 0; i < kFVpt; ++i) P[i] = floor_policy(lds128(sp + (tid + i * kFC) * 8));
 #pragma unroll
-        for (int i = 0; i < kVecPerThread; ++i)
-          store_grad<kEdges>(gs, e0 + (tid + i * kConsumers) * 8, grad_vec<false>(P[i], P[i], c), h, V);
+        for (int i = 0; i < kFVpt; ++i)
+          store_grad<kEdges>(gs, e0 + (tid + i * kFC) * 8, grad_vec<false>(P[i], P[i], c), h, V);
       } else {
-        for (int v = tid; v < nvec; v += kConsumers) {
+        for (int v = tid; v < nvec; v += kFC) {
           const uint4 P = floor_policy(lds128(sp + v * 8));
           store_grad<kEdges>(gs, e0 + v * 8, grad_vec<false>(P, P, c), h, V);
         }
       }
-      if (ys >= e0 && ys < e0 + kTile && tid == ((ys - e0) >> 3) % kConsumers) {
+      if (ys >= e0 && ys < e0 + kTile && tid == ((ys - e0) >> 3) % kFC) {
         const float x = __uint_as_float(uint32_t(sp[ys - e0]) << 16);
         gs[ys] = uint16_t(pack_bf16x2(target_grad<false>(x, 0.f, c), 0.f) & 0xffffu);
       }
@@ -950,11 +963,11 @@ int policy_loss_grad_launch(const uint16_t* pol, const int32_t* tgt, const uint8
   // the last row; the aligned-V contract keeps the fused path simple
   YATT_REQUIRE(p.V % 8 == 0, YATT_ERR_CONFIG,
                "policy_loss_grad: vocab must be a multiple of 8 (got %d)", p.V);
-  const int grid = int(min64(p.rows, int64_t(kMinBlocks) * num_sms()));
+  const int grid = int(min64(p.rows, int64_t(kFMinB) * num_sms()));
   const int rc_ = ensure_dynamic_smem(reinterpret_cast<const void*>(policy_loss_grad_kernel<false>),
                                       int(kFusedSmem));
   if (rc_) return rc_;
-  policy_loss_grad_kernel<false><<<grid, kThreads, kFusedSmem, st>>>(p);
+  policy_loss_grad_kernel<false><<<grid, kFThreads, kFusedSmem, st>>>(p);
   return check_launch("policy_loss_grad_kernel");
 }
 
