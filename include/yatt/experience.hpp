@@ -165,6 +165,9 @@ class PeerGroup {
   // prefix[i] = sum over lower ranks, total[i] = over all ranks (n <= 16)
   void scan(const std::int64_t* in, int n, std::int64_t* prefix, std::int64_t* total,
             void* stream = nullptr);
+  // Rank-major all-gather of n <= YATT_PEER_GATHER_MAX_WORDS int64 words
+  // (out: world * n), e.g. the round reports + microbatch aggregates.
+  void allgather(const std::int64_t* in, int n, std::int64_t* out, void* stream = nullptr);
   // policy_loss whose final reduction is the cross-rank all-reduce: GLOBAL sums
   void policy_loss(const float* logp, const float* old_logp, const float* advantages,
                    const float* kl, const float* entropy, const std::uint8_t* mask,

@@ -531,6 +531,13 @@ int yatt_peer_allreduce_f64(yatt_peer_t peer, const double* d_in, int32_t n,
 /* offset into the global packed layout (yatt_gather_* d_dst_offset).         */
 int yatt_peer_scan_i64(yatt_peer_t peer, const int64_t* d_in, int32_t n,
                        int64_t* d_prefix, int64_t* d_total, void* stream);
+/* All-gather of n <= YATT_PEER_GATHER_MAX_WORDS int64 words per rank:       */
+/* d_out[world * n], rank-major, identical on all ranks (the dynamic-        */
+/* sampling round reports + microbatch aggregates; -1 everywhere on a peer   */
+/* timeout).  Collective, same call order on every rank.                     */
+#define YATT_PEER_GATHER_MAX_WORDS 16384
+int yatt_peer_allgather_i64(yatt_peer_t peer, const int64_t* d_in, int32_t n,
+                            int64_t* d_out, void* stream);
 /* yatt_policy_loss whose final reduction also all-reduces across the group:  */
 /* d_sums holds the GLOBAL sums on every rank (one kernel after the partials). */
 int yatt_policy_loss_allreduce(yatt_peer_t peer, const float* d_logp,

@@ -143,6 +143,7 @@ SIGNATURES = {
     "yatt_peer_status": (C.c_int, [c_p, P(c_i32)]),
     "yatt_peer_allreduce_f64": (C.c_int, [c_p, c_p, c_i32, c_p, c_p]),
     "yatt_peer_scan_i64": (C.c_int, [c_p, c_p, c_i32, c_p, c_p, c_p]),
+    "yatt_peer_allgather_i64": (C.c_int, [c_p, c_p, c_i32, c_p, c_p]),
     "yatt_policy_loss_allreduce": (C.c_int, [c_p] * 7 + [c_i64, c_p, c_i64, P(LossConfigC), c_p, c_p,
                                                          c_sz, c_p]),
     "yatt_comm_unique_id": (C.c_int, [c_p]),

@@ -9,6 +9,7 @@
 //   slots[2][kPeerMaxWorld][kPeerMaxFields] fp64   (double-buffered by epoch parity)
 //   flags[kPeerMaxWorld] u64                       (flags[q]: last epoch rank q published here)
 //   epoch u64, status u32                          (this rank's call counter, timeout flag)
+//   gather[2][kPeerMaxWorld][16384] int64          (all-gather banks, by epoch parity)
 // One 256-thread block per call: (1) fixed-order reduction of the block
 // partials to this rank's sums, (2) stores them into slot [parity][rank] of
 // EVERY rank's buffer over NVLink, (3) system fence, then publishes the epoch
@@ -34,7 +35,10 @@ constexpr size_t kSlotBytes = size_t(2) * kPeerMaxWorld * kPeerMaxFields * sizeo
 constexpr size_t kFlagOff = kSlotBytes;
 constexpr size_t kEpochOff = kFlagOff + kPeerMaxWorld * sizeof(uint64_t);
 constexpr size_t kStatusOff = kEpochOff + sizeof(uint64_t);
-constexpr size_t kBufBytes = kStatusOff + 64;
+// all-gather region: gather[2][kPeerMaxWorld][kGatherWords] int64 (parity banks)
+constexpr int kGatherWords = YATT_PEER_GATHER_MAX_WORDS;
+constexpr size_t kGatherOff = (kStatusOff + 64 + 255) & ~size_t(255);
+constexpr size_t kBufBytes = kGatherOff + size_t(2) * kPeerMaxWorld * kGatherWords * 8;
 
 struct PeerArgs {
   uint8_t* buf[kPeerMaxWorld];  // buf[r]: rank r's buffer as mapped in this process
@@ -46,6 +50,30 @@ __device__ __forceinline__ double* slot(uint8_t* b, int parity, int q) {
 }
 __device__ __forceinline__ volatile uint64_t* flag(uint8_t* b, int q) {
   return reinterpret_cast<volatile uint64_t*>(b + kFlagOff) + q;
+}
+__device__ __forceinline__ long long* gather_slot(uint8_t* b, int parity, int q) {
+  return reinterpret_cast<long long*>(b + kGatherOff) +
+         (size_t(parity) * kPeerMaxWorld + q) * kGatherWords;
+}
+
+// Thread 0: publish this rank's epoch into every rank's flags and wait until
+// every rank has published it here (~10 s timeout -> status 1, *fail = 1).
+__device__ __forceinline__ void publish_and_wait(const PeerArgs& a, uint64_t epoch, int* fail) {
+  uint8_t* mine = a.buf[a.rank];
+  __threadfence_system();
+  for (int q = 0; q < a.world; ++q) *flag(a.buf[q], a.rank) = epoch;
+  for (int q = 0; q < a.world && !*fail; ++q) {
+    long long spins = 0;
+    while (*flag(mine, q) < epoch) {
+      if (spins > 64) __nanosleep(32);  // tight polling first: the usual wait is ~1 us
+      if (++spins > (1ll << 27)) {      // ~10 s: a rank is gone; fail loudly, do not hang
+        *fail = 1;
+        *reinterpret_cast<volatile uint32_t*>(mine + kStatusOff) = 1u;
+        break;
+      }
+    }
+  }
+  __threadfence_system();
 }
 
 // part: nparts records of nf doubles (part[nf*i + f]); out: nf global sums.
@@ -89,23 +117,8 @@ __global__ void __launch_bounds__(256) peer_reduce_allreduce_kernel(const double
     __threadfence_system();  // each writer orders its slot stores before the flags
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();  // slot stores visible before the flags, to every device
-    for (int q = 0; q < a.world; ++q) *flag(a.buf[q], a.rank) = epoch;
-    // (4) wait for every rank's contribution to this epoch
-    for (int q = 0; q < a.world && !s_fail; ++q) {
-      long long spins = 0;
-      while (*flag(mine, q) < epoch) {
-        if (spins > 64) __nanosleep(32);  // tight polling first: the usual wait is ~1 us
-        if (++spins > (1ll << 27)) {  // ~10 s: a rank is gone; fail loudly, do not hang
-          s_fail = 1;
-          *reinterpret_cast<volatile uint32_t*>(mine + kStatusOff) = 1u;
-          break;
-        }
-      }
-    }
-    __threadfence_system();
-  }
+  // (3)+(4) publish the epoch (slot stores visible first), wait for everyone's
+  if (threadIdx.x == 0) publish_and_wait(a, epoch, &s_fail);
   __syncthreads();
   // (5) identical rank-ordered sum on every rank
   if (threadIdx.x < nf) {
@@ -142,22 +155,7 @@ __global__ void peer_scan_i64_kernel(const int64_t* in, int nf, PeerArgs a, int6
     __threadfence_system();
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    for (int q = 0; q < a.world; ++q) *flag(a.buf[q], a.rank) = epoch;
-    for (int q = 0; q < a.world && !s_fail; ++q) {
-      long long spins = 0;
-      while (*flag(mine, q) < epoch) {
-        if (spins > 64) __nanosleep(32);
-        if (++spins > (1ll << 27)) {
-          s_fail = 1;
-          *reinterpret_cast<volatile uint32_t*>(mine + kStatusOff) = 1u;
-          break;
-        }
-      }
-    }
-    __threadfence_system();
-  }
+  if (threadIdx.x == 0) publish_and_wait(a, epoch, &s_fail);
   __syncthreads();
   if (threadIdx.x < nf) {
     __threadfence_system();
@@ -169,6 +167,44 @@ __global__ void peer_scan_i64_kernel(const int64_t* in, int nf, PeerArgs a, int6
     }
     if (prefix) prefix[threadIdx.x] = s_fail ? -1 : pre;
     if (total) total[threadIdx.x] = s_fail ? -1 : tot;
+  }
+}
+
+// All-gather of n int64 words per rank (rank-major out[world * n]): the
+// binary round-report / microbatch exchange of the dynamic-sampling loop
+// (replaces the reference's JSON submit_round RPC, demo.cpp:32-76, and the
+// NCCL all-gather).  Each rank pushes its words into gather[parity][rank] of
+// every rank's buffer over NVLink, fences, publishes the epoch; then copies
+// the world's words from its own buffer.  Same epoch / parity protocol as
+// the kernels above; on timeout every output word is -1.
+__global__ void __launch_bounds__(256) peer_allgather_i64_kernel(const int64_t* in, int n,
+                                                                  PeerArgs a, int64_t* out) {
+  __shared__ uint64_t s_epoch;
+  __shared__ int s_fail;
+  uint8_t* mine = a.buf[a.rank];
+  if (threadIdx.x == 0) {
+    volatile uint64_t* ep = reinterpret_cast<volatile uint64_t*>(mine + kEpochOff);
+    s_epoch = *ep + 1;
+    *ep = s_epoch;
+    s_fail = 0;
+  }
+  __syncthreads();
+  const uint64_t epoch = s_epoch;
+  const int parity = int(epoch & 1u);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const long long v = in[i];
+    for (int q = 0; q < a.world; ++q)
+      reinterpret_cast<volatile long long*>(gather_slot(a.buf[q], parity, a.rank))[i] = v;
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) publish_and_wait(a, epoch, &s_fail);
+  __syncthreads();
+  __threadfence_system();
+  for (int q = 0; q < a.world; ++q) {
+    const volatile long long* src = gather_slot(mine, parity, q);
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+      out[size_t(q) * n + i] = s_fail ? -1 : src[i];
   }
 }
 
@@ -289,6 +325,18 @@ int yatt_peer_scan_i64(yatt_peer_t p, const int64_t* d_in, int32_t n, int64_t* d
   if (rc) return rc;
   peer_scan_i64_kernel<<<1, 32, 0, as_stream(stream)>>>(d_in, n, a, d_prefix, d_total);
   return check_launch("peer_scan_i64_kernel");
+}
+
+int yatt_peer_allgather_i64(yatt_peer_t p, const int64_t* d_in, int32_t n, int64_t* d_out,
+                            void* stream) {
+  YATT_REQUIRE(n >= 1 && n <= kGatherWords, YATT_ERR_CONFIG,
+               "peer_allgather_i64: n must be in [1, %d]", kGatherWords);
+  YATT_REQUIRE(d_in && d_out, YATT_ERR_CONFIG, "peer_allgather_i64: null pointer");
+  PeerArgs a;
+  const int rc = peer_args(p, &a);
+  if (rc) return rc;
+  peer_allgather_i64_kernel<<<1, 256, 0, as_stream(stream)>>>(d_in, n, a, d_out);
+  return check_launch("peer_allgather_i64_kernel");
 }
 
 int yatt_policy_loss_allreduce(yatt_peer_t p, const float* logp, const float* old_logp,

@@ -636,6 +636,11 @@ void PeerGroup::scan(const std::int64_t* in, int n, std::int64_t* prefix, std::i
       yatt_peer_scan_i64(static_cast<yatt_peer_t>(h_), in, n, prefix, total, stream));
 }
 
+void PeerGroup::allgather(const std::int64_t* in, int n, std::int64_t* out, void* stream) {
+  detail::throw_status(
+      yatt_peer_allgather_i64(static_cast<yatt_peer_t>(h_), in, n, out, stream));
+}
+
 void PeerGroup::policy_loss(const float* logp, const float* old_logp, const float* adv,
                             const float* kl, const float* ent, const std::uint8_t* mask,
                             std::int64_t n, const std::int64_t* cu, std::int64_t nseq,

@@ -150,6 +150,15 @@ class PeerGroup:
                                        tot.data_ptr(), self._st()))
         return pre, tot
 
+    def allgather_i64(self, t: torch.Tensor) -> torch.Tensor:
+        """Rank-major all-gather of n <= 16,384 int64 words per rank in one
+        kernel over peer memory (world * n words, identical on all ranks)."""
+        t = t.contiguous().view(torch.int64)
+        out = torch.empty((self.world * t.numel(),), dtype=torch.int64, device=t.device)
+        check(lib().yatt_peer_allgather_i64(self.h, t.data_ptr(), t.numel(), out.data_ptr(),
+                                            self._st()))
+        return out
+
     def policy_loss(self, logp, old_logp, advantages, kl, entropy, mask=None, cu_seqlens=None,
                     config=None, workspace=None, sums=None):
         """ops.policy_loss whose final reduction is also the all-reduce: the
@@ -183,15 +192,22 @@ REPORT_WORDS = 6  # yatt_round_report = 48 bytes = 6 int64 words (binary wire fo
 MB_WORDS = 3      # yatt_mb_agg = 24 bytes
 
 
-def exchange_round_reports(d_reports: torch.Tensor, d_mbs: torch.Tensor, comm=None):
+def exchange_round_reports(d_reports: torch.Tensor, d_mbs: torch.Tensor, comm=None,
+                           peer: "PeerGroup | None" = None):
     """All-gather this rank's round reports (+ microbatch aggregates, fixed
     per-rank capacity) as raw int64 words and reduce them on the device —
     the binary replacement of the reference's JSON `submit_round` RPC and
     coordinator reduce (demo.cpp:32-76, :261-274; simcore.cpp:304-311).
+    With `peer` the two all-gathers are peer-memory kernels over NVLink
+    (no NCCL call); otherwise NCCL (comm) / torch.distributed.
     Returns (all_reports_words, all_mb_words, reduction[6]) on the device;
     reduction = {active, pending, forced, train_units, score_tokens, continue}."""
-    rep = allgather_counts(d_reports.view(torch.int64).contiguous(), comm)
-    mbs = allgather_counts(d_mbs.view(torch.int64).contiguous(), comm)
+    if peer is not None:
+        rep = peer.allgather_i64(d_reports.view(torch.int64))
+        mbs = peer.allgather_i64(d_mbs.view(torch.int64))
+    else:
+        rep = allgather_counts(d_reports.view(torch.int64).contiguous(), comm)
+        mbs = allgather_counts(d_mbs.view(torch.int64).contiguous(), comm)
     out = torch.empty((6,), dtype=torch.int64, device=d_reports.device)
     check(lib().yatt_reduce_round_reports(rep.data_ptr(), rep.numel() // REPORT_WORDS,
                                           out.data_ptr(), torch.cuda.current_stream().cuda_stream))

@@ -11,7 +11,7 @@
 import pytest
 import torch
 
-from paper_2508_07970_b200 import api, ops
+from paper_2508_07970_b200 import ConfigError, api, ops
 
 pytestmark = pytest.mark.gpu
 
@@ -148,6 +148,25 @@ def test_peer_group_single_rank_matches_plain_ops(cuda):
             g.replay()
         torch.cuda.synchronize()
         assert torch.equal(out, plain)
+        # all-gather (round reports / microbatch words): identity at world 1,
+        # up to the 16,384-word capacity, also from a CUDA graph
+        for n in (1, 8, 3000, 16384):
+            w = torch.arange(n, dtype=torch.int64, device=cuda) * 7 - 5
+            assert torch.equal(peer.allgather_i64(w), w)
+        w = torch.arange(100, dtype=torch.int64, device=cuda)
+        gout = torch.empty_like(w)
+        g2 = torch.cuda.CUDAGraph()
+        from paper_2508_07970_b200._lib import check, lib
+        with torch.cuda.graph(g2):
+            check(lib().yatt_peer_allgather_i64(peer.h, w.data_ptr(), 100, gout.data_ptr(),
+                                                torch.cuda.current_stream().cuda_stream))
+        for k in range(3):
+            w.add_(k)
+            g2.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(gout, w)
+        with pytest.raises(ConfigError):
+            peer.allgather_i64(torch.zeros(16385, dtype=torch.int64, device=cuda))
         assert peer.status() == 0
     finally:
         peer.close()

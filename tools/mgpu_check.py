@@ -106,6 +106,7 @@ def main():
                              api.RejectionConfig(0.3, True, 8), SEED, 8, 5)
     mk = lambda: api.RolloutBatch(0, [api.RolloutSample(i, 64 + i % 13) for i in range(n_all)])  # noqa
     ref_rounds = api.run_rollout_rounds(mk(), world, params)
+    peer = ranks.PeerGroup(world, rank)  # NVLink peer-memory collectives (below too)
     shard = api.make_shard_state(mk(), world, rank)
     ds = api._DeviceShards([shard], params, dev)
     off = (C.c_int64 * 2)(0, len(shard.samples))
@@ -116,6 +117,9 @@ def main():
                                      ds.d_rep.data_ptr(), ds.d_mbs.data_ptr(),
                                      torch.cuda.current_stream().cuda_stream))
         reps, mbs, red = ranks.exchange_round_reports(ds.d_rep, ds.d_mbs, comm)
+        # the same exchange as two peer-memory all-gather kernels: identical words
+        preps, pmbs, pred = ranks.exchange_round_reports(ds.d_rep, ds.d_mbs, peer=peer)
+        assert torch.equal(preps, reps) and torch.equal(pmbs, mbs) and torch.equal(pred, red)
         all_reps = (ReportC * world).from_buffer_copy(reps.cpu().numpy().tobytes())
         got = [(r.controller_rank, r.active_count, r.pending_count, r.accepted_train_units)
                for r in all_reps]
@@ -128,7 +132,6 @@ def main():
     assert rnd == len(ref_rounds)
 
     # loss reduction + all-reduce fused in one kernel over NVLink peer memory
-    peer = ranks.PeerGroup(world, rank)
     tri = world * (world + 1) / 2
     y = peer.allreduce_f64(torch.arange(1, 9, dtype=torch.float64, device=dev) * (rank + 1))
     assert torch.equal(y, torch.arange(1, 9, dtype=torch.float64, device=dev) * tri)
@@ -165,12 +168,19 @@ def main():
     pre, tot = peer.scan_i64(loc["counts"])
     assert int(pre[1]) == int(ops.exclusive_offset(counts, world, rank, 3, 1)[0])
     assert tot.tolist() == counts.view(world, 3).sum(0).tolist()
+    big = torch.arange(12000, dtype=torch.int64, device=dev) + 1000003 * rank
+    gb = peer.allgather_i64(big).view(world, 12000)
+    for q in range(world):
+        assert torch.equal(gb[q], torch.arange(12000, dtype=torch.int64, device=dev) + 1000003 * q)
     assert peer.status() == 0
     # latency of the 8-double all-reduce: fused peer kernel vs NCCL (device time)
     x8 = torch.ones(8, dtype=torch.float64, device=dev)
     o8 = torch.empty_like(x8)
     res = {}
-    for name, fn in [("peer", lambda: peer.allreduce_f64(x8, o8)), ("nccl", lambda: comm.allreduce_(x8))]:
+    r8 = torch.ones(8, dtype=torch.int64, device=dev)
+    for name, fn in [("peer", lambda: peer.allreduce_f64(x8, o8)), ("nccl", lambda: comm.allreduce_(x8)),
+                     ("peer_gather", lambda: peer.allgather_i64(r8)),
+                     ("nccl_gather", lambda: comm.allgather(r8))]:
         for _ in range(20):
             fn()
         torch.cuda.synchronize()
@@ -185,6 +195,8 @@ def main():
     if rank == 0:
         print(f"allreduce 8 x f64 per call: peer kernel {res['peer']:.2f} us, "
               f"NCCL {res['nccl']:.2f} us (world={world})")
+        print(f"allgather 8 x i64 per rank per call: peer kernel {res['peer_gather']:.2f} us, "
+              f"NCCL {res['nccl_gather']:.2f} us (world={world})")
     dist.barrier()
     peer.close()
     comm.close()

@@ -13,7 +13,10 @@ math is exact):
   * scan_i64: exclusive prefix + total of per-rank counters;
   * policy_loss over 8 prompt-group shards == the full batch on one rank
     (max rel 1e-12: fp64 reassociation only);
-  * the same under CUDA-graph replay.
+  * the same under CUDA-graph replay;
+  * the all-gather (9,000 words per rank) and a full dynamic-sampling round
+    loop whose reports travel only over peer memory == the single-process
+    rounds (api.run_rollout_rounds).
 Run: torchrun --nproc-per-node 8 tools/peer_world8.py   -> "peer world8 ok".
 """
 import os
@@ -89,6 +92,38 @@ def main():
         graph.replay()
         torch.cuda.synchronize()
         assert torch.equal(gs, fused), (rank, gs.tolist(), fused.tolist())
+    # all-gather + the dynamic-sampling round loop with reports exchanged over
+    # peer memory only == the single-process rounds
+    big = torch.arange(9000, dtype=torch.int64, device=dev) + 1000003 * rank
+    gb = peer.allgather_i64(big).view(world, 9000)
+    for q in range(world):
+        assert torch.equal(gb[q], torch.arange(9000, dtype=torch.int64, device=dev) + 1000003 * q)
+    import ctypes as C
+    from paper_2508_07970_b200 import api
+    from paper_2508_07970_b200._lib import ReportC, check, lib
+    params = api.RoundParams(api.LengthDistribution(api.UNIFORM, 1, 4096, 4096),
+                             api.RejectionConfig(0.3, True, 8), SEED, 8, 5)
+    mk = lambda: api.RolloutBatch(0, [api.RolloutSample(i, 64 + i % 13) for i in range(2048)])  # noqa
+    ref_rounds = api.run_rollout_rounds(mk(), world, params)
+    shard = api.make_shard_state(mk(), world, rank)
+    ds = api._DeviceShards([shard], params, dev)
+    off = (C.c_int64 * 2)(0, len(shard.samples))
+    rnd = 0
+    while True:
+        rnd += 1
+        check(lib().yatt_shard_round(ds.d.data_ptr(), off, 1, rank, 0, rnd, C.byref(params.c()),
+                                     ds.d_rep.data_ptr(), ds.d_mbs.data_ptr(),
+                                     torch.cuda.current_stream().cuda_stream))
+        reps, mbs, red = ranks.exchange_round_reports(ds.d_rep, ds.d_mbs, peer=peer)
+        all_reps = (ReportC * world).from_buffer_copy(reps.cpu().numpy().tobytes())
+        got = [(r.controller_rank, r.active_count, r.pending_count, r.accepted_train_units)
+               for r in all_reps]
+        exp = [(r.controller_rank, r.active_count, r.pending_count, r.accepted_train_units)
+               for r in ref_rounds[rnd - 1]]
+        assert got == exp, (rank, rnd, got, exp)
+        if int(red[5]) == 0:
+            break
+    assert rnd == len(ref_rounds)
     assert peer.status() == 0
     dist.barrier()
     peer.close()
