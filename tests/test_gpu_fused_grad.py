@@ -132,3 +132,21 @@ def test_fused_errors(cuda):
         ops.policy_loss_grad(pol, tgt, f, f, config=ops.loss_config(agg_mode="seq-mean-token-mean"))
     with pytest.raises(ConfigError):
         ops.policy_loss_grad(pol, tgt, f, f, norm=0.0)
+
+
+@pytest.mark.parametrize("rows,V", [(1, 8), (3, 16), (5, 8200), (2, 24576)])
+def test_fused_edge_shapes(cuda, rows, V):
+    """One row, the smallest vocabularies, a vocabulary that is not a tile
+    multiple (partial last tile) and one that is exactly three tiles."""
+    _case(cuda, rows, V, "k3", masked=rows > 2)
+
+
+def test_fused_all_rows_masked(cuda):
+    rows, V = 6, 4096
+    pol, ref, tgt = ops.synth_logits(1, 0, rows, V, device=cuda)
+    f = torch.zeros(rows, device=cuda)
+    mask = torch.zeros(rows, dtype=torch.uint8, device=cuda)
+    grad = torch.full_like(pol, 1.0)
+    lp, ent, kl, g = ops.policy_loss_grad(pol, tgt, f, f, f, mask, None, "k3", 1.0, grad)
+    torch.cuda.synchronize()
+    assert torch.all(g.float() == 0) and torch.all(lp == 0) and torch.all(ent == 0)
