@@ -22,6 +22,10 @@
  *    A misaligned pointer returns YATT_ERR_CONFIG before any launch.
  *    yatt_token_stats and yatt_logits_backward accept any vocab and 2-byte
  *    aligned logits (a generic element-wise kernel; the TMA path otherwise).
+ *  - Targets must lie in [0, vocab).  A target outside it (device data, so
+ *    not checked on the host) never causes an out-of-row access: that row's
+ *    logp / ref_logp / kl come out NaN (entropy stays valid) and its
+ *    gradient row is NaN, so the error is visible in the outputs.
  */
 #ifndef YATT_CUDA_H_
 #define YATT_CUDA_H_

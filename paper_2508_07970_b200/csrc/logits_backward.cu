@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) logits_backward_kernel(c
       }
       // the target element gets + g: its owner rewrites those two bytes
       // (same thread, program order after the vector store)
-      if (ys >= e0 && ys < e0 + kTile && tid == ((ys - e0) >> 3) % kConsumers) {
+      if (y >= 0 && y < V && ys >= e0 && ys < e0 + kTile && tid == ((ys - e0) >> 3) % kConsumers) {
         const float x = __uint_as_float(uint32_t(sp[ys - e0]) << 16);
         const float z = kFull ? __uint_as_float(uint32_t(sq[ys - e0]) << 16) : 0.f;
         gs[ys] = uint16_t(pack_bf16x2(target_grad<kFull>(x, z, c), 0.f) & 0xffffu);
@@ -261,13 +261,16 @@ __global__ void grad_coef_kernel(const uint16_t* pol, const uint16_t* ref, const
   const double rl = ref_logp ? double(ref_logp[t]) : lp;
   const double beta = double(c.kl_coef);
   const int32_t y = tgt[t];
-  const double xy = bf16_at(pol, t * int64_t(V) + y);
+  // a target outside [0, V) (caller error): NaN coefficients -> a NaN
+  // gradient row, never an out-of-row read
+  const bool yok = y >= 0 && y < V;
+  const double xy = yok ? double(bf16_at(pol, t * int64_t(V) + y)) : __longlong_as_double(0x7ff8000000000000ll);
   o[0] = float(scale * gm::dloss_dlogp(lp, old_logp[t], adv[t], rl, c, kl_mode));
   o[1] = float(scale * double(c.entropy_coef));
   o[2] = float(kl_mode == YATT_KL_FULL ? scale * beta : 0.0);
   o[3] = float(xy - lp);  // lse_p
-  o[4] = (kl_mode == YATT_KL_FULL && ref) ? float(double(bf16_at(ref, t * int64_t(V) + y)) - rl)
-                                          : 0.f;
+  o[4] = (kl_mode == YATT_KL_FULL && ref && yok) ? float(double(bf16_at(ref, t * int64_t(V) + y)) - rl)
+                                                 : 0.f;
   o[5] = ent ? ent[t] : 0.f;
   o[6] = kl ? kl[t] : 0.f;
   // o[7] is scratch: the valid-token count of the sequence at its first token

@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) token_stats_kernel(const
       const uint16_t* sp = ring + size_t(stage) * 2 * kTile;
       const uint16_t* sq = sp + kTile;
       mbar_wait(&tail->full[stage], phase);
-      if (t == ty && tid == 0) {  // target logits straight from the staged tile
+      if (t == ty && tid == 0 && y >= 0 && y < V) {  // target logits from the staged tile
         tail->tgt[par][0] = __uint_as_float(uint32_t(sp[yin]) << 16);
         tail->tgt[par][1] = __uint_as_float(uint32_t(sq[yin]) << 16);
       }
@@ -538,7 +538,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) token_stats_kernel(const
         if (kFastPath && !partial_finite<kFull>(q)) {
           p.logp[row] = __uint_as_float(kFixupSentinel);  // token_stats_fixup_kernel redoes it
         } else {
-          emit_row(p, row, q, tail->tgt[par][0], tail->tgt[par][1]);
+          // a target outside [0, V) is a caller error: NaN log-probs / KL
+          // (entropy stays valid), never an out-of-row access
+          const bool yok = y >= 0 && y < V;
+          const float nan = __uint_as_float(0x7fc00000u);
+          emit_row(p, row, q, yok ? tail->tgt[par][0] : nan, yok ? tail->tgt[par][1] : nan);
         }
       }
     }
@@ -621,8 +625,10 @@ __global__ void __launch_bounds__(kConsumers) token_stats_fixup_kernel(const A1P
         for (int off = kConsumerWarps / 2; off > 0; off >>= 1) q = combine(q, shfl_partial(q, off));
         if (lane == 0) {
           const int32_t y = p.tgt[row];
-          emit_row(p, row, q, __uint_as_float(uint32_t(p.pol[row * V + y]) << 16),
-                   __uint_as_float(uint32_t(p.ref[row * V + y]) << 16));
+          const bool yok = y >= 0 && y < V;  // else NaN log-probs / KL, no OOB read
+          const float nan = __uint_as_float(0x7fc00000u);
+          emit_row(p, row, q, yok ? __uint_as_float(uint32_t(p.pol[row * V + y]) << 16) : nan,
+                   yok ? __uint_as_float(uint32_t(p.ref[row * V + y]) << 16) : nan);
         }
       }
       __syncthreads();
@@ -814,7 +820,8 @@ __global__ void __launch_bounds__(kFThreads, kFMinB) policy_loss_grad_kernel(con
     }
     const int32_t y = __ldg(p.tgt + row);
     const int64_t ys = int64_t(y) + h;  // the target in staged coordinates
-    float xy = 0.f;                     // the target logit (thread 0)
+    const bool yok = y >= 0 && y < V;   // else NaN loss terms / gradient row, no OOB write
+    float xy = yok ? 0.f : __uint_as_float(0x7fc00000u);  // the target logit (thread 0)
     // the row's per-token inputs, loaded now so the row-end epilogue (while
     // the other warps wait at the barrier) does not wait on global memory
     float r_old = 0.f, r_adv = 0.f, r_rl = 0.f;
@@ -830,7 +837,8 @@ __global__ void __launch_bounds__(kFThreads, kFMinB) policy_loss_grad_kernel(con
       const int nvec = int(min64(kTile, S - e0) >> 3);
       const uint16_t* sp = ring + size_t(stage) * kTile;
       mbar_wait(&tail->full[stage], phase);
-      if (tid == 0 && ys >= e0 && ys < e0 + kTile) xy = __uint_as_float(uint32_t(sp[ys - e0]) << 16);
+      if (tid == 0 && yok && ys >= e0 && ys < e0 + kTile)
+        xy = __uint_as_float(uint32_t(sp[ys - e0]) << 16);
       uint4 P[kFVpt];
 #pragma unroll
       for (int i = 0; i < kFVpt; ++i) {
@@ -925,7 +933,7 @@ __global__ void __launch_bounds__(kFThreads, kFMinB) policy_loss_grad_kernel(con
           store_grad<kEdges>(gs, e0 + v * 8, grad_vec<false>(P, P, c), h, V);
         }
       }
-      if (ys >= e0 && ys < e0 + kTile && tid == ((ys - e0) >> 3) % kFC) {
+      if (yok && ys >= e0 && ys < e0 + kTile && tid == ((ys - e0) >> 3) % kFC) {
         const float x = __uint_as_float(uint32_t(sp[ys - e0]) << 16);
         gs[ys] = uint16_t(pack_bf16x2(target_grad<false>(x, 0.f, c), 0.f) & 0xffffu);
       }

@@ -238,3 +238,51 @@ def test_synth_guard(cuda):
     check(lib().yatt_synth_floats(1, 105, 3, 1001, ops.SYNTH["reward"], 8, None, f.p, _st()))
     torch.cuda.synchronize()
     assert pol.intact() and ref.intact() and tgt.intact() and f.intact()
+
+
+@pytest.mark.parametrize("vocab", [4096, 1001])
+def test_invalid_targets_are_loud_and_in_bounds(cuda, vocab):
+    """Targets outside [0, V) are a caller error: those rows get NaN log-probs
+    / KL (and a NaN gradient row), entropy stays valid, every other row is
+    unchanged, and nothing outside the outputs is touched."""
+    rows = 8
+    g = torch.Generator(device=cuda).manual_seed(11)
+    pol = (torch.randn(rows, vocab, device=cuda, generator=g) * 2).to(torch.bfloat16)
+    ref = (torch.randn(rows, vocab, device=cuda, generator=g) * 2).to(torch.bfloat16)
+    good = torch.randint(0, vocab, (rows,), device=cuda, dtype=torch.int32, generator=g)
+    tgt = good.clone()
+    bad = [1, 3, 6]
+    tgt[1], tgt[3], tgt[6] = -1, vocab, vocab + 5
+    lp, rl, ent, kl = ops.token_stats(pol, ref, tgt, None, "k3")
+    lp0, rl0, ent0, kl0 = ops.token_stats(pol, ref, good, None, "k3")
+    torch.cuda.synchronize()
+    ok = [r for r in range(rows) if r not in bad]
+    assert torch.isnan(lp[bad]).all() and torch.isnan(rl[bad]).all() and torch.isnan(kl[bad]).all()
+    assert torch.equal(ent, ent0)
+    assert torch.equal(lp[ok], lp0[ok]) and torch.equal(kl[ok], kl0[ok])
+    # the backward: NaN rows for the bad targets, the gradient buffer's
+    # neighbours untouched, good rows as with valid targets everywhere
+    old = lp0.clone()
+    adv = torch.ones(rows, device=cuda)
+    gd = Guarded(rows * vocab, torch.bfloat16, cuda, shift=0)
+    coef = Guarded(rows * 8, torch.float32, cuda, shift=0)
+    cfg = ops.loss_config()
+    check(lib().yatt_policy_grad_coef(pol.data_ptr(), ref.data_ptr(), tgt.data_ptr(), lp.data_ptr(),
+                                      rl.data_ptr(), old.data_ptr(), adv.data_ptr(), ent.data_ptr(),
+                                      kl.data_ptr(), None, rows, vocab, None, 0,
+                                      C.byref(cfg), 2, float(rows), coef.p, _st()))
+    check(lib().yatt_logits_backward(pol.data_ptr(), None, tgt.data_ptr(), None, rows, vocab,
+                                     coef.p, 0, gd.p, _st()))
+    torch.cuda.synchronize()
+    assert gd.intact() and coef.intact()
+    gr = gd.t.view(rows, vocab).float()
+    assert torch.isnan(gr[bad]).all(dim=1).all()
+    assert torch.isfinite(gr[ok]).all()
+    if vocab % 8 == 0:  # the fused op
+        gf = Guarded(rows * vocab, torch.bfloat16, cuda, shift=0)
+        flp, fent, fkl, _ = ops.policy_loss_grad(pol, tgt, old, adv, rl0, None, None, "k3",
+                                                 float(rows), gf.t.view(rows, vocab))
+        torch.cuda.synchronize()
+        assert gf.intact()
+        assert torch.isnan(flp[bad]).all() and torch.isfinite(flp[ok]).all()
+        assert torch.isnan(gf.t.view(rows, vocab).float()[bad]).all(dim=1).all()
