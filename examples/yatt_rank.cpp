@@ -159,6 +159,28 @@ int main() {
     }
     std::printf("backward: row 0 grad sum %.3e (max |g| %.3e)\n", sum, amax);
     if (!std::isfinite(sum) || std::fabs(sum) > 1e-2 * amax * 50) return 1;
+    // the fused training-side op (policy logits only, each row read twice):
+    // same gradient as the two-kernel path to bf16 rounding
+    auto* f_out = dalloc<float>(size_t(gr) * 3);
+    auto* grad2 = dalloc<std::uint16_t>(size_t(gr) * vocab);
+    experience::policy_loss_grad(pol, tgt, nullptr, ref_logp, old, tadv, gr, vocab, cfg,
+                                 experience::KlEstimator::kK3, double(rows),
+                                 {f_out, nullptr, f_out + gr, f_out + 2 * gr}, grad2);
+    std::vector<std::uint16_t> hg2(static_cast<size_t>(vocab));
+    ck(cudaMemcpy(hg2.data(), grad2, hg2.size() * 2, cudaMemcpyDeviceToHost), "D2H fused grad");
+    int off = 0;
+    for (size_t v = 0; v < hg.size(); ++v) {
+      float a, b;
+      std::uint32_t ua = std::uint32_t(hg[v]) << 16, ub = std::uint32_t(hg2[v]) << 16;
+      std::memcpy(&a, &ua, 4);
+      std::memcpy(&b, &ub, 4);
+      off += !(std::fabs(a - b) <= 0.0079 * std::fabs(a) + 1e-6 * amax);
+    }
+    std::printf("fused loss+grad: row 0 matches the two-kernel gradient (%d of %d outside bf16)\n",
+                off, vocab);
+    if (off != 0) return 1;
+    cudaFree(f_out);
+    cudaFree(grad2);
     cudaFree(coef);
     cudaFree(grad);
   }
@@ -177,6 +199,18 @@ int main() {
       return 1;
     }
     std::printf("peer group: fused loss all-reduce == policy_loss (bit-exact)\n");
+    // all-gather of the round-report words (world 1: the identity)
+    std::vector<std::int64_t> hw(100);
+    for (int i = 0; i < 100; ++i) hw[size_t(i)] = 7 * i - 3;
+    auto* dw = dalloc<std::int64_t>(100);
+    auto* dg = dalloc<std::int64_t>(100);
+    ck(cudaMemcpy(dw, hw.data(), 800, cudaMemcpyHostToDevice), "H2D words");
+    peer.allgather(dw, 100, dg);
+    std::vector<std::int64_t> hgw(100);
+    ck(cudaMemcpy(hgw.data(), dg, 800, cudaMemcpyDeviceToHost), "D2H gathered");
+    if (hgw != hw) return 1;
+    cudaFree(dw);
+    cudaFree(dg);
     cudaFree(gsums);
   }
 
