@@ -59,6 +59,14 @@ def _dense(**named) -> None:
             _dev(t, t.dtype, name)
 
 
+def _numel(n: int, **named) -> None:
+    """Per-token / per-sample arrays must hold exactly n elements (the
+    kernels read n of each: a shorter tensor would be read out of bounds)."""
+    for name, t in named.items():
+        if t is not None and t.numel() != n:
+            raise ValueError(f"{name} has {t.numel()} elements, expected {n}")
+
+
 def _mask(mask: torch.Tensor | None) -> torch.Tensor | None:
     if mask is None:
         return None
@@ -78,8 +86,12 @@ def token_stats(policy_logits: torch.Tensor, ref_logits: torch.Tensor, targets: 
     if ref_logits.shape != policy_logits.shape or targets.shape != (rows,):
         raise ValueError("shape mismatch between logits / targets")
     m = _mask(mask)
+    _numel(rows, mask=m)
     if out is None:
         out = torch.empty((4, rows), dtype=torch.float32, device=policy_logits.device)
+    elif out.shape != (4, rows):
+        raise ValueError(f"out must be [4, {rows}], got {list(out.shape)}")
+    _dev(out, torch.float32, "out")
     check(lib().yatt_token_stats(_p(policy_logits), _p(ref_logits), _p(targets), _p(m), rows,
                                  vocab, KL_MODES[kl_mode], _p(out[0]), _p(out[1]), _p(out[2]),
                                  _p(out[3]), _st()))
@@ -167,6 +179,9 @@ def broadcast_to_tokens(sample_vals: torch.Tensor, cu_seqlens: torch.Tensor, n_t
     _devs(torch.float32, sample_vals=sample_vals, out=out)
     if out is None:
         out = torch.empty((n_tokens,), dtype=torch.float32, device=sample_vals.device)
+    _numel(n_tokens, out=out, mask=mask)
+    if cu_seqlens.numel() < sample_vals.numel() + 1:
+        raise ValueError("cu_seqlens needs n_samples + 1 entries")
     check(lib().yatt_broadcast_to_tokens(_p(sample_vals), _p(cu_seqlens), sample_vals.numel(),
                                          _p(_mask(mask)), _p(out), n_tokens, _st()))
     return out
@@ -181,9 +196,10 @@ def gae(values: torch.Tensor, rewards: torch.Tensor, cu_seqlens: torch.Tensor,
     _dev(values, torch.float32, "values")
     _dev(rewards, torch.float32, "rewards")
     _dev(cu_seqlens, torch.int64, "cu_seqlens")
+    n = values.numel()
+    _numel(n, rewards=rewards, mask=mask)
     adv = torch.empty_like(values)
     ret = torch.empty_like(values)
-    n = values.numel()
     wsb = lib().yatt_gae_workspace_bytes(n)
     ws = torch.empty((max(wsb, 16),), dtype=torch.uint8, device=values.device)
     if return_moments:
@@ -200,6 +216,7 @@ def gae(values: torch.Tensor, rewards: torch.Tensor, cu_seqlens: torch.Tensor,
 
 def masked_moments(x: torch.Tensor, mask: torch.Tensor | None = None) -> torch.Tensor:
     _dev(x, torch.float32, "x")
+    _numel(x.numel(), mask=mask)
     out = torch.empty((3,), dtype=torch.float64, device=x.device)
     wsb = lib().yatt_masked_moments_workspace_bytes()
     ws = torch.empty((wsb,), dtype=torch.uint8, device=x.device)
@@ -211,6 +228,8 @@ def whiten(x: torch.Tensor, moments: torch.Tensor, mask: torch.Tensor | None = N
            shift_mean: bool = True) -> torch.Tensor:
     _dev(x, torch.float32, "x")
     _dev(moments, torch.float64, "moments")
+    _numel(x.numel(), mask=mask)
+    _numel(3, moments=moments)
     check(lib().yatt_whiten(_p(x), _p(_mask(mask)), x.numel(), _p(moments), int(shift_mean), _st()))
     return x
 
@@ -236,6 +255,8 @@ def policy_loss(logp, old_logp, advantages, kl, entropy, mask=None, cu_seqlens=N
           entropy=entropy)
     if cu_seqlens is not None:
         _dev(cu_seqlens, torch.int64, "cu_seqlens")
+    _numel(logp.numel(), old_logp=old_logp, advantages=advantages, kl=kl, entropy=entropy,
+           mask=mask)
     cfg = config or loss_config()
     ws = workspace or LossWorkspace(logp.device)
     if sums is None:
@@ -257,6 +278,7 @@ def filter_compact(rewards: torch.Tensor, seq_lens: torch.Tensor, group_size: in
     _dev(rewards, torch.float32, "rewards")
     _dev(seq_lens, torch.int64, "seq_lens")
     n = rewards.numel()
+    _numel(n, seq_lens=seq_lens)
     dev = rewards.device
     keep = torch.empty((max(n // group_size, 1),), dtype=torch.uint8, device=dev)
     imap = torch.empty((max(n, 1),), dtype=torch.int32, device=dev)
@@ -381,6 +403,10 @@ def policy_loss_grad(policy_logits, targets, old_logp, advantages, ref_logp=None
     _devs(torch.float32, ref_logp=ref_logp, old_logp=old_logp, advantages=advantages)
     _dev(targets, torch.int32, "targets")
     rows, vocab = policy_logits.shape
+    _numel(rows, targets=targets, old_logp=old_logp, advantages=advantages, ref_logp=ref_logp,
+           mask=mask)
+    if grad is not None and grad.shape != policy_logits.shape:
+        raise ValueError("grad must have the shape of policy_logits")
     out = torch.empty((3, rows), dtype=torch.float32, device=policy_logits.device)
     if grad is None:
         grad = torch.empty_like(policy_logits)
@@ -402,6 +428,10 @@ def logits_grad(policy_logits, ref_logits, targets, logp, ref_logp, old_logp, ad
           entropy=entropy, kl=kl)
     _dev(targets, torch.int32, "targets")
     rows, vocab = policy_logits.shape
+    _numel(rows, targets=targets, logp=logp, ref_logp=ref_logp, old_logp=old_logp,
+           advantages=advantages, entropy=entropy, kl=kl, mask=mask)
+    if grad is not None and grad.shape != policy_logits.shape:
+        raise ValueError("grad must have the shape of policy_logits")
     coef = torch.empty((rows, 8), dtype=torch.float32, device=policy_logits.device)
     m = _mask(mask)
     nseq = 0 if cu_seqlens is None else cu_seqlens.numel() - 1

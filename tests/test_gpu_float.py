@@ -275,6 +275,32 @@ def test_ops_reject_strided_and_mistyped_inputs(cuda):
                           torch.zeros(1, dtype=torch.int64, device=cuda), 1, x[:16])
 
 
+def test_ops_reject_short_per_token_arrays(cuda):
+    """Every per-token / per-sample array must hold the op's n elements: a
+    shorter one would be read past its end by the kernel."""
+    x = torch.randn(64, device=cuda)
+    m = torch.ones(63, dtype=torch.uint8, device=cuda)
+    cu = torch.tensor([0, 64], dtype=torch.int64, device=cuda)
+    with pytest.raises(ValueError, match="elements"):
+        ops.policy_loss(x, x, x[:32], x, x)
+    with pytest.raises(ValueError, match="elements"):
+        ops.policy_loss(x, x, x, x, x, m)
+    with pytest.raises(ValueError, match="elements"):
+        ops.gae(x, x[:63], cu)
+    with pytest.raises(ValueError, match="elements"):
+        ops.masked_moments(x, m)
+    with pytest.raises(ValueError, match="elements"):
+        ops.filter_compact(x, torch.ones(63, dtype=torch.int64, device=cuda), 8)
+    pol = torch.zeros((4, 16), dtype=torch.bfloat16, device=cuda)
+    tgt = torch.zeros(4, dtype=torch.int32, device=cuda)
+    with pytest.raises(ValueError, match="elements"):
+        ops.token_stats(pol, pol, tgt, m)
+    with pytest.raises(ValueError, match="elements"):
+        ops.policy_loss_grad(pol, tgt, x[:4], x[:3])
+    with pytest.raises(ValueError, match="shape"):
+        ops.policy_loss_grad(pol, tgt, x[:4], x[:4], grad=pol[:2])
+
+
 @pytest.mark.parametrize("masked", [False, True])
 def test_gae_fused_whitening_moments(cuda, masked):
     """yatt_gae_with_moments: the advantages' masked moments come out of the
