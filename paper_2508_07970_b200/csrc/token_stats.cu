@@ -638,6 +638,7 @@ __global__ void __launch_bounds__(kConsumers) token_stats_fixup_kernel(const A1P
 
 }  // namespace
 
+#ifndef YATT_FUSED_SMALL_TU  // token_stats_fused_small.cu compiles only the fused kernel
 #ifdef YATT_A1_SMALL_TU
 #define YATT_A1_RING token_stats_ring_small
 #else
@@ -677,6 +678,8 @@ int YATT_A1_RING(const A1Params& p, cudaStream_t st) {
     token_stats_fixup_kernel<false, false><<<fgrid, kConsumers, 0, st>>>(p);
   return check_launch("token_stats_fixup_kernel");
 }
+
+#endif  // !YATT_FUSED_SMALL_TU
 
 #ifndef YATT_A1_SMALL_TU
 
@@ -949,6 +952,25 @@ __global__ void __launch_bounds__(kFThreads, kFMinB) policy_loss_grad_kernel(con
 
 }  // namespace
 
+#ifdef YATT_FUSED_SMALL_TU
+#define YATT_FUSED_RING policy_loss_grad_ring_small
+#else
+#define YATT_FUSED_RING policy_loss_grad_ring_large
+#endif
+// The fused kernel with this translation unit's shape (validated params).
+int YATT_FUSED_RING(const FusedParams& p, cudaStream_t st) {
+  const int grid = int(min64(p.rows, int64_t(kFMinB) * num_sms()));
+  const int rc_ = ensure_dynamic_smem(reinterpret_cast<const void*>(policy_loss_grad_kernel<false>),
+                                      int(kFusedSmem));
+  if (rc_) return rc_;
+  policy_loss_grad_kernel<false><<<grid, kFThreads, kFusedSmem, st>>>(p);
+  return check_launch("policy_loss_grad_kernel");
+}
+
+#ifndef YATT_FUSED_SMALL_TU
+int policy_loss_grad_ring_small(const FusedParams& p, cudaStream_t st);  // token_stats_fused_small.cu
+int a1_small_vmax();
+
 int policy_loss_grad_launch(const uint16_t* pol, const int32_t* tgt, const uint8_t* mask,
                             const float* ref_logp, const float* old_logp, const float* adv,
                             int64_t rows, int32_t vocab, const yatt_loss_config* cfg,
@@ -971,12 +993,11 @@ int policy_loss_grad_launch(const uint16_t* pol, const int32_t* tgt, const uint8
   // the last row; the aligned-V contract keeps the fused path simple
   YATT_REQUIRE(p.V % 8 == 0, YATT_ERR_CONFIG,
                "policy_loss_grad: vocab must be a multiple of 8 (got %d)", p.V);
-  const int grid = int(min64(p.rows, int64_t(kFMinB) * num_sms()));
-  const int rc_ = ensure_dynamic_smem(reinterpret_cast<const void*>(policy_loss_grad_kernel<false>),
-                                      int(kFusedSmem));
-  if (rc_) return rc_;
-  policy_loss_grad_kernel<false><<<grid, kFThreads, kFusedSmem, st>>>(p);
-  return check_launch("policy_loss_grad_kernel");
+  // small vocabularies: 3 CTAs/SM (8,192 x 4 policy stages) hide the row-end
+  // barriers better; large: 2 CTAs/SM keep the rows live between the two
+  // passes within L2 (r1_fused_grad_ncu_v1.md)
+  return p.V <= a1_small_vmax() ? policy_loss_grad_ring_small(p, st)
+                                : policy_loss_grad_ring_large(p, st);
 }
 
 int token_stats_ring_small(const A1Params& p, cudaStream_t st);  // token_stats_small.cu
@@ -1044,6 +1065,7 @@ int token_stats_launch(const uint16_t* pol, const uint16_t* ref, const int32_t* 
   }
   return vocab <= a1_small_vmax() ? token_stats_ring_small(p, st) : token_stats_ring_large(p, st);
 }
+#endif  // !YATT_FUSED_SMALL_TU
 #endif
 
 }  // namespace yattb
