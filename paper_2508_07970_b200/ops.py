@@ -91,7 +91,10 @@ def token_stats(policy_logits: torch.Tensor, ref_logits: torch.Tensor, targets: 
         out = torch.empty((4, rows), dtype=torch.float32, device=policy_logits.device)
     elif out.shape != (4, rows):
         raise ValueError(f"out must be [4, {rows}], got {list(out.shape)}")
-    _dev(out, torch.float32, "out")
+    # the four outputs are written as four dense rows: a column slice of a
+    # wider [4, N] buffer is fine (bench.py shards one), a strided row is not
+    if not out.is_cuda or out.dtype != torch.float32 or (rows > 1 and out.stride(1) != 1):
+        raise ValueError("out must be a CUDA float32 [4, rows] tensor with dense rows")
     check(lib().yatt_token_stats(_p(policy_logits), _p(ref_logits), _p(targets), _p(m), rows,
                                  vocab, KL_MODES[kl_mode], _p(out[0]), _p(out[1]), _p(out[2]),
                                  _p(out[3]), _st()))

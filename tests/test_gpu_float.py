@@ -299,6 +299,15 @@ def test_ops_reject_short_per_token_arrays(cuda):
         ops.policy_loss_grad(pol, tgt, x[:4], x[:3])
     with pytest.raises(ValueError, match="shape"):
         ops.policy_loss_grad(pol, tgt, x[:4], x[:4], grad=pol[:2])
+    # token_stats `out`: a column slice of a wider [4, N] buffer (dense rows,
+    # as bench.py passes per rank) is accepted and written in place
+    pol2, ref2, tgt2 = ops.synth_logits(3, 0, 4, 4096, device=cuda)
+    wide = torch.zeros((4, 10), device=cuda)
+    ops.token_stats(pol2, ref2, tgt2, None, "k3", out=wide[:, 3:7])
+    want = torch.stack(ops.token_stats(pol2, ref2, tgt2, None, "k3"))
+    assert torch.equal(wide[:, 3:7], want) and torch.all(wide[:, :3] == 0)
+    with pytest.raises(ValueError, match="dense rows"):
+        ops.token_stats(pol2, ref2, tgt2, None, "k3", out=torch.zeros((4, 8), device=cuda)[:, ::2])
 
 
 @pytest.mark.parametrize("masked", [False, True])
