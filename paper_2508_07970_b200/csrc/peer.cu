@@ -18,7 +18,8 @@
 // identical global result.  A rank can run at most one call ahead of the
 // slowest (it needs everyone's flag), so two slot banks suffice.  The epoch
 // lives in device memory, so the exchange also works under CUDA-graph replay.
-// A wait that exceeds ~10 s sets status and writes NaN instead of hanging.
+// A wait that exceeds 10 s (%globaltimer) sets status and writes NaN instead
+// of hanging; the group is then out of step and should be destroyed.
 #include <cuda_runtime.h>
 
 #include <cstring>
@@ -56,17 +57,25 @@ __device__ __forceinline__ long long* gather_slot(uint8_t* b, int parity, int q)
          (size_t(parity) * kPeerMaxWorld + q) * kGatherWords;
 }
 
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // Thread 0: publish this rank's epoch into every rank's flags and wait until
 // every rank has published it here (~10 s timeout -> status 1, *fail = 1).
 __device__ __forceinline__ void publish_and_wait(const PeerArgs& a, uint64_t epoch, int* fail) {
   uint8_t* mine = a.buf[a.rank];
   __threadfence_system();
   for (int q = 0; q < a.world; ++q) *flag(a.buf[q], a.rank) = epoch;
+  const uint64_t t0 = globaltimer_ns();
   for (int q = 0; q < a.world && !*fail; ++q) {
     long long spins = 0;
     while (*flag(mine, q) < epoch) {
       if (spins > 64) __nanosleep(32);  // tight polling first: the usual wait is ~1 us
-      if (++spins > (1ll << 27)) {      // ~10 s: a rank is gone; fail loudly, do not hang
+      // 10 s of wall time: a rank is gone; fail loudly, do not hang
+      if ((++spins & 1023) == 0 && globaltimer_ns() - t0 > 10000000000ull) {
         *fail = 1;
         *reinterpret_cast<volatile uint32_t*>(mine + kStatusOff) = 1u;
         break;
