@@ -515,7 +515,8 @@ int yatt_synth_floats(uint64_t seed, uint64_t stream_id, int64_t i0, int64_t n,
 /* all_gather / the controller rendezvous), then connects.  Calls are        */
 /* collective (every rank, same order); results are bit-identical on every   */
 /* rank (rank-ordered sum).  A peer that never arrives makes the call write  */
-/* NaN after ~10 s and sets yatt_peer_status to 1 instead of hanging.        */
+/* NaN (-1 for the int64 calls) after 10 s of wall time and sets             */
+/* yatt_peer_status to 1 instead of hanging; destroy the group after that.   */
 /* ------------------------------------------------------------------------ */
 #define YATT_PEER_MAX_WORLD 8
 #define YATT_PEER_HANDLE_BYTES 64
