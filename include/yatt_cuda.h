@@ -381,19 +381,24 @@ int yatt_logits_backward(const uint16_t* d_policy_logits,
 /* L2: HBM bytes 2V read + 2V written per row instead of 6V for              */
 /* yatt_token_stats (policy only) + yatt_logits_backward.  The reference     */
 /* log-probs come from the experience stage (d_ref_logp, per token; NULL =   */
-/* no KL term).  kl_mode K1/K2/K3; token-mean only (config->agg_mode 0,      */
-/* norm = global valid-token count); vocab % 8 == 0, logits and grad 16-byte */
-/* aligned.  Writes per-token logp / entropy / kl (entropy, kl may be NULL)  */
-/* and grad [rows, vocab] bf16 (zero rows where mask == 0); the loss sums    */
-/* follow from yatt_policy_loss on those per-token outputs.                  */
+/* no KL term).  kl_mode K1/K2/K3; all three aggregations: norm = the global */
+/* valid-token count (token-mean) or the global sequence count (seq modes);  */
+/* seq-mean-token-mean also needs d_cu_seqlens and a workspace of           */
+/* yatt_policy_loss_grad_workspace_bytes (per-token scale; 0 bytes for the   */
+/* other modes).  vocab % 8 == 0, logits and grad 16-byte aligned.  Writes   */
+/* per-token logp / entropy / kl (entropy, kl may be NULL) and grad          */
+/* [rows, vocab] bf16 (zero rows where mask == 0); the loss sums follow from */
+/* yatt_policy_loss on those per-token outputs.                              */
 /* Replaces: Train stand-in simcore.cpp:404-406 (new).          */
+size_t yatt_policy_loss_grad_workspace_bytes(int64_t rows, int32_t agg_mode);
 int yatt_policy_loss_grad(const uint16_t* d_policy_logits, const int32_t* d_targets,
                           const uint8_t* d_mask, const float* d_ref_logp,
                           const float* d_old_logp, const float* d_advantages,
-                          int64_t rows, int32_t vocab, const yatt_loss_config* config,
+                          int64_t rows, int32_t vocab, const int64_t* d_cu_seqlens,
+                          int64_t n_seqs, const yatt_loss_config* config,
                           int32_t kl_mode, double norm, float* d_logp,
                           float* d_entropy, float* d_kl, uint16_t* d_grad,
-                          void* stream);
+                          void* d_workspace, size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* A5+A6  dynamic-sampling filter and compaction (bit-exact)                 */

@@ -708,7 +708,8 @@ struct FusedParams {
   int32_t V;
   int32_t kl_mode;  // K1 / K2 / K3
   yatt_loss_config cfg;
-  double inv_norm;  // 1 / global valid-token count (token-mean)
+  double inv_norm;     // 1 / norm (token-mean: global valid tokens; seq modes: global sequences)
+  const float* scale;  // seq-mean-token-mean: per-token 1 / (norm * valid tokens of its sequence)
   float* logp;
   float* ent;
   float* kl;
@@ -750,6 +751,29 @@ __device__ __forceinline__ uint64_t l2_evict_normal_policy() {
   return pol;
 }
 
+
+// seq-mean-token-mean: per-token scale 1 / (norm * valid tokens of its
+// sequence) — one CTA per sequence (grid-stride), tokens outside every
+// sequence keep the zero the launcher wrote (zero gradient).
+__global__ void __launch_bounds__(256) fused_seq_scale_kernel(const uint8_t* mask, const int64_t* cu,
+                                                               int64_t nseq, double inv_norm,
+                                                               float* scale) {
+  __shared__ int red[8];
+  for (int64_t sq = blockIdx.x; sq < nseq; sq += gridDim.x) {
+    const int64_t b = cu[sq], e = cu[sq + 1];
+    int cnt = 0;
+    for (int64_t i = b + threadIdx.x; i < e; i += 256) cnt += (mask == nullptr || mask[i]) ? 1 : 0;
+    cnt = warp_sum(cnt);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    int tot = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) tot += red[k];
+    const float sc = tot > 0 ? float(inv_norm / double(tot)) : 0.f;
+    for (int64_t i = b + threadIdx.x; i < e; i += 256) scale[i] = sc;
+    __syncthreads();
+  }
+}
 
 template <bool kEdges>
 __global__ void __launch_bounds__(kFThreads, kFMinB) policy_loss_grad_kernel(const FusedParams p) {
@@ -827,11 +851,12 @@ __global__ void __launch_bounds__(kFThreads, kFMinB) policy_loss_grad_kernel(con
     float xy = yok ? 0.f : __uint_as_float(0x7fc00000u);  // the target logit (thread 0)
     // the row's per-token inputs, loaded now so the row-end epilogue (while
     // the other warps wait at the barrier) does not wait on global memory
-    float r_old = 0.f, r_adv = 0.f, r_rl = 0.f;
+    float r_old = 0.f, r_adv = 0.f, r_rl = 0.f, r_sc = 0.f;
     if (warp == 0 && lane < 2) {
       r_old = __ldg(p.old_logp + row);
       r_adv = __ldg(p.adv + row);
       r_rl = p.ref_logp ? __ldg(p.ref_logp + row) : 0.f;
+      r_sc = p.scale ? __ldg(p.scale + row) : 0.f;
     }
     acc.reset();
     // ---- pass 1: online log2 LSE + entropy sums ----
@@ -889,7 +914,7 @@ __global__ void __launch_bounds__(kFThreads, kFMinB) policy_loss_grad_kernel(con
         H = kLn2 * (l2s - double(q.w) / double(q.s));
         p.logp[row] = float(lp);
         if (p.ent) p.ent[row] = float(H);
-        tail->coef[1] = float(p.inv_norm * double(p.cfg.entropy_coef));
+        tail->coef[1] = float((p.scale ? double(r_sc) : p.inv_norm) * double(p.cfg.entropy_coef));
         tail->coef[2] = float(lse2);
         tail->coef[3] = float(H);
       }
@@ -912,7 +937,7 @@ __global__ void __launch_bounds__(kFThreads, kFMinB) policy_loss_grad_kernel(con
       if (lane == 0) {
         const double g = gm::dloss_dlogp_pg(lp, double(r_old), double(r_adv), p.cfg) +
                          double(p.cfg.kl_coef) * dkl;
-        tail->coef[0] = float(p.inv_norm * g);
+        tail->coef[0] = float((p.scale ? double(r_sc) : p.inv_norm) * g);
       }
     }
     named_bar_sync(1, kFC);
@@ -971,21 +996,40 @@ int YATT_FUSED_RING(const FusedParams& p, cudaStream_t st) {
 int policy_loss_grad_ring_small(const FusedParams& p, cudaStream_t st);  // token_stats_fused_small.cu
 int a1_small_vmax();
 
+size_t policy_loss_grad_workspace_bytes(int64_t rows, int32_t agg_mode) {
+  return agg_mode == 1 ? size_t(max64(rows, 0)) * sizeof(float) : 0;
+}
+
 int policy_loss_grad_launch(const uint16_t* pol, const int32_t* tgt, const uint8_t* mask,
                             const float* ref_logp, const float* old_logp, const float* adv,
-                            int64_t rows, int32_t vocab, const yatt_loss_config* cfg,
-                            int32_t kl_mode, double norm, float* logp, float* ent, float* kl,
-                            uint16_t* grad, cudaStream_t st) {
+                            int64_t rows, int32_t vocab, const int64_t* cu, int64_t nseq,
+                            const yatt_loss_config* cfg, int32_t kl_mode, double norm,
+                            float* logp, float* ent, float* kl, uint16_t* grad, void* ws,
+                            size_t ws_bytes, cudaStream_t st) {
   YATT_REQUIRE(cfg != nullptr, YATT_ERR_CONFIG, "policy_loss_grad: null config");
   YATT_REQUIRE(norm > 0.0, YATT_ERR_CONFIG, "policy_loss_grad: norm must be > 0");
+  YATT_REQUIRE(cfg->agg_mode >= 0 && cfg->agg_mode <= 2, YATT_ERR_CONFIG,
+               "policy_loss_grad: unknown agg_mode %d", cfg->agg_mode);
+  float* scale = nullptr;
+  if (cfg->agg_mode == 1 && rows > 0) {  // seq-mean-token-mean: per-token scale
+    YATT_REQUIRE(cu != nullptr && nseq > 0, YATT_ERR_CONFIG,
+                 "policy_loss_grad: seq-mean-token-mean needs cu_seqlens");
+    YATT_REQUIRE(ws != nullptr && ws_bytes >= policy_loss_grad_workspace_bytes(rows, 1),
+                 YATT_ERR_WORKSPACE, "policy_loss_grad: workspace too small (%zu < %zu)",
+                 ws_bytes, policy_loss_grad_workspace_bytes(rows, 1));
+    scale = static_cast<float*>(ws);
+    YATT_TRY_CUDA(cudaMemsetAsync(scale, 0, size_t(rows) * sizeof(float), st));
+    fused_seq_scale_kernel<<<unsigned(min64(nseq, int64_t(8) * num_sms())), 256, 0, st>>>(
+        mask, cu, nseq, 1.0 / norm, scale);
+    const int rc = check_launch("fused_seq_scale_kernel");
+    if (rc) return rc;
+  }
   const FusedParams p{pol, tgt, mask, ref_logp, old_logp, adv, rows, vocab, kl_mode, *cfg,
-                      1.0 / norm, logp, ent, kl, grad};
+                      1.0 / norm, scale, logp, ent, kl, grad};
   YATT_REQUIRE(p.V > 0 && p.rows >= 0, YATT_ERR_CONFIG, "policy_loss_grad: bad shape");
   YATT_REQUIRE(p.kl_mode >= YATT_KL_K1 && p.kl_mode <= YATT_KL_K3, YATT_ERR_CONFIG,
                "policy_loss_grad: kl_mode must be k1, k2 or k3 (full-vocabulary KL needs the "
                "reference logits: use yatt_policy_grad_coef + yatt_logits_backward)");
-  YATT_REQUIRE(p.cfg.agg_mode == 0, YATT_ERR_CONFIG,
-               "policy_loss_grad: token-mean aggregation only (agg_mode 0)");
   if (p.rows == 0) return YATT_OK;
   YATT_REQUIRE(p.pol && p.tgt && p.old_logp && p.adv && p.logp && p.grad, YATT_ERR_CONFIG,
                "policy_loss_grad: null pointer");

@@ -572,15 +572,21 @@ void policy_logits_grad(const std::uint16_t* pol, const std::uint16_t* ref,
                                             kl == KlEstimator::kFull ? 1 : 0, grad, stream));
 }
 
+std::size_t policy_loss_grad_workspace_bytes(std::int64_t rows, LossAggregation a) {
+  return yatt_policy_loss_grad_workspace_bytes(rows, static_cast<int32_t>(a));
+}
+
 void policy_loss_grad(const std::uint16_t* pol, const std::int32_t* tgt, const std::uint8_t* mask,
                       const float* ref_logp, const float* old_logp, const float* adv,
-                      std::int64_t rows, int vocab, const PolicyLossConfig& c, KlEstimator kl,
-                      double norm, const TokenStats& out, std::uint16_t* grad, void* stream) {
+                      std::int64_t rows, int vocab, const std::int64_t* cu, std::int64_t nseq,
+                      const PolicyLossConfig& c, KlEstimator kl, double norm,
+                      const TokenStats& out, std::uint16_t* grad, void* ws, std::size_t ws_bytes,
+                      void* stream) {
   c.validate();
   const yatt_loss_config cc = to_c(c);
   detail::throw_status(yatt_policy_loss_grad(pol, tgt, mask, ref_logp, old_logp, adv, rows, vocab,
-                                             &cc, static_cast<int>(kl), norm, out.logp,
-                                             out.entropy, out.kl, grad, stream));
+                                             cu, nseq, &cc, static_cast<int>(kl), norm, out.logp,
+                                             out.entropy, out.kl, grad, ws, ws_bytes, stream));
 }
 
 std::size_t lmhead_workspace_bytes(std::int64_t rows, int vocab, int n_split) {

@@ -25,7 +25,8 @@ def to_f64(bits):
     return (bits.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
 
 
-def _case(cuda, rows, V, kl_mode, ent_coef=0.01, masked=False, seed=5, with_ref=True):
+def _case(cuda, rows, V, kl_mode, ent_coef=0.01, masked=False, seed=5, with_ref=True,
+          agg="token-mean"):
     pol, ref, tgt = ops.synth_logits(seed, 0, rows, V, device=cuda)
     mask = None
     if masked:
@@ -35,10 +36,14 @@ def _case(cuda, rows, V, kl_mode, ent_coef=0.01, masked=False, seed=5, with_ref=
     rlogp = drl if with_ref else None
     old = ops.synth_floats(seed, 104, 0, rows, "old_delta", base=dlp, device=cuda)
     adv = ops.synth_floats(seed, 108, 0, rows, "adv", device=cuda)
-    cfg = ops.loss_config(0.2, 0.28, 0.0, 0.05, ent_coef, "token-mean")
+    cfg = ops.loss_config(0.2, 0.28, 0.0, 0.05, ent_coef, agg)
     nvalid = rows if mask is None else int(mask.sum())
+    cu = None
+    if agg != "token-mean":  # three sequences, one of them empty -> norm = 2 sequences
+        cu = torch.tensor([0, rows // 3, rows // 3, rows], dtype=torch.int64, device=cuda)
+        nvalid = 2
     lp, ent, kl, grad = ops.policy_loss_grad(pol, tgt, old, adv, rlogp, mask, cfg, kl_mode,
-                                             float(nvalid))
+                                             float(nvalid), cu_seqlens=cu)
     torch.cuda.synchronize()
     hp = bf16_np(pol)
     ht = tgt.cpu().numpy()
@@ -59,8 +64,9 @@ def _case(cuda, rows, V, kl_mode, ent_coef=0.01, masked=False, seed=5, with_ref=
         assert np.all(lp.cpu().numpy()[~valid] == 0)
     # gradient vs the fp64 oracle backward, fed the exact logp
     eg, ecoef = O.logits_backward(hp, hp, ht, e_lp, e_rl if with_ref else None,
-                                  old.cpu().numpy(), adv.cpu().numpy(), m, None, 0.2, 0.28, 0.0,
-                                  0.05, ent_coef, 0, kl_mode, float(nvalid))
+                                  old.cpu().numpy(), adv.cpu().numpy(), m,
+                                  None if cu is None else cu.cpu().numpy(), 0.2, 0.28, 0.0,
+                                  0.05, ent_coef, ops.AGG_MODES[agg], kl_mode, float(nvalid))
     got = to_f64(bf16_np(grad))
     x = to_f64(hp)
     lpv = x - ecoef[:, 3:4]
@@ -80,6 +86,16 @@ def _case(cuda, rows, V, kl_mode, ent_coef=0.01, masked=False, seed=5, with_ref=
 @pytest.mark.parametrize("kl_mode", ["k1", "k2", "k3"])
 def test_fused_loss_grad_matches_oracle(cuda, kl_mode):
     _case(cuda, 40, 32000, kl_mode)
+
+
+@pytest.mark.parametrize("agg", ["seq-mean-token-mean", "seq-mean-token-sum"])
+@pytest.mark.parametrize("masked", [False, True])
+def test_fused_seq_aggregations(cuda, agg, masked):
+    """The seq modes: per-token scale 1 / (sequences * valid tokens of the
+    sequence) for seq-mean-token-mean (a pre-kernel over cu_seqlens), 1 /
+    sequences for seq-mean-token-sum — same gradient as the fp64 oracle."""
+    _case(cuda, 45, 4096, "k3", masked=masked, agg=agg)
+    _case(cuda, 6, 152064, "k2", agg=agg)
 
 
 def test_fused_masked_rows_and_no_reference(cuda):
@@ -128,7 +144,7 @@ def test_fused_errors(cuda):
     pol = torch.zeros((2, 16), dtype=torch.bfloat16, device=cuda)
     with pytest.raises(ConfigError):  # full-vocabulary KL needs the reference logits
         ops.policy_loss_grad(pol, tgt, f, f, kl_mode="full")
-    with pytest.raises(ConfigError):  # token-mean only
+    with pytest.raises(ConfigError):  # seq-mean-token-mean needs cu_seqlens
         ops.policy_loss_grad(pol, tgt, f, f, config=ops.loss_config(agg_mode="seq-mean-token-mean"))
     with pytest.raises(ConfigError):
         ops.policy_loss_grad(pol, tgt, f, f, norm=0.0)
