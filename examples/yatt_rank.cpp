@@ -163,7 +163,8 @@ int main() {
     // same gradient as the two-kernel path to bf16 rounding
     auto* f_out = dalloc<float>(size_t(gr) * 3);
     auto* grad2 = dalloc<std::uint16_t>(size_t(gr) * vocab);
-    experience::policy_loss_grad(pol, tgt, nullptr, ref_logp, old, tadv, gr, vocab, nullptr, 0,
+    experience::policy_loss_grad(pol, nullptr, tgt, nullptr, ref_logp, old, tadv, gr, vocab,
+                                 nullptr, 0,
                                  cfg, experience::KlEstimator::kK3, double(rows),
                                  {f_out, nullptr, f_out + gr, f_out + 2 * gr}, grad2);
     std::vector<std::uint16_t> hg2(static_cast<size_t>(vocab));

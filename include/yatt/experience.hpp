@@ -119,15 +119,17 @@ void policy_logits_grad(const std::uint16_t* policy_logits, const std::uint16_t*
 // From the policy logits alone: per-token logp / entropy / kl (vs the stored
 // ref_logp of the experience stage; nullptr = no KL term) AND the bf16
 // gradient dL/d(policy logits); each row is streamed twice, the second read
-// from L2 (HBM 4V bytes per row instead of 6V).  kl: kK1 / kK2 / kK3; all
+// from L2 (HBM 4V bytes per row instead of 6V).  kl: kK1 / kK2 / kK3 (vs
+// ref_logp; ref_logits may be nullptr) or kFull (reads ref_logits); all
 // three aggregations (norm = global valid tokens for token-mean, global
 // sequences for the seq modes; seq-mean-token-mean takes cu_seqlens and a
 // workspace of policy_loss_grad_workspace_bytes); vocab % 8 == 0, logits and
 // grad 16-byte aligned.  out.ref_logp is not written.  The loss sums:
 // policy_loss(out.logp, ...).
 std::size_t policy_loss_grad_workspace_bytes(std::int64_t rows, LossAggregation aggregation);
-void policy_loss_grad(const std::uint16_t* policy_logits, const std::int32_t* targets,
-                      const std::uint8_t* mask, const float* ref_logp, const float* old_logp,
+void policy_loss_grad(const std::uint16_t* policy_logits, const std::uint16_t* ref_logits,
+                      const std::int32_t* targets, const std::uint8_t* mask,
+                      const float* ref_logp, const float* old_logp,
                       const float* advantages, std::int64_t rows, int vocab,
                       const std::int64_t* cu_seqlens, std::int64_t n_seqs,
                       const PolicyLossConfig& config, KlEstimator kl, double norm,

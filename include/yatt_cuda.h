@@ -381,7 +381,9 @@ int yatt_logits_backward(const uint16_t* d_policy_logits,
 /* L2: HBM bytes 2V read + 2V written per row instead of 6V for              */
 /* yatt_token_stats (policy only) + yatt_logits_backward.  The reference     */
 /* log-probs come from the experience stage (d_ref_logp, per token; NULL =   */
-/* no KL term).  kl_mode K1/K2/K3; all three aggregations: norm = the global */
+/* no KL term).  kl_mode K1/K2/K3 use d_ref_logp (d_ref_logits may be NULL);*/
+/* kl_mode FULL reads d_ref_logits (same layout as the policy) in both      */
+/* passes.  All three aggregations: norm = the global                       */
 /* valid-token count (token-mean) or the global sequence count (seq modes);  */
 /* seq-mean-token-mean also needs d_cu_seqlens and a workspace of           */
 /* yatt_policy_loss_grad_workspace_bytes (per-token scale; 0 bytes for the   */
@@ -391,7 +393,8 @@ int yatt_logits_backward(const uint16_t* d_policy_logits,
 /* yatt_policy_loss on those per-token outputs.                              */
 /* Replaces: Train stand-in simcore.cpp:404-406 (new).          */
 size_t yatt_policy_loss_grad_workspace_bytes(int64_t rows, int32_t agg_mode);
-int yatt_policy_loss_grad(const uint16_t* d_policy_logits, const int32_t* d_targets,
+int yatt_policy_loss_grad(const uint16_t* d_policy_logits,
+                          const uint16_t* d_ref_logits, const int32_t* d_targets,
                           const uint8_t* d_mask, const float* d_ref_logp,
                           const float* d_old_logp, const float* d_advantages,
                           int64_t rows, int32_t vocab, const int64_t* d_cu_seqlens,

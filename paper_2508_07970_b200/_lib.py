@@ -125,7 +125,7 @@ SIGNATURES = {
                                                        c_i32, c_f64, c_p, c_p]),
     "yatt_logits_backward": (C.c_int, [c_p, c_p, c_p, c_p, c_i64, c_i32, c_p, c_i32, c_p, c_p]),
     "yatt_policy_loss_grad_workspace_bytes": (c_sz, [c_i64, c_i32]),
-    "yatt_policy_loss_grad": (C.c_int, [c_p] * 6 + [c_i64, c_i32, c_p, c_i64, P(LossConfigC),
+    "yatt_policy_loss_grad": (C.c_int, [c_p] * 7 + [c_i64, c_i32, c_p, c_i64, P(LossConfigC),
                                                     c_i32, c_f64] + [c_p] * 5 + [c_sz, c_p]),
     "yatt_filter_compact_workspace_bytes": (c_sz, [c_i64]),
     "yatt_filter_compact": (C.c_int, [c_p, c_p, c_i64, c_i32, c_p, c_p, c_p, c_p, c_p, c_sz, c_p]),

@@ -77,7 +77,8 @@ int grad_coef_launch(const uint16_t*, const uint16_t*, const int32_t*, const flo
                      const float*, const float*, const float*, const float*, const uint8_t*,
                      int64_t, int32_t, const int64_t*, int64_t, const yatt_loss_config*, int32_t,
                      double, float*, cudaStream_t);
-int policy_loss_grad_launch(const uint16_t*, const int32_t*, const uint8_t*, const float*,
+int policy_loss_grad_launch(const uint16_t*, const uint16_t*, const int32_t*, const uint8_t*,
+                            const float*,
                             const float*, const float*, int64_t, int32_t, const int64_t*, int64_t,
                             const yatt_loss_config*, int32_t, double, float*, float*, float*,
                             uint16_t*, void*, size_t, cudaStream_t);
@@ -511,7 +512,8 @@ size_t yatt_policy_loss_grad_workspace_bytes(int64_t rows, int32_t agg_mode) {
   return policy_loss_grad_workspace_bytes(rows, agg_mode);
 }
 
-int yatt_policy_loss_grad(const uint16_t* pol, const int32_t* tgt, const uint8_t* mask,
+int yatt_policy_loss_grad(const uint16_t* pol, const uint16_t* ref, const int32_t* tgt,
+                          const uint8_t* mask,
                           const float* ref_logp, const float* old_logp, const float* adv,
                           int64_t rows, int32_t vocab, const int64_t* cu, int64_t nseq,
                           const yatt_loss_config* cfg, int32_t kl_mode, double norm, float* logp,
@@ -519,10 +521,12 @@ int yatt_policy_loss_grad(const uint16_t* pol, const int32_t* tgt, const uint8_t
                           void* stream) {
   YATT_ALIGNED("policy_loss_grad", pol, 16);
   YATT_ALIGNED("policy_loss_grad", grad, 16);
+  YATT_ALIGNED("policy_loss_grad", ref, 16);
   YATT_ALIGNED4("policy_loss_grad", tgt, ref_logp, old_logp, adv);
   YATT_ALIGNED4("policy_loss_grad", logp, ent, kl, ws);
   YATT_ALIGNED("policy_loss_grad", cu, 8);
-  return policy_loss_grad_launch(pol, tgt, mask, ref_logp, old_logp, adv, rows, vocab, cu, nseq,
+  return policy_loss_grad_launch(pol, ref, tgt, mask, ref_logp, old_logp, adv, rows, vocab, cu,
+                                 nseq,
                                  cfg, kl_mode, norm, logp, ent, kl, grad, ws, ws_bytes,
                                  as_stream(stream));
 }

@@ -699,6 +699,7 @@ int YATT_A1_RING(const A1Params& p, cudaStream_t st) {
 // ======================================================================
 struct FusedParams {
   const uint16_t* pol;
+  const uint16_t* ref;    // reference logits (full-vocabulary KL only)
   const int32_t* tgt;
   const uint8_t* mask;
   const float* ref_logp;  // per-token reference log-prob (experience stage), may be null
@@ -741,7 +742,7 @@ struct __align__(16) FusedTail {
   uint64_t full[kFStages];
   uint64_t empty[kFStages];
   RowPartial red[kFCW];
-  float coef[4];  // g, h, lse_p (log2 units), H
+  float coef[8];  // g, h, f, lse_p, lse_q (log2 units), H, KL (gm::RowCoef order)
 };
 constexpr size_t kFusedSmem = size_t(kFStages) * kTile * sizeof(uint16_t) + sizeof(FusedTail);
 
@@ -775,15 +776,21 @@ __global__ void __launch_bounds__(256) fused_seq_scale_kernel(const uint8_t* mas
   }
 }
 
-template <bool kEdges>
+// kFull: full-vocabulary KL — every stage holds the policy AND the reference
+// tile (half the stages, the same bytes), pass 1 also accumulates lse_q and
+// sum p (x - z), the epilogue forms KL = sum p (log p - log q) and the f
+// coefficient, pass 2 uses the full gradient (grad_math.cuh).
+template <bool kFull, bool kEdges>
 __global__ void __launch_bounds__(kFThreads, kFMinB) policy_loss_grad_kernel(const FusedParams p) {
+  constexpr int kPS = kFull ? 2 : 1;        // tiles per stage
+  constexpr int kNS = kFStages / kPS;       // stages
   extern __shared__ __align__(128) uint8_t smem[];
   uint16_t* ring = reinterpret_cast<uint16_t*>(smem);
   FusedTail* tail = reinterpret_cast<FusedTail*>(smem + size_t(kFStages) * kTile * sizeof(uint16_t));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t V = p.V;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kFStages; ++s) {
+    for (int s = 0; s < kNS; ++s) {
       mbar_init(&tail->full[s], 1);
       mbar_init(&tail->empty[s], kFCW);
     }
@@ -806,15 +813,18 @@ __global__ void __launch_bounds__(kFThreads, kFMinB) policy_loss_grad_kernel(con
         const int64_t S = kEdges ? ((h + V + 7) & ~int64_t(7)) : V;
         const int ntiles_r = int((S + kTile - 1) / kTile);
         const uint16_t* gp = p.pol + row * V - h;
+        const uint16_t* gq = kFull ? p.ref + row * V - h : nullptr;
         for (int pass = 0; pass < 2; ++pass) {
           for (int t = 0; t < ntiles_r; ++t) {
             const int64_t e0 = int64_t(t) * kTile;
             const uint32_t n = uint32_t(min64(kTile, S - e0));
             mbar_wait(&tail->empty[stage], phase ^ 1u);
-            mbar_arrive_expect_tx(&tail->full[stage], 2u * n);
-            bulk_g2s(ring + size_t(stage) * kTile, gp + e0, 2u * n, &tail->full[stage],
-                     pass == 0 ? keep : drop);
-            if (++stage == kFStages) {
+            mbar_arrive_expect_tx(&tail->full[stage], 2u * n * kPS);
+            uint16_t* dst = ring + size_t(stage) * kPS * kTile;
+            const uint64_t pol = pass == 0 ? keep : drop;
+            bulk_g2s(dst, gp + e0, 2u * n, &tail->full[stage], pol);
+            if (kFull) bulk_g2s(dst + kTile, gq + e0, 2u * n, &tail->full[stage], pol);
+            if (++stage == kNS) {
               stage = 0;
               phase ^= 1u;
             }
@@ -829,7 +839,7 @@ __global__ void __launch_bounds__(kFThreads, kFMinB) policy_loss_grad_kernel(con
   const int tid = threadIdx.x;
   int stage = 0;
   uint32_t phase = 0;
-  Acc<false, false> acc;
+  Acc<kFull, kFull> acc;
   for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
     const int h = kEdges ? int((row * V) & 7) : 0;
     const int64_t S = kEdges ? ((h + V + 7) & ~int64_t(7)) : V;
@@ -859,70 +869,96 @@ __global__ void __launch_bounds__(kFThreads, kFMinB) policy_loss_grad_kernel(con
       r_sc = p.scale ? __ldg(p.scale + row) : 0.f;
     }
     acc.reset();
-    // ---- pass 1: online log2 LSE + entropy sums ----
+    // ---- pass 1: online log2 LSE(s) + entropy (+ full-KL) sums ----
     for (int t = 0; t < ntiles_r; ++t) {
       const int64_t e0 = int64_t(t) * kTile;
       const int nvec = int(min64(kTile, S - e0) >> 3);
-      const uint16_t* sp = ring + size_t(stage) * kTile;
+      const uint16_t* sp = ring + size_t(stage) * kPS * kTile;
+      const uint16_t* sq = sp + kTile;
       mbar_wait(&tail->full[stage], phase);
       if (tid == 0 && yok && ys >= e0 && ys < e0 + kTile)
         xy = __uint_as_float(uint32_t(sp[ys - e0]) << 16);
-      uint4 P[kFVpt];
+      uint4 P[kFVpt], Q[kFVpt];
 #pragma unroll
       for (int i = 0; i < kFVpt; ++i) {
         const int v = tid + i * kFC;
         const bool in = nvec == kVecPerTile || v < nvec;
-        P[i] = in ? lds128(sp + v * 8) : make_uint4(kNegInf2, kNegInf2, kNegInf2, kNegInf2);
+        const uint4 ninf = make_uint4(kNegInf2, kNegInf2, kNegInf2, kNegInf2);
+        P[i] = in ? lds128(sp + v * 8) : ninf;
+        Q[i] = kFull ? (in ? lds128(sq + v * 8) : ninf) : P[i];
         if (kEdges) {
           const int64_t j0 = e0 + int64_t(v) * 8 - h;
-          if (in && (j0 < 0 || j0 + 8 > V))
-            P[i] = keep_range(P[i], int(max64(0, -j0)), int(min64(8, V - j0)));
+          if (in && (j0 < 0 || j0 + 8 > V)) {
+            const int lo = int(max64(0, -j0)), hi = int(min64(8, V - j0));
+            P[i] = keep_range(P[i], lo, hi);
+            if (kFull) Q[i] = keep_range(Q[i], lo, hi);
+          }
         }
         P[i] = floor_policy(P[i]);
+        if (kFull) Q[i] = floor_policy(Q[i]);  // x - z finite when both are -inf
       }
-      uint32_t mpv = vmax4(P[0]);
+      uint32_t mpv = vmax4(P[0]), mqv = kFull ? vmax4(Q[0]) : 0u;
 #pragma unroll
-      for (int i = 1; i < kFVpt; ++i) mpv = bmax2(mpv, vmax4(P[i]));
+      for (int i = 1; i < kFVpt; ++i) {
+        mpv = bmax2(mpv, vmax4(P[i]));
+        if (kFull) mqv = bmax2(mqv, vmax4(Q[i]));
+      }
       const float fmp = pair_max(mpv);
       if (fmp > acc.thr_p) acc.rebase_p(fmp);
+      if (kFull) {
+        const float fmq = pair_max(mqv);
+        if (fmq > acc.thr_q) acc.rebase_q(fmq);
+      }
 #pragma unroll
-      for (int i = 0; i < kFVpt; ++i) acc.step(P[i], P[i]);
+      for (int i = 0; i < kFVpt; ++i) acc.step(P[i], Q[i]);
       __syncwarp();
       if (lane == 0) mbar_arrive(&tail->empty[stage]);
-      if (++stage == kFStages) {
+      if (++stage == kNS) {
         stage = 0;
         phase ^= 1u;
       }
     }
-    RowPartial r{acc.mp, Acc<false, false>::total(acc.s), Acc<false, false>::total(acc.w),
-                 float(kMinitial), 0.f, 0.f};
-    r = warp_combine<false>(r);
+    using A = Acc<kFull, kFull>;
+    RowPartial r{acc.mp, A::total(acc.s), A::total(acc.w), kFull ? acc.mq : float(kMinitial),
+                 kFull ? A::total(acc.sq) : 0.f, kFull ? A::total(acc.u) : 0.f};
+    r = warp_combine<kFull>(r);
     if (lane == 0) tail->red[warp] = r;
     named_bar_sync(1, kFC);
     if (warp == 0) {
       RowPartial q = tail->red[lane & (kFCW - 1)];
 #pragma unroll
       for (int off = kFCW / 2; off > 0; off >>= 1) q = combine(q, shfl_partial(q, off));
-      // fp64 row epilogue: lane 0 forms logp / H, then lane 0 takes the
-      // surrogate (exp of the ratio) while lane 1 takes the KL estimator
-      // (expm1) in parallel
-      double lp = 0.0, H = 0.0;
+      // fp64 row epilogue: lane 0 forms logp / H (and the full KL), then lane
+      // 0 takes the surrogate (exp of the ratio) while lane 1 takes the
+      // per-token KL estimator (expm1) in parallel
+      const double sc = p.scale ? double(r_sc) : p.inv_norm;
+      double lp = 0.0;
       if (lane == 0) {
         const double l2s = log2(double(q.s));
         const double lse2 = double(q.mp) + l2s;
         lp = double(xy) - kLn2 * lse2;
-        H = kLn2 * (l2s - double(q.w) / double(q.s));
+        const double H = kLn2 * (l2s - double(q.w) / double(q.s));
         p.logp[row] = float(lp);
         if (p.ent) p.ent[row] = float(H);
-        tail->coef[1] = float((p.scale ? double(r_sc) : p.inv_norm) * double(p.cfg.entropy_coef));
-        tail->coef[2] = float(lse2);
-        tail->coef[3] = float(H);
+        tail->coef[1] = float(sc * double(p.cfg.entropy_coef));
+        tail->coef[3] = float(lse2);
+        tail->coef[5] = float(H);
+        if (kFull) {  // KL = sum p (log p - log q), without cancelling two lse
+          const double dlse = kLn2 * ((double(q.mq) - double(q.mp)) +
+                                      log2(double(q.sq) / double(q.s)));
+          const double klf = double(q.u) / double(q.s) + dlse;
+          if (p.kl) p.kl[row] = float(klf);
+          tail->coef[2] = float(sc * double(p.cfg.kl_coef));
+          tail->coef[4] = float(double(q.mq) + log2(double(q.sq)));
+          tail->coef[6] = float(klf);
+        } else {
+          tail->coef[2] = tail->coef[4] = tail->coef[6] = 0.f;
+        }
       }
       lp = __shfl_sync(0xffffffffu, lp, 0);
-      const double rl = p.ref_logp ? double(r_rl) : lp;
       double dkl = 0.0;
-      if (lane == 1) {  // the per-token KL estimator and its derivative
-        const double delta = rl - lp;
+      if (!kFull && lane == 1) {  // the per-token KL estimator and its derivative
+        const double delta = (p.ref_logp ? double(r_rl) : lp) - lp;
         double k;
         if (p.kl_mode == YATT_KL_K1) k = -delta, dkl = 1.0;
         else if (p.kl_mode == YATT_KL_K2) k = 0.5 * delta * delta, dkl = -delta;
@@ -937,37 +973,44 @@ __global__ void __launch_bounds__(kFThreads, kFMinB) policy_loss_grad_kernel(con
       if (lane == 0) {
         const double g = gm::dloss_dlogp_pg(lp, double(r_old), double(r_adv), p.cfg) +
                          double(p.cfg.kl_coef) * dkl;
-        tail->coef[0] = float((p.scale ? double(r_sc) : p.inv_norm) * g);
+        tail->coef[0] = float(sc * g);
       }
     }
     named_bar_sync(1, kFC);
-    const gm::RowCoef c{tail->coef[0], tail->coef[1], 0.f, tail->coef[2], 0.f, tail->coef[3], 0.f};
+    const gm::RowCoef c{tail->coef[0], tail->coef[1], tail->coef[2], tail->coef[3],
+                        tail->coef[4], tail->coef[5], tail->coef[6]};
     // ---- pass 2: the gradient (second read of the row, from L2) ----
     for (int t = 0; t < ntiles_r; ++t) {
       const int64_t e0 = int64_t(t) * kTile;
       const int nvec = int(min64(kTile, S - e0) >> 3);
-      const uint16_t* sp = ring + size_t(stage) * kTile;
+      const uint16_t* sp = ring + size_t(stage) * kPS * kTile;
+      const uint16_t* sq = sp + kTile;
       mbar_wait(&tail->full[stage], phase);
       if (nvec == kVecPerTile) {
-        uint4 P[kFVpt];
+        uint4 P[kFVpt], Q[kFVpt];
 #pragma unroll
-        for (int i = 0; i < kFVpt; ++i) P[i] = floor_policy(lds128(sp + (tid + i * kFC) * 8));
+        for (int i = 0; i < kFVpt; ++i) {
+          P[i] = floor_policy(lds128(sp + (tid + i * kFC) * 8));
+          Q[i] = kFull ? floor_policy(lds128(sq + (tid + i * kFC) * 8)) : P[i];
+        }
 #pragma unroll
         for (int i = 0; i < kFVpt; ++i)
-          store_grad<kEdges>(gs, e0 + (tid + i * kFC) * 8, grad_vec<false>(P[i], P[i], c), h, V);
+          store_grad<kEdges>(gs, e0 + (tid + i * kFC) * 8, grad_vec<kFull>(P[i], Q[i], c), h, V);
       } else {
         for (int v = tid; v < nvec; v += kFC) {
           const uint4 P = floor_policy(lds128(sp + v * 8));
-          store_grad<kEdges>(gs, e0 + v * 8, grad_vec<false>(P, P, c), h, V);
+          const uint4 Q = kFull ? floor_policy(lds128(sq + v * 8)) : P;
+          store_grad<kEdges>(gs, e0 + v * 8, grad_vec<kFull>(P, Q, c), h, V);
         }
       }
       if (yok && ys >= e0 && ys < e0 + kTile && tid == ((ys - e0) >> 3) % kFC) {
         const float x = __uint_as_float(uint32_t(sp[ys - e0]) << 16);
-        gs[ys] = uint16_t(pack_bf16x2(target_grad<false>(x, 0.f, c), 0.f) & 0xffffu);
+        const float z = kFull ? __uint_as_float(uint32_t(sq[ys - e0]) << 16) : 0.f;
+        gs[ys] = uint16_t(pack_bf16x2(target_grad<kFull>(x, z, c), 0.f) & 0xffffu);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&tail->empty[stage]);
-      if (++stage == kFStages) {
+      if (++stage == kNS) {
         stage = 0;
         phase ^= 1u;
       }
@@ -985,10 +1028,24 @@ __global__ void __launch_bounds__(kFThreads, kFMinB) policy_loss_grad_kernel(con
 // The fused kernel with this translation unit's shape (validated params).
 int YATT_FUSED_RING(const FusedParams& p, cudaStream_t st) {
   const int grid = int(min64(p.rows, int64_t(kFMinB) * num_sms()));
-  const int rc_ = ensure_dynamic_smem(reinterpret_cast<const void*>(policy_loss_grad_kernel<false>),
-                                      int(kFusedSmem));
+#ifdef YATT_FUSED_SMALL_TU  // the full-KL form would spill at 3 CTAs/SM: large shape only
+  YATT_REQUIRE(p.kl_mode != YATT_KL_FULL, YATT_ERR_CONFIG, "policy_loss_grad: internal dispatch");
+  const bool full = false;
+  const void* k = reinterpret_cast<const void*>(policy_loss_grad_kernel<false, false>);
+#else
+  const bool full = p.kl_mode == YATT_KL_FULL;
+  const void* k = full ? reinterpret_cast<const void*>(policy_loss_grad_kernel<true, false>)
+                       : reinterpret_cast<const void*>(policy_loss_grad_kernel<false, false>);
+#endif
+  const int rc_ = ensure_dynamic_smem(k, int(kFusedSmem));
   if (rc_) return rc_;
-  policy_loss_grad_kernel<false><<<grid, kFThreads, kFusedSmem, st>>>(p);
+#ifndef YATT_FUSED_SMALL_TU
+  if (full)
+    policy_loss_grad_kernel<true, false><<<grid, kFThreads, kFusedSmem, st>>>(p);
+  else
+#endif
+    policy_loss_grad_kernel<false, false><<<grid, kFThreads, kFusedSmem, st>>>(p);
+  (void)full;
   return check_launch("policy_loss_grad_kernel");
 }
 
@@ -1000,8 +1057,9 @@ size_t policy_loss_grad_workspace_bytes(int64_t rows, int32_t agg_mode) {
   return agg_mode == 1 ? size_t(max64(rows, 0)) * sizeof(float) : 0;
 }
 
-int policy_loss_grad_launch(const uint16_t* pol, const int32_t* tgt, const uint8_t* mask,
-                            const float* ref_logp, const float* old_logp, const float* adv,
+int policy_loss_grad_launch(const uint16_t* pol, const uint16_t* ref, const int32_t* tgt,
+                            const uint8_t* mask, const float* ref_logp, const float* old_logp,
+                            const float* adv,
                             int64_t rows, int32_t vocab, const int64_t* cu, int64_t nseq,
                             const yatt_loss_config* cfg, int32_t kl_mode, double norm,
                             float* logp, float* ent, float* kl, uint16_t* grad, void* ws,
@@ -1024,12 +1082,13 @@ int policy_loss_grad_launch(const uint16_t* pol, const int32_t* tgt, const uint8
     const int rc = check_launch("fused_seq_scale_kernel");
     if (rc) return rc;
   }
-  const FusedParams p{pol, tgt, mask, ref_logp, old_logp, adv, rows, vocab, kl_mode, *cfg,
+  const FusedParams p{pol, ref, tgt, mask, ref_logp, old_logp, adv, rows, vocab, kl_mode, *cfg,
                       1.0 / norm, scale, logp, ent, kl, grad};
   YATT_REQUIRE(p.V > 0 && p.rows >= 0, YATT_ERR_CONFIG, "policy_loss_grad: bad shape");
-  YATT_REQUIRE(p.kl_mode >= YATT_KL_K1 && p.kl_mode <= YATT_KL_K3, YATT_ERR_CONFIG,
-               "policy_loss_grad: kl_mode must be k1, k2 or k3 (full-vocabulary KL needs the "
-               "reference logits: use yatt_policy_grad_coef + yatt_logits_backward)");
+  YATT_REQUIRE(p.kl_mode >= YATT_KL_K1 && p.kl_mode <= YATT_KL_FULL, YATT_ERR_CONFIG,
+               "policy_loss_grad: unknown kl_mode %d", p.kl_mode);
+  YATT_REQUIRE(p.kl_mode != YATT_KL_FULL || p.ref != nullptr, YATT_ERR_CONFIG,
+               "policy_loss_grad: the full-vocabulary KL needs the reference logits");
   if (p.rows == 0) return YATT_OK;
   YATT_REQUIRE(p.pol && p.tgt && p.old_logp && p.adv && p.logp && p.grad, YATT_ERR_CONFIG,
                "policy_loss_grad: null pointer");
@@ -1040,8 +1099,8 @@ int policy_loss_grad_launch(const uint16_t* pol, const int32_t* tgt, const uint8
   // small vocabularies: 3 CTAs/SM (8,192 x 4 policy stages) hide the row-end
   // barriers better; large: 2 CTAs/SM keep the rows live between the two
   // passes within L2 (r1_fused_grad_ncu_v1.md)
-  return p.V <= a1_small_vmax() ? policy_loss_grad_ring_small(p, st)
-                                : policy_loss_grad_ring_large(p, st);
+  return p.V <= a1_small_vmax() && p.kl_mode != YATT_KL_FULL ? policy_loss_grad_ring_small(p, st)
+                                                              : policy_loss_grad_ring_large(p, st);
 }
 
 int token_stats_ring_small(const A1Params& p, cudaStream_t st);  // token_stats_small.cu

@@ -576,15 +576,15 @@ std::size_t policy_loss_grad_workspace_bytes(std::int64_t rows, LossAggregation 
   return yatt_policy_loss_grad_workspace_bytes(rows, static_cast<int32_t>(a));
 }
 
-void policy_loss_grad(const std::uint16_t* pol, const std::int32_t* tgt, const std::uint8_t* mask,
-                      const float* ref_logp, const float* old_logp, const float* adv,
+void policy_loss_grad(const std::uint16_t* pol, const std::uint16_t* ref, const std::int32_t* tgt,
+                      const std::uint8_t* mask, const float* ref_logp, const float* old_logp, const float* adv,
                       std::int64_t rows, int vocab, const std::int64_t* cu, std::int64_t nseq,
                       const PolicyLossConfig& c, KlEstimator kl, double norm,
                       const TokenStats& out, std::uint16_t* grad, void* ws, std::size_t ws_bytes,
                       void* stream) {
   c.validate();
   const yatt_loss_config cc = to_c(c);
-  detail::throw_status(yatt_policy_loss_grad(pol, tgt, mask, ref_logp, old_logp, adv, rows, vocab,
+  detail::throw_status(yatt_policy_loss_grad(pol, ref, tgt, mask, ref_logp, old_logp, adv, rows, vocab,
                                              cu, nseq, &cc, static_cast<int>(kl), norm, out.logp,
                                              out.entropy, out.kl, grad, ws, ws_bytes, stream));
 }

@@ -394,17 +394,22 @@ def kl_from_logps(logp: torch.Tensor, ref_logp: torch.Tensor, kl_mode: str = "k3
 
 # --------------------------------------------------- backward (§8f #1) ----
 def policy_loss_grad(policy_logits, targets, old_logp, advantages, ref_logp=None, mask=None,
-                     config=None, kl_mode="k3", norm: float = 1.0, grad=None, cu_seqlens=None):
+                     config=None, kl_mode="k3", norm: float = 1.0, grad=None, cu_seqlens=None,
+                     ref_logits=None):
     """Fused training-side op (yatt_policy_loss_grad): from the policy logits
     alone, the per-token (logp, entropy, kl vs the stored ref_logp) AND
     dL/d(policy logits) (bf16 [rows, V]) of the A4 loss, each row streamed
     twice with the second read from L2.  norm: global valid-token count
     (token-mean) or global sequence count (seq modes; seq-mean-token-mean
-    also takes cu_seqlens).  Returns (logp, entropy, kl, grad); the loss sums
+    also takes cu_seqlens).  kl_mode "full" reads ref_logits (the
+    full-vocabulary KL) instead of ref_logp.  Returns (logp, entropy, kl,
+    grad); the loss sums
     follow from policy_loss(logp, old_logp, advantages, kl, entropy, ...)."""
     cfg = config or loss_config()
-    _devs(torch.bfloat16, policy_logits=policy_logits, grad=grad)
+    _devs(torch.bfloat16, policy_logits=policy_logits, grad=grad, ref_logits=ref_logits)
     _devs(torch.float32, ref_logp=ref_logp, old_logp=old_logp, advantages=advantages)
+    if ref_logits is not None and ref_logits.shape != policy_logits.shape:
+        raise ValueError("ref_logits must have the shape of policy_logits")
     _dev(targets, torch.int32, "targets")
     if cu_seqlens is not None:
         _dev(cu_seqlens, torch.int64, "cu_seqlens")
@@ -419,7 +424,8 @@ def policy_loss_grad(policy_logits, targets, old_logp, advantages, ref_logp=None
     wsb = lib().yatt_policy_loss_grad_workspace_bytes(rows, cfg.agg_mode)
     ws = torch.empty((max(wsb, 16),), dtype=torch.uint8, device=policy_logits.device)
     nseq = 0 if cu_seqlens is None else cu_seqlens.numel() - 1
-    check(lib().yatt_policy_loss_grad(_p(policy_logits), _p(targets), _p(_mask(mask)),
+    check(lib().yatt_policy_loss_grad(_p(policy_logits), _p(ref_logits), _p(targets),
+                                      _p(_mask(mask)),
                                       _p(ref_logp), _p(old_logp), _p(advantages), rows, vocab,
                                       _p(cu_seqlens), nseq, C.byref(cfg), KL_MODES[kl_mode],
                                       float(norm), _p(out[0]), _p(out[1]), _p(out[2]), _p(grad),

@@ -42,28 +42,33 @@ def _case(cuda, rows, V, kl_mode, ent_coef=0.01, masked=False, seed=5, with_ref=
     if agg != "token-mean":  # three sequences, one of them empty -> norm = 2 sequences
         cu = torch.tensor([0, rows // 3, rows // 3, rows], dtype=torch.int64, device=cuda)
         nvalid = 2
-    lp, ent, kl, grad = ops.policy_loss_grad(pol, tgt, old, adv, rlogp, mask, cfg, kl_mode,
-                                             float(nvalid), cu_seqlens=cu)
+    full = kl_mode == "full"
+    lp, ent, kl, grad = ops.policy_loss_grad(pol, tgt, old, adv, None if full else rlogp, mask,
+                                             cfg, kl_mode, float(nvalid), cu_seqlens=cu,
+                                             ref_logits=ref if full else None)
     torch.cuda.synchronize()
     hp = bf16_np(pol)
     ht = tgt.cpu().numpy()
     m = None if mask is None else mask.cpu().numpy()
     valid = np.ones(rows, bool) if m is None else m.astype(bool)
     # per-token terms vs the fp64 oracle
-    e_lp, _, e_ent, _ = O.token_stats(hp, hp, ht, None, "k3")
+    hr = bf16_np(ref)
+    e_lp, _, e_ent, e_klf = O.token_stats(hp, hr, ht, None, "full")
     assert O.max_rel_error(lp.cpu().numpy()[valid], e_lp[valid]) <= 1e-5
     assert O.max_rel_error(ent.cpu().numpy()[valid], e_ent[valid]) <= 1e-5
     e_rl = drl.cpu().numpy().astype(np.float64) if with_ref else e_lp
     d = e_rl - e_lp
-    e_kl = {"k1": -d, "k2": 0.5 * d * d, "k3": np.expm1(d) - d}[kl_mode]
+    e_kl = {"k1": -d, "k2": 0.5 * d * d, "k3": np.expm1(d) - d, "full": e_klf}[kl_mode]
     gk = kl.cpu().numpy().astype(np.float64)
-    # kl of (rl - logp): conditioned on |d| (logp carries the 1e-5 A1 bar)
-    tol_kl = 1e-5 * np.abs(e_kl) + 2e-5 * np.abs(e_lp) * (np.abs(d) + 1.0)
+    # kl of (rl - logp): conditioned on |d| (logp carries the 1e-5 A1 bar);
+    # full KL: the A1 bar
+    tol_kl = (1e-5 * np.abs(e_kl) + 2e-5 * np.abs(e_lp) * (np.abs(d) + 1.0) if not full
+              else 1e-5 * np.abs(e_kl) + 1e-7 * np.log(V))
     assert np.all(np.abs(gk[valid] - e_kl[valid]) <= tol_kl[valid])
     if m is not None:
         assert np.all(lp.cpu().numpy()[~valid] == 0)
     # gradient vs the fp64 oracle backward, fed the exact logp
-    eg, ecoef = O.logits_backward(hp, hp, ht, e_lp, e_rl if with_ref else None,
+    eg, ecoef = O.logits_backward(hp, hr, ht, e_lp, e_rl if with_ref else None,
                                   old.cpu().numpy(), adv.cpu().numpy(), m,
                                   None if cu is None else cu.cpu().numpy(), 0.2, 0.28, 0.0,
                                   0.05, ent_coef, ops.AGG_MODES[agg], kl_mode, float(nvalid))
@@ -73,6 +78,11 @@ def _case(cuda, rows, V, kl_mode, ent_coef=0.01, masked=False, seed=5, with_ref=
     p = np.exp(lpv)
     H = -(p * lpv).sum(1, keepdims=True)
     cond = np.abs(ecoef[:, 0:1]) + np.abs(ecoef[:, 1:2]) * (np.abs(lpv) + H)
+    if full:
+        z = to_f64(hr)
+        zm = z.max(1, keepdims=True)
+        lq = z - (zm + np.log(np.exp(z - zm).sum(1, keepdims=True)))
+        cond = cond + np.abs(ecoef[:, 2:3]) * (np.abs(lpv) + np.abs(lq) + 1.0)
     tol = 2.0 ** -8 * np.abs(eg) + 1e-5 * p * cond + 1e-30
     # the target element carries + g: relative 1e-5 of g from the logp used
     tol[np.arange(rows), ht] += 1e-5 * np.abs(ecoef[:, 0])
@@ -83,9 +93,17 @@ def _case(cuda, rows, V, kl_mode, ent_coef=0.01, masked=False, seed=5, with_ref=
     return pol, ref, tgt, mask, old, adv, rlogp, cfg, nvalid, got
 
 
-@pytest.mark.parametrize("kl_mode", ["k1", "k2", "k3"])
+@pytest.mark.parametrize("kl_mode", ["k1", "k2", "k3", "full"])
 def test_fused_loss_grad_matches_oracle(cuda, kl_mode):
     _case(cuda, 40, 32000, kl_mode)
+
+
+@pytest.mark.parametrize("agg", ["token-mean", "seq-mean-token-mean"])
+def test_fused_full_kl(cuda, agg):
+    """The full-vocabulary KL: policy AND reference tiles in every stage,
+    lse_q and sum p (x - z) in pass 1, the f term in pass 2."""
+    _case(cuda, 20, 152064, "full", masked=True, agg=agg)
+    _case(cuda, 33, 4096, "full", agg=agg)
 
 
 @pytest.mark.parametrize("agg", ["seq-mean-token-mean", "seq-mean-token-sum"])
@@ -143,7 +161,7 @@ def test_fused_errors(cuda):
         ops.policy_loss_grad(pol, tgt, f, f)
     pol = torch.zeros((2, 16), dtype=torch.bfloat16, device=cuda)
     with pytest.raises(ConfigError):  # full-vocabulary KL needs the reference logits
-        ops.policy_loss_grad(pol, tgt, f, f, kl_mode="full")
+        ops.policy_loss_grad(pol, tgt, f, f, kl_mode="full", ref_logits=None)
     with pytest.raises(ConfigError):  # seq-mean-token-mean needs cu_seqlens
         ops.policy_loss_grad(pol, tgt, f, f, config=ops.loss_config(agg_mode="seq-mean-token-mean"))
     with pytest.raises(ConfigError):

@@ -227,6 +227,20 @@ def main():
         ms = timeit(two_kernel, iters=10)
         report(f"token_stats + logits_grad (two-kernel form) {rows} x {V}", ms,
                rows * (8 * V + 60), rows, "tokens")
+        # full-vocabulary KL: policy + reference logits in both passes
+        # (HBM: 4V read + 2V written per row; the second read from L2)
+        ms = timeit(lambda: ops.policy_loss_grad(pol, tgt, old, a, None, None, cfg, "full",
+                                                 float(rows), grad, ref_logits=ref), iters=10)
+        report(f"policy_loss_grad fused FULL KL {rows} x {V}", ms, rows * (6 * V + 24), rows,
+               "tokens")
+
+        def two_kernel_full():
+            s_ = ops.token_stats(pol, ref, tgt, None, "full")
+            ops.logits_grad(pol, ref, tgt, s_[0], s_[1], old, a, s_[2], s_[3], None, None, cfg,
+                            "full", float(rows), grad)
+        ms = timeit(two_kernel_full, iters=10)
+        report(f"token_stats + logits_grad FULL KL (two-kernel form) {rows} x {V}", ms,
+               rows * (10 * V + 60), rows, "tokens")
         del pol, ref, tgt, grad
         torch.cuda.empty_cache()
 
