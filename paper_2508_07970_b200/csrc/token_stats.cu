@@ -638,7 +638,7 @@ __global__ void __launch_bounds__(kConsumers) token_stats_fixup_kernel(const A1P
 
 }  // namespace
 
-#ifndef YATT_FUSED_SMALL_TU  // token_stats_fused_small.cu compiles only the fused kernel
+#ifndef YATT_FUSED_ONLY_TU  // token_stats_fused_{small,mid}.cu compile only the fused kernel
 #ifdef YATT_A1_SMALL_TU
 #define YATT_A1_RING token_stats_ring_small
 #else
@@ -679,7 +679,7 @@ int YATT_A1_RING(const A1Params& p, cudaStream_t st) {
   return check_launch("token_stats_fixup_kernel");
 }
 
-#endif  // !YATT_FUSED_SMALL_TU
+#endif  // !YATT_FUSED_ONLY_TU
 
 #ifndef YATT_A1_SMALL_TU
 
@@ -724,12 +724,14 @@ using gm::pack_bf16x2;
 using gm::store_grad;
 using gm::target_grad;
 
-// Shape: YATT_FUSED_CW consumer warps per CTA.  8: A1's shape (2 CTAs/SM,
-// 6 policy stages of 16 KB each); 16: one CTA per SM with 12 stages — the
-// same warps and bytes in flight per SM but half the rows live between their
-// two passes (L2 reuse of the second read).
+// Shape: YATT_FUSED_CW consumer warps per CTA.  8: 2 CTAs/SM, 6 policy
+// stages of 16 KB each (the small-vocabulary TU: 3 CTAs/SM, 4 stages); 16
+// (the default for V > 60,000): one CTA per SM with 12 stages — the same
+// warps and bytes in flight per SM but half the rows live between their two
+// passes, so more of the second read hits L2: k3 3.76 vs 4.02 ms, full KL
+// 6.07 vs 7.23 ms at 32,768 x 152,064 (r1_fused_grad_ncu_v1.md).
 #ifndef YATT_FUSED_CW
-#define YATT_FUSED_CW 8
+#define YATT_FUSED_CW 16
 #endif
 constexpr int kFCW = YATT_FUSED_CW;
 constexpr int kFC = kFCW * 32;
@@ -1020,15 +1022,17 @@ __global__ void __launch_bounds__(kFThreads, kFMinB) policy_loss_grad_kernel(con
 
 }  // namespace
 
-#ifdef YATT_FUSED_SMALL_TU
+#if defined(YATT_FUSED_SMALL_TU)
 #define YATT_FUSED_RING policy_loss_grad_ring_small
+#elif defined(YATT_FUSED_MID_TU)
+#define YATT_FUSED_RING policy_loss_grad_ring_mid
 #else
 #define YATT_FUSED_RING policy_loss_grad_ring_large
 #endif
 // The fused kernel with this translation unit's shape (validated params).
 int YATT_FUSED_RING(const FusedParams& p, cudaStream_t st) {
   const int grid = int(min64(p.rows, int64_t(kFMinB) * num_sms()));
-#ifdef YATT_FUSED_SMALL_TU  // the full-KL form would spill at 3 CTAs/SM: large shape only
+#ifdef YATT_FUSED_SMALL_TU  // the full-KL form would spill at 3 CTAs/SM: the mid TU takes it
   YATT_REQUIRE(p.kl_mode != YATT_KL_FULL, YATT_ERR_CONFIG, "policy_loss_grad: internal dispatch");
   const bool full = false;
   const void* k = reinterpret_cast<const void*>(policy_loss_grad_kernel<false, false>);
@@ -1049,8 +1053,9 @@ int YATT_FUSED_RING(const FusedParams& p, cudaStream_t st) {
   return check_launch("policy_loss_grad_kernel");
 }
 
-#ifndef YATT_FUSED_SMALL_TU
+#ifndef YATT_FUSED_ONLY_TU
 int policy_loss_grad_ring_small(const FusedParams& p, cudaStream_t st);  // token_stats_fused_small.cu
+int policy_loss_grad_ring_mid(const FusedParams& p, cudaStream_t st);    // token_stats_fused_mid.cu
 int a1_small_vmax();
 
 size_t policy_loss_grad_workspace_bytes(int64_t rows, int32_t agg_mode) {
@@ -1099,8 +1104,13 @@ int policy_loss_grad_launch(const uint16_t* pol, const uint16_t* ref, const int3
   // small vocabularies: 3 CTAs/SM (8,192 x 4 policy stages) hide the row-end
   // barriers better; large: 2 CTAs/SM keep the rows live between the two
   // passes within L2 (r1_fused_grad_ncu_v1.md)
-  return p.V <= a1_small_vmax() && p.kl_mode != YATT_KL_FULL ? policy_loss_grad_ring_small(p, st)
-                                                              : policy_loss_grad_ring_large(p, st);
+  // shapes (measured, r1_fused_grad_ncu_v1.md): V <= 60,000 — 3 CTAs/SM of 8
+  // warps (the full KL, which would spill there, 2 CTAs/SM); larger — one
+  // CTA/SM of 16 warps, half the rows live between the passes (L2 reuse)
+  if (p.V <= a1_small_vmax())
+    return p.kl_mode == YATT_KL_FULL ? policy_loss_grad_ring_mid(p, st)
+                                     : policy_loss_grad_ring_small(p, st);
+  return policy_loss_grad_ring_large(p, st);
 }
 
 int token_stats_ring_small(const A1Params& p, cudaStream_t st);  // token_stats_small.cu
@@ -1168,7 +1178,7 @@ int token_stats_launch(const uint16_t* pol, const uint16_t* ref, const int32_t* 
   }
   return vocab <= a1_small_vmax() ? token_stats_ring_small(p, st) : token_stats_ring_large(p, st);
 }
-#endif  // !YATT_FUSED_SMALL_TU
+#endif  // !YATT_FUSED_ONLY_TU
 #endif
 
 }  // namespace yattb

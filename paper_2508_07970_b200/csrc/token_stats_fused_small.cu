@@ -6,6 +6,7 @@
 // rows live between the two passes stay far inside L2.  Exported as
 // policy_loss_grad_ring_small; policy_loss_grad_launch dispatches by
 // vocabulary (V <= 60,000 here).
+#define YATT_FUSED_ONLY_TU 1
 #define YATT_FUSED_SMALL_TU 1
 #undef YATT_A1_TILE
 #undef YATT_A1_STAGES
@@ -13,4 +14,6 @@
 #define YATT_A1_TILE 8192
 #define YATT_A1_STAGES 2
 #define YATT_A1_MINB 3
+#undef YATT_FUSED_CW
+#define YATT_FUSED_CW 8
 #include "token_stats.cu"
