@@ -328,3 +328,33 @@ def test_gae_fused_whitening_moments(cuda, masked):
     got = mom.cpu().numpy()
     assert got[0] == ref[0]
     assert np.all(np.abs(got - ref) <= 1e-12 * np.abs(ref) + 1e-9)
+
+
+@pytest.mark.parametrize("agg", ["token-mean", "seq-mean-token-mean", "seq-mean-token-sum"])
+def test_fully_masked_batches(cuda, agg):
+    """Everything masked: A1 writes zeros, the loss sums are all zero (and the
+    host finalize gives 0, not NaN), GAE leaves every advantage at the zero
+    carry and returns = values, the moments count zero tokens — equal to the
+    oracle on the same inputs."""
+    rows, V = 24, 4096
+    pol, ref, tgt = ops.synth_logits(4, 0, rows, V, device=cuda)
+    m0 = torch.zeros(rows, dtype=torch.uint8, device=cuda)
+    lp, rl, ent, kl = ops.token_stats(pol, ref, tgt, m0, "k3")
+    assert all(torch.all(t == 0) for t in (lp, rl, ent, kl))
+    x = ops.synth_floats(4, 107, 0, rows, "logp", device=cuda)
+    cu = torch.tensor([0, 10, 10, rows], dtype=torch.int64, device=cuda)
+    cfg = ops.loss_config(agg_mode=agg)
+    sums = ops.policy_loss(x, x, x, x, x, m0, cu, cfg)
+    assert torch.all(sums == 0)
+    assert ops.loss_finalize(sums, cfg) == 0.0
+    e = O.policy_loss(*(t.cpu().numpy() for t in (x, x, x, x, x)), m0.cpu().numpy(),
+                      cu.cpu().numpy(), 0.2, 0.2, 0.0, 0.001, 0.0, ops.AGG_MODES[agg])
+    assert np.all(e == 0)
+    v = ops.synth_floats(4, 106, 0, rows, "value", device=cuda)
+    adv, ret, mom = ops.gae(v, x, cu, m0, 1.0, 0.95, return_moments=True)
+    e_adv, e_ret = O.gae(v.cpu().numpy(), x.cpu().numpy(), cu.cpu().numpy(), m0.cpu().numpy(),
+                         1.0, 0.95)
+    assert np.array_equal(adv.cpu().numpy(), e_adv.astype(np.float32))
+    assert np.array_equal(ret.cpu().numpy(), e_ret.astype(np.float32))
+    assert torch.all(adv == 0) and torch.equal(ret, v)
+    assert mom.tolist() == [0.0, 0.0, 0.0]
