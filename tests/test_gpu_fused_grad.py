@@ -184,3 +184,40 @@ def test_fused_all_rows_masked(cuda):
     lp, ent, kl, g = ops.policy_loss_grad(pol, tgt, f, f, f, mask, None, "k3", 1.0, grad)
     torch.cuda.synchronize()
     assert torch.all(g.float() == 0) and torch.all(lp == 0) and torch.all(ent == 0)
+
+
+@pytest.mark.parametrize("kl_mode", ["k3", "full"])
+def test_fused_extreme_rows(cuda, kl_mode):
+    """The rows that overflow A1's first-tile fast path (a logit 100 nats above
+    the first tile, a fully -inf first tile, constant rows, a late jump just
+    below the threshold): the fused kernel rebases per tile, so its logp /
+    entropy / KL must come back exact (vs the fp64 oracle) and its gradient
+    finite with rows summing to ~0."""
+    rows, vocab = 8, 152064
+    pol, ref, tgt = ops.synth_logits(9, 0, rows, vocab, device=cuda)
+    ar = torch.arange(rows, device=cuda)
+    keep_p, keep_r = pol[ar, tgt.long()].clone(), ref[ar, tgt.long()].clone()
+    pol[0, 150000] = 100.0
+    ref[1, 149000] = 96.0
+    pol[2, :8192] = float("-inf")
+    ref[2, :8192] = float("-inf")
+    pol[3, :8192] -= 30.0
+    pol[3, 140000:140100] = 40.0
+    pol[4, :] = 60.0
+    ref[4, :] = -60.0
+    pol[5, 100000] = 88.0
+    pol[ar, tgt.long()], ref[ar, tgt.long()] = keep_p, keep_r
+    hp, hr = bf16_np(pol), bf16_np(ref)
+    exp = O.token_stats(hp, hr, tgt.cpu().numpy(), None, "full" if kl_mode == "full" else "k3")
+    old = torch.as_tensor(exp[0], dtype=torch.float32, device=cuda) - 0.05
+    adv = torch.ones(rows, device=cuda)
+    rl = torch.as_tensor(exp[1], dtype=torch.float32, device=cuda)
+    lp, ent, kl, grad = ops.policy_loss_grad(pol, tgt, old, adv, rl, None, None, kl_mode,
+                                             float(rows), ref_logits=ref)
+    torch.cuda.synchronize()
+    got = [t.cpu().numpy().astype(np.float64) for t in (lp, ent, kl)]
+    for g_, e_ in zip(got, (exp[0], exp[2], exp[3])):
+        assert np.all(np.abs(g_ - e_) <= 1e-5 * np.abs(e_) + 4e-6)
+    gf = grad.float()
+    assert bool(torch.isfinite(gf).all())
+    assert float((gf.sum(1).abs() / (gf.abs().amax(1) * vocab ** 0.5 + 1e-30)).max()) < 1e-2
