@@ -130,6 +130,28 @@ class ClockSampler:
 _CPU_SAMPLES = {}
 
 
+def host_cpu() -> dict:
+    """nproc + the lscpu-style model / sockets / physical cores of this host
+    (the CPU baseline is reported with the box's CPU)."""
+    model, phys, cores = None, set(), set()
+    try:
+        cur = None
+        for line in open("/proc/cpuinfo"):
+            k, _, v = line.partition(":")
+            k, v = k.strip(), v.strip()
+            if k == "model name" and model is None:
+                model = v
+            elif k == "physical id":
+                cur = v
+                phys.add(v)
+            elif k == "core id":
+                cores.add((cur, v))
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "model": model, "sockets": len(phys) or None,
+            "physical_cores": len(cores) or None}
+
+
 def cpu_experience_rate(sample_rows: int | None = None, threads: int | None = None,
                         budget_s: float = 12.0, repeat: bool = True):
     """Oracle (fp64 CPU restatement) of the same per-token path on a bounded
@@ -175,6 +197,7 @@ def cpu_experience_rate(sample_rows: int | None = None, threads: int | None = No
         total += once()
         passes += 1
     return {"value": rows * passes / total, "unit": "tokens/s", "cores": threads, "kind": "port",
+            "host": host_cpu(),
             "sample": f"{passes} pass(es) over {rows} rows x V={VOCAB} "
                       f"(A1 fp64 + GRPO adv + loss), {total:.2f} s"}
 
@@ -212,7 +235,7 @@ def integer_path_baseline():
     ours = _run_json([str(drv)]) if drv.exists() else None
     units = ours.get("train_units") if ours else None
     rounds = ours.get("rounds") if ours else None
-    return {"reference_cpu": ref, "b200": ours,
+    return {"reference_cpu": ref, "b200": ours, "host": host_cpu(),
             "train_units_bit_exact": (units is not None and units == ref.get("train_units")
                                       and rounds == ref.get("rounds"))}
 
