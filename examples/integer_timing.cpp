@@ -20,6 +20,28 @@ static double ms_since(clk::time_point t0) {
   return std::chrono::duration<double, std::milli>(clk::now() - t0).count();
 }
 
+// BASELINE.md's timing method: the median of 5 runs, each repeating the
+// operation until >= 0.5 s of timed work (per-op setup outside the timing);
+// returns ms per operation.
+template <class Setup, class Op>
+static double median_ms(Setup setup, Op op) {
+  std::vector<double> runs;
+  for (int r = 0; r < 5; ++r) {
+    double acc = 0.0;
+    int k = 0;
+    do {
+      auto st = setup();
+      const auto t0 = clk::now();
+      op(st);
+      acc += ms_since(t0);
+      ++k;
+    } while (acc < 500.0);
+    runs.push_back(acc / k);
+  }
+  std::sort(runs.begin(), runs.end());
+  return runs[2];
+}
+
 int main() {
   const int P = 8, G = 16, n = 1024 * G;
   const std::uint64_t seed = 20250814;
@@ -44,37 +66,28 @@ int main() {
     auto warm = make_batch();
     sim::run_rollout_rounds(warm, P, params);
   }
-  double best = 1e30;
   int rounds = 0;
   long long units = 0;
   workload::RolloutBatch last;
-  for (int rep = 0; rep < 5; ++rep) {
-    auto b = make_batch();
-    const auto t0 = clk::now();
+  const double loop_ms = median_ms(make_batch, [&](workload::RolloutBatch& b) {
     const auto rr = sim::run_rollout_rounds(b, P, params);
-    const double ms = ms_since(t0);
-    if (ms < best) {
-      best = ms;
-      rounds = int(rr.size());
-      units = 0;
-      for (const auto& reps : rr)
-        for (const auto& r : reps) units += r.accepted_train_units;
-    }
+    rounds = int(rr.size());
+    units = 0;
+    for (const auto& reps : rr)
+      for (const auto& r : reps) units += r.accepted_train_units;
     last = b;
-  }
+  });
   std::vector<int> lengths;
   for (const auto& s : last.samples) lengths.push_back(s.prompt_len_tokens + s.target_out_len_tokens);
-  balancer::sort_and_bucket(lengths, 16, seed);  // warm-up
-  double best_sort = 1e30;
-  for (int rep = 0; rep < 5; ++rep) {
-    const auto t0 = clk::now();
+  bool empty = false;
+  const double sort_ms = median_ms([] { return 0; }, [&](int&) {
     const auto plan = balancer::sort_and_bucket(lengths, 16, seed);
-    best_sort = std::min(best_sort, ms_since(t0));
-    if (plan.buckets.empty()) return 1;
-  }
+    empty = empty || plan.buckets.empty();
+  });
+  if (empty) return 1;
   std::printf("{\"kind\": \"b200 (C++ drop-in API)\", \"shards\": %d, \"samples\": %d, "
               "\"rounds\": %d, \"train_units\": %lld, \"round_loop_ms\": %.4f, "
               "\"sort_and_bucket_ms\": %.4f}\n",
-              P, n, rounds, units, best, best_sort);
+              P, n, rounds, units, loop_ms, sort_ms);
   return 0;
 }

@@ -8,7 +8,9 @@
 //     shard has pending samples (max_rounds 4 forces acceptance);
 //   * rejection_process (workload.cpp:145-167) over the batch, one thread;
 //   * sort_and_bucket (balancer.cpp:16-41) of the accepted lengths, B = 16.
+// Timing: the median of 5 runs of >= 0.5 s each, per operation.
 // Usage: ref_timing [P]   -> one JSON line.
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -24,6 +26,28 @@ using clk = std::chrono::steady_clock;
 
 static double ms_since(clk::time_point t0) {
   return std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+}
+
+// BASELINE.md's timing method: the median of 5 runs, each repeating the
+// operation until >= 0.5 s of timed work (per-op setup outside the timing);
+// returns ms per operation.
+template <class Setup, class Op>
+static double median_ms(Setup setup, Op op) {
+  std::vector<double> runs;
+  for (int r = 0; r < 5; ++r) {
+    double acc = 0.0;
+    int k = 0;
+    do {
+      auto st = setup();
+      const auto t0 = clk::now();
+      op(st);
+      acc += ms_since(t0);
+      ++k;
+    } while (acc < 500.0);
+    runs.push_back(acc / k);
+  }
+  std::sort(runs.begin(), runs.end());
+  return runs[2];
 }
 
 int main(int argc, char** argv) {
@@ -50,16 +74,17 @@ int main(int argc, char** argv) {
   params.microbatch_size = 16;
   params.max_rounds = 4;
 
-  // shard round loop, P threads (best of 3 fresh runs)
-  double best_loop = 1e30, best_first = 1e30;
+  // shard round loop, P threads: fresh shard states per operation
   int rounds = 0;
   long long units = 0;
-  for (int rep = 0; rep < 3; ++rep) {
+  auto mk_shards = [&] {
     std::vector<sim::ShardState> shards;
     for (int r = 0; r < P; ++r) shards.push_back(sim::make_shard_state(batch, P, r));
+    return shards;
+  };
+  double first_ms = 0.0;
+  const double loop_ms = median_ms(mk_shards, [&](std::vector<sim::ShardState>& shards) {
     std::vector<sim::ShardRoundReport> reports(static_cast<size_t>(P));
-    const auto t0 = clk::now();
-    double first = 0;
     int round = 1;
     long long u = 0;
     while (true) {
@@ -68,7 +93,7 @@ int main(int argc, char** argv) {
       for (int r = 0; r < P; ++r)
         th.emplace_back([&, r] { reports[size_t(r)] = sim::shard_round_output(shards[size_t(r)], round, params); });
       for (auto& t : th) t.join();
-      if (round == 1) first = ms_since(tr);
+      if (round == 1) first_ms = ms_since(tr);
       int pending = 0;
       for (const auto& rep_ : reports) {
         pending += rep_.pending_count;
@@ -77,35 +102,31 @@ int main(int argc, char** argv) {
       if (pending == 0) break;
       ++round;
     }
-    const double loop = ms_since(t0);
-    if (loop < best_loop) best_loop = loop, best_first = first, rounds = round, units = u;
-  }
+    rounds = round;
+    units = u;
+  });
 
-  // rejection_process over the batch (one thread), best of 5
-  double best_rej = 1e30;
-  for (int rep = 0; rep < 5; ++rep) {
-    const auto t0 = clk::now();
+  // rejection_process over the batch (one thread)
+  const double rej_ms = median_ms([] { return 0; }, [&](int&) {
     volatile size_t keep = workload::rejection_process(batch, 1, params.rejection, seed).size();
     (void)keep;
-    best_rej = std::min(best_rej, ms_since(t0));
-  }
+  });
 
-  // sort_and_bucket of n lengths (one thread), best of 5
+  // sort_and_bucket of n lengths (one thread)
   std::vector<int> lengths(static_cast<size_t>(n));
   for (int i = 0; i < n; ++i)
     lengths[size_t(i)] = 64 + workload::sample_length_keyed(params.out_dist, seed,
                                                             workload::kOutputLenStream, 1, 1,
                                                             batch.samples[size_t(i)].sample_id);
-  double best_sort = 1e30;
-  for (int rep = 0; rep < 5; ++rep) {
-    const auto t0 = clk::now();
+  bool empty = false;
+  const double sort_ms = median_ms([] { return 0; }, [&](int&) {
     const auto plan = balancer::sort_and_bucket(lengths, 16, seed);
-    best_sort = std::min(best_sort, ms_since(t0));
-    if (plan.buckets.empty()) return 1;
-  }
+    empty = empty || plan.buckets.empty();
+  });
+  if (empty) return 1;
   std::printf("{\"kind\": \"reference\", \"threads\": %d, \"samples\": %d, \"rounds\": %d, "
               "\"train_units\": %lld, \"shard_round_loop_ms\": %.4f, \"first_round_ms\": %.4f, "
               "\"rejection_process_ms\": %.4f, \"sort_and_bucket_ms\": %.4f}\n",
-              P, n, rounds, units, best_loop, best_first, best_rej, best_sort);
+              P, n, rounds, units, loop_ms, first_ms, rej_ms, sort_ms);
   return 0;
 }
