@@ -335,7 +335,7 @@ int logits_backward_launch(const uint16_t* pol, const uint16_t* ref, const int32
                "logits_backward: null pointer");
   GradParams prm{pol, ref, tgt, mask, coef, rows, V, grad};
   auto a16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
-  const bool tma_ok = a16(pol) && a16(grad) && (!full_kl || a16(ref)) && (V % 8 == 0 || rows > 1);
+  const bool tma_ok = a16(pol) && a16(grad) && (!full_kl || a16(ref)) && (V % 8 == 0 || (rows > 1 && V > 8));  // V < 8: see token_stats_launch
   auto generic = [&](const GradParams& g) {
     const int gg = int(min64(g.rows, int64_t(8) * num_sms()));
     if (full_kl)

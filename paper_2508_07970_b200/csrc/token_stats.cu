@@ -602,9 +602,12 @@ __global__ void __launch_bounds__(kConsumers) token_stats_fixup_kernel(const A1P
       acc.reset();
       const uint16_t* rp = p.pol + row * V;
       const uint16_t* rq = p.ref + row * V;
+      // rows of a V % 8 != 0 tensor are not 16-byte aligned (and a row's last
+      // vector would run into the next row): element loads, masked at V
+      const bool scalar = kGeneric || (V & 7) != 0;
       for (int64_t v = tid; v < (V + 7) / 8; v += kConsumers) {
-        const uint4 P0 = kGeneric ? load8_any(rp, v * 8, V) : __ldg(reinterpret_cast<const uint4*>(rp) + v);
-        const uint4 Q0 = kGeneric ? load8_any(rq, v * 8, V) : __ldg(reinterpret_cast<const uint4*>(rq) + v);
+        const uint4 P0 = scalar ? load8_any(rp, v * 8, V) : __ldg(reinterpret_cast<const uint4*>(rp) + v);
+        const uint4 Q0 = scalar ? load8_any(rq, v * 8, V) : __ldg(reinterpret_cast<const uint4*>(rq) + v);
         const uint4 P = floor_policy(P0);
         const uint4 Q = kFull ? floor_policy(Q0) : Q0;
         const float fmp = pair_max(vmax4(P)), fmq = pair_max(vmax4(Q));
@@ -1146,8 +1149,11 @@ int token_stats_launch(const uint16_t* pol, const uint16_t* ref, const int32_t* 
   // The TMA path needs 16-byte-aligned tensor bases; any vocab: each row is
   // staged as its aligned superset.  With V % 8 != 0 the last row's superset
   // could end past the tensor, so that one row takes the generic kernel.
+  // (V < 8 with V % 8 != 0: the superset of rows before the last can end
+  // past the tensor too — those tiny vocabularies take the generic kernel.)
   const bool tma_ok = (reinterpret_cast<uintptr_t>(pol) & 15) == 0 &&
-                      (reinterpret_cast<uintptr_t>(ref) & 15) == 0 && (vocab % 8 == 0 || rows > 1);
+                      (reinterpret_cast<uintptr_t>(ref) & 15) == 0 &&
+                      (vocab % 8 == 0 || (rows > 1 && vocab > 8));
   if (tma_ok && vocab % 8 != 0) {
     A1Params last = p;
     const int64_t off = (rows - 1) * int64_t(vocab);

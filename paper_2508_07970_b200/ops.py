@@ -101,19 +101,66 @@ def token_stats(policy_logits: torch.Tensor, ref_logits: torch.Tensor, targets: 
     return out[0], out[1], out[2], out[3]
 
 
+def _host(a, dtype, name: str, shape: tuple | None = None, optional: bool = False):
+    """Validate a HOST buffer handed to a *_host C-ABI entry (numpy array or
+    CPU torch tensor): dtype, exact shape, C-contiguity.  The library trusts
+    the sizes it is given, so a wrong dtype or shape here would be read or
+    written out of bounds."""
+    if a is None:
+        if optional:
+            return None
+        raise ValueError(f"{name} is required")
+    if isinstance(a, torch.Tensor):
+        if a.is_cuda:
+            raise ValueError(f"{name} must be a host (CPU) buffer")
+        if a.dtype != dtype[1]:
+            raise TypeError(f"{name} must be {dtype[1]}, got {a.dtype}")
+        if not a.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+        got, ptr = tuple(a.shape), a.data_ptr()
+    else:
+        a = np.asarray(a) if not isinstance(a, np.ndarray) else a
+        if a.dtype != np.dtype(dtype[0]):
+            raise TypeError(f"{name} must be {np.dtype(dtype[0])}, got {a.dtype}")
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"{name} must be C-contiguous")
+        got, ptr = tuple(a.shape), a.ctypes.data
+    if shape is not None and got != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {got}")
+    return ptr
+
+
+_U16 = (np.uint16, torch.int16)   # bf16 bit patterns (torch: int16 / bfloat16 views)
+_I32 = (np.int32, torch.int32)
+_U8 = (np.uint8, torch.uint8)
+_F32 = (np.float32, torch.float32)
+
+
+def _logits_shape(policy) -> tuple[int, int]:
+    if len(policy.shape) != 2:
+        raise ValueError(f"logits must be 2-D [rows, vocab], got shape {tuple(policy.shape)}")
+    return int(policy.shape[0]), int(policy.shape[1])
+
+
+def _as_u16(a):
+    return a.view(torch.int16) if isinstance(a, torch.Tensor) and a.dtype == torch.bfloat16 else a
+
+
 def token_stats_host(policy: np.ndarray, ref: np.ndarray, targets: np.ndarray,
                      mask: np.ndarray | None = None, kl_mode: str = "k3", out: np.ndarray | None = None):
     """Same op on HOST buffers (uint16 bf16 bits): H2D, kernel, D2H inside."""
-    rows, vocab = policy.shape
+    policy, ref = _as_u16(policy), _as_u16(ref)
+    rows, vocab = _logits_shape(policy)
     if out is None:
         out = np.empty((4, rows), dtype=np.float32)
-    for a in (policy, ref, targets, out):
-        if not a.flags["C_CONTIGUOUS"]:
-            raise ValueError("host buffers must be C-contiguous")
-    mp = None if mask is None else mask.ctypes.data
-    check(lib().yatt_token_stats_host(policy.ctypes.data, ref.ctypes.data, targets.ctypes.data, mp,
-                                      rows, vocab, KL_MODES[kl_mode], out[0].ctypes.data,
-                                      out[1].ctypes.data, out[2].ctypes.data, out[3].ctypes.data))
+    pp = _host(policy, _U16, "policy", (rows, vocab))
+    pr = _host(ref, _U16, "ref", (rows, vocab))
+    pt = _host(targets, _I32, "targets", (rows,))
+    mp = _host(mask, _U8, "mask", (rows,), optional=True)
+    _host(out, _F32, "out", (4, rows))
+    check(lib().yatt_token_stats_host(pp, pr, pt, mp, rows, vocab, KL_MODES[kl_mode],
+                                      out[0].ctypes.data, out[1].ctypes.data, out[2].ctypes.data,
+                                      out[3].ctypes.data))
     return out
 
 
@@ -122,16 +169,20 @@ def grpo_step_host(policy, ref, targets, rewards, old_logp, group_size: int, mas
                    kl_mode: str = "k3", stats_out=None):
     """One GRPO experience step through the C ABI from HOST buffers (numpy or
     CPU torch tensors, pinned for full PCIe speed): returns the 8 loss sums."""
-    def ptr(a):
-        if a is None:
-            return None
-        return a.data_ptr() if isinstance(a, torch.Tensor) else a.ctypes.data
-    rows, vocab = policy.shape
+    policy, ref = _as_u16(policy), _as_u16(ref)
+    rows, vocab = _logits_shape(policy)
+    n = int(rewards.shape[0]) if len(rewards.shape) == 1 else -1
+    if n <= 0 or rows % n != 0:
+        raise ValueError(f"rewards must be 1-D with rows ({rows}) a multiple of its length")
+    args = (_host(policy, _U16, "policy", (rows, vocab)), _host(ref, _U16, "ref", (rows, vocab)),
+            _host(targets, _I32, "targets", (rows,)), _host(mask, _U8, "mask", (rows,), True))
+    pr = _host(rewards, _F32, "rewards", (n,))
+    po = _host(old_logp, _F32, "old_logp", (rows,))
+    ps = _host(stats_out, _F32, "stats_out", (4, rows), optional=True)
     sums = LossSumsC()
-    check(lib().yatt_grpo_step_host(ptr(policy), ptr(ref), ptr(targets), ptr(mask), rows, vocab,
-                                    ptr(rewards), len(rewards), first_sample_id, group_size,
-                                    ptr(old_logp), C.byref(config or loss_config()),
-                                    KL_MODES[kl_mode], C.byref(sums), ptr(stats_out)))
+    check(lib().yatt_grpo_step_host(*args, rows, vocab, pr, n, first_sample_id, group_size, po,
+                                    C.byref(config or loss_config()), KL_MODES[kl_mode],
+                                    C.byref(sums), ps))
     return [getattr(sums, f) for f, _ in LossSumsC._fields_]
 
 

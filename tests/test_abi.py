@@ -125,3 +125,36 @@ def test_peer_group_argument_errors_before_any_cuda_call():
     with pytest.raises(ConfigError):
         check(lib().yatt_peer_scan_i64(None, 0x10000, 17, None, None, None))
     assert lib().yatt_peer_destroy(None) == 0
+
+
+def test_host_entry_points_validate_buffers_before_the_call():
+    """ops.*_host check dtype / shape / contiguity of every host buffer
+    (including the caller's `out` / `stats_out`) before the C-ABI call, which
+    trusts the sizes it is given (no compute happens here: every case raises
+    first)."""
+    import numpy as np
+    from paper_2508_07970_b200 import ops
+    rows, V = 4, 16
+    pol = np.zeros((rows, V), np.uint16)
+    tgt = np.zeros(rows, np.int32)
+    with pytest.raises(TypeError):
+        ops.token_stats_host(pol, pol, tgt.astype(np.int64))
+    with pytest.raises(TypeError):
+        ops.token_stats_host(pol.astype(np.float16), pol, tgt)
+    with pytest.raises(ValueError):
+        ops.token_stats_host(pol, pol[:, :8].copy(), tgt)
+    with pytest.raises(ValueError):
+        ops.token_stats_host(pol, pol, tgt, out=np.empty((4, rows - 1), np.float32))
+    with pytest.raises(TypeError):
+        ops.token_stats_host(pol, pol, tgt, out=np.empty((4, rows), np.float16))
+    with pytest.raises(ValueError):
+        ops.token_stats_host(pol, pol, tgt, mask=np.ones(rows + 1, np.uint8))
+    with pytest.raises(ValueError):
+        ops.token_stats_host(np.asfortranarray(pol), pol, tgt)
+    rew, old = np.zeros(2, np.float32), np.zeros(rows, np.float32)
+    with pytest.raises(ValueError):
+        ops.grpo_step_host(pol, pol, tgt, rew, old, 2, stats_out=np.empty((4, 2), np.float32))
+    with pytest.raises(TypeError):
+        ops.grpo_step_host(pol, pol, tgt, rew.astype(np.float64), old, 2)
+    with pytest.raises(ValueError):
+        ops.grpo_step_host(pol, pol, tgt, np.zeros(3, np.float32), old, 3)

@@ -253,9 +253,20 @@ def test_config1_experience_pipeline_matches_oracle(cuda):
     e_old = (st[0].astype(np.float32) + (old - logp).cpu().numpy()).astype(np.float32)
     e_sums = O.policy_loss(st[0].astype(np.float32), e_old, e_tadv, st[3].astype(np.float32),
                            st[2].astype(np.float32))
-    assert O.max_rel_error(sums, e_sums) <= 1e-4  # A1 fp32 rounding feeds the ratio
-    assert abs(ops.loss_finalize(sums, cfg) - ops.loss_finalize(e_sums, cfg)) <= \
-        1e-5 * max(1.0, abs(ops.loss_finalize(e_sums, cfg)))
+    # fields: loss, pg, kl, entropy, clip_count, ratio, token_count, seq_count
+    # (a) A4 over the device's own A1 outputs: every field at 1e-5, counts exact
+    e_dev = O.policy_loss(logp.cpu().numpy(), old.cpu().numpy(), e_tadv, kl.cpu().numpy(),
+                          ent.cpu().numpy())
+    assert O.max_rel_error(sums, e_dev) <= TOL, (sums, e_dev)
+    assert sums[4] == e_dev[4] and sums[6] == e_dev[6] and sums[7] == e_dev[7]
+    # (b) the whole chain against the oracle's own A1: counts exact, the float
+    # sums and the finalized loss at 1e-5 relative
+    assert sums[6] == e_sums[6] and sums[7] == e_sums[7]
+    assert sums[4] == e_sums[4], (sums[4], e_sums[4])
+    for f in (0, 1, 2, 3, 5):
+        assert O.max_rel_error(sums[f:f + 1], e_sums[f:f + 1]) <= TOL, (f, sums[f], e_sums[f])
+    lf, ef = ops.loss_finalize(sums, cfg), ops.loss_finalize(e_sums, cfg)
+    assert abs(lf - ef) <= TOL * abs(ef), (lf, ef)
 
 
 def test_ops_reject_strided_and_mistyped_inputs(cuda):

@@ -199,3 +199,55 @@ def test_token_stats_host_buffers_match_device(cuda):
     exp = O.token_stats(hp, hr, ht, None, "full")
     for i in range(4):
         assert O.max_rel_error(host[i], exp[i]) <= TOL
+
+
+@pytest.mark.parametrize("vocab", [50257, 8193, 16385])
+@pytest.mark.parametrize("kl_mode", ["k3", "full"])
+def test_token_stats_odd_vocab_overflow_rows(cuda, vocab, kl_mode):
+    """V % 8 != 0 rows the fast path flags for the fix-up pass (first tile
+    masked to -inf, a late logit ~100 nats above the first tile's base): the
+    fix-up must take element loads (the rows are not 16-byte aligned and a
+    row's last vector would run into the next row), not crash the context."""
+    rows = 24
+    g = torch.Generator(device=cuda).manual_seed(vocab + 11)
+    pol = (torch.randn(rows, vocab, device=cuda, generator=g) * 2).to(torch.bfloat16)
+    ref = (pol.float() + 0.2 * torch.randn(rows, vocab, device=cuda, generator=g)).to(
+        torch.bfloat16)
+    tgt = torch.randint(0, vocab, (rows,), device=cuda, generator=g, dtype=torch.int32)
+    pol[0::3, :4096] = float("-inf")
+    ref[0::3, :4096] = float("-inf")
+    tgt[0::3] = vocab - 1
+    pol[1::3, vocab - 3] = 100.0
+    ref[2::3, vocab - 1] = 96.0
+    got = torch.stack(ops.token_stats(pol, ref, tgt, None, kl_mode)).cpu().numpy()
+    torch.cuda.synchronize()
+    hp = pol.view(torch.int16).cpu().numpy().view(np.uint16)
+    hr = ref.view(torch.int16).cpu().numpy().view(np.uint16)
+    exp = O.token_stats(hp, hr, tgt.cpu().numpy(), None, kl_mode)
+    assert np.all(np.isfinite(got))
+    amax = np.abs(np.nan_to_num(pol.float().cpu().numpy(), neginf=0)).max(1)
+    for i in range(4):
+        assert np.all(np.abs(got[i] - exp[i]) <= TOL * np.abs(exp[i]) + 1e-7 * amax + 4e-6), i
+
+
+@pytest.mark.parametrize("vocab,rows", [(1, 58), (3, 29), (5, 61), (7, 33)])
+def test_token_stats_tiny_vocab_ragged_rows(cuda, vocab, rows):
+    """V < 8 with rows * V not a multiple of 8 take the generic kernel (a
+    row's 16-byte staging superset could end past the tensor; the superset's
+    foreign elements are masked, so an over-read would not change the values —
+    tools/sanitize_smoke.py runs this shape under compute-sanitizer)."""
+    g = torch.Generator(device=cuda).manual_seed(rows)
+    buf = torch.full((rows * vocab + 64,), float("nan"), dtype=torch.bfloat16, device=cuda)
+    pol = buf[: rows * vocab].view(rows, vocab)
+    pol.copy_((torch.randn(rows, vocab, device=cuda, generator=g)).to(torch.bfloat16))
+    rbuf = torch.full_like(buf, float("nan"))
+    ref = rbuf[: rows * vocab].view(rows, vocab)
+    ref.copy_((pol.float() + 0.5).to(torch.bfloat16))
+    tgt = torch.randint(0, vocab, (rows,), device=cuda, generator=g, dtype=torch.int32)
+    got = torch.stack(ops.token_stats(pol, ref, tgt, None, "k3")).cpu().numpy()
+    hp = pol.view(torch.int16).cpu().numpy().view(np.uint16)
+    hr = ref.view(torch.int16).cpu().numpy().view(np.uint16)
+    exp = O.token_stats(hp, hr, tgt.cpu().numpy(), None, "k3")
+    assert np.all(np.isfinite(got))
+    for i in range(3):
+        assert np.all(np.abs(got[i] - exp[i]) <= TOL * np.abs(exp[i]) + 1e-6), i
