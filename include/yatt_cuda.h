@@ -170,6 +170,73 @@ int yatt_reduce_round_reports(const yatt_round_report* d_reports, int32_t n,
                               int64_t* d_out, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* R3+R4+R8  the whole round loop of one step, host buffers                  */
+/* (replaces run_rlhf_step's loop simcore.cpp:470-490 over                   */
+/* shard_round_output :157-214 + feed_round's continue test :304-311, :382;  */
+/* with round_limit = 1, one shard_round_output call).                       */
+/*                                                                           */
+/*   yatt_rounds_stage   pinned (mapped) staging for n samples of nshards    */
+/*                       shards; the caller packs its samples into it        */
+/*   yatt_rounds_run     rounds first_round.. of every shard until no sample */
+/*                       is pending (or round_limit rounds; <= 0: no limit): */
+/*                       one H2D copy, ONE persistent kernel (the continue   */
+/*                       test is taken on the device), one synchronize;      */
+/*                       results land in mapped host memory                 */
+/*   yatt_rounds_result  views of the results (valid until the next run)     */
+/*                                                                           */
+/* Shard s owns samples [h_shard_offsets[s], h_shard_offsets[s+1]) with      */
+/* controller rank first_rank + s.  Reports are round-major:                 */
+/* reports[r * num_shards + s]; microbatches are concatenated in (round,     */
+/* shard, mb_index) order, reports[.].num_microbatches of them per report.   */
+/* Normal / LogNormal draws the device cannot certify equal to glibc's       */
+/* (within 1e-9 relative of a .5 rounding tie) are recomputed on the host    */
+/* with glibc and the launch is re-run with them: bit-exact by construction  */
+/* (redrawn_on_host counts them).  One handle per thread; the handle belongs */
+/* to the device current at create.                                          */
+/* ------------------------------------------------------------------------ */
+typedef struct yatt_rounds* yatt_rounds_t;
+
+typedef struct yatt_rounds_view {
+  const yatt_sample* samples;          /* final state, n_samples entries */
+  int64_t n_samples;
+  const int32_t* first_round_lens;     /* out_len after first_round (if asked) */
+  const yatt_round_report* reports;    /* rounds * num_shards */
+  int32_t rounds;
+  int32_t num_shards;
+  const yatt_mb_agg* microbatches;
+  int64_t num_microbatches;
+  int64_t redrawn_on_host;
+} yatt_rounds_view;
+
+int yatt_rounds_create(yatt_rounds_t* out);
+void yatt_rounds_destroy(yatt_rounds_t h);
+int yatt_rounds_stage(yatt_rounds_t h, int64_t n, int32_t num_shards,
+                      yatt_sample** h_samples);
+int yatt_rounds_run(yatt_rounds_t h, int64_t n, const int64_t* h_shard_offsets,
+                    int32_t num_shards, int32_t first_rank, int32_t step_index,
+                    int32_t first_round, int32_t round_limit,
+                    const yatt_round_params* params, int32_t want_first_round_lens,
+                    void* stream);
+int yatt_rounds_result(yatt_rounds_t h, yatt_rounds_view* out);
+
+/* Keyed length draws for HOST ids/out (R6, workload.cpp:109-132), bit-exact */
+/* by construction for every distribution (uncertified Normal / LogNormal    */
+/* draws are redone with glibc).  Blocks.                                    */
+int yatt_sample_lengths_host(const yatt_length_dist* dist, uint64_t seed,
+                             uint64_t stream_id, uint64_t step, uint64_t round,
+                             const uint64_t* h_sample_ids, int64_t n,
+                             int32_t* h_out);
+
+/* Certification band of the Normal / LogNormal device draws (default 1e-9, */
+/* relative).  Tests widen it to force the glibc re-draw path.              */
+int yatt_set_tie_band(double band);
+
+/* Draws of the device-resident entry points (yatt_sample_lengths_keyed,   */
+/* yatt_shard_round) that were NOT certified equal to glibc since the last */
+/* reset (their device value was used).  Synchronizes the device.           */
+int yatt_uncertified_draws(int64_t* h_count, int32_t reset);
+
+/* ------------------------------------------------------------------------ */
 /* A1  fused token statistics over policy + reference logits                 */
 /* For each row r (token) of the row-major [rows, vocab] bf16 tensors:       */
 /*   logp[r]     = log softmax(policy[r])[target[r]]                         */

@@ -48,6 +48,11 @@ def lib() -> C.CDLL:
         _lib.yo_sample_length_keyed.argtypes = [C.c_int, C.c_double, C.c_double, C.c_int,
                                                 C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
                                                 C.c_uint64]
+        _lib.yo_sample_lengths_range.argtypes = [C.c_int, C.c_double, C.c_double, C.c_int] + \
+            [C.c_uint64] * 5 + [C.c_int64, C.c_void_p]
+        _lib.yo_near_ties.restype = C.c_int64
+        _lib.yo_near_ties.argtypes = [C.c_int, C.c_double, C.c_double] + [C.c_uint64] * 5 + \
+            [C.c_int64, C.c_double, C.c_void_p, C.c_int64]
         _lib.yo_shard_dataset.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
         _lib.yo_rejection_flags.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int,
                                             C.c_double, C.c_int, C.c_int, C.c_uint64, C.c_void_p]
@@ -109,6 +114,21 @@ def uniform_from_key(key: int) -> float:
 def sample_length_keyed(kind, p1, p2, max_len, seed, stream, step, round_, sample_id) -> int:
     return lib().yo_sample_length_keyed(kind, p1, p2, max_len, seed, stream, step, round_,
                                         sample_id)
+
+
+def sample_lengths_range(kind, p1, p2, max_len, seed, stream, step, round_, id0, n):
+    out = np.empty(n, dtype=np.int32)
+    lib().yo_sample_lengths_range(kind, p1, p2, max_len, seed, stream, step, round_, id0, n,
+                                  out.ctypes.data)
+    return out
+
+
+def near_ties(kind, p1, p2, seed, stream, step, round_, id0, n, band, cap=4096):
+    """ids whose glibc pre-rounding value lies within band of a .5 tie."""
+    out = np.empty(cap, dtype=np.uint64)
+    found = lib().yo_near_ties(kind, p1, p2, seed, stream, step, round_, id0, n, band,
+                               out.ctypes.data, cap)
+    return out[:min(found, cap)], found
 
 
 def shard_dataset(total: int, p: int, r: int):

@@ -106,6 +106,36 @@ int yo_sample_length_keyed(int kind, double p1, double p2, int max_len, uint64_t
   }
 }
 
+/* Bulk draws for ids id0 .. id0+n-1 (the >= 10^7-draw parity test). */
+void yo_sample_lengths_range(int kind, double p1, double p2, int max_len, uint64_t seed,
+                             uint64_t stream, uint64_t step, uint64_t round, uint64_t id0,
+                             int64_t n, int32_t* out) {
+  for (int64_t i = 0; i < n; ++i)
+    out[i] = yo_sample_length_keyed(kind, p1, p2, max_len, seed, stream, step, round,
+                                    id0 + (uint64_t)i);
+}
+
+/* Adversarial keys: ids in [id0, id0+n) whose Normal (kind 2) / LogNormal
+ * (kind 3) pre-rounding value v (glibc) lies within band * max(1, |v|) of a
+ * .5 rounding tie -- the draws the device cannot certify (keyed_draw.cuh).
+ * Returns how many were found; the first `cap` ids go to out. */
+int64_t yo_near_ties(int kind, double p1, double p2, uint64_t seed, uint64_t stream,
+                     uint64_t step, uint64_t round, uint64_t id0, int64_t n, double band,
+                     uint64_t* out, int64_t cap) {
+  int64_t found = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const uint64_t key = hash5(seed, stream, step, round, id0 + (uint64_t)i);
+    double v = p1 + p2 * normal_from_key(key);
+    if (kind == 3) v = exp(v);
+    const double f = v - floor(v);
+    if (fabs(f - 0.5) <= band * fmax(1.0, fabs(v))) {
+      if (found < cap) out[found] = id0 + (uint64_t)i;
+      ++found;
+    }
+  }
+  return found;
+}
+
 /* ---------------------------------------------------------------- R5 ---- */
 /* workload.cpp:145-167 (validation returns 1 for ConfigError) */
 int yo_rejection_flags(const uint64_t* ids, const uint8_t* accepted, int64_t n, int step,

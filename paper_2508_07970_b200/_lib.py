@@ -70,6 +70,12 @@ class ReportC(C.Structure):
                 ("accepted_train_units", c_i64), ("num_microbatches", c_i64)]
 
 
+class RoundsViewC(C.Structure):
+    _fields_ = [("samples", c_p), ("n_samples", c_i64), ("first_round_lens", c_p),
+                ("reports", c_p), ("rounds", c_i32), ("num_shards", c_i32),
+                ("microbatches", c_p), ("num_microbatches", c_i64), ("redrawn_on_host", c_i64)]
+
+
 class LossConfigC(C.Structure):
     _fields_ = [("clip_low", c_f32), ("clip_high", c_f32), ("clip_ratio_c", c_f32),
                 ("kl_coef", c_f32), ("entropy_coef", c_f32), ("agg_mode", c_i32)]
@@ -95,6 +101,16 @@ SIGNATURES = {
     "yatt_shard_round": (C.c_int, [c_p, P(c_i64), c_i32, c_i32, c_i32, c_i32, P(RoundParamsC), c_p,
                                    c_p, c_p]),
     "yatt_reduce_round_reports": (C.c_int, [c_p, c_i32, c_p, c_p]),
+    "yatt_rounds_create": (C.c_int, [P(c_p)]),
+    "yatt_rounds_destroy": (None, [c_p]),
+    "yatt_rounds_stage": (C.c_int, [c_p, c_i64, c_i32, P(c_p)]),
+    "yatt_rounds_run": (C.c_int, [c_p, c_i64, P(c_i64), c_i32, c_i32, c_i32, c_i32, c_i32,
+                                  P(RoundParamsC), c_i32, c_p]),
+    "yatt_rounds_result": (C.c_int, [c_p, P(RoundsViewC)]),
+    "yatt_sample_lengths_host": (C.c_int, [P(LengthDist), c_u64, c_u64, c_u64, c_u64, c_p, c_i64,
+                                           c_p]),
+    "yatt_set_tie_band": (C.c_int, [c_f64]),
+    "yatt_uncertified_draws": (C.c_int, [P(c_i64), c_i32]),
     "yatt_lmhead_workspace_bytes": (c_sz, [c_i64, c_i32, c_i32]),
     "yatt_lmhead_token_stats": (C.c_int, [c_p, c_p, c_p, c_i64, c_i32, c_i32, c_i32, c_p, c_p,
                                           c_p, c_p, c_sz, c_p]),

@@ -21,7 +21,7 @@ import numpy as np
 import torch
 
 from ._lib import (ConfigError, InvalidDistribution, LengthDist, MbAggC, RejectionCfg, ReportC,
-                   RoundParamsC, SampleC, check, lib)
+                   RoundParamsC, RoundsViewC, SampleC, check, lib)
 
 CONSTANT, UNIFORM, NORMAL, LOGNORMAL = range(4)
 PROMPT_LEN_STREAM, OUTPUT_LEN_STREAM, REJECTION_STREAM = 1, 2, 3
@@ -130,15 +130,17 @@ def sample_length_keyed(dist: LengthDistribution, seed, stream, step, round_, sa
 
 
 def sample_lengths(dist: LengthDistribution, n: int, seed: int, device="cuda") -> list[int]:
-    """Batched keyed draws for ids 0..n-1 on the device (workload.cpp:134-143)."""
+    """Batched keyed draws for ids 0..n-1 (workload.cpp:134-143): device
+    draws, uncertified Normal/LogNormal ones redone with glibc (bit-exact by
+    construction, keyed_draw.cuh)."""
     if n <= 0:
         return []
-    ids = torch.arange(n, dtype=torch.int64, device=device)
-    out = torch.empty((n,), dtype=torch.int32, device=device)
-    check(lib().yatt_sample_lengths_keyed(C.byref(dist.c()), seed, OUTPUT_LEN_STREAM, 0, 0,
-                                          ids.data_ptr(), n, out.data_ptr(),
-                                          torch.cuda.current_stream().cuda_stream))
-    return out.cpu().tolist()
+    ids = np.arange(n, dtype=np.uint64)
+    out = np.empty(n, dtype=np.int32)
+    with torch.cuda.device(device):
+        check(lib().yatt_sample_lengths_host(C.byref(dist.c()), seed, OUTPUT_LEN_STREAM, 0, 0,
+                                             ids.ctypes.data, n, out.ctypes.data))
+    return out.tolist()
 
 
 def _pack(samples, sample_attr_out="target_out_len_tokens") -> np.ndarray:
@@ -281,15 +283,62 @@ class _DeviceShards:
         return (SampleC * max(self.n, 1)).from_buffer_copy(raw.ljust(C.sizeof(SampleC), b"\0"))
 
 
+_ROUNDS: dict = {}
+
+
+def _run_rounds(samples, out_attr, offsets, first_rank, step, first_round, limit,
+                params: RoundParams, device):
+    """yatt_rounds_run over host samples (one persistent kernel for every
+    round of every shard); returns (reports[round][shard], final SampleC)."""
+    if params.microbatch_size <= 0:
+        raise ConfigError("microbatch_size must be positive")
+    dev = torch.device(device)
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    with torch.cuda.device(idx):
+        h = _ROUNDS.get(idx)
+        if h is None:
+            h = C.c_void_p()
+            check(lib().yatt_rounds_create(C.byref(h)))
+            _ROUNDS[idx] = h
+        n, ns = len(samples), len(offsets) - 1
+        stage = C.c_void_p()
+        check(lib().yatt_rounds_stage(h, n, ns, C.byref(stage)))
+        if n:
+            packed = _pack(samples, out_attr)
+            C.memmove(stage.value, packed.ctypes.data, packed.nbytes)
+        off = (C.c_int64 * len(offsets))(*offsets)
+        check(lib().yatt_rounds_run(h, n, off, ns, first_rank, step, first_round, limit,
+                                    C.byref(params.c()), 0, None))
+        v = RoundsViewC()
+        check(lib().yatt_rounds_result(h, C.byref(v)))
+        reps = (ReportC * (v.rounds * ns)).from_buffer_copy(
+            C.string_at(v.reports, C.sizeof(ReportC) * v.rounds * ns))
+        mbs = (MbAggC * max(v.num_microbatches, 1)).from_buffer_copy(
+            C.string_at(v.microbatches, C.sizeof(MbAggC) * v.num_microbatches).ljust(
+                C.sizeof(MbAggC), b"\0"))
+        final = (SampleC * max(n, 1)).from_buffer_copy(
+            C.string_at(v.samples, C.sizeof(SampleC) * n).ljust(C.sizeof(SampleC), b"\0"))
+    rounds, base = [], 0
+    for r in range(v.rounds):
+        row = []
+        for s_ in range(ns):
+            rep = reps[r * ns + s_]
+            row.append(_report(rep, mbs[base: base + rep.num_microbatches]))
+            base += rep.num_microbatches
+        rounds.append(row)
+    return rounds, final
+
+
 def shard_round_output(state: ShardState, round_: int, params: RoundParams,
                        device="cuda") -> ShardRoundReport:
     """simcore.cpp:157-214 on the device; mutates `state` like the reference."""
-    ds = _DeviceShards([state], params, device)
-    rep = ds.round(round_, state.controller_rank)[0]
-    for s, c in zip(state.samples, ds.samples()):
+    rounds, final = _run_rounds(state.samples, "out_len_tokens", [0, len(state.samples)],
+                                state.controller_rank, state.step_index, round_, 1, params,
+                                device)
+    for s, c in zip(state.samples, final):
         s.out_len_tokens, s.accepted, s.accepted_round = c.out_len_tokens, bool(c.accepted), \
             c.accepted_round
-    return rep
+    return rounds[0][0]
 
 
 def reduce_round_reports(reports) -> dict:
@@ -303,8 +352,27 @@ def reduce_round_reports(reports) -> dict:
 
 def run_rollout_rounds(batch: RolloutBatch, num_controllers: int, params: RoundParams,
                        device="cuda") -> list[list[ShardRoundReport]]:
-    """The round loop of run_rlhf_step (simcore.cpp:470-494): every shard of
-    every round in one launch; copy_back in rank order (simcore.cpp:107-119)."""
+    """The round loop of run_rlhf_step (simcore.cpp:470-494): every round of
+    every shard in ONE device call (rollout_rounds.cu); copy_back in rank
+    order (simcore.cpp:107-119)."""
+    params.out_dist.validate()
+    if params.max_rounds < 1:
+        raise ConfigError("max_rounds must be at least 1")
+    n = len(batch.samples)
+    offsets = [shard_dataset(n, num_controllers, r).begin for r in range(num_controllers)] + [n]
+    rounds, final = _run_rounds(batch.samples, "target_out_len_tokens", offsets, 0,
+                                batch.step_index, 1, 0, params, device)
+    for s, c in zip(batch.samples, final):
+        s.target_out_len_tokens, s.accepted, s.accepted_round = c.out_len_tokens, \
+            bool(c.accepted), c.accepted_round
+    return rounds
+
+
+def run_rollout_rounds_per_launch(batch: RolloutBatch, num_controllers: int,
+                                  params: RoundParams, device="cuda"):
+    """Same loop through the device-resident per-round entry point
+    (yatt_shard_round: the building block of the multi-rank loop, where each
+    round's reports are exchanged between ranks before the continue test)."""
     params.out_dist.validate()
     if params.max_rounds < 1:
         raise ConfigError("max_rounds must be at least 1")

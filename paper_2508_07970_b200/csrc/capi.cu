@@ -61,6 +61,9 @@ int validate_dist(const yatt_length_dist*);
 int validate_rejection(const yatt_rejection_config*);
 int lengths_launch(const yatt_length_dist*, uint64_t, uint64_t, uint64_t, uint64_t,
                    const uint64_t*, int64_t, int32_t*, cudaStream_t);
+int lengths_host(const yatt_length_dist*, uint64_t, uint64_t, uint64_t, uint64_t, const uint64_t*,
+                 int64_t, int32_t*);
+int uncertified_draws(int64_t*, int32_t);
 int rejection_launch(const yatt_sample*, int64_t, int32_t, int32_t, const yatt_rejection_config*,
                      uint64_t, uint8_t*, cudaStream_t);
 int shard_round_launch(yatt_sample*, const int64_t*, int32_t, int32_t, int32_t, int32_t,
@@ -169,7 +172,7 @@ using namespace yattb;
 extern "C" {
 
 const char* yatt_last_error_message(void) { return yattb::g_err; }
-int yatt_abi_version(void) { return 2; }
+int yatt_abi_version(void) { return 3; }
 
 int yatt_device_info(int device, char* name, int name_len, int* sm_major, int* sm_minor,
                      int* nsms) {
@@ -202,6 +205,16 @@ int yatt_sample_lengths_keyed(const yatt_length_dist* d, uint64_t seed, uint64_t
   YATT_ALIGNED("sample_lengths_keyed", ids, 8);
   YATT_ALIGNED("sample_lengths_keyed", out, 4);
   return lengths_launch(d, seed, stream_id, step, round, ids, n, out, as_stream(stream));
+}
+
+int yatt_sample_lengths_host(const yatt_length_dist* d, uint64_t seed, uint64_t stream_id,
+                             uint64_t step, uint64_t round, const uint64_t* h_ids, int64_t n,
+                             int32_t* h_out) {
+  return lengths_host(d, seed, stream_id, step, round, h_ids, n, h_out);
+}
+
+int yatt_uncertified_draws(int64_t* h_count, int32_t reset) {
+  return uncertified_draws(h_count, reset);
 }
 
 int yatt_rejection_flags(const yatt_sample* s, int64_t n, int32_t step, int32_t round,

@@ -15,54 +15,34 @@
 // compaction order), microbatch aggregates and report counters accumulate
 // with integer atomics (exact and order-independent).
 //
-// Exactness: Constant/Uniform draws are pure IEEE multiply + nearbyint and
-// match glibc bit for bit.  Normal/LogNormal use device libm (log1p, cos, sqrt,
-// exp) which agree with glibc to <=1-2 ulp; after nearbyint() the integer
-// length can only differ if the draw lands within an ulp of a .5 tie
-// (probability ~1e-13 per draw; tests/test_gpu_integer.py checks 10^5 draws).
+// Exactness (keyed_draw.cuh): Constant/Uniform draws are pure IEEE multiply +
+// nearbyint and match glibc bit for bit.  Normal/LogNormal draws are
+// certified: a draw within 1e-9 relative of a .5 rounding tie is not trusted.
+// The host-facing entry points (lengths_host here, rollout_rounds.cu) redo
+// those with glibc; these device-resident ones count them in g_uncertified
+// (yatt_uncertified_draws) so a caller can detect the ~1e-9-per-draw event.
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <vector>
 
-#include "common.cuh"
+#include "keyed_draw.cuh"
 
 namespace yattb {
 namespace {
 
 
-constexpr double kTwoPi = 6.283185307179586476925286766559;
-
-__device__ __forceinline__ int clamp_length(double value, int max_len) {
-  const double rounded = nearbyint(value);
-  if (rounded < 1) return 1;
-  if (rounded > max_len) return max_len;
-  return int(rounded);
-}
-
-__device__ __forceinline__ double normal_from_key(uint64_t key) {
-  const double u1 = uniform_from_key(key);
-  const double u2 = uniform_from_key(splitmix64(key ^ 0x5bf0a8b1457e1d23ULL));
-  return sqrt(-2.0 * log1p(-u1)) * cos(kTwoPi * u2);
-}
+// Draws of the device-resident entry points not certified equal to glibc's
+// (keyed_draw.cuh); read and reset by yatt_uncertified_draws.
+__device__ unsigned long long g_uncertified = 0;
 
 __device__ __forceinline__ int length_keyed(const yatt_length_dist& d, uint64_t seed,
                                             uint64_t stream, uint64_t step, uint64_t round,
-                                            uint64_t id) {
-  const uint64_t key = hash5(seed, stream, step, round, id);
-  switch (d.kind) {
-    case YATT_DIST_CONSTANT: return clamp_length(d.p1, d.max_len_tokens);
-    case YATT_DIST_UNIFORM: {
-      const long long lo = llround(d.p1), hi = llround(d.p2);
-      const uint64_t span = uint64_t(hi - lo) + 1;
-      const double u = uniform_from_key(key);
-      const long long v = lo + (long long)(u * double(span));
-      return clamp_length(double(v), d.max_len_tokens);
-    }
-    case YATT_DIST_NORMAL:
-      return clamp_length(d.p1 + d.p2 * normal_from_key(key), d.max_len_tokens);
-    default:
-      return clamp_length(exp(d.p1 + d.p2 * normal_from_key(key)), d.max_len_tokens);
-  }
+                                            uint64_t id, double band) {
+  bool tie = false;
+  const int len = length_keyed_dev(d, seed, stream, step, round, id, band, &tie);
+  if (tie) atomicAdd(&g_uncertified, 1ull);
+  return len;
 }
 
 __device__ __forceinline__ bool rejected_keyed(const yatt_rejection_config& c, uint64_t seed,
@@ -72,9 +52,25 @@ __device__ __forceinline__ bool rejected_keyed(const yatt_rejection_config& c, u
 }
 
 __global__ void lengths_kernel(yatt_length_dist d, uint64_t seed, uint64_t stream, uint64_t step,
-                               uint64_t round, const uint64_t* ids, int64_t n, int32_t* out) {
+                               uint64_t round, const uint64_t* ids, int64_t n, int32_t* out,
+                               double band) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = length_keyed(d, seed, stream, step, round, ids[i]);
+  if (i < n) out[i] = length_keyed(d, seed, stream, step, round, ids[i], band);
+}
+
+// Host-facing variant: uncertified draws are listed (index) for a glibc redo.
+__global__ void lengths_cert_kernel(yatt_length_dist d, uint64_t seed, uint64_t stream,
+                                    uint64_t step, uint64_t round, const uint64_t* ids, int64_t n,
+                                    int32_t* out, double band, unsigned long long* cnt,
+                                    int64_t* list, int64_t cap) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  bool tie = false;
+  out[i] = length_keyed_dev(d, seed, stream, step, round, ids[i], band, &tie);
+  if (tie) {
+    const unsigned long long k = atomicAdd(cnt, 1ull);
+    if (k < (unsigned long long)cap) list[k] = i;
+  }
 }
 
 __global__ void rejection_kernel(const yatt_sample* s, int64_t n, uint64_t step, uint64_t round,
@@ -124,7 +120,7 @@ __global__ void shard_round_init_kernel(const ShardTable tab, int32_t first_rank
 
 __global__ void __launch_bounds__(kTileSamples) shard_round_tile_kernel(
     yatt_sample* samples, const ShardTable tab, uint64_t step, int32_t round,
-    const yatt_round_params prm, yatt_round_report* reports, yatt_mb_agg* mbs_all) {
+    const yatt_round_params prm, yatt_round_report* reports, yatt_mb_agg* mbs_all, double band) {
   int shard = 0;
   while (shard + 1 < tab.nshards && tab.tile_off[shard + 1] <= blockIdx.x) ++shard;
   const int64_t b = tab.off[shard], e = tab.off[shard + 1];
@@ -167,7 +163,7 @@ __global__ void __launch_bounds__(kTileSamples) shard_round_tile_kernel(
   if (pending) {
     tile_pending = 1;
     x.out_len_tokens = length_keyed(prm.out_dist, prm.seed, kOutputLenStream, step,
-                                    uint64_t(round), x.sample_id);
+                                    uint64_t(round), x.sample_id, band);
     yatt_mb_agg* m = mbs + before / mb;
     atomicAdd(&m->sample_count, 1);
     atomicMax(&m->max_out_len_tokens, x.out_len_tokens);
@@ -285,8 +281,64 @@ int lengths_launch(const yatt_length_dist* d, uint64_t seed, uint64_t stream_id,
   YATT_REQUIRE(n >= 0, YATT_ERR_CONFIG, "sample_lengths: n must be >= 0");
   if (n == 0) return YATT_OK;
   lengths_kernel<<<unsigned(ceil_div(n, 256)), 256, 0, st>>>(*d, seed, stream_id, step, round,
-                                                             ids, n, out);
+                                                             ids, n, out, tie_band());
   return check_launch("lengths_kernel");
+}
+
+int uncertified_draws(int64_t* count, int32_t reset) {
+  YATT_REQUIRE(count != nullptr, YATT_ERR_CONFIG, "uncertified_draws: null count");
+  YATT_TRY_CUDA(cudaDeviceSynchronize());
+  unsigned long long v = 0;
+  YATT_TRY_CUDA(cudaMemcpyFromSymbol(&v, g_uncertified, sizeof(v)));
+  *count = int64_t(v);
+  if (reset) {
+    const unsigned long long z = 0;
+    YATT_TRY_CUDA(cudaMemcpyToSymbol(g_uncertified, &z, sizeof(z)));
+  }
+  return YATT_OK;
+}
+
+// Host ids -> host lengths, bit-exact for every kind: device draws, then the
+// uncertified ones (keyed_draw.cuh) redone with glibc.
+int lengths_host(const yatt_length_dist* d, uint64_t seed, uint64_t stream_id, uint64_t step,
+                 uint64_t round, const uint64_t* h_ids, int64_t n, int32_t* h_out) {
+  int rc = validate_dist(d);
+  if (rc) return rc;
+  YATT_REQUIRE(n >= 0 && (n == 0 || (h_ids && h_out)), YATT_ERR_CONFIG,
+               "sample_lengths: bad arguments");
+  if (n == 0) return YATT_OK;
+  constexpr int64_t kCap = 4096;
+  char* buf = nullptr;
+  const size_t bytes = size_t(n) * 12 + 8 + kCap * 8;
+  YATT_TRY_CUDA(cudaMalloc(&buf, bytes));
+  uint64_t* ids = reinterpret_cast<uint64_t*>(buf);
+  int32_t* out = reinterpret_cast<int32_t*>(buf + size_t(n) * 8);
+  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(buf + ((size_t(n) * 12 + 7) & ~size_t(7)));
+  int64_t* list = reinterpret_cast<int64_t*>(cnt + 1);
+  unsigned long long h_cnt = 0;
+  std::vector<int64_t> h_list;
+  cudaError_t e = cudaMemcpy(ids, h_ids, size_t(n) * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(cnt, 0, 8);
+  if (e == cudaSuccess) {
+    lengths_cert_kernel<<<unsigned(ceil_div(n, 256)), 256>>>(*d, seed, stream_id, step, round, ids,
+                                                             n, out, tie_band(), cnt, list, kCap);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(h_out, out, size_t(n) * 4, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(&h_cnt, cnt, 8, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && h_cnt > 0 && h_cnt <= (unsigned long long)kCap) {
+    h_list.resize(size_t(h_cnt));
+    e = cudaMemcpy(h_list.data(), list, size_t(h_cnt) * 8, cudaMemcpyDeviceToHost);
+  }
+  cudaFree(buf);
+  if (e != cudaSuccess) return set_error(YATT_ERR_CUDA, "sample_lengths: %s", cudaGetErrorString(e));
+  if (h_cnt > (unsigned long long)kCap) {  // (only with a widened band) redo all on the host
+    for (int64_t i = 0; i < n; ++i)
+      h_out[i] = length_keyed_glibc(*d, seed, stream_id, step, round, h_ids[i]);
+  } else {
+    for (int64_t i : h_list) h_out[i] = length_keyed_glibc(*d, seed, stream_id, step, round, h_ids[i]);
+  }
+  return YATT_OK;
 }
 
 int rejection_launch(const yatt_sample* s, int64_t n, int32_t step, int32_t round,
@@ -341,7 +393,8 @@ int shard_round_launch(yatt_sample* samples, const int64_t* h_off, int32_t nshar
     if (rc) return rc;
     if (tab.tile_off[cnt] > 0) {
       shard_round_tile_kernel<<<unsigned(tab.tile_off[cnt]), kTileSamples, 0, st>>>(
-          samples, tab, uint64_t(int64_t(step)), round, *prm, reports + s0, mbs + mb_before);
+          samples, tab, uint64_t(int64_t(step)), round, *prm, reports + s0, mbs + mb_before,
+          tie_band());
       rc = check_launch("shard_round_tile_kernel");
       if (rc) return rc;
     }

@@ -208,14 +208,10 @@ std::vector<int> sample_lengths(const LengthDistribution& dist, int n, std::uint
   if (n <= 0) return {};
   std::vector<std::uint64_t> ids(static_cast<size_t>(n));
   std::iota(ids.begin(), ids.end(), std::uint64_t{0});
-  auto* d_ids = detail::dev<std::uint64_t>(0, ids.size());
-  auto* d_out = detail::dev<std::int32_t>(1, ids.size());
-  detail::h2d(d_ids, ids.data(), ids.size() * 8);
   const yatt_length_dist d = detail::to_c(dist);
-  detail::throw_status(yatt_sample_lengths_keyed(&d, seed, kOutputLenStream, 0, 0, d_ids, n,
-                                                 d_out, nullptr));
   std::vector<int> out(static_cast<size_t>(n));
-  detail::d2h(out.data(), d_out, out.size() * 4);
+  detail::throw_status(yatt_sample_lengths_host(&d, seed, kOutputLenStream, 0, 0, ids.data(), n,
+                                                out.data()));
   return out;
 }
 
@@ -289,36 +285,53 @@ std::int64_t mb_slots(std::int64_t n, int mb) { return mb > 0 ? (n + mb - 1) / m
 
 }  // namespace
 
+// One rounds engine per thread (rollout_rounds.cu): pinned mapped staging and
+// device scratch, grow-only; the reference's functions are callable
+// concurrently on distinct states.
+struct RoundsHandle {
+  yatt_rounds_t h = nullptr;
+  int device = -1;
+  yatt_rounds_t get() {
+    int dev = 0;
+    detail::cuda_ok(cudaGetDevice(&dev), "cudaGetDevice");
+    if (h && dev != device) {
+      yatt_rounds_destroy(h);
+      h = nullptr;
+    }
+    if (!h) {
+      detail::throw_status(yatt_rounds_create(&h));
+      device = dev;
+    }
+    return h;
+  }
+  ~RoundsHandle() { yatt_rounds_destroy(h); }
+};
+thread_local RoundsHandle g_rounds;
+
 ShardRoundReport shard_round_output(ShardState& state, int round, const RoundParams& params) {
   if (params.microbatch_size <= 0) throw ConfigError("microbatch_size must be positive");
   const std::int64_t n = static_cast<std::int64_t>(state.samples.size());
-  std::vector<yatt_sample> packed(static_cast<size_t>(n));
-  for (size_t i = 0; i < packed.size(); ++i) {
-    const ShardSampleState& s = state.samples[i];
-    packed[i] = yatt_sample{s.sample_id, s.prompt_len_tokens, s.out_len_tokens, s.accepted_round,
-                            s.accepted ? 1 : 0};
+  yatt_rounds_t h = g_rounds.get();
+  yatt_sample* st = nullptr;
+  detail::throw_status(yatt_rounds_stage(h, n, 1, &st));
+  for (std::int64_t i = 0; i < n; ++i) {
+    const ShardSampleState& s = state.samples[static_cast<size_t>(i)];
+    st[i] = yatt_sample{s.sample_id, s.prompt_len_tokens, s.out_len_tokens, s.accepted_round,
+                        s.accepted ? 1 : 0};
   }
-  const std::int64_t slots = std::max<std::int64_t>(1, mb_slots(n, params.microbatch_size));
-  auto* d_s = detail::dev<yatt_sample>(0, packed.size());
-  auto* d_r = detail::dev<yatt_round_report>(1, 1);
-  auto* d_m = detail::dev<yatt_mb_agg>(2, static_cast<size_t>(slots));
-  detail::h2d(d_s, packed.data(), packed.size() * sizeof(yatt_sample));
   const yatt_round_params p = to_c(params);
   const std::int64_t off[2] = {0, n};
-  detail::throw_status(yatt_shard_round(d_s, off, 1, state.controller_rank, state.step_index,
-                                        round, &p, d_r, d_m, nullptr));
-  yatt_round_report rep;
-  detail::d2h(&rep, d_r, sizeof(rep));
-  std::vector<yatt_mb_agg> mbs(static_cast<size_t>(rep.num_microbatches));
-  detail::d2h(mbs.data(), d_m, mbs.size() * sizeof(yatt_mb_agg));
-  detail::d2h(packed.data(), d_s, packed.size() * sizeof(yatt_sample));
-  for (size_t i = 0; i < packed.size(); ++i) {
-    ShardSampleState& s = state.samples[i];
-    s.out_len_tokens = packed[i].out_len_tokens;
-    s.accepted = packed[i].accepted != 0;
-    s.accepted_round = packed[i].accepted_round;
+  detail::throw_status(yatt_rounds_run(h, n, off, 1, state.controller_rank, state.step_index,
+                                       round, 1, &p, 0, nullptr));
+  yatt_rounds_view v{};
+  detail::throw_status(yatt_rounds_result(h, &v));
+  for (std::int64_t i = 0; i < n; ++i) {
+    ShardSampleState& s = state.samples[static_cast<size_t>(i)];
+    s.out_len_tokens = v.samples[i].out_len_tokens;
+    s.accepted = v.samples[i].accepted != 0;
+    s.accepted_round = v.samples[i].accepted_round;
   }
-  return from_c(rep, mbs.data());
+  return from_c(v.reports[0], v.microbatches);
 }
 
 ShardState make_shard_state(const workload::RolloutBatch& batch, int num_controllers,
@@ -352,58 +365,50 @@ RoundReduction reduce_round_reports(const std::vector<ShardRoundReport>& reports
 
 std::vector<std::vector<ShardRoundReport>> run_rollout_rounds(workload::RolloutBatch& batch,
                                                               int num_controllers,
-                                                              const RoundParams& params) {
+                                                              const RoundParams& params,
+                                                              std::vector<int>* first_round_lengths) {
   params.out_dist.validate();
   if (params.max_rounds < 1) throw ConfigError("max_rounds must be at least 1");
   if (num_controllers < 1) throw ConfigError("num_controllers must be positive");
   if (params.microbatch_size <= 0) throw ConfigError("microbatch_size must be positive");
   const std::int64_t n = static_cast<std::int64_t>(batch.samples.size());
   std::vector<std::int64_t> off(static_cast<size_t>(num_controllers) + 1, 0);
-  std::int64_t slots = 0;
   for (int r = 0; r < num_controllers; ++r) {
     const workload::ShardRange sr =
         workload::shard_dataset(static_cast<std::uint64_t>(n), num_controllers, r);
     off[static_cast<size_t>(r)] = static_cast<std::int64_t>(sr.begin);
     off[static_cast<size_t>(r) + 1] = static_cast<std::int64_t>(sr.end);
-    slots += mb_slots(static_cast<std::int64_t>(sr.size()), params.microbatch_size);
   }
-  std::vector<yatt_sample> packed(static_cast<size_t>(n));
-  for (size_t i = 0; i < packed.size(); ++i) {
-    const workload::RolloutSample& s = batch.samples[i];
-    packed[i] = yatt_sample{s.sample_id, s.prompt_len_tokens, s.target_out_len_tokens,
-                            s.accepted_round, s.accepted ? 1 : 0};
-  }
-  auto* d_s = detail::dev<yatt_sample>(0, packed.size());
-  auto* d_r = detail::dev<yatt_round_report>(1, static_cast<size_t>(num_controllers));
-  auto* d_m = detail::dev<yatt_mb_agg>(2, static_cast<size_t>(std::max<std::int64_t>(slots, 1)));
-  detail::h2d(d_s, packed.data(), packed.size() * sizeof(yatt_sample));
+  yatt_rounds_t h = g_rounds.get();
+  yatt_sample* st = nullptr;
+  detail::throw_status(yatt_rounds_stage(h, n, num_controllers, &st));
+  const workload::RolloutSample* src = batch.samples.data();
+  for (std::int64_t i = 0; i < n; ++i)
+    st[i] = yatt_sample{src[i].sample_id, src[i].prompt_len_tokens, src[i].target_out_len_tokens,
+                        src[i].accepted_round, src[i].accepted ? 1 : 0};
   const yatt_round_params p = to_c(params);
-  std::vector<yatt_round_report> reps(static_cast<size_t>(num_controllers));
-  std::vector<yatt_mb_agg> mbs(static_cast<size_t>(std::max<std::int64_t>(slots, 1)));
-  std::vector<std::vector<ShardRoundReport>> all;
-  for (int round = 1;; ++round) {
-    detail::throw_status(yatt_shard_round(d_s, off.data(), num_controllers, 0, batch.step_index,
-                                          round, &p, d_r, d_m, nullptr));
-    detail::d2h(reps.data(), d_r, reps.size() * sizeof(yatt_round_report));
-    detail::d2h(mbs.data(), d_m, mbs.size() * sizeof(yatt_mb_agg));
-    std::vector<ShardRoundReport> reports;
-    std::int64_t base = 0;
-    for (int r = 0; r < num_controllers; ++r) {
-      reports.push_back(from_c(reps[static_cast<size_t>(r)], mbs.data() + base));
-      base += mb_slots(off[static_cast<size_t>(r) + 1] - off[static_cast<size_t>(r)],
-                       params.microbatch_size);
+  detail::throw_status(yatt_rounds_run(h, n, off.data(), num_controllers, 0, batch.step_index, 1,
+                                       0, &p, first_round_lengths ? 1 : 0, nullptr));
+  yatt_rounds_view v{};
+  detail::throw_status(yatt_rounds_result(h, &v));
+  std::vector<std::vector<ShardRoundReport>> all(static_cast<size_t>(v.rounds));
+  const yatt_mb_agg* mb = v.microbatches;
+  for (int r = 0; r < v.rounds; ++r) {
+    auto& reports = all[static_cast<size_t>(r)];
+    reports.reserve(static_cast<size_t>(num_controllers));
+    for (int s = 0; s < num_controllers; ++s) {
+      const yatt_round_report& rep = v.reports[static_cast<size_t>(r) * num_controllers + s];
+      reports.push_back(from_c(rep, mb));
+      mb += rep.num_microbatches;
     }
-    const bool more = reduce_round_reports(reports).any_pending();
-    all.push_back(std::move(reports));
-    if (!more) break;
   }
-  detail::d2h(packed.data(), d_s, packed.size() * sizeof(yatt_sample));
-  for (size_t i = 0; i < packed.size(); ++i) {
-    workload::RolloutSample& s = batch.samples[i];
-    s.target_out_len_tokens = packed[i].out_len_tokens;
-    s.accepted = packed[i].accepted != 0;
-    s.accepted_round = packed[i].accepted_round;
+  workload::RolloutSample* dst = batch.samples.data();
+  for (std::int64_t i = 0; i < n; ++i) {  // copy_back (simcore.cpp:107-119)
+    dst[i].target_out_len_tokens = v.samples[i].out_len_tokens;
+    dst[i].accepted = v.samples[i].accepted != 0;
+    dst[i].accepted_round = v.samples[i].accepted_round;
   }
+  if (first_round_lengths) first_round_lengths->assign(v.first_round_lens, v.first_round_lens + n);
   return all;
 }
 

@@ -24,7 +24,7 @@ def test_library_exports_every_declared_symbol():
     missing = [s for s in declared_symbols() if not hasattr(h, s)]
     assert not missing, missing
     assert set(declared_symbols()) <= set(SIGNATURES) | {"yatt_abi_version"}
-    assert h.yatt_abi_version() == 2
+    assert h.yatt_abi_version() == 3
 
 
 def test_cpp_dropin_api_is_exported():

@@ -45,16 +45,77 @@ def test_keyed_lengths_match_reference(cuda):
         assert got.tolist() == case["lengths"], case["name"]
 
 
+def _host_lengths(dist, seed, stream, step, rnd, ids):
+    import ctypes as C
+    from paper_2508_07970_b200._lib import check, lib
+    ids = np.ascontiguousarray(ids, dtype=np.uint64)
+    out = np.empty(len(ids), dtype=np.int32)
+    check(lib().yatt_sample_lengths_host(C.byref(dist.c()), seed, stream, step, rnd,
+                                         ids.ctypes.data, len(ids), out.ctypes.data))
+    return out
+
+
+def _uncertified(reset=True):
+    import ctypes as C
+    from paper_2508_07970_b200._lib import check, lib
+    c = C.c_int64()
+    check(lib().yatt_uncertified_draws(C.byref(c), int(reset)))
+    return c.value
+
+
 @pytest.mark.parametrize("kind,p1,p2,mx", [(api.NORMAL, 2048, 512, 4096),
                                            (api.LOGNORMAL, 5.0, 0.5, 4096),
                                            (api.UNIFORM, 1, 16384, 16384)])
 def test_keyed_lengths_bulk_vs_oracle(cuda, kind, p1, p2, mx):
-    """10^5 draws: device libm vs glibc agree after nearbyint."""
-    n = 100_000
+    """10^7 draws through the host-facing entry (device draws + glibc re-draw
+    of the uncertified ones) == glibc for every id (keyed_draw.cuh)."""
+    n = 10_000_000
     dist = api.LengthDistribution(kind, p1, p2, mx)
-    got = _device_lengths(dist, 20250814, 2, 7, 1, range(n), cuda)
-    exp = [O.sample_length_keyed(kind, p1, p2, mx, 20250814, 2, 7, 1, i) for i in range(n)]
-    assert got.tolist() == exp
+    got = _host_lengths(dist, 20250814, 2, 7, 1, np.arange(n, dtype=np.uint64))
+    exp = O.sample_lengths_range(kind, p1, p2, mx, 20250814, 2, 7, 1, 0, n)
+    assert np.array_equal(got, exp)
+
+
+@pytest.mark.parametrize("kind,p1,p2", [(api.NORMAL, 2048, 512), (api.LOGNORMAL, 5.0, 0.5),
+                                        (api.NORMAL, 300.5, 80)])
+def test_keyed_lengths_adversarial_near_ties(cuda, kind, p1, p2):
+    """Keys whose glibc value lands within 1e-9 (relative) of a .5 rounding
+    tie, found by exhaustive search over 2x10^7 ids: the draws the device
+    cannot certify.  The host-facing entry returns glibc's length for every
+    one of them; the device-resident entry flags every one (counter)."""
+    ids, found = O.near_ties(kind, p1, p2, 20250814, 2, 7, 1, 0, 20_000_000, 1e-9)
+    assert found >= 1 and found == len(ids)
+    dist = api.LengthDistribution(kind, p1, p2, 1 << 20)
+    exp = [O.sample_length_keyed(kind, p1, p2, 1 << 20, 20250814, 2, 7, 1, int(i)) for i in ids]
+    assert _host_lengths(dist, 20250814, 2, 7, 1, ids).tolist() == exp
+    _uncertified(reset=True)
+    _device_lengths(dist, 20250814, 2, 7, 1, ids.astype(np.int64), cuda)
+    assert _uncertified(reset=True) == len(ids)
+
+
+def test_forced_redraw_path_is_exact(cuda):
+    """Widen the certification band so ~10% of Normal / LogNormal draws take
+    the glibc re-draw + re-run path of the rounds engine: every golden
+    rollout and 10^6 bulk draws stay bit-exact."""
+    import ctypes as C
+    from paper_2508_07970_b200._lib import check, lib
+    check(lib().yatt_set_tie_band(C.c_double(0.05)))
+    try:
+        for name in ["normal", "lognormal_p3"]:
+            case = load(f"rollout_{name}.json")
+            params = _params(case)
+            for run in case["runs"]:
+                batch = _make_batch(case, run)
+                rounds = api.run_rollout_rounds(batch, run["controllers"], params)
+                assert [[_as_golden(r) for r in rnd] for rnd in rounds] == run["rounds"]
+                assert [s.target_out_len_tokens for s in batch.samples] == run["final_out_len"]
+        n = 1_000_000
+        for kind, p1, p2 in [(api.NORMAL, 2048, 512), (api.LOGNORMAL, 5.0, 0.5)]:
+            dist = api.LengthDistribution(kind, p1, p2, 4096)
+            got = _host_lengths(dist, 3, 2, 0, 2, np.arange(n, dtype=np.uint64))
+            assert np.array_equal(got, O.sample_lengths_range(kind, p1, p2, 4096, 3, 2, 0, 2, 0, n))
+    finally:
+        check(lib().yatt_set_tie_band(C.c_double(1e-9)))
 
 
 def test_sample_lengths_statistics(cuda):
@@ -115,15 +176,20 @@ def _as_golden(rep):
                                                           m.score_tokens)]}
 
 
+@pytest.mark.parametrize("engine", ["rounds_engine", "per_launch"])
 @pytest.mark.parametrize("name", ["config1", "config5", "normal", "lognormal_p3"])
-def test_rollout_rounds_match_reference(cuda, name):
-    """All controller shards of a round in one launch == the reference's
-    per-shard shard_round_output loop, for P = 1/2/4/8 and misaligned P = 3."""
+def test_rollout_rounds_match_reference(cuda, name, engine):
+    """Every round of every controller shard == the reference's per-shard
+    shard_round_output loop, for P = 1/2/4/8 and misaligned P = 3: through the
+    one-call rounds engine (rollout_rounds.cu) and through one device-resident
+    launch per round (yatt_shard_round, the multi-rank building block)."""
     case = load(f"rollout_{name}.json")
     params = _params(case)
+    run_fn = api.run_rollout_rounds if engine == "rounds_engine" else \
+        api.run_rollout_rounds_per_launch
     for run in case["runs"]:
         batch = _make_batch(case, run)
-        rounds = api.run_rollout_rounds(batch, run["controllers"], params)
+        rounds = run_fn(batch, run["controllers"], params)
         assert [[_as_golden(r) for r in rnd] for rnd in rounds] == run["rounds"]
         assert [s.target_out_len_tokens for s in batch.samples] == run["final_out_len"]
         assert [int(s.accepted) for s in batch.samples] == run["final_accepted"]
@@ -197,6 +263,21 @@ def test_reference_unit_tests_pass_against_b200_library(cuda):
     res = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     assert "0 failed" in res.stdout
+
+
+def test_reference_step_tests_pass_against_b200_library(cuda):
+    """The reference's simcore_test.cpp (18 TESTs: exact prep/train charges,
+    rejection rounds + swap law, max_rounds, TraceIsIndependentOfController-
+    Count :219, probe == first round :246, ShardReportsAreIntegerOnly :322,
+    invalid contexts) compiled unchanged at the real call site: run_rlhf_step
+    from dropin/run_rlhf_step.cpp (all rounds of all shards in one device
+    call), shard_round_output / make_shard_state from libyatt_b200.so, the
+    reference's own timing layer (oracle/Makefile simcore_b200)."""
+    exe = ROOT / "oracle" / "_ref" / "simcore_b200"
+    assert exe.exists(), "build with `make -C oracle ref` (done by __graft_entry__.build)"
+    res = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    assert "18 tests, 0 failed" in res.stdout
 
 
 # ---------------------------------------------------------------- R10 ----

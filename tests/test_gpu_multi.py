@@ -1,6 +1,19 @@
-"""N >= 2 GPUs of one box: the C-ABI NCCL communicator, the sharded GRPO
-step and global compaction (tools/mgpu_check.py under torchrun).  Skipped on
-single-GPU boxes; the same host logic runs on CPU in test_multiproc_cpu.py."""
+"""Multi-rank path on a real GPU box, including the driver's 1-GPU box.
+
+* test_peer_world_oversubscribed: world 2 / 8 ranks (torchrun, gloo for the
+  plumbing) mapped onto however many GPUs the box has (rank r -> GPU r % n;
+  same-device CUDA IPC works between processes).  tools/peer_world8.py runs
+  the NVLink peer-memory collectives for real and checks, against the
+  single-process results: the sharded GRPO step's loss sums (fp64
+  reassociation only, <= 1e-12, also under CUDA-graph replay), the global
+  dynamic-sampling compaction (byte-exact packed layout from per-rank
+  filters + a peer-memory scan of survivor counts), the rank-major
+  all-gather, and the dynamic-sampling round loop whose reports travel only
+  over peer memory (== api.run_rollout_rounds, the reference's
+  TraceIsIndependentOfControllerCount invariance, simcore_test.cpp:219-244).
+* test_nccl_rank_path: tools/mgpu_check.py over the C-ABI NCCL communicator
+  (yatt_comm_*), one rank per GPU (NCCL refuses two ranks on one device, so a
+  1-GPU box runs it at world 1)."""
 import os
 import socket
 import subprocess
@@ -20,14 +33,23 @@ def _port():
         return s.getsockname()[1]
 
 
-def test_multi_gpu_rank_path(cuda):
-    n = torch.cuda.device_count()
-    if n < 2:
-        pytest.skip("needs >= 2 GPUs")
+def _torchrun(world, script, timeout):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
-           f"--nproc-per-node={min(n, 8)}", "--master-addr", "127.0.0.1", "--master-port",
-           str(_port()), str(ROOT / "tools" / "mgpu_check.py")]
-    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
-                         env={**os.environ, "NCCL_DEBUG": "WARN"})
+           f"--nproc-per-node={world}", "--master-addr", "127.0.0.1", "--master-port",
+           str(_port()), str(ROOT / "tools" / script)]
+    return subprocess.run(cmd, capture_output=True, text=True, timeout=timeout,
+                          env={**os.environ, "NCCL_DEBUG": "WARN", "OMP_NUM_THREADS": "1"})
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_peer_world_oversubscribed(cuda, world):
+    res = _torchrun(world, "peer_world8.py", 900)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
-    assert "mgpu ok" in res.stdout
+    assert f"peer world{world} ok" in res.stdout
+
+
+def test_nccl_rank_path(cuda):
+    world = min(torch.cuda.device_count(), 8)
+    res = _torchrun(world, "mgpu_check.py", 600)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    assert f"mgpu ok world={world}" in res.stdout

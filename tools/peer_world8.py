@@ -14,6 +14,8 @@ math is exact):
   * policy_loss over 8 prompt-group shards == the full batch on one rank
     (max rel 1e-12: fp64 reassociation only);
   * the same under CUDA-graph replay;
+  * global compaction: per-rank zero-variance filter + survivor counts scanned
+    over peer memory -> one packed layout == the single-process compaction;
   * the all-gather (9,000 words per rank) and a full dynamic-sampling round
     loop whose reports travel only over peer memory == the single-process
     rounds (api.run_rollout_rounds).
@@ -92,6 +94,34 @@ def main():
         graph.replay()
         torch.cuda.synchronize()
         assert torch.equal(gs, fused), (rank, gs.tolist(), fused.tolist())
+    # global dynamic-sampling compaction: per-rank filter + survivor counts
+    # scanned over peer memory (one kernel) give each rank its offsets into
+    # ONE packed layout, byte-identical to the single-process compaction
+    rewards_all = ops.synth_floats(SEED, 105, 0, P * R, "reward", R, device=dev)
+    lens_all = torch.full((P * R,), T, dtype=torch.int64, device=dev) + \
+        torch.arange(P * R, dtype=torch.int64, device=dev) % 7
+    single = ops.filter_compact(rewards_all, lens_all, R)
+    loc = ops.filter_compact(rewards_all[g0 * R:g1 * R].contiguous(),
+                             lens_all[g0 * R:g1 * R].contiguous(), R)
+    pre_c, tot_c = peer.scan_i64(loc["counts"])
+    assert tot_c.tolist() == single["counts"].tolist(), (tot_c, single["counts"])
+    cu_all = torch.zeros(P * R + 1, dtype=torch.int64, device=dev)
+    cu_all[1:] = torch.cumsum(lens_all, 0)
+    payload = torch.arange(int(cu_all[-1]), dtype=torch.int32, device=dev)
+    kt = int(single["counts"][1])
+    dst = torch.zeros(kt, dtype=torch.int32, device=dev)
+    local_cu = (cu_all[g0 * R:g1 * R + 1] - cu_all[g0 * R]).contiguous()
+    src = payload[int(cu_all[g0 * R]):int(cu_all[g1 * R])].contiguous()
+    ops.gather_varlen(src, local_cu, loc["index_map"], loc["new_cu"], loc["counts"][:1],
+                      (g1 - g0) * R, dst, pre_c[1:2].contiguous())
+    ref_dst = torch.empty(kt, dtype=torch.int32, device=dev)
+    ops.gather_varlen(payload, cu_all, single["index_map"], single["new_cu"],
+                      single["counts"][:1], P * R, ref_dst)
+    torch.cuda.synchronize()
+    mine = dst.cpu()
+    dist.all_reduce(mine)  # ranks wrote disjoint ranges of zero-initialised buffers
+    assert torch.equal(mine, ref_dst.cpu()), rank
+
     # all-gather + the dynamic-sampling round loop with reports exchanged over
     # peer memory only == the single-process rounds
     big = torch.arange(9000, dtype=torch.int64, device=dev) + 1000003 * rank
