@@ -94,12 +94,13 @@ int main() {
     for (int it = 0; it < 300; ++it) {
       auto batch = make_batch();
       const auto t0 = clk::now();
-      yatt_sample* st = nullptr;
-      yatt_rounds_stage(h, n, P, &st);
+      yatt_rounds_io io{};
+      yatt_rounds_stage(h, n, P, &io);
       for (int i = 0; i < n; ++i) {
         const auto& x = batch.samples[std::size_t(i)];
-        st[i] = yatt_sample{x.sample_id, x.prompt_len_tokens, x.target_out_len_tokens,
-                            x.accepted_round, x.accepted ? 1 : 0};
+        io.sample_id[i] = x.sample_id;
+        io.prompt_len[i] = x.prompt_len_tokens;
+        io.accepted[i] = x.accepted ? 1 : 0;
       }
       const auto t1 = clk::now();
       if (yatt_rounds_run(h, n, off.data(), P, 0, batch.step_index, 1, 0, &cp, 0, nullptr) != 0)
@@ -122,9 +123,10 @@ int main() {
         }
       for (int i = 0; i < n; ++i) {
         auto& x = batch.samples[std::size_t(i)];
-        x.target_out_len_tokens = v.samples[i].out_len_tokens;
-        x.accepted = v.samples[i].accepted != 0;
-        x.accepted_round = v.samples[i].accepted_round;
+        if (x.accepted) continue;
+        x.target_out_len_tokens = io.out_len[i];
+        x.accepted = io.accepted_out[i] != 0;
+        x.accepted_round = io.accepted_round[i];
       }
       const auto t3 = clk::now();
       using ms = std::chrono::duration<double, std::milli>;

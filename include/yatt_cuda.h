@@ -146,7 +146,9 @@ int yatt_rejection_flags(const yatt_sample* d_samples, int64_t n,
 
 /* ------------------------------------------------------------------------ */
 /* R3+R4  shard_round_output  (replaces simcore.cpp:157-214 + :17-39)        */
-/* Runs `num_shards` controller shards in ONE launch (one CTA per shard).    */
+/* One round of `num_shards` controller shards, device-resident: the        */
+/* building block of the multi-rank loop (reports are exchanged between      */
+/* ranks before the continue test; ranks.exchange_round_reports).            */
 /* Shard s owns d_samples[h_shard_offsets[s] .. h_shard_offsets[s+1]) (host  */
 /* array, num_shards+1 entries) and has controller rank first_rank + s.      */
 /* Samples are mutated in place exactly like ShardState; the report of       */
@@ -175,15 +177,22 @@ int yatt_reduce_round_reports(const yatt_round_report* d_reports, int32_t n,
 /* shard_round_output :157-214 + feed_round's continue test :304-311, :382;  */
 /* with round_limit = 1, one shard_round_output call).                       */
 /*                                                                           */
-/*   yatt_rounds_stage   pinned (mapped) staging for n samples of nshards    */
-/*                       shards; the caller packs its samples into it        */
+/*   yatt_rounds_stage   pinned, device-mapped SoA arrays for n samples of   */
+/*                       num_shards shards; the caller fills sample_id,      */
+/*                       prompt_len and accepted (1 = accepted before the    */
+/*                       call: never touched)                                */
 /*   yatt_rounds_run     rounds first_round.. of every shard until no sample */
 /*                       is pending (or round_limit rounds; <= 0: no limit): */
-/*                       one H2D copy, ONE persistent kernel (the continue   */
-/*                       test is taken on the device), one synchronize;      */
-/*                       results land in mapped host memory                 */
-/*   yatt_rounds_result  views of the results (valid until the next run)     */
+/*                       ONE persistent kernel reads the stage over PCIe,    */
+/*                       takes the continue test on the device and stores    */
+/*                       its results straight into the stage; one launch,    */
+/*                       one synchronize                                     */
+/*   yatt_rounds_result  reports / microbatches (valid until the next run)   */
 /*                                                                           */
+/* Outputs for samples pending at the start of the call: out_len,            */
+/* accepted_round, accepted_out and (if asked) first_round_len = out_len     */
+/* after first_round (the run_rlhf_step snapshot); entries of samples        */
+/* accepted before the call are placeholders.                                */
 /* Shard s owns samples [h_shard_offsets[s], h_shard_offsets[s+1]) with      */
 /* controller rank first_rank + s.  Reports are round-major:                 */
 /* reports[r * num_shards + s]; microbatches are concatenated in (round,     */
@@ -196,22 +205,30 @@ int yatt_reduce_round_reports(const yatt_round_report* d_reports, int32_t n,
 /* ------------------------------------------------------------------------ */
 typedef struct yatt_rounds* yatt_rounds_t;
 
+typedef struct yatt_rounds_io {
+  uint64_t* sample_id;       /* in  */
+  int32_t* prompt_len;       /* in  */
+  uint8_t* accepted;         /* in  */
+  int32_t* out_len;          /* out */
+  int32_t* accepted_round;   /* out */
+  uint8_t* accepted_out;     /* out */
+  int32_t* first_round_len;  /* out (want_first_round_lens) */
+} yatt_rounds_io;
+
 typedef struct yatt_rounds_view {
-  const yatt_sample* samples;          /* final state, n_samples entries */
-  int64_t n_samples;
-  const int32_t* first_round_lens;     /* out_len after first_round (if asked) */
   const yatt_round_report* reports;    /* rounds * num_shards */
   int32_t rounds;
   int32_t num_shards;
   const yatt_mb_agg* microbatches;
   int64_t num_microbatches;
   int64_t redrawn_on_host;
+  int32_t first_round_lens_valid;
 } yatt_rounds_view;
 
 int yatt_rounds_create(yatt_rounds_t* out);
 void yatt_rounds_destroy(yatt_rounds_t h);
 int yatt_rounds_stage(yatt_rounds_t h, int64_t n, int32_t num_shards,
-                      yatt_sample** h_samples);
+                      yatt_rounds_io* io);
 int yatt_rounds_run(yatt_rounds_t h, int64_t n, const int64_t* h_shard_offsets,
                     int32_t num_shards, int32_t first_rank, int32_t step_index,
                     int32_t first_round, int32_t round_limit,

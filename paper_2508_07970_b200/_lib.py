@@ -70,10 +70,15 @@ class ReportC(C.Structure):
                 ("accepted_train_units", c_i64), ("num_microbatches", c_i64)]
 
 
+class RoundsIoC(C.Structure):
+    _fields_ = [("sample_id", c_p), ("prompt_len", c_p), ("accepted", c_p), ("out_len", c_p),
+                ("accepted_round", c_p), ("accepted_out", c_p), ("first_round_len", c_p)]
+
+
 class RoundsViewC(C.Structure):
-    _fields_ = [("samples", c_p), ("n_samples", c_i64), ("first_round_lens", c_p),
-                ("reports", c_p), ("rounds", c_i32), ("num_shards", c_i32),
-                ("microbatches", c_p), ("num_microbatches", c_i64), ("redrawn_on_host", c_i64)]
+    _fields_ = [("reports", c_p), ("rounds", c_i32), ("num_shards", c_i32),
+                ("microbatches", c_p), ("num_microbatches", c_i64), ("redrawn_on_host", c_i64),
+                ("first_round_lens_valid", c_i32)]
 
 
 class LossConfigC(C.Structure):
@@ -103,7 +108,7 @@ SIGNATURES = {
     "yatt_reduce_round_reports": (C.c_int, [c_p, c_i32, c_p, c_p]),
     "yatt_rounds_create": (C.c_int, [P(c_p)]),
     "yatt_rounds_destroy": (None, [c_p]),
-    "yatt_rounds_stage": (C.c_int, [c_p, c_i64, c_i32, P(c_p)]),
+    "yatt_rounds_stage": (C.c_int, [c_p, c_i64, c_i32, P(RoundsIoC)]),
     "yatt_rounds_run": (C.c_int, [c_p, c_i64, P(c_i64), c_i32, c_i32, c_i32, c_i32, c_i32,
                                   P(RoundParamsC), c_i32, c_p]),
     "yatt_rounds_result": (C.c_int, [c_p, P(RoundsViewC)]),

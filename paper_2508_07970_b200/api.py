@@ -21,7 +21,7 @@ import numpy as np
 import torch
 
 from ._lib import (ConfigError, InvalidDistribution, LengthDist, MbAggC, RejectionCfg, ReportC,
-                   RoundParamsC, RoundsViewC, SampleC, check, lib)
+                   RoundParamsC, RoundsIoC, RoundsViewC, SampleC, check, lib)
 
 CONSTANT, UNIFORM, NORMAL, LOGNORMAL = range(4)
 PROMPT_LEN_STREAM, OUTPUT_LEN_STREAM, REJECTION_STREAM = 1, 2, 3
@@ -289,7 +289,8 @@ _ROUNDS: dict = {}
 def _run_rounds(samples, out_attr, offsets, first_rank, step, first_round, limit,
                 params: RoundParams, device):
     """yatt_rounds_run over host samples (one persistent kernel for every
-    round of every shard); returns (reports[round][shard], final SampleC)."""
+    round of every shard); returns (reports[round][shard], final state per
+    sample: (out_len, accepted, accepted_round), None if accepted before)."""
     if params.microbatch_size <= 0:
         raise ConfigError("microbatch_size must be positive")
     dev = torch.device(device)
@@ -301,11 +302,15 @@ def _run_rounds(samples, out_attr, offsets, first_rank, step, first_round, limit
             check(lib().yatt_rounds_create(C.byref(h)))
             _ROUNDS[idx] = h
         n, ns = len(samples), len(offsets) - 1
-        stage = C.c_void_p()
-        check(lib().yatt_rounds_stage(h, n, ns, C.byref(stage)))
+        io = RoundsIoC()
+        check(lib().yatt_rounds_stage(h, n, ns, C.byref(io)))
+        acc = np.array([bool(x.accepted) for x in samples], dtype=np.uint8)
         if n:
-            packed = _pack(samples, out_attr)
-            C.memmove(stage.value, packed.ctypes.data, packed.nbytes)
+            ids = np.array([x.sample_id for x in samples], dtype=np.uint64)
+            prm = np.array([x.prompt_len_tokens for x in samples], dtype=np.int32)
+            C.memmove(io.sample_id, ids.ctypes.data, ids.nbytes)
+            C.memmove(io.prompt_len, prm.ctypes.data, prm.nbytes)
+            C.memmove(io.accepted, acc.ctypes.data, acc.nbytes)
         off = (C.c_int64 * len(offsets))(*offsets)
         check(lib().yatt_rounds_run(h, n, off, ns, first_rank, step, first_round, limit,
                                     C.byref(params.c()), 0, None))
@@ -316,8 +321,11 @@ def _run_rounds(samples, out_attr, offsets, first_rank, step, first_round, limit
         mbs = (MbAggC * max(v.num_microbatches, 1)).from_buffer_copy(
             C.string_at(v.microbatches, C.sizeof(MbAggC) * v.num_microbatches).ljust(
                 C.sizeof(MbAggC), b"\0"))
-        final = (SampleC * max(n, 1)).from_buffer_copy(
-            C.string_at(v.samples, C.sizeof(SampleC) * n).ljust(C.sizeof(SampleC), b"\0"))
+        out_len = np.frombuffer(C.string_at(io.out_len, 4 * n), dtype=np.int32) if n else []
+        out_round = np.frombuffer(C.string_at(io.accepted_round, 4 * n), dtype=np.int32) if n else []
+        out_acc = np.frombuffer(C.string_at(io.accepted_out, n), dtype=np.uint8) if n else []
+        final = [None if acc[i] else (int(out_len[i]), bool(out_acc[i]), int(out_round[i]))
+                 for i in range(n)]  # None: accepted before the call, untouched
     rounds, base = [], 0
     for r in range(v.rounds):
         row = []
@@ -336,8 +344,8 @@ def shard_round_output(state: ShardState, round_: int, params: RoundParams,
                                 state.controller_rank, state.step_index, round_, 1, params,
                                 device)
     for s, c in zip(state.samples, final):
-        s.out_len_tokens, s.accepted, s.accepted_round = c.out_len_tokens, bool(c.accepted), \
-            c.accepted_round
+        if c is not None:
+            s.out_len_tokens, s.accepted, s.accepted_round = c
     return rounds[0][0]
 
 
@@ -363,8 +371,8 @@ def run_rollout_rounds(batch: RolloutBatch, num_controllers: int, params: RoundP
     rounds, final = _run_rounds(batch.samples, "target_out_len_tokens", offsets, 0,
                                 batch.step_index, 1, 0, params, device)
     for s, c in zip(batch.samples, final):
-        s.target_out_len_tokens, s.accepted, s.accepted_round = c.out_len_tokens, \
-            bool(c.accepted), c.accepted_round
+        if c is not None:
+            s.target_out_len_tokens, s.accepted, s.accepted_round = c
     return rounds
 
 

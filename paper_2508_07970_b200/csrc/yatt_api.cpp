@@ -312,12 +312,13 @@ ShardRoundReport shard_round_output(ShardState& state, int round, const RoundPar
   if (params.microbatch_size <= 0) throw ConfigError("microbatch_size must be positive");
   const std::int64_t n = static_cast<std::int64_t>(state.samples.size());
   yatt_rounds_t h = g_rounds.get();
-  yatt_sample* st = nullptr;
-  detail::throw_status(yatt_rounds_stage(h, n, 1, &st));
+  yatt_rounds_io io{};
+  detail::throw_status(yatt_rounds_stage(h, n, 1, &io));
   for (std::int64_t i = 0; i < n; ++i) {
     const ShardSampleState& s = state.samples[static_cast<size_t>(i)];
-    st[i] = yatt_sample{s.sample_id, s.prompt_len_tokens, s.out_len_tokens, s.accepted_round,
-                        s.accepted ? 1 : 0};
+    io.sample_id[i] = s.sample_id;
+    io.prompt_len[i] = s.prompt_len_tokens;
+    io.accepted[i] = s.accepted ? 1 : 0;
   }
   const yatt_round_params p = to_c(params);
   const std::int64_t off[2] = {0, n};
@@ -327,9 +328,10 @@ ShardRoundReport shard_round_output(ShardState& state, int round, const RoundPar
   detail::throw_status(yatt_rounds_result(h, &v));
   for (std::int64_t i = 0; i < n; ++i) {
     ShardSampleState& s = state.samples[static_cast<size_t>(i)];
-    s.out_len_tokens = v.samples[i].out_len_tokens;
-    s.accepted = v.samples[i].accepted != 0;
-    s.accepted_round = v.samples[i].accepted_round;
+    if (s.accepted) continue;  // untouched by the round
+    s.out_len_tokens = io.out_len[i];
+    s.accepted = io.accepted_out[i] != 0;
+    s.accepted_round = io.accepted_round[i];
   }
   return from_c(v.reports[0], v.microbatches);
 }
@@ -380,12 +382,14 @@ std::vector<std::vector<ShardRoundReport>> run_rollout_rounds(workload::RolloutB
     off[static_cast<size_t>(r) + 1] = static_cast<std::int64_t>(sr.end);
   }
   yatt_rounds_t h = g_rounds.get();
-  yatt_sample* st = nullptr;
-  detail::throw_status(yatt_rounds_stage(h, n, num_controllers, &st));
-  const workload::RolloutSample* src = batch.samples.data();
-  for (std::int64_t i = 0; i < n; ++i)
-    st[i] = yatt_sample{src[i].sample_id, src[i].prompt_len_tokens, src[i].target_out_len_tokens,
-                        src[i].accepted_round, src[i].accepted ? 1 : 0};
+  yatt_rounds_io io{};
+  detail::throw_status(yatt_rounds_stage(h, n, num_controllers, &io));
+  workload::RolloutSample* smp = batch.samples.data();
+  for (std::int64_t i = 0; i < n; ++i) {
+    io.sample_id[i] = smp[i].sample_id;
+    io.prompt_len[i] = smp[i].prompt_len_tokens;
+    io.accepted[i] = smp[i].accepted ? 1 : 0;
+  }
   const yatt_round_params p = to_c(params);
   detail::throw_status(yatt_rounds_run(h, n, off.data(), num_controllers, 0, batch.step_index, 1,
                                        0, &p, first_round_lengths ? 1 : 0, nullptr));
@@ -402,13 +406,17 @@ std::vector<std::vector<ShardRoundReport>> run_rollout_rounds(workload::RolloutB
       mb += rep.num_microbatches;
     }
   }
-  workload::RolloutSample* dst = batch.samples.data();
+  if (first_round_lengths) first_round_lengths->resize(static_cast<size_t>(n));
   for (std::int64_t i = 0; i < n; ++i) {  // copy_back (simcore.cpp:107-119)
-    dst[i].target_out_len_tokens = v.samples[i].out_len_tokens;
-    dst[i].accepted = v.samples[i].accepted != 0;
-    dst[i].accepted_round = v.samples[i].accepted_round;
+    if (smp[i].accepted) {  // accepted before the step: untouched
+      if (first_round_lengths) (*first_round_lengths)[static_cast<size_t>(i)] = smp[i].target_out_len_tokens;
+      continue;
+    }
+    smp[i].target_out_len_tokens = io.out_len[i];
+    smp[i].accepted = io.accepted_out[i] != 0;
+    smp[i].accepted_round = io.accepted_round[i];
+    if (first_round_lengths) (*first_round_lengths)[static_cast<size_t>(i)] = io.first_round_len[i];
   }
-  if (first_round_lengths) first_round_lengths->assign(v.first_round_lens, v.first_round_lens + n);
   return all;
 }
 
