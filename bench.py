@@ -443,8 +443,8 @@ def run_b200(args):
 
 def run_e2e(args, dev, ops, cfg, ws, world=1):
     """Same metric through the reference-facing C-ABI call with HOST buffers
-    (yatt_grpo_step_host): each step hands pinned host logits (one prompt
-    group: 8 responses x 512 tokens = 4,096 rows, 2 x 1.25 GB bf16), targets,
+    (yatt_grpo_step_host): each step hands pinned host logits (one configs[1]
+    prompt group: 8 responses x 4,096 tokens = 32,768 rows, 2 x 9.97 GB bf16), targets,
     mask, the group's rewards and old log-probs to one call that streams them
     H2D (chunked, overlapped with A1), runs A1 -> GRPO -> A4 and returns the
     loss sums to the host.  Every rank runs it on its own GPU and host link
@@ -452,13 +452,26 @@ def run_e2e(args, dev, ops, cfg, ws, world=1):
     value = tokens of all ranks / that time."""
     import torch
     import torch.distributed as dist
-    rows = T
     def pinned(t):  # device -> pinned host without a pageable staging copy
         h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
         h.copy_(t)
         return h
+    # the configs[1] group (32,768 rows); halve only if the host cannot pin it
+    rows = CHUNK_ROWS
+    while True:
+        try:
+            h_pol = torch.empty((rows, VOCAB), dtype=torch.bfloat16, pin_memory=True)
+            h_ref = torch.empty((rows, VOCAB), dtype=torch.bfloat16, pin_memory=True)
+            break
+        except RuntimeError as e:
+            if rows <= RESPONSES * 512:
+                raise
+            print(f"e2e: pinning 2 x {rows} rows failed ({e}); halving", file=sys.stderr)
+            rows //= 2
     pol, ref, tgt = ops.synth_logits(SEED, 0, rows, VOCAB, device=dev)
-    h_pol, h_ref, h_tgt = pinned(pol), pinned(ref), pinned(tgt)
+    h_pol.copy_(pol)
+    h_ref.copy_(ref)
+    h_tgt = pinned(tgt)
     h_mask = torch.ones((rows,), dtype=torch.uint8).pin_memory()
     h_rew = pinned(ops.synth_floats(SEED, 105, 0, RESPONSES, "reward", RESPONSES, device=dev))
     logp = ops.token_stats(pol, ref, tgt, None, "k3")[0]

@@ -310,6 +310,18 @@ int yatt_grpo_advantages(const float* d_rewards, int64_t n_samples,
                          float eps, int32_t norm_by_std,
                          const double* d_group_moments /* NULL: compute */,
                          float* d_sample_adv, void* stream);
+/* Boundary exchange for straddling groups, on the device: this rank's      */
+/* 8-double record {group, n, mean, M2} x {first, last local group}; after   */
+/* an all-gather of every rank's record (world x 8, rank order), the merge   */
+/* replaces rows 0 and n_local-1 of the moments table with the Chan merge    */
+/* of all pieces of those groups (same order on every rank: identical bits). */
+int yatt_grpo_boundary_record(const double* d_group_moments, int64_t n_samples,
+                              uint64_t first_sample_id, int32_t group_size,
+                              double* d_record /* [8] */, void* stream);
+int yatt_grpo_merge_boundaries(double* d_group_moments, int64_t n_samples,
+                               uint64_t first_sample_id, int32_t group_size,
+                               const double* d_all_records, int32_t world,
+                               void* stream);
 /* Broadcast one value per sample over its tokens: out[t] = val[s(t)]*mask[t] */
 /* where sample s owns tokens [cu[s], cu[s+1]).  d_mask may be NULL.         */
 int yatt_broadcast_to_tokens(const float* d_sample_vals,
@@ -490,8 +502,9 @@ int yatt_policy_loss_grad(const uint16_t* d_policy_logits,
 /* ------------------------------------------------------------------------ */
 /* A5+A6  dynamic-sampling filter and compaction (bit-exact)                 */
 /* keep_g = !(all rewards of group g are bitwise identical).  Groups are     */
-/* `group_size` consecutive local samples (the local batch is group-aligned, */
-/* n_samples % group_size == 0).  Survivors keep sample order:               */
+/* `group_size` consecutive sample ids; yatt_filter_compact takes a batch    */
+/* starting at id 0 (a trailing partial group is a group of its own).        */
+/* Survivors keep sample order:                                              */
 /*   d_index_map[j] = local index of the j-th kept sample                    */
 /*   d_new_cu[j]    = packed token start of kept sample j (local, from 0);   */
 /*                    d_new_cu[n_kept] = kept tokens                         */
@@ -506,6 +519,28 @@ int yatt_filter_compact(const float* d_rewards, const int64_t* d_seq_lens,
                         uint8_t* d_keep_groups, int32_t* d_index_map,
                         int64_t* d_new_cu, int64_t* d_counts, void* d_workspace,
                         size_t workspace_bytes, void* stream);
+/* Sharded form (groups straddling ranks: sample-level shard_dataset,       */
+/* workload.cpp:183-198, with the group unit sample_id / group_size on      */
+/* GLOBAL ids, workload.cpp:158-160).  The local batch holds global samples  */
+/* [first_sample_id, first_sample_id + n); its first / last local group may  */
+/* be partial.  Each rank writes its 6-word boundary record                  */
+/* (yatt_filter_boundary_record: {group, first reward bits, any-differs} of  */
+/* its first and last local group), the records of all ranks are gathered    */
+/* in rank order (world x 6 int64; yatt_peer_allgather_i64 or                */
+/* yatt_comm_allgather_i64) and passed as d_all_records: every rank holding  */
+/* a piece of a group takes the same exact keep decision.  keep has          */
+/* yatt_grpo_num_local_groups(n, first_sample_id, group_size) entries;       */
+/* counts[2] counts the groups whose first sample is local (once globally).  */
+int yatt_filter_boundary_record(const float* d_rewards, int64_t n_samples,
+                                uint64_t first_sample_id, int32_t group_size,
+                                int64_t* d_record /* [6] */, void* stream);
+int yatt_filter_compact_sharded(const float* d_rewards, const int64_t* d_seq_lens,
+                                int64_t n_samples, uint64_t first_sample_id,
+                                int32_t group_size, const int64_t* d_all_records,
+                                int32_t world, uint8_t* d_keep_groups,
+                                int32_t* d_index_map, int64_t* d_new_cu,
+                                int64_t* d_counts, void* d_workspace,
+                                size_t workspace_bytes, void* stream);
 /* Gather variable-length per-token payload of the kept samples:             */
 /*   dst[off + new_cu[j] + k] = src[old_cu[map[j]] + k], k < len(map[j])     */
 /* for j < *d_n_kept (device count; max_kept bounds the grid).  off =        */
@@ -635,6 +670,26 @@ int yatt_peer_scan_i64(yatt_peer_t peer, const int64_t* d_in, int32_t n,
 #define YATT_PEER_GATHER_MAX_WORDS 16384
 int yatt_peer_allgather_i64(yatt_peer_t peer, const int64_t* d_in, int32_t n,
                             int64_t* d_out, void* stream);
+
+/* Group-level ops of a rank whose shard may split groups with its           */
+/* neighbours, in one call over the peer group: boundary record -> peer      */
+/* all-gather -> device merge -> the op (all stream-ordered; collective:     */
+/* every rank calls).  Advantages equal a single rank's to fp64 rounding of  */
+/* the merged moments; the filter's layout is bit-exact.  Workspace:         */
+/* yatt_straddle_workspace_bytes(n_samples, first_sample_id, G, world).      */
+size_t yatt_straddle_workspace_bytes(int64_t n_samples, uint64_t first_sample_id,
+                                     int32_t group_size, int32_t world);
+int yatt_peer_world(yatt_peer_t p, int32_t* h_world, int32_t* h_rank);
+int yatt_peer_grpo_advantages(yatt_peer_t p, const float* d_rewards, int64_t n_samples,
+                              uint64_t first_sample_id, int32_t group_size, float eps,
+                              int32_t norm_by_std, float* d_sample_adv, void* d_workspace,
+                              size_t workspace_bytes, void* stream);
+int yatt_peer_filter_compact(yatt_peer_t p, const float* d_rewards,
+                             const int64_t* d_seq_lens, int64_t n_samples,
+                             uint64_t first_sample_id, int32_t group_size,
+                             uint8_t* d_keep_groups, int32_t* d_index_map,
+                             int64_t* d_new_cu, int64_t* d_counts, void* d_workspace,
+                             size_t workspace_bytes, void* stream);
 /* yatt_policy_loss whose final reduction also all-reduces across the group:  */
 /* d_sums holds the GLOBAL sums on every rank (one kernel after the partials). */
 int yatt_policy_loss_allreduce(yatt_peer_t peer, const float* d_logp,

@@ -254,13 +254,14 @@ def filter_compact(rewards, lens, group_size):
     r = np.ascontiguousarray(rewards, dtype=np.float32)
     ln = np.ascontiguousarray(lens, dtype=np.int64)
     n = len(r)
-    keep = np.zeros(max(n // group_size, 1), dtype=np.uint8)
+    ng = -(-n // group_size)  # a trailing partial group is a group of its own
+    keep = np.zeros(max(ng, 1), dtype=np.uint8)
     imap = np.zeros(max(n, 1), dtype=np.int32)
     new_cu = np.zeros(n + 1, dtype=np.int64)
     counts = np.zeros(3, dtype=np.int64)
     k = lib().yo_filter_compact(_ptr(r), _ptr(ln), n, group_size, _ptr(keep), _ptr(imap),
                                 _ptr(new_cu), _ptr(counts))
-    return {"keep_groups": keep[: n // group_size], "index_map": imap[:k], "new_cu": new_cu[: k + 1],
+    return {"keep_groups": keep[:ng], "index_map": imap[:k], "new_cu": new_cu[: k + 1],
             "counts": counts}
 
 

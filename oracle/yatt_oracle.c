@@ -499,15 +499,18 @@ void yo_policy_loss(const float* logp, const float* old_logp, const float* adv, 
 }
 
 /* ------------------------------------------------------------- A5/A6 ---- */
-/* Returns kept samples; counts[3] = {samples, tokens, groups}. */
+/* Returns kept samples; counts[3] = {samples, tokens, groups}.  Group of    */
+/* sample i is i / G (workload.cpp:158-160); a trailing partial group (n not  */
+/* a multiple of G) is a group of its own, keep has ceil(n / G) entries.      */
 int64_t yo_filter_compact(const float* r, const int64_t* lens, int64_t n, int G, uint8_t* keep,
                           int32_t* map, int64_t* new_cu, int64_t* counts) {
   int64_t j = 0, tok = 0, kg = 0;
-  for (int64_t g = 0; g < n / G; ++g) {
+  for (int64_t g = 0; g < (n + G - 1) / G; ++g) {
     uint32_t b0;
     memcpy(&b0, &r[g * G], 4);
     uint8_t k = 0;
-    for (int i = 1; i < G; ++i) {
+    const int64_t m = n - g * G < G ? n - g * G : G;
+    for (int64_t i = 1; i < m; ++i) {
       uint32_t bi;
       memcpy(&bi, &r[g * G + i], 4);
       k |= bi != b0;

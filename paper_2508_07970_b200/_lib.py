@@ -149,6 +149,17 @@ SIGNATURES = {
     "yatt_policy_loss_grad": (C.c_int, [c_p] * 7 + [c_i64, c_i32, c_p, c_i64, P(LossConfigC),
                                                     c_i32, c_f64] + [c_p] * 5 + [c_sz, c_p]),
     "yatt_filter_compact_workspace_bytes": (c_sz, [c_i64]),
+    "yatt_filter_boundary_record": (C.c_int, [c_p, c_i64, c_u64, c_i32, c_p, c_p]),
+    "yatt_filter_compact_sharded": (C.c_int, [c_p, c_p, c_i64, c_u64, c_i32, c_p, c_i32, c_p, c_p,
+                                              c_p, c_p, c_p, c_sz, c_p]),
+    "yatt_grpo_boundary_record": (C.c_int, [c_p, c_i64, c_u64, c_i32, c_p, c_p]),
+    "yatt_grpo_merge_boundaries": (C.c_int, [c_p, c_i64, c_u64, c_i32, c_p, c_i32, c_p]),
+    "yatt_straddle_workspace_bytes": (c_sz, [c_i64, c_u64, c_i32, c_i32]),
+    "yatt_peer_world": (C.c_int, [c_p, P(c_i32), P(c_i32)]),
+    "yatt_peer_grpo_advantages": (C.c_int, [c_p, c_p, c_i64, c_u64, c_i32, c_f32, c_i32, c_p, c_p,
+                                            c_sz, c_p]),
+    "yatt_peer_filter_compact": (C.c_int, [c_p, c_p, c_p, c_i64, c_u64, c_i32, c_p, c_p, c_p, c_p,
+                                           c_p, c_sz, c_p]),
     "yatt_filter_compact": (C.c_int, [c_p, c_p, c_i64, c_i32, c_p, c_p, c_p, c_p, c_p, c_sz, c_p]),
     "yatt_gather_varlen": (C.c_int, [c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_i32, c_p, c_p]),
     "yatt_gather_varlen_multi": (C.c_int, [c_i32, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_p,

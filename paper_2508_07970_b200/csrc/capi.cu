@@ -44,7 +44,8 @@ int policy_loss_launch(const float*, const float*, const float*, const float*, c
                        yatt_loss_sums*, void*, size_t, cudaStream_t);
 double loss_finalize(const yatt_loss_sums*, const yatt_loss_config*);
 size_t compact_workspace_bytes(int64_t);
-int filter_compact_launch(const float*, const int64_t*, int64_t, int32_t, uint8_t*, int32_t*,
+int filter_compact_launch(const float*, const int64_t*, int64_t, uint64_t, int32_t, const int64_t*,
+                          int32_t, uint8_t*, int32_t*,
                           int64_t*, int64_t*, void*, size_t, cudaStream_t);
 int gather_varlen_multi_launch(int32_t, const void* const*, void* const*, const int32_t*,
                                const int64_t*, const int32_t*, const int64_t*, const int64_t*,
@@ -554,8 +555,22 @@ int yatt_filter_compact(const float* r, const int64_t* lens, int64_t n, int32_t 
   YATT_ALIGNED("filter_compact", new_cu, 8);
   YATT_ALIGNED("filter_compact", counts, 8);
   YATT_ALIGNED("filter_compact", ws, 8);
-  return filter_compact_launch(r, lens, n, G, keep, map, new_cu, counts, ws, ws_bytes,
-                               as_stream(stream));
+  return filter_compact_launch(r, lens, n, 0, G, nullptr, 1, keep, map, new_cu, counts, ws,
+                               ws_bytes, as_stream(stream));
+}
+
+int yatt_filter_compact_sharded(const float* r, const int64_t* lens, int64_t n,
+                                uint64_t first_sample_id, int32_t G, const int64_t* d_all_records,
+                                int32_t world, uint8_t* keep, int32_t* map, int64_t* new_cu,
+                                int64_t* counts, void* ws, size_t ws_bytes, void* stream) {
+  YATT_ALIGNED4("filter_compact_sharded", r, map, nullptr, nullptr);
+  YATT_ALIGNED("filter_compact_sharded", lens, 8);
+  YATT_ALIGNED("filter_compact_sharded", new_cu, 8);
+  YATT_ALIGNED("filter_compact_sharded", counts, 8);
+  YATT_ALIGNED("filter_compact_sharded", ws, 8);
+  YATT_ALIGNED("filter_compact_sharded", d_all_records, 8);
+  return filter_compact_launch(r, lens, n, first_sample_id, G, d_all_records, world, keep, map,
+                               new_cu, counts, ws, ws_bytes, as_stream(stream));
 }
 
 int yatt_gather_varlen(const void* src, const int64_t* old_cu, const int32_t* map,

@@ -25,15 +25,39 @@ constexpr int kGatherThreads = 256;  // gather_varlen_kernel block size
 constexpr int kScanPerThread = 4;
 constexpr int kScanTile = kScanThreads * kScanPerThread;
 
-__global__ void group_filter_kernel(const float* r, int64_t n, int32_t G, uint8_t* keep) {
-  const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t ng = n / G;
-  if (g >= ng) return;
-  const uint32_t* bits = reinterpret_cast<const uint32_t*>(r) + g * G;
-  const uint32_t b0 = bits[0];
-  uint8_t k = 0;
-  for (int i = 1; i < G; ++i) k |= (bits[i] != b0);
-  keep[g] = k;
+// Local group k of a shard that starts at global sample first_id covers
+// global group g0 + k (g0 = first_id / G), i.e. local samples
+// [max(0, (g0+k)*G - first_id), min(n, (g0+k+1)*G - first_id)); the first and
+// last local groups may be partial when groups straddle ranks (sample-level
+// shard_dataset, workload.cpp:183-198).  keep = some reward differs bitwise
+// from the group's first; for a partial group the other ranks' boundary
+// records (straddle.cu: {group, first reward bits, any-differs} for their
+// first and last local groups) are folded in, so every rank holding a piece
+// of the group takes the same exact decision.
+struct FilterRecord {
+  int64_t g, bits, anydiff;
+};
+
+__global__ void group_filter_kernel(const float* r, int64_t n, uint64_t first_id, int32_t G,
+                                    int64_t ng, const int64_t* recs, int32_t world,
+                                    uint8_t* keep) {
+  const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= ng) return;
+  const uint64_t g = first_id / uint64_t(G) + uint64_t(k);
+  const int64_t lo = max64(0, int64_t(g * uint64_t(G)) - int64_t(first_id));
+  const int64_t hi = min64(n, int64_t((g + 1) * uint64_t(G)) - int64_t(first_id));
+  const uint32_t* bits = reinterpret_cast<const uint32_t*>(r);
+  const uint32_t b0 = bits[lo];
+  uint8_t any = 0;
+  for (int64_t i = lo + 1; i < hi; ++i) any |= (bits[i] != b0);
+  if (recs != nullptr && (k == 0 || k == ng - 1)) {
+    for (int32_t q = 0; q < world; ++q)
+      for (int side = 0; side < 2; ++side) {
+        const int64_t* rec = recs + 6 * q + 3 * side;
+        if (rec[0] == int64_t(g)) any |= uint8_t(rec[2] != 0 || uint32_t(rec[1]) != b0);
+      }
+  }
+  keep[k] = any;
 }
 
 // Block-wide exclusive scan of int64 pairs (samples, tokens); returns totals.
@@ -85,13 +109,14 @@ __device__ __forceinline__ Pair block_exclusive_scan(Pair x, Pair* total) {
 
 // Pass 1: per-tile kept (samples, tokens).
 __global__ void __launch_bounds__(kScanThreads) compact_count_kernel(
-    const uint8_t* keep, const int64_t* lens, int64_t n, int32_t G, int64_t* tile_tot) {
+    const uint8_t* keep, const int64_t* lens, int64_t n, int32_t G, int32_t first_mod,
+    int64_t* tile_tot) {
   const int64_t base = int64_t(blockIdx.x) * kScanTile + int64_t(threadIdx.x) * kScanPerThread;
   Pair x{0, 0};
 #pragma unroll
   for (int k = 0; k < kScanPerThread; ++k) {
     const int64_t i = base + k;
-    if (i < n && keep[i / G]) {
+    if (i < n && keep[(first_mod + i) / G]) {
       x.a += 1;
       x.b += lens[i];
     }
@@ -105,9 +130,11 @@ __global__ void __launch_bounds__(kScanThreads) compact_count_kernel(
 }
 
 // Pass 2: exclusive scan of tile totals (single CTA, sequential chunks).
+// kept_groups counts the groups whose FIRST sample is local (a straddling
+// group is counted once, by the rank holding its start).
 __global__ void __launch_bounds__(kScanThreads) compact_tiles_kernel(
-    int64_t* tile_tot, int64_t ntiles, int64_t n_groups, const uint8_t* keep, int64_t* new_cu,
-    int64_t* counts) {
+    int64_t* tile_tot, int64_t ntiles, int64_t n_groups, int32_t first_mod, const uint8_t* keep,
+    int64_t* new_cu, int64_t* counts) {
   Pair carry{0, 0};
   for (int64_t b0 = 0; b0 < ntiles; b0 += kScanThreads) {
     const int64_t t = b0 + threadIdx.x;
@@ -124,7 +151,8 @@ __global__ void __launch_bounds__(kScanThreads) compact_tiles_kernel(
   }
   // kept groups
   int64_t kg = 0;
-  for (int64_t g = threadIdx.x; g < n_groups; g += kScanThreads) kg += keep[g];
+  for (int64_t g = (first_mod != 0 ? 1 : 0) + threadIdx.x; g < n_groups; g += kScanThreads)
+    kg += keep[g];
   __shared__ int64_t red[kScanThreads / 32];
   kg = warp_sum(kg);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = kg;
@@ -141,15 +169,15 @@ __global__ void __launch_bounds__(kScanThreads) compact_tiles_kernel(
 
 // Pass 3: scatter index map and packed offsets.
 __global__ void __launch_bounds__(kScanThreads) compact_scatter_kernel(
-    const uint8_t* keep, const int64_t* lens, int64_t n, int32_t G, const int64_t* tile_off,
-    int32_t* index_map, int64_t* new_cu) {
+    const uint8_t* keep, const int64_t* lens, int64_t n, int32_t G, int32_t first_mod,
+    const int64_t* tile_off, int32_t* index_map, int64_t* new_cu) {
   const int64_t base = int64_t(blockIdx.x) * kScanTile + int64_t(threadIdx.x) * kScanPerThread;
   Pair x{0, 0};
   bool kk[kScanPerThread];
 #pragma unroll
   for (int k = 0; k < kScanPerThread; ++k) {
     const int64_t i = base + k;
-    kk[k] = i < n && keep[i / G];
+    kk[k] = i < n && keep[(first_mod + i) / G];
     if (kk[k]) {
       x.a += 1;
       x.b += lens[i];
@@ -327,38 +355,80 @@ size_t compact_workspace_bytes(int64_t n) {
   return size_t(2 * ceil_div(n > 0 ? n : 1, kScanTile)) * sizeof(int64_t);
 }
 
-int filter_compact_launch(const float* r, const int64_t* lens, int64_t n, int32_t G,
-                          uint8_t* keep, int32_t* map, int64_t* new_cu, int64_t* counts, void* ws,
+int filter_compact_launch(const float* r, const int64_t* lens, int64_t n, uint64_t first_id,
+                          int32_t G, const int64_t* recs, int32_t world, uint8_t* keep,
+                          int32_t* map, int64_t* new_cu, int64_t* counts, void* ws,
                           size_t ws_bytes, cudaStream_t st) {
   YATT_REQUIRE(G > 0, YATT_ERR_CONFIG, "filter_compact: group_size must be positive");
-  YATT_REQUIRE(n >= 0 && n % G == 0, YATT_ERR_CONFIG,
-               "filter_compact: n_samples (%lld) must be a multiple of group_size (%d)",
-               (long long)n, G);
+  YATT_REQUIRE(n >= 0, YATT_ERR_CONFIG, "filter_compact: n_samples must be >= 0");
   YATT_REQUIRE(n < (int64_t(1) << 31), YATT_ERR_CONFIG, "filter_compact: too many samples");
+  YATT_REQUIRE(recs == nullptr || (world >= 1 && world <= 4096), YATT_ERR_CONFIG,
+               "filter_compact: world must be in [1, 4096] with boundary records");
   YATT_REQUIRE(ws != nullptr && ws_bytes >= compact_workspace_bytes(n), YATT_ERR_WORKSPACE,
                "filter_compact: workspace too small");
-  const int64_t ng = n / G;
+  const int64_t ng = n > 0 ? int64_t((first_id + uint64_t(n) - 1) / uint64_t(G) -
+                                     first_id / uint64_t(G) + 1) : 0;
+  const int32_t first_mod = int32_t(first_id % uint64_t(G));
   if (ng > 0) {
-    group_filter_kernel<<<unsigned(ceil_div(ng, 256)), 256, 0, st>>>(r, n, G, keep);
+    group_filter_kernel<<<unsigned(ceil_div(ng, 256)), 256, 0, st>>>(r, n, first_id, G, ng, recs,
+                                                                     world, keep);
     int rc = check_launch("group_filter_kernel");
     if (rc) return rc;
   }
   const int64_t ntiles = ceil_div(n, kScanTile);
   int64_t* tiles = static_cast<int64_t*>(ws);
   if (ntiles > 0) {
-    compact_count_kernel<<<unsigned(ntiles), kScanThreads, 0, st>>>(keep, lens, n, G, tiles);
+    compact_count_kernel<<<unsigned(ntiles), kScanThreads, 0, st>>>(keep, lens, n, G, first_mod,
+                                                                    tiles);
     int rc = check_launch("compact_count_kernel");
     if (rc) return rc;
   }
-  compact_tiles_kernel<<<1, kScanThreads, 0, st>>>(tiles, ntiles, ng, keep, new_cu, counts);
+  compact_tiles_kernel<<<1, kScanThreads, 0, st>>>(tiles, ntiles, ng, first_mod, keep, new_cu,
+                                                   counts);
   int rc = check_launch("compact_tiles_kernel");
   if (rc) return rc;
   if (ntiles > 0) {
-    compact_scatter_kernel<<<unsigned(ntiles), kScanThreads, 0, st>>>(keep, lens, n, G, tiles,
-                                                                      map, new_cu);
+    compact_scatter_kernel<<<unsigned(ntiles), kScanThreads, 0, st>>>(keep, lens, n, G, first_mod,
+                                                                      tiles, map, new_cu);
     rc = check_launch("compact_scatter_kernel");
   }
   return rc;
+}
+
+// One boundary record {g, first reward bits, any-differs} x {first, last
+// local group}: what the other ranks need to decide a straddling group.
+__global__ void filter_record_kernel(const float* r, int64_t n, uint64_t first_id, int32_t G,
+                                     int64_t* rec) {
+  const uint32_t* bits = reinterpret_cast<const uint32_t*>(r);
+  const uint64_t g0 = first_id / uint64_t(G);
+  const uint64_t g1 = (first_id + uint64_t(n) - 1) / uint64_t(G);
+  for (int side = 0; side < 2; ++side) {
+    const uint64_t g = side == 0 ? g0 : g1;
+    const int64_t lo = max64(0, int64_t(g * uint64_t(G)) - int64_t(first_id));
+    const int64_t hi = min64(n, int64_t((g + 1) * uint64_t(G)) - int64_t(first_id));
+    const uint32_t b0 = bits[lo];
+    int any = 0;
+    for (int64_t i = lo + 1 + threadIdx.x; i < hi; i += blockDim.x) any |= (bits[i] != b0);
+    any = __syncthreads_or(any);
+    if (threadIdx.x == 0) {
+      rec[3 * side + 0] = int64_t(g);
+      rec[3 * side + 1] = int64_t(b0);
+      rec[3 * side + 2] = any;
+    }
+  }
+}
+
+int filter_record_launch(const float* r, int64_t n, uint64_t first_id, int32_t G, int64_t* rec,
+                         cudaStream_t st) {
+  YATT_REQUIRE(G > 0, YATT_ERR_CONFIG, "filter_boundary_record: group_size must be positive");
+  YATT_REQUIRE(rec != nullptr, YATT_ERR_CONFIG, "filter_boundary_record: null record");
+  if (n <= 0) {  // an empty shard holds no group: a record matching nothing
+    const int64_t none[6] = {-1, 0, 0, -1, 0, 0};
+    YATT_TRY_CUDA(cudaMemcpyAsync(rec, none, sizeof(none), cudaMemcpyHostToDevice, st));
+    return YATT_OK;
+  }
+  filter_record_kernel<<<1, 256, 0, st>>>(r, n, first_id, G, rec);
+  return check_launch("filter_record_kernel");
 }
 
 int gather_varlen_multi_launch(int32_t n_arrays, const void* const* srcs, void* const* dsts,

@@ -295,6 +295,15 @@ int yatt_peer_destroy(yatt_peer_t p) {
   return YATT_OK;
 }
 
+int yatt_peer_world(yatt_peer_t p, int32_t* world, int32_t* rank) {
+  YATT_REQUIRE(p != nullptr && world != nullptr && rank != nullptr, YATT_ERR_CONFIG,
+               "peer_world: null arg");
+  YATT_REQUIRE(p->connected, YATT_ERR_CONFIG, "peer: create + connect the peer group first");
+  *world = p->world;
+  *rank = p->rank;
+  return YATT_OK;
+}
+
 int yatt_peer_status(yatt_peer_t p, int32_t* h_status) {
   YATT_REQUIRE(p != nullptr && h_status != nullptr, YATT_ERR_CONFIG, "peer_status: null arg");
   uint32_t s = 0;

@@ -328,22 +328,62 @@ def loss_finalize(sums, config: LossConfigC | None = None) -> float:
 
 
 # ------------------------------------------------------------- A5 / A6 ----
-def filter_compact(rewards: torch.Tensor, seq_lens: torch.Tensor, group_size: int):
+def filter_compact(rewards: torch.Tensor, seq_lens: torch.Tensor, group_size: int,
+                   first_sample_id: int = 0, all_records: torch.Tensor | None = None,
+                   world: int = 1):
+    """A5+A6.  first_sample_id / all_records: a shard of a sample-level split
+    whose boundary groups straddle ranks (yatt_filter_compact_sharded; the
+    records are every rank's filter_boundary_record, gathered in rank order)."""
     _dev(rewards, torch.float32, "rewards")
     _dev(seq_lens, torch.int64, "seq_lens")
     n = rewards.numel()
     _numel(n, seq_lens=seq_lens)
     dev = rewards.device
-    keep = torch.empty((max(n // group_size, 1),), dtype=torch.uint8, device=dev)
+    ng = lib().yatt_grpo_num_local_groups(n, first_sample_id, group_size)
+    keep = torch.empty((max(ng, 1),), dtype=torch.uint8, device=dev)
     imap = torch.empty((max(n, 1),), dtype=torch.int32, device=dev)
     new_cu = torch.empty((n + 1,), dtype=torch.int64, device=dev)
     counts = torch.empty((3,), dtype=torch.int64, device=dev)
     wsb = lib().yatt_filter_compact_workspace_bytes(n)
     ws = torch.empty((wsb,), dtype=torch.uint8, device=dev)
-    check(lib().yatt_filter_compact(_p(rewards), _p(seq_lens), n, group_size, _p(keep), _p(imap),
-                                    _p(new_cu), _p(counts), _p(ws), wsb, _st()))
-    return {"keep_groups": keep[: n // group_size], "index_map": imap, "new_cu": new_cu,
-            "counts": counts}
+    if first_sample_id == 0 and all_records is None:
+        check(lib().yatt_filter_compact(_p(rewards), _p(seq_lens), n, group_size, _p(keep),
+                                        _p(imap), _p(new_cu), _p(counts), _p(ws), wsb, _st()))
+    else:
+        if all_records is not None:
+            _dev(all_records, torch.int64, "all_records")
+        check(lib().yatt_filter_compact_sharded(_p(rewards), _p(seq_lens), n, first_sample_id,
+                                                group_size, _p(all_records), world, _p(keep),
+                                                _p(imap), _p(new_cu), _p(counts), _p(ws), wsb,
+                                                _st()))
+    return {"keep_groups": keep[:ng], "index_map": imap, "new_cu": new_cu, "counts": counts}
+
+
+def filter_boundary_record(rewards: torch.Tensor, group_size: int,
+                           first_sample_id: int = 0) -> torch.Tensor:
+    _dev(rewards, torch.float32, "rewards")
+    rec = torch.empty((6,), dtype=torch.int64, device=rewards.device)
+    check(lib().yatt_filter_boundary_record(_p(rewards), rewards.numel(), first_sample_id,
+                                            group_size, _p(rec), _st()))
+    return rec
+
+
+def grpo_boundary_record(moments: torch.Tensor, n: int, group_size: int,
+                         first_sample_id: int = 0) -> torch.Tensor:
+    _dev(moments, torch.float64, "moments")
+    rec = torch.empty((8,), dtype=torch.float64, device=moments.device)
+    check(lib().yatt_grpo_boundary_record(_p(moments), n, first_sample_id, group_size, _p(rec),
+                                          _st()))
+    return rec
+
+
+def grpo_merge_boundaries(moments: torch.Tensor, n: int, group_size: int, first_sample_id: int,
+                          all_records: torch.Tensor) -> torch.Tensor:
+    _dev(moments, torch.float64, "moments")
+    _dev(all_records, torch.float64, "all_records")
+    check(lib().yatt_grpo_merge_boundaries(_p(moments), n, first_sample_id, group_size,
+                                           _p(all_records), all_records.numel() // 8, _st()))
+    return moments
 
 
 def gather_varlen(src: torch.Tensor, old_cu: torch.Tensor, index_map: torch.Tensor,

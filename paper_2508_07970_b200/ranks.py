@@ -177,6 +177,38 @@ class PeerGroup:
                                                ws.buf.numel(), self._st()))
         return sums
 
+    def _straddle_ws(self, n, first_sample_id, group_size, device):
+        wsb = lib().yatt_straddle_workspace_bytes(n, first_sample_id, group_size, self.world)
+        return torch.empty((wsb,), dtype=torch.uint8, device=device), wsb
+
+    def grpo_advantages(self, rewards, group_size, first_sample_id=0, eps=1e-6, norm_by_std=True):
+        """GRPO advantages of this rank's shard (global ids [first_sample_id,
+        + n)) whose first / last groups may straddle ranks: boundary moments
+        exchanged over peer memory and merged on the device, one call
+        (yatt_peer_grpo_advantages)."""
+        adv = torch.empty_like(rewards)
+        ws, wsb = self._straddle_ws(rewards.numel(), first_sample_id, group_size, rewards.device)
+        check(lib().yatt_peer_grpo_advantages(self.h, rewards.data_ptr(), rewards.numel(),
+                                              first_sample_id, group_size, eps, int(norm_by_std),
+                                              adv.data_ptr(), ws.data_ptr(), wsb, self._st()))
+        return adv
+
+    def filter_compact(self, rewards, seq_lens, group_size, first_sample_id=0):
+        """Zero-variance filter + compaction of this rank's shard with exact
+        decisions for straddling groups (yatt_peer_filter_compact)."""
+        n, dev = rewards.numel(), rewards.device
+        ng = lib().yatt_grpo_num_local_groups(n, first_sample_id, group_size)
+        keep = torch.empty((max(ng, 1),), dtype=torch.uint8, device=dev)
+        imap = torch.empty((max(n, 1),), dtype=torch.int32, device=dev)
+        new_cu = torch.empty((n + 1,), dtype=torch.int64, device=dev)
+        counts = torch.empty((3,), dtype=torch.int64, device=dev)
+        ws, wsb = self._straddle_ws(n, first_sample_id, group_size, dev)
+        check(lib().yatt_peer_filter_compact(self.h, rewards.data_ptr(), seq_lens.data_ptr(), n,
+                                             first_sample_id, group_size, keep.data_ptr(),
+                                             imap.data_ptr(), new_cu.data_ptr(), counts.data_ptr(),
+                                             ws.data_ptr(), wsb, self._st()))
+        return {"keep_groups": keep[:ng], "index_map": imap, "new_cu": new_cu, "counts": counts}
+
     def status(self) -> int:
         s = C.c_int32()
         check(lib().yatt_peer_status(self.h, C.byref(s)))

@@ -363,9 +363,22 @@ def test_filter_compact_edge_cases(cuda):
     e = ops.filter_compact(torch.empty(0, device=cuda), torch.empty(0, dtype=torch.int64,
                                                                       device=cuda), G)
     assert e["counts"].cpu().tolist() == [0, 0, 0]
+    # a trailing partial group (n % G != 0) is a group of its own
+    # (group = sample_id / G, workload.cpp:158-160); a lone sample is zero-variance
+    for r_list in ([1, 1, 1, 1, 2, 3], [1, 2, 1, 1, 5, 5, 5], [0, 1, 0, 0, 7],
+                   [3, 3, 3, 3, 1, 2, 2, 2, 9]):
+        r = torch.tensor(r_list, dtype=torch.float32, device=cuda)
+        ln = torch.arange(1, len(r_list) + 1, dtype=torch.int64, device=cuda)
+        out = ops.filter_compact(r, ln, G)
+        exp = O.filter_compact(r.cpu().numpy(), ln.cpu().numpy(), G)
+        k = int(exp["counts"][0])
+        assert out["counts"].cpu().tolist() == exp["counts"].tolist(), r_list
+        assert np.array_equal(out["keep_groups"].cpu().numpy(), exp["keep_groups"]), r_list
+        assert np.array_equal(out["index_map"][:k].cpu().numpy(), exp["index_map"]), r_list
+        assert np.array_equal(out["new_cu"][:k + 1].cpu().numpy(), exp["new_cu"]), r_list
     with pytest.raises(ConfigError):
         ops.filter_compact(torch.ones(6, device=cuda), torch.ones(6, dtype=torch.int64,
-                                                                 device=cuda), 4)
+                                                                 device=cuda), 0)
 
 
 def test_microbatch_aggregates_over_survivors(cuda):
@@ -494,3 +507,50 @@ def test_gather_varlen_multi_matches_single(cuda):
     with pytest.raises(ConfigError):
         ops.gather_varlen_multi(srcs * 2, old_cu, plan["index_map"], plan["new_cu"],
                                 plan["counts"][:1], n, fused * 2)
+
+
+# ----------------------------------------------- groups straddling ranks ----
+@pytest.mark.parametrize("P", [3, 7])
+def test_straddling_groups_emulated_ranks(cuda, P):
+    """The reference's SAMPLE-level shard_dataset (workload.cpp:183-198) over
+    configs[4]'s 1,024 x 16 samples at P = 3 / 7 splits groups across ranks.
+    Each emulated rank writes its boundary records, the records are stacked
+    in rank order (what the all-gather delivers), and every rank's sharded
+    filter + GRPO merge run on its own slice: the global compaction layout is
+    byte-identical to one rank's and the advantages match to 1e-12."""
+    n, G, lens_np, rew = _config5_batch(cuda, token_scale=512)
+    lens = torch.as_tensor(lens_np, device=cuda)
+    single = ops.filter_compact(rew, lens, G)
+    adv_one = ops.grpo_advantages(rew, G)
+    shards = [api.shard_dataset(n, P, r) for r in range(P)]
+    assert any(s.begin % G for s in shards)  # some group really straddles
+    frecs = torch.stack([ops.filter_boundary_record(rew[s.begin:s.end].contiguous(), G, s.begin)
+                         for s in shards]).view(-1)
+    moms = [ops.grpo_group_moments(rew[s.begin:s.end].contiguous(), G, s.begin) for s in shards]
+    grecs = torch.stack([ops.grpo_boundary_record(m, s.size(), G, s.begin)
+                         for m, s in zip(moms, shards)]).view(-1)
+    cu = torch.zeros(n + 1, dtype=torch.int64, device=cuda)
+    cu[1:] = torch.cumsum(lens, 0)
+    payload = torch.arange(int(cu[-1]), dtype=torch.int32, device=cuda)
+    kt = int(single["counts"][1])
+    dst = torch.full((kt,), -1, dtype=torch.int32, device=cuda)
+    off = torch.zeros(3, dtype=torch.int64, device=cuda)
+    kept_groups = 0
+    for s, m in zip(shards, moms):
+        sl = slice(s.begin, s.end)
+        loc = ops.filter_compact(rew[sl].contiguous(), lens[sl].contiguous(), G, s.begin, frecs, P)
+        lcu = (cu[s.begin:s.end + 1] - cu[s.begin]).contiguous()
+        ops.gather_varlen(payload[int(cu[s.begin]):int(cu[s.end])].contiguous(), lcu,
+                          loc["index_map"], loc["new_cu"], loc["counts"][:1], s.size(), dst,
+                          off[1:2].clone())
+        off += loc["counts"]
+        kept_groups += int(loc["counts"][2])
+        ops.grpo_merge_boundaries(m, s.size(), G, s.begin, grecs)
+        adv = ops.grpo_advantages(rew[sl].contiguous(), G, first_sample_id=s.begin, moments=m)
+        assert torch.allclose(adv.double(), adv_one[sl].double(), rtol=1e-12, atol=1e-12)
+    ref = torch.empty(kt, dtype=torch.int32, device=cuda)
+    ops.gather_varlen(payload, cu, single["index_map"], single["new_cu"], single["counts"][:1], n,
+                      ref)
+    assert off.tolist() == single["counts"].tolist()
+    assert kept_groups == int(single["counts"][2])
+    assert torch.equal(dst, ref)

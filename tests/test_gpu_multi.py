@@ -1,6 +1,6 @@
 """Multi-rank path on a real GPU box, including the driver's 1-GPU box.
 
-* test_peer_world_oversubscribed: world 2 / 8 ranks (torchrun, gloo for the
+* test_peer_world_oversubscribed: world 2 / 3 / 7 / 8 ranks (torchrun, gloo for the
   plumbing) mapped onto however many GPUs the box has (rank r -> GPU r % n;
   same-device CUDA IPC works between processes).  tools/peer_world8.py runs
   the NVLink peer-memory collectives for real and checks, against the
@@ -41,7 +41,7 @@ def _torchrun(world, script, timeout):
                           env={**os.environ, "NCCL_DEBUG": "WARN", "OMP_NUM_THREADS": "1"})
 
 
-@pytest.mark.parametrize("world", [2, 8])
+@pytest.mark.parametrize("world", [2, 3, 7, 8])
 def test_peer_world_oversubscribed(cuda, world):
     res = _torchrun(world, "peer_world8.py", 900)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]

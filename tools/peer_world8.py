@@ -14,6 +14,8 @@ math is exact):
   * policy_loss over 8 prompt-group shards == the full batch on one rank
     (max rel 1e-12: fp64 reassociation only);
   * the same under CUDA-graph replay;
+  * groups straddling ranks (sample-level shard_dataset; world 3 / 7):
+    GRPO advantages and the filter + compaction layout == one rank's;
   * global compaction: per-rank zero-variance filter + survivor counts scanned
     over peer memory -> one packed layout == the single-process compaction;
   * the all-gather (9,000 words per rank) and a full dynamic-sampling round
@@ -154,6 +156,46 @@ def main():
         if int(red[5]) == 0:
             break
     assert rnd == len(ref_rounds)
+    # groups straddling ranks: the reference's SAMPLE-level shard_dataset
+    # (workload.cpp:183-198) of N = 16 x 8 samples; at world 3 / 7 groups of 8
+    # split across ranks.  Advantages == one rank's (fp64 moments merged on
+    # the device), filter + compaction layout byte-identical.
+    n_all = P * R
+    from paper_2508_07970_b200 import api
+    sr = api.shard_dataset(n_all, world, rank)
+    b, e = sr.begin, sr.end
+    rew_all = ops.synth_floats(SEED, 105, 0, n_all, "reward", R, device=dev)
+    mine = rew_all[b:e].contiguous()
+    adv = peer.grpo_advantages(mine, R, b)
+    adv_one = ops.grpo_advantages(rew_all, R)
+    torch.cuda.synchronize()
+    assert torch.allclose(adv.double(), adv_one[b:e].double(), rtol=1e-12, atol=1e-12), rank
+    got = torch.zeros(n_all, dtype=torch.float32)
+    got[b:e] = adv.cpu()
+    dist.all_reduce(got)
+    assert torch.equal(got, adv_one.cpu()), "straddle advantages"
+    lens_all = torch.full((n_all,), T, dtype=torch.int64, device=dev) + \
+        torch.arange(n_all, dtype=torch.int64, device=dev) % 5
+    single2 = ops.filter_compact(rew_all, lens_all, R)
+    loc2 = peer.filter_compact(mine, lens_all[b:e].contiguous(), R, b)
+    pre2, tot2 = peer.scan_i64(loc2["counts"])
+    assert tot2.tolist() == single2["counts"].tolist(), (tot2, single2["counts"])
+    cu2 = torch.zeros(n_all + 1, dtype=torch.int64, device=dev)
+    cu2[1:] = torch.cumsum(lens_all, 0)
+    pay2 = torch.arange(int(cu2[-1]), dtype=torch.int32, device=dev)
+    kt2 = int(single2["counts"][1])
+    dst2 = torch.zeros(kt2, dtype=torch.int32, device=dev)
+    lcu = (cu2[b:e + 1] - cu2[b]).contiguous()
+    ops.gather_varlen(pay2[int(cu2[b]):int(cu2[e])].contiguous(), lcu, loc2["index_map"],
+                      loc2["new_cu"], loc2["counts"][:1], e - b, dst2, pre2[1:2].contiguous())
+    ref2 = torch.empty(kt2, dtype=torch.int32, device=dev)
+    ops.gather_varlen(pay2, cu2, single2["index_map"], single2["new_cu"], single2["counts"][:1],
+                      n_all, ref2)
+    torch.cuda.synchronize()
+    m2 = dst2.cpu()
+    dist.all_reduce(m2)
+    assert torch.equal(m2, ref2.cpu()), "straddle compaction"
+
     assert peer.status() == 0
     dist.barrier()
     peer.close()
