@@ -441,6 +441,17 @@ def run_b200(args):
     return 0
 
 
+def _mem_available_bytes() -> int:
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
 def run_e2e(args, dev, ops, cfg, ws, world=1):
     """Same metric through the reference-facing C-ABI call with HOST buffers
     (yatt_grpo_step_host): each step hands pinned host logits (one configs[1]
@@ -456,8 +467,15 @@ def run_e2e(args, dev, ops, cfg, ws, world=1):
         h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
         h.copy_(t)
         return h
-    # the configs[1] group (32,768 rows); halve only if the host cannot pin it
+    # the configs[1] group (32,768 rows); halved while two pinned copies would
+    # take more than half the host's available memory split over the local
+    # ranks (8 ranks on one box must not drive the host out of memory), and
+    # again if pinning itself fails
+    local = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    avail = _mem_available_bytes()
     rows = CHUNK_ROWS
+    while avail and rows > RESPONSES * 512 and 2 * rows * VOCAB * 2 > 0.5 * avail / local:
+        rows //= 2
     while True:
         try:
             h_pol = torch.empty((rows, VOCAB), dtype=torch.bfloat16, pin_memory=True)

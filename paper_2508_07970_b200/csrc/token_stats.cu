@@ -35,6 +35,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -1023,7 +1024,389 @@ __global__ void __launch_bounds__(kFThreads, kFMinB) policy_loss_grad_kernel(con
   }
 }
 
+#if !defined(YATT_FUSED_ONLY_TU)
+// ----------------------------------------------------------------------
+// Large-vocabulary form of the fused loss + gradient: the kernel above with
+// the row-end bubble and most of the instruction overhead removed.
+//
+// The kernel above is issue-bound, not HBM-bound (ncu, 8,192 x 152,064 k3:
+// 19.8 thread instructions per logit for ~10 of arithmetic, issue 66%, DRAM
+// 62%): every CTA stalls twice per row at named barriers around a one-warp
+// fp64 epilogue, the consumers' per-tile bookkeeping is 64-bit, and the spin
+// loops of idle warps take issue slots.  Here:
+//   * a dedicated EPILOGUE warp owns the row end.  Consumers publish their
+//     warp partials (double-buffered by row parity) and arrive on an
+//     mbarrier; the epilogue warp combines them, derives the coefficients
+//     pass 2 needs in fp32 (only a ratio within 1e-4 of a clip boundary
+//     redoes the surrogate's branch from the fp64 log-prob) and releases the
+//     consumers, then writes the fp64 per-token outputs off the critical path;
+//   * pass 2 uses folded coefficients: t = c1 a + c0 (- f z), one FFMA2 per
+//     pair instead of FMUL2 + FADD2 + FFMA2 (+ 3 for the full KL);
+//   * 32-bit tile bookkeeping, full tiles unpredicated, and k3 stages of
+//     16,384 logits (32 KB, 6 stages) so each warp's per-tile overhead covers
+//     twice the work;
+//   * every mbarrier wait carries a suspend-time hint, so waiting warps sleep
+//     instead of spinning (the spin loops were ~9% of issued instructions).
+// Pass order per row stays pass 1 -> pass 2 (pipelining pass 1 of the next
+// row ahead, or splitting rows over a CTA cluster, was measured slower: the
+// extra live rows overflow L2 / the cluster exchange couples the CTAs,
+// profiles/r2_fused_pipe_v1.jsonl).  HBM bytes per row: 2V (4V full KL) read
+// once, 2V written.
+// ----------------------------------------------------------------------
+constexpr int kPThreads = kFThreads + 32;  // consumers + producer + epilogue warp
+constexpr size_t kPRing = size_t(kFStages) * kTile * sizeof(uint16_t);  // 192 KB
+
+struct __align__(16) PipeTail {
+  uint64_t full[kFStages];
+  uint64_t empty[kFStages];
+  uint64_t pfull[2];  // consumer warps' partials published (count kFCW)
+  uint64_t cfull[2];  // row coefficients ready (count 1)
+  RowPartial red[2][kFCW];
+  float2 xy[2];       // {target logit, valid}
+  float coef[2][12];  // gm::RowCoef order, then the folded c1, c0, f
+};
+constexpr size_t kPipeSmem = kPRing + sizeof(PipeTail);
+
+// try_wait with a suspend-time hint: the warp sleeps until the phase
+// completes (or the hint expires) instead of spinning on issue slots.
+__device__ __forceinline__ void mbar_sleep_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+        : "memory");
+  }
+}
+
+// Gradient of 8 logits with the folded row coefficients:
+//   a = x log2e - lse2, p = 2^a, t = c1 a + c0 (- f z), grad = p t
+// (= p (h (log p + H) - g + f (log p - log q - KL)), grad_math.cuh).
+template <bool kFull>
+__device__ __forceinline__ uint4 grad_vec_folded(const uint4& P, const uint4& Q, float2 nl,
+                                                 float2 c1, float2 c0, float2 nf) {
+  const uint32_t pw[4] = {P.x, P.y, P.z, P.w};
+  const uint32_t qw[4] = {Q.x, Q.y, Q.z, Q.w};
+  uint32_t out[4];
+  const float2 L2 = f2(kLog2e, kLog2e);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 a = __ffma2_rn(f2(bf16_lo(pw[k]), bf16_hi(pw[k])), L2, nl);
+    const float2 e = ex2x2(a);
+    float2 t = __ffma2_rn(c1, a, c0);
+    if (kFull) t = __ffma2_rn(nf, f2(bf16_lo(qw[k]), bf16_hi(qw[k])), t);
+    const float2 gr = __fmul2_rn(e, t);
+    out[k] = pack_bf16x2(gr.x, gr.y);
+  }
+  return make_uint4(out[0], out[1], out[2], out[3]);
+}
+
+template <bool kFull>
+__global__ void __launch_bounds__(kPThreads, 1) policy_loss_grad_pipe_kernel(const FusedParams p) {
+  constexpr int kPS = kFull ? 2 : 1;               // tensors per stage
+  constexpr int kPT = kFull ? kTile : 2 * kTile;   // logits per tensor per stage
+  constexpr int kNS = kFStages * kTile / (kPS * kPT);  // stages
+  constexpr int kPVec = kPT / 8;                   // 16-byte vectors per tensor tile
+  constexpr int kPV = kPVec / kFC;                 // per consumer thread
+  static_assert(kPVec % kFC == 0, "pipe tile");
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint16_t* ring = reinterpret_cast<uint16_t*>(smem);
+  PipeTail* tail = reinterpret_cast<PipeTail*>(smem + kPRing);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int V = p.V;
+  const int ntiles = (V + kPT - 1) / kPT, nfull = V / kPT;
+  const int last_nvec = (V - nfull * kPT) >> 3;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kNS; ++s) {
+      mbar_init(&tail->full[s], 1);
+      mbar_init(&tail->empty[s], kFCW);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tail->pfull[b], kFCW);
+      mbar_init(&tail->cfull[b], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == kFCW) {
+    // ---------------- producer: every valid row twice ----------------
+    if (lane == 0) {
+      const uint64_t keep = l2_evict_normal_policy(), drop = l2_evict_first_policy();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
+        if (p.mask != nullptr && p.mask[row] == 0) continue;
+        const uint16_t* gp = p.pol + row * int64_t(V);
+        const uint16_t* gq = kFull ? p.ref + row * int64_t(V) : nullptr;
+        for (int pass = 0; pass < 2; ++pass) {
+          const uint64_t pol = pass == 0 ? keep : drop;
+          for (int t = 0; t < ntiles; ++t) {
+            const int e0 = t * kPT;
+            const uint32_t n = uint32_t(min(kPT, V - e0));
+            mbar_sleep_wait(&tail->empty[stage], phase ^ 1u);
+            mbar_arrive_expect_tx(&tail->full[stage], 2u * n * kPS);
+            uint16_t* dst = ring + size_t(stage) * kPS * kPT;
+            bulk_g2s(dst, gp + e0, 2u * n, &tail->full[stage], pol);
+            if (kFull) bulk_g2s(dst + kPT, gq + e0, 2u * n, &tail->full[stage], pol);
+            if (++stage == kNS) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == kFCW + 1) {
+    // ---------------- epilogue warp: row partials -> coefficients ----------
+    int j = 0;
+    for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
+      if (p.mask != nullptr && p.mask[row] == 0) continue;
+      const int b = j & 1;
+      // per-token inputs first: their latency hides under the wait
+      float r_old = 0.f, r_adv = 0.f, r_rl = 0.f, r_sc = 0.f;
+      if (lane < 2) {
+        r_old = __ldg(p.old_logp + row);
+        r_adv = __ldg(p.adv + row);
+        r_rl = p.ref_logp ? __ldg(p.ref_logp + row) : 0.f;
+        r_sc = p.scale ? __ldg(p.scale + row) : 0.f;
+      }
+      mbar_sleep_wait(&tail->pfull[b], uint32_t(j >> 1) & 1u);
+      RowPartial q = tail->red[b][lane & (kFCW - 1)];
+#pragma unroll
+      for (int off = kFCW / 2; off > 0; off >>= 1) q = combine(q, shfl_partial(q, off));
+      const float2 xyh = tail->xy[b];
+      const float xy = xyh.y != 0.f ? xyh.x : __uint_as_float(0x7fc00000u);
+      // (1) the coefficients pass 2 waits on, in fp32 (they scale a bf16
+      // gradient); a ratio within 1e-4 of a clip boundary takes the branch
+      // from the fp64 log-prob, so the clip decision is the fp64 one
+      if (lane == 0) {
+        const float sc = p.scale ? r_sc : float(p.inv_norm);
+        const float l2s = log2f(q.s);
+        const float lse2 = q.mp + l2s;
+        const float lpf = xy - kLn2f * lse2;
+        const float Hf = kLn2f * (l2s - q.w / q.s);
+        const float h = sc * p.cfg.entropy_coef;
+        float f = 0.f, lseq2 = 0.f, klf = 0.f;
+        if (kFull) {
+          f = sc * p.cfg.kl_coef;
+          lseq2 = q.mq + log2f(q.sq);
+          klf = q.u / q.s + kLn2f * ((q.mq - q.mp) + log2f(q.sq / q.s));
+        }
+        const float A = r_adv, ratio = expf(lpf - r_old);
+        const float lo = 1.f - p.cfg.clip_low, hi = 1.f + p.cfg.clip_high;
+        const float band = 1e-4f * ratio;
+        bool near = fabsf(ratio - lo) <= band || fabsf(ratio - hi) <= band || !(ratio < 3e38f);
+        float dpg;
+        {
+          const float pg1 = -A * ratio, pg2 = -A * fminf(fmaxf(ratio, lo), hi);
+          const float pg = fmaxf(pg1, pg2);
+          bool active = !(pg2 > pg1);
+          if (p.cfg.clip_ratio_c > 1.f && A < 0.f) {
+            const float bound = -A * p.cfg.clip_ratio_c;
+            near = near || fabsf(pg - bound) <= 1e-4f * fabsf(bound);
+            if (bound < pg) active = false;
+          }
+          dpg = active ? -A * ratio : 0.f;
+        }
+        if (near) {  // rare: the exact fp64 decision
+          const double lp64 = double(xy) - kLn2 * (double(q.mp) + log2(double(q.s)));
+          dpg = float(gm::dloss_dlogp_pg(lp64, double(r_old), double(A), p.cfg));
+        }
+        float dkl = 0.f;
+        if (!kFull) {
+          const float delta = (p.ref_logp ? r_rl : lpf) - lpf;
+          dkl = p.kl_mode == YATT_KL_K1 ? 1.f : p.kl_mode == YATT_KL_K2 ? -delta : -expm1f(delta);
+        }
+        const float g = sc * (dpg + p.cfg.kl_coef * dkl);
+        float* cf = tail->coef[b];
+        cf[0] = g;
+        cf[1] = h;
+        cf[2] = f;
+        cf[3] = lse2;
+        cf[4] = lseq2;
+        cf[5] = Hf;
+        cf[6] = klf;
+        cf[8] = (h + f) * kLn2f;
+        cf[9] = fmaf(h, Hf, -g) + f * fmaf(kLn2f, lseq2, -klf);
+        cf[10] = -f;
+        mbar_arrive(&tail->cfull[b]);
+      }
+      // (2) the per-token outputs in fp64 (A1's numerics), off the critical
+      // path: lane 0 logp / H (/ the full KL), lane 1 the KL estimator
+      if (lane < 2) {
+        const double l2s = log2(double(q.s));
+        const double lp = double(xy) - kLn2 * (double(q.mp) + l2s);
+        if (lane == 0) {
+          p.logp[row] = float(lp);
+          if (p.ent) p.ent[row] = float(kLn2 * (l2s - double(q.w) / double(q.s)));
+          if (kFull && p.kl) {
+            const double dlse = kLn2 * ((double(q.mq) - double(q.mp)) +
+                                        log2(double(q.sq) / double(q.s)));
+            p.kl[row] = float(double(q.u) / double(q.s) + dlse);
+          }
+        } else if (!kFull && p.kl) {
+          const double delta = (p.ref_logp ? double(r_rl) : lp) - lp;
+          double k;
+          if (p.kl_mode == YATT_KL_K1) k = -delta;
+          else if (p.kl_mode == YATT_KL_K2) k = 0.5 * delta * delta;
+          else k = expm1(delta) - delta;
+          p.kl[row] = float(k);
+        }
+      }
+      __syncwarp();
+      ++j;
+    }
+  } else {
+    // ---------------- consumers ----------------
+    const int tid = threadIdx.x;
+    int stage = 0;
+    uint32_t phase = 0;
+    Acc<kFull, kFull> acc;
+    const uint4 ninf = make_uint4(kNegInf2, kNegInf2, kNegInf2, kNegInf2);
+    int j = 0;
+    for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
+      uint16_t* gs = p.grad + row * int64_t(V);
+      if (p.mask != nullptr && p.mask[row] == 0) {
+        if (tid == 0) {
+          p.logp[row] = 0.f;
+          if (p.ent) p.ent[row] = 0.f;
+          if (p.kl) p.kl[row] = 0.f;
+        }
+        for (int v = tid; v < V / 8; v += kFC) gm::stg_cs_128(gs + v * 8, make_uint4(0, 0, 0, 0));
+        continue;
+      }
+      const int b = j & 1;
+      const int32_t y = __ldg(p.tgt + row);
+      const bool yok = y >= 0 && y < V;
+      const int ty = yok ? y / kPT : -1, yin = yok ? y - ty * kPT : 0;
+      float xy = 0.f;
+      acc.reset();
+      // ---- pass 1: online log2 LSE(s) + entropy (+ full-KL) sums ----
+      for (int t = 0; t < ntiles; ++t) {
+        const uint16_t* sp = ring + size_t(stage) * kPS * kPT;
+        const uint16_t* sq = sp + kPT;
+        const bool whole = t < nfull;
+        mbar_sleep_wait(&tail->full[stage], phase);
+        if (tid == 0 && t == ty) xy = __uint_as_float(uint32_t(sp[yin]) << 16);
+        uint4 P[kPV], Q[kPV];
+        if (whole) {
+#pragma unroll
+          for (int i = 0; i < kPV; ++i) {
+            P[i] = floor_policy(lds128(sp + (tid + i * kFC) * 8));
+            Q[i] = kFull ? floor_policy(lds128(sq + (tid + i * kFC) * 8)) : P[i];
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < kPV; ++i) {
+            const int v = tid + i * kFC;
+            P[i] = floor_policy(v < last_nvec ? lds128(sp + v * 8) : ninf);
+            Q[i] = kFull ? floor_policy(v < last_nvec ? lds128(sq + v * 8) : ninf) : P[i];
+          }
+        }
+        uint32_t mpv = vmax4(P[0]), mqv = kFull ? vmax4(Q[0]) : 0u;
+#pragma unroll
+        for (int i = 1; i < kPV; ++i) {
+          mpv = bmax2(mpv, vmax4(P[i]));
+          if (kFull) mqv = bmax2(mqv, vmax4(Q[i]));
+        }
+        const float fmp = pair_max(mpv);
+        if (fmp > acc.thr_p) acc.rebase_p(fmp);
+        if (kFull) {
+          const float fmq = pair_max(mqv);
+          if (fmq > acc.thr_q) acc.rebase_q(fmq);
+        }
+#pragma unroll
+        for (int i = 0; i < kPV; ++i) acc.step(P[i], Q[i]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tail->empty[stage]);
+        if (++stage == kNS) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+      using A = Acc<kFull, kFull>;
+      RowPartial r{acc.mp, A::total(acc.s), A::total(acc.w), kFull ? acc.mq : float(kMinitial),
+                   kFull ? A::total(acc.sq) : 0.f, kFull ? A::total(acc.u) : 0.f};
+      r = warp_combine<kFull>(r);
+      if (tid == 0) tail->xy[b] = make_float2(xy, yok ? 1.f : 0.f);
+      if (lane == 0) {
+        tail->red[b][warp] = r;
+        mbar_arrive(&tail->pfull[b]);  // release: the partial (and xy) before it
+      }
+      // ---- pass 2: the gradient (second read of the row, from L2) ----
+      mbar_sleep_wait(&tail->cfull[b], uint32_t(j >> 1) & 1u);
+      const float* cf = tail->coef[b];
+      const float2 nl = f2(-cf[3], -cf[3]), c1 = f2(cf[8], cf[8]), c0 = f2(cf[9], cf[9]),
+                   nf = f2(cf[10], cf[10]);
+      for (int t = 0; t < ntiles; ++t) {
+        const int e0 = t * kPT;
+        const uint16_t* sp = ring + size_t(stage) * kPS * kPT;
+        const uint16_t* sq = sp + kPT;
+        mbar_sleep_wait(&tail->full[stage], phase);
+        if (t < nfull) {
+          uint4 P[kPV], Q[kPV];
+#pragma unroll
+          for (int i = 0; i < kPV; ++i) {
+            P[i] = floor_policy(lds128(sp + (tid + i * kFC) * 8));
+            Q[i] = kFull ? floor_policy(lds128(sq + (tid + i * kFC) * 8)) : P[i];
+          }
+#pragma unroll
+          for (int i = 0; i < kPV; ++i)
+            gm::stg_cs_128(gs + e0 + (tid + i * kFC) * 8,
+                           grad_vec_folded<kFull>(P[i], Q[i], nl, c1, c0, nf));
+        } else {
+          for (int v = tid; v < last_nvec; v += kFC) {
+            const uint4 P = floor_policy(lds128(sp + v * 8));
+            const uint4 Q = kFull ? floor_policy(lds128(sq + v * 8)) : P;
+            gm::stg_cs_128(gs + e0 + v * 8, grad_vec_folded<kFull>(P, Q, nl, c1, c0, nf));
+          }
+        }
+        if (t == ty && tid == (yin >> 3) % kFC) {  // the target element carries + g
+          const gm::RowCoef c{cf[0], cf[1], cf[2], cf[3], cf[4], cf[5], cf[6]};
+          const float x = __uint_as_float(uint32_t(sp[yin]) << 16);
+          const float z = kFull ? __uint_as_float(uint32_t(sq[yin]) << 16) : 0.f;
+          gs[y] = uint16_t(pack_bf16x2(target_grad<kFull>(x, z, c), 0.f) & 0xffffu);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tail->empty[stage]);
+        if (++stage == kNS) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+      ++j;
+    }
+  }
+}
+#endif  // !YATT_FUSED_ONLY_TU
+
 }  // namespace
+
+#if !defined(YATT_FUSED_ONLY_TU)
+int policy_loss_grad_ring_large(const FusedParams& p, cudaStream_t st);
+
+// V > 60,000: the issue-lean kernel (YATT_FUSED_PIPE=0 selects the kernel
+// above, measurement only).
+int policy_loss_grad_pipe(const FusedParams& p, cudaStream_t st) {
+  const char* env = std::getenv("YATT_FUSED_PIPE");
+  if (env != nullptr && std::atoi(env) == 0) return policy_loss_grad_ring_large(p, st);
+  const bool full = p.kl_mode == YATT_KL_FULL;
+  const void* k = full ? reinterpret_cast<const void*>(policy_loss_grad_pipe_kernel<true>)
+                       : reinterpret_cast<const void*>(policy_loss_grad_pipe_kernel<false>);
+  const int rc = ensure_dynamic_smem(k, int(kPipeSmem));
+  if (rc) return rc;
+  const int grid = int(min64(p.rows, num_sms()));
+  if (full)
+    policy_loss_grad_pipe_kernel<true><<<grid, kPThreads, kPipeSmem, st>>>(p);
+  else
+    policy_loss_grad_pipe_kernel<false><<<grid, kPThreads, kPipeSmem, st>>>(p);
+  return check_launch("policy_loss_grad_pipe_kernel");
+}
+#endif
 
 #if defined(YATT_FUSED_SMALL_TU)
 #define YATT_FUSED_RING policy_loss_grad_ring_small
@@ -1113,7 +1496,7 @@ int policy_loss_grad_launch(const uint16_t* pol, const uint16_t* ref, const int3
   if (p.V <= a1_small_vmax())
     return p.kl_mode == YATT_KL_FULL ? policy_loss_grad_ring_mid(p, st)
                                      : policy_loss_grad_ring_small(p, st);
-  return policy_loss_grad_ring_large(p, st);
+  return policy_loss_grad_pipe(p, st);
 }
 
 int token_stats_ring_small(const A1Params& p, cudaStream_t st);  // token_stats_small.cu

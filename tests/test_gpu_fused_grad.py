@@ -7,6 +7,8 @@ KL estimator against the stored ref_logp, the gradient with the same bf16 +
 conditioning bound as test_gpu_backward.py (oracle fed the exact fp64 logp),
 and against the two-kernel device path (yatt_policy_grad_coef +
 yatt_logits_backward).  Masked rows are exactly zero; rows sum to ~0."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -221,3 +223,14 @@ def test_fused_extreme_rows(cuda, kl_mode):
     gf = grad.float()
     assert bool(torch.isfinite(gf).all())
     assert float((gf.sum(1).abs() / (gf.abs().amax(1) * vocab ** 0.5 + 1e-30)).max()) < 1e-2
+
+
+@pytest.mark.parametrize("shape", ["1", "0"])
+@pytest.mark.parametrize("kl_mode", ["k3", "full"])
+def test_fused_pipelined_many_rows_per_cta(cuda, kl_mode, shape, monkeypatch):
+    """Large vocabulary with several rows per CTA, so the double-buffered
+    partials / coefficients of the epilogue-warp kernel cycle (and the
+    kernel it replaced, YATT_FUSED_PIPE=0) against the fp64 oracle, masked
+    rows included."""
+    monkeypatch.setenv("YATT_FUSED_PIPE", shape)
+    _case(cuda, 3 * 148 + 13, 65536, kl_mode, masked=True, ent_coef=0.001)
