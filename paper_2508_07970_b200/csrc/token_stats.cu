@@ -1104,7 +1104,17 @@ __device__ __forceinline__ uint4 grad_vec_folded(const uint4& P, const uint4& Q,
   return make_uint4(out[0], out[1], out[2], out[3]);
 }
 
-template <bool kFull>
+// Pass-2 tile order (kOrder): 0 forward, 1 reverse (the default).  In
+// reverse the last tiles of pass 1 — the most recently read — are re-read
+// first, so the tiles L2 still holds are taken before they age out: DRAM
+// reads of the full-KL kernel 1.32x -> 1.23x the algorithmic bytes.  (Taking
+// the ring-resident tail of pass 1 straight from shared memory cut DRAM
+// reads further, to 1.13x, but ran slower — profiles/r2_fused_pipe_v6.jsonl.)
+__device__ __forceinline__ int pass2_tile(int k, int ntiles, int order) {
+  return order == 1 ? ntiles - 1 - k : k;
+}
+
+template <bool kFull, int kOrder>
 __global__ void __launch_bounds__(kPThreads, 1) policy_loss_grad_pipe_kernel(const FusedParams p) {
   constexpr int kPS = kFull ? 2 : 1;               // tensors per stage
   constexpr int kPT = kFull ? kTile : 2 * kTile;   // logits per tensor per stage
@@ -1143,10 +1153,12 @@ __global__ void __launch_bounds__(kPThreads, 1) policy_loss_grad_pipe_kernel(con
         const uint16_t* gp = p.pol + row * int64_t(V);
         const uint16_t* gq = kFull ? p.ref + row * int64_t(V) : nullptr;
         for (int pass = 0; pass < 2; ++pass) {
-          const uint64_t pol = pass == 0 ? keep : drop;
-          for (int t = 0; t < ntiles; ++t) {
+          for (int k = 0; k < ntiles; ++k) {
+            const int t = pass == 0 ? k : pass2_tile(k, ntiles, kOrder);
             const int e0 = t * kPT;
             const uint32_t n = uint32_t(min(kPT, V - e0));
+            // pass 1 keeps the row in L2 for pass 2 (evict-normal), pass 2 drops it
+            const uint64_t pol = pass == 0 ? keep : drop;
             mbar_sleep_wait(&tail->empty[stage], phase ^ 1u);
             mbar_arrive_expect_tx(&tail->full[stage], 2u * n * kPS);
             uint16_t* dst = ring + size_t(stage) * kPS * kPT;
@@ -1342,7 +1354,8 @@ __global__ void __launch_bounds__(kPThreads, 1) policy_loss_grad_pipe_kernel(con
       const float* cf = tail->coef[b];
       const float2 nl = f2(-cf[3], -cf[3]), c1 = f2(cf[8], cf[8]), c0 = f2(cf[9], cf[9]),
                    nf = f2(cf[10], cf[10]);
-      for (int t = 0; t < ntiles; ++t) {
+      for (int k = 0; k < ntiles; ++k) {
+        const int t = pass2_tile(k, ntiles, kOrder);
         const int e0 = t * kPT;
         const uint16_t* sp = ring + size_t(stage) * kPS * kPT;
         const uint16_t* sq = sp + kPT;
@@ -1389,21 +1402,23 @@ __global__ void __launch_bounds__(kPThreads, 1) policy_loss_grad_pipe_kernel(con
 #if !defined(YATT_FUSED_ONLY_TU)
 int policy_loss_grad_ring_large(const FusedParams& p, cudaStream_t st);
 
-// V > 60,000: the issue-lean kernel (YATT_FUSED_PIPE=0 selects the kernel
-// above, measurement only).
+// V > 60,000: the issue-lean kernel.
 int policy_loss_grad_pipe(const FusedParams& p, cudaStream_t st) {
-  const char* env = std::getenv("YATT_FUSED_PIPE");
-  if (env != nullptr && std::atoi(env) == 0) return policy_loss_grad_ring_large(p, st);
   const bool full = p.kl_mode == YATT_KL_FULL;
-  const void* k = full ? reinterpret_cast<const void*>(policy_loss_grad_pipe_kernel<true>)
-                       : reinterpret_cast<const void*>(policy_loss_grad_pipe_kernel<false>);
+  const char* ord_env = std::getenv("YATT_FUSED_ORDER");  // measurement only
+  const int order = ord_env ? std::atoi(ord_env) : 1;
+  YATT_REQUIRE(order == 0 || order == 1, YATT_ERR_CONFIG, "YATT_FUSED_ORDER must be 0 or 1");
+  const void* const kernels[2][2] = {
+      {reinterpret_cast<const void*>(policy_loss_grad_pipe_kernel<false, 0>),
+       reinterpret_cast<const void*>(policy_loss_grad_pipe_kernel<false, 1>)},
+      {reinterpret_cast<const void*>(policy_loss_grad_pipe_kernel<true, 0>),
+       reinterpret_cast<const void*>(policy_loss_grad_pipe_kernel<true, 1>)}};
+  const void* k = kernels[full ? 1 : 0][order];
   const int rc = ensure_dynamic_smem(k, int(kPipeSmem));
   if (rc) return rc;
   const int grid = int(min64(p.rows, num_sms()));
-  if (full)
-    policy_loss_grad_pipe_kernel<true><<<grid, kPThreads, kPipeSmem, st>>>(p);
-  else
-    policy_loss_grad_pipe_kernel<false><<<grid, kPThreads, kPipeSmem, st>>>(p);
+  void* args[] = {const_cast<FusedParams*>(&p)};
+  YATT_TRY_CUDA(cudaLaunchKernel(k, dim3(unsigned(grid)), dim3(kPThreads), args, kPipeSmem, st));
   return check_launch("policy_loss_grad_pipe_kernel");
 }
 #endif
@@ -1493,10 +1508,15 @@ int policy_loss_grad_launch(const uint16_t* pol, const uint16_t* ref, const int3
   // shapes (measured, r1_fused_grad_ncu_v1.md): V <= 60,000 — 3 CTAs/SM of 8
   // warps (the full KL, which would spill there, 2 CTAs/SM); larger — one
   // CTA/SM of 16 warps, half the rows live between the passes (L2 reuse)
+  // YATT_FUSED_PIPE (measurement only): 1 = the epilogue-warp kernel at any
+  // vocabulary, 0 = the kernels it replaced
+  const char* env = std::getenv("YATT_FUSED_PIPE");
+  const int pipe = env ? std::atoi(env) : -1;
+  if (pipe == 1) return policy_loss_grad_pipe(p, st);
   if (p.V <= a1_small_vmax())
     return p.kl_mode == YATT_KL_FULL ? policy_loss_grad_ring_mid(p, st)
                                      : policy_loss_grad_ring_small(p, st);
-  return policy_loss_grad_pipe(p, st);
+  return pipe == 0 ? policy_loss_grad_ring_large(p, st) : policy_loss_grad_pipe(p, st);
 }
 
 int token_stats_ring_small(const A1Params& p, cudaStream_t st);  // token_stats_small.cu

@@ -19,7 +19,7 @@ from paper_2508_07970_b200 import ops  # noqa: E402
 
 rows = int(os.environ.get("ROWS", 32768))
 V = int(os.environ.get("VOCAB", 152064))
-shapes = os.environ.get("SHAPES", "0,1").split(",")
+shapes = os.environ.get("SHAPES", "0,10,11").split(",")
 seed = 20250814
 pol, ref, tgt = ops.synth_logits(seed, 0, rows, V)
 lp, rl, en, kl = ops.token_stats(pol, ref, tgt, None, "k3")
@@ -31,7 +31,8 @@ grad = torch.empty_like(pol)
 for mode in ("k3", "full"):
     base = None
     for sh in shapes:
-        os.environ["YATT_FUSED_PIPE"] = sh
+        os.environ["YATT_FUSED_PIPE"] = sh[0]
+        os.environ["YATT_FUSED_ORDER"] = sh[1:] or "1"  # pass-2 order: 0 forward, 1 reverse
 
         def run(m=None):
             return ops.policy_loss_grad(pol, tgt, old, adv, rl if mode != "full" else None, m, cfg,
