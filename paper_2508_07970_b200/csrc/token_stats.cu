@@ -428,14 +428,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) token_stats_kernel(const
   int stage = 0;
   uint32_t phase = 0;
   int iter = 0;
+  // the next row's target prefetched a row ahead (the full KL, 8 more
+  // accumulators live, loads it at the row start instead: no spills)
   int64_t next_row = blockIdx.x;
-  int32_t y_next = next_row < p.rows ? __ldg(p.tgt + next_row) : 0;
+  int32_t y_next = !kFull && next_row < p.rows ? __ldg(p.tgt + next_row) : 0;
   Acc<kFull> acc;
 
   for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
-    const int32_t y = (row == next_row) ? y_next : __ldg(p.tgt + row);
-    next_row = row + gridDim.x;
-    if (next_row < p.rows) y_next = __ldg(p.tgt + next_row);
+    const int32_t y = (!kFull && row == next_row) ? y_next : __ldg(p.tgt + row);
+    if (!kFull) {
+      next_row = row + gridDim.x;
+      if (next_row < p.rows) y_next = __ldg(p.tgt + next_row);
+    }
     if (p.mask != nullptr && p.mask[row] == 0) {
       if (tid == 0) {
         p.logp[row] = 0.f;
@@ -447,15 +451,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) token_stats_kernel(const
     }
     const int par = iter & 1;
     const int h = kEdges ? int((row * V) & 7) : 0;  // staged row starts h elements early
-    const int64_t S = kEdges ? ((h + V + 7) & ~int64_t(7)) : V;
-    const int ntiles_r = int((S + kTile - 1) / kTile);
+    const int S = kEdges ? ((h + int(V) + 7) & ~7) : int(V);  // 32-bit: V < 2^31 - 15
+    const int ntiles_r = (S + kTile - 1) / kTile;
     const int ty = (y + h) / kTile;    // tile holding the target logit
     const int yin = (y + h) - ty * kTile;
     acc.reset();
 
     for (int t = 0; t < ntiles_r; ++t) {
-      const int64_t e0 = int64_t(t) * kTile;
-      const int nvec = int(min64(kTile, S - e0) >> 3);
+      const int e0 = t * kTile;
+      const int nvec = min(kTile, S - e0) >> 3;
       const uint16_t* sp = ring + size_t(stage) * 2 * kTile;
       const uint16_t* sq = sp + kTile;
       mbar_wait(&tail->full[stage], phase);
@@ -475,9 +479,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) token_stats_kernel(const
           P[i] = in ? lds128(sp + v * 8) : make_uint4(kNegInf2, kNegInf2, kNegInf2, kNegInf2);
           Q[i] = in ? lds128(sq + v * 8) : make_uint4(kNegInf2, kNegInf2, kNegInf2, kNegInf2);
           if (kEdges) {  // staged elements outside the row read as -inf
-            const int64_t j0 = e0 + int64_t(v) * 8 - h;  // row index of element 0
-            if (in && (j0 < 0 || j0 + 8 > V)) {
-              const int lo = int(max64(0, -j0)), hi = int(min64(8, V - j0));
+            const int j0 = e0 + v * 8 - h;  // row index of element 0
+            if (in && (j0 < 0 || j0 + 8 > int(V))) {
+              const int lo = max(0, -j0), hi = min(8, int(V) - j0);
               P[i] = keep_range(P[i], lo, hi);
               Q[i] = keep_range(Q[i], lo, hi);
             }
