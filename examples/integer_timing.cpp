@@ -78,9 +78,11 @@ int main() {
       for (const auto& r : reps) units += r.accepted_train_units;
     last = b;
   });
-  // Where a call's time goes (C ABI underneath sim::run_rollout_rounds):
-  // packing into the pinned stage, the device call (H2D copy + persistent
-  // kernel + synchronize, results in mapped host memory), unpacking.
+  // Where a call's time goes (C ABI underneath sim::run_rollout_rounds),
+  // single-threaded here (the API splits the pack / copy-back loops over 2
+  // host threads): packing into the pinned stage, the device call (the
+  // persistent kernel reads the stage in place, results in mapped host
+  // memory, one synchronize), unpacking.
   double pack_ms = 0, call_ms = 0, unpack_ms = 0;
   {
     yatt_rounds_t h = nullptr;

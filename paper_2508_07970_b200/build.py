@@ -28,7 +28,7 @@ NVCC_FLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
     "--expt-relaxed-constexpr", "-Xptxas", "-v", f"-I{ROOT / 'include'}",
 ]
-CXX_FLAGS = ["-O2", "-fPIC", "-std=c++20", f"-I{ROOT / 'include'}",
+CXX_FLAGS = ["-O2", "-fPIC", "-fopenmp", "-std=c++20", f"-I{ROOT / 'include'}",
              "-I/usr/local/cuda/include"]
 
 
@@ -82,7 +82,7 @@ def build(verbose: bool = False) -> Path:
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc(), "-shared", "-o", str(tmp)] + ARCH + [str(o) for o in objs] + [
         "-L/usr/lib/x86_64-linux-gnu", "-lnccl", "-lcudart_static", "-lrt", "-ldl", "-lpthread",
-        "-Xlinker", "--no-undefined"]
+        "-lgomp", "-Xlinker", "--no-undefined"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed: {' '.join(cmd)}\n{res.stdout}{res.stderr}")
@@ -103,7 +103,7 @@ def build_variant(name: str, defines: dict) -> Path:
     out = PKG / "_variants" / f"libyatt_b200_{name}.so"
     out.parent.mkdir(exist_ok=True)
     cmd = [nvcc(), "-shared", "-o", str(out)] + ARCH + [str(o) for o in objs] + [
-        "-L/usr/lib/x86_64-linux-gnu", "-lnccl", "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+        "-L/usr/lib/x86_64-linux-gnu", "-lnccl", "-lcudart_static", "-lrt", "-ldl", "-lpthread", "-lgomp"]
     subprocess.run(cmd, check=True, capture_output=True)
     return out
 
