@@ -8,8 +8,8 @@
 //   3. repack accepted lengths into balanced buckets (balancer::sort_and_bucket)
 //   4. experience making on the device: logprob/entropy/KL, GRPO advantages,
 //      clipped-surrogate + KL loss (experience.hpp), loss finalised on host
-//   5. the backward into the logits, the node peer group (world = 1 here) and
-//      the survivors' payload gather
+//   5. the backward into the logits, the node peer group (world = 1 here),
+//      the survivors' payload gather and groups straddling emulated ranks
 // Prints a short report and "rank ok"; exits non-zero on any mismatch.
 #include <cuda_runtime.h>
 
@@ -236,6 +236,94 @@ int main() {
     std::printf("dynamic sampling: %lld of %d samples kept, %lld tokens gathered\n",
                 (long long)counts[0], n, (long long)counts[1]);
     if (counts[1] != counts[0] * T) return 1;
+  }
+
+  // 5d. groups straddling ranks (sample-level shard_dataset at P = 3): each
+  // emulated rank's boundary records, stacked in rank order (what the
+  // all-gather delivers), merged on the device -> advantages and the filter's
+  // global layout equal the single-rank ones; the peer group's one-call form
+  // (world 1) equals the plain op
+  {
+    const int n = prompts * group, P = 3;
+    std::vector<float> one(static_cast<size_t>(n));
+    ck(cudaMemcpy(one.data(), sadv, size_t(n) * 4, cudaMemcpyDeviceToHost), "D2H adv");
+    auto* lens = dalloc<std::int64_t>(size_t(n));
+    std::vector<std::int64_t> hl(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) hl[size_t(i)] = 100 + i % 7;
+    ck(cudaMemcpy(lens, hl.data(), hl.size() * 8, cudaMemcpyHostToDevice), "H2D lens");
+    auto* grecs = dalloc<double>(size_t(P) * 8);
+    auto* frecs = dalloc<std::int64_t>(size_t(P) * 6);
+    std::vector<workload::ShardRange> sh;
+    std::vector<double*> moms;
+    for (int r = 0; r < P; ++r) {
+      sh.push_back(workload::shard_dataset(std::uint64_t(n), P, r));
+      const std::int64_t b = std::int64_t(sh.back().begin), m = std::int64_t(sh.back().size());
+      const std::int64_t ng = experience::grpo_num_local_groups(m, std::uint64_t(b), group);
+      moms.push_back(dalloc<double>(size_t(ng) * 3));
+      experience::grpo_group_moments(rewards + b, m, std::uint64_t(b), group, moms.back());
+      experience::grpo_boundary_record(moms.back(), m, std::uint64_t(b), group, grecs + 8 * r);
+      experience::dynamic_sampling_boundary_record(rewards + b, m, std::uint64_t(b), group,
+                                                   frecs + 6 * r);
+    }
+    bool straddles = false;
+    std::int64_t kept[3] = {0, 0, 0};
+    std::vector<float> got(static_cast<size_t>(n));
+    for (int r = 0; r < P; ++r) {
+      const std::int64_t b = std::int64_t(sh[size_t(r)].begin);
+      const std::int64_t m = std::int64_t(sh[size_t(r)].size());
+      straddles = straddles || b % group != 0;
+      experience::grpo_merge_boundaries(moms[size_t(r)], m, std::uint64_t(b), group, grecs, P);
+      auto* adv_r = dalloc<float>(size_t(m));
+      experience::grpo_advantages(rewards + b, m, std::uint64_t(b), experience::GrpoConfig{group},
+                                  adv_r, moms[size_t(r)]);
+      ck(cudaMemcpy(got.data() + b, adv_r, size_t(m) * 4, cudaMemcpyDeviceToHost), "D2H adv_r");
+      const std::int64_t ng = experience::grpo_num_local_groups(m, std::uint64_t(b), group);
+      experience::CompactionBuffers pl{dalloc<std::uint8_t>(size_t(ng)),
+                                       dalloc<std::int32_t>(size_t(m)),
+                                       dalloc<std::int64_t>(size_t(m) + 1),
+                                       dalloc<std::int64_t>(3)};
+      const size_t wsb = experience::dynamic_sampling_workspace_bytes(m);
+      void* w = dalloc<std::uint8_t>(wsb);
+      experience::dynamic_sampling_filter_sharded(rewards + b, lens + b, m, std::uint64_t(b),
+                                                  group, frecs, P, pl, w, wsb);
+      std::int64_t c[3];
+      ck(cudaMemcpy(c, pl.counts, sizeof(c), cudaMemcpyDeviceToHost), "D2H counts_r");
+      for (int k = 0; k < 3; ++k) kept[k] += c[k];
+      cudaFree(adv_r);
+      cudaFree(w);
+    }
+    double worst = 0;
+    for (int i = 0; i < n; ++i)
+      worst = std::fmax(worst, std::fabs(double(got[size_t(i)]) - double(one[size_t(i)])));
+    experience::CompactionBuffers all{dalloc<std::uint8_t>(size_t(n) / group),
+                                      dalloc<std::int32_t>(size_t(n)),
+                                      dalloc<std::int64_t>(size_t(n) + 1),
+                                      dalloc<std::int64_t>(3)};
+    const size_t wsb = experience::dynamic_sampling_workspace_bytes(n);
+    void* w = dalloc<std::uint8_t>(wsb);
+    experience::dynamic_sampling_filter(rewards, lens, n, group, all, w, wsb);
+    std::int64_t c1[3];
+    ck(cudaMemcpy(c1, all.counts, sizeof(c1), cudaMemcpyDeviceToHost), "D2H counts_1");
+    std::printf("straddling groups (P = %d): max |adv - single rank| %.1e, kept %lld/%lld/%lld "
+                "(single rank %lld/%lld/%lld)\n", P, worst, (long long)kept[0],
+                (long long)kept[1], (long long)kept[2], (long long)c1[0], (long long)c1[1],
+                (long long)c1[2]);
+    if (!straddles || worst > 1e-6 || std::memcmp(kept, c1, sizeof(c1)) != 0) return 1;
+    experience::PeerGroup peer(1, 0);
+    peer.connect(peer.handle());
+    const size_t pwsb = peer.straddle_workspace_bytes(n, 0, group);
+    void* pws = dalloc<std::uint8_t>(pwsb);
+    auto* padv = dalloc<float>(size_t(n));
+    peer.grpo_advantages(rewards, n, 0, experience::GrpoConfig{group}, padv, pws, pwsb);
+    ck(cudaMemcpy(got.data(), padv, size_t(n) * 4, cudaMemcpyDeviceToHost), "D2H peer adv");
+    if (std::memcmp(got.data(), one.data(), size_t(n) * 4) != 0) return 1;
+    peer.dynamic_sampling_filter(rewards, lens, n, 0, group, all, pws, pwsb);
+    ck(cudaMemcpy(c1 + 0, all.counts, sizeof(c1), cudaMemcpyDeviceToHost), "D2H peer counts");
+    if (std::memcmp(kept, c1, sizeof(c1)) != 0) return 1;
+    for (double* mm : moms) cudaFree(mm);
+    cudaFree(w);
+    cudaFree(pws);
+    cudaFree(padv);
   }
 
   // errors keep the reference's types

@@ -88,9 +88,30 @@ void policy_loss(const float* logp, const float* old_logp, const float* advantag
                  std::size_t workspace_bytes, void* stream = nullptr);
 double finalize_loss(const LossSums& global_sums, const PolicyLossConfig& config);
 
+// Groups straddling ranks (the reference's SAMPLE-level shard_dataset,
+// workload.cpp:183-198, with the group unit sample_id / group_size,
+// workload.cpp:158-160): the first / last local group of a shard may hold only
+// part of a group.  Per-rank moments of the local groups (n, mean, M2; fp64,
+// one row per local group); the 8-double boundary record of the first / last
+// local group; the merge of every rank's records (gathered in rank order,
+// world x 8 doubles) into rows 0 and last — identical bits on every rank.
+// Pass the merged moments to grpo_advantages.  PeerGroup::grpo_advantages
+// does all of it in one call.
+std::int64_t grpo_num_local_groups(std::int64_t n_samples, std::uint64_t first_sample_id,
+                                   int group_size);
+void grpo_group_moments(const float* rewards, std::int64_t n_samples,
+                        std::uint64_t first_sample_id, int group_size, double* moments,
+                        void* stream = nullptr);
+void grpo_boundary_record(const double* moments, std::int64_t n_samples,
+                          std::uint64_t first_sample_id, int group_size, double* record,
+                          void* stream = nullptr);
+void grpo_merge_boundaries(double* moments, std::int64_t n_samples,
+                           std::uint64_t first_sample_id, int group_size,
+                           const double* all_records, int world, void* stream = nullptr);
+
 // ---- A5 + A6 --------------------------------------------------------------
 struct CompactionBuffers {
-  std::uint8_t* keep_groups = nullptr;  // [n_samples / group_size]
+  std::uint8_t* keep_groups = nullptr;  // [grpo_num_local_groups(n, first_sample_id, G)]
   std::int32_t* index_map = nullptr;    // [n_samples]
   std::int64_t* new_cu = nullptr;       // [n_samples + 1]
   std::int64_t* counts = nullptr;       // [3] kept samples, tokens, groups
@@ -101,6 +122,20 @@ void dynamic_sampling_filter(const float* rewards, const std::int64_t* seq_lens,
                              std::int64_t n_samples, int group_size, const CompactionBuffers& out,
                              void* workspace, std::size_t workspace_bytes,
                              void* stream = nullptr);
+// A shard of a sample-level split (global ids from first_sample_id): every
+// rank writes its 6-word boundary record ({group, first reward bits,
+// any-differs} of its first and last local group); with the records of all
+// ranks gathered in rank order (world x 6 int64), every rank holding a piece
+// of a straddling group takes the same exact keep decision.  counts[2]
+// counts the groups whose first sample is local (each group once globally).
+void dynamic_sampling_boundary_record(const float* rewards, std::int64_t n_samples,
+                                      std::uint64_t first_sample_id, int group_size,
+                                      std::int64_t* record, void* stream = nullptr);
+void dynamic_sampling_filter_sharded(const float* rewards, const std::int64_t* seq_lens,
+                                     std::int64_t n_samples, std::uint64_t first_sample_id,
+                                     int group_size, const std::int64_t* all_records, int world,
+                                     const CompactionBuffers& out, void* workspace,
+                                     std::size_t workspace_bytes, void* stream = nullptr);
 
 // ---- backward into the policy logits -------------------
 // dL/d(policy logits) of the A4 loss as bf16 [rows, vocab].  `stats` are A1's
@@ -181,11 +216,29 @@ class PeerGroup {
                    std::int64_t n_tokens, const std::int64_t* cu_seqlens, std::int64_t n_seqs,
                    const PolicyLossConfig& config, LossSums* device_sums, void* workspace,
                    std::size_t workspace_bytes, void* stream = nullptr);
+  // Group-level ops of a shard whose first / last groups may straddle ranks
+  // (sample-level sharding): boundary record -> peer all-gather -> device
+  // merge -> the op, stream-ordered, one call (collective).  Workspace:
+  // straddle_workspace_bytes.  Advantages equal a single rank's to fp64
+  // rounding of the merged moments; the filter's layout is bit-exact.
+  std::size_t straddle_workspace_bytes(std::int64_t n_samples, std::uint64_t first_sample_id,
+                                       int group_size) const;
+  void grpo_advantages(const float* rewards, std::int64_t n_samples,
+                       std::uint64_t first_sample_id, const GrpoConfig& config,
+                       float* advantages, void* workspace, std::size_t workspace_bytes,
+                       void* stream = nullptr);
+  void dynamic_sampling_filter(const float* rewards, const std::int64_t* seq_lens,
+                               std::int64_t n_samples, std::uint64_t first_sample_id,
+                               int group_size, const CompactionBuffers& out, void* workspace,
+                               std::size_t workspace_bytes, void* stream = nullptr);
+  int world() const { return world_; }
+  int rank() const { return rank_; }
   int status() const;  // 1 after a call timed out waiting for a rank
 
  private:
   void* h_ = nullptr;
   std::vector<std::uint8_t> handle_;
+  int world_ = 0, rank_ = 0;
 };
 
 }  // namespace yatt::experience

@@ -654,7 +654,8 @@ void gather_payload(const std::vector<PayloadArray>& arrays, const std::int64_t*
                                                 dst_offset, stream));
 }
 
-PeerGroup::PeerGroup(int world, int rank) : handle_(YATT_PEER_HANDLE_BYTES) {
+PeerGroup::PeerGroup(int world, int rank)
+    : handle_(YATT_PEER_HANDLE_BYTES), world_(world), rank_(rank) {
   yatt_peer_t p = nullptr;
   detail::throw_status(yatt_peer_create(world, rank, &p, handle_.data()));
   h_ = p;
@@ -693,6 +694,30 @@ void PeerGroup::policy_loss(const float* logp, const float* old_logp, const floa
       reinterpret_cast<yatt_loss_sums*>(sums), ws, ws_bytes, stream));
 }
 
+std::size_t PeerGroup::straddle_workspace_bytes(std::int64_t n, std::uint64_t first_id,
+                                                int G) const {
+  return yatt_straddle_workspace_bytes(n, first_id, G, world_);
+}
+
+void PeerGroup::grpo_advantages(const float* rewards, std::int64_t n, std::uint64_t first_id,
+                                const GrpoConfig& c, float* adv, void* ws, std::size_t ws_bytes,
+                                void* stream) {
+  c.validate();
+  detail::throw_status(yatt_peer_grpo_advantages(static_cast<yatt_peer_t>(h_), rewards, n,
+                                                 first_id, c.group_size, c.eps,
+                                                 c.norm_by_std ? 1 : 0, adv, ws, ws_bytes,
+                                                 stream));
+}
+
+void PeerGroup::dynamic_sampling_filter(const float* rewards, const std::int64_t* lens,
+                                        std::int64_t n, std::uint64_t first_id, int G,
+                                        const CompactionBuffers& o, void* ws,
+                                        std::size_t ws_bytes, void* stream) {
+  detail::throw_status(yatt_peer_filter_compact(static_cast<yatt_peer_t>(h_), rewards, lens, n,
+                                                first_id, G, o.keep_groups, o.index_map,
+                                                o.new_cu, o.counts, ws, ws_bytes, stream));
+}
+
 int PeerGroup::status() const {
   std::int32_t s = 0;
   detail::throw_status(yatt_peer_status(static_cast<yatt_peer_t>(h_), &s));
@@ -708,6 +733,43 @@ void dynamic_sampling_filter(const float* rewards, const std::int64_t* lens, std
                              void* stream) {
   detail::throw_status(yatt_filter_compact(rewards, lens, n, G, o.keep_groups, o.index_map,
                                            o.new_cu, o.counts, ws, ws_bytes, stream));
+}
+
+void dynamic_sampling_boundary_record(const float* rewards, std::int64_t n,
+                                      std::uint64_t first_id, int G, std::int64_t* record,
+                                      void* stream) {
+  detail::throw_status(yatt_filter_boundary_record(rewards, n, first_id, G, record, stream));
+}
+
+void dynamic_sampling_filter_sharded(const float* rewards, const std::int64_t* lens,
+                                     std::int64_t n, std::uint64_t first_id, int G,
+                                     const std::int64_t* all_records, int world,
+                                     const CompactionBuffers& o, void* ws, std::size_t ws_bytes,
+                                     void* stream) {
+  detail::throw_status(yatt_filter_compact_sharded(rewards, lens, n, first_id, G, all_records,
+                                                   world, o.keep_groups, o.index_map, o.new_cu,
+                                                   o.counts, ws, ws_bytes, stream));
+}
+
+std::int64_t grpo_num_local_groups(std::int64_t n, std::uint64_t first_id, int G) {
+  if (G <= 0) throw ConfigError("group_size must be positive");
+  return yatt_grpo_num_local_groups(n, first_id, G);
+}
+
+void grpo_group_moments(const float* rewards, std::int64_t n, std::uint64_t first_id, int G,
+                        double* moments, void* stream) {
+  detail::throw_status(yatt_grpo_group_moments(rewards, n, first_id, G, moments, stream));
+}
+
+void grpo_boundary_record(const double* moments, std::int64_t n, std::uint64_t first_id, int G,
+                          double* record, void* stream) {
+  detail::throw_status(yatt_grpo_boundary_record(moments, n, first_id, G, record, stream));
+}
+
+void grpo_merge_boundaries(double* moments, std::int64_t n, std::uint64_t first_id, int G,
+                           const double* all_records, int world, void* stream) {
+  detail::throw_status(
+      yatt_grpo_merge_boundaries(moments, n, first_id, G, all_records, world, stream));
 }
 
 }  // namespace experience
