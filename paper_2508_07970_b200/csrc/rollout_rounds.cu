@@ -30,7 +30,8 @@
 //   results (final state of the samples, reports, occupied microbatch slots)
 //   are stored straight into mapped pinned host memory; the host compacts the
 //   slots into the (round, shard, mb_index) list while it builds the reports.
-// A call is: one H2D DMA of the packed input, one launch, one synchronize.
+// A call is: one launch (phase 1 reads the packed input in place from the
+// mapped stage; YATT_ROUNDS_ZC=0 restores one H2D DMA first), one synchronize.
 //
 // Normal / LogNormal draws that are not certified equal to glibc
 // (keyed_draw.cuh) are logged; the host recomputes exactly those with glibc
