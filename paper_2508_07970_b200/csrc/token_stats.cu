@@ -1057,19 +1057,37 @@ __global__ void __launch_bounds__(kFThreads, kFMinB) policy_loss_grad_kernel(con
 // profiles/r2_fused_pipe_v1.jsonl).  HBM bytes per row: 2V (4V full KL) read
 // once, 2V written.
 // ----------------------------------------------------------------------
-constexpr int kPThreads = kFThreads + 32;  // consumers + producer + epilogue warp
-constexpr size_t kPRing = size_t(kFStages) * kTile * sizeof(uint16_t);  // 192 KB
+// Kernel shapes.  Large vocabularies: one CTA per SM, 16 consumer warps and
+// a 192 KB ring; small ones (V <= 60,000, short rows): 8 consumer warps, two
+// CTAs per SM and a 96 KB ring each, so one CTA streams while the other is at
+// its row end.
+template <int kCW_, int kMinB_, int kRingBytes_, int kTileK3_, int kTileFull_>
+struct PipeShape {
+  static constexpr int kCW = kCW_;                // consumer warps
+  static constexpr int kC = kCW * 32;             // consumer threads
+  static constexpr int kThreads = kC + 64;        // + producer + epilogue warp
+  static constexpr int kMinB = kMinB_;            // resident CTAs per SM
+  static constexpr int kRing = kRingBytes_;       // smem ring bytes
+  static constexpr int kTileK3 = kTileK3_;        // logits per stage (policy only)
+  static constexpr int kTileFull = kTileFull_;    // logits per tensor per stage (pol + ref)
+  static constexpr int kMaxStages = kRing / (2 * kTileK3) > kRing / (4 * kTileFull)
+                                        ? kRing / (2 * kTileK3) : kRing / (4 * kTileFull);
+};
+using PipeLarge = PipeShape<16, 1, 196608, 16384, 8192>;
+using PipeSmall = PipeShape<8, 2, 98304, 8192, 4096>;
 
+template <class S>
 struct __align__(16) PipeTail {
-  uint64_t full[kFStages];
-  uint64_t empty[kFStages];
-  uint64_t pfull[2];  // consumer warps' partials published (count kFCW)
+  uint64_t full[S::kMaxStages];
+  uint64_t empty[S::kMaxStages];
+  uint64_t pfull[2];  // consumer warps' partials published (count kCW)
   uint64_t cfull[2];  // row coefficients ready (count 1)
-  RowPartial red[2][kFCW];
+  RowPartial red[2][S::kCW];
   float2 xy[2];       // {target logit, valid}
   float coef[2][12];  // gm::RowCoef order, then the folded c1, c0, f
 };
-constexpr size_t kPipeSmem = kPRing + sizeof(PipeTail);
+template <class S>
+constexpr size_t pipe_smem() { return size_t(S::kRing) + sizeof(PipeTail<S>); }
 
 // try_wait with a suspend-time hint: the warp sleeps until the phase
 // completes (or the hint expires) instead of spinning on issue slots.
@@ -1118,17 +1136,19 @@ __device__ __forceinline__ int pass2_tile(int k, int ntiles, int order) {
   return order == 1 ? ntiles - 1 - k : k;
 }
 
-template <bool kFull, int kOrder>
-__global__ void __launch_bounds__(kPThreads, 1) policy_loss_grad_pipe_kernel(const FusedParams p) {
-  constexpr int kPS = kFull ? 2 : 1;               // tensors per stage
-  constexpr int kPT = kFull ? kTile : 2 * kTile;   // logits per tensor per stage
-  constexpr int kNS = kFStages * kTile / (kPS * kPT);  // stages
-  constexpr int kPVec = kPT / 8;                   // 16-byte vectors per tensor tile
-  constexpr int kPV = kPVec / kFC;                 // per consumer thread
-  static_assert(kPVec % kFC == 0, "pipe tile");
+template <bool kFull, int kOrder, class S>
+__global__ void __launch_bounds__(S::kThreads, S::kMinB) policy_loss_grad_pipe_kernel(
+    const FusedParams p) {
+  constexpr int kFCW = S::kCW, kFC = S::kC;
+  constexpr int kPS = kFull ? 2 : 1;                          // tensors per stage
+  constexpr int kPT = kFull ? S::kTileFull : S::kTileK3;      // logits per tensor per stage
+  constexpr int kNS = S::kRing / (2 * kPS * kPT);             // stages
+  constexpr int kPVec = kPT / 8;                              // 16-byte vectors per tensor tile
+  constexpr int kPV = kPVec / kFC;                            // per consumer thread
+  static_assert(kPVec % kFC == 0 && kNS >= 2 && kNS <= S::kMaxStages, "pipe shape");
   extern __shared__ __align__(128) uint8_t smem[];
   uint16_t* ring = reinterpret_cast<uint16_t*>(smem);
-  PipeTail* tail = reinterpret_cast<PipeTail*>(smem + kPRing);
+  PipeTail<S>* tail = reinterpret_cast<PipeTail<S>*>(smem + S::kRing);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int V = p.V;
   const int ntiles = (V + kPT - 1) / kPT, nfull = V / kPT;
@@ -1406,23 +1426,26 @@ __global__ void __launch_bounds__(kPThreads, 1) policy_loss_grad_pipe_kernel(con
 #if !defined(YATT_FUSED_ONLY_TU)
 int policy_loss_grad_ring_large(const FusedParams& p, cudaStream_t st);
 
-// V > 60,000: the issue-lean kernel.
+// The issue-lean kernel: PipeLarge for V > 60,000, PipeSmall below (the
+// caller dispatches; YATT_FUSED_ORDER = pass-2 tile order, measurement only).
+template <class S>
 int policy_loss_grad_pipe(const FusedParams& p, cudaStream_t st) {
   const bool full = p.kl_mode == YATT_KL_FULL;
   const char* ord_env = std::getenv("YATT_FUSED_ORDER");  // measurement only
   const int order = ord_env ? std::atoi(ord_env) : 1;
   YATT_REQUIRE(order == 0 || order == 1, YATT_ERR_CONFIG, "YATT_FUSED_ORDER must be 0 or 1");
   const void* const kernels[2][2] = {
-      {reinterpret_cast<const void*>(policy_loss_grad_pipe_kernel<false, 0>),
-       reinterpret_cast<const void*>(policy_loss_grad_pipe_kernel<false, 1>)},
-      {reinterpret_cast<const void*>(policy_loss_grad_pipe_kernel<true, 0>),
-       reinterpret_cast<const void*>(policy_loss_grad_pipe_kernel<true, 1>)}};
+      {reinterpret_cast<const void*>(policy_loss_grad_pipe_kernel<false, 0, S>),
+       reinterpret_cast<const void*>(policy_loss_grad_pipe_kernel<false, 1, S>)},
+      {reinterpret_cast<const void*>(policy_loss_grad_pipe_kernel<true, 0, S>),
+       reinterpret_cast<const void*>(policy_loss_grad_pipe_kernel<true, 1, S>)}};
   const void* k = kernels[full ? 1 : 0][order];
-  const int rc = ensure_dynamic_smem(k, int(kPipeSmem));
+  const int rc = ensure_dynamic_smem(k, int(pipe_smem<S>()));
   if (rc) return rc;
-  const int grid = int(min64(p.rows, num_sms()));
+  const int grid = int(min64(p.rows, int64_t(S::kMinB) * num_sms()));
   void* args[] = {const_cast<FusedParams*>(&p)};
-  YATT_TRY_CUDA(cudaLaunchKernel(k, dim3(unsigned(grid)), dim3(kPThreads), args, kPipeSmem, st));
+  YATT_TRY_CUDA(cudaLaunchKernel(k, dim3(unsigned(grid)), dim3(S::kThreads), args,
+                                 pipe_smem<S>(), st));
   return check_launch("policy_loss_grad_pipe_kernel");
 }
 #endif
@@ -1506,21 +1529,24 @@ int policy_loss_grad_launch(const uint16_t* pol, const uint16_t* ref, const int3
   // the last row; the aligned-V contract keeps the fused path simple
   YATT_REQUIRE(p.V % 8 == 0, YATT_ERR_CONFIG,
                "policy_loss_grad: vocab must be a multiple of 8 (got %d)", p.V);
-  // small vocabularies: 3 CTAs/SM (8,192 x 4 policy stages) hide the row-end
-  // barriers better; large: 2 CTAs/SM keep the rows live between the two
-  // passes within L2 (r1_fused_grad_ncu_v1.md)
-  // shapes (measured, r1_fused_grad_ncu_v1.md): V <= 60,000 — 3 CTAs/SM of 8
-  // warps (the full KL, which would spill there, 2 CTAs/SM); larger — one
-  // CTA/SM of 16 warps, half the rows live between the passes (L2 reuse)
-  // YATT_FUSED_PIPE (measurement only): 1 = the epilogue-warp kernel at any
-  // vocabulary, 0 = the kernels it replaced
+  // Shape by vocabulary (k3 / full-KL fraction of the HBM roofline,
+  // profiles/r2_fused_pipe_v8/v9.jsonl): the small pipe shape (2 CTAs/SM)
+  // vs the large one (1 CTA/SM) at V=65,536 0.933 vs 0.861 / 0.857 vs 0.806;
+  // 81,920 0.906 vs 0.911 / 0.844 vs 0.850; 98,304 0.862 vs 0.947 / 0.802 vs
+  // 0.870.  YATT_FUSED_PIPE (measurement only): 1 / 2 = the large / small
+  // pipe shape at any vocabulary, 0 = the round-1 kernels (3 CTAs/SM of 8
+  // warps for V <= 60,000, the full KL at 2; one 16-warp CTA/SM above).
+  constexpr int kFusedSmallVmax = 73728;
   const char* env = std::getenv("YATT_FUSED_PIPE");
   const int pipe = env ? std::atoi(env) : -1;
-  if (pipe == 1) return policy_loss_grad_pipe(p, st);
-  if (p.V <= a1_small_vmax())
+  if (pipe == 0) {
+    if (p.V > a1_small_vmax()) return policy_loss_grad_ring_large(p, st);
     return p.kl_mode == YATT_KL_FULL ? policy_loss_grad_ring_mid(p, st)
                                      : policy_loss_grad_ring_small(p, st);
-  return pipe == 0 ? policy_loss_grad_ring_large(p, st) : policy_loss_grad_pipe(p, st);
+  }
+  if (pipe == 2 || (pipe != 1 && p.V <= kFusedSmallVmax))
+    return policy_loss_grad_pipe<PipeSmall>(p, st);
+  return policy_loss_grad_pipe<PipeLarge>(p, st);
 }
 
 int token_stats_ring_small(const A1Params& p, cudaStream_t st);  // token_stats_small.cu
