@@ -171,6 +171,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// try_wait with a suspend-time hint: the warp sleeps until the phase
+// completes (or the hint expires) instead of spinning on issue slots (used
+// where the kernel is issue-bound: the fused loss + gradient kernel).
+__device__ __forceinline__ void mbar_sleep_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+        : "memory");
+  }
+}
+
 // L2 policy: streamed-once inputs should not displace reused lines.
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
   uint64_t pol;

@@ -317,6 +317,25 @@ __device__ __forceinline__ RowPartial warp_combine(RowPartial r) {
 #define YATT_A1_FASTPATH 1
 #endif
 constexpr bool kFastPath = YATT_A1_FASTPATH != 0;
+
+// A1's ring waits: 0 = spin, 1 = the producer sleeps (suspend-time hint),
+// 2 = producer and consumers sleep.  The producer's spin on free slots is
+// ~11% of A1's issued instructions (ncu), yet spinning measured fastest in
+// the sustained bench step on a power-capped box (10.16 / 10.10 / 10.08 M
+// tok/s for 0 / 1 / 2, same box, two runs each): the wake-up latency of a
+// sleeping waiter costs more than the issue slots the spin takes.  (The
+// fused loss + gradient kernel, issue-bound, gains from sleeping waits.)
+#ifndef YATT_A1_SLEEP
+#define YATT_A1_SLEEP 0
+#endif
+__device__ __forceinline__ void a1_producer_wait(uint64_t* bar, uint32_t parity) {
+  if (YATT_A1_SLEEP >= 1) mbar_sleep_wait(bar, parity);
+  else mbar_wait(bar, parity);
+}
+__device__ __forceinline__ void a1_consumer_wait(uint64_t* bar, uint32_t parity) {
+  if (YATT_A1_SLEEP >= 2) mbar_sleep_wait(bar, parity);
+  else mbar_wait(bar, parity);
+}
 constexpr uint32_t kFixupSentinel = 0x7fc0fadeu;  // quiet NaN payload: "recompute me"
 constexpr uint32_t kNegInf2 = 0xFF80FF80u;        // two bf16 -inf
 
@@ -408,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) token_stats_kernel(const
         for (int t = 0; t < ntiles_r; ++t) {
           const int64_t e0 = int64_t(t) * kTile;
           const uint32_t n = uint32_t(min64(kTile, S - e0));
-          mbar_wait(&tail->empty[stage], phase ^ 1u);
+          a1_producer_wait(&tail->empty[stage], phase ^ 1u);
           mbar_arrive_expect_tx(&tail->full[stage], 4u * n);
           uint16_t* dst = ring + size_t(stage) * 2 * kTile;
           bulk_g2s(dst, gp + e0, 2u * n, &tail->full[stage], pol);
@@ -462,7 +481,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) token_stats_kernel(const
       const int nvec = min(kTile, S - e0) >> 3;
       const uint16_t* sp = ring + size_t(stage) * 2 * kTile;
       const uint16_t* sq = sp + kTile;
-      mbar_wait(&tail->full[stage], phase);
+      a1_consumer_wait(&tail->full[stage], phase);
       if (t == ty && tid == 0 && y >= 0 && y < V) {  // target logits from the staged tile
         tail->tgt[par][0] = __uint_as_float(uint32_t(sp[yin]) << 16);
         tail->tgt[par][1] = __uint_as_float(uint32_t(sq[yin]) << 16);
@@ -1088,21 +1107,6 @@ struct __align__(16) PipeTail {
 };
 template <class S>
 constexpr size_t pipe_smem() { return size_t(S::kRing) + sizeof(PipeTail<S>); }
-
-// try_wait with a suspend-time hint: the warp sleeps until the phase
-// completes (or the hint expires) instead of spinning on issue slots.
-__device__ __forceinline__ void mbar_sleep_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t ok = 0;
-  while (!ok) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
-        : "memory");
-  }
-}
 
 // Gradient of 8 logits with the folded row coefficients:
 //   a = x log2e - lse2, p = 2^a, t = c1 a + c0 (- f z), grad = p t
