@@ -37,6 +37,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "grad_math.cuh"
@@ -486,15 +487,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) token_stats_kernel(const
         tail->tgt[par][0] = __uint_as_float(uint32_t(sp[yin]) << 16);
         tail->tgt[par][1] = __uint_as_float(uint32_t(sq[yin]) << 16);
       }
-      {
-        // Full and partial tiles take the same unrolled path: vectors past the
-        // row end read as -inf (2^-inf = 0 in every sum, also after the floor).
-        const bool full = nvec == kVecPerTile;
+      // Whole tiles take an unpredicated path; a partial tile the same
+      // unrolled code with vectors past the row end read as -inf (2^-inf = 0
+      // in every sum, also after the floor).  (One shared predicated path
+      // cost 26 -inf register fills + predicate logic per warp-tile, ~8% of
+      // the tile's instructions.)
+      auto tile = [&](auto whole_tag) {
+        constexpr bool kWhole = decltype(whole_tag)::value;
         uint4 P[kVecPerThread], Q[kVecPerThread];
 #pragma unroll
         for (int i = 0; i < kVecPerThread; ++i) {
           const int v = tid + i * kConsumers;
-          const bool in = full || v < nvec;
+          const bool in = kWhole || v < nvec;
           P[i] = in ? lds128(sp + v * 8) : make_uint4(kNegInf2, kNegInf2, kNegInf2, kNegInf2);
           Q[i] = in ? lds128(sq + v * 8) : make_uint4(kNegInf2, kNegInf2, kNegInf2, kNegInf2);
           if (kEdges) {  // staged elements outside the row read as -inf
@@ -529,7 +533,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) token_stats_kernel(const
         }
 #pragma unroll
         for (int i = 0; i < kVecPerThread; ++i) acc.step(P[i], Q[i]);
-      }
+      };
+      if (nvec == kVecPerTile)
+        tile(std::true_type{});
+      else
+        tile(std::false_type{});
       __syncwarp();
       if (lane == 0) mbar_arrive(&tail->empty[stage]);
       if (++stage == kStages) {
