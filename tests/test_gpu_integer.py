@@ -280,6 +280,30 @@ def test_reference_step_tests_pass_against_b200_library(cuda):
     assert "18 tests, 0 failed" in res.stdout
 
 
+def test_reference_runner_traces_byte_identical(cuda, tmp_path):
+    """The reference's own runner end to end (runner.cpp run_scenario ->
+    make_step_batch -> run_rlhf_step, :152-166, :240-241) over its built-in
+    scenarios table1 (50 steps), sweep and demo: trace.csv, summary.json and
+    scenario.json from the drop-in build (oracle/_ref/runner_b200: every
+    round of every shard on the B200) are byte-identical to the reference's
+    own (runner_ref) — acceptance criterion 11 (acceptance_test.cpp:609-628)
+    across implementations."""
+    exes = {k: ROOT / "oracle" / "_ref" / f"runner_{k}" for k in ("ref", "b200")}
+    for exe in exes.values():
+        assert exe.exists(), "build with `make -C oracle ref` (done by __graft_entry__.build)"
+    outs = {}
+    for k, exe in exes.items():
+        out = tmp_path / k
+        res = subprocess.run([str(exe), str(out)], capture_output=True, text=True, timeout=600)
+        assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+        outs[k] = out
+    files = sorted(p.relative_to(outs["ref"]) for p in outs["ref"].rglob("*") if p.is_file())
+    assert len(files) == 9, files
+    for f in files:
+        a, b = (outs["ref"] / f).read_bytes(), (outs["b200"] / f).read_bytes()
+        assert a == b, f"{f} differs"
+
+
 # ---------------------------------------------------------------- R10 ----
 def test_sort_order_matches_oracle(cuda):
     rng = np.random.default_rng(0)
