@@ -438,6 +438,147 @@ __global__ void __launch_bounds__(kConsumers) token_stats_fixup_kernel(const A1P
   }
 }
 
+#ifndef YATT_A1_SMALL_TU
+// ----------------------------------------------------------------------
+// Small vocabularies: one WARP per row.  With short rows the ring kernel's
+// per-row cost (a CTA-wide barrier after the thread -> warp combine, then a
+// rotating warp's fp64 epilogue) is a large share of a row: at V = 8,192 it
+// ran at 0.55-0.61 of the HBM peak.  Here every warp owns whole rows: its
+// lane 0 streams the warp's rows in 1,024-logit chunks of both tensors into
+// the warp's own 2-stage shared-memory ring (cp.async.bulk, an mbarrier per
+// stage), the lanes fold each chunk into their accumulators with a per-chunk
+// max + exact rebase (no overflow, no fix-up pass), and the row end is a warp
+// shuffle combine plus lane 0's fp64 epilogue — no CTA barrier, and while a
+// warp is at its row end its next chunks keep loading.  2 CTAs x 8 warps per
+// SM (1 x 8 with 4 stages: 0.73 at V = 8,192, 3 x 8: spills).  V % 8 == 0,
+// 16-byte-aligned tensors.
+#ifndef YATT_A1_RW_MINB
+#define YATT_A1_RW_MINB 2
+#endif
+#ifndef YATT_A1_RW_STAGES
+#define YATT_A1_RW_STAGES 2
+#endif
+constexpr int kRWWarps = 8;                    // warps per CTA
+constexpr int kRWMinB = YATT_A1_RW_MINB;       // CTAs per SM
+constexpr int kRWChunk = 1024;                 // logits per tensor per chunk
+constexpr int kRWStages = YATT_A1_RW_STAGES;   // chunks in flight per warp
+constexpr int kRWVec = kRWChunk / 8 / 32;      // 16-byte vectors per lane per tensor
+constexpr size_t kRWStageBytes = size_t(2) * kRWChunk * sizeof(uint16_t);  // pol + ref
+constexpr size_t kRWWarpBytes = kRWStages * kRWStageBytes + kRWStages * sizeof(uint64_t);
+constexpr size_t kRWSmem = kRWWarps * kRWWarpBytes;
+static_assert(kRWVec * 8 * 32 == kRWChunk, "row-warp chunk");
+
+template <bool kFull>
+__global__ void __launch_bounds__(kRWWarps * 32, kRWMinB) token_stats_rowwarp_kernel(
+    const A1Params p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* wbase = smem + size_t(warp) * kRWStages * kRWStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRWWarps * kRWStages * kRWStageBytes) +
+                   warp * kRWStages;
+  const int V = int(p.V);
+  const int nch = (V + kRWChunk - 1) / kRWChunk;
+  const int64_t gw = int64_t(blockIdx.x) * kRWWarps + warp, nw = int64_t(gridDim.x) * kRWWarps;
+  if (lane == 0) {
+    for (int s = 0; s < kRWStages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  // The warp's chunk stream: (row, chunk) for its valid rows, in order.
+  // Lane 0 keeps kRWStages chunks in flight ahead of the consumer.
+  const uint64_t pol_hint = l2_evict_first_policy();
+  int64_t prow = gw;  // producer cursor
+  int pch = 0;
+  auto next_valid = [&](int64_t r) {
+    while (r < p.rows && p.mask != nullptr && p.mask[r] == 0) r += nw;
+    return r;
+  };
+  auto issue = [&](int slot) {  // lane 0: the next chunk of the stream into `slot`
+    if (prow >= p.rows) return;
+    const int e0 = pch * kRWChunk;
+    const uint32_t n = uint32_t(min(kRWChunk, V - e0));
+    uint16_t* dst = reinterpret_cast<uint16_t*>(wbase + size_t(slot) * kRWStageBytes);
+    mbar_arrive_expect_tx(&full[slot], 4u * n);
+    bulk_g2s(dst, p.pol + prow * int64_t(V) + e0, 2u * n, &full[slot], pol_hint);
+    bulk_g2s(dst + kRWChunk, p.ref + prow * int64_t(V) + e0, 2u * n, &full[slot], pol_hint);
+    if (++pch == nch) {
+      pch = 0;
+      prow = next_valid(prow + nw);
+    }
+  };
+  if (lane == 0) {
+    prow = next_valid(prow);
+    for (int s = 0; s < kRWStages; ++s) issue(s);
+  }
+  int slot = 0;
+  uint32_t phase = 0;
+  Acc<kFull> acc;
+  for (int64_t row = gw; row < p.rows; row += nw) {
+    if (p.mask != nullptr && p.mask[row] == 0) {
+      if (lane == 0) {
+        p.logp[row] = 0.f;
+        if (p.ref_logp) p.ref_logp[row] = 0.f;
+        if (p.ent) p.ent[row] = 0.f;
+        if (p.kl) p.kl[row] = 0.f;
+      }
+      continue;
+    }
+    const int32_t y = __ldg(p.tgt + row);
+    const bool yok = y >= 0 && y < V;
+    const int yc = yok ? y / kRWChunk : -1, yin = yok ? y - yc * kRWChunk : 0;
+    const int ylane = (yin >> 3) & 31;
+    float xy = 0.f, zy = 0.f;
+    acc.reset();
+    for (int c = 0; c < nch; ++c) {
+      const uint16_t* sp = reinterpret_cast<const uint16_t*>(wbase + size_t(slot) * kRWStageBytes);
+      const uint16_t* sq = sp + kRWChunk;
+      const int nvec = min(kRWChunk, V - c * kRWChunk) >> 3;
+      mbar_wait(&full[slot], phase);
+      if (c == yc && lane == ylane) {
+        xy = __uint_as_float(uint32_t(sp[yin]) << 16);
+        zy = __uint_as_float(uint32_t(sq[yin]) << 16);
+      }
+      uint4 P[kRWVec], Q[kRWVec];
+      const uint4 ninf = make_uint4(kNegInf2, kNegInf2, kNegInf2, kNegInf2);
+#pragma unroll
+      for (int i = 0; i < kRWVec; ++i) {
+        const int v = lane + 32 * i;
+        const bool in = nvec == kRWChunk / 8 || v < nvec;
+        P[i] = floor_policy(in ? lds128(sp + v * 8) : ninf);
+        Q[i] = in ? lds128(sq + v * 8) : ninf;
+        if (kFull) Q[i] = floor_policy(Q[i]);
+      }
+      uint32_t mpv = vmax4(P[0]), mqv = vmax4(Q[0]);
+#pragma unroll
+      for (int i = 1; i < kRWVec; ++i) {
+        mpv = bmax2(mpv, vmax4(P[i]));
+        mqv = bmax2(mqv, vmax4(Q[i]));
+      }
+      const float fmp = pair_max(mpv), fmq = pair_max(mqv);
+      if (fmp > acc.thr_p) acc.rebase_p(fmp);
+      if (fmq > acc.thr_q) acc.rebase_q(fmq);
+#pragma unroll
+      for (int i = 0; i < kRWVec; ++i) acc.step(P[i], Q[i]);
+      __syncwarp();  // every lane's reads of the slot are done: refill it
+      if (lane == 0) issue(slot);
+      if (++slot == kRWStages) {
+        slot = 0;
+        phase ^= 1u;
+      }
+    }
+    RowPartial r{acc.mp, Acc<kFull>::total(acc.s), Acc<kFull>::total(acc.w), acc.mq,
+                 Acc<kFull>::total(acc.sq), kFull ? Acc<kFull>::total(acc.u) : 0.f};
+    r = warp_combine<kFull>(r);
+    xy = __shfl_sync(0xffffffffu, xy, ylane);
+    zy = __shfl_sync(0xffffffffu, zy, ylane);
+    if (lane == 0) {
+      const float nan = __uint_as_float(0x7fc00000u);
+      emit_row(p, row, r, yok ? xy : nan, yok ? zy : nan);
+    }
+  }
+}
+#endif  // !YATT_A1_SMALL_TU
+
 }  // namespace
 
 #ifdef YATT_A1_SMALL_TU
@@ -493,6 +634,17 @@ int token_stats_ring_small(const A1Params& p, cudaStream_t st);  // token_stats_
 #ifndef YATT_A1_SMALL_VMAX
 #define YATT_A1_SMALL_VMAX 60000
 #endif
+// Vocabularies up to this (V % 8 == 0) take the warp-per-row kernel.
+// Fraction of the measured HBM peak, warp-per-row vs ring (k3 / full KL,
+// profiles/r2_a1_rowwarp_v*.jsonl): V=8,192 0.911 vs 0.611 / 0.860 vs 0.576;
+// 24,576 0.959 vs 0.887 / 0.934 vs 0.819; 32,000 0.942 vs 0.903 / 0.898 vs
+// 0.832; 40,960 0.924 vs 0.934 / 0.890 vs 0.892; 65,536 0.869 vs 0.957.
+// YATT_A1_ROWWARP_VMAX overrides (measurement only).
+int a1_rowwarp_vmax() {
+  const char* e = std::getenv("YATT_A1_ROWWARP_VMAX");
+  return e ? std::atoi(e) : 36864;
+}
+
 int a1_small_vmax() {
   static const int v = [] {
     const char* e = std::getenv("YATT_A1_SMALL_VMAX");
@@ -547,6 +699,19 @@ int token_stats_launch(const uint16_t* pol, const uint16_t* ref, const int32_t* 
     else
       token_stats_fixup_kernel<false, true><<<ggrid, kConsumers, 0, st>>>(p);
     return check_launch("token_stats_generic_kernel");
+  }
+  if (vocab % 8 == 0 && vocab <= a1_rowwarp_vmax()) {
+    const void* k = kl_mode == YATT_KL_FULL
+                        ? reinterpret_cast<const void*>(token_stats_rowwarp_kernel<true>)
+                        : reinterpret_cast<const void*>(token_stats_rowwarp_kernel<false>);
+    const int rc = ensure_dynamic_smem(k, int(kRWSmem));
+    if (rc) return rc;
+    const int grid = int(min64(ceil_div(rows, kRWWarps), int64_t(kRWMinB) * num_sms()));
+    if (kl_mode == YATT_KL_FULL)
+      token_stats_rowwarp_kernel<true><<<grid, kRWWarps * 32, kRWSmem, st>>>(p);
+    else
+      token_stats_rowwarp_kernel<false><<<grid, kRWWarps * 32, kRWSmem, st>>>(p);
+    return check_launch("token_stats_rowwarp_kernel");
   }
   return vocab <= a1_small_vmax() ? token_stats_ring_small(p, st) : token_stats_ring_large(p, st);
 }

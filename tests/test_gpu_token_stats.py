@@ -252,3 +252,41 @@ def test_token_stats_tiny_vocab_ragged_rows(cuda, vocab, rows):
     assert np.all(np.isfinite(got))
     for i in range(3):
         assert np.all(np.abs(got[i] - exp[i]) <= TOL * np.abs(exp[i]) + 1e-6), i
+
+
+@pytest.mark.parametrize("vocab", [4096, 8200, 32000])
+@pytest.mark.parametrize("kl_mode", ["k3", "full"])
+def test_token_stats_rowwarp_many_rows_per_warp(cuda, vocab, kl_mode):
+    """Small vocabularies take the warp-per-row kernel (2 x 148 CTAs x 8 warps
+    = 2,368 warps): three-plus rows per warp so each warp's chunk stream runs
+    across rows (a partial last chunk at V = 8,200), masked rows skipped in
+    the stream, and extreme rows — a -inf first chunk, a logit 100 nats above
+    the rest late in the row, constant rows — exact against the fp64 oracle
+    (per-chunk rebase: no fix-up pass)."""
+    rows = 3 * 2368 + 17
+    pol, ref, tgt = ops.synth_logits(11, 0, rows, vocab, device=cuda)
+    ar = torch.arange(rows, device=cuda)
+    keep_p, keep_r = pol[ar, tgt.long()].clone(), ref[ar, tgt.long()].clone()
+    pol[5, :1024] = float("-inf")
+    ref[5, :1024] = float("-inf")
+    pol[2400, vocab - 3] = 100.0
+    ref[4800, vocab // 2] = 96.0
+    pol[7000, :] = 60.0
+    ref[7000, :] = -60.0
+    pol[ar, tgt.long()], ref[ar, tgt.long()] = keep_p, keep_r
+    mask_np = (np.arange(rows) % 5 != 3).astype(np.uint8)
+    out = torch.stack(ops.token_stats(pol, ref, tgt, torch.from_numpy(mask_np).to(cuda),
+                                      kl_mode)).cpu().numpy()
+    hp = pol.view(torch.int16).cpu().numpy().view(np.uint16)
+    hr = ref.view(torch.int16).cpu().numpy().view(np.uint16)
+    exp = O.token_stats(hp, hr, tgt.cpu().numpy(), mask_np, kl_mode)
+    assert np.all(np.isfinite(out))
+    valid = mask_np.astype(bool)
+    assert np.all(out[:, ~valid] == 0)
+    for i in range(4):
+        # rows with p(target) ~ 1 or a one-hot row (entropy ~ 0): ~1e-6 absolute
+        assert np.all(np.abs(out[i][valid] - exp[i][valid])
+                      <= TOL * np.abs(exp[i][valid]) + 4e-6), i
+    typical = valid & ~np.isin(np.arange(rows), [5, 2400, 4800, 7000])
+    for i in range(3):
+        assert O.max_rel_error(out[i][typical], exp[i][typical]) <= TOL, i
