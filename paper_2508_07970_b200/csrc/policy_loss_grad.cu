@@ -167,7 +167,7 @@ __device__ __forceinline__ int pass2_tile(int k, int ntiles, int order) {
   return order == 1 ? ntiles - 1 - k : k;
 }
 
-template <bool kFull, int kOrder, class S>
+template <bool kFull, int kOrder, class S, int kLag>
 __global__ void __launch_bounds__(S::kThreads, S::kMinB) policy_loss_grad_pipe_kernel(
     const FusedParams p) {
   constexpr int kFCW = S::kCW, kFC = S::kC;
@@ -203,29 +203,40 @@ __global__ void __launch_bounds__(S::kThreads, S::kMinB) policy_loss_grad_pipe_k
       const uint64_t keep = l2_evict_normal_policy(), drop = l2_evict_first_policy();
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
-        if (p.mask != nullptr && p.mask[row] == 0) continue;
+      auto issue = [&](int64_t row, int pass) {
         const uint16_t* gp = p.pol + row * int64_t(V);
         const uint16_t* gq = kFull ? p.ref + row * int64_t(V) : nullptr;
-        for (int pass = 0; pass < 2; ++pass) {
-          for (int k = 0; k < ntiles; ++k) {
-            const int t = pass == 0 ? k : pass2_tile(k, ntiles, kOrder);
-            const int e0 = t * kPT;
-            const uint32_t n = uint32_t(min(kPT, V - e0));
-            // pass 1 keeps the row in L2 for pass 2 (evict-normal), pass 2 drops it
-            const uint64_t pol = pass == 0 ? keep : drop;
-            mbar_sleep_wait(&tail->empty[stage], phase ^ 1u);
-            mbar_arrive_expect_tx(&tail->full[stage], 2u * n * kPS);
-            uint16_t* dst = ring + size_t(stage) * kPS * kPT;
-            bulk_g2s(dst, gp + e0, 2u * n, &tail->full[stage], pol);
-            if (kFull) bulk_g2s(dst + kPT, gq + e0, 2u * n, &tail->full[stage], pol);
-            if (++stage == kNS) {
-              stage = 0;
-              phase ^= 1u;
-            }
+        for (int k = 0; k < ntiles; ++k) {
+          const int t = pass == 0 ? k : pass2_tile(k, ntiles, kOrder);
+          const int e0 = t * kPT;
+          const uint32_t n = uint32_t(min(kPT, V - e0));
+          // pass 1 keeps the row in L2 for pass 2 (evict-normal), pass 2 drops it
+          const uint64_t pol = pass == 0 ? keep : drop;
+          mbar_sleep_wait(&tail->empty[stage], phase ^ 1u);
+          mbar_arrive_expect_tx(&tail->full[stage], 2u * n * kPS);
+          uint16_t* dst = ring + size_t(stage) * kPS * kPT;
+          bulk_g2s(dst, gp + e0, 2u * n, &tail->full[stage], pol);
+          if (kFull) bulk_g2s(dst + kPT, gq + e0, 2u * n, &tail->full[stage], pol);
+          if (++stage == kNS) {
+            stage = 0;
+            phase ^= 1u;
           }
         }
+      };
+      // kLag = 1: pass 1 of row j before pass 2 of row j - 1 (the order the
+      // consumers take them in)
+      int64_t prev = -1;
+      for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
+        if (p.mask != nullptr && p.mask[row] == 0) continue;
+        issue(row, 0);
+        if (kLag == 0) {
+          issue(row, 1);
+        } else {
+          if (prev >= 0) issue(prev, 1);
+          prev = row;
+        }
       }
+      if (kLag != 0 && prev >= 0) issue(prev, 1);
     }
   } else if (warp == kFCW + 1) {
     // ---------------- epilogue warp: row partials -> coefficients ----------
@@ -334,10 +345,60 @@ __global__ void __launch_bounds__(S::kThreads, S::kMinB) policy_loss_grad_pipe_k
     uint32_t phase = 0;
     Acc<kFull, kFull> acc;
     const uint4 ninf = make_uint4(kNegInf2, kNegInf2, kNegInf2, kNegInf2);
-    int j = 0;
-    for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
+    // ---- pass 2 of row `row` (the jr-th valid row): the gradient, second
+    // read of the row from L2 ----
+    auto pass2 = [&](int64_t row, int jr) {
       uint16_t* gs = p.grad + row * int64_t(V);
+      const int32_t y = __ldg(p.tgt + row);
+      const bool yok = y >= 0 && y < V;
+      const int ty = yok ? y / kPT : -1, yin = yok ? y - ty * kPT : 0;
+      mbar_sleep_wait(&tail->cfull[jr & 1], uint32_t(jr >> 1) & 1u);
+      const float* cf = tail->coef[jr & 1];
+      const float2 nl = f2(-cf[3], -cf[3]), c1 = f2(cf[8], cf[8]), c0 = f2(cf[9], cf[9]),
+                   nf = f2(cf[10], cf[10]);
+      for (int k = 0; k < ntiles; ++k) {
+        const int t = pass2_tile(k, ntiles, kOrder);
+        const int e0 = t * kPT;
+        const uint16_t* sp = ring + size_t(stage) * kPS * kPT;
+        const uint16_t* sq = sp + kPT;
+        mbar_sleep_wait(&tail->full[stage], phase);
+        if (t < nfull) {
+          uint4 P[kPV], Q[kPV];
+#pragma unroll
+          for (int i = 0; i < kPV; ++i) {
+            P[i] = floor_policy(lds128(sp + (tid + i * kFC) * 8));
+            Q[i] = kFull ? floor_policy(lds128(sq + (tid + i * kFC) * 8)) : P[i];
+          }
+#pragma unroll
+          for (int i = 0; i < kPV; ++i)
+            gm::stg_cs_128(gs + e0 + (tid + i * kFC) * 8,
+                           grad_vec_folded<kFull>(P[i], Q[i], nl, c1, c0, nf));
+        } else {
+          for (int v = tid; v < last_nvec; v += kFC) {
+            const uint4 P = floor_policy(lds128(sp + v * 8));
+            const uint4 Q = kFull ? floor_policy(lds128(sq + v * 8)) : P;
+            gm::stg_cs_128(gs + e0 + v * 8, grad_vec_folded<kFull>(P, Q, nl, c1, c0, nf));
+          }
+        }
+        if (t == ty && tid == (yin >> 3) % kFC) {  // the target element carries + g
+          const gm::RowCoef c{cf[0], cf[1], cf[2], cf[3], cf[4], cf[5], cf[6]};
+          const float x = __uint_as_float(uint32_t(sp[yin]) << 16);
+          const float z = kFull ? __uint_as_float(uint32_t(sq[yin]) << 16) : 0.f;
+          gs[y] = uint16_t(pack_bf16x2(target_grad<kFull>(x, z, c), 0.f) & 0xffffu);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tail->empty[stage]);
+        if (++stage == kNS) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+    };
+    int j = 0;
+    int64_t prev = -1;
+    for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
       if (p.mask != nullptr && p.mask[row] == 0) {
+        uint16_t* gs = p.grad + row * int64_t(V);
         if (tid == 0) {
           p.logp[row] = 0.f;
           if (p.ent) p.ent[row] = 0.f;
@@ -404,66 +465,28 @@ __global__ void __launch_bounds__(S::kThreads, S::kMinB) policy_loss_grad_pipe_k
         tail->red[b][warp] = r;
         mbar_arrive(&tail->pfull[b]);  // release: the partial (and xy) before it
       }
-      // ---- pass 2: the gradient (second read of the row, from L2) ----
-      mbar_sleep_wait(&tail->cfull[b], uint32_t(j >> 1) & 1u);
-      const float* cf = tail->coef[b];
-      const float2 nl = f2(-cf[3], -cf[3]), c1 = f2(cf[8], cf[8]), c0 = f2(cf[9], cf[9]),
-                   nf = f2(cf[10], cf[10]);
-      for (int k = 0; k < ntiles; ++k) {
-        const int t = pass2_tile(k, ntiles, kOrder);
-        const int e0 = t * kPT;
-        const uint16_t* sp = ring + size_t(stage) * kPS * kPT;
-        const uint16_t* sq = sp + kPT;
-        mbar_sleep_wait(&tail->full[stage], phase);
-        if (t < nfull) {
-          uint4 P[kPV], Q[kPV];
-#pragma unroll
-          for (int i = 0; i < kPV; ++i) {
-            P[i] = floor_policy(lds128(sp + (tid + i * kFC) * 8));
-            Q[i] = kFull ? floor_policy(lds128(sq + (tid + i * kFC) * 8)) : P[i];
-          }
-#pragma unroll
-          for (int i = 0; i < kPV; ++i)
-            gm::stg_cs_128(gs + e0 + (tid + i * kFC) * 8,
-                           grad_vec_folded<kFull>(P[i], Q[i], nl, c1, c0, nf));
-        } else {
-          for (int v = tid; v < last_nvec; v += kFC) {
-            const uint4 P = floor_policy(lds128(sp + v * 8));
-            const uint4 Q = kFull ? floor_policy(lds128(sq + v * 8)) : P;
-            gm::stg_cs_128(gs + e0 + v * 8, grad_vec_folded<kFull>(P, Q, nl, c1, c0, nf));
-          }
-        }
-        if (t == ty && tid == (yin >> 3) % kFC) {  // the target element carries + g
-          const gm::RowCoef c{cf[0], cf[1], cf[2], cf[3], cf[4], cf[5], cf[6]};
-          const float x = __uint_as_float(uint32_t(sp[yin]) << 16);
-          const float z = kFull ? __uint_as_float(uint32_t(sq[yin]) << 16) : 0.f;
-          gs[y] = uint16_t(pack_bf16x2(target_grad<kFull>(x, z, c), 0.f) & 0xffffu);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tail->empty[stage]);
-        if (++stage == kNS) {
-          stage = 0;
-          phase ^= 1u;
-        }
+      if (kLag == 0) {
+        pass2(row, j);
+      } else {  // pass 1 of the next row first: the row end overlaps a whole pass
+        if (prev >= 0) pass2(prev, j - 1);
+        prev = row;
       }
       ++j;
     }
+    if (kLag != 0 && prev >= 0) pass2(prev, j - 1);
   }
 }
 }  // namespace
 
 // Launch with shape S (YATT_FUSED_ORDER = pass-2 tile order, measurement only).
-template <class S>
-int policy_loss_grad_pipe(const FusedParams& p, cudaStream_t st) {
+template <class S, int kLag>
+int policy_loss_grad_pipe_launch(const FusedParams& p, int order, cudaStream_t st) {
   const bool full = p.kl_mode == YATT_KL_FULL;
-  const char* ord_env = std::getenv("YATT_FUSED_ORDER");  // measurement only
-  const int order = ord_env ? std::atoi(ord_env) : 1;
-  YATT_REQUIRE(order == 0 || order == 1, YATT_ERR_CONFIG, "YATT_FUSED_ORDER must be 0 or 1");
   const void* const kernels[2][2] = {
-      {reinterpret_cast<const void*>(policy_loss_grad_pipe_kernel<false, 0, S>),
-       reinterpret_cast<const void*>(policy_loss_grad_pipe_kernel<false, 1, S>)},
-      {reinterpret_cast<const void*>(policy_loss_grad_pipe_kernel<true, 0, S>),
-       reinterpret_cast<const void*>(policy_loss_grad_pipe_kernel<true, 1, S>)}};
+      {reinterpret_cast<const void*>(policy_loss_grad_pipe_kernel<false, 0, S, kLag>),
+       reinterpret_cast<const void*>(policy_loss_grad_pipe_kernel<false, 1, S, kLag>)},
+      {reinterpret_cast<const void*>(policy_loss_grad_pipe_kernel<true, 0, S, kLag>),
+       reinterpret_cast<const void*>(policy_loss_grad_pipe_kernel<true, 1, S, kLag>)}};
   const void* k = kernels[full ? 1 : 0][order];
   const int rc = ensure_dynamic_smem(k, int(pipe_smem<S>()));
   if (rc) return rc;
@@ -473,6 +496,21 @@ int policy_loss_grad_pipe(const FusedParams& p, cudaStream_t st) {
                                  pipe_smem<S>(), st));
   return check_launch("policy_loss_grad_pipe_kernel");
 }
+
+// Launch with shape S; kLagDefault = whether pass 1 of the next row runs
+// before pass 2 of this one (measurement only: YATT_FUSED_ORDER = pass-2
+// tile order, YATT_FUSED_LAG = 0 / 1 overrides the lag).
+template <class S, int kLagDefault>
+int policy_loss_grad_pipe(const FusedParams& p, cudaStream_t st) {
+  const char* ord_env = std::getenv("YATT_FUSED_ORDER");
+  const int order = ord_env ? std::atoi(ord_env) : 1;
+  YATT_REQUIRE(order == 0 || order == 1, YATT_ERR_CONFIG, "YATT_FUSED_ORDER must be 0 or 1");
+  const char* lag_env = std::getenv("YATT_FUSED_LAG");
+  const int lag = lag_env ? std::atoi(lag_env) : kLagDefault;
+  return lag ? policy_loss_grad_pipe_launch<S, 1>(p, order, st)
+             : policy_loss_grad_pipe_launch<S, 0>(p, order, st);
+}
+
 size_t policy_loss_grad_workspace_bytes(int64_t rows, int32_t agg_mode) {
   return agg_mode == 1 ? size_t(max64(rows, 0)) * sizeof(float) : 0;
 }
@@ -516,17 +554,26 @@ int policy_loss_grad_launch(const uint16_t* pol, const uint16_t* ref, const int3
   // the last row; the aligned-V contract keeps the fused path simple
   YATT_REQUIRE(p.V % 8 == 0, YATT_ERR_CONFIG,
                "policy_loss_grad: vocab must be a multiple of 8 (got %d)", p.V);
-  // Shape by vocabulary (k3 / full-KL fraction of the HBM roofline,
-  // profiles/r2_fused_pipe_v8/v9.jsonl): the small shape (2 CTAs/SM) vs the
-  // large one (1 CTA/SM) at V=65,536 0.933 vs 0.861 / 0.857 vs 0.806; 81,920
-  // 0.906 vs 0.911 / 0.844 vs 0.850; 98,304 0.862 vs 0.947 / 0.802 vs 0.870.
-  // YATT_FUSED_PIPE = 1 / 2 forces the large / small shape (measurement).
-  constexpr int kFusedSmallVmax = 73728;
+  // Shape by vocabulary, i.e. by how many rows can stay live in L2 between
+  // their two passes (profiles/r2_fused_pipe_v11_lag.jsonl, fraction of the
+  // HBM roofline, k3 / full KL):
+  //   small shape (2 CTAs/SM) + lag (pass 1 of the next row before pass 2 of
+  //     this one; 4 live rows per SM): k3 V=32,000 0.897 (no lag 0.830)
+  //   large shape (1 CTA/SM) + lag (2 live rows per SM): k3 V=65,536 0.998
+  //     (small 0.933, large 0.856); full KL V=32,000 0.780, 50,264 0.792,
+  //     65,536 0.817 (small 0.770 / 0.769 / 0.819)
+  //   large shape, no lag (1 live row per SM) above: k3 V=98,304 0.942 (with
+  //     lag 0.796), 152,064 0.965 (0.691); full KL 98,304 0.863 (0.654)
+  // YATT_FUSED_PIPE = 1 / 2 forces the large / small shape, YATT_FUSED_LAG
+  // the lag (measurement only).
+  constexpr int kSmallLagVmax = 36864, kLagVmax = 73728;
   const char* env = std::getenv("YATT_FUSED_PIPE");
   const int pipe = env ? std::atoi(env) : 0;
-  if (pipe == 2 || (pipe != 1 && p.V <= kFusedSmallVmax))
-    return policy_loss_grad_pipe<PipeSmall>(p, st);
-  return policy_loss_grad_pipe<PipeLarge>(p, st);
+  const bool full = p.kl_mode == YATT_KL_FULL;
+  if (pipe == 2 || (pipe == 0 && !full && p.V <= kSmallLagVmax))
+    return policy_loss_grad_pipe<PipeSmall, 1>(p, st);
+  if (p.V <= kLagVmax) return policy_loss_grad_pipe<PipeLarge, 1>(p, st);
+  return policy_loss_grad_pipe<PipeLarge, 0>(p, st);
 }
 
 }  // namespace yattb

@@ -232,16 +232,18 @@ def test_fused_extreme_rows(cuda, kl_mode):
     assert float((gf.sum(1).abs() / (gf.abs().amax(1) * vocab ** 0.5 + 1e-30)).max()) < 1e-2
 
 
-@pytest.mark.parametrize("shape", ["1:1", "1:0", "2:1", "2:0"])
+@pytest.mark.parametrize("shape", ["1:1:0", "1:0:0", "1:1:1", "2:1:1", "2:0:0"])
 @pytest.mark.parametrize("kl_mode", ["k3", "full"])
 def test_fused_pipelined_many_rows_per_cta(cuda, kl_mode, shape, monkeypatch):
     """Large vocabulary with several rows per CTA, so the double-buffered
     partials / coefficients of the epilogue-warp kernel cycle, in both
-    compiled shapes (YATT_FUSED_PIPE = 1 large / 2 small) and both pass-2
-    tile orders, against the fp64 oracle, masked rows included."""
-    kernel, order = shape.split(":")
+    compiled shapes (YATT_FUSED_PIPE = 1 large / 2 small), both pass-2 tile
+    orders and with / without the one-row lag, against the fp64 oracle,
+    masked rows included."""
+    kernel, order, lag = shape.split(":")
     monkeypatch.setenv("YATT_FUSED_PIPE", kernel)
     monkeypatch.setenv("YATT_FUSED_ORDER", order)  # pass-2 tile order: forward / reverse
+    monkeypatch.setenv("YATT_FUSED_LAG", lag)  # pass 1 of the next row before pass 2
     _case(cuda, 3 * 148 + 13, 65536, kl_mode, masked=True, ent_coef=0.001)
     # ragged tile counts: a last tile of one vector, a partial last tile
     _case(cuda, 2 * 148 + 3, 65544, kl_mode, ent_coef=0.001)

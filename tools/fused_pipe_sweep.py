@@ -1,8 +1,9 @@
 #!/usr/bin/env python3
 """The fused loss + gradient kernel (policy_loss_grad.cu) by shape:
-SHAPES entries "<pipe><order>" — YATT_FUSED_PIPE 1 (large: 1 CTA/SM) or 2
-(small: 2 CTAs/SM), YATT_FUSED_ORDER 0 (forward pass 2) / 1 (reverse, the
-default); k3 and full KL at 32,768 x
+SHAPES entries "<pipe>[order][l|n]" — YATT_FUSED_PIPE 0 (the default
+dispatch), 1 (large: 1 CTA/SM) or 2 (small: 2 CTAs/SM); YATT_FUSED_ORDER 0
+(forward pass 2) / 1 (reverse, the default); "l" / "n" forces the one-row lag
+on / off; k3 and full KL at 32,768 x
 152,064 (a configs[1] prompt group).  Device time as tools/bench_kernels.py
 (CUDA graph, L2 flushed), achieved algorithmic GB/s vs the measured peak, and
 every shape's outputs against the first shape's."""
@@ -20,7 +21,7 @@ from paper_2508_07970_b200 import ops  # noqa: E402
 
 rows = int(os.environ.get("ROWS", 32768))
 V = int(os.environ.get("VOCAB", 152064))
-shapes = os.environ.get("SHAPES", "1,2,10").split(",")
+shapes = os.environ.get("SHAPES", "0,1n,1l,2n,2l").split(",")
 seed = 20250814
 pol, ref, tgt = ops.synth_logits(seed, 0, rows, V)
 lp, rl, en, kl = ops.token_stats(pol, ref, tgt, None, "k3")
@@ -32,8 +33,11 @@ grad = torch.empty_like(pol)
 for mode in ("k3", "full"):
     base = None
     for sh in shapes:
-        os.environ["YATT_FUSED_PIPE"] = sh[0]
-        os.environ["YATT_FUSED_ORDER"] = sh[1:] or "1"  # pass-2 order: 0 forward, 1 reverse
+        os.environ["YATT_FUSED_PIPE"] = sh[0]  # 0 = the default dispatch by vocabulary
+        os.environ.pop("YATT_FUSED_LAG", None)
+        if "l" in sh or "n" in sh:  # force the lag on ("l") / off ("n")
+            os.environ["YATT_FUSED_LAG"] = "1" if "l" in sh else "0"
+        os.environ["YATT_FUSED_ORDER"] = sh[1:].replace("l", "").replace("n", "") or "1"
 
         def run(m=None):
             return ops.policy_loss_grad(pol, tgt, old, adv, rl if mode != "full" else None, m, cfg,
