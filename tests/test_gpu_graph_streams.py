@@ -170,3 +170,37 @@ def test_peer_group_single_rank_matches_plain_ops(cuda):
         assert peer.status() == 0
     finally:
         peer.close()
+
+
+@pytest.mark.parametrize("V", [32000, 65536, 152064])
+def test_fused_loss_grad_replays_bit_exact_from_a_cuda_graph(cuda, V):
+    """The fused loss + gradient op (each shape the dispatch picks: 2 CTAs/SM
+    + lag, 1 CTA/SM + lag, 1 CTA/SM) captured into a CUDA graph: replays
+    reproduce the eager outputs bit for bit (no host sync, no allocation)."""
+    rows = 3 * 148 + 5
+    pol, ref, tgt = ops.synth_logits(3, 0, rows, V, device=cuda)
+    lp, rl, _, _ = ops.token_stats(pol, ref, tgt, None, "k3")
+    old = ops.synth_floats(3, 104, 0, rows, "old_delta", base=lp, device=cuda)
+    adv = ops.synth_floats(3, 108, 0, rows, "adv", device=cuda)
+    cfg = ops.loss_config(0.2, 0.28, 0.0, 0.001, 0.001, "token-mean")
+    grad = torch.empty_like(pol)
+
+    def run():
+        return ops.policy_loss_grad(pol, tgt, old, adv, rl, None, cfg, "k3", float(rows), grad)
+    eager = [t.clone() for t in run()]
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        run()
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        outs = run()
+    for t in outs:
+        t.zero_()
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(eager, outs):
+        assert torch.equal(a, b)
