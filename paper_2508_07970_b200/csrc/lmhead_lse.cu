@@ -132,10 +132,15 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 // multicast into both CTAs' shared memory (a third less L2->SM traffic per
 // CTA); a ring stage is reused only after BOTH CTAs' MMAs retired it
 // (multicast tcgen05.commit, empty barriers count 2).
+// Work units (row tile, vocabulary split), split fastest.  A launch either
+// maps one unit per CTA (grid = units, the first waves' tail idles SMs) or
+// runs persistent CTAs (grid = SMs) that walk the units in the same order
+// with their ring / accumulator pipelines continuing across units.
 template <int kCluster>
 __global__ void __launch_bounds__(kGemmThreads, 1) lmhead_lse_kernel(
     const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-    int64_t rows, int32_t V, int32_t d, int32_t v_per_split, float4* partial) {
+    int64_t rows, int32_t V, int32_t d, int32_t v_per_split, int32_t nsplit, int64_t nunits,
+    float4* partial) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -144,12 +149,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1) lmhead_lse_kernel(
   // Rasterisation: vocabulary split fastest, so the CTAs resident at one time
   // cover few row tiles (their hidden tiles stay in L2) and walk the same
   // weight tiles together.
-  const int64_t m0 = int64_t(blockIdx.y) * BM;
-  const int split = blockIdx.x;
-  const int v0 = split * v_per_split;
-  const int v1 = min(V, v0 + v_per_split);
-  const int ntiles = (v1 - v0 + BN - 1) / BN;
+  const int64_t u_first = int64_t(blockIdx.y) * gridDim.x + blockIdx.x;
+  const int64_t u_stride = int64_t(gridDim.x) * gridDim.y;
   const int nk = (d + BK - 1) / BK;
+  struct Unit {
+    int64_t m0;
+    int v0, v1, ntiles;
+  };
+  auto unit = [&](int64_t u) {
+    Unit x;
+    x.m0 = (u / nsplit) * BM;
+    x.v0 = int(u % nsplit) * v_per_split;
+    x.v1 = min(V, x.v0 + v_per_split);
+    x.ntiles = (x.v1 - x.v0 + BN - 1) / BN;
+    return x;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStagesG; ++s) {
@@ -182,8 +196,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) lmhead_lse_kernel(
     if (lane == 0) {  // ---- TMA producer ----
       int stage = 0;
       uint32_t phase = 0;
-      for (int j = 0; j < ntiles; ++j) {
-        const int n0 = v0 + j * BN;
+      for (int64_t u = u_first; u < nunits; u += u_stride) {
+      const Unit w = unit(u);
+      const int64_t m0 = w.m0;
+      for (int j = 0; j < w.ntiles; ++j) {
+        const int n0 = w.v0 + j * BN;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&bars->empty[stage], phase ^ 1u);
           mbar_arrive_expect_tx(&bars->full[stage], kStageBytes);
@@ -200,14 +217,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1) lmhead_lse_kernel(
           }
         }
       }
+      }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer ----
       int stage = 0;
       uint32_t phase = 0;
-      for (int j = 0; j < ntiles; ++j) {
-        const int acc = j & 1;
-        const uint32_t aphase = (j >> 1) & 1;
+      int jg = 0;  // accumulator tiles so far (across units)
+      for (int64_t u = u_first; u < nunits; u += u_stride) {
+      const Unit w = unit(u);
+      for (int j = 0; j < w.ntiles; ++j, ++jg) {
+        const int acc = jg & 1;
+        const uint32_t aphase = (jg >> 1) & 1;
         mbar_wait(&bars->tempty[acc], aphase ^ 1u);
         tc_fence_after();
         const uint32_t tmem_d = tmem + uint32_t(acc * BN);
@@ -234,18 +255,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1) lmhead_lse_kernel(
         }
         umma_commit(&bars->tfull[acc]);  // accumulator ready for the epilogue
       }
+      }
     }
   } else {
     // ---- epilogue: warps 2..5, TMEM lane quarter = warp % 4 ----
     const int quarter = warp & 3;
-    const int64_t row = m0 + quarter * 32 + lane;
+    int jg = 0;
+    for (int64_t u = u_first; u < nunits; u += u_stride) {
+    const Unit w = unit(u);
+    const int v1 = w.v1;
+    const int64_t row = w.m0 + quarter * 32 + lane;
     LseState st{-float(1 << 24), 0.0, 0.0};
-    for (int j = 0; j < ntiles; ++j) {
-      const int acc = j & 1;
-      const uint32_t aphase = (j >> 1) & 1;
+    for (int j = 0; j < w.ntiles; ++j, ++jg) {
+      const int acc = jg & 1;
+      const uint32_t aphase = (jg >> 1) & 1;
       mbar_wait(&bars->tfull[acc], aphase);
       tc_fence_after();
-      const int n0 = v0 + j * BN;
+      const int n0 = w.v0 + j * BN;
       const uint32_t tbase = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
@@ -287,8 +313,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) lmhead_lse_kernel(
     }
     if (row < rows) {  // normalised so s fits fp32 exactly enough
       const int k = st.s > 0 ? ilogb(st.s) : 0;
-      partial[int64_t(split) * rows + row] =
+      partial[(u % nsplit) * rows + row] =
           make_float4(st.m + float(k), float(ldexp(st.s, -k)), float(ldexp(st.w - k * st.s, -k)), 0.f);
+    }
     }
   }
   __syncthreads();
@@ -418,7 +445,13 @@ int lmhead_token_stats_launch(const uint16_t* hidden, const uint16_t* W, const i
     }
   const int64_t mtiles = ceil_div(ceil_div(rows, BM), cluster) * cluster;
   YATT_REQUIRE(mtiles <= 65535, YATT_ERR_CONFIG, "lmhead: too many rows per launch");
-  const dim3 grid{unsigned(nsplit_eff), unsigned(mtiles), 1u};
+  const int64_t nunits = mtiles * nsplit_eff;
+  // YATT_LMHEAD_PERSIST=1: one persistent CTA per SM walking the units
+  // (measurement only)
+  const char* pe = getenv("YATT_LMHEAD_PERSIST");
+  const bool persist = cluster == 1 && pe && pe[0] == '1';
+  const dim3 grid = persist ? dim3(unsigned(min64(nunits, num_sms())), 1u, 1u)
+                            : dim3(unsigned(nsplit_eff), unsigned(mtiles), 1u);
   float4* partial = static_cast<float4*>(ws);
   if (cluster == 2) {
     cudaLaunchConfig_t lc = {};
@@ -434,10 +467,10 @@ int lmhead_token_stats_launch(const uint16_t* hidden, const uint16_t* W, const i
     lc.attrs = at;
     lc.numAttrs = 1;
     YATT_TRY_CUDA(cudaLaunchKernelEx(&lc, lmhead_lse_kernel<2>, ta, tb, rows, V, d, v_per_split,
-                                     partial));
+                                     int32_t(nsplit_eff), nunits, partial));
   } else {
-    lmhead_lse_kernel<1><<<grid, kGemmThreads, kGemmSmem, st>>>(ta, tb, rows, V, d, v_per_split,
-                                                                partial);
+    lmhead_lse_kernel<1><<<grid, kGemmThreads, kGemmSmem, st>>>(
+        ta, tb, rows, V, d, v_per_split, int32_t(nsplit_eff), nunits, partial);
   }
   rc = check_launch("lmhead_lse_kernel");
   if (rc) return rc;
