@@ -102,6 +102,45 @@ struct LseState {
   double s, w;    // sum 2^a, sum 2^a * a (fp64 across the ~5K chunks of a row)
 };
 
+// Online log2 LSE + entropy over one BN-column accumulator tile: this
+// thread's row, columns [n0, min(n0 + BN, v1)) read from TMEM 32 at a time.
+__device__ __forceinline__ void lse_tile(uint32_t tbase, int n0, int v1, LseState& st) {
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    uint32_t r[32];
+    TMEM_LD32(tbase + uint32_t(c * 32), r);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    const int colbase = n0 + c * 32;
+    const int valid = min(32, v1 - colbase);  // partial last tile
+    float cmax = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+      if (k < valid) cmax = fmaxf(cmax, __uint_as_float(r[k]));
+    if (valid > 0 && cmax * kL2e > st.m + 24.f) {  // rebase (exact power of two)
+      const float mn = ceilf(cmax * kL2e);
+      const double dd = double(st.m) - double(mn);
+      const double cs = exp2(fmax(dd, -1000.0));
+      st.w = cs * (dd * st.s + st.w);
+      st.s *= cs;
+      st.m = mn;
+    }
+    float2 s2 = make_float2(0.f, 0.f), w2 = s2;
+    const float2 L2 = make_float2(kL2e, kL2e), nm = make_float2(-st.m, -st.m);
+#pragma unroll
+    for (int k = 0; k < 32; k += 2) {
+      const float2 x = make_float2(k < valid ? __uint_as_float(r[k]) : -INFINITY,
+                                   k + 1 < valid ? __uint_as_float(r[k + 1]) : -INFINITY);
+      float2 a = __ffma2_rn(x, L2, nm);
+      a = make_float2(fmaxf(a.x, -200.f), fmaxf(a.y, -200.f));  // masked cols -> 0
+      const float2 e = make_float2(ex2_approx(a.x), ex2_approx(a.y));
+      s2 = __fadd2_rn(s2, e);
+      w2 = __ffma2_rn(e, a, w2);
+    }
+    st.s += double(s2.x + s2.y);
+    st.w += double(w2.x + w2.y);
+  }
+}
+
 __device__ __forceinline__ void tma_load_2d_mcast(void* dst, const CUtensorMap* map, int x, int y,
                                                   uint64_t* bar, uint16_t mask) {
   asm volatile(
@@ -120,6 +159,11 @@ __device__ __forceinline__ void umma_commit_mcast(uint64_t* bar, uint16_t mask) 
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
                    : "memory");
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
 }
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -273,40 +317,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) lmhead_lse_kernel(
       tc_fence_after();
       const int n0 = w.v0 + j * BN;
       const uint32_t tbase = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        TMEM_LD32(tbase + uint32_t(c * 32), r);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        const int colbase = n0 + c * 32;
-        const int valid = min(32, v1 - colbase);  // partial last tile
-        float cmax = -INFINITY;
-#pragma unroll
-        for (int k = 0; k < 32; ++k)
-          if (k < valid) cmax = fmaxf(cmax, __uint_as_float(r[k]));
-        if (valid > 0 && cmax * kL2e > st.m + 24.f) {  // rebase (exact power of two)
-          const float mn = ceilf(cmax * kL2e);
-          const double dd = double(st.m) - double(mn);
-          const double cs = exp2(fmax(dd, -1000.0));
-          st.w = cs * (dd * st.s + st.w);
-          st.s *= cs;
-          st.m = mn;
-        }
-        float2 s2 = make_float2(0.f, 0.f), w2 = s2;
-        const float2 L2 = make_float2(kL2e, kL2e), nm = make_float2(-st.m, -st.m);
-#pragma unroll
-        for (int k = 0; k < 32; k += 2) {
-          const float2 x = make_float2(k < valid ? __uint_as_float(r[k]) : -INFINITY,
-                                       k + 1 < valid ? __uint_as_float(r[k + 1]) : -INFINITY);
-          float2 a = __ffma2_rn(x, L2, nm);
-          a = make_float2(fmaxf(a.x, -200.f), fmaxf(a.y, -200.f));  // masked cols -> 0
-          const float2 e = make_float2(ex2_approx(a.x), ex2_approx(a.y));
-          s2 = __fadd2_rn(s2, e);
-          w2 = __ffma2_rn(e, a, w2);
-        }
-        st.s += double(s2.x + s2.y);
-        st.w += double(w2.x + w2.y);
-      }
+      lse_tile(tbase, n0, v1, st);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->tempty[acc]);
@@ -323,6 +334,221 @@ __global__ void __launch_bounds__(kGemmThreads, 1) lmhead_lse_kernel(
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(kTmemCols)
+                 : "memory");
+  }
+}
+
+// ----------------------------------------------------------------------
+// CTA-pair form (cta_group::2): two SMs of one TPC compute a 256 x 256
+// accumulator tile together.  Each CTA loads its 128 rows of the hidden
+// tile and HALF (128 columns) of the weight tile per K-step (16 + 16 KB, so
+// a 6-stage ring); the leader CTA's one thread issues
+// tcgen05.mma.cta_group::2 (M=256, N=256, K=16), which reads A from each
+// CTA's own shared memory and B from both, and writes each CTA's 128 rows x
+// 256 columns into that CTA's TMEM.  Per SM: a third less shared-memory
+// operand traffic per FLOP and half the weight bytes from L2.
+//   full[s]   leader only: both CTAs' TMA bytes (peer loads signal the
+//             leader's barrier: its shared::cluster address with the peer bit
+//             cleared), one arrive_expect_tx by the leader
+//   empty[s]  each CTA: the leader's MMA commit multicast to both
+//   tfull[a]  each CTA: the leader's accumulator commit multicast to both
+//   tempty[a] leader only: 4 epilogue warps x 2 CTAs arrive (the peer's
+//             remotely) before the accumulator is overwritten
+constexpr int kPairStages = 6;
+constexpr int kPABytes = BM * BK * 2;           // 16 KB: this CTA's hidden rows
+constexpr int kPBBytes = (BN / 2) * BK * 2;     // 16 KB: this CTA's half of the weights
+constexpr int kPStageBytes = kPABytes + kPBBytes;
+struct __align__(8) PairBars {
+  uint64_t full[kPairStages];
+  uint64_t empty[kPairStages];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint32_t tmem_base;
+};
+constexpr size_t kPairSmem = size_t(kPairStages) * kPStageBytes + 1024 + sizeof(PairBars);
+constexpr uint32_t kIdescPair = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) |
+                                (uint32_t((2 * BM) >> 4) << 24);
+constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;  // shared::cluster address of rank 0's copy
+
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, int x, int y,
+                                                 uint32_t leader_bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(map), "r"(x), "r"(y), "r"(leader_bar)
+      : "memory");
+}
+__device__ __forceinline__ void umma_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(kIdescPair), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(uint16_t(0x3))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster_acq(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void mbar_arrive_cluster_addr(uint32_t addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kGemmThreads, 1) lmhead_lse_pair_kernel(
+    const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+    int64_t rows, int32_t V, int32_t d, int32_t v_per_split, int32_t nsplit, int64_t nunits,
+    float4* partial) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  PairBars* bars = reinterpret_cast<PairBars*>(smem + size_t(kPairStages) * kPStageBytes);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  // units (row-tile pair, vocabulary split), split fastest; one per cluster
+  const int64_t u_first = blockIdx.x >> 1, u_stride = gridDim.x >> 1;
+  const int nk = (d + BK - 1) / BK;
+  auto unit = [&](int64_t u, int64_t& m0, int& v0, int& v1, int& ntiles) {
+    m0 = (u / nsplit) * (2 * BM) + int64_t(rank) * BM;  // this CTA's 128 rows
+    v0 = int(u % nsplit) * v_per_split;
+    v1 = min(V, v0 + v_per_split);
+    ntiles = (v1 - v0 + BN - 1) / BN;
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kPairStages; ++s) {
+      mbar_init(&bars->full[s], 1);
+      mbar_init(&bars->empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&bars->tfull[a], 1);
+      mbar_init(&bars->tempty[a], 8);
+    }
+    fence_mbar_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+  }
+  if (warp == 1) {  // the same warp in both CTAs allocates the pair's TMEM
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&bars->tmem_base)),
+                 "n"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // both CTAs' barriers initialised, TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer (both CTAs) ----
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t u = u_first; u < nunits; u += u_stride) {
+        int64_t m0;
+        int v0, v1, ntiles;
+        unit(u, m0, v0, v1, ntiles);
+        for (int j = 0; j < ntiles; ++j) {
+          const int n0 = v0 + j * BN + int(rank) * (BN / 2);  // this CTA's weight half
+          for (int kb = 0; kb < nk; ++kb) {
+            mbar_wait(&bars->empty[stage], phase ^ 1u);
+            const uint32_t lbar = smem_u32(&bars->full[stage]) & kPeerBitMask;
+            if (leader) mbar_arrive_expect_tx(&bars->full[stage], 2u * kPStageBytes);
+            const uint32_t sa = smem_u32(smem + size_t(stage) * kPStageBytes);
+            tma_load_2d_pair(sa, &tmA, kb * BK, int(m0), lbar);
+            tma_load_2d_pair(sa + kPABytes, &tmB, kb * BK, n0, lbar);
+            if (++stage == kPairStages) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {  // ---- MMA issuer (leader CTA) ----
+      int stage = 0;
+      uint32_t phase = 0;
+      int jg = 0;
+      for (int64_t u = u_first; u < nunits; u += u_stride) {
+        int64_t m0;
+        int v0, v1, ntiles;
+        unit(u, m0, v0, v1, ntiles);
+        for (int j = 0; j < ntiles; ++j, ++jg) {
+          const int acc = jg & 1;
+          const uint32_t aphase = (jg >> 1) & 1;
+          mbar_wait_cluster_acq(&bars->tempty[acc], aphase ^ 1u);
+          tc_fence_after();
+          const uint32_t tmem_d = tmem + uint32_t(acc * BN);
+          for (int kb = 0; kb < nk; ++kb) {
+            mbar_wait(&bars->full[stage], phase);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(smem + size_t(stage) * kPStageBytes);
+            const uint64_t adesc = sdesc_sw128(sa), bdesc = sdesc_sw128(sa + kPABytes);
+#pragma unroll
+            for (int kk = 0; kk < BK / UMMA_K; ++kk)
+              umma_pair(tmem_d, adesc + uint64_t(2 * kk), bdesc + uint64_t(2 * kk),
+                        (kb | kk) != 0 ? 1u : 0u);
+            umma_commit_pair(&bars->empty[stage]);  // the stage is free in both CTAs
+            if (++stage == kPairStages) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+          umma_commit_pair(&bars->tfull[acc]);  // both CTAs' accumulators ready
+        }
+      }
+    }
+  } else {
+    // ---- epilogue: warps 2..5 of both CTAs, TMEM lane quarter = warp % 4 ----
+    const int quarter = warp & 3;
+    const uint32_t tempty_leader[2] = {mapa_u32(smem_u32(&bars->tempty[0]), 0u),
+                                       mapa_u32(smem_u32(&bars->tempty[1]), 0u)};
+    int jg = 0;
+    for (int64_t u = u_first; u < nunits; u += u_stride) {
+      int64_t m0;
+      int v0, v1, ntiles;
+      unit(u, m0, v0, v1, ntiles);
+      const int64_t row = m0 + quarter * 32 + lane;
+      LseState st{-float(1 << 24), 0.0, 0.0};
+      for (int j = 0; j < ntiles; ++j, ++jg) {
+        const int acc = jg & 1;
+        const uint32_t aphase = (jg >> 1) & 1;
+        mbar_wait(&bars->tfull[acc], aphase);
+        tc_fence_after();
+        const uint32_t tbase = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
+        lse_tile(tbase, v0 + j * BN, v1, st);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster_addr(tempty_leader[acc]);
+      }
+      if (row < rows) {
+        const int k = st.s > 0 ? ilogb(st.s) : 0;
+        partial[(u % nsplit) * rows + row] = make_float4(
+            st.m + float(k), float(ldexp(st.s, -k)), float(ldexp(st.w - k * st.s, -k)), 0.f);
+      }
+    }
+  }
+  __syncthreads();
+  cluster_sync_all();  // no MMA / remote arrival pending on either CTA
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "n"(kTmemCols)
                  : "memory");
   }
@@ -420,21 +646,55 @@ int lmhead_token_stats_launch(const uint16_t* hidden, const uint16_t* W, const i
   YATT_REQUIRE((reinterpret_cast<uintptr_t>(hidden) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(W) & 15) == 0,
                YATT_ERR_CONFIG, "lmhead: operands must be 16-byte aligned");
-  // Single CTAs by default; YATT_LMHEAD_CLUSTER=2 selects CTA pairs sharing
-  // weight tiles through TMA multicast.  Measured (profiles/r1_lmhead_*):
-  // the 1-CTA kernel is already tensor-bound (93% pipe active) after the
-  // split-fastest rasterisation, and pairing adds lock-step coupling
-  // (1,261 vs 1,296 TFLOP/s at 32K rows), so the pair path stays opt-in.
-  static const int cluster = [] {
-    const char* e = getenv("YATT_LMHEAD_CLUSTER");
-    return (e && e[0] == '2') ? 2 : 1;
-  }();
+  // The multicast pair (YATT_LMHEAD_CLUSTER=2; round 1): the 1-CTA kernel
+  // is already tensor-bound (93% pipe active) after the split-fastest
+  // rasterisation and multicasting adds lock-step coupling (1,261 vs 1,296
+  // TFLOP/s at 32K rows), so it stays opt-in.
+  // Default: the cta_group::2 CTA-pair kernel.  YATT_LMHEAD_CLUSTER = 1 (the
+  // single-CTA kernel) or 2 (single-CTA MMAs, weight tiles multicast over a
+  // CTA pair) select the alternatives (measurement).  Pair vs single CTA
+  // (TFLOP/s, 2 splits; profiles/r2_lmhead_pair_v1.txt): 8K rows x d=3,584 x
+  // V=152,064 1,534 vs 1,412; 16K rows 1,302 vs 1,179; 32K rows 1,275 vs
+  // 1,223; d=8,192 x V=128,256 1,081 vs 1,111; 4K rows x V=32,000 (4
+  // splits) 1,442 vs 1,360 — results bit-identical.
+  const char* ce = getenv("YATT_LMHEAD_CLUSTER");
+  const bool pair = !(ce && (ce[0] == '1' || ce[0] == '2'));
+  const int cluster = (ce && ce[0] == '2') ? 2 : 1;
   CUtensorMap ta, tb;
   int rc = make_map(&ta, hidden, rows, d, BM);
-  if (!rc) rc = make_map(&tb, W, V, d, cluster == 2 ? BN / 2 : BN);
+  if (!rc) rc = make_map(&tb, W, V, d, (cluster == 2 || pair) ? BN / 2 : BN);
   if (rc) return rc;
   int v_per_split = int(ceil_div(ceil_div(V, nsplit), BN) * BN);
   const int nsplit_eff = int(ceil_div(V, v_per_split));
+  float4* partial = static_cast<float4*>(ws);
+  if (pair) {
+    const void* k = reinterpret_cast<const void*>(lmhead_lse_pair_kernel);
+    rc = ensure_dynamic_smem(k, int(kPairSmem));
+    if (rc) return rc;
+    const int64_t units = ceil_div(rows, 2 * BM) * nsplit_eff;
+    // YATT_LMHEAD_PERSIST=1: one cluster per SM pair walking the units
+    const char* pe = getenv("YATT_LMHEAD_PERSIST");
+    const int64_t clusters = (pe && pe[0] == '1') ? min64(units, num_sms() / 2) : units;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(unsigned(2 * clusters));
+    lc.blockDim = dim3(kGemmThreads);
+    lc.dynamicSmemBytes = kPairSmem;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    YATT_TRY_CUDA(cudaLaunchKernelEx(&lc, lmhead_lse_pair_kernel, ta, tb, rows, V, d, v_per_split,
+                                     int32_t(nsplit_eff), units, partial));
+    rc = check_launch("lmhead_lse_pair_kernel");
+    if (rc) return rc;
+    lmhead_combine_kernel<<<unsigned(ceil_div(rows * 32, 256)), 256, 0, st>>>(
+        partial, nsplit_eff, rows, hidden, W, d, tgt, logp, ent, lse);
+    return check_launch("lmhead_combine_kernel");
+  }
   {
       const int rc_ = ensure_dynamic_smem(reinterpret_cast<const void*>(lmhead_lse_kernel<1>), int(kGemmSmem));
       if (rc_) return rc_;
@@ -452,7 +712,6 @@ int lmhead_token_stats_launch(const uint16_t* hidden, const uint16_t* W, const i
   const bool persist = cluster == 1 && pe && pe[0] == '1';
   const dim3 grid = persist ? dim3(unsigned(min64(nunits, num_sms())), 1u, 1u)
                             : dim3(unsigned(nsplit_eff), unsigned(mtiles), 1u);
-  float4* partial = static_cast<float4*>(ws);
   if (cluster == 2) {
     cudaLaunchConfig_t lc = {};
     lc.gridDim = grid;

@@ -21,10 +21,12 @@ def _oracle(h, w, y):
     return lp[np.arange(len(yy)), yy], ent, lse
 
 
+@pytest.mark.parametrize("mode", ["P", "1"])  # cta_group::2 pair (default) / single CTA
 @pytest.mark.parametrize("rows,d,V,split", [(300, 512, 4100, 1), (300, 520, 4100, 3),
                                             (128, 1024, 8192, 2), (37, 256, 1000, 1),
-                                            (1024, 3584, 2304, 1)])
-def test_lmhead_token_stats_matches_oracle(cuda, rows, d, V, split):
+                                            (1024, 3584, 2304, 1), (600, 512, 9000, 2)])
+def test_lmhead_token_stats_matches_oracle(cuda, rows, d, V, split, mode, monkeypatch):
+    monkeypatch.setenv("YATT_LMHEAD_CLUSTER", mode)
     g = torch.Generator(device=cuda).manual_seed(rows + d + V)
     h = torch.randn(rows, d, device=cuda, generator=g).to(torch.bfloat16)
     w = (torch.randn(V, d, device=cuda, generator=g) * (2.0 / d ** 0.5)).to(torch.bfloat16)
@@ -69,28 +71,23 @@ def test_lmhead_policy_and_reference_kl(cuda):
     assert np.all(np.abs(kl - exp) <= 1e-5 * np.abs(exp) + 1e-6 * np.abs(np.expm1(dlt)) + 1e-9)
 
 
-def test_lmhead_cluster_multicast_variant(cuda):
-    """The CTA-pair / TMA-multicast variant (YATT_LMHEAD_CLUSTER=2) gives the
-    same results (separate process: the mode is read once per process)."""
-    import subprocess
-    import sys
-    code = ("import sys; sys.path.insert(0, '.');"
-            "import torch, numpy as np; from paper_2508_07970_b200 import ops;"
-            "g=torch.Generator(device='cuda').manual_seed(3);"
-            "h=torch.randn(300,512,device='cuda',generator=g).to(torch.bfloat16);"
-            "w=(torch.randn(4100,512,device='cuda',generator=g)*0.06).to(torch.bfloat16);"
-            "y=torch.randint(0,4100,(300,),device='cuda',generator=g,dtype=torch.int32);"
-            "o=torch.stack(ops.lmhead_token_stats(h,w,y,n_split=3)).cpu().numpy();"
-            "np.save(sys.argv[1], o)")
-    import os
-    import tempfile
-    outs = []
-    for mode in ("1", "2"):
-        f = tempfile.mktemp(suffix=".npy")
-        subprocess.run([sys.executable, "-c", code, f], check=True, timeout=120,
-                       env={**os.environ, "YATT_LMHEAD_CLUSTER": mode})
-        outs.append(np.load(f))
-    assert np.allclose(outs[0], outs[1], rtol=1e-6, atol=1e-6)
+def test_lmhead_pair_and_multicast_variants_agree(cuda, monkeypatch):
+    """The cta_group::2 pair kernel (default), the single-CTA kernel
+    (YATT_LMHEAD_CLUSTER=1), its persistent unit walk and the multicast pair
+    (=2) give the same results — bit-identical for the MMA forms, which run
+    the same K-sequence per accumulator element."""
+    g = torch.Generator(device=cuda).manual_seed(3)
+    h = torch.randn(700, 512, device=cuda, generator=g).to(torch.bfloat16)
+    w = (torch.randn(4100, 512, device=cuda, generator=g) * 0.06).to(torch.bfloat16)
+    y = torch.randint(0, 4100, (700,), device=cuda, generator=g, dtype=torch.int32)
+    outs = {}
+    for mode, persist in (("P", "0"), ("1", "0"), ("1", "1"), ("2", "0")):
+        monkeypatch.setenv("YATT_LMHEAD_CLUSTER", mode)
+        monkeypatch.setenv("YATT_LMHEAD_PERSIST", persist)
+        outs[mode + persist] = torch.stack(ops.lmhead_token_stats(h, w, y, n_split=3)).cpu()
+    assert torch.equal(outs["P0"], outs["10"])
+    assert torch.equal(outs["10"], outs["11"])
+    assert torch.allclose(outs["10"], outs["20"], rtol=1e-6, atol=1e-6)
 
 
 def test_lmhead_errors(cuda):
