@@ -517,8 +517,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1) lmhead_lse_pair_kernel(
   } else {
     // ---- epilogue: warps 2..5 of both CTAs, TMEM lane quarter = warp % 4 ----
     const int quarter = warp & 3;
-    const uint32_t tempty_leader[2] = {mapa_u32(smem_u32(&bars->tempty[0]), 0u),
-                                       mapa_u32(smem_u32(&bars->tempty[1]), 0u)};
     int jg = 0;
     for (int64_t u = u_first; u < nunits; u += u_stride) {
       int64_t m0;
@@ -535,7 +533,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) lmhead_lse_pair_kernel(
         lse_tile(tbase, v0 + j * BN, v1, st);
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster_addr(tempty_leader[acc]);
+        if (lane == 0) mbar_arrive_cluster_addr(mapa_u32(smem_u32(&bars->tempty[acc]), 0u));
       }
       if (row < rows) {
         const int k = st.s > 0 ? ilogb(st.s) : 0;

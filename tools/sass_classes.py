@@ -21,16 +21,18 @@ KERNELS = [  # (label, mangled-name substring)
     ("A1 token_stats k3 (large vocab)", "token_stats_cu_308a9ff918token_stats_kernelILb0ELb0E"),
     ("A1 token_stats full KL (large vocab)", "token_stats_cu_308a9ff918token_stats_kernelILb1ELb0E"),
     ("A1 token_stats k3 (small vocab)", "token_stats_small_cu_0a19fc3018token_stats_kernelILb0ELb0E"),
+    ("A1 token_stats_rowwarp k3 (V <= 36,864)", "token_stats_rowwarp_kernelILb0E"),
     ("8f#1 policy_loss_grad_pipe k3 (reverse pass 2)", "policy_loss_grad_pipe_kernelILb0ELi1E"),
     ("8f#1 policy_loss_grad_pipe full KL (reverse pass 2)", "policy_loss_grad_pipe_kernelILb1ELi1E"),
     ("8f#1 logits_backward k3", "logits_backward_kernelILb0E"),
-    ("8f#4 lmhead_lse (tcgen05)", "lmhead_lse_kernel"),
+    ("8f#4 lmhead_lse single CTA (tcgen05)", "lmhead_lse_kernelILi1E"),
+    ("8f#4 lmhead_lse_pair (tcgen05 cta_group::2)", "lmhead_lse_pair_kernel"),
     ("A3 gae_warp", "gae_warp_kernelILb0ELb0E"),
     ("A4 loss_token", "loss_token_kernelILb0E"),
 ]
 CLASSES = ["UBLKCP", "UTMALDG", "SYNCS", "MUFU.EX2", "FFMA2", "FADD2", "FMUL2", "HMNMX2",
            "VHMNMX", "F2FP", "LDS.128", "LDS", "STG.E.EF.128", "STG.E.128", "STG", "LDG",
-           "UTCHMMA", "LDTM", "DFMA", "STL", "LDL"]
+           "UTCHMMA", "UTCBAR", "LDTM", "DFMA", "STL", "LDL"]
 
 
 def main():
