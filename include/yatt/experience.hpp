@@ -174,6 +174,8 @@ void policy_loss_grad(const std::uint16_t* policy_logits, const std::uint16_t* r
 // ---- fused LM head + online log-softmax (tcgen05; §8f #4) -------------------
 // logp / entropy / lse per row of softmax(hidden @ lm_head^T) without writing
 // the logits; hidden [rows, hidden_dim], lm_head [vocab, hidden_dim] bf16.
+// n_split: vocabulary splits (1..64), 0 = the library picks (pass the same
+// value to lmhead_workspace_bytes).
 std::size_t lmhead_workspace_bytes(std::int64_t rows, int vocab, int n_split);
 void lmhead_token_stats(const std::uint16_t* hidden, const std::uint16_t* lm_head,
                         const std::int32_t* targets, std::int64_t rows, int hidden_dim, int vocab,

@@ -430,7 +430,8 @@ int yatt_grpo_step_host(const uint16_t* h_policy_logits,
 /* accumulate in TMEM) are never materialised; per row writes               */
 /* logp (target log-prob), entropy and lse (any output but logp may be      */
 /* NULL).  n_split splits the vocabulary across CTAs (1..64) to fill the    */
-/* GPU when rows are few; hidden % 8 == 0; operands 16-byte aligned.         */
+/* GPU when rows are few (0: the library picks; pass the same value to      */
+/* yatt_lmhead_workspace_bytes); hidden % 8 == 0; operands 16-B aligned.     */
 /* Run once per model (policy, reference) then yatt_kl_from_logps.           */
 /* ------------------------------------------------------------------------ */
 size_t yatt_lmhead_workspace_bytes(int64_t rows, int32_t vocab, int32_t n_split);

@@ -625,7 +625,16 @@ int make_map(CUtensorMap* map, const void* base, int64_t rows, int32_t d, int bo
 
 }  // namespace
 
+// n_split = 0: the library picks — few splits keep the weight stream shared
+// in L2, enough to fill the SMs when rows are few (tools/lmhead_sweep.py).
+int32_t lmhead_auto_split(int64_t rows, int32_t nsplit) {
+  if (nsplit != 0) return nsplit;
+  const int64_t tiles = ceil_div(rows > 0 ? rows : 1, BM);
+  return int32_t(min64(64, max64(2, num_sms() / tiles)));
+}
+
 size_t lmhead_workspace_bytes(int64_t rows, int32_t V, int32_t nsplit) {
+  nsplit = lmhead_auto_split(rows, nsplit);
   (void)V;
   return size_t(rows) * size_t(nsplit > 0 ? nsplit : 1) * sizeof(float4);
 }
@@ -636,7 +645,8 @@ int lmhead_token_stats_launch(const uint16_t* hidden, const uint16_t* W, const i
                               cudaStream_t st) {
   YATT_REQUIRE(rows >= 0 && d > 0 && V > 0, YATT_ERR_CONFIG, "lmhead: bad sizes");
   YATT_REQUIRE(d % 8 == 0, YATT_ERR_CONFIG, "lmhead: hidden size must be a multiple of 8");
-  YATT_REQUIRE(nsplit >= 1 && nsplit <= 64, YATT_ERR_CONFIG, "lmhead: nsplit in [1, 64]");
+  nsplit = lmhead_auto_split(rows, nsplit);
+  YATT_REQUIRE(nsplit >= 1 && nsplit <= 64, YATT_ERR_CONFIG, "lmhead: nsplit in [0, 64]");
   if (rows == 0) return YATT_OK;
   YATT_REQUIRE(hidden && W && tgt && logp, YATT_ERR_CONFIG, "lmhead: null pointer");
   YATT_REQUIRE(ws && ws_bytes >= lmhead_workspace_bytes(rows, V, nsplit), YATT_ERR_WORKSPACE,

@@ -461,10 +461,8 @@ def lmhead_token_stats(hidden: torch.Tensor, lm_head: torch.Tensor, targets: tor
     _dev(targets, torch.int32, "targets")
     rows, d = hidden.shape
     vocab = lm_head.shape[0]
-    if n_split is None:  # measured (tools/lmhead_sweep.py): few splits keep the weight
-        # stream shared in L2; enough splits to fill the SMs when rows are few
-        sms = torch.cuda.get_device_properties(hidden.device).multi_processor_count
-        n_split = min(64, max(2, sms // max(1, -(-rows // 128))))
+    if n_split is None:
+        n_split = 0  # the library picks (yatt_lmhead_token_stats)
     if out is None:
         out = torch.empty((3, rows), dtype=torch.float32, device=hidden.device)
     wsb = lib().yatt_lmhead_workspace_bytes(rows, vocab, n_split)
