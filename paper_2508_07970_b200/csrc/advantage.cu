@@ -247,8 +247,11 @@ __global__ void gae_mark_ends_kernel(const int64_t* cu, int64_t nseq, int64_t n_
 #endif
 // kMom: also the masked moments (count, sum, sum^2) of the advantages it
 // stores, one fp64 partial per tile (whitening without a second pass).
+// (The scalar-load form for unaligned views keeps 4 CTAs/SM: at 6 its extra
+// address registers spilled.)
 template <bool kVec, bool kMom>
-__global__ void __launch_bounds__(128, YATT_GAE_MINB) gae_warp_kernel(const GaeArgs g, GaeWs ws) {
+__global__ void __launch_bounds__(128, kVec ? YATT_GAE_MINB : 4) gae_warp_kernel(const GaeArgs g,
+                                                                                 GaeWs ws) {
   const int lane = threadIdx.x & 31;
   const double gamma = g.gamma, gl = g.gamma * g.lam;
   int64_t t = 0;

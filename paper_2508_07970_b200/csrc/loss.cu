@@ -79,8 +79,9 @@ __device__ __forceinline__ void add_token(const LossIn& in, int64_t i, const Los
 // Four tokens [4j, 4j+4) from 16-byte loads (float inputs 16-B aligned, mask
 // 4-B aligned).
 struct Vec4 {
-  float4 lp, olp, a, kl, h;
-  uint32_t m;
+  float4 lp, olp, a;
+  float k4, h4;  // masked kl / H sums of the four tokens, formed at load time so
+  uint32_t m;    // two vectors in flight fit the 64-register cap without spills
 };
 __device__ __forceinline__ Vec4 load_vec(const LossIn& in, int64_t j) {
   Vec4 x;
@@ -88,25 +89,28 @@ __device__ __forceinline__ Vec4 load_vec(const LossIn& in, int64_t j) {
   x.lp = ldg4(in.logp, i);
   x.olp = ldg4(in.old_logp, i);
   x.a = ldg4(in.adv, i);
-  x.kl = in.kl ? ldg4(in.kl, i) : make_float4(0.f, 0.f, 0.f, 0.f);
-  x.h = in.ent ? ldg4(in.ent, i) : make_float4(0.f, 0.f, 0.f, 0.f);
   x.m = in.mask ? __ldg(reinterpret_cast<const uint32_t*>(in.mask + i)) : 0x01010101u;
+  const float4 kl = in.kl ? ldg4(in.kl, i) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 h = in.ent ? ldg4(in.ent, i) : make_float4(0.f, 0.f, 0.f, 0.f);
+  // same order and rounding as the per-token loop it replaces: ((0 + t0) + t1) + ...
+  x.k4 = 0.f;
+  x.h4 = 0.f;
+  if (x.m & 0xffu) x.k4 += kl.x, x.h4 += h.x;
+  if ((x.m >> 8) & 0xffu) x.k4 += kl.y, x.h4 += h.y;
+  if ((x.m >> 16) & 0xffu) x.k4 += kl.z, x.h4 += h.z;
+  if (x.m >> 24) x.k4 += kl.w, x.h4 += h.w;
   return x;
 }
 __device__ __forceinline__ void add_vec(const Vec4& x, const LossCfg& c, Acc& s) {
   const float lp[4] = {x.lp.x, x.lp.y, x.lp.z, x.lp.w}, olp[4] = {x.olp.x, x.olp.y, x.olp.z, x.olp.w};
-  const float a[4] = {x.a.x, x.a.y, x.a.z, x.a.w}, kl[4] = {x.kl.x, x.kl.y, x.kl.z, x.kl.w};
-  const float h[4] = {x.h.x, x.h.y, x.h.z, x.h.w};
-  float k4 = 0.f, h4 = 0.f;
+  const float a[4] = {x.a.x, x.a.y, x.a.z, x.a.w};
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     if (((x.m >> (8 * k)) & 0xffu) == 0) continue;
     pg_term(lp[k], olp[k], a[k], c, s);
-    k4 += kl[k];
-    h4 += h[k];
   }
-  s.kl += double(k4);
-  s.ent += double(h4);
+  s.kl += double(x.k4);
+  s.ent += double(x.h4);
 }
 
 // Block-wide sum of kFields doubles; result valid in thread 0.
@@ -180,7 +184,10 @@ __global__ void __launch_bounds__(kThreads, YATT_LOSS_MINB) loss_token_kernel(co
 // fields accumulate per thread.  Vector path: scalar head up to the first
 // 4-aligned token, 16-byte body (two vectors in flight), scalar tail.
 template <bool kVec>
-__global__ void __launch_bounds__(kThreads, YATT_LOSS_MINB) loss_seq_kernel(const LossIn in, const int64_t* cu,
+#ifndef YATT_LOSS_SEQ_MINB  // the per-sequence kernel keeps more state live
+#define YATT_LOSS_SEQ_MINB 3
+#endif
+__global__ void __launch_bounds__(kThreads, YATT_LOSS_SEQ_MINB) loss_seq_kernel(const LossIn in, const int64_t* cu,
                                                             int64_t nseq,
                                                             const yatt_loss_config cfg,
                                                             double* part) {
@@ -189,8 +196,9 @@ __global__ void __launch_bounds__(kThreads, YATT_LOSS_MINB) loss_seq_kernel(cons
   const LossCfg c = loss_cfg(cfg);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const double beta = cfg.kl_coef, ec = cfg.entropy_coef;
-  Acc tot;
+  Acc tot;  // ratio / clip per thread; pg / kl / H / count from the block totals
   double loss = 0.0, seqs = 0.0;  // thread 0 only
+  double t_pg = 0.0, t_kl = 0.0, t_ent = 0.0, t_cnt = 0.0;  // thread 0 only
   for (int64_t sq = blockIdx.x; sq < nseq; sq += gridDim.x) {
     const int64_t b = __ldg(cu + sq), e = __ldg(cu + sq + 1);
     Acc s;
@@ -227,14 +235,20 @@ __global__ void __launch_bounds__(kThreads, YATT_LOSS_MINB) loss_seq_kernel(cons
         loss += cfg.agg_mode == 1 ? Ls / t[3] : Ls;
         seqs += 1.0;
       }
+      t_pg += t[0];
+      t_kl += t[1];
+      t_ent += t[2];
+      t_cnt += t[3];
     }
     __syncthreads();
-    tot.pg += s.pg;
-    tot.kl += s.kl;
-    tot.ent += s.ent;
-    tot.ratio += s.ratio;
+    tot.ratio += s.ratio;  // (fewer live doubles: no spills at the 64-register cap)
     tot.clip += s.clip;
-    tot.cnt += s.cnt;
+  }
+  if (threadIdx.x == 0) {
+    tot.pg = t_pg;
+    tot.kl = t_kl;
+    tot.ent = t_ent;
+    tot.cnt = int32_t(t_cnt);
   }
   emit_part(tot, loss, seqs, cfg, false, red, part);
 }

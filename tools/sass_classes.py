@@ -27,7 +27,8 @@ KERNELS = [  # (label, mangled-name substring)
     ("8f#1 logits_backward k3", "logits_backward_kernelILb0E"),
     ("8f#4 lmhead_lse single CTA (tcgen05)", "lmhead_lse_kernelILi1E"),
     ("8f#4 lmhead_lse_pair (tcgen05 cta_group::2)", "lmhead_lse_pair_kernel"),
-    ("A3 gae_warp", "gae_warp_kernelILb0ELb0E"),
+    ("A3 gae_warp (16-B loads)", "gae_warp_kernelILb1ELb0E"),
+    ("A3 gae_warp (scalar loads, unaligned views)", "gae_warp_kernelILb0ELb0E"),
     ("A4 loss_token", "loss_token_kernelILb0E"),
 ]
 CLASSES = ["UBLKCP", "UTMALDG", "SYNCS", "MUFU.EX2", "FFMA2", "FADD2", "FMUL2", "HMNMX2",
