@@ -703,14 +703,9 @@ int lmhead_token_stats_launch(const uint16_t* hidden, const uint16_t* W, const i
         partial, nsplit_eff, rows, hidden, W, d, tgt, logp, ent, lse);
     return check_launch("lmhead_combine_kernel");
   }
-  {
-      const int rc_ = ensure_dynamic_smem(reinterpret_cast<const void*>(lmhead_lse_kernel<1>), int(kGemmSmem));
-      if (rc_) return rc_;
-    }
-    {
-      const int rc_ = ensure_dynamic_smem(reinterpret_cast<const void*>(lmhead_lse_kernel<2>), int(kGemmSmem));
-      if (rc_) return rc_;
-    }
+  rc = ensure_dynamic_smem(reinterpret_cast<const void*>(lmhead_lse_kernel<1>), int(kGemmSmem));
+  if (!rc) rc = ensure_dynamic_smem(reinterpret_cast<const void*>(lmhead_lse_kernel<2>), int(kGemmSmem));
+  if (rc) return rc;
   const int64_t mtiles = ceil_div(ceil_div(rows, BM), cluster) * cluster;
   YATT_REQUIRE(mtiles <= 65535, YATT_ERR_CONFIG, "lmhead: too many rows per launch");
   const int64_t nunits = mtiles * nsplit_eff;
