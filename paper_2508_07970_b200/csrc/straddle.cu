@@ -116,20 +116,30 @@ int grpo_merge_launch(double* mom, int64_t n, uint64_t first_id, int32_t G, cons
 
 using namespace yattb;
 
+#define STRADDLE_ALIGNED(fn, ptr, a)                                                      \
+  YATT_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & uintptr_t((a) - 1)) == 0, YATT_ERR_CONFIG, \
+               "%s: %s must be %d-byte aligned", fn, #ptr, int(a))
+
 extern "C" {
 
 int yatt_grpo_boundary_record(const double* d_moments, int64_t n, uint64_t first_id, int32_t G,
                               double* d_record, void* stream) {
+  STRADDLE_ALIGNED("grpo_boundary_record", d_moments, 8);
+  STRADDLE_ALIGNED("grpo_boundary_record", d_record, 8);
   return grpo_record_launch(d_moments, n, first_id, G, d_record, as_stream(stream));
 }
 
 int yatt_grpo_merge_boundaries(double* d_moments, int64_t n, uint64_t first_id, int32_t G,
                                const double* d_all_records, int32_t world, void* stream) {
+  STRADDLE_ALIGNED("grpo_merge_boundaries", d_moments, 8);
+  STRADDLE_ALIGNED("grpo_merge_boundaries", d_all_records, 8);
   return grpo_merge_launch(d_moments, n, first_id, G, d_all_records, world, as_stream(stream));
 }
 
 int yatt_filter_boundary_record(const float* d_rewards, int64_t n, uint64_t first_id, int32_t G,
                                 int64_t* d_record, void* stream) {
+  STRADDLE_ALIGNED("filter_boundary_record", d_rewards, 4);
+  STRADDLE_ALIGNED("filter_boundary_record", d_record, 8);
   return filter_record_launch(d_rewards, n, first_id, G, d_record, as_stream(stream));
 }
 
@@ -147,6 +157,9 @@ int yatt_peer_world(yatt_peer_t p, int32_t* world, int32_t* rank);
 int yatt_peer_grpo_advantages(yatt_peer_t p, const float* d_rewards, int64_t n,
                               uint64_t first_id, int32_t G, float eps, int32_t norm_by_std,
                               float* d_adv, void* d_ws, size_t ws_bytes, void* stream) {
+  STRADDLE_ALIGNED("peer_grpo_advantages", d_rewards, 4);
+  STRADDLE_ALIGNED("peer_grpo_advantages", d_adv, 4);
+  STRADDLE_ALIGNED("peer_grpo_advantages", d_ws, 8);
   int32_t world = 0, rank = 0;
   int rc = yatt_peer_world(p, &world, &rank);
   if (rc) return rc;
@@ -171,6 +184,12 @@ int yatt_peer_filter_compact(yatt_peer_t p, const float* d_rewards, const int64_
                              int64_t n, uint64_t first_id, int32_t G, uint8_t* d_keep,
                              int32_t* d_map, int64_t* d_new_cu, int64_t* d_counts, void* d_ws,
                              size_t ws_bytes, void* stream) {
+  STRADDLE_ALIGNED("peer_filter_compact", d_rewards, 4);
+  STRADDLE_ALIGNED("peer_filter_compact", d_lens, 8);
+  STRADDLE_ALIGNED("peer_filter_compact", d_map, 4);
+  STRADDLE_ALIGNED("peer_filter_compact", d_new_cu, 8);
+  STRADDLE_ALIGNED("peer_filter_compact", d_counts, 8);
+  STRADDLE_ALIGNED("peer_filter_compact", d_ws, 8);
   int32_t world = 0, rank = 0;
   int rc = yatt_peer_world(p, &world, &rank);
   if (rc) return rc;

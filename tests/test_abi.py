@@ -101,6 +101,13 @@ def test_misaligned_pointers_are_config_errors_before_any_launch():
         ("out", lambda: lib().yatt_token_stats(A, A, A, None, 1, 8, 2, A, A, A + 1, A, None)),
         ("ws", lambda: lib().yatt_lmhead_token_stats(A, A, A, 1, 64, 8, 1, A, A, A, A + 8, 64,
                                                      None)),
+        ("d_record", lambda: lib().yatt_grpo_boundary_record(A, 8, 0, 8, A + 4, None)),
+        ("d_all_records", lambda: lib().yatt_grpo_merge_boundaries(A, 8, 0, 8, A + 4, 2, None)),
+        ("d_rewards", lambda: lib().yatt_filter_boundary_record(M, 8, 0, 8, A, None)),
+        ("d_ws", lambda: lib().yatt_peer_grpo_advantages(None, A, 8, 0, 8, 1e-6, 1, A, A + 4, 4096,
+                                                         None)),
+        ("d_new_cu", lambda: lib().yatt_peer_filter_compact(None, A, A, 8, 0, 8, A, A, A + 4, A, A,
+                                                            4096, None)),
     ]
     for what, fn in calls:
         with pytest.raises(ConfigError, match="aligned"):
