@@ -304,6 +304,30 @@ def test_reference_runner_traces_byte_identical(cuda, tmp_path):
         assert a == b, f"{f} differs"
 
 
+def test_reference_acceptance_suite_passes_against_b200_library(cuda):
+    """The reference's scenario-level suites compiled unchanged — its 11
+    acceptance criteria (acceptance_test.cpp: :64 rollout totals across
+    rejection rates, :130 swap-count law, :371 balancer waste and bias, :609
+    byte-identical traces, ...) plus runner_test, controller_test and
+    scenario_test, 38 TESTs — with the on-path functions (run_rlhf_step ->
+    every round of every shard, sort_and_bucket, sample_length_keyed, ...)
+    from the drop-in (oracle/Makefile accept_b200).  Each criterion's report
+    line equals the reference-only build's (accept_ref) once wall-clock
+    seconds are masked."""
+    import re
+    outs = {}
+    for k in ("ref", "b200"):
+        exe = ROOT / "oracle" / "_ref" / f"accept_{k}"
+        assert exe.exists(), "build with `make -C oracle ref` (done by __graft_entry__.build)"
+        res = subprocess.run([str(exe)], capture_output=True, text=True, timeout=900)
+        assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+        assert "38 tests, 0 failed" in res.stdout
+        outs[k] = [re.sub(r"\d+\.\d+ s\b", "<t> s", ln) for ln in res.stdout.splitlines()
+                   if ln.startswith("[CRITERION")]
+    assert len(outs["b200"]) == 11 and all("] PASS - " in ln for ln in outs["b200"]), outs["b200"]
+    assert outs["b200"] == outs["ref"]
+
+
 # ---------------------------------------------------------------- R10 ----
 def test_sort_order_matches_oracle(cuda):
     rng = np.random.default_rng(0)
