@@ -6,8 +6,10 @@
 // with << message streaming, and ::testing::Test::HasFailure().
 #pragma once
 
+#include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <functional>
 #include <iostream>
 #include <sstream>
@@ -76,10 +78,16 @@ inline bool almost_equal(double a, double b) {
   return d <= 4 * 2.220446049250313e-16 * std::fmax(std::fabs(a), std::fabs(b));
 }
 
+// GTEST_FILTER=<substring>: run only the tests whose "Suite.Name" contains it.
 inline int RunAllTests() {
   int failed = 0;
+  size_t ran = 0;
+  const char* filter = std::getenv("GTEST_FILTER");
   for (auto& c : Registry::get().cases) {
+    if (filter && c.name.find(filter) == std::string::npos) continue;
+    ++ran;
     Registry::get().current_failed = false;
+    const auto t0 = std::chrono::steady_clock::now();
     try {
       c.fn();
     } catch (const Fatal&) {
@@ -87,11 +95,13 @@ inline int RunAllTests() {
       Registry::get().current_failed = true;
       std::cerr << "uncaught exception: " << e.what() << "\n";
     }
-    std::printf("[%s] %s\n", Registry::get().current_failed ? "  FAILED  " : "       OK ",
-                c.name.c_str());
+    const double ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    std::printf("[%s] %s (%.1f ms)\n", Registry::get().current_failed ? "  FAILED  " : "       OK ",
+                c.name.c_str(), ms);
     failed += Registry::get().current_failed ? 1 : 0;
   }
-  std::printf("%zu tests, %d failed\n", Registry::get().cases.size(), failed);
+  std::printf("%zu tests, %d failed\n", ran, failed);
   return failed ? 1 : 0;
 }
 
