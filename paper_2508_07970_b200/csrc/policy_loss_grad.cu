@@ -545,9 +545,9 @@ int policy_loss_grad_launch(const uint16_t* pol, const uint16_t* ref, const int3
   YATT_REQUIRE(p.V > 0 && p.rows >= 0, YATT_ERR_CONFIG, "policy_loss_grad: bad shape");
   YATT_REQUIRE(p.kl_mode >= YATT_KL_K1 && p.kl_mode <= YATT_KL_FULL, YATT_ERR_CONFIG,
                "policy_loss_grad: unknown kl_mode %d", p.kl_mode);
+  if (p.rows == 0) return YATT_OK;  // (an empty tensor's data pointer may be null)
   YATT_REQUIRE(p.kl_mode != YATT_KL_FULL || p.ref != nullptr, YATT_ERR_CONFIG,
                "policy_loss_grad: the full-vocabulary KL needs the reference logits");
-  if (p.rows == 0) return YATT_OK;
   YATT_REQUIRE(p.pol && p.tgt && p.old_logp && p.adv && p.logp && p.grad, YATT_ERR_CONFIG,
                "policy_loss_grad: null pointer");
   // V % 8 != 0: a row's aligned staging superset can end past the tensor on
