@@ -9,6 +9,10 @@ sampled rows / the full arrays where the C oracle is fast enough.
   with which CTA it ran).
 * GAE over configs[3]'s 2,048 packed sequences (~8.4M tokens) vs the oracle.
 * A4 over the same ~8.4M tokens vs the oracle, all three aggregations.
+* The fused loss + gradient (§8f#1) over the same bench chunk (k3 and the
+  full-vocabulary KL; gradient offsets past 2^31 elements): per-token terms
+  equal A1's to the 1e-5 bar, 8 sampled gradient rows vs the fp64 oracle
+  backward, bit-exact row permutation equivariance.
 """
 import numpy as np
 import pytest
@@ -81,3 +85,71 @@ def test_policy_loss_full_token_count(cuda, agg):
     exp = O.policy_loss(*(t.cpu().numpy() for t in (logp, old, adv, kl, ent)),
                         mask.cpu().numpy(), cu, 0.2, 0.28, 3.0, 0.01, 0.001, ops.AGG_MODES[agg])
     assert O.max_rel_error(got, exp) <= TOL
+
+
+def _bf16_np(t):
+    return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def _to_f64(bits):
+    return (bits.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+@pytest.mark.parametrize("kl_mode", ["k3", "full"])
+def test_fused_loss_grad_full_bench_chunk(cuda, kl_mode):
+    rows, V = 32768, 152064
+    full = kl_mode == "full"
+    pol, ref, tgt = ops.synth_logits(SEED, 0, rows, V, device=cuda)
+    lp1, rl1, ent1, kl1 = ops.token_stats(pol, ref, tgt, None, "full" if full else "k3")
+    old = ops.synth_floats(SEED, 104, 0, rows, "old_delta", base=lp1, device=cuda)
+    adv = ops.synth_floats(SEED, 108, 0, rows, "adv", device=cuda)
+    cfg = ops.loss_config(0.2, 0.28, 0.0, 0.05, 0.01, "token-mean")
+    args = dict(config=cfg, kl_mode=kl_mode, norm=float(rows),
+                ref_logits=ref if full else None)
+    lp, ent, kl, grad = ops.policy_loss_grad(pol, tgt, old, adv, None if full else rl1, None,
+                                             **args)
+    torch.cuda.synchronize()
+    # per-token terms: A1's (parity-checked against the oracle) to the 1e-5 bar
+    assert O.max_rel_error(lp.cpu().numpy(), lp1.cpu().numpy().astype(np.float64)) <= TOL
+    assert O.max_rel_error(ent.cpu().numpy(), ent1.cpu().numpy().astype(np.float64)) <= TOL
+    if full:
+        assert O.max_rel_error(kl.cpu().numpy(), kl1.cpu().numpy().astype(np.float64)) <= TOL
+    assert bool(torch.isfinite(grad.float()[:: rows // 64]).all())
+    # 8 sampled gradient rows (incl. the last: offsets past 2^31) vs the oracle
+    idx = np.sort(np.concatenate([np.random.default_rng(2).choice(rows - 1, 7, replace=False),
+                                  [rows - 1]]))
+    sel = torch.as_tensor(idx, device=cuda)
+    hp, hr = _bf16_np(pol.index_select(0, sel)), _bf16_np(ref.index_select(0, sel))
+    ht = tgt.index_select(0, sel).cpu().numpy()
+    e_lp = O.token_stats(hp, hr, ht, None, "k3")[0]
+    s_rl = rl1.index_select(0, sel).cpu().numpy().astype(np.float64)  # the stored ref log-probs
+    eg, ecoef = O.logits_backward(hp, hr, ht, e_lp, None if full else s_rl,
+                                  old.index_select(0, sel).cpu().numpy(),
+                                  adv.index_select(0, sel).cpu().numpy(), None, None, 0.2, 0.28,
+                                  0.0, 0.05, 0.01, ops.AGG_MODES["token-mean"], kl_mode,
+                                  float(rows))
+    got = _to_f64(_bf16_np(grad.index_select(0, sel)))
+    x = _to_f64(hp)
+    lpv = x - ecoef[:, 3:4]
+    p = np.exp(lpv)
+    H = -(p * lpv).sum(1, keepdims=True)
+    cond = np.abs(ecoef[:, 0:1]) + np.abs(ecoef[:, 1:2]) * (np.abs(lpv) + H)
+    if full:
+        z = _to_f64(hr)
+        zm = z.max(1, keepdims=True)
+        lq = z - (zm + np.log(np.exp(z - zm).sum(1, keepdims=True)))
+        cond = cond + np.abs(ecoef[:, 2:3]) * (np.abs(lpv) + np.abs(lq) + 1.0)
+    tol = 2.0 ** -8 * np.abs(eg) + 1e-5 * p * cond + 1e-30
+    tol[np.arange(len(idx)), ht] += 1e-5 * np.abs(ecoef[:, 0])
+    bad = np.abs(got - eg) > tol
+    assert not bad.any(), (np.argwhere(bad)[:5], got[bad][:5], eg[bad][:5])
+    # bit-exact row permutation equivariance on 2,048 rows
+    perm = torch.randperm(rows, generator=torch.Generator().manual_seed(4))[:2048].to(cuda)
+    out2 = ops.policy_loss_grad(pol.index_select(0, perm), tgt.index_select(0, perm),
+                                old.index_select(0, perm), adv.index_select(0, perm),
+                                None if full else rl1.index_select(0, perm), None,
+                                **{**args, "ref_logits": ref.index_select(0, perm) if full
+                                   else None})
+    for a, b in zip(out2, (lp, ent, kl, grad)):
+        assert torch.equal(a, b.index_select(0, perm))
+    del pol, ref, grad
