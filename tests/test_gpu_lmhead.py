@@ -95,3 +95,44 @@ def test_lmhead_errors(cuda):
     w = torch.zeros((16, 12), dtype=torch.bfloat16, device=cuda)
     with pytest.raises(ConfigError):
         ops.lmhead_token_stats(h, w, torch.zeros(4, dtype=torch.int32, device=cuda))
+
+
+def test_lmhead_qwen_head_full_size(cuda):
+    """The bench shape of §8f #4: 8,192 rows x d=3,584 x V=152,064 (the
+    Qwen2.5-7B head, 64 row tiles x the library's vocabulary split), 16
+    sampled rows (incl. the last tile) against the fp64 GEMM oracle,
+    computed over the vocabulary in chunks."""
+    rows, d, V = 8192, 3584, 152064
+    g = torch.Generator(device=cuda).manual_seed(11)
+    h = torch.randn(rows, d, device=cuda, generator=g).to(torch.bfloat16)
+    w = (torch.randn(V, d, device=cuda, generator=g) * (2.0 / d ** 0.5)).to(torch.bfloat16)
+    y = torch.randint(0, V, (rows,), device=cuda, generator=g, dtype=torch.int32)
+    logp, ent, lse = ops.lmhead_token_stats(h, w, y)
+    torch.cuda.synchronize()
+    idx = np.sort(np.concatenate([np.random.default_rng(0).choice(rows - 1, 15, replace=False),
+                                  [rows - 1]]))
+    sel = torch.as_tensor(idx, device=cuda)
+    hs = h.index_select(0, sel).double().cpu().numpy()
+    logits = np.empty((len(idx), V))
+    logits32 = np.empty((len(idx), V))
+    for v0 in range(0, V, 16384):
+        wc = w[v0:v0 + 16384]
+        logits[:, v0:v0 + wc.shape[0]] = hs @ wc.double().cpu().numpy().T
+        logits32[:, v0:v0 + wc.shape[0]] = torch.mm(h.index_select(0, sel), wc.t(),
+                                                    out_dtype=torch.float32).double().cpu().numpy()
+
+    def stats(lg):
+        mx = lg.max(1, keepdims=True)
+        ls = mx[:, 0] + np.log(np.exp(lg - mx).sum(1))
+        lp = lg - ls[:, None]
+        return lp[np.arange(len(idx)), y.cpu().numpy()[idx]], -(np.exp(lp) * lp).sum(1), ls
+
+    e_lp, e_ent, e_lse = stats(logits)
+    assert O.max_rel_error(logp.cpu().numpy()[idx], e_lp) <= 1e-5
+    assert O.max_rel_error(lse.cpu().numpy()[idx], e_lse) <= 1e-5
+    # entropy at K = 3,584: the long-K bar of the test above (cuBLAS's own
+    # fp32-accumulated GEMM of the same operands as the yardstick)
+    err = O.max_rel_error(ent.cpu().numpy()[idx], e_ent)
+    ref_err = O.max_rel_error(stats(logits32)[1], e_ent)
+    assert err <= max(1.25 * ref_err, 1e-5) and err <= 5e-5, (err, ref_err)
+    assert bool(torch.isfinite(logp).all()) and bool((logp <= 0).all())
