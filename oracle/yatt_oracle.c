@@ -11,11 +11,15 @@
  * known-answer tests — see tests/golden/ and tests/test_oracle_*.py.
  *
  * Float path (A1-A4): the reference has NO implementation of these (SURVEY.md
- * §0.2, §8c: "parity unpinned" by the reference).  They are restated here
- * from the standard GRPO / PPO / DAPO definitions, in fp64 with the
- * reference's numerics convention (two-pass max-subtracted softmax,
- * proj/src/distattn.cpp:99-123) and cross-checked against an independent
- * second implementation (torch fp64, tests/test_oracle_float.py).
+ * §0.2, §8c).  They are restated here from the standard GRPO / PPO / DAPO
+ * definitions, in fp64 with the reference's numerics convention (two-pass
+ * max-subtracted softmax, proj/src/distattn.cpp:99-123) and cross-checked
+ * against an independent second implementation (torch fp64,
+ * tests/test_oracle_float.py).  A1 (logp / ref_logp / entropy / every KL
+ * mode) is PINNED to the reference's own fp64 softmax: one
+ * distattn::reference_attention head per token row (oracle/softmax_pin.cpp,
+ * tests/golden/softmax_pin.json) agrees to 1e-12.  GRPO, GAE and the loss
+ * have no reference counterpart at all: "parity unpinned" for A2-A4.
  *
  * Conventions (never changed silently; mirrored in DESIGN.md):
  *   entropy   H = -sum_v p_v log p_v (nats)

@@ -116,3 +116,41 @@ def test_filter_compact_oracle_semantics():
     # -0.0 and 0.0 differ bitwise: a group mixing them is kept (bitwise rule)
     r2 = np.array([0.0, -0.0, 0.0, 0.0], dtype=np.float32)
     assert O.filter_compact(r2, lens[:4], 4)["keep_groups"].tolist() == [1]
+
+
+def test_token_stats_oracle_pinned_to_reference_softmax():
+    """The oracle's A1 quantities against the reference's OWN fp64 softmax
+    (yatt::distattn::reference_attention, distattn.cpp:79-123, run here by
+    oracle/softmax_pin.cpp; tests/golden/softmax_pin.json from
+    oracle/softmax_golden.py): one attention head per token row whose scores
+    are the logits gives E_p[x], p_y and E_p[z], hence logp = ln p_y,
+    lse = x_y - logp, H = lse - E_p[x] and the full KL; keyed rows (V = 2,048
+    and odd 1,000) plus edge rows (uniform, one dominant logit, target 60
+    nats below the rest, ties, large offsets)."""
+    import json
+    from pathlib import Path
+
+    from oracle.softmax_golden import inputs, to_f64
+    g = json.loads((Path(__file__).parent / "golden" / "softmax_pin.json").read_text())
+    checked = 0
+    for case in g["cases"]:
+        pol, ref, tgt = inputs(case)
+        assert tgt.tolist() == case["targets"]
+        x, z = to_f64(pol), to_f64(ref)
+        r = np.arange(len(tgt))
+        P = np.array([o["pol"] for o in case["rows_out"]])
+        Q = np.array([o["ref"] for o in case["rows_out"]])
+        assert np.allclose(P[:, 3], 1.0, rtol=0, atol=1e-14)
+        logp, rlogp = np.log(P[:, 1]), np.log(Q[:, 1])
+        lse_p, lse_q = x[r, tgt] - logp, z[r, tgt] - rlogp
+        ent = lse_p - P[:, 0]
+        d = rlogp - logp
+        want = {"k1": -d, "k2": 0.5 * d * d, "k3": np.expm1(d) - d,
+                "full": P[:, 0] - lse_p - P[:, 2] + lse_q}
+        for mode, kl in want.items():
+            got = O.token_stats(pol, ref, tgt, None, mode, threads=2)
+            for a, b in zip(got, (logp, rlogp, ent, kl)):
+                assert np.all(np.abs(a - b) <= 1e-12 * np.maximum(np.abs(a), np.abs(b)) + 1e-12), \
+                    (case["name"], mode, a, b)
+            checked += 1
+    assert checked == 12
