@@ -290,3 +290,46 @@ def test_token_stats_rowwarp_many_rows_per_warp(cuda, vocab, kl_mode):
     typical = valid & ~np.isin(np.arange(rows), [5, 2400, 4800, 7000])
     for i in range(3):
         assert O.max_rel_error(out[i][typical], exp[i][typical]) <= TOL, i
+
+
+@pytest.mark.parametrize("path", ["rowwarp", "ring"])
+def test_token_stats_matches_reference_softmax_pin(cuda, path, monkeypatch):
+    """The device A1 directly against the reference's own fp64 softmax
+    (tests/golden/softmax_pin.json: distattn::reference_attention, one head
+    per token row — see test_oracle_float.py), keyed and edge rows, both A1
+    kernels (the warp-per-row kernel and the TMA ring), every KL mode; the
+    fused loss + gradient kernel's logp / entropy too."""
+    import json
+    from pathlib import Path
+
+    from oracle.softmax_golden import inputs, to_f64
+    if path == "ring":
+        monkeypatch.setenv("YATT_A1_ROWWARP_VMAX", "0")
+    g = json.loads((Path(__file__).parent / "golden" / "softmax_pin.json").read_text())
+    for case in g["cases"]:
+        pol, ref, tgt = inputs(case)
+        x, z = to_f64(pol), to_f64(ref)
+        r = np.arange(len(tgt))
+        P = np.array([o["pol"] for o in case["rows_out"]])
+        Q = np.array([o["ref"] for o in case["rows_out"]])
+        logp, rlogp = np.log(P[:, 1]), np.log(Q[:, 1])
+        lse_p, lse_q = x[r, tgt] - logp, z[r, tgt] - rlogp
+        ent = lse_p - P[:, 0]
+        d = rlogp - logp
+        want = {"k1": -d, "k2": 0.5 * d * d, "k3": np.expm1(d) - d,
+                "full": P[:, 0] - lse_p - P[:, 2] + lse_q}
+        dp = torch.from_numpy(pol.view(np.int16)).to(cuda).view(torch.bfloat16)
+        dr = torch.from_numpy(ref.view(np.int16)).to(cuda).view(torch.bfloat16)
+        dt = torch.from_numpy(tgt).to(cuda)
+        for mode, kl in want.items():
+            got = [t.cpu().numpy().astype(np.float64) for t in ops.token_stats(dp, dr, dt, None, mode)]
+            for k, (a, b) in enumerate(zip(got, (logp, rlogp, ent, kl))):
+                # the A1 bar (1e-5 relative), absolute floor for values that are
+                # ~0 in exact arithmetic (a dominant logit: logp, H ~ 1e-24)
+                assert np.all(np.abs(a - b) <= TOL * np.abs(b) + 1e-6), (case["name"], mode, k, a, b)
+        if path == "rowwarp":
+            old = torch.zeros(len(tgt), device=cuda)
+            lp, en, _, _ = ops.policy_loss_grad(dp, dt, old, old, torch.as_tensor(
+                rlogp, dtype=torch.float32, device=cuda), None, None, "k3", float(len(tgt)))
+            assert np.all(np.abs(lp.cpu().numpy() - logp) <= TOL * np.abs(logp) + 1e-6)
+            assert np.all(np.abs(en.cpu().numpy() - ent) <= TOL * np.abs(ent) + 1e-6)
