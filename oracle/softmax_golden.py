@@ -60,6 +60,36 @@ def inputs(case):
     return _bf16_bits(np.stack(rows_p)), _bf16_bits(np.stack(rows_q)), tgt
 
 
+LMHEAD_CASES = [
+    {"name": "lmhead_d64_v1024", "seed": 3, "rows": 4, "d": 64, "V": 1024},
+    {"name": "lmhead_d256_v520", "seed": 4, "rows": 3, "d": 256, "V": 520},
+]
+
+
+def lmhead_inputs(case):
+    """(hidden bits [rows, d], W bits [V, d], targets) of an LM-head case."""
+    rng = np.random.default_rng(case["seed"])
+    d, V = case["d"], case["V"]
+    h = _bf16_bits(rng.standard_normal((case["rows"], d)).astype(np.float32))
+    w = _bf16_bits((rng.standard_normal((V, d)) * (2.0 / d ** 0.5)).astype(np.float32))
+    tgt = rng.integers(0, V, case["rows"]).astype(np.int32)
+    return h, w, tgt
+
+
+def run_reference_lmhead(h, w, tgt):
+    exe = HERE / "_ref" / "softmax_pin"
+    rows, d = h.shape
+    payload = (np.array([rows, d, w.shape[0]], dtype=np.int32).tobytes() + to_f64(h).tobytes()
+               + to_f64(w).tobytes() + np.ascontiguousarray(tgt, dtype=np.int32).tobytes())
+    res = subprocess.run([str(exe), "lmhead"], input=payload, capture_output=True, check=True)
+    out = []
+    for line in res.stdout.decode().split("\n"):
+        if line.strip():
+            _, py, *ew = line.split()
+            out.append({"p_y": float(py), "E_p_W": [float(v) for v in ew]})
+    return out
+
+
 def to_f64(bits):
     return (bits.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
 
@@ -83,12 +113,19 @@ def main():
     for case in CASES:
         pol, ref, tgt = inputs(case)
         golden.append({**case, "targets": tgt.tolist(), "rows_out": run_reference(pol, ref, tgt)})
+    lm = []
+    for case in LMHEAD_CASES:
+        h, w, tgt = lmhead_inputs(case)
+        lm.append({**case, "targets": tgt.tolist(), "rows_out": run_reference_lmhead(h, w, tgt)})
     dst = HERE.parent / "tests" / "golden" / "softmax_pin.json"
     dst.write_text(json.dumps({"source": "yatt::distattn::reference_attention "
                                          "(proj/src/distattn.cpp:79-123) via oracle/softmax_pin.cpp",
                                "columns": "per head: (E_p[x], p_y, E_p[z], 1); pol head x = policy, "
                                           "z = reference; ref head swapped",
-                               "cases": golden}, indent=1))
+                               "cases": golden,
+                               "lmhead_columns": "per token row: p_y and E_p[W] (softmax over "
+                                                 "h . W_j, q = sqrt(d) h, k_j = W_j)",
+                               "lmhead_cases": lm}, indent=1))
     print(f"wrote {dst}")
 
 

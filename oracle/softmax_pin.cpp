@@ -19,15 +19,68 @@
 // logits, rows*V float64 reference logits, rows int32 targets.
 // stdout: one line per (row, tensor): "row tensor c0 c1 c2 c3" (%.17g).
 // Linked against oracle/_ref/libyatt_ref.a (oracle/Makefile softmax_pin).
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <string>
 #include <vector>
 
 #include "yatt/distattn.hpp"
 
 using namespace yatt::distattn;
 
-int main() {
+// `softmax_pin lmhead`: the fused LM-head path (§8f #4) the same way — one
+// head per token row with q_i = sqrt(d) h (d a power of 4: exact scale),
+// k_j = W_j (the vocabulary rows), so score_j = h . W_j: head A with
+// v_j = W_j gives E_p[W] (E_p[logit] = h . E_p[W]); head B with
+// v_j = ([j == y], 0, ...) gives p_y.
+// stdin: int32 rows, d, V; rows*d float64 hidden; V*d float64 W; rows int32
+// targets.  stdout per row: "row p_y E_p[W]_0 ... E_p[W]_{d-1}".
+static int lmhead_main() {
+  int32_t rows = 0, d = 0, V = 0;
+  if (std::fread(&rows, 4, 1, stdin) != 1 || std::fread(&d, 4, 1, stdin) != 1 ||
+      std::fread(&V, 4, 1, stdin) != 1 || rows <= 0 || d <= 0 || V <= 0)
+    return 2;
+  std::vector<double> h(size_t(rows) * d), w(size_t(V) * d);
+  std::vector<int32_t> tgt(static_cast<size_t>(rows));
+  if (std::fread(h.data(), 8, h.size(), stdin) != h.size() ||
+      std::fread(w.data(), 8, w.size(), stdin) != w.size() ||
+      std::fread(tgt.data(), 4, tgt.size(), stdin) != tgt.size())
+    return 2;
+  const double sq = std::sqrt(double(d));
+  for (int32_t r = 0; r < rows; ++r) {
+    double py = 0;
+    std::vector<double> ew(static_cast<size_t>(d));
+    for (int head = 0; head < 2; ++head) {
+      AttentionProblem pb;
+      pb.seq_len = V;
+      pb.head_dim = d;
+      pb.num_heads = 1;
+      pb.q = Tensor3(1, V, d);
+      pb.k = Tensor3(1, V, d);
+      pb.v = Tensor3(1, V, d);
+      for (int j = 0; j < V; ++j)
+        for (int c = 0; c < d; ++c) {
+          pb.q.at(0, j, c) = sq * h[size_t(r) * d + c];
+          pb.k.at(0, j, c) = w[size_t(j) * d + c];
+          pb.v.at(0, j, c) = head == 0 ? w[size_t(j) * d + c]
+                                       : (c == 0 && j == tgt[size_t(r)] ? 1.0 : 0.0);
+        }
+      const Tensor3 o = reference_attention(pb);
+      if (head == 0)
+        for (int c = 0; c < d; ++c) ew[size_t(c)] = o.at(0, 0, c);
+      else
+        py = o.at(0, 0, 0);
+    }
+    std::printf("%d %.17g", r, py);
+    for (int c = 0; c < d; ++c) std::printf(" %.17g", ew[size_t(c)]);
+    std::printf("\n");
+  }
+  return 0;
+}
+
+int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "lmhead") return lmhead_main();
   int32_t rows = 0, V = 0;
   if (std::fread(&rows, 4, 1, stdin) != 1 || std::fread(&V, 4, 1, stdin) != 1 || rows <= 0 ||
       V <= 0)

@@ -136,3 +136,32 @@ def test_lmhead_qwen_head_full_size(cuda):
     ref_err = O.max_rel_error(stats(logits32)[1], e_ent)
     assert err <= max(1.25 * ref_err, 1e-5) and err <= 5e-5, (err, ref_err)
     assert bool(torch.isfinite(logp).all()) and bool((logp <= 0).all())
+
+
+@pytest.mark.parametrize("mode", ["P", "1"])
+def test_lmhead_matches_reference_softmax_pin(cuda, mode, monkeypatch):
+    """The fused LM head directly against the reference's own fp64 softmax
+    (distattn::reference_attention with the hidden row as the query and the
+    vocabulary rows as keys; tests/golden/softmax_pin.json, generated by
+    oracle/softmax_golden.py from the reference's sources)."""
+    import json
+    from pathlib import Path
+
+    from oracle.softmax_golden import lmhead_inputs, to_f64
+    monkeypatch.setenv("YATT_LMHEAD_CLUSTER", mode)
+    g = json.loads((Path(__file__).parent / "golden" / "softmax_pin.json").read_text())
+    for case in g["lmhead_cases"]:
+        hb, wb, y = lmhead_inputs(case)
+        h64, w64 = to_f64(hb), to_f64(wb)
+        r = np.arange(len(y))
+        py = np.array([o["p_y"] for o in case["rows_out"]])
+        ew = np.array([o["E_p_W"] for o in case["rows_out"]])
+        want_lp = np.log(py)
+        want_lse = (h64 * w64[y]).sum(1) - want_lp
+        want_ent = want_lse - (h64 * ew).sum(1)
+        dh = torch.from_numpy(hb.view(np.int16)).to(cuda).view(torch.bfloat16)
+        dw = torch.from_numpy(wb.view(np.int16)).to(cuda).view(torch.bfloat16)
+        lp, ent, lse = ops.lmhead_token_stats(dh, dw, torch.from_numpy(y).to(cuda))
+        assert O.max_rel_error(lp.cpu().numpy(), want_lp) <= 1e-5
+        assert O.max_rel_error(lse.cpu().numpy(), want_lse) <= 1e-5
+        assert O.max_rel_error(ent.cpu().numpy(), want_ent) <= 1e-5

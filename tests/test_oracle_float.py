@@ -154,3 +154,33 @@ def test_token_stats_oracle_pinned_to_reference_softmax():
                     (case["name"], mode, a, b)
             checked += 1
     assert checked == 12
+
+
+def test_lmhead_oracle_pinned_to_reference_softmax():
+    """The LM-head tests' fp64 oracle (numpy GEMM of the bf16 operands + two-
+    pass softmax, tests/test_gpu_lmhead.py::_oracle) against the reference's
+    attention softmax with the hidden row as the query and the vocabulary
+    rows as keys (tests/golden/softmax_pin.json "lmhead_cases")."""
+    import json
+    from pathlib import Path
+
+    from oracle.softmax_golden import lmhead_inputs, to_f64
+    g = json.loads((Path(__file__).parent / "golden" / "softmax_pin.json").read_text())
+    assert len(g["lmhead_cases"]) == 2
+    for case in g["lmhead_cases"]:
+        hb, wb, y = lmhead_inputs(case)
+        assert y.tolist() == case["targets"]
+        h, w = to_f64(hb), to_f64(wb)
+        logits = h @ w.T
+        mx = logits.max(1, keepdims=True)
+        lse = mx[:, 0] + np.log(np.exp(logits - mx).sum(1))
+        lp = logits - lse[:, None]
+        r = np.arange(len(y))
+        py = np.array([o["p_y"] for o in case["rows_out"]])
+        ew = np.array([o["E_p_W"] for o in case["rows_out"]])
+        want_lp = np.log(py)
+        want_lse = logits[r, y] - want_lp
+        want_ent = want_lse - (h * ew).sum(1)
+        assert np.allclose(lp[r, y], want_lp, rtol=1e-12, atol=1e-12)
+        assert np.allclose(lse, want_lse, rtol=1e-12, atol=1e-12)
+        assert np.allclose(-(np.exp(lp) * lp).sum(1), want_ent, rtol=1e-11, atol=1e-12)
