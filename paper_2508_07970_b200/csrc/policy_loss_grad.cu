@@ -490,7 +490,10 @@ int policy_loss_grad_pipe_launch(const FusedParams& p, int order, cudaStream_t s
   const void* k = kernels[full ? 1 : 0][order];
   const int rc = ensure_dynamic_smem(k, int(pipe_smem<S>()));
   if (rc) return rc;
-  const int grid = int(min64(p.rows, int64_t(S::kMinB) * num_sms()));
+  // YATT_FUSED_GRID: fewer CTAs than resident slots (measurement only)
+  const char* ge = std::getenv("YATT_FUSED_GRID");
+  const int64_t slots = int64_t(S::kMinB) * num_sms();
+  const int grid = int(min64(p.rows, ge ? std::max<int64_t>(1, min64(slots, std::atoi(ge))) : slots));
   void* args[] = {const_cast<FusedParams*>(&p)};
   YATT_TRY_CUDA(cudaLaunchKernel(k, dim3(unsigned(grid)), dim3(S::kThreads), args,
                                  pipe_smem<S>(), st));

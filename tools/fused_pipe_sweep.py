@@ -6,7 +6,8 @@ dispatch), 1 (large: 1 CTA/SM) or 2 (small: 2 CTAs/SM); YATT_FUSED_ORDER 0
 on / off; k3 and full KL at 32,768 x
 152,064 (a configs[1] prompt group).  Device time as tools/bench_kernels.py
 (CUDA graph, L2 flushed), achieved algorithmic GB/s vs the measured peak, and
-every shape's outputs against the first shape's."""
+every shape's outputs against the first shape's.  GRIDS="148,128,..." also
+sweeps the CTA count (YATT_FUSED_GRID) per shape; MODES="full" limits modes.""" 
 import json
 import os
 import sys
@@ -30,9 +31,15 @@ adv = ops.synth_floats(seed, 108, 0, rows, "adv")
 mask = (torch.arange(rows, device=pol.device) % 97 != 5).to(torch.uint8)
 cfg = ops.loss_config(0.2, 0.28, 0.0, 0.001, 0.001, "token-mean")
 grad = torch.empty_like(pol)
-for mode in ("k3", "full"):
+grids = [g for g in os.environ.get("GRIDS", "").split(",") if g]
+for mode in os.environ.get("MODES", "k3,full").split(","):
     base = None
-    for sh in shapes:
+    for sh in [f"{s}@{g}" for s in shapes for g in grids] if grids else shapes:
+        if "@" in sh:
+            sh, g = sh.split("@")
+            os.environ["YATT_FUSED_GRID"] = g
+        else:
+            os.environ.pop("YATT_FUSED_GRID", None)
         os.environ["YATT_FUSED_PIPE"] = sh[0]  # 0 = the default dispatch by vocabulary
         os.environ.pop("YATT_FUSED_LAG", None)
         if "l" in sh or "n" in sh:  # force the lag on ("l") / off ("n")
@@ -58,6 +65,7 @@ for mode in ("k3", "full"):
         ms = timeit(lambda: run(None), iters=10)
         per_row = (6 if mode == "full" else 4) * V + (24 if mode == "full" else 28)
         gbs = rows * per_row / (ms / 1e3) / 1e9
-        print(json.dumps({"mode": mode, "shape": sh, "rows": rows, "V": V, "ms": round(ms, 4),
+        print(json.dumps({"mode": mode, "shape": sh, "grid": os.environ.get("YATT_FUSED_GRID"),
+                          "rows": rows, "V": V, "ms": round(ms, 4),
                           "achieved_gbs": round(gbs, 1), "frac": round(gbs / PEAK, 3),
                           "vs_first_shape": diff}), flush=True)
