@@ -242,7 +242,7 @@ __global__ void gae_mark_ends_kernel(const int64_t* cu, int64_t nseq, int64_t n_
   if (e > b && e >= 1) atomicOr(ends + ((e - 1) >> 5), 1u << ((e - 1) & 31));
 }
 
-#ifndef YATT_GAE_MINB  // 6 CTAs/SM (80 regs, no spills): 59 us vs 64 us at 5 (96 regs)
+#ifndef YATT_GAE_MINB  // 6 CTAs/SM (80 regs, no spills): 59 us vs 64 us at 5 (96 regs); 7 / 8 (spilling) no faster
 #define YATT_GAE_MINB 6
 #endif
 // kMom: also the masked moments (count, sum, sum^2) of the advantages it
