@@ -407,6 +407,12 @@ def run_b200(args):
 
     # ---- e2e through the public API: pinned host inputs -> device -> loss ----
     e2e = run_e2e(args, dev, ops, cfg, ws, world)
+    hidden = None
+    if world == 1 and not args.no_hidden_path:
+        try:
+            hidden = run_hidden_state_path(dev, ops, cfg, ws)
+        except Exception as e:  # noqa: BLE001 - informational; the bench line must print
+            hidden = {"error": f"{type(e).__name__}: {e}"[:300]}
 
     cpu = None
     integer = None
@@ -427,7 +433,7 @@ def run_b200(args):
                 "dtype": "bf16", "data": "synthetic (keyed integer-derived bf16 logits, "
                 "binary group rewards; DESIGN.md)", "config": workload_config(world, args.collective),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "integer_path": integer,
+                "integer_path": integer, "hidden_state_path": hidden,
                 # per group: token_stats + its fix-up pass; per step: grpo_adv,
                 # broadcast, loss partials + final
                 "gpu_launches": args.steps * (2 * ng + 4), "clocks": clk,
@@ -540,6 +546,66 @@ def run_e2e(args, dev, ops, cfg, ws, world=1):
                       f"({h2d / 1e9:.2f} GB H2D from pinned memory)"}
 
 
+def run_hidden_state_path(dev, ops, cfg, ws, steps=3):
+    """The same experience metric from HIDDEN STATES (logits never
+    materialised): per step one configs[1] prompt group (32,768 rows) through
+    the fused tcgen05 LM head + log-softmax twice (policy and reference
+    heads, Qwen2.5-7B shape d=3,584 x V=152,064, random-init bf16 weights),
+    the k3 KL from the two log-probs, GRPO advantages and the loss.
+    Informational (outside the timed region of the headline): what the path
+    costs when the logits are produced on the device instead of read."""
+    import torch
+    rows, d = CHUNK_ROWS, 3584
+    g = torch.Generator(device=dev).manual_seed(SEED)
+    h = torch.randn(rows, d, device=dev, generator=g).to(torch.bfloat16)
+    hr = (h.float() + 0.05 * torch.randn(rows, d, device=dev, generator=g)).to(torch.bfloat16)
+    w = (torch.randn(VOCAB, d, device=dev, generator=g) * (2.0 / d ** 0.5)).to(torch.bfloat16)
+    wr = (w.float() + 0.01 * torch.randn(VOCAB, d, device=dev, generator=g)).to(torch.bfloat16)
+    y = torch.randint(0, VOCAB, (rows,), device=dev, generator=g, dtype=torch.int32)
+    rewards = ops.synth_floats(SEED, 105, 0, RESPONSES, "reward", RESPONSES, device=dev)
+    cu = torch.arange(0, RESPONSES + 1, dtype=torch.int64, device=dev) * T
+    tok_adv = torch.empty((rows,), dtype=torch.float32, device=dev)
+    sums = torch.empty((8,), dtype=torch.float64, device=dev)
+    out_p = torch.empty((3, rows), dtype=torch.float32, device=dev)
+    out_r = torch.empty((3, rows), dtype=torch.float32, device=dev)
+    old = None
+
+    def step():
+        lp, ent, _ = ops.lmhead_token_stats(h, w, y, out=out_p)
+        rl, _, _ = ops.lmhead_token_stats(hr, wr, y, out=out_r)
+        kl = ops.kl_from_logps(lp, rl, "k3")
+        adv = ops.grpo_advantages(rewards, RESPONSES)
+        ops.broadcast_to_tokens(adv, cu, rows, None, out=tok_adv)
+        ops.policy_loss(lp, old if old is not None else lp, tok_adv, kl, ent, None, None, cfg,
+                        ws, sums)
+
+    step()
+    old = out_p[0].clone()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        step()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    flops = 2 * 2.0 * rows * d * VOCAB  # two heads
+    peak, sustained = 1646.0, 1377.5  # MEASURED_PEAKS.json burst / sustained cuBLAS bf16
+    try:
+        mp = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        peak, sustained = float(mp["bf16_tflops"]), float(mp["bf16_tflops_sustained"])
+    except Exception:  # noqa: BLE001
+        pass
+    tf = flops / (ms / 1e3) / 1e12
+    return {"value": rows / (ms / 1e3), "unit": "tokens/s", "ms_per_group": ms,
+            "sample": f"{steps} x one prompt group ({rows} rows), hidden {d}, V={VOCAB}",
+            "roofline": {"bound": "tensor", "kernel": "lmhead_lse_pair_kernel (cta_group::2)",
+                         "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
+                         "peak_sustained": sustained, "frac_of_sustained": tf / sustained,
+                         "flops": "GEMM only (2 x 2 rows d V); the step's time includes the "
+                                  "split combine, KL, GRPO and loss kernels"}}
+
+
 _JSON_OUT = None
 
 
@@ -563,6 +629,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-hidden-path", action="store_true",
+                    help="skip the informational hidden-state (LM head) measurement")
     ap.add_argument("--ref-budget-s", type=float, default=12.0)
     ap.add_argument("--collective", choices=["peer", "nccl"], default="peer",
                     help="N>1 loss/token-count all-reduce: fused into the loss's final "
