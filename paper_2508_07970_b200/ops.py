@@ -359,6 +359,14 @@ def filter_compact(rewards: torch.Tensor, seq_lens: torch.Tensor, group_size: in
     return {"keep_groups": keep[:ng], "index_map": imap, "new_cu": new_cu, "counts": counts}
 
 
+def _moments_fit(moments: torch.Tensor, n: int, group_size: int, first_sample_id: int) -> None:
+    """The per-group moments table must cover this shard's local groups."""
+    ng = lib().yatt_grpo_num_local_groups(n, first_sample_id, group_size)
+    if moments.numel() < 3 * ng:
+        raise ValueError(f"moments holds {moments.numel()} doubles, the shard's {ng} groups "
+                         f"need {3 * ng}")
+
+
 def filter_boundary_record(rewards: torch.Tensor, group_size: int,
                            first_sample_id: int = 0) -> torch.Tensor:
     _dev(rewards, torch.float32, "rewards")
@@ -371,6 +379,7 @@ def filter_boundary_record(rewards: torch.Tensor, group_size: int,
 def grpo_boundary_record(moments: torch.Tensor, n: int, group_size: int,
                          first_sample_id: int = 0) -> torch.Tensor:
     _dev(moments, torch.float64, "moments")
+    _moments_fit(moments, n, group_size, first_sample_id)
     rec = torch.empty((8,), dtype=torch.float64, device=moments.device)
     check(lib().yatt_grpo_boundary_record(_p(moments), n, first_sample_id, group_size, _p(rec),
                                           _st()))
@@ -381,6 +390,9 @@ def grpo_merge_boundaries(moments: torch.Tensor, n: int, group_size: int, first_
                           all_records: torch.Tensor) -> torch.Tensor:
     _dev(moments, torch.float64, "moments")
     _dev(all_records, torch.float64, "all_records")
+    _moments_fit(moments, n, group_size, first_sample_id)
+    if all_records.numel() == 0 or all_records.numel() % 8:
+        raise ValueError("all_records must hold 8 doubles per rank")
     check(lib().yatt_grpo_merge_boundaries(_p(moments), n, first_sample_id, group_size,
                                            _p(all_records), all_records.numel() // 8, _st()))
     return moments

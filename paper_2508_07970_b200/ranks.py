@@ -137,7 +137,11 @@ class PeerGroup:
         return torch.cuda.current_stream().cuda_stream
 
     def allreduce_f64(self, t: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        from .ops import _dev, _numel
+        _dev(t, torch.float64, "t")
         out = torch.empty_like(t) if out is None else out
+        _dev(out, torch.float64, "out")
+        _numel(t.numel(), out=out)
         check(lib().yatt_peer_allreduce_f64(self.h, t.data_ptr(), t.numel(), out.data_ptr(),
                                             self._st()))
         return out
@@ -145,6 +149,8 @@ class PeerGroup:
     def scan_i64(self, t: torch.Tensor):
         """(exclusive prefix over lower ranks, total over all ranks) of the
         int64 counters t (<= 16) in one kernel."""
+        from .ops import _dev
+        _dev(t, torch.int64, "t")
         pre, tot = torch.empty_like(t), torch.empty_like(t)
         check(lib().yatt_peer_scan_i64(self.h, t.data_ptr(), t.numel(), pre.data_ptr(),
                                        tot.data_ptr(), self._st()))
@@ -164,6 +170,12 @@ class PeerGroup:
         """ops.policy_loss whose final reduction is also the all-reduce: the
         GLOBAL yatt_loss_sums on every rank."""
         from . import ops
+        ops._devs(torch.float32, logp=logp, old_logp=old_logp, advantages=advantages, kl=kl,
+                  entropy=entropy)
+        if cu_seqlens is not None:
+            ops._dev(cu_seqlens, torch.int64, "cu_seqlens")
+        ops._numel(logp.numel(), old_logp=old_logp, advantages=advantages, kl=kl,
+                   entropy=entropy, mask=mask)
         cfg = config or ops.loss_config()
         ws = workspace or ops.LossWorkspace(logp.device)
         if sums is None:
@@ -186,6 +198,8 @@ class PeerGroup:
         + n)) whose first / last groups may straddle ranks: boundary moments
         exchanged over peer memory and merged on the device, one call
         (yatt_peer_grpo_advantages)."""
+        from .ops import _dev
+        _dev(rewards, torch.float32, "rewards")
         adv = torch.empty_like(rewards)
         ws, wsb = self._straddle_ws(rewards.numel(), first_sample_id, group_size, rewards.device)
         check(lib().yatt_peer_grpo_advantages(self.h, rewards.data_ptr(), rewards.numel(),
@@ -196,6 +210,10 @@ class PeerGroup:
     def filter_compact(self, rewards, seq_lens, group_size, first_sample_id=0):
         """Zero-variance filter + compaction of this rank's shard with exact
         decisions for straddling groups (yatt_peer_filter_compact)."""
+        from .ops import _dev, _numel
+        _dev(rewards, torch.float32, "rewards")
+        _dev(seq_lens, torch.int64, "seq_lens")
+        _numel(rewards.numel(), seq_lens=seq_lens)
         n, dev = rewards.numel(), rewards.device
         ng = lib().yatt_grpo_num_local_groups(n, first_sample_id, group_size)
         keep = torch.empty((max(ng, 1),), dtype=torch.uint8, device=dev)

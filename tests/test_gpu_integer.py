@@ -602,3 +602,20 @@ def test_straddling_groups_emulated_ranks(cuda, P):
     assert off.tolist() == single["counts"].tolist()
     assert kept_groups == int(single["counts"][2])
     assert torch.equal(dst, ref)
+
+
+def test_straddle_python_layer_validates_shapes(cuda):
+    """The Python straddle helpers refuse tables that do not cover the shard
+    (the C ABI would read / write moments rows 0 .. ng-1 of them)."""
+    r = torch.zeros(20, device=cuda)
+    mom = ops.grpo_group_moments(r, 8, 4)           # ids 4..23: 3 local groups
+    assert mom.shape == (3, 3)
+    with pytest.raises(ValueError, match="groups"):
+        ops.grpo_boundary_record(mom[:2].contiguous(), 20, 8, 4)
+    rec = ops.grpo_boundary_record(mom, 20, 8, 4)
+    with pytest.raises(ValueError, match="8 doubles"):
+        ops.grpo_merge_boundaries(mom, 20, 8, 4, rec[:5].contiguous())
+    with pytest.raises(TypeError):
+        ops.grpo_merge_boundaries(mom.float(), 20, 8, 4, rec)
+    ops.grpo_merge_boundaries(mom, 20, 8, 4, rec)     # one rank: its own record
+    torch.cuda.synchronize()
