@@ -398,10 +398,22 @@ def grpo_merge_boundaries(moments: torch.Tensor, n: int, group_size: int, first_
     return moments
 
 
+def _plan_arrays(old_cu, index_map, new_cu, n_kept, max_kept, dst_offset=None):
+    """The compaction plan's device arrays: dtypes, and sizes the gather
+    kernels index up to max_kept."""
+    _devs(torch.int64, old_cu=old_cu, new_cu=new_cu, n_kept=n_kept, dst_offset=dst_offset)
+    _dev(index_map, torch.int32, "index_map")
+    if max_kept < 0 or index_map.numel() < max_kept or new_cu.numel() < max_kept + 1:
+        raise ValueError(f"index_map / new_cu must cover max_kept = {max_kept} samples")
+    if n_kept.numel() < 1 or (dst_offset is not None and dst_offset.numel() < 1):
+        raise ValueError("n_kept / dst_offset are one-element device counters")
+
+
 def gather_varlen(src: torch.Tensor, old_cu: torch.Tensor, index_map: torch.Tensor,
                   new_cu: torch.Tensor, n_kept: torch.Tensor, max_kept: int, dst: torch.Tensor,
                   dst_offset: torch.Tensor | None = None) -> torch.Tensor:
     _dense(src=src, dst=dst)
+    _plan_arrays(old_cu, index_map, new_cu, n_kept, max_kept, dst_offset)
     check(lib().yatt_gather_varlen(_p(src), _p(old_cu), _p(index_map), _p(new_cu), _p(n_kept),
                                    max_kept, _p(dst_offset), src.element_size(), _p(dst), _st()))
     return dst
@@ -411,6 +423,7 @@ def gather_varlen_multi(srcs, old_cu: torch.Tensor, index_map: torch.Tensor, new
                         n_kept: torch.Tensor, max_kept: int, dsts,
                         dst_offset: torch.Tensor | None = None):
     """gather_varlen over several per-token arrays (<= 8) in one launch."""
+    _plan_arrays(old_cu, index_map, new_cu, n_kept, max_kept, dst_offset)
     n = len(srcs)
     if n != len(dsts):
         raise ValueError("srcs and dsts differ in length")
@@ -429,6 +442,10 @@ def gather_varlen_multi(srcs, old_cu: torch.Tensor, index_map: torch.Tensor, new
 def gather_rows(src: torch.Tensor, index_map: torch.Tensor, n_kept: torch.Tensor, max_kept: int,
                 dst: torch.Tensor, dst_offset: torch.Tensor | None = None) -> torch.Tensor:
     _dense(src=src, dst=dst)
+    _devs(torch.int64, n_kept=n_kept, dst_offset=dst_offset)
+    _dev(index_map, torch.int32, "index_map")
+    if max_kept < 0 or index_map.numel() < max_kept:
+        raise ValueError(f"index_map must cover max_kept = {max_kept} rows")
     row_bytes = src[0].numel() * src.element_size() if src.dim() > 1 else src.element_size()
     check(lib().yatt_gather_rows(_p(src), _p(index_map), _p(n_kept), max_kept, row_bytes,
                                  _p(dst_offset), _p(dst), _st()))
@@ -438,7 +455,13 @@ def gather_rows(src: torch.Tensor, index_map: torch.Tensor, n_kept: torch.Tensor
 def microbatch_aggregates(prompt_len: torch.Tensor, out_len: torch.Tensor, microbatch_size: int,
                           controller_rank: int = 0, n: torch.Tensor | None = None,
                           max_n: int | None = None) -> torch.Tensor:
+    _devs(torch.int32, prompt_len=prompt_len, out_len=out_len)
+    _numel(prompt_len.numel(), out_len=out_len)
+    if n is not None:
+        _dev(n, torch.int64, "n")
     cap = prompt_len.numel() if max_n is None else max_n
+    if cap > prompt_len.numel():
+        raise ValueError("max_n exceeds the length arrays")
     nmb = -(-cap // microbatch_size)
     out = torch.zeros((max(nmb, 1), 6), dtype=torch.int32, device=prompt_len.device)  # 24 B rows
     check(lib().yatt_microbatch_aggregates(_p(prompt_len), _p(out_len), _p(n), cap,
@@ -447,6 +470,9 @@ def microbatch_aggregates(prompt_len: torch.Tensor, out_len: torch.Tensor, micro
 
 
 def exclusive_offset(counts: torch.Tensor, nranks: int, rank: int, stride: int, field: int):
+    _dev(counts, torch.int64, "counts")
+    if counts.numel() < nranks * stride or not 0 <= field < stride:
+        raise ValueError("counts must hold nranks x stride words and field < stride")
     out = torch.empty((1,), dtype=torch.int64, device=counts.device)
     check(lib().yatt_exclusive_offset(_p(counts), nranks, rank, stride, field, _p(out), _st()))
     return out
@@ -487,6 +513,7 @@ def lmhead_token_stats(hidden: torch.Tensor, lm_head: torch.Tensor, targets: tor
 
 def kl_from_logps(logp: torch.Tensor, ref_logp: torch.Tensor, kl_mode: str = "k3"):
     _devs(torch.float32, logp=logp, ref_logp=ref_logp)
+    _numel(logp.numel(), ref_logp=ref_logp)
     kl = torch.empty_like(logp)
     check(lib().yatt_kl_from_logps(_p(logp), _p(ref_logp), logp.numel(), KL_MODES[kl_mode],
                                    _p(kl), _st()))
