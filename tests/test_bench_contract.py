@@ -7,6 +7,8 @@ import subprocess
 import sys
 from pathlib import Path
 
+import pytest
+
 ROOT = Path(__file__).resolve().parents[1]
 
 
@@ -39,3 +41,26 @@ def test_reference_arm_nonzero_ranks_exit_silently():
                {"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
     assert res.returncode == 0, res.stderr[-2000:]
     assert res.stdout.strip() == ""
+
+
+@pytest.mark.gpu
+def test_b200_arm_prints_one_contract_line(cuda):
+    """The GPU arm end to end (1 step): the base keys plus roofline,
+    cpu_baseline, e2e (host buffers through the C ABI), clocks, gpu_launches
+    and the informational hidden-state path."""
+    res = _run(["--steps", "1", "--warmup", "1", "--ref-budget-s", "1"])
+    assert res.returncode == 0, res.stderr[-3000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, res.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 1 and d["value"] > 1e6 and d["dtype"] == "bf16"
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0.3 < r["frac"] < 1.3
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["value"] > 0
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 1e9 and e["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] == 1 * (2 * 256 + 4)
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+    assert d["hidden_state_path"]["roofline"]["bound"] == "tensor"
+    assert d["integer_path"] is None or d["integer_path"]["train_units_bit_exact"] is True
