@@ -156,6 +156,33 @@ def main():
         if int(red[5]) == 0:
             break
     assert rnd == len(ref_rounds)
+    # the same step with ONE exchange: every rank runs its shard's rounds to
+    # completion in one persistent kernel, the reports travel once
+    # (PeerGroup.run_rollout_rounds) — every field and microbatch of every
+    # round == the single-process rounds, and the shard's final states too
+    ref_batch = mk()
+    ref_rounds = api.run_rollout_rounds(ref_batch, world, params)
+    sr0 = api.shard_dataset(2048, world, rank)
+    mine_s = mk().samples[sr0.begin:sr0.end]
+    got_rounds = peer.run_rollout_rounds(mine_s, 0, params, dev)
+    assert got_rounds == ref_rounds, (rank, len(got_rounds), len(ref_rounds))
+    assert [(x.target_out_len_tokens, x.accepted, x.accepted_round) for x in mine_s] == \
+        [(x.target_out_len_tokens, x.accepted, x.accepted_round)
+         for x in ref_batch.samples[sr0.begin:sr0.end]], rank
+    # a later step whose shards finish in different rounds (high rejection,
+    # one rank's shard already accepted): zero reports pad the finished ones
+    params_hi = api.RoundParams(api.LengthDistribution(api.NORMAL, 900, 300, 4096),
+                                api.RejectionConfig(0.6, False, 1), SEED + 1, 4, 6)
+    mk2 = lambda: api.RolloutBatch(3, [api.RolloutSample(3 * 512 + i, 32, accepted=(  # noqa
+        api.shard_dataset(512, world, 0).begin <= i < api.shard_dataset(512, world, 0).end))
+        for i in range(512)])
+    ref_b2 = mk2()
+    ref_r2 = api.run_rollout_rounds(ref_b2, world, params_hi)
+    sr2 = api.shard_dataset(512, world, rank)
+    mine2 = mk2().samples[sr2.begin:sr2.end]
+    assert peer.run_rollout_rounds(mine2, 3, params_hi, dev) == ref_r2, rank
+    assert [x.target_out_len_tokens for x in mine2] == \
+        [x.target_out_len_tokens for x in ref_b2.samples[sr2.begin:sr2.end]], rank
     # groups straddling ranks: the reference's SAMPLE-level shard_dataset
     # (workload.cpp:183-198) of N = 16 x 8 samples; at world 3 / 7 groups of 8
     # split across ranks.  Advantages == one rank's (fp64 moments merged on
