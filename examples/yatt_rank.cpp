@@ -213,6 +213,31 @@ int main() {
     cudaFree(dw);
     cudaFree(dg);
     cudaFree(gsums);
+    // the one-exchange multi-rank rounds (world 1: this rank holds every
+    // sample) == the single-process round loop, report for report
+    workload::RolloutBatch fresh = one;
+    for (auto& s : fresh.samples) s.accepted = false, s.accepted_round = 0, s.target_out_len_tokens = 0;
+    workload::RolloutBatch fresh2 = fresh;
+    const auto single = sim::run_rollout_rounds(fresh, 1, params);
+    const auto viapeer = peer.run_rollout_rounds(fresh2.samples, fresh2.step_index, params);
+    bool same = single.size() == viapeer.size();
+    for (size_t r = 0; same && r < single.size(); ++r) {
+      const auto& a = single[r][0];
+      const auto& b = viapeer[r][0];
+      same = a.controller_rank == b.controller_rank && a.round == b.round &&
+             a.active_count == b.active_count && a.pending_count == b.pending_count &&
+             a.accepted_train_units == b.accepted_train_units &&
+             a.microbatches.size() == b.microbatches.size();
+    }
+    for (size_t i = 0; same && i < fresh.samples.size(); ++i)
+      same = fresh.samples[i].target_out_len_tokens == fresh2.samples[i].target_out_len_tokens &&
+             fresh.samples[i].accepted_round == fresh2.samples[i].accepted_round;
+    if (!same) {
+      std::fprintf(stderr, "peer rounds differ from the single-process rounds\n");
+      return 1;
+    }
+    std::printf("peer group: one-exchange rounds == single-process rounds (%zu rounds)\n",
+                viapeer.size());
   }
 
   // 5c. dynamic sampling on the rewards + the survivors' payload in one launch

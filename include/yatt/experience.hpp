@@ -12,6 +12,8 @@
 #include <cstdint>
 #include <vector>
 
+#include "yatt/simcore.hpp"
+
 namespace yatt::experience {
 
 // ---- A1 -------------------------------------------------------------------
@@ -233,6 +235,16 @@ class PeerGroup {
                                std::int64_t n_samples, std::uint64_t first_sample_id,
                                int group_size, const CompactionBuffers& out, void* workspace,
                                std::size_t workspace_bytes, void* stream = nullptr);
+  // The multi-rank dynamic-sampling step with ONE exchange
+  // (yatt_peer_rounds_run): this rank's controller shard (the reference's
+  // shard_dataset range, workload.cpp:183-198) runs every round in one
+  // persistent kernel and every rank's reports travel once; returns the
+  // GLOBAL reports[round][rank] (what the reference's coordinator feeds to
+  // StepAssembler::feed_round, demo.cpp:468-476) and updates the shard's
+  // samples like copy_back (simcore.cpp:107-119).  Collective.
+  std::vector<std::vector<sim::ShardRoundReport>> run_rollout_rounds(
+      std::vector<workload::RolloutSample>& shard_samples, int step_index,
+      const sim::RoundParams& params, std::vector<int>* first_round_lengths = nullptr);
   int world() const { return world_; }
   int rank() const { return rank_; }
   int status() const;  // 1 after a call timed out waiting for a rank

@@ -681,6 +681,19 @@ int yatt_peer_allgather_i64(yatt_peer_t peer, const int64_t* d_in, int32_t n,
 size_t yatt_straddle_workspace_bytes(int64_t n_samples, uint64_t first_sample_id,
                                      int32_t group_size, int32_t world);
 int yatt_peer_world(yatt_peer_t p, int32_t* h_world, int32_t* h_rank);
+
+/* The multi-rank dynamic-sampling step with ONE exchange (replaces the      */
+/* per-round submit_round / feed_round / continue protocol, demo.cpp:468-476 */
+/* and simcore.cpp:470-490): this rank's controller shard (n samples staged  */
+/* with yatt_rounds_stage(h, n, 1, ...)) runs every round in one persistent  */
+/* kernel, then every rank's reports + microbatch aggregates are all-gathered */
+/* over the peer group.  Afterwards yatt_rounds_result(h) is the GLOBAL view: */
+/* reports[round][rank] (rounds = max over ranks; a finished shard reports    */
+/* zeros) and the microbatches in that order; the staged outputs are this     */
+/* rank's samples.  Collective: every rank calls, same step and params.      */
+int yatt_peer_rounds_run(yatt_peer_t peer, yatt_rounds_t h, int64_t n, int32_t step_index,
+                         const yatt_round_params* params, int32_t want_first_lens,
+                         void* stream);
 int yatt_peer_grpo_advantages(yatt_peer_t p, const float* d_rewards, int64_t n_samples,
                               uint64_t first_sample_id, int32_t group_size, float eps,
                               int32_t norm_by_std, float* d_sample_adv, void* d_workspace,

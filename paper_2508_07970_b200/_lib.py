@@ -111,6 +111,7 @@ SIGNATURES = {
     "yatt_rounds_stage": (C.c_int, [c_p, c_i64, c_i32, P(RoundsIoC)]),
     "yatt_rounds_run": (C.c_int, [c_p, c_i64, P(c_i64), c_i32, c_i32, c_i32, c_i32, c_i32,
                                   P(RoundParamsC), c_i32, c_p]),
+    "yatt_peer_rounds_run": (C.c_int, [c_p, c_p, c_i64, c_i32, P(RoundParamsC), c_i32, c_p]),
     "yatt_rounds_result": (C.c_int, [c_p, P(RoundsViewC)]),
     "yatt_sample_lengths_host": (C.c_int, [P(LengthDist), c_u64, c_u64, c_u64, c_u64, c_p, c_i64,
                                            c_p]),

@@ -287,10 +287,12 @@ _ROUNDS: dict = {}
 
 
 def _run_rounds(samples, out_attr, offsets, first_rank, step, first_round, limit,
-                params: RoundParams, device):
+                params: RoundParams, device, peer=None):
     """yatt_rounds_run over host samples (one persistent kernel for every
     round of every shard); returns (reports[round][shard], final state per
-    sample: (out_len, accepted, accepted_round), None if accepted before)."""
+    sample: (out_len, accepted, accepted_round), None if accepted before).
+    With `peer` (ranks.PeerGroup): yatt_peer_rounds_run — `samples` are this
+    rank's controller shard, the reports come back for every rank."""
     if params.microbatch_size <= 0:
         raise ConfigError("microbatch_size must be positive")
     dev = torch.device(device)
@@ -311,11 +313,15 @@ def _run_rounds(samples, out_attr, offsets, first_rank, step, first_round, limit
             C.memmove(io.sample_id, ids.ctypes.data, ids.nbytes)
             C.memmove(io.prompt_len, prm.ctypes.data, prm.nbytes)
             C.memmove(io.accepted, acc.ctypes.data, acc.nbytes)
-        off = (C.c_int64 * len(offsets))(*offsets)
-        check(lib().yatt_rounds_run(h, n, off, ns, first_rank, step, first_round, limit,
-                                    C.byref(params.c()), 0, None))
+        if peer is None:
+            off = (C.c_int64 * len(offsets))(*offsets)
+            check(lib().yatt_rounds_run(h, n, off, ns, first_rank, step, first_round, limit,
+                                        C.byref(params.c()), 0, None))
+        else:
+            check(lib().yatt_peer_rounds_run(peer.h, h, n, step, C.byref(params.c()), 0, None))
         v = RoundsViewC()
         check(lib().yatt_rounds_result(h, C.byref(v)))
+        ns = v.num_shards
         reps = (ReportC * (v.rounds * ns)).from_buffer_copy(
             C.string_at(v.reports, C.sizeof(ReportC) * v.rounds * ns))
         mbs = (MbAggC * max(v.num_microbatches, 1)).from_buffer_copy(

@@ -536,6 +536,7 @@ struct yatt_rounds {
   int grid_cap = 0;
   int64_t staged_n = -1;
   int32_t staged_shards = 0;
+  DevBuf xin, xout;  // yatt_peer_rounds_run: the exchange's device words
   // accumulated over the launches of one call
   std::vector<yatt_round_report> reps;
   std::vector<yatt_mb_agg> mbs;
@@ -843,6 +844,98 @@ int yatt_rounds_result(yatt_rounds_t h, yatt_rounds_view* v) {
   v->num_microbatches = int64_t(h->mbs.size());
   v->redrawn_on_host = h->redrawn;
   v->first_round_lens_valid = h->have_first ? 1 : 0;
+  return YATT_OK;
+}
+
+// The multi-rank step with ONE exchange (fates first: acceptance never
+// depends on the drawn lengths, so every rank can run its own controller
+// shard to completion without hearing from the others).  The global loop of
+// the reference (simcore.cpp:470-490; the coordinator's continue test,
+// demo.cpp:468-476) runs max-over-ranks rounds, a finished shard reporting
+// zeros; this rank's reports + microbatch aggregates travel once, as int64
+// words through the peer all-gather kernel, and the handle's result view
+// becomes the GLOBAL one: reports[round][rank], microbatches in that order.
+int yatt_peer_rounds_run(yatt_peer_t peer, yatt_rounds_t h, int64_t n, int32_t step_index,
+                         const yatt_round_params* prm, int32_t want_first_lens, void* stream) {
+  YATT_REQUIRE(h != nullptr && prm != nullptr, YATT_ERR_CONFIG, "peer_rounds_run: null argument");
+  int32_t world = 0, rank = 0;
+  int rc = yatt_peer_world(peer, &world, &rank);
+  if (rc) return rc;
+  const int64_t off[2] = {0, n};
+  rc = yatt_rounds_run(h, n, off, 1, rank, step_index, 1, 0, prm, want_first_lens, stream);
+  if (rc) return rc;
+  // wire: [rounds, reports (6 words each), microbatches (3 words each)]
+  static_assert(sizeof(yatt_round_report) == 48 && sizeof(yatt_mb_agg) == 24, "wire words");
+  const int64_t R = h->rounds, M = int64_t(h->mbs.size());
+  std::vector<int64_t> mine(size_t(1 + 6 * R + 3 * M));
+  mine[0] = R;
+  std::memcpy(mine.data() + 1, h->reps.data(), size_t(48 * R));
+  std::memcpy(mine.data() + 1 + 6 * R, h->mbs.data(), size_t(24 * M));
+  const cudaStream_t st = stream ? as_stream(stream) : h->own_stream;
+  const int64_t cap = YATT_PEER_GATHER_MAX_WORDS;
+  rc = h->xin.reserve(size_t(8 * cap));
+  if (!rc) rc = h->xout.reserve(size_t(8 * cap * world));
+  if (rc) return rc;
+  int64_t* din = static_cast<int64_t*>(h->xin.p);
+  int64_t* dout = static_cast<int64_t*>(h->xout.p);
+  const int64_t my_words = int64_t(mine.size());
+  std::vector<int64_t> sizes(static_cast<size_t>(world));
+  YATT_TRY_CUDA(cudaMemcpyAsync(din, &my_words, 8, cudaMemcpyHostToDevice, st));
+  rc = yatt_peer_allgather_i64(peer, din, 1, dout, st);
+  if (rc) return rc;
+  YATT_TRY_CUDA(cudaMemcpyAsync(sizes.data(), dout, 8 * size_t(world), cudaMemcpyDeviceToHost, st));
+  YATT_TRY_CUDA(cudaStreamSynchronize(st));
+  const int64_t width = *std::max_element(sizes.begin(), sizes.end());
+  mine.resize(size_t(width), 0);
+  std::vector<int64_t> all(size_t(world * width)), chunk(size_t(world * cap));
+  for (int64_t c0 = 0; c0 < width; c0 += cap) {
+    const int64_t cw = std::min(cap, width - c0);
+    YATT_TRY_CUDA(cudaMemcpyAsync(din, mine.data() + c0, size_t(8 * cw), cudaMemcpyHostToDevice, st));
+    rc = yatt_peer_allgather_i64(peer, din, int32_t(cw), dout, st);
+    if (rc) return rc;
+    YATT_TRY_CUDA(cudaMemcpyAsync(chunk.data(), dout, size_t(8 * cw * world), cudaMemcpyDeviceToHost,
+                                  st));
+    YATT_TRY_CUDA(cudaStreamSynchronize(st));
+    for (int32_t r = 0; r < world; ++r)
+      std::memcpy(all.data() + size_t(r * width + c0), chunk.data() + size_t(r * cw), size_t(8 * cw));
+  }
+  // the global view, round-major then rank
+  int64_t rounds_g = 0;
+  std::vector<int64_t> mb_cursor(static_cast<size_t>(world));
+  for (int32_t r = 0; r < world; ++r) {
+    const int64_t* w = all.data() + size_t(r * width);
+    YATT_REQUIRE(w[0] >= 0 && 1 + 6 * w[0] <= sizes[size_t(r)], YATT_ERR_CUDA,
+                 "peer_rounds_run: malformed words from rank %d", r);
+    rounds_g = std::max(rounds_g, w[0]);
+    mb_cursor[size_t(r)] = 1 + 6 * w[0];
+  }
+  h->reps.clear();
+  h->mbs.clear();
+  for (int64_t k = 0; k < rounds_g; ++k)
+    for (int32_t r = 0; r < world; ++r) {
+      const int64_t* w = all.data() + size_t(r * width);
+      if (k < w[0]) {
+        yatt_round_report rep;
+        std::memcpy(&rep, w + 1 + 6 * k, 48);
+        YATT_REQUIRE(rep.num_microbatches >= 0 &&
+                         mb_cursor[size_t(r)] + 3 * rep.num_microbatches <= sizes[size_t(r)],
+                     YATT_ERR_CUDA, "peer_rounds_run: malformed microbatches from rank %d", r);
+        for (int64_t q = 0; q < rep.num_microbatches; ++q) {
+          yatt_mb_agg m;
+          std::memcpy(&m, w + mb_cursor[size_t(r)] + 3 * q, 24);
+          h->mbs.push_back(m);
+        }
+        mb_cursor[size_t(r)] += 3 * rep.num_microbatches;
+        h->reps.push_back(rep);
+      } else {  // this shard finished earlier: the coordinator's zero report
+        yatt_round_report z{};
+        z.controller_rank = r;
+        z.round = int32_t(k + 1);
+        h->reps.push_back(z);
+      }
+    }
+  h->rounds = int32_t(rounds_g);
+  h->nshards = world;
   return YATT_OK;
 }
 

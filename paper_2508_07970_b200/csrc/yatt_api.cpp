@@ -381,26 +381,17 @@ static int host_threads(std::int64_t n) {
   return n >= 8192 ? cap : 1;
 }
 
-std::vector<std::vector<ShardRoundReport>> run_rollout_rounds(workload::RolloutBatch& batch,
-                                                              int num_controllers,
-                                                              const RoundParams& params,
-                                                              std::vector<int>* first_round_lengths) {
-  params.out_dist.validate();
-  if (params.max_rounds < 1) throw ConfigError("max_rounds must be at least 1");
-  if (num_controllers < 1) throw ConfigError("num_controllers must be positive");
-  if (params.microbatch_size <= 0) throw ConfigError("microbatch_size must be positive");
-  const std::int64_t n = static_cast<std::int64_t>(batch.samples.size());
-  std::vector<std::int64_t> off(static_cast<size_t>(num_controllers) + 1, 0);
-  for (int r = 0; r < num_controllers; ++r) {
-    const workload::ShardRange sr =
-        workload::shard_dataset(static_cast<std::uint64_t>(n), num_controllers, r);
-    off[static_cast<size_t>(r)] = static_cast<std::int64_t>(sr.begin);
-    off[static_cast<size_t>(r) + 1] = static_cast<std::int64_t>(sr.end);
-  }
+// The round loop over host samples: smp[0..n) split into the controller
+// shards `off` (all shards of one process), or, with a peer group, this
+// rank's single shard with every rank's reports gathered once
+// (yatt_peer_rounds_run).
+static std::vector<std::vector<ShardRoundReport>> rounds_impl(
+    workload::RolloutSample* smp, std::int64_t n, const std::vector<std::int64_t>& off,
+    int num_controllers, int step_index, const RoundParams& params,
+    std::vector<int>* first_round_lengths, yatt_peer_t peer) {
   yatt_rounds_t h = g_rounds.get();
   yatt_rounds_io io{};
   detail::throw_status(yatt_rounds_stage(h, n, num_controllers, &io));
-  workload::RolloutSample* smp = batch.samples.data();
   // AoS -> SoA into the pinned stage; large batches split over a few host
   // threads (the reference runs one host thread per shard, simcore.cpp:470)
   const int nt = host_threads(n);
@@ -411,17 +402,22 @@ std::vector<std::vector<ShardRoundReport>> run_rollout_rounds(workload::RolloutB
     io.accepted[i] = smp[i].accepted ? 1 : 0;
   }
   const yatt_round_params p = to_c(params);
-  detail::throw_status(yatt_rounds_run(h, n, off.data(), num_controllers, 0, batch.step_index, 1,
-                                       0, &p, first_round_lengths ? 1 : 0, nullptr));
+  if (peer == nullptr)
+    detail::throw_status(yatt_rounds_run(h, n, off.data(), num_controllers, 0, step_index, 1, 0,
+                                         &p, first_round_lengths ? 1 : 0, nullptr));
+  else
+    detail::throw_status(
+        yatt_peer_rounds_run(peer, h, n, step_index, &p, first_round_lengths ? 1 : 0, nullptr));
   yatt_rounds_view v{};
   detail::throw_status(yatt_rounds_result(h, &v));
   std::vector<std::vector<ShardRoundReport>> all(static_cast<size_t>(v.rounds));
   const yatt_mb_agg* mb = v.microbatches;
+  const int shards = v.num_shards;  // == num_controllers, or the world with a peer group
   for (int r = 0; r < v.rounds; ++r) {
     auto& reports = all[static_cast<size_t>(r)];
-    reports.reserve(static_cast<size_t>(num_controllers));
-    for (int s = 0; s < num_controllers; ++s) {
-      const yatt_round_report& rep = v.reports[static_cast<size_t>(r) * num_controllers + s];
+    reports.reserve(static_cast<size_t>(shards));
+    for (int s = 0; s < shards; ++s) {
+      const yatt_round_report& rep = v.reports[static_cast<size_t>(r) * shards + s];
       reports.push_back(from_c(rep, mb));
       mb += rep.num_microbatches;
     }
@@ -439,6 +435,27 @@ std::vector<std::vector<ShardRoundReport>> run_rollout_rounds(workload::RolloutB
     if (first_round_lengths) (*first_round_lengths)[static_cast<size_t>(i)] = io.first_round_len[i];
   }
   return all;
+}
+
+
+std::vector<std::vector<ShardRoundReport>> run_rollout_rounds(workload::RolloutBatch& batch,
+                                                              int num_controllers,
+                                                              const RoundParams& params,
+                                                              std::vector<int>* first_round_lengths) {
+  params.out_dist.validate();
+  if (params.max_rounds < 1) throw ConfigError("max_rounds must be at least 1");
+  if (num_controllers < 1) throw ConfigError("num_controllers must be positive");
+  if (params.microbatch_size <= 0) throw ConfigError("microbatch_size must be positive");
+  const std::int64_t n = static_cast<std::int64_t>(batch.samples.size());
+  std::vector<std::int64_t> off(static_cast<size_t>(num_controllers) + 1, 0);
+  for (int r = 0; r < num_controllers; ++r) {
+    const workload::ShardRange sr =
+        workload::shard_dataset(static_cast<std::uint64_t>(n), num_controllers, r);
+    off[static_cast<size_t>(r)] = static_cast<std::int64_t>(sr.begin);
+    off[static_cast<size_t>(r) + 1] = static_cast<std::int64_t>(sr.end);
+  }
+  return rounds_impl(batch.samples.data(), n, off, num_controllers, batch.step_index, params,
+                     first_round_lengths, nullptr);
 }
 
 }  // namespace sim
@@ -716,6 +733,17 @@ void PeerGroup::dynamic_sampling_filter(const float* rewards, const std::int64_t
   detail::throw_status(yatt_peer_filter_compact(static_cast<yatt_peer_t>(h_), rewards, lens, n,
                                                 first_id, G, o.keep_groups, o.index_map,
                                                 o.new_cu, o.counts, ws, ws_bytes, stream));
+}
+
+std::vector<std::vector<sim::ShardRoundReport>> PeerGroup::run_rollout_rounds(
+    std::vector<workload::RolloutSample>& shard_samples, int step_index,
+    const sim::RoundParams& params, std::vector<int>* first_round_lengths) {
+  params.out_dist.validate();
+  if (params.max_rounds < 1) throw ConfigError("max_rounds must be at least 1");
+  if (params.microbatch_size <= 0) throw ConfigError("microbatch_size must be positive");
+  const std::int64_t n = static_cast<std::int64_t>(shard_samples.size());
+  return sim::rounds_impl(shard_samples.data(), n, {0, n}, 1, step_index, params,
+                          first_round_lengths, static_cast<yatt_peer_t>(h_));
 }
 
 int PeerGroup::status() const {

@@ -247,54 +247,24 @@ class PeerGroup:
     def run_rollout_rounds(self, samples, step_index: int, params, device="cuda"):
         """Dynamic-sampling rounds of THIS rank's controller shard (the
         reference's sample-level shard_dataset range, workload.cpp:183-198)
-        with ONE cross-rank exchange per step instead of one per round.
-        Acceptance never depends on the drawn lengths (the rounds engine
-        decides every sample's fate first), so each rank runs its own rounds
-        to completion in one persistent kernel (rollout_rounds.cu); the
-        global loop (simcore.cpp:470-490, the coordinator's continue test in
-        demo.cpp:468-476) runs max over ranks of those round counts, a shard
-        that is done reporting zeros.  The ranks' reports + microbatch
-        aggregates travel once, as binary words over peer memory.  Returns
-        the global reports[round][rank] (== api.run_rollout_rounds of the
-        whole batch over `world` controllers) and updates `samples` like the
-        reference's copy_back (simcore.cpp:107-119)."""
+        with ONE cross-rank exchange per step instead of one per round
+        (yatt_peer_rounds_run): acceptance never depends on the drawn lengths,
+        so each rank runs its shard to completion in one persistent kernel;
+        the global loop (simcore.cpp:470-490, the coordinator's continue test
+        in demo.cpp:468-476) runs max over ranks of those round counts, a
+        finished shard reporting zeros, and the reports + microbatch
+        aggregates travel once over peer memory.  Returns the global
+        reports[round][rank] (== api.run_rollout_rounds of the whole batch
+        over `world` controllers) and updates `samples` like the reference's
+        copy_back (simcore.cpp:107-119)."""
         from . import api
-        from ._lib import MbAggC, ReportC
-        local, final = api._run_rounds(samples, "target_out_len_tokens", [0, len(samples)],
-                                       self.rank, step_index, 1, 0, params, device)
+        params.out_dist.validate()
+        rounds, final = api._run_rounds(samples, "target_out_len_tokens", [0, len(samples)],
+                                        self.rank, step_index, 1, 0, params, device, peer=self)
         for x, c in zip(samples, final):
             if c is not None:
                 x.target_out_len_tokens, x.accepted, x.accepted_round = c
-        # wire: [rounds, then per round: report (6 words), its microbatches (3 each)]
-        blob = bytearray(np.int64(len(local)).tobytes())
-        for (rep,) in local:
-            blob += bytes(ReportC(rep.controller_rank, rep.round, rep.active_count,
-                                  rep.newly_accepted_count, rep.forced_accept_count,
-                                  rep.pending_count, rep.accepted_score_tokens,
-                                  rep.accepted_train_units, len(rep.microbatches)))
-            for m in rep.microbatches:
-                blob += bytes(MbAggC(m.controller_rank, m.mb_index, m.sample_count,
-                                     m.max_out_len_tokens, m.score_tokens))
-        words = torch.from_numpy(np.frombuffer(bytes(blob), dtype=np.int64).copy()).to(device)
-        table, sizes = self.allgather_words(words)
-        table = table.cpu().numpy()
-        per_rank = []
-        for r in range(self.world):
-            raw = table[r, : sizes[r]].tobytes()
-            nr, off, reps = int(np.frombuffer(raw[:8], dtype=np.int64)[0]), 8, []
-            for _ in range(nr):
-                rc = ReportC.from_buffer_copy(raw[off: off + C.sizeof(ReportC)])
-                off += C.sizeof(ReportC)
-                mbs = (MbAggC * max(rc.num_microbatches, 1)).from_buffer_copy(
-                    raw[off: off + C.sizeof(MbAggC) * rc.num_microbatches].ljust(
-                        C.sizeof(MbAggC), b"\0"))
-                off += C.sizeof(MbAggC) * rc.num_microbatches
-                reps.append(api._report(rc, mbs))
-            per_rank.append(reps)
-        n_rounds = max(len(x) for x in per_rank)
-        return [[per_rank[r][k] if k < len(per_rank[r]) else
-                 api.ShardRoundReport(r, k + 1, 0, 0, 0, 0, 0, 0, [])
-                 for r in range(self.world)] for k in range(n_rounds)]
+        return rounds
 
     def status(self) -> int:
         s = C.c_int32()
