@@ -38,16 +38,31 @@ struct Acc {
 };
 struct LossCfg {
   double lo, hi, cc;
+  float flo, fhi, fcc;
   bool dual;
 };
 __device__ __forceinline__ LossCfg loss_cfg(const yatt_loss_config& c) {
-  return LossCfg{1.0 - double(c.clip_low), 1.0 + double(c.clip_high), double(c.clip_ratio_c),
+  const double lo = 1.0 - double(c.clip_low), hi = 1.0 + double(c.clip_high);
+  return LossCfg{lo, hi, double(c.clip_ratio_c), float(lo), float(hi), c.clip_ratio_c,
                  c.clip_ratio_c > 1.f};
+}
+
+// The ratio: fp32 expf (rel. error ~1e-7, incl. the fp32 difference), and the
+// fp64 exp only where a decision could flip — within 1e-4 of a clip bound
+// (or of the dual-clip bound), or an extreme value.  Every clip decision is
+// then the fp64 one (the count is exact) and each summed term carries at most
+// ~1e-7 relative error.  (Round 1 took the fp64 exp for every token.)
+__device__ __forceinline__ double ratio_of(float logp, float old_logp, const LossCfg& c) {
+  const float rf = expf(logp - old_logp);
+  const float band = 1e-4f * rf;
+  const bool near = fabsf(rf - c.flo) <= band || fabsf(rf - c.fhi) <= band ||
+                    (c.dual && fabsf(rf - c.fcc) <= band) || !(rf < 3e38f) || !(rf > 1e-30f);
+  return near ? exp(double(logp) - double(old_logp)) : double(rf);
 }
 
 __device__ __forceinline__ void pg_term(float logp, float old_logp, float A, const LossCfg& c,
                                         Acc& s) {
-  const double ratio = exp(double(logp) - double(old_logp));
+  const double ratio = ratio_of(logp, old_logp, c);
   const double a = double(A);
   const double pg1 = -a * ratio;
   const double pg2 = -a * fmin(fmax(ratio, c.lo), c.hi);
@@ -101,14 +116,40 @@ __device__ __forceinline__ Vec4 load_vec(const LossIn& in, int64_t j) {
   if (x.m >> 24) x.k4 += kl.w, x.h4 += h.w;
   return x;
 }
+// Four tokens of a vector in fp32, branch-free: clip decisions from the fp32
+// ratio against the bounds (exact: a token within 1e-4 of a bound, or with an
+// extreme ratio, takes the fp64 pg_term instead), pg = -A * (clipped ratio),
+// the four pg / ratio values summed in fp32 (one rounding per add, like kl /
+// H) and added to the fp64 accumulators once per vector.
 __device__ __forceinline__ void add_vec(const Vec4& x, const LossCfg& c, Acc& s) {
   const float lp[4] = {x.lp.x, x.lp.y, x.lp.z, x.lp.w}, olp[4] = {x.olp.x, x.olp.y, x.olp.z, x.olp.w};
   const float a[4] = {x.a.x, x.a.y, x.a.z, x.a.w};
+  float pg4 = 0.f, r4 = 0.f;
+  int clip = 0, cnt = 0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    if (((x.m >> (8 * k)) & 0xffu) == 0) continue;
-    pg_term(lp[k], olp[k], a[k], c, s);
+    const bool valid = ((x.m >> (8 * k)) & 0xffu) != 0;
+    const float rf = __expf(lp[k] - olp[k]);  // ex2.approx: ~1e-6 relative for |d| <= 20
+    const float band = 1e-4f * rf;
+    const bool near = fabsf(rf - c.flo) <= band || fabsf(rf - c.fhi) <= band ||
+                      (c.dual && fabsf(rf - c.fcc) <= band) || !(rf < 3e38f) || !(rf > 1e-30f);
+    if (valid && near) {  // rare: the fp64 algebra decides
+      pg_term(lp[k], olp[k], a[k], c, s);
+      continue;
+    }
+    const bool clipped = (a[k] > 0.f && rf > c.fhi) || (a[k] < 0.f && rf < c.flo);
+    float pg = -a[k] * (clipped ? fminf(fmaxf(rf, c.flo), c.fhi) : rf);
+    if (c.dual && a[k] < 0.f) pg = fminf(pg, -a[k] * c.fcc);
+    const bool use = valid && !near;
+    pg4 += use ? pg : 0.f;
+    r4 += use ? rf : 0.f;
+    clip += (use && clipped) ? 1 : 0;
+    cnt += use ? 1 : 0;
   }
+  s.pg += double(pg4);
+  s.ratio += double(r4);
+  s.clip += clip;
+  s.cnt += cnt;
   s.kl += double(x.k4);
   s.ent += double(x.h4);
 }
