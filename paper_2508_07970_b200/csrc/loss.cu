@@ -2,8 +2,9 @@
 // token sums.  Replaces the Training-stage cost stand-in of the reference
 // (proj/src/simcore.cpp:404-406) for the loss value itself.
 //
-// Per valid token t (fp64 ratio/clip arithmetic, deterministic reduction
-// order; see Acc below for how the sums are formed):
+// Per valid token t (the ratio / clip algebra in fp32 with the fp64 algebra
+// for any token within 1e-4 of a clip bound, so every clip decision is the
+// fp64 one; fp64 accumulation in a deterministic order; see Acc and add_vec):
 //   ratio = exp(logp - old_logp)
 //   pg    = max(-A*ratio, -A*clip(ratio, 1-eps_lo, 1+eps_hi))     [clipped if 2nd > 1st]
 //   dual clip (clip_ratio_c > 1, A < 0): pg = min(pg, -A*clip_ratio_c)
