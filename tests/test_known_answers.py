@@ -180,7 +180,11 @@ def test_loss_clip_higher(backend):
     s = _loss(backend, logp, old, adv, z, z, clip_low=0.2, clip_high=0.28)
     hi = 1.0 + float(np.float32(0.28))
     pg = n * (-hi) + n * math.e
-    assert O.max_rel_error(s[1:2], [pg]) <= 1e-12
+    # the oracle is fp64 throughout; the device forms each ratio in fp32
+    # (ex2, ~1e-7 relative; every clip decision is still the fp64 one, so the
+    # count is exact) — 100x inside the north star's 1e-5
+    tol = 1e-12 if backend == "oracle" else 1e-6
+    assert O.max_rel_error(s[1:2], [pg]) <= tol
     assert s[4] == n  # clip count
-    assert O.max_rel_error(s[5:6], [2 * n * math.e]) <= 1e-12
+    assert O.max_rel_error(s[5:6], [2 * n * math.e]) <= tol
     assert s[6] == 2 * n
