@@ -885,6 +885,9 @@ int yatt_peer_rounds_run(yatt_peer_t peer, yatt_rounds_t h, int64_t n, int32_t s
   if (rc) return rc;
   YATT_TRY_CUDA(cudaMemcpyAsync(sizes.data(), dout, 8 * size_t(world), cudaMemcpyDeviceToHost, st));
   YATT_TRY_CUDA(cudaStreamSynchronize(st));
+  for (int32_t r = 0; r < world; ++r)  // a timed-out gather leaves -1 words (yatt_peer_status)
+    YATT_REQUIRE(sizes[size_t(r)] >= 1 && sizes[size_t(r)] <= (int64_t(1) << 40), YATT_ERR_CUDA,
+                 "peer_rounds_run: rank %d sent no report words (peer timeout?)", r);
   const int64_t width = *std::max_element(sizes.begin(), sizes.end());
   mine.resize(size_t(width), 0);
   std::vector<int64_t> all(size_t(world * width)), chunk(size_t(world * cap));
