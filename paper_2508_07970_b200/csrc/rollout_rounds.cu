@@ -902,6 +902,11 @@ int yatt_peer_rounds_run(yatt_peer_t peer, yatt_rounds_t h, int64_t n, int32_t s
     for (int32_t r = 0; r < world; ++r)
       std::memcpy(all.data() + size_t(r * width + c0), chunk.data() + size_t(r * cw), size_t(8 * cw));
   }
+  int32_t peer_status = 0;
+  rc = yatt_peer_status(peer, &peer_status);
+  if (rc) return rc;
+  YATT_REQUIRE(peer_status == 0, YATT_ERR_CUDA,
+               "peer_rounds_run: a rank did not arrive (peer all-gather timed out)");
   // the global view, round-major then rank
   int64_t rounds_g = 0;
   std::vector<int64_t> mb_cursor(static_cast<size_t>(world));
